@@ -1,0 +1,225 @@
+/*
+ * bimine_b200.h -- C ABI of the B200 comparable-corpus miner (libbimine_b200.so).
+ *
+ * Hot path of the reference package `bimine` (arXiv 1509.08639 reproduction):
+ *   score     build_similarity_matrix   bimine/aligner.py:313-339   (+ classifier.py:54-117,
+ *                                                                    lexicon.py:88-105)
+ *   align     nw_align / _nw_costs      bimine/aligner.py:116-134, 176-206, 216-220
+ *             nw_align_wavefront        bimine/aligner.py:137-173, 223-241
+ *   extract   extract_pairs             bimine/aligner.py:342-368
+ *   tune      tune / f_measure          bimine/tuner.py:67-154
+ *
+ * The reference has no FFI: its only compiled boundary is the numba kernel
+ * `_nw_costs(S: float64[n,m], penalty) -> float64[n+1,m+1]` (aligner.py:116).
+ * Every entry point below replaces one of the Python/numba functions above; the
+ * file:line each replaces is given on the declaration. INTEGRATION.md shows the
+ * ctypes binding a bimine maintainer would add.
+ *
+ * Conventions
+ *  - Plain C types only. Pointers inside the bm_* structs passed to the
+ *    *device* entry points are DEVICE pointers; the `_host` entry points take
+ *    HOST pointers and do their own H2D/D2H copies.
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and does not synchronize unless documented.
+ *  - Return 0 on success or a negative BM_E* code; bm_last_error() returns a
+ *    thread-local message for the last failure.
+ *  - Arithmetic is IEEE fp64 with the exact operation order of the reference
+ *    (no FMA contraction, glibc-exact exp) so results are bit-identical.
+ */
+#ifndef BIMINE_B200_H
+#define BIMINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BM_ABI_VERSION 1
+
+#define BM_OK 0
+#define BM_EINVAL -1   /* bad argument (maps to ValueError)            */
+#define BM_ECUDA -2    /* CUDA runtime error                           */
+#define BM_ENOMEM -3   /* device allocation failed                     */
+#define BM_ELIMIT -4   /* size over a hard bound (ResourceLimitError)  */
+
+/* Move codes (bimine/aligner.py:76-82): diagonal, skip-source, skip-target. */
+#define BM_MOVE_D 0
+#define BM_MOVE_GS 1
+#define BM_MOVE_GT 2
+
+/*
+ * Packed sentences. Token strings are interned into one id space per pack
+ * (normalized tokens and raw digit tokens share it; equal strings = equal id).
+ * Per sentence (bimine/classifier.py:54-97, lexicon.py:95-98):
+ *   n_tok   = len(tokens)                                  (T)
+ *   n_punct = #tokens with no alphanumeric character        (P)
+ *   n_alpha = #tokens with str.isalpha()                    (|A|)
+ *   tok_*   = the set U of normalize(token) ids, ascending, with the number
+ *             of isalpha() tokens that normalize to each id (A as multiplicities)
+ *   dig_*   = the set D of raw isdigit() token ids, ascending
+ */
+typedef struct bm_sentences {
+  int32_t n_sent;
+  const int32_t* n_tok;
+  const int32_t* n_punct;
+  const int32_t* n_alpha;
+  const int32_t* tok_off;    /* [n_sent + 1] */
+  const int32_t* tok_id;     /* [tok_off[n_sent]] */
+  const uint16_t* tok_alpha; /* [tok_off[n_sent]] */
+  const int32_t* dig_off;    /* [n_sent + 1] */
+  const int32_t* dig_id;     /* [dig_off[n_sent]] */
+} bm_sentences;
+
+/* Document pairs: source sentences [src0, src0+n), target [tgt0, tgt0+m). */
+typedef struct bm_docs {
+  int32_t n_docs;
+  const int32_t* src0;
+  const int32_t* n;
+  const int32_t* tgt0;
+  const int32_t* m;
+} bm_docs;
+
+/*
+ * Lexicon over the same id space (bimine/lexicon.py:16-46): fwd = the model's
+ * lexicon (source word -> candidate target words), rev = lex.reversed().
+ * Only candidates that occur in the id space are kept (others can never hit).
+ */
+typedef struct bm_lexicon {
+  int32_t n_ids;
+  const int32_t* fwd_off; /* [n_ids + 1] */
+  const int32_t* fwd_cand;
+  const int32_t* rev_off; /* [n_ids + 1] */
+  const int32_t* rev_cand;
+} bm_lexicon;
+
+/* Linear classifier (bimine/classifier.py:41-49,107-117). */
+typedef struct bm_model {
+  double w[7];
+  double bias;
+} bm_model;
+
+/* One mined pair (bimine/aligner.py:103-113 minus the Sentence objects). */
+typedef struct bm_record {
+  int32_t doc;  /* index into bm_docs */
+  int32_t i;    /* source sentence index (src_index) */
+  int32_t j;    /* target sentence index (tgt_index) */
+  int32_t pad;
+  double conf;  /* S[i, j] */
+} bm_record;
+
+int bm_abi_version(void);
+const char* bm_last_error(void);
+/* Number of CUDA devices visible (0 = no GPU). */
+int bm_device_count(void);
+
+/*
+ * K1 -- replaces build_similarity_matrix (aligner.py:313-339) for a batch:
+ * S[d] is written row-major with row pitch `pitch[d]` doubles at S + s_off[d].
+ * pitch[d] must be a multiple of 4 and S + s_off[d] 32-byte aligned (the NW
+ * kernel reads S with 16-byte vector loads). n_host/m_host: host copies of
+ * docs->n / docs->m (used to plan the tile grid).
+ */
+int bm_score(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+             const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
+             const int64_t* s_off, const int32_t* pitch, double* S, void* stream);
+
+/*
+ * Feature vectors / confidences for explicit (src, tgt, pos_s, pos_t) tuples:
+ * replaces extract_features (classifier.py:68-97) and confidence (:107-117).
+ * feats: [n_q, 7]; conf: [n_q] (either may be NULL).
+ */
+int bm_features(const bm_sentences* sent, const bm_lexicon* lex, const int32_t* q_src,
+                const int32_t* q_tgt, const double* q_pos_s, const double* q_pos_t,
+                int32_t n_q, double* feats, void* stream);
+int bm_confidence(const double* feats, int32_t n_q, const bm_model* model, double* conf,
+                  void* stream);
+
+/*
+ * K2/K3 -- replaces _nw_costs / _nw_costs_wavefront + the fill half of
+ * nw_align (aligner.py:116-173, 216-241) for a batch of matrices.
+ * S: as written by bm_score. dirs: 2-bit traceback codes, layout private to
+ * the library, sized by bm_dirs_words(n, m) uint32 words at dirs + dir_off[d].
+ * cost[d] = C[n, m].
+ */
+int64_t bm_dirs_words(int32_t n, int32_t m);
+int bm_nw(const double* S, const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+          const int32_t* m, const int32_t* n_host, const int32_t* m_host, int32_t n_docs,
+          double penalty, uint32_t* dirs, const int64_t* dir_off, double* cost, void* stream);
+
+/*
+ * K4a -- the traceback of aligner.py:176-206 (tie order D > GS > GT): the
+ * moves of doc d are written at mv_off[d] (capacity n+m) in REVERSE path
+ * order; mv_op = BM_MOVE_*, mv_i / mv_j = cell indices (-1 where the move has
+ * none: GS has no j, GT no i), mv_len[d] = path length.
+ */
+int bm_traceback(const uint32_t* dirs, const int64_t* dir_off, const int32_t* n,
+                 const int32_t* m, int32_t n_docs, const int64_t* mv_off, int8_t* mv_op,
+                 int32_t* mv_i, int32_t* mv_j, int32_t* mv_len, void* stream);
+
+/*
+ * K4b -- extract_pairs (aligner.py:342-368) fused with the traceback: every
+ * diagonal move with S[i,j] >= threshold becomes a record, in path order.
+ * Records of doc d land at rec + rec_off[d] (capacity min(n,m)); rec_count[d].
+ */
+int bm_extract(const uint32_t* dirs, const int64_t* dir_off, const double* S,
+               const int64_t* s_off, const int32_t* pitch, const int32_t* n, const int32_t* m,
+               int32_t n_docs, double threshold, const int64_t* rec_off, bm_record* rec,
+               int32_t* rec_count, void* stream);
+
+/*
+ * extract_pairs for an explicit path (aligner.py:352-357): conf[q] =
+ * S[ci[q], cj[q]] (row pitch `pitch` doubles), keep[q] = conf[q] >= threshold.
+ */
+int bm_select(const double* S, int64_t pitch, const int32_t* ci, const int32_t* cj, int32_t k,
+              double threshold, double* conf, uint8_t* keep, void* stream);
+
+/*
+ * Fused score -> NW -> traceback -> threshold for a batch (mine_document,
+ * miner.py:84-128, forward orientation). Records land at rec + rec_off[d]
+ * (capacity min(n,m)), counts in rec_count, path costs C[n,m] in cost. Docs of
+ * any size are accepted: the library routes each one either to the fused
+ * warp-per-document kernel (no similarity matrix is materialised) or to the
+ * banded K1 -> K2/K3 -> K4 path. n_host/m_host/amax_host are host arrays
+ * (amax = the largest n_alpha of any sentence of the doc). Scratch is
+ * stream-ordered (cudaMallocAsync on `stream`).
+ */
+int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+            const int32_t* m_host, const int32_t* amax_host, const bm_lexicon* lex,
+            const bm_model* model, double threshold, double penalty, const int64_t* rec_off,
+            bm_record* rec, int32_t* rec_count, double* cost, void* stream);
+
+/*
+ * Same as bm_mine but every array (sentences, docs, lexicon) is in HOST
+ * memory: the call copies inputs to the device, mines, compacts the records
+ * and copies them back into rec_out (capacity rec_cap) in document order.
+ * *n_rec receives the record count. Synchronizes `stream` before returning.
+ * This is the end-to-end entry point a foreign-language binding would call.
+ */
+int bm_mine_host(const bm_sentences* sent_h, const bm_docs* docs_h, const bm_lexicon* lex_h,
+                 const bm_model* model, double threshold, double penalty, bm_record* rec_out,
+                 int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream);
+
+/*
+ * K5 -- tune (tuner.py:87-154): for every penalty p_k and threshold t_l,
+ * pred[k*n_thr + l] += #diagonal moves with S >= t_l over all docs, and
+ * hit[k*n_thr + l] += those whose (i, j) is in the doc's gold set.
+ * gold: per doc ascending keys i*m + j at gold + gold_off[d] (gold_off[n_docs]).
+ */
+int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+            const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
+            const double* penalties_host, int32_t n_pen, const double* thresholds, int32_t n_thr,
+            const int64_t* gold, const int64_t* gold_off, unsigned long long* pred,
+            unsigned long long* hit, void* stream);
+
+/* Exclusive-scan compaction of per-doc record slots into a dense,
+ * document-ordered array; *total (device) receives the record count. */
+int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_count,
+               int32_t n_docs, bm_record* dense, int64_t* total, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BIMINE_B200_H */

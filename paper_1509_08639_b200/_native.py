@@ -1,0 +1,134 @@
+"""ctypes binding of libbimine_b200.so (include/bimine_b200.h).
+
+The library is the only compute path: if it is missing, fails to load, or no
+CUDA device is visible, every hot-path call raises NativeUnavailableError.
+There is no CPU fallback anywhere in the package.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import NativeUnavailableError, ResourceLimitError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbimine_b200.so")
+
+BM_OK, BM_EINVAL, BM_ECUDA, BM_ENOMEM, BM_ELIMIT = 0, -1, -2, -3, -4
+MOVE_D, MOVE_GS, MOVE_GT = 0, 1, 2
+
+_p = C.c_void_p
+_i32p = C.POINTER(C.c_int32)
+
+
+class Sentences(C.Structure):
+    _fields_ = [
+        ("n_sent", C.c_int32),
+        ("n_tok", _p), ("n_punct", _p), ("n_alpha", _p),
+        ("tok_off", _p), ("tok_id", _p), ("tok_alpha", _p),
+        ("dig_off", _p), ("dig_id", _p),
+    ]
+
+
+class Docs(C.Structure):
+    _fields_ = [("n_docs", C.c_int32), ("src0", _p), ("n", _p), ("tgt0", _p), ("m", _p)]
+
+
+class LexiconC(C.Structure):
+    _fields_ = [("n_ids", C.c_int32), ("fwd_off", _p), ("fwd_cand", _p),
+                ("rev_off", _p), ("rev_cand", _p)]
+
+
+class ModelC(C.Structure):
+    _fields_ = [("w", C.c_double * 7), ("bias", C.c_double)]
+
+
+class Record(C.Structure):
+    _fields_ = [("doc", C.c_int32), ("i", C.c_int32), ("j", C.c_int32),
+                ("pad", C.c_int32), ("conf", C.c_double)]
+
+
+RECORD_DTYPE = [("doc", "<i4"), ("i", "<i4"), ("j", "<i4"), ("pad", "<i4"), ("conf", "<f8")]
+
+_SIGS = {
+    "bm_abi_version": (C.c_int, []),
+    "bm_last_error": (C.c_char_p, []),
+    "bm_device_count": (C.c_int, []),
+    "bm_dirs_words": (C.c_int64, [C.c_int32, C.c_int32]),
+    "bm_score": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, C.POINTER(LexiconC),
+                           C.POINTER(ModelC), _p, _p, _p, _p]),
+    "bm_features": (C.c_int, [C.POINTER(Sentences), C.POINTER(LexiconC), _p, _p, _p, _p,
+                              C.c_int32, _p, _p]),
+    "bm_confidence": (C.c_int, [_p, C.c_int32, C.POINTER(ModelC), _p, _p]),
+    "bm_nw": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, C.c_int32, C.c_double, _p, _p, _p, _p]),
+    "bm_traceback": (C.c_int, [_p, _p, _p, _p, C.c_int32, _p, _p, _p, _p, _p, _p]),
+    "bm_extract": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, C.c_int32, C.c_double, _p, _p, _p, _p]),
+    "bm_select": (C.c_int, [_p, C.c_int64, _p, _p, C.c_int32, C.c_double, _p, _p, _p]),
+    "bm_mine": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, _p,
+                          C.POINTER(LexiconC), C.POINTER(ModelC), C.c_double, C.c_double,
+                          _p, _p, _p, _p, _p]),
+    "bm_mine_host": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), C.POINTER(LexiconC),
+                               C.POINTER(ModelC), C.c_double, C.c_double, _p, C.c_int64,
+                               C.POINTER(C.c_int64), _p, _p]),
+    "bm_tune": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, C.POINTER(LexiconC),
+                          C.POINTER(ModelC), _p, C.c_int32, _p, C.c_int32, _p, _p, _p, _p, _p]),
+    "bm_compact": (C.c_int, [_p, _p, _p, C.c_int32, _p, _p, _p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+
+def load_library(require_device: bool = False) -> C.CDLL:
+    """Load the library (no GPU needed just to load and inspect it)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeUnavailableError(
+                    f"{LIB_PATH} is missing; build it with "
+                    "`python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            lib = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    if require_device and _lib.bm_device_count() < 1:
+        raise NativeUnavailableError("no CUDA device visible: the B200 kernels cannot run")
+    return _lib
+
+
+def lib() -> C.CDLL:
+    """The library, with a usable CUDA device (hot-path entry)."""
+    return load_library(require_device=True)
+
+
+def check(rc: int) -> None:
+    if rc == BM_OK:
+        return
+    msg = (load_library().bm_last_error() or b"").decode("utf-8", "replace")
+    if rc == BM_EINVAL:
+        raise ValueError(msg)
+    if rc == BM_ELIMIT:
+        raise ResourceLimitError(msg)
+    if rc == BM_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"libbimine_b200 error {rc}: {msg}")
+
+
+def model_struct(model) -> ModelC:
+    # confidence() zips weights with the 7 features (classifier.py:114-116):
+    # extra weights are ignored, missing ones contribute nothing (z + 0.0 == z
+    # for every z the sigmoid can tell apart), so pad/truncate to 7.
+    m = ModelC()
+    w = [float(x) for x in list(model.weights)[:7]]
+    w += [0.0] * (7 - len(w))
+    for k in range(7):
+        m.w[k] = w[k]
+    m.bias = float(model.bias)
+    return m

@@ -1,0 +1,557 @@
+// C ABI of libbimine_b200.so (declared in include/bimine_b200.h).
+//
+// Host-side planning only: which kernel tier each document goes to, tile and
+// band work lists, offsets into stream-ordered scratch (cudaMallocAsync), and
+// error mapping. No arithmetic of the hot path happens here.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bimine_b200.h"
+#include "bm_kernels.cuh"
+
+
+using namespace bm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? BM_ENOMEM : BM_ECUDA,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define BM_CK(expr, what)                        \
+  do {                                           \
+    cudaError_t _e = (expr);                     \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+// Stream-ordered scratch: allocated on `st`, freed on `st` when it goes out of
+// scope, so it stays valid for every kernel enqueued before the free.
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t st) : st_(st) {}
+  ~Scratch() {
+    for (void* p : ptrs_) cudaFreeAsync(p, st_);
+  }
+  template <class T>
+  cudaError_t alloc(T** out, size_t count) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), st_);
+    if (e != cudaSuccess) return e;
+    ptrs_.push_back(p);
+    *out = (T*)p;
+    return cudaSuccess;
+  }
+  template <class T>
+  cudaError_t upload(T** out, const std::vector<T>& v) {
+    cudaError_t e = alloc(out, v.size());
+    if (e != cudaSuccess || v.empty()) return e;
+    return cudaMemcpyAsync(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st_);
+  }
+
+ private:
+  cudaStream_t st_;
+  std::vector<void*> ptrs_;
+};
+
+Model to_model(const bm_model* m) {
+  Model M;
+  for (int k = 0; k < 7; ++k) M.w[k] = m->w[k];
+  M.bias = m->bias;
+  return M;
+}
+
+inline int32_t pitch_of(int32_t m) { return (m + 3) & ~3; }
+
+// Unfused general path for a subset of documents: K1 -> K2/K3 -> consumer.
+struct GeneralPlan {
+  std::vector<int32_t> docs;  // indices into the batch
+  std::vector<int64_t> s_off, dir_off, bnd_off, prog_off;
+  std::vector<int32_t> pitch, n, m;
+  std::vector<int4> tiles;    // doc field = local index
+  std::vector<WorkItem> items;
+  int64_t s_total = 0, dir_total = 0, bnd_total = 0, prog_total = 0;
+
+  void add(int32_t d, int32_t nd, int32_t md) {
+    const int32_t local = (int32_t)docs.size();
+    docs.push_back(d);
+    n.push_back(nd);
+    m.push_back(md);
+    pitch.push_back(pitch_of(md));
+    s_off.push_back(s_total);
+    s_total += (int64_t)nd * pitch_of(md);
+    dir_off.push_back(dir_total);
+    dir_total += band_dirs_words(nd, md);
+    const int nb = (nd + kBandRows - 1) / kBandRows;
+    bnd_off.push_back(bnd_total);
+    bnd_total += (int64_t)(nb - 1) * md;
+    prog_off.push_back(prog_total);
+    prog_total += nb;
+    for (int r0 = 0; r0 < nd; r0 += kTile)
+      for (int c0 = 0; c0 < md; c0 += kTile) tiles.push_back(make_int4(local, r0, c0, 0));
+    for (int b = 0; b < nb; ++b) items.push_back(WorkItem{local, b});
+  }
+};
+
+// Device copies of a GeneralPlan plus the subset's own bm_docs view.
+struct GeneralDev {
+  int64_t *s_off, *dir_off, *bnd_off, *prog_off;
+  int32_t *pitch, *n, *m, *src0, *tgt0;
+  int4* tiles;
+  WorkItem* items;
+  double *S, *bnd;
+  uint32_t *dirs, *prog;
+  unsigned int* ticket;
+};
+
+// Gathers src0/tgt0/n/m of the subset on the device from the batch arrays.
+__global__ void gather_docs_kernel(bm_docs D, const int32_t* idx, int k, int32_t* src0,
+                                   int32_t* tgt0) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < k) {
+    src0[q] = D.src0[idx[q]];
+    tgt0[q] = D.tgt0[idx[q]];
+  }
+}
+
+__global__ void scatter_results_kernel(const int32_t* idx, int k, const double* cost_local,
+                                       double* cost, const bm_record* rec_local,
+                                       const int64_t* rec_off_local, const int32_t* cnt_local,
+                                       const int64_t* rec_off, bm_record* rec, int32_t* cnt) {
+  int q = blockIdx.x;
+  if (q >= k) return;
+  const int d = idx[q];
+  if (threadIdx.x == 0) {
+    cost[d] = cost_local[q];
+    cnt[d] = cnt_local[q];
+  }
+  for (int t = threadIdx.x; t < cnt_local[q]; t += blockDim.x) {
+    bm_record r = rec_local[rec_off_local[q] + t];
+    r.doc = d;
+    rec[rec_off[d] + t] = r;
+  }
+}
+
+int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, GeneralDev& dv,
+                    cudaStream_t st) {
+  const int k = (int)g.docs.size();
+  int32_t* idx = nullptr;
+  BM_CK(sc.upload(&idx, g.docs), "upload");
+  BM_CK(sc.upload(&dv.s_off, g.s_off), "upload");
+  BM_CK(sc.upload(&dv.dir_off, g.dir_off), "upload");
+  BM_CK(sc.upload(&dv.bnd_off, g.bnd_off), "upload");
+  BM_CK(sc.upload(&dv.prog_off, g.prog_off), "upload");
+  BM_CK(sc.upload(&dv.pitch, g.pitch), "upload");
+  BM_CK(sc.upload(&dv.n, g.n), "upload");
+  BM_CK(sc.upload(&dv.m, g.m), "upload");
+  BM_CK(sc.upload(&dv.tiles, g.tiles), "upload");
+  BM_CK(sc.upload(&dv.items, g.items), "upload");
+  BM_CK(sc.alloc(&dv.src0, k), "alloc");
+  BM_CK(sc.alloc(&dv.tgt0, k), "alloc");
+  BM_CK(sc.alloc(&dv.S, (size_t)g.s_total), "alloc S");
+  BM_CK(sc.alloc(&dv.dirs, (size_t)g.dir_total), "alloc dirs");
+  BM_CK(sc.alloc(&dv.bnd, (size_t)g.bnd_total), "alloc boundary");
+  BM_CK(sc.alloc(&dv.prog, (size_t)g.prog_total), "alloc progress");
+  BM_CK(sc.alloc(&dv.ticket, 1), "alloc ticket");
+  gather_docs_kernel<<<(k + 255) / 256, 256, 0, st>>>(*docs, idx, k, dv.src0, dv.tgt0);
+  BM_CK(cudaGetLastError(), "gather_docs");
+  return BM_OK;
+}
+
+bm_docs local_docs(const GeneralDev& dv, int k) {
+  bm_docs D;
+  D.n_docs = k;
+  D.src0 = dv.src0;
+  D.n = dv.n;
+  D.tgt0 = dv.tgt0;
+  D.m = dv.m;
+  return D;
+}
+
+int general_nw(const GeneralPlan& g, GeneralDev& dv, double penalty, double* cost,
+               cudaStream_t st) {
+  BM_CK(cudaMemsetAsync(dv.prog, 0, std::max<int64_t>(g.prog_total, 1) * 4, st), "memset");
+  BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
+  NwArgs a;
+  a.S = dv.S;
+  a.s_off = dv.s_off;
+  a.pitch = dv.pitch;
+  a.n = dv.n;
+  a.m = dv.m;
+  a.p = penalty;
+  a.dirs = dv.dirs;
+  a.dir_off = dv.dir_off;
+  a.cost = cost;
+  a.items = dv.items;
+  a.n_items = (int)g.items.size();
+  a.ticket = dv.ticket;
+  a.bnd = dv.bnd;
+  a.bnd_off = dv.bnd_off;
+  a.prog = dv.prog;
+  a.prog_off = dv.prog_off;
+  const int warps = std::min<int>(nw_resident_warps(), a.n_items);
+  BM_CK(launch_nw(a, warps, st), "nw_band_kernel");
+  return BM_OK;
+}
+
+bool check_penalty(double p) { return p >= 0.0; }  // NaN fails (aligner.py:209-213)
+
+}  // namespace
+
+extern "C" {
+
+int bm_abi_version(void) { return BM_ABI_VERSION; }
+
+const char* bm_last_error(void) { return g_err.c_str(); }
+
+int bm_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int64_t bm_dirs_words(int32_t n, int32_t m) { return band_dirs_words(n, m); }
+
+int bm_score(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+             const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
+             const int64_t* s_off, const int32_t* pitch, double* S, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int4> tiles;
+  for (int d = 0; d < docs->n_docs; ++d)
+    for (int r0 = 0; r0 < n_host[d]; r0 += kTile)
+      for (int c0 = 0; c0 < m_host[d]; c0 += kTile) tiles.push_back(make_int4(d, r0, c0, 0));
+  Scratch sc(st);
+  int4* dt = nullptr;
+  BM_CK(sc.upload(&dt, tiles), "upload tiles");
+  BM_CK(launch_score(*sent, *docs, *lex, to_model(model), dt, (int)tiles.size(), s_off, pitch, S, st),
+        "score_tile_kernel");
+  return BM_OK;
+}
+
+int bm_features(const bm_sentences* sent, const bm_lexicon* lex, const int32_t* q_src,
+                const int32_t* q_tgt, const double* q_pos_s, const double* q_pos_t, int32_t n_q,
+                double* feats, void* stream) {
+  BM_CK(launch_features(*sent, *lex, q_src, q_tgt, q_pos_s, q_pos_t, n_q, feats,
+                        (cudaStream_t)stream),
+        "features_kernel");
+  return BM_OK;
+}
+
+int bm_confidence(const double* feats, int32_t n_q, const bm_model* model, double* conf,
+                  void* stream) {
+  BM_CK(launch_confidence(feats, n_q, to_model(model), conf, (cudaStream_t)stream),
+        "confidence_kernel");
+  return BM_OK;
+}
+
+int bm_nw(const double* S, const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+          const int32_t* m, const int32_t* n_host, const int32_t* m_host, int32_t n_docs,
+          double penalty, uint32_t* dirs, const int64_t* dir_off, double* cost, void* stream) {
+  if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<WorkItem> items;
+  std::vector<int64_t> bnd_off(n_docs), prog_off(n_docs);
+  int64_t bt = 0, pt = 0;
+  for (int d = 0; d < n_docs; ++d) {
+    const int nb = (n_host[d] + kBandRows - 1) / kBandRows;
+    bnd_off[d] = bt;
+    bt += (int64_t)std::max(nb - 1, 0) * m_host[d];
+    prog_off[d] = pt;
+    pt += nb;
+    for (int b = 0; b < nb; ++b) items.push_back(WorkItem{d, b});
+  }
+  Scratch sc(st);
+  NwArgs a;
+  WorkItem* di = nullptr;
+  int64_t *dbo = nullptr, *dpo = nullptr;
+  BM_CK(sc.upload(&di, items), "upload");
+  BM_CK(sc.upload(&dbo, bnd_off), "upload");
+  BM_CK(sc.upload(&dpo, prog_off), "upload");
+  double* bnd = nullptr;
+  uint32_t* prog = nullptr;
+  unsigned int* ticket = nullptr;
+  BM_CK(sc.alloc(&bnd, (size_t)bt), "alloc");
+  BM_CK(sc.alloc(&prog, (size_t)pt), "alloc");
+  BM_CK(sc.alloc(&ticket, 1), "alloc");
+  BM_CK(cudaMemsetAsync(prog, 0, std::max<int64_t>(pt, 1) * 4, st), "memset");
+  BM_CK(cudaMemsetAsync(ticket, 0, 4, st), "memset");
+  a.S = S;
+  a.s_off = s_off;
+  a.pitch = pitch;
+  a.n = n;
+  a.m = m;
+  a.p = penalty;
+  a.dirs = dirs;
+  a.dir_off = dir_off;
+  a.cost = cost;
+  a.items = di;
+  a.n_items = (int)items.size();
+  a.ticket = ticket;
+  a.bnd = bnd;
+  a.bnd_off = dbo;
+  a.prog = prog;
+  a.prog_off = dpo;
+  BM_CK(launch_nw(a, std::min<int>(nw_resident_warps(), a.n_items), st), "nw_band_kernel");
+  return BM_OK;
+}
+
+int bm_traceback(const uint32_t* dirs, const int64_t* dir_off, const int32_t* n, const int32_t* m,
+                 int32_t n_docs, const int64_t* mv_off, int8_t* mv_op, int32_t* mv_i,
+                 int32_t* mv_j, int32_t* mv_len, void* stream) {
+  BM_CK(launch_traceback(dirs, dir_off, n, m, n_docs, mv_off, mv_op, mv_i, mv_j, mv_len,
+                         (cudaStream_t)stream),
+        "traceback_kernel");
+  return BM_OK;
+}
+
+int bm_extract(const uint32_t* dirs, const int64_t* dir_off, const double* S, const int64_t* s_off,
+               const int32_t* pitch, const int32_t* n, const int32_t* m, int32_t n_docs,
+               double threshold, const int64_t* rec_off, bm_record* rec, int32_t* rec_count,
+               void* stream) {
+  BM_CK(launch_extract(dirs, dir_off, S, s_off, pitch, n, m, n_docs, threshold, rec_off, rec,
+                       rec_count, (cudaStream_t)stream),
+        "extract_kernel");
+  return BM_OK;
+}
+
+int bm_select(const double* S, int64_t pitch, const int32_t* ci, const int32_t* cj, int32_t k,
+              double threshold, double* conf, uint8_t* keep, void* stream) {
+  BM_CK(launch_select(S, pitch, ci, cj, k, threshold, conf, keep, (cudaStream_t)stream),
+        "select_kernel");
+  return BM_OK;
+}
+
+int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+            const int32_t* m_host, const int32_t* amax_host, const bm_lexicon* lex,
+            const bm_model* model, double threshold, double penalty, const int64_t* rec_off,
+            bm_record* rec, int32_t* rec_count, double* cost, void* stream) {
+  if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nd = docs->n_docs;
+  BM_CK(cudaMemsetAsync(rec_count, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
+  std::vector<int32_t> fused[4];
+  size_t fused_smem[4] = {0, 0, 0, 0};
+  GeneralPlan g;
+  for (int d = 0; d < nd; ++d) {
+    const int n = n_host[d], m = m_host[d];
+    if (n <= 0 || m <= 0) continue;
+    const size_t sl = fused_slice_bytes(n, m);
+    if (n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax_host[d] <= 255) {
+      const int R = fused_rows_per_lane(n);
+      const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
+      fused[q].push_back(d);
+      fused_smem[q] = std::max(fused_smem[q], sl);
+    } else {
+      g.add(d, n, m);
+    }
+  }
+  Scratch sc(st);
+  const Model M = to_model(model);
+  for (int q = 0; q < 4; ++q) {
+    if (fused[q].empty()) continue;
+    int32_t* list = nullptr;
+    BM_CK(sc.upload(&list, fused[q]), "upload");
+    FusedArgs a;
+    a.S = *sent;
+    a.D = *docs;
+    a.L = *lex;
+    a.M = M;
+    a.threshold = threshold;
+    a.p = penalty;
+    a.list = list;
+    a.n_list = (int)fused[q].size();
+    a.rec_off = rec_off;
+    a.rec = rec;
+    a.rec_count = rec_count;
+    a.cost = cost;
+    BM_CK(launch_fused(a, 1 << q, fused_smem[q], st), "mine_fused_kernel");
+  }
+  if (!g.docs.empty()) {
+    const int k = (int)g.docs.size();
+    GeneralDev dv;
+    int rc = general_prepare(g, docs, sc, dv, st);
+    if (rc) return rc;
+    const bm_docs D = local_docs(dv, k);
+    BM_CK(launch_score(*sent, D, *lex, M, dv.tiles, (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S,
+                       st),
+          "score_tile_kernel");
+    double* cost_l = nullptr;
+    BM_CK(sc.alloc(&cost_l, k), "alloc");
+    rc = general_nw(g, dv, penalty, cost_l, st);
+    if (rc) return rc;
+    std::vector<int64_t> roff(k);
+    int64_t rt = 0;
+    for (int q = 0; q < k; ++q) {
+      roff[q] = rt;
+      rt += std::min(g.n[q], g.m[q]);
+    }
+    int64_t* droff = nullptr;
+    bm_record* rl = nullptr;
+    int32_t* cl = nullptr;
+    int32_t* idx = nullptr;
+    BM_CK(sc.upload(&droff, roff), "upload");
+    BM_CK(sc.alloc(&rl, (size_t)rt), "alloc");
+    BM_CK(sc.alloc(&cl, k), "alloc");
+    BM_CK(sc.upload(&idx, g.docs), "upload");
+    BM_CK(launch_extract(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, k, threshold,
+                         droff, rl, cl, st),
+          "extract_kernel");
+    scatter_results_kernel<<<k, 128, 0, st>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
+                                              rec_count);
+    BM_CK(cudaGetLastError(), "scatter_results");
+  }
+  return BM_OK;
+}
+
+int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_count,
+               int32_t n_docs, bm_record* dense, int64_t* total, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch sc(st);
+  int64_t* doff = nullptr;
+  BM_CK(sc.alloc(&doff, n_docs), "alloc");
+  BM_CK(launch_compact(rec, rec_off, rec_count, n_docs, doff, total, dense, st), "compact");
+  return BM_OK;
+}
+
+int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh,
+                 const bm_model* model, double threshold, double penalty, bm_record* rec_out,
+                 int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ns = sh->n_sent, nd = dh->n_docs;
+  const int64_t ne = ns ? sh->tok_off[ns] : 0;
+  const int64_t ndig = ns ? sh->dig_off[ns] : 0;
+  const int nid = lh->n_ids;
+  // per-doc limits computed on the host (routing input of bm_mine)
+  std::vector<int32_t> amax(nd, 0);
+  std::vector<int64_t> roff(nd);
+  int64_t rt = 0;
+  for (int d = 0; d < nd; ++d) {
+    int a = 0;
+    for (int k = 0; k < dh->n[d]; ++k) a = std::max(a, sh->n_alpha[dh->src0[d] + k]);
+    for (int k = 0; k < dh->m[d]; ++k) a = std::max(a, sh->n_alpha[dh->tgt0[d] + k]);
+    amax[d] = a;
+    roff[d] = rt;
+    rt += std::max(0, std::min(dh->n[d], dh->m[d]));
+  }
+  Scratch sc(st);
+  auto up = [&](auto** dst, const auto* src, size_t count) -> cudaError_t {
+    cudaError_t e = sc.alloc(dst, count);
+    if (e != cudaSuccess || count == 0) return e;
+    return cudaMemcpyAsync(*dst, src, count * sizeof(**dst), cudaMemcpyHostToDevice, st);
+  };
+  bm_sentences sd;
+  sd.n_sent = ns;
+  int32_t *a0, *a1, *a2, *a3, *a4, *a5, *a6;
+  uint16_t* a7;
+  BM_CK(up(&a0, sh->n_tok, ns), "h2d");
+  BM_CK(up(&a1, sh->n_punct, ns), "h2d");
+  BM_CK(up(&a2, sh->n_alpha, ns), "h2d");
+  BM_CK(up(&a3, sh->tok_off, ns + 1), "h2d");
+  BM_CK(up(&a4, sh->tok_id, ne), "h2d");
+  BM_CK(up(&a7, sh->tok_alpha, ne), "h2d");
+  BM_CK(up(&a5, sh->dig_off, ns + 1), "h2d");
+  BM_CK(up(&a6, sh->dig_id, ndig), "h2d");
+  sd.n_tok = a0;
+  sd.n_punct = a1;
+  sd.n_alpha = a2;
+  sd.tok_off = a3;
+  sd.tok_id = a4;
+  sd.tok_alpha = a7;
+  sd.dig_off = a5;
+  sd.dig_id = a6;
+  bm_docs dd;
+  dd.n_docs = nd;
+  int32_t *b0, *b1, *b2, *b3;
+  BM_CK(up(&b0, dh->src0, nd), "h2d");
+  BM_CK(up(&b1, dh->n, nd), "h2d");
+  BM_CK(up(&b2, dh->tgt0, nd), "h2d");
+  BM_CK(up(&b3, dh->m, nd), "h2d");
+  dd.src0 = b0;
+  dd.n = b1;
+  dd.tgt0 = b2;
+  dd.m = b3;
+  bm_lexicon ld;
+  ld.n_ids = nid;
+  int32_t *c0, *c1, *c2, *c3;
+  BM_CK(up(&c0, lh->fwd_off, nid + 1), "h2d");
+  BM_CK(up(&c1, lh->fwd_cand, nid ? lh->fwd_off[nid] : 0), "h2d");
+  BM_CK(up(&c2, lh->rev_off, nid + 1), "h2d");
+  BM_CK(up(&c3, lh->rev_cand, nid ? lh->rev_off[nid] : 0), "h2d");
+  ld.fwd_off = c0;
+  ld.fwd_cand = c1;
+  ld.rev_off = c2;
+  ld.rev_cand = c3;
+  int64_t* droff = nullptr;
+  bm_record *rec = nullptr, *dense = nullptr;
+  int32_t* cnt = nullptr;
+  double* cost = nullptr;
+  int64_t* total = nullptr;
+  BM_CK(up(&droff, roff.data(), nd), "h2d");
+  BM_CK(sc.alloc(&rec, (size_t)rt), "alloc");
+  BM_CK(sc.alloc(&dense, (size_t)rt), "alloc");
+  BM_CK(sc.alloc(&cnt, nd), "alloc");
+  BM_CK(sc.alloc(&cost, nd), "alloc");
+  BM_CK(sc.alloc(&total, 1), "alloc");
+  int rc = bm_mine(&sd, &dd, dh->n, dh->m, amax.data(), &ld, model, threshold, penalty, droff, rec,
+                   cnt, cost, stream);
+  if (rc) return rc;
+  rc = bm_compact(rec, droff, cnt, nd, dense, total, stream);
+  if (rc) return rc;
+  int64_t tot = 0;
+  BM_CK(cudaMemcpyAsync(&tot, total, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "d2h");
+  BM_CK(cudaStreamSynchronize(st), "sync");
+  if (tot > rec_cap) return fail(BM_ELIMIT, "record buffer too small");
+  if (tot) BM_CK(cudaMemcpyAsync(rec_out, dense, tot * sizeof(bm_record), cudaMemcpyDeviceToHost, st), "d2h");
+  if (cost_out) BM_CK(cudaMemcpyAsync(cost_out, cost, nd * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+  BM_CK(cudaStreamSynchronize(st), "sync");
+  *n_rec = tot;
+  return BM_OK;
+}
+
+int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+            const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
+            const double* penalties_host, int32_t n_pen, const double* thresholds, int32_t n_thr,
+            const int64_t* gold, const int64_t* gold_off, unsigned long long* pred,
+            unsigned long long* hit, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int k = 0; k < n_pen; ++k)
+    if (!check_penalty(penalties_host[k])) return fail(BM_EINVAL, "penalty must be >= 0");
+  if (n_thr > 64) return fail(BM_EINVAL, "at most 64 thresholds per call");
+  GeneralPlan g;
+  for (int d = 0; d < docs->n_docs; ++d) g.add(d, n_host[d], m_host[d]);
+  Scratch sc(st);
+  GeneralDev dv;
+  int rc = general_prepare(g, docs, sc, dv, st);
+  if (rc) return rc;
+  const int k = (int)g.docs.size();
+  const bm_docs D = local_docs(dv, k);
+  BM_CK(launch_score(*sent, D, *lex, to_model(model), dv.tiles, (int)g.tiles.size(), dv.s_off,
+                     dv.pitch, dv.S, st),
+        "score_tile_kernel");
+  double* cost_l = nullptr;
+  BM_CK(sc.alloc(&cost_l, k), "alloc");
+  for (int q = 0; q < n_pen; ++q) {
+    rc = general_nw(g, dv, penalties_host[q], cost_l, st);
+    if (rc) return rc;
+    BM_CK(launch_tune_count(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, k,
+                            thresholds, n_thr, gold, gold_off, pred + (size_t)q * n_thr,
+                            hit + (size_t)q * n_thr, st),
+          "tune_count_kernel");
+  }
+  return BM_OK;
+}
+
+}  // extern "C"

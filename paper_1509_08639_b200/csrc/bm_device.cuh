@@ -1,0 +1,289 @@
+// Device building blocks shared by the kernels: per-cell features and score
+// (bimine/classifier.py:54-117, aligner.py:332-338) and the dictionary join
+// that turns token ids into per-cell coverage hit counts (lexicon.py:88-105).
+//
+// Arithmetic order is the reference's, operation by operation:
+//   features are int/int true divisions (correctly rounded == __ddiv_rn),
+//   z = bias; z += w_k * f_k  (separately rounded multiply and add, no FMA),
+//   S = clamp(sigmoid(z)) with the glibc exp replica.
+#pragma once
+#include <stdint.h>
+
+#include "bimine_b200.h"
+#include "glibc_exp.cuh"
+
+namespace bm {
+
+constexpr int WARP = 32;
+constexpr int kExpTableWords = 256;
+
+struct Model {
+  double w[7];
+  double bias;
+};
+
+// min(a,b)/max(a,b), 1.0 when both are zero (classifier.py:62-65).
+__device__ __forceinline__ double ratio_min_max(int a, int b) {
+  if (a == 0 && b == 0) return 1.0;
+  int lo = a < b ? a : b;
+  int hi = a < b ? b : a;
+  return __ddiv_rn((double)lo, (double)hi);
+}
+
+// Python int/int true division; 0.0 for an empty denominator (lexicon.py:96-97).
+__device__ __forceinline__ double frac_or_zero(int num, int den) {
+  return den == 0 ? 0.0 : __ddiv_rn((double)num, (double)den);
+}
+
+// |D_s & D_t| for two ascending id lists (classifier.py:82-87).
+__device__ __forceinline__ int sorted_intersection(const int32_t* a, int na, const int32_t* b,
+                                                   int nb) {
+  int i = 0, j = 0, k = 0;
+  while (i < na && j < nb) {
+    int x = __ldg(a + i), y = __ldg(b + j);
+    k += (x == y);
+    i += (x <= y);
+    j += (y <= x);
+  }
+  return k;
+}
+
+// Per-sentence scalars the score needs (loaded once per row / column).
+struct SentScalars {
+  int T, P, nA, nD, d0;
+};
+
+__device__ __forceinline__ SentScalars load_scalars(const bm_sentences& S, int g) {
+  SentScalars r;
+  r.T = __ldg(S.n_tok + g);
+  r.P = __ldg(S.n_punct + g);
+  r.nA = __ldg(S.n_alpha + g);
+  r.d0 = __ldg(S.dig_off + g);
+  r.nD = __ldg(S.dig_off + g + 1) - r.d0;
+  return r;
+}
+
+// Feature vector of one cell (classifier.py:68-97). hf/hr: coverage hit counts.
+__device__ __forceinline__ void cell_features(const bm_sentences& S, const SentScalars& a,
+                                              const SentScalars& b, int hf, int hr,
+                                              double pos_s, double pos_t, double f[7]) {
+  f[0] = ratio_min_max(a.T, b.T);
+  f[1] = frac_or_zero(hf, a.nA);
+  f[2] = frac_or_zero(hr, b.nA);
+  if (a.nD == 0 && b.nD == 0) {
+    f[3] = 1.0;
+  } else {
+    int inter = (a.nD && b.nD) ? sorted_intersection(S.dig_id + a.d0, a.nD, S.dig_id + b.d0, b.nD)
+                               : 0;
+    f[3] = __ddiv_rn((double)inter, (double)(a.nD + b.nD - inter));
+  }
+  f[4] = ratio_min_max(a.P, b.P);
+  f[5] = __dsub_rn(1.0, fabs(__dsub_rn(pos_s, pos_t)));
+  f[6] = 1.0;
+}
+
+// z = bias; z += w_k * f_k (classifier.py:114-116), each op separately rounded.
+__device__ __forceinline__ double margin(const Model& M, const double f[7]) {
+  double z = M.bias;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) z = __dadd_rn(z, __dmul_rn(M.w[k], f[k]));
+  return z;
+}
+
+__device__ __forceinline__ double cell_score(const bm_sentences& S, const Model& M,
+                                             const uint64_t* exp_tab, const SentScalars& a,
+                                             const SentScalars& b, int hf, int hr, double pos_s,
+                                             double pos_t) {
+  double f[7];
+  cell_features(S, a, b, hf, hr, pos_s, pos_t, f);
+  return bmexp::confidence_from_z(margin(M, f), exp_tab);
+}
+
+// i / max(1, n-1): document position of a sentence (aligner.py:332-333).
+__device__ __forceinline__ double doc_pos(int i, int n) {
+  return __ddiv_rn((double)i, (double)(n > 1 ? n - 1 : 1));
+}
+
+// ---------------------------------------------------------------------------
+// Dictionary join. For a tile of source sentences [s0, s0+ns) x target
+// sentences [t0, t0+nt) it accumulates, per cell,
+//   hf(s,t) = sum over alpha entries a of s (with multiplicity) of
+//             [ FWD[a] intersects U_t ]                 (coverage src->tgt)
+//   hr(s,t) = same with the target's alpha entries, REV and U_s.
+// One side's U entries are bucketed by id (a counting sort into a chained hash
+// table in shared memory, chunked so any sentence length fits), the other
+// side's candidates probe it. Counts are added with shared-memory atomics into
+// packed counters: hits are order independent, so the result is deterministic.
+// ---------------------------------------------------------------------------
+
+struct JoinSmem {
+  int32_t* key;      // [emax] bucketed token ids
+  uint16_t* owner;   // [emax] local sentence index of each bucketed id
+  int32_t* bstart;   // [nbuckets + 1]
+  int32_t* bfill;    // [nbuckets]
+  int emax;
+  int nbuckets;      // power of two
+  int bshift;        // 32 - log2(nbuckets)
+};
+
+__device__ __forceinline__ uint32_t bucket_of(int32_t id, int bshift) {
+  return ((uint32_t)id * 0x9E3779B1u) >> bshift;
+}
+
+// Thread groups: whole CTA or a single warp.
+struct CtaGroup {
+  __device__ int rank() const { return threadIdx.x; }
+  __device__ int size() const { return blockDim.x; }
+  __device__ void sync() const { __syncthreads(); }
+  __device__ bool scanner() const { return threadIdx.x < WARP; }
+};
+struct WarpGroup {
+  __device__ int rank() const { return threadIdx.x & (WARP - 1); }
+  __device__ int size() const { return WARP; }
+  __device__ void sync() const { __syncwarp(); }
+  __device__ bool scanner() const { return true; }
+};
+
+// Is id present in the ascending list [p, p+n)?
+__device__ __forceinline__ bool sorted_contains(const int32_t* p, int n, int32_t id) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    int v = __ldg(p + mid);
+    if (v < id)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo < n && __ldg(p + lo) == id;
+}
+
+// One direction of the join: index side B (sentences [b0, b0+nb_sent)), probe
+// with the alpha entries of side A (sentences [a0, a0+na_sent)) through the
+// lexicon CSR (off, cand). add(la, lb, w) accumulates hits for local indices.
+template <class G, class AddFn>
+__device__ void join_direction(G g, const bm_sentences& S, const int32_t* off,
+                               const int32_t* cand, int a0, int na_sent, int b0, int nb_sent,
+                               JoinSmem& js, AddFn add) {
+  const int e_begin = __ldg(S.tok_off + b0);
+  const int e_end = __ldg(S.tok_off + b0 + nb_sent);
+  for (int c0 = e_begin; c0 < e_end; c0 += js.emax) {
+    const int c1 = min(e_end, c0 + js.emax);
+    // 1. bucket counts
+    for (int b = g.rank(); b < js.nbuckets; b += g.size()) js.bfill[b] = 0;
+    g.sync();
+    for (int k = g.rank(); k < nb_sent; k += g.size()) {
+      int e0 = max(c0, __ldg(S.tok_off + b0 + k));
+      int e1 = min(c1, __ldg(S.tok_off + b0 + k + 1));
+      for (int e = e0; e < e1; ++e) atomicAdd(&js.bfill[bucket_of(__ldg(S.tok_id + e), js.bshift)], 1);
+    }
+    g.sync();
+    if (g.scanner()) {
+      // counts live in bfill; scan into bstart and reset bfill to the starts
+      int lane = threadIdx.x & (WARP - 1);
+      int per = (js.nbuckets + WARP - 1) / WARP;
+      int q0 = lane * per, q1 = min(js.nbuckets, q0 + per);
+      int sum = 0;
+      for (int b = q0; b < q1; ++b) sum += js.bfill[b];
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < WARP; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int run = incl - sum;
+      for (int b = q0; b < q1; ++b) {
+        int c = js.bfill[b];
+        js.bstart[b] = run;
+        js.bfill[b] = run;
+        run += c;
+      }
+      if (lane == WARP - 1) js.bstart[js.nbuckets] = incl;
+    }
+    g.sync();
+    // 2. scatter ids into buckets
+    for (int k = g.rank(); k < nb_sent; k += g.size()) {
+      int e0 = max(c0, __ldg(S.tok_off + b0 + k));
+      int e1 = min(c1, __ldg(S.tok_off + b0 + k + 1));
+      for (int e = e0; e < e1; ++e) {
+        int32_t id = __ldg(S.tok_id + e);
+        int slot = atomicAdd(&js.bfill[bucket_of(id, js.bshift)], 1);
+        js.key[slot] = id;
+        js.owner[slot] = (uint16_t)k;
+      }
+    }
+    g.sync();
+    // 3. probe with side A's alpha entries
+    for (int k = g.rank(); k < na_sent; k += g.size()) {
+      const int e0 = __ldg(S.tok_off + a0 + k);
+      const int e1 = __ldg(S.tok_off + a0 + k + 1);
+      for (int e = e0; e < e1; ++e) {
+        const int w = __ldg(S.tok_alpha + e);
+        if (w == 0) continue;
+        const int32_t id = __ldg(S.tok_id + e);
+        const int q0 = __ldg(off + id), q1 = __ldg(off + id + 1);
+        for (int q = q0; q < q1; ++q) {
+          const int32_t c = __ldg(cand + q);
+          const uint32_t bk = bucket_of(c, js.bshift);
+          for (int slot = js.bstart[bk]; slot < js.bstart[bk + 1]; ++slot) {
+            if (js.key[slot] != c) continue;
+            const int lb = js.owner[slot];
+            // an entry hits a sentence once however many candidates it holds:
+            // skip if an earlier candidate of this entry is also in U_lb
+            bool dup = false;
+            if (q > q0) {
+              const int u0 = __ldg(S.tok_off + b0 + lb);
+              const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
+              for (int qq = q0; qq < q && !dup; ++qq) dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
+            }
+            if (!dup) add(k, lb, w);
+          }
+        }
+      }
+    }
+    g.sync();
+  }
+}
+
+// Full join for a tile. Hits are packed per cell into `hits` words:
+//   kPacked16: 16-bit cells, hf in bits 0-7, hr in bits 8-15 (counts <= 255)
+//   otherwise: 32-bit cells, hf in bits 0-15, hr in bits 16-31
+template <bool kPacked16, class G>
+__device__ void tile_join(G g, const bm_sentences& S, const bm_lexicon& L, int s0, int ns,
+                          int t0, int nt, uint32_t* hits, JoinSmem& js) {
+  const int ncell = ns * nt;
+  const int nwords = kPacked16 ? (ncell + 1) / 2 : ncell;
+  for (int k = g.rank(); k < nwords; k += g.size()) hits[k] = 0u;
+  g.sync();
+  // forward: source alpha entries through FWD into target U sets
+  join_direction(g, S, L.fwd_off, L.fwd_cand, s0, ns, t0, nt, js, [&](int ls, int lt, int w) {
+    int cell = ls * nt + lt;
+    if (kPacked16)
+      atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16));
+    else
+      atomicAdd(&hits[cell], (uint32_t)w);
+  });
+  // reverse: target alpha entries through REV into source U sets
+  join_direction(g, S, L.rev_off, L.rev_cand, t0, nt, s0, ns, js, [&](int lt, int ls, int w) {
+    int cell = ls * nt + lt;
+    if (kPacked16)
+      atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16 + 8));
+    else
+      atomicAdd(&hits[cell], (uint32_t)w << 16);
+  });
+}
+
+template <bool kPacked16>
+__device__ __forceinline__ void read_hits(const uint32_t* hits, int cell, int& hf, int& hr) {
+  if (kPacked16) {
+    uint32_t v = hits[cell >> 1] >> ((cell & 1) * 16);
+    hf = v & 0xff;
+    hr = (v >> 8) & 0xff;
+  } else {
+    uint32_t v = hits[cell];
+    hf = v & 0xffff;
+    hr = v >> 16;
+  }
+}
+
+}  // namespace bm

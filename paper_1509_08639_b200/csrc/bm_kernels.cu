@@ -1,0 +1,794 @@
+// sm_100a kernels of the miner hot path.
+//
+//   score_tile_kernel   K1  build_similarity_matrix   (aligner.py:313-339)
+//   nw_band_kernel      K2/K3 _nw_costs(_wavefront)  (aligner.py:116-173)
+//   traceback_kernel    K4a _traceback               (aligner.py:176-206)
+//   extract_kernel      K4b extract_pairs            (aligner.py:342-368)
+//   mine_fused_kernel   K1+K2+K4 for one document per warp (miner.py:84-128)
+//   tune_count_kernel   K5 per-(penalty, threshold) counts (tuner.py:119-145)
+//
+// Everything is fp64 with explicitly rounded intrinsics (the TU is also built
+// with -fmad=false) so every value matches the reference bit for bit.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bm_kernels.cuh"
+
+namespace bm {
+
+__device__ const uint64_t g_exp_table[kExpTableWords] = BM_EXP_TABLE_INIT;
+
+__device__ __forceinline__ void stage_exp_table(uint64_t* dst, int rank, int size) {
+  for (int k = rank; k < kExpTableWords; k += size) dst[k] = g_exp_table[k];
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+
+__device__ __forceinline__ JoinSmem carve_join(uint8_t* p) {
+  JoinSmem js;
+  js.key = (int32_t*)p;
+  p += kJoinEmax * 4;
+  js.bstart = (int32_t*)p;
+  p += (kJoinBuckets + 1) * 4;
+  js.bfill = (int32_t*)p;
+  p += kJoinBuckets * 4;
+  js.owner = (uint16_t*)p;
+  js.emax = kJoinEmax;
+  js.nbuckets = kJoinBuckets;
+  js.bshift = 32 - 9;  // log2(512)
+  return js;
+}
+
+// ---------------------------------------------------------------------------
+// K1: one CTA per 64x64 tile of one document's similarity matrix.
+// ---------------------------------------------------------------------------
+struct TileScalars {
+  int T[kTile], P[kTile], nA[kTile], nD[kTile], d0[kTile];
+  double pos[kTile];
+};
+
+__device__ __forceinline__ SentScalars get_scalars(const TileScalars& t, int k) {
+  SentScalars r;
+  r.T = t.T[k];
+  r.P = t.P[k];
+  r.nA = t.nA[k];
+  r.nD = t.nD[k];
+  r.d0 = t.d0[k];
+  return r;
+}
+
+__global__ void __launch_bounds__(kTileThreads) score_tile_kernel(
+    bm_sentences S, bm_docs D, bm_lexicon L, Model M, const int4* __restrict__ tiles,
+    const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch, double* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* exp_tab = (uint64_t*)smem;
+  uint32_t* hits = (uint32_t*)(smem + kExpTableWords * 8);
+  TileScalars* rows = (TileScalars*)(smem + kExpTableWords * 8 + kTile * kTile * 4);
+  TileScalars* cols = rows + 1;
+  JoinSmem js = carve_join((uint8_t*)(cols + 1));
+
+  const int4 tile = tiles[blockIdx.x];
+  const int doc = tile.x, r0 = tile.y, c0 = tile.z;
+  const int n = D.n[doc], m = D.m[doc];
+  const int ns = min(kTile, n - r0), nt = min(kTile, m - c0);
+  const int s0 = D.src0[doc] + r0, t0 = D.tgt0[doc] + c0;
+
+  stage_exp_table(exp_tab, threadIdx.x, blockDim.x);
+  for (int k = threadIdx.x; k < ns + nt; k += blockDim.x) {
+    const bool is_row = k < ns;
+    const int local = is_row ? k : k - ns;
+    SentScalars sc = load_scalars(S, is_row ? s0 + local : t0 + local);
+    TileScalars* dst = is_row ? rows : cols;
+    dst->T[local] = sc.T;
+    dst->P[local] = sc.P;
+    dst->nA[local] = sc.nA;
+    dst->nD[local] = sc.nD;
+    dst->d0[local] = sc.d0;
+    dst->pos[local] = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
+  }
+  tile_join<false>(CtaGroup(), S, L, s0, ns, t0, nt, hits, js);  // ends with a barrier
+
+  double* dst = out + s_off[doc] + (int64_t)r0 * pitch[doc] + c0;
+  const int64_t ld = pitch[doc];
+  for (int c = threadIdx.x; c < ns * nt; c += blockDim.x) {
+    const int i = c / nt, j = c - (c / nt) * nt;
+    int hf, hr;
+    read_hits<false>(hits, c, hf, hr);
+    dst[i * ld + j] = cell_score(S, M, exp_tab, get_scalars(*rows, i), get_scalars(*cols, j), hf,
+                                 hr, rows->pos[i], cols->pos[j]);
+  }
+}
+
+size_t score_smem_bytes() {
+  return kExpTableWords * 8 + kTile * kTile * 4 + 2 * sizeof(TileScalars) + join_smem_bytes();
+}
+
+cudaError_t launch_score(const bm_sentences& S, const bm_docs& D, const bm_lexicon& L,
+                         const Model& M, const int4* tiles, int n_tiles, const int64_t* s_off,
+                         const int32_t* pitch, double* out, cudaStream_t st) {
+  if (n_tiles == 0) return cudaSuccess;
+  const size_t sm = score_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(score_tile_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  score_tile_kernel<<<n_tiles, kTileThreads, sm, st>>>(S, D, L, M, tiles, s_off, pitch, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Features / confidence of explicit tuples (API primitives).
+// ---------------------------------------------------------------------------
+__global__ void features_kernel(bm_sentences S, bm_lexicon L, const int32_t* q_src,
+                                const int32_t* q_tgt, const double* q_ps, const double* q_pt,
+                                int n_q, double* feats) {
+  // one warp per query: a 1x1 join, then the 7 features
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int q = blockIdx.x;
+  JoinSmem js = carve_join(smem);
+  uint32_t* hit = (uint32_t*)(smem + join_smem_bytes());
+  const int s = q_src[q], t = q_tgt[q];
+  tile_join<false>(WarpGroup(), S, L, s, 1, t, 1, hit, js);
+  if (threadIdx.x == 0) {
+    int hf, hr;
+    read_hits<false>(hit, 0, hf, hr);
+    double f[7];
+    cell_features(S, load_scalars(S, s), load_scalars(S, t), hf, hr, q_ps[q], q_pt[q], f);
+    for (int k = 0; k < 7; ++k) feats[(int64_t)q * 7 + k] = f[k];
+  }
+}
+
+cudaError_t launch_features(const bm_sentences& S, const bm_lexicon& L, const int32_t* q_src,
+                            const int32_t* q_tgt, const double* ps, const double* pt, int n_q,
+                            double* feats, cudaStream_t st) {
+  if (n_q == 0) return cudaSuccess;
+  features_kernel<<<n_q, WARP, join_smem_bytes() + 16, st>>>(S, L, q_src, q_tgt, ps, pt, n_q,
+                                                              feats);
+  return cudaGetLastError();
+}
+
+__global__ void confidence_kernel(const double* __restrict__ feats, int n_q, Model M,
+                                  double* __restrict__ conf) {
+  __shared__ uint64_t exp_tab[kExpTableWords];
+  stage_exp_table(exp_tab, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_q) return;
+  double f[7];
+  for (int k = 0; k < 7; ++k) f[k] = feats[(int64_t)q * 7 + k];
+  conf[q] = bmexp::confidence_from_z(margin(M, f), exp_tab);
+}
+
+cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, double* conf,
+                              cudaStream_t st) {
+  if (n_q == 0) return cudaSuccess;
+  confidence_kernel<<<(n_q + 255) / 256, 256, 0, st>>>(feats, n_q, M, conf);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K2/K3: banded anti-diagonal wavefront.
+//
+// A document's rows are cut into bands of 128 (32 lanes x 4 rows). A warp
+// owns one band; lane L owns rows 4L..4L+3 and runs one column behind lane
+// L-1, so the value a lane needs from the row above arrives by one 64-bit
+// shuffle of the previous step (the anti-diagonal dependency). The 4 rows of a
+// lane are a short in-register chain. Bands are chained through a per-band
+// boundary row in global memory, published every kPublish columns with
+// release/acquire flags; warps are persistent and take (doc, band) items in
+// increasing order from an atomic ticket, so waits always target a band that
+// is resident or finished (no deadlock).
+// S is read with 16-byte loads, one 4-column group ahead.
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(WARP) nw_band_kernel(NwArgs a) {
+  const int lane = threadIdx.x;
+  const unsigned FULL = 0xffffffffu;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = (int)atomicAdd(a.ticket, 1u);
+    it = __shfl_sync(FULL, it, 0);
+    if (it >= a.n_items) return;
+    const WorkItem w = a.items[it];
+    const int d = w.doc, band = w.band;
+    const int n = a.n[d], m = a.m[d];
+    const double p = a.p;
+    const int row0 = band * kBandRows;
+    const int rows_here = min(kBandRows, n - row0);
+    const int nl = (rows_here + kBandR - 1) / kBandR;
+    const int nbands = (n + kBandRows - 1) / kBandRows;
+    const double* Sd = a.S + a.s_off[d];
+    const int64_t ld = a.pitch[d];
+    const int ncg = (m + kBandCols - 1) / kBandCols;
+    uint32_t* dirs = a.dirs + a.dir_off[d] + (int64_t)band * ncg * WARP + lane;
+    const double* bnd_up = band > 0 ? a.bnd + a.bnd_off[d] + (int64_t)(band - 1) * m : nullptr;
+    double* bnd_me = band < nbands - 1 ? a.bnd + a.bnd_off[d] + (int64_t)band * m : nullptr;
+    const uint32_t* prog_up = band > 0 ? a.prog + a.prog_off[d] + band - 1 : nullptr;
+    uint32_t* prog_me = a.prog + a.prog_off[d] + band;
+
+    const int i0 = row0 + lane * kBandR;  // first row of this lane
+    const int my_rows = lane < nl ? min(kBandR, n - i0) : 0;
+    double left[kBandR];
+#pragma unroll
+    for (int r = 0; r < kBandR; ++r) left[r] = (double)(i0 + r + 1) * p;  // C[i+1][0]
+    double bot = my_rows > 0 ? left[my_rows - 1] : 0.0;
+    double prev_recv = (double)i0 * p;
+    // one 4-column group of S per row, prefetched one group ahead
+    double cur[kBandR][4], nxt[kBandR][4];
+    auto load_group = [&](double (&buf)[kBandR][4], int g) {
+#pragma unroll
+      for (int r = 0; r < kBandR; ++r) {
+        if (r < my_rows && g * 4 < m) {
+          const double2* src = (const double2*)(Sd + (int64_t)(i0 + r) * ld + g * 4);
+          double2 x = __ldg(src), y = __ldg(src + 1);
+          buf[r][0] = x.x;
+          buf[r][1] = x.y;
+          buf[r][2] = y.x;
+          buf[r][3] = y.y;
+        }
+      }
+    };
+    load_group(nxt, 0);
+    uint32_t dword = 0;
+    const int steps = m + nl - 1;
+    for (int s = 0; s < steps; ++s) {
+      const int j = s - lane;
+      const bool active = lane < nl && j >= 0 && j < m;
+      // lane 0 of a lower band waits for the band above to publish column j
+      if (lane == 0 && band > 0 && j < m && (j % kPublish) == 0) {
+        const uint32_t need = (uint32_t)min(j + kPublish, m);
+        while (ld_acquire(prog_up) < need) __nanosleep(32);
+      }
+      const double recv = __shfl_up_sync(FULL, bot, 1);
+      double up, dg;
+      if (lane == 0) {
+        if (band == 0) {
+          up = (double)(j + 1) * p;
+          dg = (double)j * p;
+        } else {
+          up = j < m ? bnd_up[j] : 0.0;
+          dg = j == 0 ? (double)row0 * p : (j < m ? bnd_up[j - 1] : 0.0);
+        }
+      } else {
+        up = recv;
+        dg = prev_recv;
+      }
+      prev_recv = recv;
+      if (active) {
+        const int jj = j & 3;
+        if (jj == 0) {
+#pragma unroll
+          for (int r = 0; r < kBandR; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cur[r][c] = nxt[r][c];
+          load_group(nxt, (j >> 2) + 1);
+        }
+        uint32_t codes = 0;
+#pragma unroll
+        for (int r = 0; r < kBandR; ++r) {
+          if (r < my_rows) {
+            double sv = jj == 0 ? cur[r][0] : jj == 1 ? cur[r][1] : jj == 2 ? cur[r][2] : cur[r][3];
+            const double dcand = __dadd_rn(dg, __dsub_rn(1.0, sv));
+            const double ucand = __dadd_rn(up, p);
+            const double lcand = __dadd_rn(left[r], p);
+            double best = dcand;
+            if (ucand < best) best = ucand;
+            if (lcand < best) best = lcand;
+            const uint32_t code = best == dcand ? 0u : (best == ucand ? 1u : 2u);
+            codes |= code << (2 * r);
+            dg = left[r];
+            left[r] = best;
+            up = best;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kBandR; ++r)
+          if (r == my_rows - 1) bot = left[r];
+        dword |= codes << (8 * jj);
+        if (jj == 3 || j == m - 1) {
+          dirs[(int64_t)(j >> 2) * WARP] = dword;
+          dword = 0;
+        }
+        if (bnd_me != nullptr && lane == nl - 1) {
+          bnd_me[j] = bot;
+          if (((j + 1) % kPublish) == 0 || j == m - 1) st_release(prog_me, (uint32_t)(j + 1));
+        }
+      }
+    }
+    // C[n][m] lives in the last band, in the lane that owns row n-1
+    if (band == nbands - 1 && lane == (n - 1 - row0) / kBandR) {
+#pragma unroll
+      for (int r = 0; r < kBandR; ++r)
+        if (i0 + r == n - 1) a.cost[d] = left[r];
+    }
+  }
+}
+
+cudaError_t launch_nw(const NwArgs& a, int n_warps, cudaStream_t st) {
+  if (a.n_items == 0) return cudaSuccess;
+  nw_band_kernel<<<n_warps, WARP, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+int nw_resident_warps() {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel, WARP, 0);
+  if (per_sm < 1) per_sm = 1;
+  return sms * per_sm;
+}
+
+// ---------------------------------------------------------------------------
+// K4: traceback over the 2-bit codes (tie order D > GS > GT is baked into the
+// codes; borders walk GS on column 0 and GT on row 0, aligner.py:176-206).
+// One thread per document; codes are read through L1 with the next group to
+// the left prefetched.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t band_code(const uint32_t* dirs, int ncg, int i, int j) {
+  const int band = i / kBandRows;
+  const int li = i - band * kBandRows;
+  const uint32_t wv = __ldg(dirs + ((int64_t)band * ncg + (j >> 2)) * WARP + (li >> 2));
+  return (wv >> (8 * (j & 3) + 2 * (li & 3))) & 3u;
+}
+
+__global__ void traceback_kernel(const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+                                 const int32_t* __restrict__ nn, const int32_t* __restrict__ mm,
+                                 int n_docs, const int64_t* __restrict__ mv_off, int8_t* mv_op,
+                                 int32_t* mv_i, int32_t* mv_j, int32_t* mv_len) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n_docs) return;
+  const int n = nn[d], m = mm[d];
+  const int ncg = (m + kBandCols - 1) / kBandCols;
+  const uint32_t* dd = dirs + dir_off[d];
+  const int64_t base = mv_off[d];
+  int i = n, j = m, k = 0;
+  while (i > 0 || j > 0) {
+    int op;
+    if (i > 0 && j > 0)
+      op = (int)band_code(dd, ncg, i - 1, j - 1);
+    else
+      op = i > 0 ? BM_MOVE_GS : BM_MOVE_GT;
+    mv_op[base + k] = (int8_t)op;
+    mv_i[base + k] = op == BM_MOVE_GT ? -1 : i - 1;
+    mv_j[base + k] = op == BM_MOVE_GS ? -1 : j - 1;
+    ++k;
+    if (op == BM_MOVE_D) {
+      --i;
+      --j;
+    } else if (op == BM_MOVE_GS) {
+      --i;
+    } else {
+      --j;
+    }
+  }
+  mv_len[d] = k;  // moves are stored in reverse path order
+}
+
+cudaError_t launch_traceback(const uint32_t* dirs, const int64_t* dir_off, const int32_t* n,
+                             const int32_t* m, int n_docs, const int64_t* mv_off, int8_t* op,
+                             int32_t* mi, int32_t* mj, int32_t* len, cudaStream_t st) {
+  if (n_docs == 0) return cudaSuccess;
+  traceback_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, n, m, n_docs, mv_off, op,
+                                                          mi, mj, len);
+  return cudaGetLastError();
+}
+
+__global__ void extract_kernel(const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+                               const double* __restrict__ S, const int64_t* __restrict__ s_off,
+                               const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
+                               const int32_t* __restrict__ mm, int n_docs, double threshold,
+                               const int64_t* __restrict__ rec_off, bm_record* rec,
+                               int32_t* rec_count) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n_docs) return;
+  const int n = nn[d], m = mm[d];
+  const int ncg = (m + kBandCols - 1) / kBandCols;
+  const uint32_t* dd = dirs + dir_off[d];
+  const double* Sd = S + s_off[d];
+  const int64_t ld = pitch[d];
+  const int cap = min(n, m);
+  bm_record* out = rec + rec_off[d];
+  int i = n, j = m, k = 0;
+  while (i > 0 && j > 0) {
+    const uint32_t op = band_code(dd, ncg, i - 1, j - 1);
+    if (op == BM_MOVE_D) {
+      const double c = Sd[(int64_t)(i - 1) * ld + (j - 1)];
+      if (c >= threshold) {
+        ++k;
+        bm_record r;
+        r.doc = d;
+        r.i = i - 1;
+        r.j = j - 1;
+        r.pad = 0;
+        r.conf = c;
+        out[cap - k] = r;  // filled back to front
+      }
+      --i;
+      --j;
+    } else if (op == BM_MOVE_GS) {
+      --i;
+    } else {
+      --j;
+    }
+  }
+  for (int q = 0; q < k; ++q) out[q] = out[cap - k + q];
+  rec_count[d] = k;
+}
+
+cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const double* S,
+                           const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+                           const int32_t* m, int n_docs, double thr, const int64_t* rec_off,
+                           bm_record* rec, int32_t* cnt, cudaStream_t st) {
+  if (n_docs == 0) return cudaSuccess;
+  extract_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, S, s_off, pitch, n, m, n_docs,
+                                                        thr, rec_off, rec, cnt);
+  return cudaGetLastError();
+}
+
+// extract_pairs for an explicit path (API primitive): gather S at the given
+// cells and compare with the threshold (aligner.py:352-357).
+__global__ void select_kernel(const double* __restrict__ S, int64_t pitch, const int32_t* ci,
+                              const int32_t* cj, int k, double thr, double* conf, uint8_t* keep) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= k) return;
+  const double c = S[(int64_t)ci[q] * pitch + cj[q]];
+  conf[q] = c;
+  keep[q] = c >= thr ? 1 : 0;
+}
+
+cudaError_t launch_select(const double* S, int64_t pitch, const int32_t* ci, const int32_t* cj,
+                          int k, double thr, double* conf, uint8_t* keep, cudaStream_t st) {
+  if (k == 0) return cudaSuccess;
+  select_kernel<<<(k + 255) / 256, 256, 0, st>>>(S, pitch, ci, cj, k, thr, conf, keep);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Fused miner: one warp (= one CTA) per document, nothing but the records
+// leaves the SM. Shared memory per warp:
+//   [hits: n*m 16-bit cells][ region2: join buffers | (dirs + D list) ]
+// The DP is the same lane-skewed wavefront as K2 but with R = 1..8 rows per
+// lane (n <= 256) and the cell score computed inline where the DP needs it.
+// ---------------------------------------------------------------------------
+int fused_rows_per_lane(int n) {
+  int r = (n + WARP - 1) / WARP;
+  if (r <= 1) return 1;
+  if (r <= 2) return 2;
+  if (r <= 4) return 4;
+  return 8;
+}
+
+
+size_t fused_slice_bytes(int n, int m) {
+  const int R = fused_rows_per_lane(n);
+  const int cpw = 16 / R;
+  const size_t hits = align16(((size_t)n * m + 1) / 2 * 4);
+  const size_t dirs = (size_t)((m + cpw - 1) / cpw) * WARP * 4;
+  const size_t dlist = (size_t)(n < m ? n : m) * 4;
+  const size_t r2 = join_smem_bytes() > dirs + dlist ? join_smem_bytes() : dirs + dlist;
+  return kExpTableWords * 8 + hits + align16(r2);
+}
+
+
+template <int R>
+__global__ void __launch_bounds__(WARP) mine_fused_kernel(FusedArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int CPW = 16 / R;  // columns per direction word
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x;
+  const int doc = a.list[blockIdx.x];
+  const int n = a.D.n[doc], m = a.D.m[doc];
+  const int s0 = a.D.src0[doc], t0 = a.D.tgt0[doc];
+  const double p = a.p;
+  const bm_sentences& S = a.S;
+
+  uint64_t* exp_tab = (uint64_t*)smem;
+  uint32_t* hits = (uint32_t*)(smem + kExpTableWords * 8);
+  uint8_t* region2 = (uint8_t*)hits + align16(((size_t)n * m + 1) / 2 * 4);
+  stage_exp_table(exp_tab, lane, WARP);
+  JoinSmem js = carve_join(region2);
+  tile_join<true>(WarpGroup(), S, a.L, s0, n, t0, m, hits, js);  // ends with __syncwarp
+
+  uint32_t* dirs = (uint32_t*)region2;  // the join buffers are dead now
+  const int ncg = (m + CPW - 1) / CPW;
+  int32_t* dlist = (int32_t*)(dirs + (size_t)ncg * WARP);
+
+  const int nl = (n + R - 1) / R;
+  const int i0 = lane * R;
+  const int my_rows = lane < nl ? min(R, n - i0) : 0;
+  SentScalars rs[R];
+  double rpos[R], left[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    left[r] = (double)(i0 + r + 1) * p;
+    if (r < my_rows) {
+      rs[r] = load_scalars(S, s0 + i0 + r);
+      rpos[r] = doc_pos(i0 + r, n);
+    }
+  }
+  double bot = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r == my_rows - 1) bot = left[r];
+  double prev_recv = (double)i0 * p;
+  uint32_t dword = 0;
+  const int steps = m + nl - 1;
+  for (int s = 0; s < steps; ++s) {
+    const int j = s - lane;
+    const double recv = __shfl_up_sync(FULL, bot, 1);
+    double up, dg;
+    if (lane == 0) {
+      up = (double)(j + 1) * p;
+      dg = (double)j * p;
+    } else {
+      up = recv;
+      dg = prev_recv;
+    }
+    prev_recv = recv;
+    if (lane < nl && j >= 0 && j < m) {
+      const SentScalars cs = load_scalars(S, t0 + j);
+      const double cpos = doc_pos(j, m);
+      uint32_t codes = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r < my_rows) {
+          int hf, hr;
+          read_hits<true>(hits, (i0 + r) * m + j, hf, hr);
+          const double sv = cell_score(S, a.M, exp_tab, rs[r], cs, hf, hr, rpos[r], cpos);
+          const double dcand = __dadd_rn(dg, __dsub_rn(1.0, sv));
+          const double ucand = __dadd_rn(up, p);
+          const double lcand = __dadd_rn(left[r], p);
+          double best = dcand;
+          if (ucand < best) best = ucand;
+          if (lcand < best) best = lcand;
+          const uint32_t code = best == dcand ? 0u : (best == ucand ? 1u : 2u);
+          codes |= code << (2 * r);
+          dg = left[r];
+          left[r] = best;
+          up = best;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r == my_rows - 1) bot = left[r];
+      const int slot = j % CPW;
+      dword |= codes << (2 * R * slot);
+      if (slot == CPW - 1 || j == m - 1) {
+        dirs[(j / CPW) * WARP + lane] = dword;
+        dword = 0;
+      }
+    }
+  }
+  if (lane == (n - 1) / R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (i0 + r == n - 1) a.cost[doc] = left[r];
+  }
+  __syncwarp();
+
+  // traceback (lane 0) collecting the diagonal cells, reverse path order
+  int K = 0;
+  if (lane == 0) {
+    int i = n, j = m;
+    while (i > 0 && j > 0) {
+      const int ci = i - 1, cj = j - 1;
+      const uint32_t wv = dirs[(cj / CPW) * WARP + ci / R];
+      const uint32_t op = (wv >> (2 * R * (cj % CPW) + 2 * (ci % R))) & 3u;
+      if (op == BM_MOVE_D) {
+        dlist[K++] = ci * m + cj;
+        --i;
+        --j;
+      } else if (op == BM_MOVE_GS) {
+        --i;
+      } else {
+        --j;
+      }
+    }
+  }
+  K = __shfl_sync(FULL, K, 0);
+  __syncwarp();
+
+  // threshold + order-preserving warp compaction (extract_pairs)
+  bm_record* out = a.rec + a.rec_off[doc];
+  int base = 0;
+  for (int f0 = 0; f0 < K; f0 += WARP) {
+    const int f = f0 + lane;
+    bool keep = false;
+    int ci = 0, cj = 0;
+    double sv = 0.0;
+    if (f < K) {
+      const int cell = dlist[K - 1 - f];
+      ci = cell / m;
+      cj = cell - ci * m;
+      int hf, hr;
+      read_hits<true>(hits, cell, hf, hr);
+      sv = cell_score(S, a.M, exp_tab, load_scalars(S, s0 + ci), load_scalars(S, t0 + cj), hf, hr,
+                      doc_pos(ci, n), doc_pos(cj, m));
+      keep = sv >= a.threshold;
+    }
+    const unsigned mask = __ballot_sync(FULL, keep);
+    if (keep) {
+      bm_record r;
+      r.doc = doc;
+      r.i = ci;
+      r.j = cj;
+      r.pad = 0;
+      r.conf = sv;
+      out[base + __popc(mask & ((1u << lane) - 1u))] = r;
+    }
+    base += __popc(mask);
+  }
+  if (lane == 0) a.rec_count[doc] = base;
+}
+
+cudaError_t launch_fused(const FusedArgs& a, int R, size_t smem, cudaStream_t st) {
+  if (a.n_list == 0) return cudaSuccess;
+  cudaError_t e;
+#define BM_LAUNCH_FUSED(RR)                                                                   \
+  e = cudaFuncSetAttribute(mine_fused_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                        \
+  if (e != cudaSuccess) return e;                                                             \
+  mine_fused_kernel<RR><<<a.n_list, WARP, smem, st>>>(a);
+  switch (R) {
+    case 1: BM_LAUNCH_FUSED(1); break;
+    case 2: BM_LAUNCH_FUSED(2); break;
+    case 4: BM_LAUNCH_FUSED(4); break;
+    case 8: BM_LAUNCH_FUSED(8); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef BM_LAUNCH_FUSED
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K5: per-(penalty, threshold) prediction and gold-hit counts of one penalty.
+// One thread per document walks its path; a warp reduces before the atomics.
+// ---------------------------------------------------------------------------
+constexpr int kMaxThr = 64;
+
+__global__ void tune_count_kernel(const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+                                  const double* __restrict__ S, const int64_t* __restrict__ s_off,
+                                  const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
+                                  const int32_t* __restrict__ mm, int n_docs,
+                                  const double* __restrict__ thr, int n_thr,
+                                  const int64_t* __restrict__ gold,
+                                  const int64_t* __restrict__ gold_off, unsigned long long* pred,
+                                  unsigned long long* hit) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t cp[kMaxThr], ch[kMaxThr];
+  for (int l = 0; l < n_thr; ++l) cp[l] = ch[l] = 0;
+  if (d < n_docs) {
+    const int n = nn[d], m = mm[d];
+    const int ncg = (m + kBandCols - 1) / kBandCols;
+    const uint32_t* dd = dirs + dir_off[d];
+    const double* Sd = S + s_off[d];
+    const int64_t ld = pitch[d];
+    const int64_t g0 = gold_off[d], g1 = gold_off[d + 1];
+    int i = n, j = m;
+    while (i > 0 && j > 0) {
+      const uint32_t op = band_code(dd, ncg, i - 1, j - 1);
+      if (op == BM_MOVE_D) {
+        const double c = Sd[(int64_t)(i - 1) * ld + (j - 1)];
+        const int64_t key = (int64_t)(i - 1) * m + (j - 1);
+        int64_t lo = g0, hi = g1;
+        while (lo < hi) {
+          int64_t mid = (lo + hi) >> 1;
+          if (gold[mid] < key)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        const uint32_t g = (lo < g1 && gold[lo] == key) ? 1u : 0u;
+        for (int l = 0; l < n_thr; ++l) {
+          const uint32_t ok = c >= thr[l] ? 1u : 0u;
+          cp[l] += ok;
+          ch[l] += ok & g;
+        }
+        --i;
+        --j;
+      } else if (op == BM_MOVE_GS) {
+        --i;
+      } else {
+        --j;
+      }
+    }
+  }
+  for (int l = 0; l < n_thr; ++l) {
+    const uint32_t sp = __reduce_add_sync(0xffffffffu, cp[l]);
+    const uint32_t sh = __reduce_add_sync(0xffffffffu, ch[l]);
+    if ((threadIdx.x & 31) == 0) {
+      if (sp) atomicAdd(pred + l, (unsigned long long)sp);
+      if (sh) atomicAdd(hit + l, (unsigned long long)sh);
+    }
+  }
+}
+
+cudaError_t launch_tune_count(const uint32_t* dirs, const int64_t* dir_off, const double* S,
+                              const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+                              const int32_t* m, int n_docs, const double* thr, int n_thr,
+                              const int64_t* gold, const int64_t* gold_off,
+                              unsigned long long* pred, unsigned long long* hit, cudaStream_t st) {
+  if (n_docs == 0) return cudaSuccess;
+  if (n_thr > kMaxThr) return cudaErrorInvalidValue;
+  tune_count_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, S, s_off, pitch, n, m,
+                                                           n_docs, thr, n_thr, gold, gold_off, pred,
+                                                           hit);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Record compaction: exclusive scan of per-doc counts (one CTA, chunked) and
+// a warp-per-doc gather into a dense, document-ordered array.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) scan_counts_kernel(const int32_t* __restrict__ cnt, int n,
+                                                           int64_t* __restrict__ off,
+                                                           int64_t* __restrict__ total) {
+  __shared__ int64_t warp_sums[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int k = c0 + threadIdx.x;
+    const int64_t v = k < n ? cnt[k] : 0;
+    int64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+      int64_t wi = ws;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t u = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += u;
+      }
+      warp_sums[lane] = wi - ws;
+    }
+    __syncthreads();
+    const int64_t base = carry;
+    if (k < n) off[k] = base + warp_sums[wid] + incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = base + warp_sums[wid] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void gather_records_kernel(const bm_record* __restrict__ rec,
+                                      const int64_t* __restrict__ rec_off,
+                                      const int32_t* __restrict__ cnt,
+                                      const int64_t* __restrict__ dense_off, int n_docs,
+                                      bm_record* __restrict__ dense) {
+  const int d = blockIdx.x * (blockDim.x / WARP) + threadIdx.x / WARP;
+  if (d >= n_docs) return;
+  const int lane = threadIdx.x & (WARP - 1);
+  const bm_record* src = rec + rec_off[d];
+  bm_record* dst = dense + dense_off[d];
+  for (int k = lane; k < cnt[d]; k += WARP) dst[k] = src[k];
+}
+
+cudaError_t launch_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* cnt,
+                           int n_docs, int64_t* dense_off, int64_t* total, bm_record* dense,
+                           cudaStream_t st) {
+  if (n_docs == 0) return cudaMemsetAsync(total, 0, sizeof(int64_t), st);
+  scan_counts_kernel<<<1, 1024, 0, st>>>(cnt, n_docs, dense_off, total);
+  gather_records_kernel<<<(n_docs + 7) / 8, 256, 0, st>>>(rec, rec_off, cnt, dense_off, n_docs,
+                                                          dense);
+  return cudaGetLastError();
+}
+
+}  // namespace bm

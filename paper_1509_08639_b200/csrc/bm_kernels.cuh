@@ -1,0 +1,103 @@
+// Kernel declarations and launch-shape constants shared by bm_kernels.cu and
+// bm_api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bm_device.cuh"
+
+namespace bm {
+
+// K1 tile shape and join capacity.
+constexpr int kTile = 64;              // 64 x 64 cells per CTA
+constexpr int kTileThreads = 256;
+constexpr int kJoinEmax = 1024;        // bucketed ids per join chunk
+constexpr int kJoinBuckets = 512;
+
+// Banded NW (K2/K3): 4 rows per lane, 128 rows per warp band.
+constexpr int kBandR = 4;
+constexpr int kBandRows = WARP * kBandR;
+constexpr int kBandCols = 16 / kBandR;   // columns per packed direction word
+constexpr int kPublish = 16;             // boundary publication granularity
+
+// Fused miner limits (warp per document, everything in shared memory).
+constexpr int kFusedMaxRows = 256;       // n <= 32 * 8
+constexpr int kFusedMaxSmem = 200 * 1024;
+
+struct WorkItem {
+  int32_t doc;
+  int32_t band;
+};
+
+__host__ __device__ constexpr size_t join_smem_bytes() {
+  return (size_t)kJoinEmax * 4 + (size_t)kJoinEmax * 2 + (size_t)(kJoinBuckets + 1) * 4 +
+         (size_t)kJoinBuckets * 4;
+}
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+int fused_rows_per_lane(int n);
+size_t fused_slice_bytes(int n, int m);
+
+__host__ __device__ inline int64_t band_dirs_words(int32_t n, int32_t m) {
+  int64_t nb = (n + kBandRows - 1) / kBandRows;
+  int64_t ncg = (m + kBandCols - 1) / kBandCols;
+  return nb * ncg * WARP;
+}
+
+struct NwArgs {
+  const double* S;
+  const int64_t* s_off;
+  const int32_t* pitch;
+  const int32_t* n;
+  const int32_t* m;
+  double p;
+  uint32_t* dirs;
+  const int64_t* dir_off;
+  double* cost;
+  const WorkItem* items;
+  int n_items;
+  unsigned int* ticket;
+  double* bnd;               // boundary rows
+  const int64_t* bnd_off;    // per doc: start of its (nb-1) x m boundary rows
+  uint32_t* prog;            // per band publication progress (columns)
+  const int64_t* prog_off;   // per doc
+};
+
+struct FusedArgs {
+  bm_sentences S;
+  bm_docs D;
+  bm_lexicon L;
+  Model M;
+  double threshold;
+  double p;
+  const int32_t* list;
+  int n_list;
+  const int64_t* rec_off;
+  bm_record* rec;
+  int32_t* rec_count;
+  double* cost;
+};
+
+cudaError_t launch_score(const bm_sentences&, const bm_docs&, const bm_lexicon&, const Model&,
+                         const int4*, int, const int64_t*, const int32_t*, double*, cudaStream_t);
+cudaError_t launch_features(const bm_sentences&, const bm_lexicon&, const int32_t*, const int32_t*,
+                            const double*, const double*, int, double*, cudaStream_t);
+cudaError_t launch_confidence(const double*, int, const Model&, double*, cudaStream_t);
+cudaError_t launch_nw(const NwArgs&, int, cudaStream_t);
+int nw_resident_warps();
+cudaError_t launch_traceback(const uint32_t*, const int64_t*, const int32_t*, const int32_t*, int,
+                             const int64_t*, int8_t*, int32_t*, int32_t*, int32_t*, cudaStream_t);
+cudaError_t launch_extract(const uint32_t*, const int64_t*, const double*, const int64_t*,
+                           const int32_t*, const int32_t*, const int32_t*, int, double,
+                           const int64_t*, bm_record*, int32_t*, cudaStream_t);
+cudaError_t launch_fused(const FusedArgs&, int, size_t, cudaStream_t);
+cudaError_t launch_tune_count(const uint32_t*, const int64_t*, const double*, const int64_t*,
+                              const int32_t*, const int32_t*, const int32_t*, int, const double*,
+                              int, const int64_t*, const int64_t*, unsigned long long*,
+                              unsigned long long*, cudaStream_t);
+cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int, int64_t*,
+                           int64_t*, bm_record*, cudaStream_t);
+size_t score_smem_bytes();
+cudaError_t launch_select(const double*, int64_t, const int32_t*, const int32_t*, int, double,
+                          double*, uint8_t*, cudaStream_t);
+
+}  // namespace bm

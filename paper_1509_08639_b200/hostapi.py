@@ -1,0 +1,85 @@
+"""End-to-end call through the C ABI with HOST buffers (bm_mine_host).
+
+This is what a foreign binding of the reference's mining API would call: the
+packed corpus, lexicon and model live in host memory; one call copies them to
+the GPU, mines every document, compacts the records and copies them back in
+document order. ``PinnedBatch`` stages the arrays in page-locked memory once
+so the per-call H2D copies run at full PCIe/C2C bandwidth.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .pack import PackedCorpus, PackedLexicon
+
+_SENT = ("n_tok", "n_punct", "n_alpha", "tok_off", "tok_id", "tok_alpha", "dig_off", "dig_id")
+_DOCS = ("src0", "n", "tgt0", "m")
+_LEX = ("fwd_off", "fwd_cand", "rev_off", "rev_cand")
+
+
+def _pinned(a: np.ndarray) -> tuple[object, np.ndarray]:
+    import torch
+
+    a = np.ascontiguousarray(a)
+    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    view = t.numpy().view(a.dtype).reshape(a.shape)
+    view[...] = a
+    return t, view
+
+
+class PinnedBatch:
+    """Packed arrays copied once into page-locked host memory + C structs."""
+
+    def __init__(self, corpus: PackedCorpus, plex: PackedLexicon, pin: bool = True):
+        self.keep = []
+        arrs = {}
+        for name in _SENT + _DOCS:
+            arrs[name] = getattr(corpus, name)
+        for name in _LEX:
+            arrs[name] = getattr(plex, name)
+        self.h2d_bytes = 0
+        for k, v in arrs.items():
+            if pin:
+                t, view = _pinned(v)
+                self.keep.append(t)
+            else:
+                view = np.ascontiguousarray(v)
+            arrs[k] = view
+            self.keep.append(view)
+            self.h2d_bytes += view.nbytes
+        self.arrs = arrs
+        self.sent = N.Sentences(corpus.n_sent, *[arrs[k].ctypes.data for k in _SENT])
+        self.docs = N.Docs(corpus.n_docs, *[arrs[k].ctypes.data for k in _DOCS])
+        self.lex = N.LexiconC(plex.n_ids, *[arrs[k].ctypes.data for k in _LEX])
+        n, m = arrs["n"], arrs["m"]
+        self.rec_cap = int(np.minimum(n, m).clip(min=0).sum())
+        self.n_docs = corpus.n_docs
+        if pin:
+            self.rec_t, self.rec = _pinned(np.zeros(max(self.rec_cap, 1), dtype=np.dtype(N.RECORD_DTYPE)))
+            self.cost_t, self.cost = _pinned(np.zeros(max(self.n_docs, 1), dtype=np.float64))
+        else:
+            self.rec = np.zeros(max(self.rec_cap, 1), dtype=np.dtype(N.RECORD_DTYPE))
+            self.cost = np.zeros(max(self.n_docs, 1), dtype=np.float64)
+
+
+def mine_pinned(pb: PinnedBatch, model, threshold: float, penalty: float, stream: int = 0):
+    """One bm_mine_host call; returns (records view, n_records, d2h bytes)."""
+    lib = N.lib()
+    n_rec = C.c_int64(0)
+    N.check(lib.bm_mine_host(C.byref(pb.sent), C.byref(pb.docs), C.byref(pb.lex),
+                             C.byref(N.model_struct(model)), float(threshold), float(penalty),
+                             pb.rec.ctypes.data, pb.rec_cap, C.byref(n_rec), pb.cost.ctypes.data,
+                             stream))
+    k = n_rec.value
+    d2h = k * 24 + pb.n_docs * 8 + 8
+    return pb.rec[:k], k, d2h
+
+
+def mine_host(corpus: PackedCorpus, plex: PackedLexicon, model, threshold: float, penalty: float):
+    pb = PinnedBatch(corpus, plex, pin=False)
+    recs, k, _ = mine_pinned(pb, model, threshold, penalty)
+    return recs.copy(), pb.cost[: pb.n_docs].copy()

@@ -1,0 +1,336 @@
+"""GPU parity: the sm_100a path against the reference's golden outputs and the
+(pinned) CPU oracle. Bit-exact for every score, cost, path and record."""
+
+import hashlib
+import io
+import json
+import math
+
+import numpy as np
+import pytest
+
+import paper_1509_08639_b200 as bm
+from conftest import dp_cases, golden, load_docs, moves_from_ops, pairs_of, stacked, stress_lexicon
+from oracle_pipeline import oracle_mine_text
+from test_oracle_golden import REGEN
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+# ---------------------------------------------------------------- K1 scoring
+def test_scores_docs40_bit_exact(world500):
+    lex, fwd, _ = world500
+    got = bm.build_similarity_matrices(pairs_of(load_docs("docs40.jsonl")), fwd, lex)
+    for g, w in zip(got, stacked("S40.npz")):
+        assert np.array_equal(bits(g.cells), bits(w))
+
+
+def test_scores_200x200_bit_exact(world5k):
+    lex, fwd, _ = world5k
+    got = bm.build_similarity_matrix(pairs_of(load_docs("doc200.jsonl"))[0], fwd, lex)
+    assert np.array_equal(bits(got.cells), bits(np.load(golden("S200.npz"))["S"]))
+
+
+def test_scores_stress_bit_exact():
+    lex = stress_lexicon()
+    model = bm.load_model(golden("model_stress.json"))
+    got = bm.build_similarity_matrices(pairs_of(load_docs("docs_stress.jsonl")), model, lex)
+    for g, w in zip(got, stacked("S_stress.npz")):
+        assert np.array_equal(bits(g.cells), bits(w))
+
+
+def test_confidence_exp_sweep(oracle_mod):
+    """bm_confidence over 200k margins == libm-based oracle (glibc exp port)."""
+    rng = np.random.default_rng(1)
+    z = np.concatenate([rng.uniform(-40, 40, 150000), rng.uniform(-800, 800, 50000),
+                        [0.0, -0.0, 1e-300, -1e-300, 700.0, -745.0, -1100.0]])
+    feats = np.zeros((z.size, 7))
+    feats[:, 0] = 1.0
+    model = bm.ClassifierModel("pairwise-v1", [1.0] + [0.0] * 6, 0.0, ("a", "b"), 0.5, 0.2)
+    from paper_1509_08639_b200 import engine
+
+    out = np.empty(z.size)
+    for k0 in range(0, z.size, 50000):
+        f = feats[k0 : k0 + 50000].copy()
+        f[:, 0] = z[k0 : k0 + 50000]
+        out[k0 : k0 + 50000] = engine.confidences(f, model)
+    w = np.array([1.0] + [0.0] * 6)
+    import ctypes
+
+    want = np.array([oracle_mod.lib().oracle_confidence(w.ctypes.data, 0.0,
+                     np.array([x, 0, 0, 0, 0, 0, 0.0]).ctypes.data) for x in z])
+    assert np.array_equal(bits(out), bits(want))
+
+
+def test_single_cell_confidence_known_answer():
+    # test_miner.py:79-93: all-zero weights, bias 2 -> sigmoid(2)
+    model = bm.ClassifierModel("pairwise-v1", [0.0] * 7, 2.0, ("xx", "yy"), 0.5, 0.2)
+    f = bm.FeatureVector(values=[0.3, 0.9, 0.1, 1.0, 0.5, 0.7, 1.0])
+    assert bm.confidence(model, f) == 1.0 / (1.0 + math.exp(-2.0))
+    zero = bm.ClassifierModel("pairwise-v1", [0.0] * 7, 0.0, ("xx", "yy"), 0.5, 0.2)
+    assert bm.confidence(zero, f) == 0.5
+
+
+def test_features_and_coverage_vs_oracle(oracle_mod):
+    lex = stress_lexicon()
+    pairs = pairs_of(load_docs("docs_stress.jsonl"))
+    sents_s = [s for p in pairs for s in p.source.sentences]
+    sents_t = [s for p in pairs for s in p.target.sentences]
+    rng = np.random.default_rng(3)
+    items = [(sents_s[rng.integers(len(sents_s))], sents_t[rng.integers(len(sents_t))],
+              float(rng.random()), float(rng.random())) for _ in range(64)]
+    got = bm.classifier._features_batch(items, lex)
+    from paper_1509_08639_b200.pack import Packer, pack_lexicon
+
+    pk = Packer()
+    idx = [pk.add_sentence_pair(a, b) for a, b, _, _ in items]
+    corpus = pk.finish()
+    hb = oracle_mod.HostBatch(corpus, pack_lexicon(lex, corpus))
+    for k, ((a, b), (_, _, ps, pt)) in enumerate(zip(idx, items)):
+        want = oracle_mod.features(hb, a, b, ps, pt)
+        assert np.array_equal(bits(got[k]), bits(want))
+    # the lexicon.coverage API primitive (lexicon.py:88-105 known answers)
+    simple = bm.Lexicon(("xx", "yy"), {"hund": [("dog", 0.9)], "katze": [("cat", 0.8)]})
+    assert bm.coverage(simple, ["hund", "katze"], ["dog", "fish"]) == 0.5
+    assert bm.coverage(simple, ["Hund"], ["DOG"]) == 1.0
+    assert bm.coverage(simple, ["42", "."], ["dog"]) == 0.0
+
+
+# ---------------------------------------------------------------- K2/K3/K4a DP
+@pytest.mark.parametrize("name", ["dp_grid2x2.npz", "dp_s202.npz", "dp_s12_tiles.npz",
+                                  "dp_quantized.npz", "dp_s31_shapes.npz", "dp_s303_2000.npz"])
+def test_dp_matches_reference(name):
+    mats = REGEN(name)
+    cases = dp_cases(name)
+    by_p: dict[float, list[int]] = {}
+    for k, p in enumerate(mats["p"]):
+        by_p.setdefault(p, []).append(k)
+    for p, ks in by_p.items():
+        paths = bm.aligner.align_many([bm.SimilarityMatrix(mats["S"][k]) for k in ks], p)
+        for k, path in zip(ks, paths):
+            shape, cost, ops = cases[k]
+            assert path.total_cost == cost
+            assert path.moves == moves_from_ops(ops)
+
+
+def test_dp_known_answers():
+    # test_aligner.py:150-177
+    p = bm.nw_align(bm.SimilarityMatrix(np.array([[1.0, 0.0], [0.0, 1.0]])), 0.5)
+    assert p.total_cost == 0.0 and [m.op for m in p.moves] == ["D", "D"]
+    p = bm.nw_align(bm.SimilarityMatrix(np.array([[0.9]])), 0.5)
+    assert p.moves == [bm.Move("D", 0, 0)] and abs(p.total_cost - 0.1) < 1e-12
+    p = bm.nw_align(bm.SimilarityMatrix(np.zeros((2, 2))), 0.1)
+    assert [m.op for m in p.moves] == ["GT", "GT", "GS", "GS"]
+    p = bm.nw_align(bm.SimilarityMatrix(np.array([[1.0, 1.0]])), 0.2)
+    assert [m.op for m in p.moves].count("GT") == 1
+    S = bm.SimilarityMatrix(np.array([[0.9, 0.0], [0.0, 0.8]]))
+    assert bm.format_path(bm.nw_align(S, 0.5), S) == ["D 0 0 0.100000", "D 1 1 0.200000",
+                                                       "TOTAL 0.300000"]
+
+
+def test_dp_penalty_edges(oracle_mod):
+    rng = np.random.default_rng(9)
+    for p in (0.0, float("inf"), 1e300, 5e-324):
+        for shape in ((1, 1), (3, 7), (200, 150)):
+            S = rng.random(shape)
+            got = bm.nw_align(bm.SimilarityMatrix(S), p)
+            c, ops, _, _ = oracle_mod.nw(S, p)
+            assert (got.total_cost == c) or (math.isnan(c) and math.isnan(got.total_cost))
+            assert got.moves == moves_from_ops(ops)
+    with pytest.raises(ValueError, match="penalty"):
+        bm.nw_align(bm.SimilarityMatrix(np.eye(2)), -0.1)
+    with pytest.raises(ValueError, match="penalty"):
+        bm.nw_align(bm.SimilarityMatrix(np.eye(2)), float("nan"))
+
+
+def test_dp_long_pair_vs_oracle(oracle_mod):
+    """A 4096 x 3000 DP (multi-band, inter-warp boundary handoff)."""
+    S = np.random.default_rng(4).random((4096, 3000))
+    got = bm.nw_align(bm.SimilarityMatrix(S), 0.25)
+    c, ops, _, _ = oracle_mod.nw(S, 0.25)
+    assert got.total_cost == c
+    assert got.moves == moves_from_ops(ops)
+
+
+def test_extract_pairs_api(world500):
+    lex, fwd, _ = world500
+    pair = pairs_of(load_docs("docs40.jsonl"))[0]
+    S = bm.build_similarity_matrix(pair, fwd, lex)
+    path = bm.nw_align(S, 0.2)
+    got = bm.extract_pairs(path, S, pair, bm.MiningParams(0.5, 0.2))
+    want = [(mv.i, mv.j) for mv in path.moves if mv.op == "D" and S.cells[mv.i, mv.j] >= 0.5]
+    assert [(r.src_index, r.tgt_index) for r in got] == want
+    assert all(r.confidence == S.cells[r.src_index, r.tgt_index] for r in got)
+
+
+# ---------------------------------------------------------------- mining
+def _mine_text(pairs, fwd, bwd, lex, t=0.5, p=0.2):
+    sink = io.StringIO()
+    rep = bm.mine_corpus(iter(pairs), fwd, bwd, lex, bm.MinerConfig(bm.MiningParams(t, p)), sink)
+    rep.wall_clock_seconds = 0.0
+    return sink.getvalue(), bm.report_to_json(rep)
+
+
+@pytest.mark.parametrize("docs,tsv,bidir,t,p,world", [
+    ("docs40.jsonl", "mine40_fwd.tsv", False, 0.5, 0.2, "world500"),
+    ("docs40.jsonl", "mine40_bi.tsv", True, 0.5, 0.2, "world500"),
+    ("docs40.jsonl", "mine40_bi_t03_p005.tsv", True, 0.3, 0.05, "world500"),
+    ("doc200.jsonl", "mine200_fwd.tsv", False, 0.5, 0.2, "world5k"),
+    ("doc200.jsonl", "mine200_bi.tsv", True, 0.5, 0.2, "world5k"),
+    ("docs100x6.jsonl", "mine100x6_bi.tsv", True, 0.5, 0.2, "world5k"),
+])
+def test_mine_corpus_tsv_byte_identical(docs, tsv, bidir, t, p, world, request):
+    lex, fwd, bwd = request.getfixturevalue(world)
+    text, rep = _mine_text(pairs_of(load_docs(docs)), fwd, bwd if bidir else None, lex, t, p)
+    assert text == open(golden(tsv), encoding="utf-8").read()
+    if tsv in ("mine40_fwd.tsv", "mine40_bi.tsv"):
+        assert rep == open(golden(tsv.replace(".tsv", ".report.json"))).read()
+
+
+def test_mine_corpus_1000_docs_sha256(world500):
+    lex, fwd, bwd = world500
+    text, _ = _mine_text(pairs_of(load_docs("docs1000_s77.jsonl.gz")), fwd, bwd, lex)
+    want = json.load(open(golden("mine1000_bi.json")))
+    assert text.count("\n") == want["lines"]
+    assert hashlib.sha256(text.encode()).hexdigest() == want["sha256"]
+
+
+def test_mine_document_orientation_and_errors(world500):
+    lex, fwd, bwd = world500
+    pair = pairs_of(load_docs("docs40.jsonl"))[3]
+    cfg = bm.MinerConfig(bm.MiningParams(0.5, 0.2))
+    got = bm.mine_document(pair, bwd, lex.reversed(), cfg)
+    assert got and all(r.direction == "backward" for r in got)
+    for engine_name in bm.ENGINES:
+        a = bm.mine_document(pair, fwd, lex, bm.MinerConfig(bm.MiningParams(0.5, 0.2), engine=engine_name))
+        assert a == bm.mine_document(pair, fwd, lex, cfg)
+    with pytest.raises(bm.DataError, match="lexicon direction"):
+        bm.mine_document(pair, fwd, lex.reversed(), cfg)
+
+
+def test_mine_corpus_skips_over_cap(world500, monkeypatch):
+    lex, fwd, _ = world500
+    pairs = pairs_of(load_docs("docs40.jsonl"))[:5]
+    monkeypatch.setattr("paper_1509_08639_b200.aligner.MAX_CELLS", 16)
+    rep = bm.mine_corpus(iter(pairs), fwd, None, lex, bm.MinerConfig(bm.MiningParams(0.5, 0.2)),
+                         io.StringIO())
+    assert rep.docs_skipped == 5 and rep.docs_processed == 0
+
+
+def _synth_mixed(seed):
+    from paper_1509_08639_b200 import synth
+
+    r = np.random.default_rng(seed)
+    D = 96
+    n = r.integers(1, 420, D)
+    m = r.integers(1, 420, D)
+    n[:6] = [1, 1, 300, 257, 40, 700]
+    m[:6] = [1, 300, 1, 100, 700, 40]
+    g = np.minimum(n, m) // 2
+    return synth.make_corpus(g, n - g, m - g, vocab=2000, seed=seed)
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_mine_mixed_sizes_vs_oracle(oracle_mod, seed):
+    """Docs routed to both tiers (fused warp-per-doc and banded) == oracle."""
+    from paper_1509_08639_b200 import engine
+
+    sc = _synth_mixed(seed)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    dc = engine.DeviceCorpus.upload(sc.packed)
+    dl = engine.DeviceLexicon.upload(plex)
+    view = engine.DocView.of(sc.packed)
+    for t, p in ((0.5, 0.2), (0.2, 0.05)):
+        recs, cost = engine.mine(dc, dl, view, model, t, p)
+        hb = oracle_mod.HostBatch(sc.packed, plex)
+        want, wcost = oracle_mod.mine(hb, model, t, p, threads=8)
+        assert np.array_equal(bits(cost), bits(wcost))
+        assert recs.shape == want.shape
+        for f in ("doc", "i", "j"):
+            assert np.array_equal(recs[f], want[f])
+        assert np.array_equal(bits(recs["conf"]), bits(want["conf"]))
+
+
+def test_mine_long_sentences_general_path(oracle_mod):
+    """A sentence with > 255 alpha tokens forces the 32-bit-hit banded path."""
+    long_src = " ".join(["waaa"] * 300 + ["wbbb"] * 10) + "."
+    long_tgt = " ".join(["vaaa"] * 280) + " 1999."
+    doc = {"id": "long", "src_lang": "xx", "tgt_lang": "yy",
+           "src": ["waaa wbbb.", long_src, "wccc 1999."], "tgt": [long_tgt, "vaaa vbbb.", "vccc."]}
+    lex = bm.Lexicon(("xx", "yy"), {"waaa": [("vaaa", 0.9)], "wbbb": [("vbbb", 0.9)],
+                                     "wccc": [("vccc", 0.9)]})
+    model = bm.load_model(golden("model5k_fwd.json"))
+    pairs = pairs_of([doc])
+    cfg = bm.MinerConfig(bm.MiningParams(0.1, 0.3))
+    got = bm.mine_document(pairs[0], model, lex, cfg)
+    from oracle_pipeline import oracle_records
+
+    recs, _ = oracle_records(oracle_mod, pairs, model, lex, [False], 0.1, 0.3)
+    assert [(r.src_index, r.tgt_index, r.confidence) for r in got] == \
+        [(int(a), int(b), float(c)) for a, b, c in zip(recs["i"], recs["j"], recs["conf"])]
+
+
+def test_synth_text_round_trip_same_records():
+    """Packed-by-generator and packed-from-text corpora mine identically."""
+    from paper_1509_08639_b200 import engine, synth
+    from paper_1509_08639_b200.pack import pack_lexicon, pack_pairs
+
+    sc = synth.make_corpus(*synth.c2_shape(40), seed=8)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    a, _ = engine.mine(engine.DeviceCorpus.upload(sc.packed),
+                       engine.DeviceLexicon.upload(sc.world.packed_lexicon()),
+                       engine.DocView.of(sc.packed), model, 0.5, 0.2)
+    pairs = sc.doc_pairs(range(40))
+    pc = pack_pairs(pairs)
+    b, _ = engine.mine(engine.DeviceCorpus.upload(pc),
+                       engine.DeviceLexicon.upload(pack_lexicon(sc.world.lexicon(), pc)),
+                       engine.DocView.of(pc), model, 0.5, 0.2)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_mine_host_entry_point_matches_device_path(oracle_mod):
+    """bm_mine_host (host buffers in, records out) == oracle."""
+    from paper_1509_08639_b200 import hostapi, synth
+
+    sc = synth.make_corpus(*synth.c2_shape(64), seed=11)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    recs, cost = hostapi.mine_host(sc.packed, plex, model, 0.5, 0.2)
+    want, wcost = oracle_mod.mine(oracle_mod.HostBatch(sc.packed, plex), model, 0.5, 0.2, threads=8)
+    assert recs.tobytes() == want.tobytes()
+    assert np.array_equal(bits(cost), bits(wcost))
+
+
+# ---------------------------------------------------------------- tuning
+@pytest.mark.parametrize("docs,tfile,k,grid", [
+    ("docs40.jsonl", "tune10.json", 10, None),
+    ("docs10_noisy.jsonl", "tune_noisy.json", 10, None),
+    ("docs10_noisy.jsonl", "tune_noisy_small.json", 3, ([0.3, 0.6], [0.1, 0.4])),
+])
+def test_tune_matches_reference(world500, docs, tfile, k, grid):
+    lex, fwd, _ = world500
+    raw = load_docs(docs)[:k]
+    dev = bm.GoldSet(docs=pairs_of(raw), gold=[{(i, j) for i, j in d["gold"]} for d in raw])
+    kw = {} if grid is None else {"thresholds": grid[0], "penalties": grid[1]}
+    got = bm.tune(fwd, lex, dev, **kw)
+    assert bm.tune_result_to_json(got) == open(golden(tfile)).read()
+
+
+def test_tune_synthetic_vs_oracle(oracle_mod):
+    from paper_1509_08639_b200 import engine, synth
+
+    sc = synth.make_corpus(*synth.c2_shape(48), seed=12)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    pens = [0.05, 0.1, 0.2, 0.3, 0.4, 0.6, 0.8, 1.6]
+    thrs = [0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9]
+    keys = [np.asarray(g[:, 0] * int(sc.packed.m[d]) + g[:, 1], np.int64) for d, g in enumerate(sc.gold)]
+    p, h = engine.tune_counts(engine.DeviceCorpus.upload(sc.packed), engine.DeviceLexicon.upload(plex),
+                              engine.DocView.of(sc.packed), model, pens, thrs, keys)
+    wp, wh = oracle_mod.tune(oracle_mod.HostBatch(sc.packed, plex), model, pens, thrs, keys, threads=8)
+    assert np.array_equal(p, wp) and np.array_equal(h, wh)
