@@ -113,6 +113,11 @@ int bm_abi_version(void);
 const char* bm_last_error(void);
 /* Number of CUDA devices visible (0 = no GPU). */
 int bm_device_count(void);
+/* Kernels this library has launched since it was loaded (instrumentation). */
+int64_t bm_launches(void);
+/* FP64 pipe probe (8 DFMA chains x 256 threads x blocks x iters); used by the
+ * benchmark to measure the FP64 roof of the device. Not part of the path. */
+int bm_probe_fp64(double* out, int32_t iters, int32_t blocks, void* stream);
 
 /*
  * K1 -- replaces build_similarity_matrix (aligner.py:313-339) for a batch:

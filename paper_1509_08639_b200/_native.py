@@ -56,6 +56,8 @@ _SIGS = {
     "bm_last_error": (C.c_char_p, []),
     "bm_device_count": (C.c_int, []),
     "bm_dirs_words": (C.c_int64, [C.c_int32, C.c_int32]),
+    "bm_launches": (C.c_int64, []),
+    "bm_probe_fp64": (C.c_int, [_p, C.c_int32, C.c_int32, _p]),
     "bm_score": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, C.POINTER(LexiconC),
                            C.POINTER(ModelC), _p, _p, _p, _p]),
     "bm_features": (C.c_int, [C.POINTER(Sentences), C.POINTER(LexiconC), _p, _p, _p, _p,

@@ -67,6 +67,8 @@ class Scratch {
   std::vector<void*> ptrs_;
 };
 
+void note_launch() { bm::g_launches += 1; }
+
 Model to_model(const bm_model* m) {
   Model M;
   for (int k = 0; k < 7; ++k) M.w[k] = m->w[k];
@@ -168,6 +170,7 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
   BM_CK(sc.alloc(&dv.ticket, 1), "alloc ticket");
   gather_docs_kernel<<<(k + 255) / 256, 256, 0, st>>>(*docs, idx, k, dv.src0, dv.tgt0);
   BM_CK(cudaGetLastError(), "gather_docs");
+  note_launch();
   return BM_OK;
 }
 
@@ -224,6 +227,13 @@ int bm_device_count(void) {
 }
 
 int64_t bm_dirs_words(int32_t n, int32_t m) { return band_dirs_words(n, m); }
+
+int64_t bm_launches(void) { return (int64_t)launches(); }
+
+int bm_probe_fp64(double* out, int32_t iters, int32_t blocks, void* stream) {
+  BM_CK(launch_fp64_probe(out, iters, blocks, (cudaStream_t)stream), "fp64_probe_kernel");
+  return BM_OK;
+}
 
 int bm_score(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
              const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
@@ -412,6 +422,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     scatter_results_kernel<<<k, 128, 0, st>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
                                               rec_count);
     BM_CK(cudaGetLastError(), "scatter_results");
+    note_launch();
   }
   return BM_OK;
 }

@@ -12,11 +12,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "bm_kernels.cuh"
 
 namespace bm {
 
 __device__ const uint64_t g_exp_table[kExpTableWords] = BM_EXP_TABLE_INIT;
+
+// Kernels launched by this library since load (bm_launches()).
+std::atomic<long long> g_launches{0};
+
+static inline cudaError_t counted(cudaError_t e, int n = 1) {
+  if (e == cudaSuccess) g_launches += n;
+  return e;
+}
 
 __device__ __forceinline__ void stage_exp_table(uint64_t* dst, int rank, int size) {
   for (int k = rank; k < kExpTableWords; k += size) dst[k] = g_exp_table[k];
@@ -121,7 +131,7 @@ cudaError_t launch_score(const bm_sentences& S, const bm_docs& D, const bm_lexic
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   score_tile_kernel<<<n_tiles, kTileThreads, sm, st>>>(S, D, L, M, tiles, s_off, pitch, out);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------
@@ -152,7 +162,7 @@ cudaError_t launch_features(const bm_sentences& S, const bm_lexicon& L, const in
   if (n_q == 0) return cudaSuccess;
   features_kernel<<<n_q, WARP, join_smem_bytes() + 16, st>>>(S, L, q_src, q_tgt, ps, pt, n_q,
                                                               feats);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 __global__ void confidence_kernel(const double* __restrict__ feats, int n_q, Model M,
@@ -171,7 +181,7 @@ cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, doub
                               cudaStream_t st) {
   if (n_q == 0) return cudaSuccess;
   confidence_kernel<<<(n_q + 255) / 256, 256, 0, st>>>(feats, n_q, M, conf);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------
@@ -315,7 +325,7 @@ __global__ void __launch_bounds__(WARP) nw_band_kernel(NwArgs a) {
 cudaError_t launch_nw(const NwArgs& a, int n_warps, cudaStream_t st) {
   if (a.n_items == 0) return cudaSuccess;
   nw_band_kernel<<<n_warps, WARP, 0, st>>>(a);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 int nw_resident_warps() {
@@ -379,7 +389,7 @@ cudaError_t launch_traceback(const uint32_t* dirs, const int64_t* dir_off, const
   if (n_docs == 0) return cudaSuccess;
   traceback_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, n, m, n_docs, mv_off, op,
                                                           mi, mj, len);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 __global__ void extract_kernel(const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
@@ -431,7 +441,7 @@ cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const d
   if (n_docs == 0) return cudaSuccess;
   extract_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, S, s_off, pitch, n, m, n_docs,
                                                         thr, rec_off, rec, cnt);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 // extract_pairs for an explicit path (API primitive): gather S at the given
@@ -449,7 +459,7 @@ cudaError_t launch_select(const double* S, int64_t pitch, const int32_t* ci, con
                           int k, double thr, double* conf, uint8_t* keep, cudaStream_t st) {
   if (k == 0) return cudaSuccess;
   select_kernel<<<(k + 255) / 256, 256, 0, st>>>(S, pitch, ci, cj, k, thr, conf, keep);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------
@@ -646,7 +656,7 @@ cudaError_t launch_fused(const FusedArgs& a, int R, size_t smem, cudaStream_t st
     default: return cudaErrorInvalidValue;
   }
 #undef BM_LAUNCH_FUSED
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------
@@ -722,7 +732,7 @@ cudaError_t launch_tune_count(const uint32_t* dirs, const int64_t* dir_off, cons
   tune_count_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, S, s_off, pitch, n, m,
                                                            n_docs, thr, n_thr, gold, gold_off, pred,
                                                            hit);
-  return cudaGetLastError();
+  return counted(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------
@@ -788,7 +798,33 @@ cudaError_t launch_compact(const bm_record* rec, const int64_t* rec_off, const i
   scan_counts_kernel<<<1, 1024, 0, st>>>(cnt, n_docs, dense_off, total);
   gather_records_kernel<<<(n_docs + 7) / 8, 256, 0, st>>>(rec, rec_off, cnt, dense_off, n_docs,
                                                           dense);
-  return cudaGetLastError();
+  return counted(cudaGetLastError(), 2);
 }
 
+}  // namespace bm
+
+namespace bm {
+// FP64 pipe probe: 8 independent DFMA chains per thread. Used by bench.py to
+// measure the FP64 roof of the box (not part of the hot path).
+__global__ void fp64_probe_kernel(double* out, int iters) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  const double b = 0.999999999, c = 1e-12;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __fma_rn(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 42.0) out[0] = s;  // keep the chains alive
+}
+
+cudaError_t launch_fp64_probe(double* out, int iters, int blocks, cudaStream_t st) {
+  fp64_probe_kernel<<<blocks, 256, 0, st>>>(out, iters);
+  return counted(cudaGetLastError());
+}
+
+long long launches() { return g_launches.load(); }
 }  // namespace bm

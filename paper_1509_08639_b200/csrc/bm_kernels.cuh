@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "bm_device.cuh"
 
 namespace bm {
@@ -97,6 +99,9 @@ cudaError_t launch_tune_count(const uint32_t*, const int64_t*, const double*, co
 cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int, int64_t*,
                            int64_t*, bm_record*, cudaStream_t);
 size_t score_smem_bytes();
+cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
+long long launches();
+extern std::atomic<long long> g_launches;
 cudaError_t launch_select(const double*, int64_t, const int32_t*, const int32_t*, int, double,
                           double*, uint8_t*, cudaStream_t);
 
