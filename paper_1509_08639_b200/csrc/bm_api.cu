@@ -238,6 +238,7 @@ int bm_probe_fp64(double* out, int32_t iters, int32_t blocks, void* stream) {
 int bm_score(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
              const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
              const int64_t* s_off, const int32_t* pitch, double* S, void* stream) {
+  BM_CK(ensure_quot_table(), "quotient table");
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int4> tiles;
   for (int d = 0; d < docs->n_docs; ++d)
@@ -254,6 +255,7 @@ int bm_score(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_hos
 int bm_features(const bm_sentences* sent, const bm_lexicon* lex, const int32_t* q_src,
                 const int32_t* q_tgt, const double* q_pos_s, const double* q_pos_t, int32_t n_q,
                 double* feats, void* stream) {
+  BM_CK(ensure_quot_table(), "quotient table");
   BM_CK(launch_features(*sent, *lex, q_src, q_tgt, q_pos_s, q_pos_t, n_q, feats,
                         (cudaStream_t)stream),
         "features_kernel");
@@ -348,6 +350,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
             const int32_t* m_host, const int32_t* amax_host, const bm_lexicon* lex,
             const bm_model* model, double threshold, double penalty, const int64_t* rec_off,
             bm_record* rec, int32_t* rec_count, double* cost, void* stream) {
+  BM_CK(ensure_quot_table(), "quotient table");
   if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
   cudaStream_t st = (cudaStream_t)stream;
   const int nd = docs->n_docs;
@@ -537,6 +540,7 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
             const double* penalties_host, int32_t n_pen, const double* thresholds, int32_t n_thr,
             const int64_t* gold, const int64_t* gold_off, unsigned long long* pred,
             unsigned long long* hit, void* stream) {
+  BM_CK(ensure_quot_table(), "quotient table");
   cudaStream_t st = (cudaStream_t)stream;
   for (int k = 0; k < n_pen; ++k)
     if (!check_penalty(penalties_host[k])) return fail(BM_EINVAL, "penalty must be >= 0");

@@ -22,17 +22,32 @@ struct Model {
   double bias;
 };
 
+// Correctly rounded quotients k/d for 0 <= k <= d <= kQuotMax (Python's
+// int/int true division of small counts), filled once by the host. The five
+// count ratios of a cell are table loads instead of IEEE divisions; a zero
+// numerator never reaches a division (its slow path is a called subroutine).
+constexpr int kQuotMax = 64;
+constexpr int kQuotEntries = (kQuotMax + 1) * (kQuotMax + 2) / 2;
+static __device__ double g_quot[kQuotEntries];  // filled by ensure_quot_table()
+
+__device__ __forceinline__ double quot(int num, int den) {  // 0 < num <= den
+  if (den <= kQuotMax) return __ldg(&g_quot[den * (den + 1) / 2 + num]);
+  return __ddiv_rn((double)num, (double)den);
+}
+
 // min(a,b)/max(a,b), 1.0 when both are zero (classifier.py:62-65).
 __device__ __forceinline__ double ratio_min_max(int a, int b) {
-  if (a == 0 && b == 0) return 1.0;
   int lo = a < b ? a : b;
   int hi = a < b ? b : a;
-  return __ddiv_rn((double)lo, (double)hi);
+  if (hi == 0) return 1.0;
+  if (lo == 0) return 0.0;
+  return quot(lo, hi);
 }
 
 // Python int/int true division; 0.0 for an empty denominator (lexicon.py:96-97).
 __device__ __forceinline__ double frac_or_zero(int num, int den) {
-  return den == 0 ? 0.0 : __ddiv_rn((double)num, (double)den);
+  if (den == 0 || num == 0) return 0.0;
+  return quot(num, den);
 }
 
 // |D_s & D_t| for two ascending id lists (classifier.py:82-87).
@@ -75,7 +90,7 @@ __device__ __forceinline__ void cell_features(const bm_sentences& S, const SentS
   } else {
     int inter = (a.nD && b.nD) ? sorted_intersection(S.dig_id + a.d0, a.nD, S.dig_id + b.d0, b.nD)
                                : 0;
-    f[3] = __ddiv_rn((double)inter, (double)(a.nD + b.nD - inter));
+    f[3] = frac_or_zero(inter, a.nD + b.nD - inter);
   }
   f[4] = ratio_min_max(a.P, b.P);
   f[5] = __dsub_rn(1.0, fabs(__dsub_rn(pos_s, pos_t)));

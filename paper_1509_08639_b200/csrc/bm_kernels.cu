@@ -20,6 +20,22 @@ namespace bm {
 
 __device__ const uint64_t g_exp_table[kExpTableWords] = BM_EXP_TABLE_INIT;
 
+// Fill g_quot on the current device (host IEEE division is correctly rounded,
+// exactly like CPython's int/int true division of small ints).
+cudaError_t ensure_quot_table() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (done_dev == dev) return cudaSuccess;
+  static double host[kQuotEntries];
+  for (int d = 0; d <= kQuotMax; ++d)
+    for (int k = 0; k <= d; ++k) host[d * (d + 1) / 2 + k] = d ? (double)k / (double)d : 0.0;
+  e = cudaMemcpyToSymbol(g_quot, host, sizeof(host));
+  if (e == cudaSuccess) done_dev = dev;
+  return e;
+}
+
 // Kernels launched by this library since load (bm_launches()).
 std::atomic<long long> g_launches{0};
 
@@ -76,7 +92,7 @@ __device__ __forceinline__ SentScalars get_scalars(const TileScalars& t, int k) 
   return r;
 }
 
-__global__ void __launch_bounds__(kTileThreads) score_tile_kernel(
+__global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
     bm_sentences S, bm_docs D, bm_lexicon L, Model M, const int4* __restrict__ tiles,
     const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch, double* __restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -199,7 +215,7 @@ cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, doub
 // S is read with 16-byte loads, one 4-column group ahead.
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(WARP) nw_band_kernel(NwArgs a) {
+__global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   const int lane = threadIdx.x;
   const unsigned FULL = 0xffffffffu;
   for (;;) {
@@ -485,12 +501,12 @@ size_t fused_slice_bytes(int n, int m) {
   const size_t dirs = (size_t)((m + cpw - 1) / cpw) * WARP * 4;
   const size_t dlist = (size_t)(n < m ? n : m) * 4;
   const size_t r2 = join_smem_bytes() > dirs + dlist ? join_smem_bytes() : dirs + dlist;
-  return kExpTableWords * 8 + hits + align16(r2);
+  return kExpTableWords * 8 + hits + align16((size_t)m * 8) + align16(r2);
 }
 
 
 template <int R>
-__global__ void __launch_bounds__(WARP) mine_fused_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(WARP, 1) mine_fused_kernel(FusedArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int CPW = 16 / R;  // columns per direction word
   const unsigned FULL = 0xffffffffu;
@@ -503,8 +519,10 @@ __global__ void __launch_bounds__(WARP) mine_fused_kernel(FusedArgs a) {
 
   uint64_t* exp_tab = (uint64_t*)smem;
   uint32_t* hits = (uint32_t*)(smem + kExpTableWords * 8);
-  uint8_t* region2 = (uint8_t*)hits + align16(((size_t)n * m + 1) / 2 * 4);
+  double* cpos = (double*)((uint8_t*)hits + align16(((size_t)n * m + 1) / 2 * 4));
+  uint8_t* region2 = (uint8_t*)cpos + align16((size_t)m * 8);
   stage_exp_table(exp_tab, lane, WARP);
+  for (int j = lane; j < m; j += WARP) cpos[j] = doc_pos(j, m);
   JoinSmem js = carve_join(region2);
   tile_join<true>(WarpGroup(), S, a.L, s0, n, t0, m, hits, js);  // ends with __syncwarp
 
@@ -546,14 +564,14 @@ __global__ void __launch_bounds__(WARP) mine_fused_kernel(FusedArgs a) {
     prev_recv = recv;
     if (lane < nl && j >= 0 && j < m) {
       const SentScalars cs = load_scalars(S, t0 + j);
-      const double cpos = doc_pos(j, m);
+      const double cp = cpos[j];
       uint32_t codes = 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r < my_rows) {
           int hf, hr;
           read_hits<true>(hits, (i0 + r) * m + j, hf, hr);
-          const double sv = cell_score(S, a.M, exp_tab, rs[r], cs, hf, hr, rpos[r], cpos);
+          const double sv = cell_score(S, a.M, exp_tab, rs[r], cs, hf, hr, rpos[r], cp);
           const double dcand = __dadd_rn(dg, __dsub_rn(1.0, sv));
           const double ucand = __dadd_rn(up, p);
           const double lcand = __dadd_rn(left[r], p);
@@ -622,7 +640,7 @@ __global__ void __launch_bounds__(WARP) mine_fused_kernel(FusedArgs a) {
       int hf, hr;
       read_hits<true>(hits, cell, hf, hr);
       sv = cell_score(S, a.M, exp_tab, load_scalars(S, s0 + ci), load_scalars(S, t0 + cj), hf, hr,
-                      doc_pos(ci, n), doc_pos(cj, m));
+                      doc_pos(ci, n), cpos[cj]);
       keep = sv >= a.threshold;
     }
     const unsigned mask = __ballot_sync(FULL, keep);

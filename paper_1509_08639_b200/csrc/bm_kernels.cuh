@@ -101,6 +101,7 @@ cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int
 size_t score_smem_bytes();
 cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();
+cudaError_t ensure_quot_table();
 extern std::atomic<long long> g_launches;
 cudaError_t launch_select(const double*, int64_t, const int32_t*, const int32_t*, int, double,
                           double*, uint8_t*, cudaStream_t);
