@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -358,11 +359,15 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   std::vector<int32_t> fused[4];
   size_t fused_smem[4] = {0, 0, 0, 0};
   GeneralPlan g;
+  // BM_ROUTE=banded forces every document onto the K1 -> K2/K3 -> K4 tier
+  // (benchmarking / testing both tiers on the same workload).
+  const char* route = getenv("BM_ROUTE");
+  const bool force_banded = route != nullptr && strcmp(route, "banded") == 0;
   for (int d = 0; d < nd; ++d) {
     const int n = n_host[d], m = m_host[d];
     if (n <= 0 || m <= 0) continue;
     const size_t sl = fused_slice_bytes(n, m);
-    if (n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax_host[d] <= 255) {
+    if (!force_banded && n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax_host[d] <= 255) {
       const int R = fused_rows_per_lane(n);
       const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
       fused[q].push_back(d);
