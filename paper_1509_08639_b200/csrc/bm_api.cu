@@ -366,9 +366,9 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   for (int d = 0; d < nd; ++d) {
     const int n = n_host[d], m = m_host[d];
     if (n <= 0 || m <= 0) continue;
-    const size_t sl = fused_slice_bytes(n, m);
+    const int R = fused_rows_per_lane(n);
+    const size_t sl = ring_slice_bytes(n, m, R);
     if (!force_banded && n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax_host[d] <= 255) {
-      const int R = fused_rows_per_lane(n);
       const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
       fused[q].push_back(d);
       fused_smem[q] = std::max(fused_smem[q], sl);
@@ -395,7 +395,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     a.rec = rec;
     a.rec_count = rec_count;
     a.cost = cost;
-    BM_CK(launch_fused(a, 1 << q, fused_smem[q], st), "mine_fused_kernel");
+    BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
   }
   if (!g.docs.empty()) {
     const int k = (int)g.docs.size();

@@ -18,7 +18,6 @@
 
 namespace bm {
 
-__device__ const uint64_t g_exp_table[kExpTableWords] = BM_EXP_TABLE_INIT;
 
 // Fill g_quot on the current device (host IEEE division is correctly rounded,
 // exactly like CPython's int/int true division of small ints).
@@ -44,9 +43,6 @@ static inline cudaError_t counted(cudaError_t e, int n = 1) {
   return e;
 }
 
-__device__ __forceinline__ void stage_exp_table(uint64_t* dst, int rank, int size) {
-  for (int k = rank; k < kExpTableWords; k += size) dst[k] = g_exp_table[k];
-}
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -59,20 +55,6 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 }
 
 
-__device__ __forceinline__ JoinSmem carve_join(uint8_t* p) {
-  JoinSmem js;
-  js.key = (int32_t*)p;
-  p += kJoinEmax * 4;
-  js.bstart = (int32_t*)p;
-  p += (kJoinBuckets + 1) * 4;
-  js.bfill = (int32_t*)p;
-  p += kJoinBuckets * 4;
-  js.owner = (uint16_t*)p;
-  js.emax = kJoinEmax;
-  js.nbuckets = kJoinBuckets;
-  js.bshift = 32 - 9;  // log2(512)
-  return js;
-}
 
 // ---------------------------------------------------------------------------
 // K1: one CTA per 64x64 tile of one document's similarity matrix.

@@ -36,6 +36,28 @@ __host__ __device__ constexpr size_t join_smem_bytes() {
          (size_t)kJoinBuckets * 4;
 }
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+static __device__ const uint64_t g_exp_table[kExpTableWords] = BM_EXP_TABLE_INIT;
+
+__device__ __forceinline__ void stage_exp_table(uint64_t* dst, int rank, int size) {
+  for (int k = rank; k < kExpTableWords; k += size) dst[k] = g_exp_table[k];
+}
+
+__device__ __forceinline__ JoinSmem carve_join(uint8_t* p) {
+  JoinSmem js;
+  js.key = (int32_t*)p;
+  p += kJoinEmax * 4;
+  js.bstart = (int32_t*)p;
+  p += (kJoinBuckets + 1) * 4;
+  js.bfill = (int32_t*)p;
+  p += kJoinBuckets * 4;
+  js.owner = (uint16_t*)p;
+  js.emax = kJoinEmax;
+  js.nbuckets = kJoinBuckets;
+  js.bshift = 32 - 9;  // log2(512)
+  return js;
+}
+
 int fused_rows_per_lane(int n);
 size_t fused_slice_bytes(int n, int m);
 
@@ -102,6 +124,8 @@ size_t score_smem_bytes();
 cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();
 cudaError_t ensure_quot_table();
+size_t ring_slice_bytes(int n, int m, int R);
+cudaError_t launch_ring(const FusedArgs& a, int R, size_t smem, cudaStream_t st);
 extern std::atomic<long long> g_launches;
 cudaError_t launch_select(const double*, int64_t, const int32_t*, const int32_t*, int, double,
                           double*, uint8_t*, cudaStream_t);
