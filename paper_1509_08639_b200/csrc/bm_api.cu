@@ -395,6 +395,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     a.rec = rec;
     a.rec_count = rec_count;
     a.cost = cost;
+    a.debug = getenv("BM_RING_DEBUG") ? atoi(getenv("BM_RING_DEBUG")) : 0;
     BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
   }
   if (!g.docs.empty()) {

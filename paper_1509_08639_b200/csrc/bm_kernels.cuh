@@ -99,6 +99,7 @@ struct FusedArgs {
   bm_record* rec;
   int32_t* rec_count;
   double* cost;
+  int debug;  // ring kernel diagnostics (BM_RING_DEBUG): 1 = sum of hits, 2 = sum of S
 };
 
 cudaError_t launch_score(const bm_sentences&, const bm_docs&, const bm_lexicon&, const Model&,

@@ -116,6 +116,19 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
     JoinSmem js = carve_join((uint8_t*)ring);  // the ring is idle during the join
     tile_join<true>(CtaGroup(), S, a.L, s0, n, t0, m, hits, js);  // ends with __syncthreads
 
+    if (a.debug == 1) {
+      if (tid == 0) {
+        double sum = 0.0;
+        for (int c = 0; c < n * m; ++c) {
+          int hf, hr;
+          read_hits<true>(hits, c, hf, hr);
+          sum += hf + 1000.0 * hr;
+        }
+        a.cost[doc] = sum;
+        a.rec_count[doc] = 0;
+      }
+      continue;
+    }
     const int nl = (n + R - 1) / R;
     const int steps = m + nl - 1;
     const int nblocks = (steps + kGroup - 1) / kGroup;
@@ -133,6 +146,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         if (r == my_rows - 1) bot = left[r];
       double prev_recv = (double)i0 * p;
       uint32_t dword = 0;
+      double dbg_acc = 0.0;
       for (int b = 0; b < nblocks; ++b) {
         mbar_wait(bar_full + (b % NB), (uint32_t)((b / NB) & 1));
         const int s_end = min(steps, (b + 1) * kGroup);
@@ -153,6 +167,18 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
             double omv[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) omv[r] = om[r];
+            if (a.debug == 2)
+              for (int r = 0; r < R; ++r)
+                if (r < my_rows) dbg_acc += omv[r];
+            if (a.debug >= 5)
+              for (int r = 0; r < R; ++r)
+                if (r < my_rows) {
+                  int hf, hr;
+                  read_hits<true>(hits, (i0 + r) * m + j, hf, hr);
+                  const double sv = cell_score(S, a.M, exp_tab, load_scalars(S, s0 + i0 + r),
+                                               load_scalars(S, t0 + j), hf, hr, rpos[i0 + r], cpos[j]);
+                  dbg_acc += (__dsub_rn(1.0, sv) != omv[r]) ? 1.0 : 0.0;
+                }
             uint32_t codes = 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -191,11 +217,16 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         for (int r = 0; r < R; ++r)
           if (i0 + r == n - 1) a.cost[doc] = left[r];
       }
+      if (a.debug == 2 || a.debug >= 5) {
+        for (int o = 16; o > 0; o >>= 1) dbg_acc += __shfl_xor_sync(FULL, dbg_acc, o);
+        if (lane == 0) a.cost[doc] = dbg_acc;
+      }
     } else {
       // ------------------------------------------------------ score warps
       const int ptid = tid - WARP;
       for (int b = 0; b < nblocks; ++b) {
         if (b >= NB) mbar_wait(bar_empty + (b % NB), (uint32_t)(((b / NB) - 1) & 1));
+        if (a.debug == 6) __nanosleep(20000);
         // valid (lane, row) slots of each step of the block, prefix-summed
         int cnt[kGroup];
         int total = 0;
