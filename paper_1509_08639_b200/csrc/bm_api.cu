@@ -357,7 +357,9 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   const int nd = docs->n_docs;
   BM_CK(cudaMemsetAsync(rec_count, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
   std::vector<int32_t> fused[4];
-  size_t fused_smem[4] = {0, 0, 0, 0};
+  size_t fused_smem[4] = {0, 0, 0, 0}, hits_smem[4] = {0, 0, 0, 0};
+  std::vector<int64_t> hit_off(nd, 0);
+  int64_t hit_total = 0;
   GeneralPlan g;
   // BM_ROUTE=banded forces every document onto the K1 -> K2/K3 -> K4 tier
   // (benchmarking / testing both tiers on the same workload).
@@ -372,31 +374,42 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
       fused[q].push_back(d);
       fused_smem[q] = std::max(fused_smem[q], sl);
+      hits_smem[q] = std::max(hits_smem[q], hits_kernel_smem(n, m));
+      hit_off[d] = hit_total;
+      hit_total += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
     } else {
       g.add(d, n, m);
     }
   }
   Scratch sc(st);
   const Model M = to_model(model);
-  for (int q = 0; q < 4; ++q) {
-    if (fused[q].empty()) continue;
-    int32_t* list = nullptr;
-    BM_CK(sc.upload(&list, fused[q]), "upload");
-    FusedArgs a;
-    a.S = *sent;
-    a.D = *docs;
-    a.L = *lex;
-    a.M = M;
-    a.threshold = threshold;
-    a.p = penalty;
-    a.list = list;
-    a.n_list = (int)fused[q].size();
-    a.rec_off = rec_off;
-    a.rec = rec;
-    a.rec_count = rec_count;
-    a.cost = cost;
-    a.debug = getenv("BM_RING_DEBUG") ? atoi(getenv("BM_RING_DEBUG")) : 0;
-    BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
+  if (hit_total > 0) {
+    uint8_t* hits = nullptr;
+    int64_t* dho = nullptr;
+    BM_CK(sc.alloc(&hits, (size_t)hit_total), "alloc hits");
+    BM_CK(sc.upload(&dho, hit_off), "upload");
+    for (int q = 0; q < 4; ++q) {
+      if (fused[q].empty()) continue;
+      int32_t* list = nullptr;
+      BM_CK(sc.upload(&list, fused[q]), "upload");
+      FusedArgs a;
+      a.S = *sent;
+      a.D = *docs;
+      a.L = *lex;
+      a.M = M;
+      a.threshold = threshold;
+      a.p = penalty;
+      a.list = list;
+      a.n_list = (int)fused[q].size();
+      a.rec_off = rec_off;
+      a.rec = rec;
+      a.rec_count = rec_count;
+      a.cost = cost;
+      a.hits = hits;
+      a.hit_off = dho;
+      BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
+      BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
+    }
   }
   if (!g.docs.empty()) {
     const int k = (int)g.docs.size();

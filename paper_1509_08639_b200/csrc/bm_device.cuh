@@ -27,11 +27,12 @@ struct Model {
 // count ratios of a cell are table loads instead of IEEE divisions; a zero
 // numerator never reaches a division (its slow path is a called subroutine).
 constexpr int kQuotMax = 64;
-constexpr int kQuotEntries = (kQuotMax + 1) * (kQuotMax + 2) / 2;
+constexpr int kQuotStride = kQuotMax + 1;
+constexpr int kQuotEntries = kQuotStride * kQuotStride;  // [den][num]
 static __device__ double g_quot[kQuotEntries];  // filled by ensure_quot_table()
 
 __device__ __forceinline__ double quot(int num, int den) {  // 0 < num <= den
-  if (den <= kQuotMax) return __ldg(&g_quot[den * (den + 1) / 2 + num]);
+  if (den <= kQuotMax) return __ldg(&g_quot[den * kQuotStride + num]);
   return __ddiv_rn((double)num, (double)den);
 }
 

@@ -29,7 +29,8 @@ cudaError_t ensure_quot_table() {
   if (done_dev == dev) return cudaSuccess;
   static double host[kQuotEntries];
   for (int d = 0; d <= kQuotMax; ++d)
-    for (int k = 0; k <= d; ++k) host[d * (d + 1) / 2 + k] = d ? (double)k / (double)d : 0.0;
+    for (int k = 0; k <= kQuotMax; ++k)
+      host[d * kQuotStride + k] = (d && k <= d) ? (double)k / (double)d : 0.0;
   e = cudaMemcpyToSymbol(g_quot, host, sizeof(host));
   if (e == cudaSuccess) done_dev = dev;
   return e;
@@ -127,6 +128,8 @@ cudaError_t launch_score(const bm_sentences& S, const bm_docs& D, const bm_lexic
   const size_t sm = score_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(score_tile_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(score_tile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   score_tile_kernel<<<n_tiles, kTileThreads, sm, st>>>(S, D, L, M, tiles, s_off, pitch, out);
   return counted(cudaGetLastError());
@@ -460,203 +463,13 @@ cudaError_t launch_select(const double* S, int64_t pitch, const int32_t* ci, con
   return counted(cudaGetLastError());
 }
 
-// ---------------------------------------------------------------------------
-// Fused miner: one warp (= one CTA) per document, nothing but the records
-// leaves the SM. Shared memory per warp:
-//   [hits: n*m 16-bit cells][ region2: join buffers | (dirs + D list) ]
-// The DP is the same lane-skewed wavefront as K2 but with R = 1..8 rows per
-// lane (n <= 256) and the cell score computed inline where the DP needs it.
-// ---------------------------------------------------------------------------
+// Rows per lane of the fused (ring) kernel's DP warp: n <= 32 * R.
 int fused_rows_per_lane(int n) {
   int r = (n + WARP - 1) / WARP;
   if (r <= 1) return 1;
   if (r <= 2) return 2;
   if (r <= 4) return 4;
   return 8;
-}
-
-
-size_t fused_slice_bytes(int n, int m) {
-  const int R = fused_rows_per_lane(n);
-  const int cpw = 16 / R;
-  const size_t hits = align16(((size_t)n * m + 1) / 2 * 4);
-  const size_t dirs = (size_t)((m + cpw - 1) / cpw) * WARP * 4;
-  const size_t dlist = (size_t)(n < m ? n : m) * 4;
-  const size_t r2 = join_smem_bytes() > dirs + dlist ? join_smem_bytes() : dirs + dlist;
-  return kExpTableWords * 8 + hits + align16((size_t)m * 8) + align16(r2);
-}
-
-
-template <int R>
-__global__ void __launch_bounds__(WARP, 1) mine_fused_kernel(FusedArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int CPW = 16 / R;  // columns per direction word
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x;
-  const int doc = a.list[blockIdx.x];
-  const int n = a.D.n[doc], m = a.D.m[doc];
-  const int s0 = a.D.src0[doc], t0 = a.D.tgt0[doc];
-  const double p = a.p;
-  const bm_sentences& S = a.S;
-
-  uint64_t* exp_tab = (uint64_t*)smem;
-  uint32_t* hits = (uint32_t*)(smem + kExpTableWords * 8);
-  double* cpos = (double*)((uint8_t*)hits + align16(((size_t)n * m + 1) / 2 * 4));
-  uint8_t* region2 = (uint8_t*)cpos + align16((size_t)m * 8);
-  stage_exp_table(exp_tab, lane, WARP);
-  for (int j = lane; j < m; j += WARP) cpos[j] = doc_pos(j, m);
-  JoinSmem js = carve_join(region2);
-  tile_join<true>(WarpGroup(), S, a.L, s0, n, t0, m, hits, js);  // ends with __syncwarp
-
-  uint32_t* dirs = (uint32_t*)region2;  // the join buffers are dead now
-  const int ncg = (m + CPW - 1) / CPW;
-  int32_t* dlist = (int32_t*)(dirs + (size_t)ncg * WARP);
-
-  const int nl = (n + R - 1) / R;
-  const int i0 = lane * R;
-  const int my_rows = lane < nl ? min(R, n - i0) : 0;
-  SentScalars rs[R];
-  double rpos[R], left[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    left[r] = (double)(i0 + r + 1) * p;
-    if (r < my_rows) {
-      rs[r] = load_scalars(S, s0 + i0 + r);
-      rpos[r] = doc_pos(i0 + r, n);
-    }
-  }
-  double bot = 0.0;
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (r == my_rows - 1) bot = left[r];
-  double prev_recv = (double)i0 * p;
-  uint32_t dword = 0;
-  const int steps = m + nl - 1;
-  for (int s = 0; s < steps; ++s) {
-    const int j = s - lane;
-    const double recv = __shfl_up_sync(FULL, bot, 1);
-    double up, dg;
-    if (lane == 0) {
-      up = (double)(j + 1) * p;
-      dg = (double)j * p;
-    } else {
-      up = recv;
-      dg = prev_recv;
-    }
-    prev_recv = recv;
-    if (lane < nl && j >= 0 && j < m) {
-      const SentScalars cs = load_scalars(S, t0 + j);
-      const double cp = cpos[j];
-      uint32_t codes = 0;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (r < my_rows) {
-          int hf, hr;
-          read_hits<true>(hits, (i0 + r) * m + j, hf, hr);
-          const double sv = cell_score(S, a.M, exp_tab, rs[r], cs, hf, hr, rpos[r], cp);
-          const double dcand = __dadd_rn(dg, __dsub_rn(1.0, sv));
-          const double ucand = __dadd_rn(up, p);
-          const double lcand = __dadd_rn(left[r], p);
-          double best = dcand;
-          if (ucand < best) best = ucand;
-          if (lcand < best) best = lcand;
-          const uint32_t code = best == dcand ? 0u : (best == ucand ? 1u : 2u);
-          codes |= code << (2 * r);
-          dg = left[r];
-          left[r] = best;
-          up = best;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (r == my_rows - 1) bot = left[r];
-      const int slot = j % CPW;
-      dword |= codes << (2 * R * slot);
-      if (slot == CPW - 1 || j == m - 1) {
-        dirs[(j / CPW) * WARP + lane] = dword;
-        dword = 0;
-      }
-    }
-  }
-  if (lane == (n - 1) / R) {
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (i0 + r == n - 1) a.cost[doc] = left[r];
-  }
-  __syncwarp();
-
-  // traceback (lane 0) collecting the diagonal cells, reverse path order
-  int K = 0;
-  if (lane == 0) {
-    int i = n, j = m;
-    while (i > 0 && j > 0) {
-      const int ci = i - 1, cj = j - 1;
-      const uint32_t wv = dirs[(cj / CPW) * WARP + ci / R];
-      const uint32_t op = (wv >> (2 * R * (cj % CPW) + 2 * (ci % R))) & 3u;
-      if (op == BM_MOVE_D) {
-        dlist[K++] = ci * m + cj;
-        --i;
-        --j;
-      } else if (op == BM_MOVE_GS) {
-        --i;
-      } else {
-        --j;
-      }
-    }
-  }
-  K = __shfl_sync(FULL, K, 0);
-  __syncwarp();
-
-  // threshold + order-preserving warp compaction (extract_pairs)
-  bm_record* out = a.rec + a.rec_off[doc];
-  int base = 0;
-  for (int f0 = 0; f0 < K; f0 += WARP) {
-    const int f = f0 + lane;
-    bool keep = false;
-    int ci = 0, cj = 0;
-    double sv = 0.0;
-    if (f < K) {
-      const int cell = dlist[K - 1 - f];
-      ci = cell / m;
-      cj = cell - ci * m;
-      int hf, hr;
-      read_hits<true>(hits, cell, hf, hr);
-      sv = cell_score(S, a.M, exp_tab, load_scalars(S, s0 + ci), load_scalars(S, t0 + cj), hf, hr,
-                      doc_pos(ci, n), cpos[cj]);
-      keep = sv >= a.threshold;
-    }
-    const unsigned mask = __ballot_sync(FULL, keep);
-    if (keep) {
-      bm_record r;
-      r.doc = doc;
-      r.i = ci;
-      r.j = cj;
-      r.pad = 0;
-      r.conf = sv;
-      out[base + __popc(mask & ((1u << lane) - 1u))] = r;
-    }
-    base += __popc(mask);
-  }
-  if (lane == 0) a.rec_count[doc] = base;
-}
-
-cudaError_t launch_fused(const FusedArgs& a, int R, size_t smem, cudaStream_t st) {
-  if (a.n_list == 0) return cudaSuccess;
-  cudaError_t e;
-#define BM_LAUNCH_FUSED(RR)                                                                   \
-  e = cudaFuncSetAttribute(mine_fused_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                        \
-  if (e != cudaSuccess) return e;                                                             \
-  mine_fused_kernel<RR><<<a.n_list, WARP, smem, st>>>(a);
-  switch (R) {
-    case 1: BM_LAUNCH_FUSED(1); break;
-    case 2: BM_LAUNCH_FUSED(2); break;
-    case 4: BM_LAUNCH_FUSED(4); break;
-    case 8: BM_LAUNCH_FUSED(8); break;
-    default: return cudaErrorInvalidValue;
-  }
-#undef BM_LAUNCH_FUSED
-  return counted(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------

@@ -59,7 +59,6 @@ __device__ __forceinline__ JoinSmem carve_join(uint8_t* p) {
 }
 
 int fused_rows_per_lane(int n);
-size_t fused_slice_bytes(int n, int m);
 
 __host__ __device__ inline int64_t band_dirs_words(int32_t n, int32_t m) {
   int64_t nb = (n + kBandRows - 1) / kBandRows;
@@ -99,7 +98,8 @@ struct FusedArgs {
   bm_record* rec;
   int32_t* rec_count;
   double* cost;
-  int debug;  // ring kernel diagnostics (BM_RING_DEBUG): 1 = sum of hits, 2 = sum of S
+  uint8_t* hits;           // per-doc dense coverage hit counts (hits_kernel output)
+  const int64_t* hit_off;  // byte offset of each doc's hits (16-byte aligned)
 };
 
 cudaError_t launch_score(const bm_sentences&, const bm_docs&, const bm_lexicon&, const Model&,
@@ -114,7 +114,6 @@ cudaError_t launch_traceback(const uint32_t*, const int64_t*, const int32_t*, co
 cudaError_t launch_extract(const uint32_t*, const int64_t*, const double*, const int64_t*,
                            const int32_t*, const int32_t*, const int32_t*, int, double,
                            const int64_t*, bm_record*, int32_t*, cudaStream_t);
-cudaError_t launch_fused(const FusedArgs&, int, size_t, cudaStream_t);
 cudaError_t launch_tune_count(const uint32_t*, const int64_t*, const double*, const int64_t*,
                               const int32_t*, const int32_t*, const int32_t*, int, const double*,
                               int, const int64_t*, const int64_t*, unsigned long long*,
@@ -126,6 +125,8 @@ cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();
 cudaError_t ensure_quot_table();
 size_t ring_slice_bytes(int n, int m, int R);
+size_t hits_kernel_smem(int n, int m);
+cudaError_t launch_hits(const FusedArgs& a, size_t smem, cudaStream_t st);
 cudaError_t launch_ring(const FusedArgs& a, int R, size_t smem, cudaStream_t st);
 extern std::atomic<long long> g_launches;
 cudaError_t launch_select(const double*, int64_t, const int32_t*, const int32_t*, int, double,

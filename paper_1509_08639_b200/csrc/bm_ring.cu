@@ -1,20 +1,24 @@
-// Fused miner, producer/consumer form ("ring" kernel): score -> NW DP ->
-// traceback -> threshold -> records for one document per CTA, nothing but the
-// records leaving the SM (miner.py:84-128, aligner.py:116-206, 342-368).
+// Fused miner for documents with n <= 256 rows: score -> NW DP -> traceback
+// -> threshold -> records (miner.py:84-128, aligner.py:116-206, 342-368).
 //
-// CTA = 4 warps.
-//   1. all 128 threads: dictionary join -> per-cell coverage hit counts (smem)
-//   2. warps 1-3 (producers): score exactly the cells the DP wavefront needs,
-//      in wavefront-step order, and write (1 - S) into a shared-memory ring of
-//      K steps x 32 lanes x R rows; warp 0 (consumer) runs the lane-skewed
-//      anti-diagonal DP over the ring. Full/empty mbarriers per block of
-//      kGroup steps hand ring slots back and forth, so the FP64-heavy scoring
-//      runs on 96 threads at full lane utilisation while the latency-bound DP
-//      chain runs on its own warp.
-//   3. thread 0: traceback over the 2-bit codes in smem (tie order D > GS > GT)
-//   4. all threads: re-score the diagonal cells of the path, threshold, and
-//      compact them in path order.
-// Same arithmetic, operation for operation, as bm_kernels.cu's kernels.
+// Two kernels:
+//   hits_kernel       one CTA per document: the dictionary join (lexicon.py:
+//                     88-105) into dense per-cell coverage hit counts, written
+//                     to HBM scratch (2 B/cell). High occupancy hides the
+//                     dependent lexicon lookups.
+//   mine_ring_kernel  one CTA (4 warps) per document. The document's hit
+//                     counts arrive in shared memory by one TMA bulk copy
+//                     (cp.async.bulk + mbarrier complete_tx). Warps 1-3
+//                     (producers) score exactly the cells the DP wavefront
+//                     needs, in wavefront-step order, into a shared-memory ring
+//                     of (1 - S) values; warp 0 runs the lane-skewed
+//                     anti-diagonal DP over the ring (full/empty mbarriers per
+//                     block of kGroup steps). Thread 0 then walks the 2-bit
+//                     codes (tie order D > GS > GT) and all threads re-score
+//                     the diagonal cells of the path, threshold them and
+//                     compact them in path order.
+// The similarity matrix never exists in memory; every value is computed with
+// the same operation order as bm_kernels.cu (bit-identical to the reference).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,9 +28,9 @@ namespace bm {
 
 constexpr int kRingThreads = 128;
 constexpr int kProducers = kRingThreads - WARP;
-constexpr int kRingBytes = 32 * 1024;
-constexpr int kGroup = 8;       // wavefront steps per mbarrier block
+constexpr int kGroup = 8;  // wavefront steps per mbarrier block
 constexpr int kFixedBytes = kExpTableWords * 8 + 256;
+constexpr int kHitsThreads = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -39,6 +43,14 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile(
       "{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile(
+      "{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(bytes)
       : "memory");
 }
 
@@ -56,28 +68,97 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       : "memory");
 }
 
-__host__ __device__ constexpr int ring_depth(int R) { return kRingBytes / (WARP * R * 8); }
+// TMA 1-D bulk copy global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
-// Per-document variable shared memory (must match the device carve below).
+// Ring of (1 - S) values: at least two mbarrier blocks of kGroup steps.
+__host__ __device__ constexpr int ring_bytes(int R) {
+  return (2 * kGroup * WARP * R * 8) > 16384 ? 2 * kGroup * WARP * R * 8 : 16384;
+}
+__host__ __device__ constexpr int ring_depth(int R) { return ring_bytes(R) / (WARP * R * 8); }
+
+__host__ __device__ inline size_t hits_bytes(int n, int m) { return align16(((size_t)n * m + 1) / 2 * 4); }
+
+// Per-document shared memory of the ring kernel (must match the carve below).
 __host__ __device__ inline size_t ring_var_bytes(int n, int m, int R) {
   const int cpw = 16 / R;
-  size_t b = align16(((size_t)n * m + 1) / 2 * 4);   // hits (16-bit cells)
-  b += align16((size_t)m * 8);                        // column positions
-  b += align16((size_t)n * 8);                        // row positions
-  b += align16((size_t)((m + cpw - 1) / cpw) * WARP * 4);  // direction codes
-  b += align16((size_t)(n < m ? n : m) * 4);          // diagonal cells of the path
+  size_t b = hits_bytes(n, m);
+  b += align16((size_t)(n + m) * 16);                          // T, P, nA, nD
+  b += align16((size_t)(n + m) * 4);                           // digit offsets
+  b += align16((size_t)(n + m) * 8);                           // positions
+  b += align16((size_t)((m + cpw - 1) / cpw) * WARP * 4);      // direction codes
+  b += align16((size_t)(n < m ? n : m) * 4);                   // path diagonal cells
   return b;
 }
 
 size_t ring_slice_bytes(int n, int m, int R) {
-  return kFixedBytes + kRingBytes + ring_var_bytes(n, m, R);
+  return kFixedBytes + ring_bytes(R) + ring_var_bytes(n, m, R);
+}
+
+size_t hits_kernel_smem(int n, int m) { return join_smem_bytes() + hits_bytes(n, m); }
+
+// ---------------------------------------------------------------------------
+// hits_kernel: dictionary join of one document -> HBM scratch
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, bm_docs D,
+                                                            bm_lexicon L, const int32_t* list,
+                                                            int n_list, const int64_t* hit_off,
+                                                            uint8_t* hits_out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int item = blockIdx.x;
+  if (item >= n_list) return;
+  const int doc = list[item];
+  const int n = D.n[doc], m = D.m[doc];
+  JoinSmem js = carve_join(smem);
+  uint32_t* hits = (uint32_t*)(smem + join_smem_bytes());
+  tile_join<true>(CtaGroup(), S, L, D.src0[doc], n, D.tgt0[doc], m, hits, js);
+  const int words4 = (int)(hits_bytes(n, m) / 16);
+  const uint4* src = (const uint4*)hits;
+  uint4* dst = (uint4*)(hits_out + hit_off[doc]);
+  for (int k = threadIdx.x; k < words4; k += blockDim.x) dst[k] = src[k];
+}
+
+// Features of one cell from staged sentence scalars (same arithmetic as
+// bm_device.cuh cell_features / margin / confidence_from_z).
+__device__ __forceinline__ double staged_score(const bm_sentences& S, const Model& M,
+                                               const uint64_t* exp_tab, int4 a, int ad0, int4 b,
+                                               int bd0, int hf, int hr, double ps, double pt) {
+  double f[7];
+  f[0] = ratio_min_max(a.x, b.x);
+  f[1] = frac_or_zero(hf, a.z);
+  f[2] = frac_or_zero(hr, b.z);
+  if (a.w == 0 && b.w == 0) {
+    f[3] = 1.0;
+  } else {
+    const int inter = (a.w && b.w) ? sorted_intersection(S.dig_id + ad0, a.w, S.dig_id + bd0, b.w) : 0;
+    f[3] = frac_or_zero(inter, a.w + b.w - inter);
+  }
+  f[4] = ratio_min_max(a.y, b.y);
+  f[5] = __dsub_rn(1.0, fabs(__dsub_rn(ps, pt)));
+  f[6] = 1.0;
+  return bmexp::confidence_from_z(margin(M, f), exp_tab);
+}
+
+// Valid (lane, row) slots of wavefront step s: lanes max(0, s-m+1) ..
+// min(nl-1, s), R rows each.
+__device__ __forceinline__ int step_slots(int s, int steps, int m, int nl, int R) {
+  if (s >= steps) return 0;
+  const int L0 = max(0, s - (m - 1));
+  const int L1 = min(nl - 1, s);
+  return (L1 - L0 + 1) * R;
 }
 
 template <int R>
 __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a) {
-  constexpr int K = ring_depth(R);   // ring depth in steps
-  constexpr int NB = K / kGroup;     // mbarrier blocks in the ring
-  constexpr int CPW = 16 / R;        // columns per direction word
+  constexpr int K = ring_depth(R);  // ring depth in steps
+  constexpr int NB = K / kGroup;    // mbarrier blocks in the ring
+  constexpr int CPW = 16 / R;       // columns per direction word
   static_assert(NB >= 2, "ring too shallow");
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -87,9 +168,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
   uint64_t* exp_tab = (uint64_t*)smem;
   uint64_t* bar_full = (uint64_t*)(smem + kExpTableWords * 8);
   uint64_t* bar_empty = bar_full + NB;
-  int* misc = (int*)(bar_empty + NB);
+  uint64_t* bar_load = bar_empty + NB;
+  int* misc = (int*)(bar_load + 1);
   double* ring = (double*)(smem + kFixedBytes);
-  uint8_t* var = smem + kFixedBytes + kRingBytes;
+  uint8_t* var = smem + kFixedBytes + ring_bytes(R);
   stage_exp_table(exp_tab, tid, kRingThreads);
 
   for (int item = blockIdx.x; item < a.n_list; item += gridDim.x) {
@@ -97,38 +179,38 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
     const int n = a.D.n[doc], m = a.D.m[doc];
     const int s0 = a.D.src0[doc], t0 = a.D.tgt0[doc];
     const double p = a.p;
-    uint32_t* hits = (uint32_t*)var;
-    double* cpos = (double*)(var + align16(((size_t)n * m + 1) / 2 * 4));
-    double* rpos = (double*)((uint8_t*)cpos + align16((size_t)m * 8));
-    uint32_t* dirs = (uint32_t*)((uint8_t*)rpos + align16((size_t)n * 8));
     const int ncg = (m + CPW - 1) / CPW;
+    uint32_t* hits = (uint32_t*)var;
+    int4* sc = (int4*)(var + hits_bytes(n, m));
+    int* scd0 = (int*)((uint8_t*)sc + align16((size_t)(n + m) * 16));
+    double* pos = (double*)((uint8_t*)scd0 + align16((size_t)(n + m) * 4));
+    uint32_t* dirs = (uint32_t*)((uint8_t*)pos + align16((size_t)(n + m) * 8));
     int32_t* dlist = (int32_t*)((uint8_t*)dirs + align16((size_t)ncg * WARP * 4));
 
-    __syncthreads();  // the previous document is completely done with smem
+    __syncthreads();  // the previous document is done with every buffer
     if (tid == 0) {
       for (int q = 0; q < NB; ++q) {
         mbar_init(bar_full + q, kProducers);
         mbar_init(bar_empty + q, 1);
       }
+      mbar_init(bar_load, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t bytes = (uint32_t)hits_bytes(n, m);
+      mbar_arrive_expect_tx(bar_load, bytes);
+      bulk_g2s(hits, a.hits + a.hit_off[doc], bytes, bar_load);
     }
-    for (int j = tid; j < m; j += kRingThreads) cpos[j] = doc_pos(j, m);
-    for (int i = tid; i < n; i += kRingThreads) rpos[i] = doc_pos(i, n);
-    JoinSmem js = carve_join((uint8_t*)ring);  // the ring is idle during the join
-    tile_join<true>(CtaGroup(), S, a.L, s0, n, t0, m, hits, js);  // ends with __syncthreads
+    // sentence scalars and positions (rows 0..n-1, then columns)
+    for (int k = tid; k < n + m; k += kRingThreads) {
+      const bool row = k < n;
+      const int g = row ? s0 + k : t0 + (k - n);
+      const SentScalars v = load_scalars(S, g);
+      sc[k] = make_int4(v.T, v.P, v.nA, v.nD);
+      scd0[k] = v.d0;
+      pos[k] = row ? doc_pos(k, n) : doc_pos(k - n, m);
+    }
+    __syncthreads();
+    mbar_wait(bar_load, 0);
 
-    if (a.debug == 1) {
-      if (tid == 0) {
-        double sum = 0.0;
-        for (int c = 0; c < n * m; ++c) {
-          int hf, hr;
-          read_hits<true>(hits, c, hf, hr);
-          sum += hf + 1000.0 * hr;
-        }
-        a.cost[doc] = sum;
-        a.rec_count[doc] = 0;
-      }
-      continue;
-    }
     const int nl = (n + R - 1) / R;
     const int steps = m + nl - 1;
     const int nblocks = (steps + kGroup - 1) / kGroup;
@@ -146,7 +228,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         if (r == my_rows - 1) bot = left[r];
       double prev_recv = (double)i0 * p;
       uint32_t dword = 0;
-      double dbg_acc = 0.0;
       for (int b = 0; b < nblocks; ++b) {
         mbar_wait(bar_full + (b % NB), (uint32_t)((b / NB) & 1));
         const int s_end = min(steps, (b + 1) * kGroup);
@@ -167,18 +248,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
             double omv[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) omv[r] = om[r];
-            if (a.debug == 2)
-              for (int r = 0; r < R; ++r)
-                if (r < my_rows) dbg_acc += omv[r];
-            if (a.debug >= 5)
-              for (int r = 0; r < R; ++r)
-                if (r < my_rows) {
-                  int hf, hr;
-                  read_hits<true>(hits, (i0 + r) * m + j, hf, hr);
-                  const double sv = cell_score(S, a.M, exp_tab, load_scalars(S, s0 + i0 + r),
-                                               load_scalars(S, t0 + j), hf, hr, rpos[i0 + r], cpos[j]);
-                  dbg_acc += (__dsub_rn(1.0, sv) != omv[r]) ? 1.0 : 0.0;
-                }
             uint32_t codes = 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -217,53 +286,42 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         for (int r = 0; r < R; ++r)
           if (i0 + r == n - 1) a.cost[doc] = left[r];
       }
-      if (a.debug == 2 || a.debug >= 5) {
-        for (int o = 16; o > 0; o >>= 1) dbg_acc += __shfl_xor_sync(FULL, dbg_acc, o);
-        if (lane == 0) a.cost[doc] = dbg_acc;
-      }
     } else {
       // ------------------------------------------------------ score warps
       const int ptid = tid - WARP;
       for (int b = 0; b < nblocks; ++b) {
         if (b >= NB) mbar_wait(bar_empty + (b % NB), (uint32_t)(((b / NB) - 1) & 1));
-        if (a.debug == 6) __nanosleep(20000);
-        // valid (lane, row) slots of each step of the block, prefix-summed
-        int cnt[kGroup];
-        int total = 0;
-#pragma unroll
-        for (int g = 0; g < kGroup; ++g) {
-          const int s = b * kGroup + g;
-          const int L0 = max(0, s - (m - 1));
-          const int L1 = min(nl - 1, s);
-          cnt[g] = (s < steps && L1 >= L0) ? (L1 - L0 + 1) * R : 0;
-          total += cnt[g];
+        const int s_end = min(steps, (b + 1) * kGroup);
+        // walk this thread's slots (stride kProducers over the concatenated
+        // valid slots of the block's steps) without re-searching each time
+        int s = b * kGroup, rem = ptid;
+        int cnt = step_slots(s, steps, m, nl, R);
+        while (s < s_end && rem >= cnt) {
+          rem -= cnt;
+          cnt = step_slots(++s, steps, m, nl, R);
         }
-        for (int f = ptid; f < total; f += kProducers) {
-          int g = 0, rem = f;
-#pragma unroll
-          for (int q = 0; q < kGroup - 1; ++q) {
-            if (g == q && rem >= cnt[q]) {
-              rem -= cnt[q];
-              g = q + 1;
-            }
-          }
-          const int s = b * kGroup + g;
+        while (s < s_end) {
           const int L = max(0, s - (m - 1)) + rem / R;
-          const int r = rem - (rem / R) * R;
+          const int r = rem % R;
           const int i = L * R + r;
           if (i < n) {
             const int j = s - L;
             int hf, hr;
             read_hits<true>(hits, i * m + j, hf, hr);
-            const double sv = cell_score(S, a.M, exp_tab, load_scalars(S, s0 + i),
-                                         load_scalars(S, t0 + j), hf, hr, rpos[i], cpos[j]);
+            const double sv = staged_score(S, a.M, exp_tab, sc[i], scd0[i], sc[n + j], scd0[n + j],
+                                           hf, hr, pos[i], pos[n + j]);
             ring[((size_t)(s % K) * WARP + L) * R + r] = __dsub_rn(1.0, sv);
+          }
+          rem += kProducers;
+          while (s < s_end && rem >= cnt) {
+            rem -= cnt;
+            cnt = step_slots(++s, steps, m, nl, R);
           }
         }
         mbar_arrive(bar_full + (b % NB));
       }
     }
-    __syncthreads();  // DP complete: dirs final
+    __syncthreads();  // DP complete: direction codes final
 
     if (tid == 0) {
       int k = 0, i = n, j = m;
@@ -300,8 +358,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         cj = cell - ci * m;
         int hf, hr;
         read_hits<true>(hits, cell, hf, hr);
-        sv = cell_score(S, a.M, exp_tab, load_scalars(S, s0 + ci), load_scalars(S, t0 + cj), hf,
-                        hr, rpos[ci], cpos[cj]);
+        sv = staged_score(S, a.M, exp_tab, sc[ci], scd0[ci], sc[n + cj], scd0[n + cj], hf, hr,
+                          pos[ci], pos[n + cj]);
         keep = sv >= a.threshold;
       }
       const unsigned mask = __ballot_sync(FULL, keep);
@@ -330,12 +388,29 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
   }
 }
 
+cudaError_t launch_hits(const FusedArgs& a, size_t smem, cudaStream_t st) {
+  if (a.n_list == 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(hits_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  hits_kernel<<<a.n_list, kHitsThreads, smem, st>>>(a.S, a.D, a.L, a.list, a.n_list, a.hit_off,
+                                                     a.hits);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) g_launches += 1;
+  return e;
+}
+
 cudaError_t launch_ring(const FusedArgs& a, int R, size_t smem, cudaStream_t st) {
   if (a.n_list == 0) return cudaSuccess;
   cudaError_t e;
 #define BM_LAUNCH_RING(RR)                                                                   \
   e = cudaFuncSetAttribute(mine_ring_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                       \
+  if (e != cudaSuccess) return e;                                                            \
+  e = cudaFuncSetAttribute(mine_ring_kernel<RR>,                                             \
+                           cudaFuncAttributePreferredSharedMemoryCarveout, 100);             \
   if (e != cudaSuccess) return e;                                                            \
   mine_ring_kernel<RR><<<a.n_list, kRingThreads, smem, st>>>(a);
   switch (R) {

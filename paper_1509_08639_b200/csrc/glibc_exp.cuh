@@ -150,22 +150,17 @@ BM_HD double exp_glibc(double x, const uint64_t* T) {
 // bimine/classifier.py:100-117: sigmoid, then clamp into [1e-300, 1-2^-53]
 // with Python's min/max semantics (first argument wins unless strictly beaten).
 BM_HD double confidence_from_z(double z, const uint64_t* T) {
-  double p;
-  if (z >= 0.0) {
-    double e = exp_glibc(-z, T);
+  // Branch-free form of the two sigmoid branches: exactly one exp and one
+  // division per call, so lanes of a warp with mixed signs do not execute both.
+  //   z >= 0: 1 / (1 + exp(-z))      z < 0 (or NaN): exp(z) / (1 + exp(z))
+  const bool nonneg = z >= 0.0;
+  const double e = exp_glibc(nonneg ? -z : z, T);
+  const double num = nonneg ? 1.0 : e;
 #if defined(__CUDA_ARCH__)
-    p = __ddiv_rn(1.0, add_(1.0, e));
+  const double p = __ddiv_rn(num, add_(1.0, e));
 #else
-    p = 1.0 / (1.0 + e);
+  const double p = num / (1.0 + e);
 #endif
-  } else {
-    double e = exp_glibc(z, T);
-#if defined(__CUDA_ARCH__)
-    p = __ddiv_rn(e, add_(1.0, e));
-#else
-    p = e / (1.0 + e);
-#endif
-  }
   const double PMIN = 1e-300;
   const double PMAX = 1.0 - 0x1p-53;
   double lo = (PMIN > p) ? PMIN : p;   // max(p, PMIN)
