@@ -101,7 +101,7 @@ size_t ring_slice_bytes(int n, int m, int R) {
   return kFixedBytes + ring_bytes(R) + ring_var_bytes(n, m, R);
 }
 
-size_t hits_kernel_smem(int n, int m) { return join_smem_bytes() + hits_bytes(n, m); }
+size_t hits_kernel_smem(int n, int m) { return align16(join_smem_bytes()) + hits_bytes(n, m); }
 
 // ---------------------------------------------------------------------------
 // hits_kernel: dictionary join of one document -> HBM scratch
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, b
   const int doc = list[item];
   const int n = D.n[doc], m = D.m[doc];
   JoinSmem js = carve_join(smem);
-  uint32_t* hits = (uint32_t*)(smem + join_smem_bytes());
+  uint32_t* hits = (uint32_t*)(smem + align16(join_smem_bytes()));
   tile_join<true>(CtaGroup(), S, L, D.src0[doc], n, D.tgt0[doc], m, hits, js);
   const int words4 = (int)(hits_bytes(n, m) / 16);
   const uint4* src = (const uint4*)hits;
