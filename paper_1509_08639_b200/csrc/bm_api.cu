@@ -7,6 +7,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -213,6 +215,20 @@ int general_nw(const GeneralPlan& g, GeneralDev& dv, double penalty, double* cos
 
 bool check_penalty(double p) { return p >= 0.0; }  // NaN fails (aligner.py:209-213)
 
+// BM_TRACE=1: host-side phase timings of the planning code on stderr.
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  const char* fn;
+  explicit HostTrace(const char* f) : on(getenv("BM_TRACE") != nullptr), t0(std::chrono::steady_clock::now()), fn(f) {}
+  void mark(const char* what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[bm trace] %s %-24s %8.3f ms\n", fn, what,
+            std::chrono::duration<double, std::milli>(t - t0).count());
+  }
+};
+
 }  // namespace
 
 extern "C" {
@@ -354,8 +370,10 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   BM_CK(ensure_quot_table(), "quotient table");
   if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
   cudaStream_t st = (cudaStream_t)stream;
+  HostTrace tr("bm_mine");
   const int nd = docs->n_docs;
   BM_CK(cudaMemsetAsync(rec_count, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
+  tr.mark("memset");
   std::vector<int32_t> fused[4];
   size_t fused_smem[4] = {0, 0, 0, 0}, hits_smem[4] = {0, 0, 0, 0};
   std::vector<int64_t> hit_off(nd, 0);
@@ -381,13 +399,16 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       g.add(d, n, m);
     }
   }
+  tr.mark("route");
   Scratch sc(st);
   const Model M = to_model(model);
   if (hit_total > 0) {
     uint8_t* hits = nullptr;
     int64_t* dho = nullptr;
     BM_CK(sc.alloc(&hits, (size_t)hit_total), "alloc hits");
+    tr.mark("alloc hits");
     BM_CK(sc.upload(&dho, hit_off), "upload");
+    tr.mark("upload hit_off");
     for (int q = 0; q < 4; ++q) {
       if (fused[q].empty()) continue;
       int32_t* list = nullptr;
@@ -407,8 +428,11 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       a.cost = cost;
       a.hits = hits;
       a.hit_off = dho;
+      tr.mark("upload list");
       BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
+      tr.mark("launch hits");
       BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
+      tr.mark("launch ring");
     }
   }
   if (!g.docs.empty()) {
@@ -459,44 +483,64 @@ int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_
   return BM_OK;
 }
 
+// Copy stream of the calling thread on the current device (H2D of chunk k+1
+// overlaps the kernels of chunk k in bm_mine_host).
+cudaStream_t copy_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  static thread_local int dev_of = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (s == nullptr || dev_of != dev) {
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    dev_of = dev;
+  }
+  return s;
+}
+
 int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh,
                  const bm_model* model, double threshold, double penalty, bm_record* rec_out,
                  int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  HostTrace tr("bm_mine_host");
+  BM_CK(ensure_quot_table(), "device init");
+  cudaStream_t cs = copy_stream();
   const int ns = sh->n_sent, nd = dh->n_docs;
   const int64_t ne = ns ? sh->tok_off[ns] : 0;
   const int64_t ndig = ns ? sh->dig_off[ns] : 0;
   const int nid = lh->n_ids;
-  // per-doc limits computed on the host (routing input of bm_mine)
+  // routing input: per-doc max |A|; one vectorisable pass decides whether any
+  // document can exceed the fused kernel's 8-bit hit counters at all
+  int32_t gmax = 0;
+  for (int k = 0; k < ns; ++k) gmax = std::max(gmax, sh->n_alpha[k]);
   std::vector<int32_t> amax(nd, 0);
+  if (gmax > 255) {
+    for (int d = 0; d < nd; ++d) {
+      int v = 0;
+      for (int k = 0; k < dh->n[d]; ++k) v = std::max(v, sh->n_alpha[dh->src0[d] + k]);
+      for (int k = 0; k < dh->m[d]; ++k) v = std::max(v, sh->n_alpha[dh->tgt0[d] + k]);
+      amax[d] = v;
+    }
+  }
   std::vector<int64_t> roff(nd);
   int64_t rt = 0;
   for (int d = 0; d < nd; ++d) {
-    int a = 0;
-    for (int k = 0; k < dh->n[d]; ++k) a = std::max(a, sh->n_alpha[dh->src0[d] + k]);
-    for (int k = 0; k < dh->m[d]; ++k) a = std::max(a, sh->n_alpha[dh->tgt0[d] + k]);
-    amax[d] = a;
     roff[d] = rt;
     rt += std::max(0, std::min(dh->n[d], dh->m[d]));
   }
+  tr.mark("host prep");
   Scratch sc(st);
-  auto up = [&](auto** dst, const auto* src, size_t count) -> cudaError_t {
-    cudaError_t e = sc.alloc(dst, count);
-    if (e != cudaSuccess || count == 0) return e;
-    return cudaMemcpyAsync(*dst, src, count * sizeof(**dst), cudaMemcpyHostToDevice, st);
-  };
   bm_sentences sd;
   sd.n_sent = ns;
   int32_t *a0, *a1, *a2, *a3, *a4, *a5, *a6;
   uint16_t* a7;
-  BM_CK(up(&a0, sh->n_tok, ns), "h2d");
-  BM_CK(up(&a1, sh->n_punct, ns), "h2d");
-  BM_CK(up(&a2, sh->n_alpha, ns), "h2d");
-  BM_CK(up(&a3, sh->tok_off, ns + 1), "h2d");
-  BM_CK(up(&a4, sh->tok_id, ne), "h2d");
-  BM_CK(up(&a7, sh->tok_alpha, ne), "h2d");
-  BM_CK(up(&a5, sh->dig_off, ns + 1), "h2d");
-  BM_CK(up(&a6, sh->dig_id, ndig), "h2d");
+  BM_CK(sc.alloc(&a0, ns), "alloc");
+  BM_CK(sc.alloc(&a1, ns), "alloc");
+  BM_CK(sc.alloc(&a2, ns), "alloc");
+  BM_CK(sc.alloc(&a3, ns + 1), "alloc");
+  BM_CK(sc.alloc(&a4, ne), "alloc");
+  BM_CK(sc.alloc(&a7, ne), "alloc");
+  BM_CK(sc.alloc(&a5, ns + 1), "alloc");
+  BM_CK(sc.alloc(&a6, ndig), "alloc");
   sd.n_tok = a0;
   sd.n_punct = a1;
   sd.n_alpha = a2;
@@ -508,21 +552,18 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
   bm_docs dd;
   dd.n_docs = nd;
   int32_t *b0, *b1, *b2, *b3;
-  BM_CK(up(&b0, dh->src0, nd), "h2d");
-  BM_CK(up(&b1, dh->n, nd), "h2d");
-  BM_CK(up(&b2, dh->tgt0, nd), "h2d");
-  BM_CK(up(&b3, dh->m, nd), "h2d");
-  dd.src0 = b0;
-  dd.n = b1;
-  dd.tgt0 = b2;
-  dd.m = b3;
+  BM_CK(sc.alloc(&b0, nd), "alloc");
+  BM_CK(sc.alloc(&b1, nd), "alloc");
+  BM_CK(sc.alloc(&b2, nd), "alloc");
+  BM_CK(sc.alloc(&b3, nd), "alloc");
   bm_lexicon ld;
   ld.n_ids = nid;
   int32_t *c0, *c1, *c2, *c3;
-  BM_CK(up(&c0, lh->fwd_off, nid + 1), "h2d");
-  BM_CK(up(&c1, lh->fwd_cand, nid ? lh->fwd_off[nid] : 0), "h2d");
-  BM_CK(up(&c2, lh->rev_off, nid + 1), "h2d");
-  BM_CK(up(&c3, lh->rev_cand, nid ? lh->rev_off[nid] : 0), "h2d");
+  const int64_t nf = nid ? lh->fwd_off[nid] : 0, nr = nid ? lh->rev_off[nid] : 0;
+  BM_CK(sc.alloc(&c0, nid + 1), "alloc");
+  BM_CK(sc.alloc(&c1, nf), "alloc");
+  BM_CK(sc.alloc(&c2, nid + 1), "alloc");
+  BM_CK(sc.alloc(&c3, nr), "alloc");
   ld.fwd_off = c0;
   ld.fwd_cand = c1;
   ld.rev_off = c2;
@@ -532,24 +573,94 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
   int32_t* cnt = nullptr;
   double* cost = nullptr;
   int64_t* total = nullptr;
-  BM_CK(up(&droff, roff.data(), nd), "h2d");
+  BM_CK(sc.alloc(&droff, nd), "alloc");
   BM_CK(sc.alloc(&rec, (size_t)rt), "alloc");
   BM_CK(sc.alloc(&dense, (size_t)rt), "alloc");
   BM_CK(sc.alloc(&cnt, nd), "alloc");
   BM_CK(sc.alloc(&cost, nd), "alloc");
   BM_CK(sc.alloc(&total, 1), "alloc");
-  int rc = bm_mine(&sd, &dd, dh->n, dh->m, amax.data(), &ld, model, threshold, penalty, droff, rec,
-                   cnt, cost, stream);
-  if (rc) return rc;
-  rc = bm_compact(rec, droff, cnt, nd, dense, total, stream);
+  // the copy stream may only touch the scratch once it is allocated on st
+  cudaEvent_t ready;
+  BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+  BM_CK(cudaEventRecord(ready, st), "event");
+  BM_CK(cudaStreamWaitEvent(cs, ready, 0), "event");
+  auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs) : cudaSuccess;
+  };
+  BM_CK(h2d(c0, lh->fwd_off, (nid + 1) * 4), "h2d");
+  BM_CK(h2d(c1, lh->fwd_cand, nf * 4), "h2d");
+  BM_CK(h2d(c2, lh->rev_off, (nid + 1) * 4), "h2d");
+  BM_CK(h2d(c3, lh->rev_cand, nr * 4), "h2d");
+  BM_CK(h2d(droff, roff.data(), nd * 8), "h2d");
+  BM_CK(h2d(b0, dh->src0, nd * 4), "h2d");
+  BM_CK(h2d(b1, dh->n, nd * 4), "h2d");
+  BM_CK(h2d(b2, dh->tgt0, nd * 4), "h2d");
+  BM_CK(h2d(b3, dh->m, nd * 4), "h2d");
+  tr.mark("alloc + small h2d");
+  // chunks of documents: H2D the sentence range each chunk touches on the
+  // copy stream, mine it on the compute stream once its copy event fired
+  const int64_t kChunkCells = 16ll << 20;
+  std::vector<cudaEvent_t> evs;
+  int d0 = 0;
+  while (d0 < nd) {
+    int d1 = d0;
+    int64_t cells = 0;
+    int lo = ns, hi = 0;
+    while (d1 < nd && (d1 == d0 || cells < kChunkCells)) {
+      cells += (int64_t)dh->n[d1] * dh->m[d1];
+      if (dh->n[d1] > 0) {
+        lo = std::min(lo, dh->src0[d1]);
+        hi = std::max(hi, dh->src0[d1] + dh->n[d1]);
+      }
+      if (dh->m[d1] > 0) {
+        lo = std::min(lo, dh->tgt0[d1]);
+        hi = std::max(hi, dh->tgt0[d1] + dh->m[d1]);
+      }
+      ++d1;
+    }
+    if (hi > lo) {
+      const int64_t e0 = sh->tok_off[lo], e1 = sh->tok_off[hi];
+      const int64_t g0 = sh->dig_off[lo], g1 = sh->dig_off[hi];
+      const size_t cntS = (size_t)(hi - lo);
+      BM_CK(h2d(a0 + lo, sh->n_tok + lo, cntS * 4), "h2d");
+      BM_CK(h2d(a1 + lo, sh->n_punct + lo, cntS * 4), "h2d");
+      BM_CK(h2d(a2 + lo, sh->n_alpha + lo, cntS * 4), "h2d");
+      BM_CK(h2d(a3 + lo, sh->tok_off + lo, (cntS + 1) * 4), "h2d");
+      BM_CK(h2d(a5 + lo, sh->dig_off + lo, (cntS + 1) * 4), "h2d");
+      BM_CK(h2d(a4 + e0, sh->tok_id + e0, (size_t)(e1 - e0) * 4), "h2d");
+      BM_CK(h2d(a7 + e0, sh->tok_alpha + e0, (size_t)(e1 - e0) * 2), "h2d");
+      BM_CK(h2d(a6 + g0, sh->dig_id + g0, (size_t)(g1 - g0) * 4), "h2d");
+    }
+    cudaEvent_t ev;
+    BM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    BM_CK(cudaEventRecord(ev, cs), "event");
+    evs.push_back(ev);
+    BM_CK(cudaStreamWaitEvent(st, ev, 0), "event");
+    bm_docs dc = dd;
+    dc.n_docs = d1 - d0;
+    dc.src0 = b0 + d0;
+    dc.n = b1 + d0;
+    dc.tgt0 = b2 + d0;
+    dc.m = b3 + d0;
+    int rc = bm_mine(&sd, &dc, dh->n + d0, dh->m + d0, amax.data() + d0, &ld, model, threshold,
+                     penalty, droff + d0, rec, cnt + d0, cost + d0, stream);
+    if (rc) return rc;
+    d0 = d1;
+  }
+  tr.mark("chunks enqueued");
+  int rc = bm_compact(rec, droff, cnt, nd, dense, total, stream);
   if (rc) return rc;
   int64_t tot = 0;
   BM_CK(cudaMemcpyAsync(&tot, total, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "d2h");
-  BM_CK(cudaStreamSynchronize(st), "sync");
-  if (tot > rec_cap) return fail(BM_ELIMIT, "record buffer too small");
-  if (tot) BM_CK(cudaMemcpyAsync(rec_out, dense, tot * sizeof(bm_record), cudaMemcpyDeviceToHost, st), "d2h");
   if (cost_out) BM_CK(cudaMemcpyAsync(cost_out, cost, nd * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
   BM_CK(cudaStreamSynchronize(st), "sync");
+  tr.mark("mined + compacted");
+  if (tot > rec_cap) return fail(BM_ELIMIT, "record buffer too small");
+  if (tot) BM_CK(cudaMemcpyAsync(rec_out, dense, tot * sizeof(bm_record), cudaMemcpyDeviceToHost, st), "d2h");
+  BM_CK(cudaStreamSynchronize(st), "sync");
+  tr.mark("records d2h");
+  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+  cudaEventDestroy(ready);
   *n_rec = tot;
   return BM_OK;
 }

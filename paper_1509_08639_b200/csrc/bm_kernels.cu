@@ -32,6 +32,14 @@ cudaError_t ensure_quot_table() {
     for (int k = 0; k <= kQuotMax; ++k)
       host[d * kQuotStride + k] = (d && k <= d) ? (double)k / (double)d : 0.0;
   e = cudaMemcpyToSymbol(g_quot, host, sizeof(host));
+  if (e != cudaSuccess) return e;
+  // Keep stream-ordered scratch cached in the device pool between calls
+  // (the default threshold hands it back to the driver at every sync).
+  cudaMemPool_t pool;
+  e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = ~0ull;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   if (e == cudaSuccess) done_dev = dev;
   return e;
 }
@@ -601,7 +609,11 @@ __global__ void gather_records_kernel(const bm_record* __restrict__ rec,
   const int lane = threadIdx.x & (WARP - 1);
   const bm_record* src = rec + rec_off[d];
   bm_record* dst = dense + dense_off[d];
-  for (int k = lane; k < cnt[d]; k += WARP) dst[k] = src[k];
+  for (int k = lane; k < cnt[d]; k += WARP) {
+    bm_record r = src[k];
+    r.doc = d;  // document index of the compacted batch
+    dst[k] = r;
+  }
 }
 
 cudaError_t launch_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* cnt,
