@@ -302,6 +302,7 @@ def run_ours(args):
         "n_tok", "n_punct", "n_alpha", "tok_off", "tok_id", "tok_alpha", "dig_off", "dig_id")))
     alg_bytes = 8 * cells + in_bytes + 24 * n_rec
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic, traffic_src = measured_traffic()
     fp64 = fp64_roof(lib, torch, dev, stream)
 
     # end to end through the C ABI with host buffers (pinned)
@@ -336,9 +337,10 @@ def run_ours(args):
             "nw_gcups": cells * world * args.steps / (tot_ms / 1e3) / 1e9,
             "records_per_step": n_rec,
             "roofline": {
-                "bound": "hbm", "kernel": "mine_fused_kernel<4>",
+                "bound": "hbm", "kernel": "bm_mine = hits_kernel + mine_ring_kernel<4>",
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
+                "frac": achieved / hbm_peak, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "alg_bytes_per_launch": alg_bytes,
                 "alg_bytes_def": "SURVEY 8(d): 8 B/cell similarity matrix + packed inputs + records",
                 "kernel_ms": kern_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)",
@@ -380,6 +382,22 @@ def kernel_ms(lib, dc, view, dl, mstruct, n_h, m_h, amax, rec_off_d, rec, cnt, c
         b.synchronize()
         out.append(a.elapsed_time(b))
     return float(np.mean(out[1:])) if len(out) > 1 else float(out[0])
+
+
+def measured_traffic():
+    """DRAM bytes of one C2 bm_mine launch pair from the committed ncu capture
+    (profiles/, dram__bytes_read.sum + dram__bytes_write.sum)."""
+    prof = sorted(p for p in os.listdir(os.path.join(ROOT, "profiles"))
+                  if p.endswith("_ncu_raw_metrics.json")) if os.path.isdir(os.path.join(ROOT, "profiles")) else []
+    if not prof:
+        return None, None
+    d = json.load(open(os.path.join(ROOT, "profiles", prof[-1])))
+    tot = 0.0
+    for k in ("hits_kernel", "mine_ring_kernel<4>"):
+        if k not in d:
+            return None, None
+        tot += float(d[k]["dram__bytes_read.sum"]) + float(d[k]["dram__bytes_write.sum"])
+    return tot * 1e6, f"profiles/{prof[-1]} (ncu --set full, MB -> bytes)"
 
 
 def fp64_roof(lib, torch, dev, stream):

@@ -334,3 +334,16 @@ def test_tune_synthetic_vs_oracle(oracle_mod):
                               engine.DocView.of(sc.packed), model, pens, thrs, keys)
     wp, wh = oracle_mod.tune(oracle_mod.HostBatch(sc.packed, plex), model, pens, thrs, keys, threads=8)
     assert np.array_equal(p, wp) and np.array_equal(h, wh)
+
+
+def test_sharded_mining_equals_single(oracle_mod):
+    """Two LPT shards mined separately (as two ranks would) == one batch."""
+    from paper_1509_08639_b200 import engine, shard, synth
+
+    sc = _synth_mixed(7)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    parts = [shard.mine_shard(sc.packed, plex, model, 0.5, 0.2, r, 2)[0] for r in range(2)]
+    got = shard.restore_order(parts)
+    want, _ = oracle_mod.mine(oracle_mod.HostBatch(sc.packed, plex), model, 0.5, 0.2, threads=8)
+    assert got.tobytes() == want.tobytes()
