@@ -233,7 +233,7 @@ def run_ours(args):
     dl = engine.DeviceLexicon.upload(plex)
     view = engine.DocView.of(c)
     n_h, m_h = view.n, view.m
-    amax = np.ascontiguousarray(view.alpha_max(c), dtype=np.int32)
+    amax = np.ascontiguousarray(view.token_max(c), dtype=np.int32)
     dev = torch.device("cuda", local)
     rec_off = engine.record_offsets(n_h, m_h)
     cap = int(np.minimum(n_h, m_h).sum())

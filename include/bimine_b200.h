@@ -187,7 +187,8 @@ int bm_select(const double* S, int64_t pitch, const int32_t* ci, const int32_t* 
  * any size are accepted: the library routes each one either to the fused
  * warp-per-document kernel (no similarity matrix is materialised) or to the
  * banded K1 -> K2/K3 -> K4 path. n_host/m_host/amax_host are host arrays
- * (amax = the largest n_alpha of any sentence of the doc). Scratch is
+ * (amax = the largest n_tok of any sentence of the doc; <= 255 allows the
+ * fused tier). Scratch is
  * stream-ordered (cudaMallocAsync on `stream`).
  */
 int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,

@@ -508,16 +508,16 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
   const int64_t ne = ns ? sh->tok_off[ns] : 0;
   const int64_t ndig = ns ? sh->dig_off[ns] : 0;
   const int nid = lh->n_ids;
-  // routing input: per-doc max |A|; one vectorisable pass decides whether any
-  // document can exceed the fused kernel's 8-bit hit counters at all
+  // routing input: per-doc max token count; one vectorisable pass decides
+  // whether any document can exceed the fused kernel's 8-bit counters at all
   int32_t gmax = 0;
-  for (int k = 0; k < ns; ++k) gmax = std::max(gmax, sh->n_alpha[k]);
+  for (int k = 0; k < ns; ++k) gmax = std::max(gmax, sh->n_tok[k]);
   std::vector<int32_t> amax(nd, 0);
   if (gmax > 255) {
     for (int d = 0; d < nd; ++d) {
       int v = 0;
-      for (int k = 0; k < dh->n[d]; ++k) v = std::max(v, sh->n_alpha[dh->src0[d] + k]);
-      for (int k = 0; k < dh->m[d]; ++k) v = std::max(v, sh->n_alpha[dh->tgt0[d] + k]);
+      for (int k = 0; k < dh->n[d]; ++k) v = std::max(v, sh->n_tok[dh->src0[d] + k]);
+      for (int k = 0; k < dh->m[d]; ++k) v = std::max(v, sh->n_tok[dh->tgt0[d] + k]);
       amax[d] = v;
     }
   }

@@ -33,6 +33,17 @@ cudaError_t ensure_quot_table() {
       host[d * kQuotStride + k] = (d && k <= d) ? (double)k / (double)d : 0.0;
   e = cudaMemcpyToSymbol(g_quot, host, sizeof(host));
   if (e != cudaSuccess) return e;
+  static double r2[kPairMax * kPairMax], f2[kPairMax * kPairMax];
+  for (int a = 0; a < kPairMax; ++a)
+    for (int b = 0; b < kPairMax; ++b) {
+      const int lo = a < b ? a : b, hi = a < b ? b : a;
+      r2[a * kPairMax + b] = hi == 0 ? 1.0 : (double)lo / (double)hi;
+      f2[a * kPairMax + b] = b == 0 ? 0.0 : (double)a / (double)b;
+    }
+  e = cudaMemcpyToSymbol(g_ratio2, r2, sizeof(r2));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyToSymbol(g_frac2, f2, sizeof(f2));
+  if (e != cudaSuccess) return e;
   // Keep stream-ordered scratch cached in the device pool between calls
   // (the default threshold hands it back to the driver at every sync).
   cudaMemPool_t pool;

@@ -89,9 +89,7 @@ __host__ __device__ inline size_t hits_bytes(int n, int m) { return align16(((si
 __host__ __device__ inline size_t ring_var_bytes(int n, int m, int R) {
   const int cpw = 16 / R;
   size_t b = hits_bytes(n, m);
-  b += align16((size_t)(n + m) * 16);                          // T, P, nA, nD
-  b += align16((size_t)(n + m) * 4);                           // digit offsets
-  b += align16((size_t)(n + m) * 8);                           // positions
+  b += (size_t)(n + m) * 16;                                   // SPack per sentence
   b += align16((size_t)((m + cpw - 1) / cpw) * WARP * 4);      // direction codes
   b += align16((size_t)(n < m ? n : m) * 4);                   // path diagonal cells
   return b;
@@ -124,23 +122,36 @@ __global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, b
   for (int k = threadIdx.x; k < words4; k += blockDim.x) dst[k] = src[k];
 }
 
-// Features of one cell from staged sentence scalars (same arithmetic as
-// bm_device.cuh cell_features / margin / confidence_from_z).
+// One sentence as the fused kernel stages it in shared memory (16 bytes):
+// T, P, |A|, |D| in one byte each (routing guarantees T <= 255 and T bounds
+// the other three), the offset of its digit set, its document position.
+struct __align__(16) SPack {
+  uint32_t tpad;  // T | P << 8 | nA << 16 | nD << 24
+  int32_t d0;
+  double pos;
+};
+
+// Features of one cell from staged sentences (same values, operation by
+// operation, as bm_device.cuh cell_features / margin / confidence_from_z).
 __device__ __forceinline__ double staged_score(const bm_sentences& S, const Model& M,
-                                               const uint64_t* exp_tab, int4 a, int ad0, int4 b,
-                                               int bd0, int hf, int hr, double ps, double pt) {
+                                               const uint64_t* exp_tab, const SPack a,
+                                               const SPack b, int hf, int hr) {
+  const int aT = a.tpad & 0xff, aP = (a.tpad >> 8) & 0xff, aA = (a.tpad >> 16) & 0xff,
+            aD = a.tpad >> 24;
+  const int bT = b.tpad & 0xff, bP = (b.tpad >> 8) & 0xff, bA = (b.tpad >> 16) & 0xff,
+            bD = b.tpad >> 24;
   double f[7];
-  f[0] = ratio_min_max(a.x, b.x);
-  f[1] = frac_or_zero(hf, a.z);
-  f[2] = frac_or_zero(hr, b.z);
-  if (a.w == 0 && b.w == 0) {
+  f[0] = ratio_pair(aT, bT);
+  f[1] = frac_pair(hf, aA);
+  f[2] = frac_pair(hr, bA);
+  if ((aD | bD) == 0) {
     f[3] = 1.0;
   } else {
-    const int inter = (a.w && b.w) ? sorted_intersection(S.dig_id + ad0, a.w, S.dig_id + bd0, b.w) : 0;
-    f[3] = frac_or_zero(inter, a.w + b.w - inter);
+    const int inter = (aD && bD) ? sorted_intersection(S.dig_id + a.d0, aD, S.dig_id + b.d0, bD) : 0;
+    f[3] = frac_pair(inter, aD + bD - inter);
   }
-  f[4] = ratio_min_max(a.y, b.y);
-  f[5] = __dsub_rn(1.0, fabs(__dsub_rn(ps, pt)));
+  f[4] = ratio_pair(aP, bP);
+  f[5] = __dsub_rn(1.0, fabs(__dsub_rn(a.pos, b.pos)));
   f[6] = 1.0;
   return bmexp::confidence_from_z(margin(M, f), exp_tab);
 }
@@ -181,10 +192,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
     const double p = a.p;
     const int ncg = (m + CPW - 1) / CPW;
     uint32_t* hits = (uint32_t*)var;
-    int4* sc = (int4*)(var + hits_bytes(n, m));
-    int* scd0 = (int*)((uint8_t*)sc + align16((size_t)(n + m) * 16));
-    double* pos = (double*)((uint8_t*)scd0 + align16((size_t)(n + m) * 4));
-    uint32_t* dirs = (uint32_t*)((uint8_t*)pos + align16((size_t)(n + m) * 8));
+    SPack* sp = (SPack*)(var + hits_bytes(n, m));
+    uint32_t* dirs = (uint32_t*)((uint8_t*)sp + (size_t)(n + m) * 16);
     int32_t* dlist = (int32_t*)((uint8_t*)dirs + align16((size_t)ncg * WARP * 4));
 
     __syncthreads();  // the previous document is done with every buffer
@@ -199,14 +208,16 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
       mbar_arrive_expect_tx(bar_load, bytes);
       bulk_g2s(hits, a.hits + a.hit_off[doc], bytes, bar_load);
     }
-    // sentence scalars and positions (rows 0..n-1, then columns)
+    // sentences of the document (rows 0..n-1, then columns)
     for (int k = tid; k < n + m; k += kRingThreads) {
       const bool row = k < n;
       const int g = row ? s0 + k : t0 + (k - n);
       const SentScalars v = load_scalars(S, g);
-      sc[k] = make_int4(v.T, v.P, v.nA, v.nD);
-      scd0[k] = v.d0;
-      pos[k] = row ? doc_pos(k, n) : doc_pos(k - n, m);
+      SPack q;
+      q.tpad = (uint32_t)v.T | ((uint32_t)v.P << 8) | ((uint32_t)v.nA << 16) | ((uint32_t)v.nD << 24);
+      q.d0 = v.d0;
+      q.pos = row ? doc_pos(k, n) : doc_pos(k - n, m);
+      sp[k] = q;
     }
     __syncthreads();
     mbar_wait(bar_load, 0);
@@ -308,8 +319,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
             const int j = s - L;
             int hf, hr;
             read_hits<true>(hits, i * m + j, hf, hr);
-            const double sv = staged_score(S, a.M, exp_tab, sc[i], scd0[i], sc[n + j], scd0[n + j],
-                                           hf, hr, pos[i], pos[n + j]);
+            const double sv = staged_score(S, a.M, exp_tab, sp[i], sp[n + j], hf, hr);
             ring[((size_t)(s % K) * WARP + L) * R + r] = __dsub_rn(1.0, sv);
           }
           rem += kProducers;
@@ -358,8 +368,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         cj = cell - ci * m;
         int hf, hr;
         read_hits<true>(hits, cell, hf, hr);
-        sv = staged_score(S, a.M, exp_tab, sc[ci], scd0[ci], sc[n + cj], scd0[n + cj], hf, hr,
-                          pos[ci], pos[n + cj]);
+        sv = staged_score(S, a.M, exp_tab, sp[ci], sp[n + cj], hf, hr);
         keep = sv >= a.threshold;
       }
       const unsigned mask = __ballot_sync(FULL, keep);

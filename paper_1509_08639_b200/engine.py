@@ -114,11 +114,11 @@ class DocView:
             n, m = np.where(sw, m, n), np.where(sw, n, m)
         return cls.upload(s0, n, t0, m)
 
-    def alpha_max(self, corpus: PackedCorpus) -> np.ndarray:
+    def token_max(self, corpus: PackedCorpus) -> np.ndarray:
         view = PackedCorpus(corpus.n_tok, corpus.n_punct, corpus.n_alpha, corpus.tok_off,
                             corpus.tok_id, corpus.tok_alpha, corpus.dig_off, corpus.dig_id,
                             self.src0, self.n, self.tgt0, self.m)
-        return view.doc_alpha_max()
+        return view.doc_token_max()
 
 
 def _i64(x) -> np.ndarray:
@@ -242,7 +242,7 @@ def mine(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, threshold: f
     cnt = torch.zeros(max(k, 1), dtype=torch.int32, device=dev)
     cost = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
     rec_off_d = to_dev(rec_off, dev)
-    amax = view.alpha_max(dc.corpus)
+    amax = view.token_max(dc.corpus)
     n_h, m_h, a_h = _i32(n), _i32(m), _i32(amax)
     N.check(lib.bm_mine(C.byref(dc.sent), C.byref(docs), n_h.ctypes.data, m_h.ctypes.data,
                         a_h.ctypes.data, C.byref(lex), C.byref(N.model_struct(model)),

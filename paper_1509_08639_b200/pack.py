@@ -52,12 +52,14 @@ class PackedCorpus:
     def n_docs(self) -> int:
         return int(self.n.shape[0])
 
-    def doc_alpha_max(self) -> np.ndarray:
-        """Largest |A| of any sentence of each doc (routing input of bm_mine)."""
+    def doc_token_max(self) -> np.ndarray:
+        """Largest token count T of any sentence of each doc (routing input of
+        bm_mine: T bounds |A|, P and |D|, so T <= 255 lets the fused kernel
+        keep all four in one byte each)."""
         out = np.zeros(self.n_docs, dtype=np.int32)
         if self.n_sent == 0 or self.n_docs == 0:
             return out
-        a = np.append(self.n_alpha, 0).astype(np.int32)  # sentinel: e may equal n_sent
+        a = np.append(self.n_tok, 0).astype(np.int32)  # sentinel: e may equal n_sent
         for lo, cnt in ((self.src0, self.n), (self.tgt0, self.m)):
             lo = lo.astype(np.int64)
             ind = np.empty(2 * lo.size, dtype=np.int64)

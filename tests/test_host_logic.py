@@ -263,10 +263,10 @@ def test_pack_lexicon_keeps_only_present_candidates(world500):
         assert cands == want
 
 
-def test_doc_alpha_max_matches_loop():
+def test_doc_token_max_matches_loop():
     corpus = pack_pairs(pairs_of(load_docs("docs_stress.jsonl")))
-    am = corpus.doc_alpha_max()
+    am = corpus.doc_token_max()
     for d in range(corpus.n_docs):
-        s = corpus.n_alpha[corpus.src0[d]:corpus.src0[d] + corpus.n[d]].tolist()
-        t = corpus.n_alpha[corpus.tgt0[d]:corpus.tgt0[d] + corpus.m[d]].tolist()
+        s = corpus.n_tok[corpus.src0[d]:corpus.src0[d] + corpus.n[d]].tolist()
+        t = corpus.n_tok[corpus.tgt0[d]:corpus.tgt0[d] + corpus.m[d]].tolist()
         assert am[d] == max(s + t + [0])

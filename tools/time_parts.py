@@ -12,7 +12,7 @@ plex = sc.world.packed_lexicon()
 dc = engine.DeviceCorpus.upload(c); dl = engine.DeviceLexicon.upload(plex)
 view = engine.DocView.of(c)
 n_h, m_h = view.n, view.m
-amax = np.ascontiguousarray(view.alpha_max(c), dtype=np.int32)
+amax = np.ascontiguousarray(view.token_max(c), dtype=np.int32)
 dev = torch.device("cuda")
 rec_off = engine.record_offsets(n_h, m_h); cap = int(np.minimum(n_h, m_h).sum())
 rec = torch.empty(cap * 24, dtype=torch.uint8, device=dev); dense = torch.empty_like(rec)
