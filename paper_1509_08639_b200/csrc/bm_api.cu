@@ -428,6 +428,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       a.cost = cost;
       a.hits = hits;
       a.hit_off = dho;
+      a.tabs = pair_tables();
       tr.mark("upload list");
       BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
       tr.mark("launch hits");

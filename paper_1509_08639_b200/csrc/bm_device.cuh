@@ -32,12 +32,15 @@ constexpr int kQuotEntries = kQuotStride * kQuotStride;  // [den][num]
 static __device__ double g_quot[kQuotEntries];  // filled by ensure_quot_table()
 
 // Branch-free feature tables for counts < kPairMax, indexed by the two counts
-// as they occur (filled by ensure_quot_table(), host IEEE division):
-//   g_ratio2[a * kPairMax + b] = min(a,b)/max(a,b), 1.0 for a = b = 0 (classifier.py:62-65)
-//   g_frac2[k * kPairMax + d]  = k/d, 0.0 for d = 0              (lexicon.py:96-105)
-constexpr int kPairMax = 64;
-static __device__ double g_ratio2[kPairMax * kPairMax];
-static __device__ double g_frac2[kPairMax * kPairMax];
+// as they occur (global memory, filled once per device by ensure_quot_table()
+// with host IEEE division; read through L1):
+//   ratio2[a * kPairMax + b] = min(a,b)/max(a,b), 1.0 for a = b = 0 (classifier.py:62-65)
+//   frac2[k * kPairMax + d]  = k/d, 0.0 for d = 0              (lexicon.py:96-105)
+constexpr int kPairMax = 256;
+struct PairTables {
+  const double* ratio2;
+  const double* frac2;
+};
 
 __device__ __forceinline__ double quot(int num, int den) {  // 0 < num <= den
   if (den <= kQuotMax) return __ldg(&g_quot[den * kQuotStride + num]);
@@ -48,15 +51,6 @@ __device__ __forceinline__ double quot(int num, int den) {  // 0 < num <= den
 __device__ __forceinline__ double ratio_min_max(int a, int b);
 __device__ __forceinline__ double frac_or_zero(int num, int den);
 
-__device__ __forceinline__ double ratio_pair(int a, int b) {
-  if ((a | b) < kPairMax) return __ldg(&g_ratio2[a * kPairMax + b]);
-  return ratio_min_max(a, b);
-}
-
-__device__ __forceinline__ double frac_pair(int num, int den) {
-  if ((num | den) < kPairMax) return __ldg(&g_frac2[num * kPairMax + den]);
-  return frac_or_zero(num, den);
-}
 
 __device__ __forceinline__ double ratio_min_max(int a, int b) {
   int lo = a < b ? a : b;

@@ -13,11 +13,20 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <vector>
 
 #include "bm_kernels.cuh"
 
 namespace bm {
 
+
+PairTables g_pair_tables[64];
+
+PairTables pair_tables() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return g_pair_tables[dev];
+}
 
 // Fill g_quot on the current device (host IEEE division is correctly rounded,
 // exactly like CPython's int/int true division of small ints).
@@ -33,17 +42,22 @@ cudaError_t ensure_quot_table() {
       host[d * kQuotStride + k] = (d && k <= d) ? (double)k / (double)d : 0.0;
   e = cudaMemcpyToSymbol(g_quot, host, sizeof(host));
   if (e != cudaSuccess) return e;
-  static double r2[kPairMax * kPairMax], f2[kPairMax * kPairMax];
+  static std::vector<double> r2(kPairMax * kPairMax), f2(kPairMax * kPairMax);
   for (int a = 0; a < kPairMax; ++a)
     for (int b = 0; b < kPairMax; ++b) {
       const int lo = a < b ? a : b, hi = a < b ? b : a;
       r2[a * kPairMax + b] = hi == 0 ? 1.0 : (double)lo / (double)hi;
       f2[a * kPairMax + b] = b == 0 ? 0.0 : (double)a / (double)b;
     }
-  e = cudaMemcpyToSymbol(g_ratio2, r2, sizeof(r2));
+  double* tab = nullptr;
+  e = cudaMalloc(&tab, 2 * r2.size() * sizeof(double));
   if (e != cudaSuccess) return e;
-  e = cudaMemcpyToSymbol(g_frac2, f2, sizeof(f2));
+  e = cudaMemcpy(tab, r2.data(), r2.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
+  e = cudaMemcpy(tab + r2.size(), f2.data(), f2.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  g_pair_tables[dev].ratio2 = tab;
+  g_pair_tables[dev].frac2 = tab + r2.size();
   // Keep stream-ordered scratch cached in the device pool between calls
   // (the default threshold hands it back to the driver at every sync).
   cudaMemPool_t pool;

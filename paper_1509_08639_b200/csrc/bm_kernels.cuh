@@ -98,6 +98,7 @@ struct FusedArgs {
   bm_record* rec;
   int32_t* rec_count;
   double* cost;
+  PairTables tabs;         // branch-free feature tables (device pointers)
   uint8_t* hits;           // per-doc dense coverage hit counts (hits_kernel output)
   const int64_t* hit_off;  // byte offset of each doc's hits (16-byte aligned)
 };
@@ -124,6 +125,7 @@ size_t score_smem_bytes();
 cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();
 cudaError_t ensure_quot_table();
+PairTables pair_tables();
 size_t ring_slice_bytes(int n, int m, int R);
 size_t hits_kernel_smem(int n, int m);
 cudaError_t launch_hits(const FusedArgs& a, size_t smem, cudaStream_t st);

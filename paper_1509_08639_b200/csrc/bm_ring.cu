@@ -78,6 +78,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // Ring of (1 - S) values: at least two mbarrier blocks of kGroup steps.
+// Same as mbar_wait but sleeps between polls: the DP warp idles on the
+// producers and must not steal their issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred P1;\n mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+  }
+}
+
 __host__ __device__ constexpr int ring_bytes(int R) {
   return (2 * kGroup * WARP * R * 8) > 16384 ? 2 * kGroup * WARP * R * 8 : 16384;
 }
@@ -134,23 +150,26 @@ struct __align__(16) SPack {
 // Features of one cell from staged sentences (same values, operation by
 // operation, as bm_device.cuh cell_features / margin / confidence_from_z).
 __device__ __forceinline__ double staged_score(const bm_sentences& S, const Model& M,
-                                               const uint64_t* exp_tab, const SPack a,
-                                               const SPack b, int hf, int hr) {
+                                               const uint64_t* exp_tab, const PairTables& tb,
+                                               const SPack a, const SPack b, int hf, int hr) {
+  // every count is < 256 here (routing: T <= 255 bounds P, |A|, |D| and hits)
   const int aT = a.tpad & 0xff, aP = (a.tpad >> 8) & 0xff, aA = (a.tpad >> 16) & 0xff,
             aD = a.tpad >> 24;
   const int bT = b.tpad & 0xff, bP = (b.tpad >> 8) & 0xff, bA = (b.tpad >> 16) & 0xff,
             bD = b.tpad >> 24;
   double f[7];
-  f[0] = ratio_pair(aT, bT);
-  f[1] = frac_pair(hf, aA);
-  f[2] = frac_pair(hr, bA);
+  f[0] = __ldg(tb.ratio2 + aT * kPairMax + bT);
+  f[1] = __ldg(tb.frac2 + hf * kPairMax + aA);
+  f[2] = __ldg(tb.frac2 + hr * kPairMax + bA);
   if ((aD | bD) == 0) {
     f[3] = 1.0;
+  } else if (aD == 0 || bD == 0) {
+    f[3] = 0.0;  // 0 / |D_s | D_t|
   } else {
-    const int inter = (aD && bD) ? sorted_intersection(S.dig_id + a.d0, aD, S.dig_id + b.d0, bD) : 0;
-    f[3] = frac_pair(inter, aD + bD - inter);
+    const int inter = sorted_intersection(S.dig_id + a.d0, aD, S.dig_id + b.d0, bD);
+    f[3] = frac_or_zero(inter, aD + bD - inter);
   }
-  f[4] = ratio_pair(aP, bP);
+  f[4] = __ldg(tb.ratio2 + aP * kPairMax + bP);
   f[5] = __dsub_rn(1.0, fabs(__dsub_rn(a.pos, b.pos)));
   f[6] = 1.0;
   return bmexp::confidence_from_z(margin(M, f), exp_tab);
@@ -166,7 +185,7 @@ __device__ __forceinline__ int step_slots(int s, int steps, int m, int nl, int R
 }
 
 template <int R>
-__global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kRingThreads, 5) mine_ring_kernel(FusedArgs a) {
   constexpr int K = ring_depth(R);  // ring depth in steps
   constexpr int NB = K / kGroup;    // mbarrier blocks in the ring
   constexpr int CPW = 16 / R;       // columns per direction word
@@ -240,7 +259,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
       double prev_recv = (double)i0 * p;
       uint32_t dword = 0;
       for (int b = 0; b < nblocks; ++b) {
-        mbar_wait(bar_full + (b % NB), (uint32_t)((b / NB) & 1));
+        mbar_wait_sleep(bar_full + (b % NB), (uint32_t)((b / NB) & 1));
         const int s_end = min(steps, (b + 1) * kGroup);
         for (int s = b * kGroup; s < s_end; ++s) {
           const int j = s - lane;
@@ -304,28 +323,33 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         if (b >= NB) mbar_wait(bar_empty + (b % NB), (uint32_t)(((b / NB) - 1) & 1));
         const int s_end = min(steps, (b + 1) * kGroup);
         // walk this thread's slots (stride kProducers over the concatenated
-        // valid slots of the block's steps) without re-searching each time
+        // valid slots of the block's steps); the step state (s, first valid
+        // lane L0, slot count) only changes when the walk crosses a step
         int s = b * kGroup, rem = ptid;
+        int L0 = max(0, s - (m - 1));
         int cnt = step_slots(s, steps, m, nl, R);
         while (s < s_end && rem >= cnt) {
           rem -= cnt;
-          cnt = step_slots(++s, steps, m, nl, R);
+          ++s;
+          L0 = max(0, s - (m - 1));
+          cnt = step_slots(s, steps, m, nl, R);
         }
         while (s < s_end) {
-          const int L = max(0, s - (m - 1)) + rem / R;
+          const int L = L0 + rem / R;
           const int r = rem % R;
           const int i = L * R + r;
           if (i < n) {
             const int j = s - L;
-            int hf, hr;
-            read_hits<true>(hits, i * m + j, hf, hr);
-            const double sv = staged_score(S, a.M, exp_tab, sp[i], sp[n + j], hf, hr);
-            ring[((size_t)(s % K) * WARP + L) * R + r] = __dsub_rn(1.0, sv);
+            const uint32_t hv = ((const uint16_t*)hits)[i * m + j];
+            const double sv = staged_score(S, a.M, exp_tab, a.tabs, sp[i], sp[n + j], hv & 0xff, hv >> 8);
+            ring[((s % K) * WARP + L) * R + r] = __dsub_rn(1.0, sv);
           }
           rem += kProducers;
-          while (s < s_end && rem >= cnt) {
+          while (rem >= cnt && s < s_end) {
             rem -= cnt;
-            cnt = step_slots(++s, steps, m, nl, R);
+            ++s;
+            L0 = max(0, s - (m - 1));
+            cnt = step_slots(s, steps, m, nl, R);
           }
         }
         mbar_arrive(bar_full + (b % NB));
@@ -366,9 +390,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) mine_ring_kernel(FusedArgs a)
         const int cell = dlist[K_path - 1 - f];
         ci = cell / m;
         cj = cell - ci * m;
-        int hf, hr;
-        read_hits<true>(hits, cell, hf, hr);
-        sv = staged_score(S, a.M, exp_tab, sp[ci], sp[n + cj], hf, hr);
+        const uint32_t hv = ((const uint16_t*)hits)[cell];
+        sv = staged_score(S, a.M, exp_tab, a.tabs, sp[ci], sp[n + cj], hv & 0xff, hv >> 8);
         keep = sv >= a.threshold;
       }
       const unsigned mask = __ballot_sync(FULL, keep);
