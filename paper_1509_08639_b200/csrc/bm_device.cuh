@@ -276,6 +276,120 @@ __device__ void join_direction(G g, const bm_sentences& S, const int32_t* off,
   }
 }
 
+// Sentence (local index) owning entry e: the largest k with off[k] <= e, over
+// the side's staged offsets off[0..nsent].
+__device__ __forceinline__ int owner_of(const int32_t* off, int nsent, int e) {
+  int lo = 0, hi = nsent - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= e)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// Entry-parallel form of join_direction: every loop runs over token entries
+// (coalesced loads, all lanes busy) instead of over sentences. offA / offB are
+// the two sides' tok_off slices staged in shared memory (na+1 / nb+1 ints).
+template <class G, class AddFn>
+__device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t* off,
+                                       const int32_t* cand, const int32_t* offA, int na,
+                                       const int32_t* offB, int b0, int nb, JoinSmem& js,
+                                       AddFn add) {
+  const int eA0 = offA[0], eA1 = offA[na];
+  const int eB0 = offB[0], eB1 = offB[nb];
+  for (int c0 = eB0; c0 < eB1; c0 += js.emax) {
+    const int c1 = min(eB1, c0 + js.emax);
+    for (int b = g.rank(); b < js.nbuckets; b += g.size()) js.bfill[b] = 0;
+    g.sync();
+    for (int e = c0 + g.rank(); e < c1; e += g.size())
+      atomicAdd(&js.bfill[bucket_of(__ldg(S.tok_id + e), js.bshift)], 1);
+    g.sync();
+    if (g.scanner()) {
+      int lane = threadIdx.x & (WARP - 1);
+      int per = (js.nbuckets + WARP - 1) / WARP;
+      int q0 = lane * per, q1 = min(js.nbuckets, q0 + per);
+      int sum = 0;
+      for (int b = q0; b < q1; ++b) sum += js.bfill[b];
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < WARP; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int run = incl - sum;
+      for (int b = q0; b < q1; ++b) {
+        int c = js.bfill[b];
+        js.bstart[b] = run;
+        js.bfill[b] = run;
+        run += c;
+      }
+      if (lane == WARP - 1) js.bstart[js.nbuckets] = incl;
+    }
+    g.sync();
+    for (int e = c0 + g.rank(); e < c1; e += g.size()) {
+      const int32_t id = __ldg(S.tok_id + e);
+      const int slot = atomicAdd(&js.bfill[bucket_of(id, js.bshift)], 1);
+      js.key[slot] = id;
+      js.owner[slot] = (uint16_t)owner_of(offB, nb, e);
+    }
+    g.sync();
+    for (int e = eA0 + g.rank(); e < eA1; e += g.size()) {
+      const int w = __ldg(S.tok_alpha + e);
+      if (w == 0) continue;
+      const int32_t id = __ldg(S.tok_id + e);
+      const int q0 = __ldg(off + id), q1 = __ldg(off + id + 1);
+      if (q0 == q1) continue;
+      const int la = owner_of(offA, na, e);
+      for (int q = q0; q < q1; ++q) {
+        const int32_t c = __ldg(cand + q);
+        const uint32_t bk = bucket_of(c, js.bshift);
+        for (int slot = js.bstart[bk]; slot < js.bstart[bk + 1]; ++slot) {
+          if (js.key[slot] != c) continue;
+          const int lb = js.owner[slot];
+          bool dup = false;
+          if (q > q0) {
+            const int u0 = __ldg(S.tok_off + b0 + lb);
+            const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
+            for (int qq = q0; qq < q && !dup; ++qq) dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
+          }
+          if (!dup) add(la, lb, w);
+        }
+      }
+    }
+    g.sync();
+  }
+}
+
+// Entry-parallel full join; offS / offT: staged tok_off slices (ns+1 / nt+1).
+template <bool kPacked16, class G>
+__device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& L, int s0,
+                                  int ns, int t0, int nt, const int32_t* offS,
+                                  const int32_t* offT, uint32_t* hits, JoinSmem& js) {
+  const int ncell = ns * nt;
+  const int nwords = kPacked16 ? (ncell + 1) / 2 : ncell;
+  for (int k = g.rank(); k < nwords; k += g.size()) hits[k] = 0u;
+  g.sync();
+  join_direction_entries(g, S, L.fwd_off, L.fwd_cand, offS, ns, offT, t0, nt, js,
+                         [&](int ls, int lt, int w) {
+                           int cell = ls * nt + lt;
+                           if (kPacked16)
+                             atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16));
+                           else
+                             atomicAdd(&hits[cell], (uint32_t)w);
+                         });
+  join_direction_entries(g, S, L.rev_off, L.rev_cand, offT, nt, offS, s0, ns, js,
+                         [&](int lt, int ls, int w) {
+                           int cell = ls * nt + lt;
+                           if (kPacked16)
+                             atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16 + 8));
+                           else
+                             atomicAdd(&hits[cell], (uint32_t)w << 16);
+                         });
+}
+
 // Full join for a tile. Hits are packed per cell into `hits` words:
 //   kPacked16: 16-bit cells, hf in bits 0-7, hr in bits 8-15 (counts <= 255)
 //   otherwise: 32-bit cells, hf in bits 0-15, hr in bits 16-31

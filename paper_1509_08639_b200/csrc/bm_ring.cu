@@ -115,7 +115,9 @@ size_t ring_slice_bytes(int n, int m, int R) {
   return kFixedBytes + ring_bytes(R) + ring_var_bytes(n, m, R);
 }
 
-size_t hits_kernel_smem(int n, int m) { return align16(join_smem_bytes()) + hits_bytes(n, m); }
+size_t hits_kernel_smem(int n, int m) {
+  return align16(join_smem_bytes()) + hits_bytes(n, m) + align16((size_t)(n + m + 2) * 4);
+}
 
 // ---------------------------------------------------------------------------
 // hits_kernel: dictionary join of one document -> HBM scratch
@@ -131,7 +133,17 @@ __global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, b
   const int n = D.n[doc], m = D.m[doc];
   JoinSmem js = carve_join(smem);
   uint32_t* hits = (uint32_t*)(smem + align16(join_smem_bytes()));
-  tile_join<true>(CtaGroup(), S, L, D.src0[doc], n, D.tgt0[doc], m, hits, js);
+  int32_t* offS = (int32_t*)((uint8_t*)hits + hits_bytes(n, m));
+  int32_t* offT = offS + n + 1;
+  const int s0 = D.src0[doc], t0 = D.tgt0[doc];
+  for (int k = threadIdx.x; k <= n + m + 1; k += blockDim.x) {
+    if (k <= n)
+      offS[k] = __ldg(S.tok_off + s0 + k);
+    else
+      offT[k - n - 1] = __ldg(S.tok_off + t0 + (k - n - 1));
+  }
+  __syncthreads();
+  tile_join_entries<true>(CtaGroup(), S, L, s0, n, t0, m, offS, offT, hits, js);
   const int words4 = (int)(hits_bytes(n, m) / 16);
   const uint4* src = (const uint4*)hits;
   uint4* dst = (uint4*)(hits_out + hit_off[doc]);
