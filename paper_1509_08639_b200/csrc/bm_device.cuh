@@ -297,7 +297,7 @@ template <class G, class AddFn>
 __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t* off,
                                        const int32_t* cand, const int32_t* offA, int na,
                                        const int32_t* offB, int b0, int nb, JoinSmem& js,
-                                       AddFn add) {
+                                       uint16_t* chunk_owner, AddFn add) {
   const int eA0 = offA[0], eA1 = offA[na];
   const int eB0 = offB[0], eB1 = offB[nb];
   for (int c0 = eB0; c0 < eB1; c0 += js.emax) {
@@ -306,6 +306,11 @@ __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t
     g.sync();
     for (int e = c0 + g.rank(); e < c1; e += g.size())
       atomicAdd(&js.bfill[bucket_of(__ldg(S.tok_id + e), js.bshift)], 1);
+    // owner sentence of every entry of the chunk (stores only)
+    for (int k = g.rank(); k < nb; k += g.size()) {
+      const int e0 = max(c0, offB[k]), e1 = min(c1, offB[k + 1]);
+      for (int e = e0; e < e1; ++e) chunk_owner[e - c0] = (uint16_t)k;
+    }
     g.sync();
     if (g.scanner()) {
       int lane = threadIdx.x & (WARP - 1);
@@ -333,7 +338,7 @@ __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t
       const int32_t id = __ldg(S.tok_id + e);
       const int slot = atomicAdd(&js.bfill[bucket_of(id, js.bshift)], 1);
       js.key[slot] = id;
-      js.owner[slot] = (uint16_t)owner_of(offB, nb, e);
+      js.owner[slot] = chunk_owner[e - c0];
     }
     g.sync();
     // probe, 4 entries per thread per round so their dependent lexicon loads
@@ -393,12 +398,13 @@ __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t
 template <bool kPacked16, class G>
 __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& L, int s0,
                                   int ns, int t0, int nt, const int32_t* offS,
-                                  const int32_t* offT, uint32_t* hits, JoinSmem& js) {
+                                  const int32_t* offT, uint32_t* hits, JoinSmem& js,
+                                  uint16_t* chunk_owner) {
   const int ncell = ns * nt;
   const int nwords = kPacked16 ? (ncell + 1) / 2 : ncell;
   for (int k = g.rank(); k < nwords; k += g.size()) hits[k] = 0u;
   g.sync();
-  join_direction_entries(g, S, L.fwd_off, L.fwd_cand, offS, ns, offT, t0, nt, js,
+  join_direction_entries(g, S, L.fwd_off, L.fwd_cand, offS, ns, offT, t0, nt, js, chunk_owner,
                          [&](int ls, int lt, int w) {
                            int cell = ls * nt + lt;
                            if (kPacked16)
@@ -406,7 +412,7 @@ __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& 
                            else
                              atomicAdd(&hits[cell], (uint32_t)w);
                          });
-  join_direction_entries(g, S, L.rev_off, L.rev_cand, offT, nt, offS, s0, ns, js,
+  join_direction_entries(g, S, L.rev_off, L.rev_cand, offT, nt, offS, s0, ns, js, chunk_owner,
                          [&](int lt, int ls, int w) {
                            int cell = ls * nt + lt;
                            if (kPacked16)

@@ -116,7 +116,8 @@ size_t ring_slice_bytes(int n, int m, int R) {
 }
 
 size_t hits_kernel_smem(int n, int m) {
-  return align16(join_smem_bytes()) + hits_bytes(n, m) + align16((size_t)(n + m + 2) * 4);
+  return align16(join_smem_bytes()) + hits_bytes(n, m) + align16((size_t)(n + m + 2) * 4) +
+         (size_t)kJoinEmax * 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, b
   uint32_t* hits = (uint32_t*)(smem + align16(join_smem_bytes()));
   int32_t* offS = (int32_t*)((uint8_t*)hits + hits_bytes(n, m));
   int32_t* offT = offS + n + 1;
+  uint16_t* chunk_owner = (uint16_t*)((uint8_t*)offS + align16((size_t)(n + m + 2) * 4));
   const int s0 = D.src0[doc], t0 = D.tgt0[doc];
   for (int k = threadIdx.x; k <= n + m + 1; k += blockDim.x) {
     if (k <= n)
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, b
       offT[k - n - 1] = __ldg(S.tok_off + t0 + (k - n - 1));
   }
   __syncthreads();
-  tile_join_entries<true>(CtaGroup(), S, L, s0, n, t0, m, offS, offT, hits, js);
+  tile_join_entries<true>(CtaGroup(), S, L, s0, n, t0, m, offS, offT, hits, js, chunk_owner);
   const int words4 = (int)(hits_bytes(n, m) / 16);
   const uint4* src = (const uint4*)hits;
   uint4* dst = (uint4*)(hits_out + hit_off[doc]);
