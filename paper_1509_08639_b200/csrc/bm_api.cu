@@ -406,6 +406,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     uint8_t* hits = nullptr;
     int64_t* dho = nullptr;
     BM_CK(sc.alloc(&hits, (size_t)hit_total), "alloc hits");
+    BM_CK(cudaMemsetAsync(hits, 0, (size_t)hit_total, st), "memset hits");
     tr.mark("alloc hits");
     BM_CK(sc.upload(&dho, hit_off), "upload");
     tr.mark("upload hit_off");

@@ -341,51 +341,28 @@ __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t
       js.owner[slot] = chunk_owner[e - c0];
     }
     g.sync();
-    // probe, 4 entries per thread per round so their dependent lexicon loads
-    // (entry -> CSR range -> first candidate) overlap
-    constexpr int kB = 4;
-    const int stride = g.size();
-    for (int base = eA0 + g.rank(); base < eA1; base += kB * stride) {
-      int w[kB], q0[kB], q1[kB];
-      int32_t c0[kB];
-#pragma unroll
-      for (int k = 0; k < kB; ++k) {
-        const int e = base + k * stride;
-        w[k] = e < eA1 ? __ldg(S.tok_alpha + e) : 0;
-      }
-      int32_t id[kB];
-#pragma unroll
-      for (int k = 0; k < kB; ++k) id[k] = w[k] ? __ldg(S.tok_id + base + k * stride) : 0;
-#pragma unroll
-      for (int k = 0; k < kB; ++k) {
-        q0[k] = w[k] ? __ldg(off + id[k]) : 0;
-        q1[k] = w[k] ? __ldg(off + id[k] + 1) : 0;
-      }
-#pragma unroll
-      for (int k = 0; k < kB; ++k) c0[k] = q1[k] > q0[k] ? __ldg(cand + q0[k]) : -1;
-#pragma unroll
-      for (int k = 0; k < kB; ++k) {
-        if (c0[k] < 0) continue;
-        const int e = base + k * stride;
-        int la = -1;
-        for (int q = q0[k]; q < q1[k]; ++q) {
-          const int32_t c = q == q0[k] ? c0[k] : __ldg(cand + q);
-          const uint32_t bk = bucket_of(c, js.bshift);
-          for (int slot = js.bstart[bk]; slot < js.bstart[bk + 1]; ++slot) {
-            if (js.key[slot] != c) continue;
-            const int lb = js.owner[slot];
-            // an entry hits a sentence once however many candidates it holds
-            bool dup = false;
-            if (q > q0[k]) {
-              const int u0 = __ldg(S.tok_off + b0 + lb);
-              const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
-              for (int qq = q0[k]; qq < q && !dup; ++qq)
-                dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
-            }
-            if (!dup) {
-              if (la < 0) la = owner_of(offA, na, e);
-              add(la, lb, w[k]);
-            }
+    for (int e = eA0 + g.rank(); e < eA1; e += g.size()) {
+      const int w = __ldg(S.tok_alpha + e);
+      if (w == 0) continue;
+      const int32_t id = __ldg(S.tok_id + e);
+      const int q0 = __ldg(off + id), q1 = __ldg(off + id + 1);
+      int la = -1;
+      for (int q = q0; q < q1; ++q) {
+        const int32_t c = __ldg(cand + q);
+        const uint32_t bk = bucket_of(c, js.bshift);
+        for (int slot = js.bstart[bk]; slot < js.bstart[bk + 1]; ++slot) {
+          if (js.key[slot] != c) continue;
+          const int lb = js.owner[slot];
+          // an entry hits a sentence once however many candidates it holds
+          bool dup = false;
+          if (q > q0) {
+            const int u0 = __ldg(S.tok_off + b0 + lb);
+            const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
+            for (int qq = q0; qq < q && !dup; ++qq) dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
+          }
+          if (!dup) {
+            if (la < 0) la = owner_of(offA, na, e);
+            add(la, lb, w);
           }
         }
       }
@@ -399,11 +376,13 @@ template <bool kPacked16, class G>
 __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& L, int s0,
                                   int ns, int t0, int nt, const int32_t* offS,
                                   const int32_t* offT, uint32_t* hits, JoinSmem& js,
-                                  uint16_t* chunk_owner) {
+                                  uint16_t* chunk_owner, bool zero_hits = true) {
   const int ncell = ns * nt;
   const int nwords = kPacked16 ? (ncell + 1) / 2 : ncell;
-  for (int k = g.rank(); k < nwords; k += g.size()) hits[k] = 0u;
-  g.sync();
+  if (zero_hits) {
+    for (int k = g.rank(); k < nwords; k += g.size()) hits[k] = 0u;
+    g.sync();
+  }
   join_direction_entries(g, S, L.fwd_off, L.fwd_cand, offS, ns, offT, t0, nt, js, chunk_owner,
                          [&](int ls, int lt, int w) {
                            int cell = ls * nt + lt;

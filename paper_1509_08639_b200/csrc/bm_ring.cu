@@ -30,7 +30,7 @@ constexpr int kRingThreads = 128;
 constexpr int kProducers = kRingThreads - WARP;
 constexpr int kGroup = 8;  // wavefront steps per mbarrier block
 constexpr int kFixedBytes = kExpTableWords * 8 + 256;
-constexpr int kHitsThreads = 128;
+constexpr int kHitsThreads = 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -116,25 +116,25 @@ size_t ring_slice_bytes(int n, int m, int R) {
 }
 
 size_t hits_kernel_smem(int n, int m) {
-  return align16(join_smem_bytes()) + hits_bytes(n, m) + align16((size_t)(n + m + 2) * 4) +
-         (size_t)kJoinEmax * 2;
+  return align16(join_smem_bytes()) + align16((size_t)(n + m + 2) * 4) + (size_t)kJoinEmax * 2;
 }
 
 // ---------------------------------------------------------------------------
 // hits_kernel: dictionary join of one document -> HBM scratch
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, bm_docs D,
+__global__ void __launch_bounds__(kHitsThreads) hits_kernel(bm_sentences S, bm_docs D,
                                                             bm_lexicon L, const int32_t* list,
                                                             int n_list, const int64_t* hit_off,
                                                             uint8_t* hits_out) {
+  // hit counters accumulate straight into the (pre-zeroed) HBM scratch with
+  // L2 atomics: no per-document smem matrix, so many documents fit per SM
   extern __shared__ __align__(16) uint8_t smem[];
   const int item = blockIdx.x;
   if (item >= n_list) return;
   const int doc = list[item];
   const int n = D.n[doc], m = D.m[doc];
   JoinSmem js = carve_join(smem);
-  uint32_t* hits = (uint32_t*)(smem + align16(join_smem_bytes()));
-  int32_t* offS = (int32_t*)((uint8_t*)hits + hits_bytes(n, m));
+  int32_t* offS = (int32_t*)(smem + align16(join_smem_bytes()));
   int32_t* offT = offS + n + 1;
   uint16_t* chunk_owner = (uint16_t*)((uint8_t*)offS + align16((size_t)(n + m + 2) * 4));
   const int s0 = D.src0[doc], t0 = D.tgt0[doc];
@@ -145,11 +145,9 @@ __global__ void __launch_bounds__(kHitsThreads, 4) hits_kernel(bm_sentences S, b
       offT[k - n - 1] = __ldg(S.tok_off + t0 + (k - n - 1));
   }
   __syncthreads();
-  tile_join_entries<true>(CtaGroup(), S, L, s0, n, t0, m, offS, offT, hits, js, chunk_owner);
-  const int words4 = (int)(hits_bytes(n, m) / 16);
-  const uint4* src = (const uint4*)hits;
-  uint4* dst = (uint4*)(hits_out + hit_off[doc]);
-  for (int k = threadIdx.x; k < words4; k += blockDim.x) dst[k] = src[k];
+  uint32_t* hits = (uint32_t*)(hits_out + hit_off[doc]);
+  tile_join_entries<true>(CtaGroup(), S, L, s0, n, t0, m, offS, offT, hits, js, chunk_owner,
+                          /*zero_hits=*/false);
 }
 
 // One sentence as the fused kernel stages it in shared memory (16 bytes):
@@ -443,6 +441,7 @@ cudaError_t launch_hits(const FusedArgs& a, size_t smem, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   hits_kernel<<<a.n_list, kHitsThreads, smem, st>>>(a.S, a.D, a.L, a.list, a.n_list, a.hit_off,
                                                      a.hits);
+  (void)0;
   e = cudaGetLastError();
   if (e == cudaSuccess) g_launches += 1;
   return e;
