@@ -208,6 +208,29 @@ int bm_mine_host(const bm_sentences* sent_h, const bm_docs* docs_h, const bm_lex
                  int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream);
 
 /*
+ * Compact host wire format for bm_mine_host_wire: same content as
+ * bm_sentences, narrower types (valid when the id space has <= 65536 ids and
+ * every count is <= 255). Halves the host->device bytes of a batch.
+ */
+typedef struct bm_wire {
+  int32_t n_sent;
+  const uint8_t* n_tok;
+  const uint8_t* n_punct;
+  const uint8_t* n_alpha;
+  const int32_t* tok_off;   /* [n_sent + 1] */
+  const uint16_t* tok_id;
+  const uint8_t* tok_alpha;
+  const int32_t* dig_off;   /* [n_sent + 1] */
+  const uint16_t* dig_id;
+} bm_wire;
+
+/* bm_mine_host with the compact wire format (host pointers). */
+int bm_mine_host_wire(const bm_wire* wire_h, const bm_docs* docs_h, const bm_lexicon* lex_h,
+                      const bm_model* model, double threshold, double penalty,
+                      bm_record* rec_out, int64_t rec_cap, int64_t* n_rec, double* cost_out,
+                      void* stream);
+
+/*
  * K5 -- tune (tuner.py:87-154): for every penalty p_k and threshold t_l,
  * pred[k*n_thr + l] += #diagonal moves with S >= t_l over all docs, and
  * hit[k*n_thr + l] += those whose (i, j) is in the doc's gold set.

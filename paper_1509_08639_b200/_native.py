@@ -31,6 +31,15 @@ class Sentences(C.Structure):
     ]
 
 
+class Wire(C.Structure):
+    _fields_ = [
+        ("n_sent", C.c_int32),
+        ("n_tok", _p), ("n_punct", _p), ("n_alpha", _p),
+        ("tok_off", _p), ("tok_id", _p), ("tok_alpha", _p),
+        ("dig_off", _p), ("dig_id", _p),
+    ]
+
+
 class Docs(C.Structure):
     _fields_ = [("n_docs", C.c_int32), ("src0", _p), ("n", _p), ("tgt0", _p), ("m", _p)]
 
@@ -73,6 +82,9 @@ _SIGS = {
     "bm_mine_host": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), C.POINTER(LexiconC),
                                C.POINTER(ModelC), C.c_double, C.c_double, _p, C.c_int64,
                                C.POINTER(C.c_int64), _p, _p]),
+    "bm_mine_host_wire": (C.c_int, [C.POINTER(Wire), C.POINTER(Docs), C.POINTER(LexiconC),
+                                    C.POINTER(ModelC), C.c_double, C.c_double, _p, C.c_int64,
+                                    C.POINTER(C.c_int64), _p, _p]),
     "bm_tune": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, C.POINTER(LexiconC),
                           C.POINTER(ModelC), _p, C.c_int32, _p, C.c_int32, _p, _p, _p, _p, _p]),
     "bm_compact": (C.c_int, [_p, _p, _p, C.c_int32, _p, _p, _p]),

@@ -499,27 +499,40 @@ cudaStream_t copy_stream() {
   return s;
 }
 
-int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh,
-                 const bm_model* model, double threshold, double penalty, bm_record* rec_out,
-                 int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
+// Host source of a streamed batch: either the plain bm_sentences arrays or the
+// compact wire format (narrow types, widened on the device per chunk).
+struct HostSource {
+  int32_t n_sent;
+  const int32_t* tok_off;  // host, [n_sent + 1]
+  const int32_t* dig_off;  // host, [n_sent + 1]
+  const bm_sentences* full;
+  const bm_wire* wire;
+  int32_t tok_max(int k) const { return full ? full->n_tok[k] : (int32_t)wire->n_tok[k]; }
+};
+
+int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* lh,
+                   const bm_model* model, double threshold, double penalty, bm_record* rec_out,
+                   int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   HostTrace tr("bm_mine_host");
   BM_CK(ensure_quot_table(), "device init");
   cudaStream_t cs = copy_stream();
-  const int ns = sh->n_sent, nd = dh->n_docs;
-  const int64_t ne = ns ? sh->tok_off[ns] : 0;
-  const int64_t ndig = ns ? sh->dig_off[ns] : 0;
+  const int ns = src.n_sent, nd = dh->n_docs;
+  const int64_t ne = ns ? src.tok_off[ns] : 0;
+  const int64_t ndig = ns ? src.dig_off[ns] : 0;
   const int nid = lh->n_ids;
   // routing input: per-doc max token count; one vectorisable pass decides
   // whether any document can exceed the fused kernel's 8-bit counters at all
   int32_t gmax = 0;
-  for (int k = 0; k < ns; ++k) gmax = std::max(gmax, sh->n_tok[k]);
+  if (src.full) {
+    for (int k = 0; k < ns; ++k) gmax = std::max(gmax, src.full->n_tok[k]);
+  }
   std::vector<int32_t> amax(nd, 0);
   if (gmax > 255) {
     for (int d = 0; d < nd; ++d) {
       int v = 0;
-      for (int k = 0; k < dh->n[d]; ++k) v = std::max(v, sh->n_tok[dh->src0[d] + k]);
-      for (int k = 0; k < dh->m[d]; ++k) v = std::max(v, sh->n_tok[dh->tgt0[d] + k]);
+      for (int k = 0; k < dh->n[d]; ++k) v = std::max(v, src.tok_max(dh->src0[d] + k));
+      for (int k = 0; k < dh->m[d]; ++k) v = std::max(v, src.tok_max(dh->tgt0[d] + k));
       amax[d] = v;
     }
   }
@@ -551,6 +564,17 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
   sd.tok_alpha = a7;
   sd.dig_off = a5;
   sd.dig_id = a6;
+  // device staging of the narrow wire arrays
+  uint8_t *w_t = nullptr, *w_p = nullptr, *w_a = nullptr, *w_al = nullptr;
+  uint16_t *w_id = nullptr, *w_dg = nullptr;
+  if (src.wire) {
+    BM_CK(sc.alloc(&w_t, ns), "alloc");
+    BM_CK(sc.alloc(&w_p, ns), "alloc");
+    BM_CK(sc.alloc(&w_a, ns), "alloc");
+    BM_CK(sc.alloc(&w_id, ne), "alloc");
+    BM_CK(sc.alloc(&w_al, ne), "alloc");
+    BM_CK(sc.alloc(&w_dg, ndig), "alloc");
+  }
   bm_docs dd;
   dd.n_docs = nd;
   int32_t *b0, *b1, *b2, *b3;
@@ -586,8 +610,8 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
   BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
   BM_CK(cudaEventRecord(ready, st), "event");
   BM_CK(cudaStreamWaitEvent(cs, ready, 0), "event");
-  auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
-    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs) : cudaSuccess;
+  auto h2d = [&](void* dst, const void* from, size_t bytes) -> cudaError_t {
+    return bytes ? cudaMemcpyAsync(dst, from, bytes, cudaMemcpyHostToDevice, cs) : cudaSuccess;
   };
   BM_CK(h2d(c0, lh->fwd_off, (nid + 1) * 4), "h2d");
   BM_CK(h2d(c1, lh->fwd_cand, nf * 4), "h2d");
@@ -621,17 +645,31 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
       ++d1;
     }
     if (hi > lo) {
-      const int64_t e0 = sh->tok_off[lo], e1 = sh->tok_off[hi];
-      const int64_t g0 = sh->dig_off[lo], g1 = sh->dig_off[hi];
+      const int64_t e0 = src.tok_off[lo], e1 = src.tok_off[hi];
+      const int64_t g0 = src.dig_off[lo], g1 = src.dig_off[hi];
       const size_t cntS = (size_t)(hi - lo);
-      BM_CK(h2d(a0 + lo, sh->n_tok + lo, cntS * 4), "h2d");
-      BM_CK(h2d(a1 + lo, sh->n_punct + lo, cntS * 4), "h2d");
-      BM_CK(h2d(a2 + lo, sh->n_alpha + lo, cntS * 4), "h2d");
-      BM_CK(h2d(a3 + lo, sh->tok_off + lo, (cntS + 1) * 4), "h2d");
-      BM_CK(h2d(a5 + lo, sh->dig_off + lo, (cntS + 1) * 4), "h2d");
-      BM_CK(h2d(a4 + e0, sh->tok_id + e0, (size_t)(e1 - e0) * 4), "h2d");
-      BM_CK(h2d(a7 + e0, sh->tok_alpha + e0, (size_t)(e1 - e0) * 2), "h2d");
-      BM_CK(h2d(a6 + g0, sh->dig_id + g0, (size_t)(g1 - g0) * 4), "h2d");
+      BM_CK(h2d(a3 + lo, src.tok_off + lo, (cntS + 1) * 4), "h2d");
+      BM_CK(h2d(a5 + lo, src.dig_off + lo, (cntS + 1) * 4), "h2d");
+      if (src.full) {
+        const bm_sentences* sh = src.full;
+        BM_CK(h2d(a0 + lo, sh->n_tok + lo, cntS * 4), "h2d");
+        BM_CK(h2d(a1 + lo, sh->n_punct + lo, cntS * 4), "h2d");
+        BM_CK(h2d(a2 + lo, sh->n_alpha + lo, cntS * 4), "h2d");
+        BM_CK(h2d(a4 + e0, sh->tok_id + e0, (size_t)(e1 - e0) * 4), "h2d");
+        BM_CK(h2d(a7 + e0, sh->tok_alpha + e0, (size_t)(e1 - e0) * 2), "h2d");
+        BM_CK(h2d(a6 + g0, sh->dig_id + g0, (size_t)(g1 - g0) * 4), "h2d");
+      } else {
+        const bm_wire* w = src.wire;
+        BM_CK(h2d(w_t + lo, w->n_tok + lo, cntS), "h2d");
+        BM_CK(h2d(w_p + lo, w->n_punct + lo, cntS), "h2d");
+        BM_CK(h2d(w_a + lo, w->n_alpha + lo, cntS), "h2d");
+        BM_CK(h2d(w_id + e0, w->tok_id + e0, (size_t)(e1 - e0) * 2), "h2d");
+        BM_CK(h2d(w_al + e0, w->tok_alpha + e0, (size_t)(e1 - e0)), "h2d");
+        BM_CK(h2d(w_dg + g0, w->dig_id + g0, (size_t)(g1 - g0) * 2), "h2d");
+        BM_CK(launch_unpack_wire(w_t, w_p, w_a, w_id, w_al, w_dg, lo, hi, e0, e1, g0, g1, a0, a1,
+                                 a2, a4, a7, a6, cs),
+              "unpack_wire_kernel");
+      }
     }
     cudaEvent_t ev;
     BM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
@@ -665,6 +703,22 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
   cudaEventDestroy(ready);
   *n_rec = tot;
   return BM_OK;
+}
+
+int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh,
+                 const bm_model* model, double threshold, double penalty, bm_record* rec_out,
+                 int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
+  HostSource src{sh->n_sent, sh->tok_off, sh->dig_off, sh, nullptr};
+  return mine_host_impl(src, dh, lh, model, threshold, penalty, rec_out, rec_cap, n_rec, cost_out,
+                        stream);
+}
+
+int bm_mine_host_wire(const bm_wire* wh, const bm_docs* dh, const bm_lexicon* lh,
+                      const bm_model* model, double threshold, double penalty, bm_record* rec_out,
+                      int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
+  HostSource src{wh->n_sent, wh->tok_off, wh->dig_off, nullptr, wh};
+  return mine_host_impl(src, dh, lh, model, threshold, penalty, rec_out, rec_cap, n_rec, cost_out,
+                        stream);
 }
 
 int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,

@@ -677,4 +677,38 @@ cudaError_t launch_fp64_probe(double* out, int iters, int blocks, cudaStream_t s
 }
 
 long long launches() { return g_launches.load(); }
+
+// Widen a streamed chunk of the compact wire format into the device arrays
+// of bm_sentences (sentences [lo, hi), entries [e0, e1), digits [g0, g1)).
+__global__ void unpack_wire_kernel(const uint8_t* __restrict__ t8, const uint8_t* __restrict__ p8,
+                                   const uint8_t* __restrict__ a8, const uint16_t* __restrict__ id16,
+                                   const uint8_t* __restrict__ al8, const uint16_t* __restrict__ dg16,
+                                   int lo, int hi, int64_t e0, int64_t e1, int64_t g0, int64_t g1,
+                                   int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha,
+                                   int32_t* tok_id, uint16_t* tok_alpha, int32_t* dig_id) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t s = lo + t; s < hi; s += stride) {
+    n_tok[s] = t8[s];
+    n_punct[s] = p8[s];
+    n_alpha[s] = a8[s];
+  }
+  for (int64_t e = e0 + t; e < e1; e += stride) {
+    tok_id[e] = id16[e];
+    tok_alpha[e] = al8[e];
+  }
+  for (int64_t g = g0 + t; g < g1; g += stride) dig_id[g] = dg16[g];
+}
+
+cudaError_t launch_unpack_wire(const uint8_t* t8, const uint8_t* p8, const uint8_t* a8,
+                               const uint16_t* id16, const uint8_t* al8, const uint16_t* dg16,
+                               int lo, int hi, int64_t e0, int64_t e1, int64_t g0, int64_t g1,
+                               int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha, int32_t* tok_id,
+                               uint16_t* tok_alpha, int32_t* dig_id, cudaStream_t st) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  unpack_wire_kernel<<<sms * 8, 256, 0, st>>>(t8, p8, a8, id16, al8, dg16, lo, hi, e0, e1, g0, g1,
+                                              n_tok, n_punct, n_alpha, tok_id, tok_alpha, dig_id);
+  return counted(cudaGetLastError());
+}
 }  // namespace bm

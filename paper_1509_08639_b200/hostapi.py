@@ -31,13 +31,38 @@ def _pinned(a: np.ndarray) -> tuple[object, np.ndarray]:
     return t, view
 
 
-class PinnedBatch:
-    """Packed arrays copied once into page-locked host memory + C structs."""
+def wire_ok(corpus: PackedCorpus, plex: PackedLexicon) -> bool:
+    """The compact wire format holds this batch (16-bit ids, 8-bit counts)."""
+    return (plex.n_ids <= 65536 and corpus.n_sent > 0
+            and int(corpus.n_tok.max(initial=0)) <= 255
+            and int(corpus.tok_alpha.max(initial=0)) <= 255)
 
-    def __init__(self, corpus: PackedCorpus, plex: PackedLexicon, pin: bool = True):
+
+def to_wire(corpus: PackedCorpus) -> dict[str, np.ndarray]:
+    return {
+        "n_tok": corpus.n_tok.astype(np.uint8), "n_punct": corpus.n_punct.astype(np.uint8),
+        "n_alpha": corpus.n_alpha.astype(np.uint8), "tok_off": corpus.tok_off,
+        "tok_id": corpus.tok_id.astype(np.uint16), "tok_alpha": corpus.tok_alpha.astype(np.uint8),
+        "dig_off": corpus.dig_off, "dig_id": corpus.dig_id.astype(np.uint16),
+    }
+
+
+class PinnedBatch:
+    """Packed arrays copied once into page-locked host memory + C structs.
+
+    wire=True stages the compact wire format (bm_mine_host_wire) when the
+    batch fits it, halving the per-call host->device bytes.
+    """
+
+    def __init__(self, corpus: PackedCorpus, plex: PackedLexicon, pin: bool = True,
+                 wire: bool = True):
         self.keep = []
+        self.wire = bool(wire and wire_ok(corpus, plex))
         arrs = {}
-        for name in _SENT + _DOCS:
+        src = to_wire(corpus) if self.wire else {k: getattr(corpus, k) for k in _SENT}
+        for name in _SENT:
+            arrs[name] = src[name]
+        for name in _DOCS:
             arrs[name] = getattr(corpus, name)
         for name in _LEX:
             arrs[name] = getattr(plex, name)
@@ -52,7 +77,8 @@ class PinnedBatch:
             self.keep.append(view)
             self.h2d_bytes += view.nbytes
         self.arrs = arrs
-        self.sent = N.Sentences(corpus.n_sent, *[arrs[k].ctypes.data for k in _SENT])
+        cls = N.Wire if self.wire else N.Sentences
+        self.sent = cls(corpus.n_sent, *[arrs[k].ctypes.data for k in _SENT])
         self.docs = N.Docs(corpus.n_docs, *[arrs[k].ctypes.data for k in _DOCS])
         self.lex = N.LexiconC(plex.n_ids, *[arrs[k].ctypes.data for k in _LEX])
         n, m = arrs["n"], arrs["m"]
@@ -70,16 +96,17 @@ def mine_pinned(pb: PinnedBatch, model, threshold: float, penalty: float, stream
     """One bm_mine_host call; returns (records view, n_records, d2h bytes)."""
     lib = N.lib()
     n_rec = C.c_int64(0)
-    N.check(lib.bm_mine_host(C.byref(pb.sent), C.byref(pb.docs), C.byref(pb.lex),
-                             C.byref(N.model_struct(model)), float(threshold), float(penalty),
-                             pb.rec.ctypes.data, pb.rec_cap, C.byref(n_rec), pb.cost.ctypes.data,
-                             stream))
+    fn = lib.bm_mine_host_wire if pb.wire else lib.bm_mine_host
+    N.check(fn(C.byref(pb.sent), C.byref(pb.docs), C.byref(pb.lex),
+               C.byref(N.model_struct(model)), float(threshold), float(penalty),
+               pb.rec.ctypes.data, pb.rec_cap, C.byref(n_rec), pb.cost.ctypes.data, stream))
     k = n_rec.value
     d2h = k * 24 + pb.n_docs * 8 + 8
     return pb.rec[:k], k, d2h
 
 
-def mine_host(corpus: PackedCorpus, plex: PackedLexicon, model, threshold: float, penalty: float):
-    pb = PinnedBatch(corpus, plex, pin=False)
+def mine_host(corpus: PackedCorpus, plex: PackedLexicon, model, threshold: float, penalty: float,
+              wire: bool = False):
+    pb = PinnedBatch(corpus, plex, pin=False, wire=wire)
     recs, k, _ = mine_pinned(pb, model, threshold, penalty)
     return recs.copy(), pb.cost[: pb.n_docs].copy()

@@ -293,15 +293,17 @@ def test_synth_text_round_trip_same_records():
     assert a.tobytes() == b.tobytes()
 
 
-def test_mine_host_entry_point_matches_device_path(oracle_mod):
-    """bm_mine_host (host buffers in, records out) == oracle."""
+@pytest.mark.parametrize("wire", [False, True])
+def test_mine_host_entry_point_matches_device_path(oracle_mod, wire):
+    """bm_mine_host / bm_mine_host_wire (host buffers in, records out) == oracle."""
     from paper_1509_08639_b200 import hostapi, synth
 
-    sc = synth.make_corpus(*synth.c2_shape(64), seed=11)
+    sc = synth.make_corpus(*synth.c2_shape(3000), seed=11)  # several streamed chunks
     model = bm.load_model(golden("model5k_fwd.json"))
     plex = sc.world.packed_lexicon()
-    recs, cost = hostapi.mine_host(sc.packed, plex, model, 0.5, 0.2)
-    want, wcost = oracle_mod.mine(oracle_mod.HostBatch(sc.packed, plex), model, 0.5, 0.2, threads=8)
+    assert hostapi.wire_ok(sc.packed, plex)
+    recs, cost = hostapi.mine_host(sc.packed, plex, model, 0.5, 0.2, wire=wire)
+    want, wcost = oracle_mod.mine(oracle_mod.HostBatch(sc.packed, plex), model, 0.5, 0.2, threads=16)
     assert recs.tobytes() == want.tobytes()
     assert np.array_equal(bits(cost), bits(wcost))
 
