@@ -84,6 +84,12 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ double ld_acquire_f64(const double* p) {
+  double v;
+  asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -225,17 +231,40 @@ cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, doub
 // owns one band; lane L owns rows 4L..4L+3 and runs one column behind lane
 // L-1, so the value a lane needs from the row above arrives by one 64-bit
 // shuffle of the previous step (the anti-diagonal dependency). The 4 rows of a
-// lane are a short in-register chain. Bands are chained through a per-band
-// boundary row in global memory, published every kPublish columns with
-// release/acquire flags; warps are persistent and take (doc, band) items in
-// increasing order from an atomic ticket, so waits always target a band that
-// is resident or finished (no deadlock).
-// S is read with 16-byte loads, one 4-column group ahead.
+// lane are a short in-register chain.
+//  * S: every lane streams its own 4 rows with cp.async (16-byte LDGSTS) into
+//    a private slice of a shared-memory ring kNwDepth groups of 4 columns deep,
+//    so HBM latency is hidden ~32 columns ahead of use.
+//  * Bands hand their bottom row to the band below through global memory in
+//    32-column chunks: the producer lane stores values as it goes and releases
+//    a progress flag per chunk; the consumer warp acquires the flag once per
+//    chunk, loads the chunk with one coalesced load and hands values to lane 0
+//    by shuffle.
+// Warps are persistent and take (doc, band) items in increasing order from an
+// atomic ticket, so a wait always targets a band that is resident or finished.
 // ---------------------------------------------------------------------------
+constexpr int kNwDepth = 8;                                // groups in flight per lane
+constexpr int kNwSmem = kNwDepth * WARP * kBandR * 4 * 8;  // 32 KB per warp
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_depth() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kNwDepth - 1) : "memory");
+}
 
 __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
+  extern __shared__ __align__(16) double nw_ring[];
   const int lane = threadIdx.x;
   const unsigned FULL = 0xffffffffu;
+  // this lane's ring: kNwDepth groups x 4 rows x 4 columns
+  double* my_ring = nw_ring + (size_t)lane * (kBandR * 4);
   for (;;) {
     int it = 0;
     if (lane == 0) it = (int)atomicAdd(a.ticket, 1u);
@@ -252,6 +281,7 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     const double* Sd = a.S + a.s_off[d];
     const int64_t ld = a.pitch[d];
     const int ncg = (m + kBandCols - 1) / kBandCols;
+    const int ngroups = (m + 3) >> 2;
     uint32_t* dirs = a.dirs + a.dir_off[d] + (int64_t)band * ncg * WARP + lane;
     const double* bnd_up = band > 0 ? a.bnd + a.bnd_off[d] + (int64_t)(band - 1) * m : nullptr;
     double* bnd_me = band < nbands - 1 ? a.bnd + a.bnd_off[d] + (int64_t)band * m : nullptr;
@@ -260,46 +290,60 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
 
     const int i0 = row0 + lane * kBandR;  // first row of this lane
     const int my_rows = lane < nl ? min(kBandR, n - i0) : 0;
+    auto issue_group = [&](int g) {
+      if (g < ngroups) {
+        double* dst = my_ring + (size_t)(g % kNwDepth) * (WARP * kBandR * 4);
+#pragma unroll
+        for (int r = 0; r < kBandR; ++r) {
+          if (r < my_rows) {
+            const double* src = Sd + (int64_t)(i0 + r) * ld + g * 4;
+            cp_async16(dst + r * 4, src);
+            cp_async16(dst + r * 4 + 2, src + 2);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+    __syncwarp();  // the previous item's ring reads are complete
+#pragma unroll 1
+    for (int g = 0; g < kNwDepth - 1; ++g) issue_group(g);
+
     double left[kBandR];
 #pragma unroll
     for (int r = 0; r < kBandR; ++r) left[r] = (double)(i0 + r + 1) * p;  // C[i+1][0]
-    double bot = my_rows > 0 ? left[my_rows - 1] : 0.0;
-    double prev_recv = (double)i0 * p;
-    // one 4-column group of S per row, prefetched one group ahead
-    double cur[kBandR][4], nxt[kBandR][4];
-    auto load_group = [&](double (&buf)[kBandR][4], int g) {
+    double bot = 0.0;
 #pragma unroll
-      for (int r = 0; r < kBandR; ++r) {
-        if (r < my_rows && g * 4 < m) {
-          const double2* src = (const double2*)(Sd + (int64_t)(i0 + r) * ld + g * 4);
-          double2 x = __ldg(src), y = __ldg(src + 1);
-          buf[r][0] = x.x;
-          buf[r][1] = x.y;
-          buf[r][2] = y.x;
-          buf[r][3] = y.y;
-        }
-      }
-    };
-    load_group(nxt, 0);
+    for (int r = 0; r < kBandR; ++r)
+      if (r == my_rows - 1) bot = left[r];
+    double prev_recv = (double)i0 * p;
+    double bchunk = 0.0;                 // boundary values of the current 32-column chunk
+    double prev_up = (double)row0 * p;   // C[row0][j] for lane 0 (the diagonal)
     uint32_t dword = 0;
     const int steps = m + nl - 1;
     for (int s = 0; s < steps; ++s) {
       const int j = s - lane;
       const bool active = lane < nl && j >= 0 && j < m;
-      // lane 0 of a lower band waits for the band above to publish column j
-      if (lane == 0 && band > 0 && j < m && (j % kPublish) == 0) {
-        const uint32_t need = (uint32_t)min(j + kPublish, m);
-        while (ld_acquire(prog_up) < need) __nanosleep(32);
+      // band > 0: lane 0's column s needs chunk s/32 of the band above
+      if (band > 0 && (s & 31) == 0 && s < m) {
+        if (lane == 0) {
+          const uint32_t need = (uint32_t)min(s + 32, m);
+          while (ld_acquire(prog_up) < need) __nanosleep(20);
+        }
+        __syncwarp();
+        const int c = s + lane;
+        bchunk = c < m ? ld_acquire_f64(bnd_up + c) : 0.0;
       }
       const double recv = __shfl_up_sync(FULL, bot, 1);
+      const double bval = __shfl_sync(FULL, bchunk, s & 31);
       double up, dg;
       if (lane == 0) {
         if (band == 0) {
           up = (double)(j + 1) * p;
           dg = (double)j * p;
         } else {
-          up = j < m ? bnd_up[j] : 0.0;
-          dg = j == 0 ? (double)row0 * p : (j < m ? bnd_up[j - 1] : 0.0);
+          up = bval;
+          dg = prev_up;
+          prev_up = bval;
         }
       } else {
         up = recv;
@@ -308,24 +352,24 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
       prev_recv = recv;
       if (active) {
         const int jj = j & 3;
+        const int g = j >> 2;
         if (jj == 0) {
-#pragma unroll
-          for (int r = 0; r < kBandR; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) cur[r][c] = nxt[r][c];
-          load_group(nxt, (j >> 2) + 1);
+          issue_group(g + kNwDepth - 1);
+          cp_async_wait_depth();
         }
+        const double* cur = my_ring + (size_t)(g % kNwDepth) * (WARP * kBandR * 4);
         uint32_t codes = 0;
 #pragma unroll
         for (int r = 0; r < kBandR; ++r) {
           if (r < my_rows) {
-            double sv = jj == 0 ? cur[r][0] : jj == 1 ? cur[r][1] : jj == 2 ? cur[r][2] : cur[r][3];
+            const double sv = cur[r * 4 + jj];
             const double dcand = __dadd_rn(dg, __dsub_rn(1.0, sv));
-            const double ucand = __dadd_rn(up, p);
             const double lcand = __dadd_rn(left[r], p);
+            // reference comparison semantics; l folded first (order-equivalent)
             double best = dcand;
-            if (ucand < best) best = ucand;
             if (lcand < best) best = lcand;
+            const double ucand = __dadd_rn(up, p);
+            if (ucand < best) best = ucand;
             const uint32_t code = best == dcand ? 0u : (best == ucand ? 1u : 2u);
             codes |= code << (2 * r);
             dg = left[r];
@@ -338,15 +382,16 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
           if (r == my_rows - 1) bot = left[r];
         dword |= codes << (8 * jj);
         if (jj == 3 || j == m - 1) {
-          dirs[(int64_t)(j >> 2) * WARP] = dword;
+          dirs[(int64_t)g * WARP] = dword;
           dword = 0;
         }
         if (bnd_me != nullptr && lane == nl - 1) {
           bnd_me[j] = bot;
-          if (((j + 1) % kPublish) == 0 || j == m - 1) st_release(prog_me, (uint32_t)(j + 1));
+          if (((j + 1) & 31) == 0 || j == m - 1) st_release(prog_me, (uint32_t)(j + 1));
         }
       }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     // C[n][m] lives in the last band, in the lane that owns row n-1
     if (band == nbands - 1 && lane == (n - 1 - row0) / kBandR) {
 #pragma unroll
@@ -358,7 +403,12 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
 
 cudaError_t launch_nw(const NwArgs& a, int n_warps, cudaStream_t st) {
   if (a.n_items == 0) return cudaSuccess;
-  nw_band_kernel<<<n_warps, WARP, 0, st>>>(a);
+  cudaError_t e = cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kNwSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  nw_band_kernel<<<n_warps, WARP, kNwSmem, st>>>(a);
   return counted(cudaGetLastError());
 }
 
@@ -366,7 +416,9 @@ int nw_resident_warps() {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel, WARP, 0);
+  cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem);
+  cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel, WARP, kNwSmem);
   if (per_sm < 1) per_sm = 1;
   return sms * per_sm;
 }
