@@ -191,6 +191,8 @@ int general_nw(const GeneralPlan& g, GeneralDev& dv, double penalty, double* cos
                cudaStream_t st) {
   BM_CK(cudaMemsetAsync(dv.prog, 0, std::max<int64_t>(g.prog_total, 1) * 4, st), "memset");
   BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
+  // boundary rows start as the sentinel (negative) pattern consumers spin on
+  BM_CK(cudaMemsetAsync(dv.bnd, 0xde, std::max<int64_t>(g.bnd_total, 1) * 8, st), "memset");
   NwArgs a;
   a.S = dv.S;
   a.s_off = dv.s_off;
@@ -317,6 +319,7 @@ int bm_nw(const double* S, const int64_t* s_off, const int32_t* pitch, const int
   BM_CK(sc.alloc(&ticket, 1), "alloc");
   BM_CK(cudaMemsetAsync(prog, 0, std::max<int64_t>(pt, 1) * 4, st), "memset");
   BM_CK(cudaMemsetAsync(ticket, 0, 4, st), "memset");
+  BM_CK(cudaMemsetAsync(bnd, 0xde, std::max<int64_t>(bt, 1) * 8, st), "memset");
   a.S = S;
   a.s_off = s_off;
   a.pitch = pitch;

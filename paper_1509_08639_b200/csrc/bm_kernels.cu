@@ -84,11 +84,16 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
-__device__ __forceinline__ double ld_acquire_f64(const double* p) {
-  double v;
-  asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const double* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+
+// Boundary rows are pre-filled with this byte pattern (cudaMemsetAsync 0xde):
+// a negative double, and a DP cost is never negative (>= 0, +inf or NaN), so a
+// consumer can spin on the value itself -- no flag, no fence, no ERRBAR.
+constexpr uint64_t kBndSentinel = 0xdededededededededeull;
 
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -323,15 +328,15 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     for (int s = 0; s < steps; ++s) {
       const int j = s - lane;
       const bool active = lane < nl && j >= 0 && j < m;
-      // band > 0: lane 0's column s needs chunk s/32 of the band above
+      // band > 0: lane 0's column s needs chunk s/32 of the band above; each
+      // lane waits for its own value of the chunk to be published
       if (band > 0 && (s & 31) == 0 && s < m) {
-        if (lane == 0) {
-          const uint32_t need = (uint32_t)min(s + 32, m);
-          while (ld_acquire(prog_up) < need) __nanosleep(20);
-        }
-        __syncwarp();
         const int c = s + lane;
-        bchunk = c < m ? ld_acquire_f64(bnd_up + c) : 0.0;
+        if (c < m) {
+          uint64_t v;
+          while ((v = ld_relaxed_u64(bnd_up + c)) == kBndSentinel) __nanosleep(32);
+          bchunk = __longlong_as_double((long long)v);
+        }
       }
       const double recv = __shfl_up_sync(FULL, bot, 1);
       const double bval = __shfl_sync(FULL, bchunk, s & 31);
@@ -375,20 +380,16 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
             dg = left[r];
             left[r] = best;
             up = best;
+            bot = best;  // the last valid row of the lane ends the chain
           }
         }
-#pragma unroll
-        for (int r = 0; r < kBandR; ++r)
-          if (r == my_rows - 1) bot = left[r];
         dword |= codes << (8 * jj);
         if (jj == 3 || j == m - 1) {
           dirs[(int64_t)g * WARP] = dword;
           dword = 0;
         }
-        if (bnd_me != nullptr && lane == nl - 1) {
-          bnd_me[j] = bot;
-          if (((j + 1) & 31) == 0 || j == m - 1) st_release(prog_me, (uint32_t)(j + 1));
-        }
+        if (bnd_me != nullptr && lane == nl - 1)
+          asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(bnd_me + j), "d"(bot) : "memory");
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");

@@ -307,11 +307,9 @@ __global__ void __launch_bounds__(kRingThreads, 5) mine_ring_kernel(FusedArgs a)
                 dg = left[r];
                 left[r] = best;
                 up = best;
+                bot = best;  // the last valid row of the lane ends the chain
               }
             }
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-              if (r == my_rows - 1) bot = left[r];
             const int slot = j % CPW;
             dword |= codes << (2 * R * slot);
             if (slot == CPW - 1 || j == m - 1) {
