@@ -13,7 +13,9 @@ import threading
 
 from .errors import NativeUnavailableError, ResourceLimitError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbimine_b200.so")
+# BM_LIB_PATH: load an instrumented variant (tools/nw_trace.py); default in-tree
+LIB_PATH = os.environ.get("BM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                        "libbimine_b200.so")
 
 BM_OK, BM_EINVAL, BM_ECUDA, BM_ENOMEM, BM_ELIMIT = 0, -1, -2, -3, -4
 MOVE_D, MOVE_GS, MOVE_GT = 0, 1, 2

@@ -759,3 +759,12 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
 }
 
 }  // extern "C"
+
+#ifdef BM_NW_PROFILE
+extern "C" int bm_nw_prof(unsigned long long* host, int n_items) {
+  return (int)cudaMemcpyFromSymbol(host, bm::g_nw_prof, sizeof(unsigned long long) * 4 * n_items);
+}
+extern "C" int bm_nw_chunks(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, bm::g_nw_chunk, sizeof(unsigned long long) * 16 * 256 * 3);
+}
+#endif

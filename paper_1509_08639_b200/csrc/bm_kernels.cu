@@ -93,7 +93,7 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const double* p) {
 // Boundary rows are pre-filled with this byte pattern (cudaMemsetAsync 0xde):
 // a negative double, and a DP cost is never negative (>= 0, +inf or NaN), so a
 // consumer can spin on the value itself -- no flag, no fence, no ERRBAR.
-constexpr uint64_t kBndSentinel = 0xdededededededededeull;
+constexpr uint64_t kBndSentinel = 0xdedededededededeull;
 
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -233,29 +233,36 @@ cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, doub
 // K2/K3: banded anti-diagonal wavefront.
 //
 // A document's rows are cut into bands of 128 (32 lanes x 4 rows). A warp
-// owns one band; lane L owns rows 4L..4L+3 and runs one column behind lane
-// L-1, so the value a lane needs from the row above arrives by one 64-bit
-// shuffle of the previous step (the anti-diagonal dependency). The 4 rows of a
-// lane are a short in-register chain.
-//  * S: every lane streams its own 4 rows with cp.async (16-byte LDGSTS) into
-//    a private slice of a shared-memory ring kNwDepth groups of 4 columns deep,
-//    so HBM latency is hidden ~32 columns ahead of use.
-//  * Bands hand their bottom row to the band below through global memory in
-//    32-column chunks: the producer lane stores values as it goes and releases
-//    a progress flag per chunk; the consumer warp acquires the flag once per
-//    chunk, loads the chunk with one coalesced load and hands values to lane 0
-//    by shuffle.
+// owns one band; lane L owns rows 4L..4L+3 and runs one 4-column group
+// behind lane L-1 (blocked wavefront, see nw_band_kernel).
+//  * S: every lane streams its own 4x4 blocks with cp.async (16-byte LDGSTS)
+//    into a private, bank-padded slice of a shared-memory ring kNwDepth
+//    groups deep, so HBM latency is hidden ~32 columns ahead of use.
+//  * Bands hand their bottom row to the band below through global memory: the
+//    band's rows are pre-filled with a sentinel byte pattern, the producer lane
+//    stores values with relaxed stores, and the consumer warp spins on the
+//    value itself (one coalesced 32-column load per 8 super-steps), handing
+//    values to lane 0 by shuffle. No fences or flags are needed because the
+//    payload is the signal.
 // Warps are persistent and take (doc, band) items in increasing order from an
 // atomic ticket, so a wait always targets a band that is resident or finished.
 // ---------------------------------------------------------------------------
+constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNwDepth = 8;                                // groups in flight per lane
-constexpr int kNwSmem = kNwDepth * WARP * kBandR * 4 * 8;  // 32 KB per warp
+constexpr int kNwLane = kBandR * 4 + 2;                     // doubles per lane slice (+pad)
+constexpr int kNwSmem = kNwDepth * WARP * kNwLane * 8 + WARP * 8;  // ~37 KB per warp
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                    (uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src)
                : "memory");
+}
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -264,152 +271,276 @@ __device__ __forceinline__ void cp_async_wait_depth() {
   asm volatile("cp.async.wait_group %0;" ::"n"(kNwDepth - 1) : "memory");
 }
 
+// Blocked wavefront: per super-step t, lane L computes the 4x4 block of its
+// rows (4L..4L+3) x columns 4(t-L)..4(t-L)+3. The block above-left
+// dependencies arrive from lane L-1's previous super-step (4 values + the
+// diagonal by shuffle), so every per-group operation (S prefetch, code store,
+// boundary publication) is warp-uniform, and the 16 cells expose ILP.
+__device__ __forceinline__ void nw_cell(double dg, double up, double lf, double om, double p,
+                                        double& best, uint32_t& code) {
+  const double dcand = __dadd_rn(dg, om);
+  const double lcand = __dadd_rn(lf, p);
+  double b = dcand;
+  if (lcand < b) b = lcand;  // reference comparison semantics; l first is order-equivalent
+  const double ucand = __dadd_rn(up, p);
+  if (ucand < b) b = ucand;
+  code = b == dcand ? 0u : (b == ucand ? 1u : 2u);
+  best = b;
+}
+
+// One 4x4 block, every cell valid: straight-line code in anti-diagonal
+// order, so the 4-wide independent cells of a diagonal interleave in the
+// in-order issue stream. On entry u* is the row above (columns 0..3), dg the
+// cell above-left of column 0 and l* the column left of the block; on exit u*
+// is the block's last row and l* its last column.
+__device__ __forceinline__ void nw_block_full(const double* cur, double p, double dg, double& u0,
+                                              double& u1, double& u2, double& u3, double& l0,
+                                              double& l1, double& l2, double& l3, uint32_t& codes) {
+  double o[16];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double2 s = *(const double2*)(cur + 2 * q);
+    o[2 * q] = __dsub_rn(1.0, s.x);
+    o[2 * q + 1] = __dsub_rn(1.0, s.y);
+  }
+  double v[4][4];
+  uint32_t k[4][4];
+  const double up[4] = {u0, u1, u2, u3};
+  const double lf[4] = {l0, l1, l2, l3};
+#pragma unroll
+  for (int diag = 0; diag < 7; ++diag) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int c = diag - r;
+      if (c < 0 || c > 3) continue;
+      const double dgv = r == 0 ? (c == 0 ? dg : up[c - 1]) : (c == 0 ? lf[r - 1] : v[r - 1][c - 1]);
+      const double upv = r == 0 ? up[c] : v[r - 1][c];
+      const double lfv = c == 0 ? lf[r] : v[r][c - 1];
+      nw_cell(dgv, upv, lfv, o[4 * r + c], p, v[r][c], k[r][c]);
+    }
+  }
+  uint32_t cw = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cw |= k[r][c] << (8 * c + 2 * r);
+  codes = cw;
+  u0 = v[3][0];
+  u1 = v[3][1];
+  u2 = v[3][2];
+  u3 = v[3][3];
+  l0 = v[0][3];
+  l1 = v[1][3];
+  l2 = v[2][3];
+  l3 = v[3][3];
+}
+
+// The last block of a lane: cmax (1..4) valid columns; writes the DP cost of
+// the matrix when this lane holds row n-1 (cost_r = its index in the block).
+__device__ __forceinline__ void nw_block_last(const double* cur, double p, double dg, double& u0,
+                                           double& u1, double& u2, double& u3, double& l0,
+                                           double& l1, double& l2, double& l3, uint32_t& codes,
+                                           int cmax, int cost_r, double* cost) {
+  double up[4] = {u0, u1, u2, u3};
+  double lf[4] = {l0, l1, l2, l3};
+  uint32_t cw = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    double left = lf[r];
+    double d = dg;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c < cmax) {
+        double v;
+        uint32_t kk;
+        nw_cell(d, up[c], left, __dsub_rn(1.0, cur[4 * r + c]), p, v, kk);
+        cw |= kk << (8 * c + 2 * r);
+        d = up[c];
+        up[c] = v;
+        left = v;
+      }
+    }
+    dg = lf[r];
+    lf[r] = left;
+    if (r == cost_r) *cost = left;
+  }
+  codes = cw;
+  u0 = up[0];
+  u1 = up[1];
+  u2 = up[2];
+  u3 = up[3];
+  l0 = lf[0];
+  l1 = lf[1];
+  l2 = lf[2];
+  l3 = lf[3];
+}
+
+#ifdef BM_NW_PROFILE
+// tools/nw_trace.py builds a variant with per-item timestamps (globaltimer):
+// [0] ticket taken, [1] first block, [2] done, [3] boundary wait ns after the first chunk
+__device__ unsigned long long g_nw_prof[8192][4];
+// per (band < 16, chunk < 256): [0] wait start, [1] wait end (consumer lane 0),
+// [2] publish time of the chunk's last group (producer lane nl-1, after store)
+__device__ unsigned long long g_nw_chunk[16][256][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define NW_PROF(stmt) stmt
+#else
+#define NW_PROF(stmt)
+#endif
+
 __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   extern __shared__ __align__(16) double nw_ring[];
   const int lane = threadIdx.x;
-  const unsigned FULL = 0xffffffffu;
-  // this lane's ring: kNwDepth groups x 4 rows x 4 columns
-  double* my_ring = nw_ring + (size_t)lane * (kBandR * 4);
+  double* bnd_s = nw_ring + kNwDepth * WARP * kNwLane;  // current 32-column boundary chunk
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(nw_ring + (size_t)lane * kNwLane);
   for (;;) {
     int it = 0;
     if (lane == 0) it = (int)atomicAdd(a.ticket, 1u);
-    it = __shfl_sync(FULL, it, 0);
+    it = __shfl_sync(kFull, it, 0);
     if (it >= a.n_items) return;
     const WorkItem w = a.items[it];
+    NW_PROF(unsigned long long spins = 0; bool first = true;
+            if (lane == 0 && it < 8192) g_nw_prof[it][0] = gtimer();)
     const int d = w.doc, band = w.band;
     const int n = a.n[d], m = a.m[d];
     const double p = a.p;
     const int row0 = band * kBandRows;
-    const int rows_here = min(kBandRows, n - row0);
-    const int nl = (rows_here + kBandR - 1) / kBandR;
+    const int nl = (min(kBandRows, n - row0) + kBandR - 1) / kBandR;
     const int nbands = (n + kBandRows - 1) / kBandRows;
-    const double* Sd = a.S + a.s_off[d];
     const int64_t ld = a.pitch[d];
-    const int ncg = (m + kBandCols - 1) / kBandCols;
     const int ngroups = (m + 3) >> 2;
-    uint32_t* dirs = a.dirs + a.dir_off[d] + (int64_t)band * ncg * WARP + lane;
+    uint32_t* dirs = a.dirs + a.dir_off[d] + (int64_t)band * ngroups * WARP + lane;
     const double* bnd_up = band > 0 ? a.bnd + a.bnd_off[d] + (int64_t)(band - 1) * m : nullptr;
     double* bnd_me = band < nbands - 1 ? a.bnd + a.bnd_off[d] + (int64_t)band * m : nullptr;
-    const uint32_t* prog_up = band > 0 ? a.prog + a.prog_off[d] + band - 1 : nullptr;
-    uint32_t* prog_me = a.prog + a.prog_off[d] + band;
-
-    const int i0 = row0 + lane * kBandR;  // first row of this lane
-    const int my_rows = lane < nl ? min(kBandR, n - i0) : 0;
+    const int i0 = row0 + lane * kBandR;
+    const bool lane_on = lane < nl;
+    // rows past n (only in the last lane of the last band) re-read row n-1:
+    // they compute unused values, which keeps the block free of row checks
+    const double* src0 = a.S + a.s_off[d] + (int64_t)min(i0 + 0, n - 1) * ld;
+    const double* src1 = a.S + a.s_off[d] + (int64_t)min(i0 + 1, n - 1) * ld;
+    const double* src2 = a.S + a.s_off[d] + (int64_t)min(i0 + 2, n - 1) * ld;
+    const double* src3 = a.S + a.s_off[d] + (int64_t)min(i0 + 3, n - 1) * ld;
     auto issue_group = [&](int g) {
-      if (g < ngroups) {
-        double* dst = my_ring + (size_t)(g % kNwDepth) * (WARP * kBandR * 4);
-#pragma unroll
-        for (int r = 0; r < kBandR; ++r) {
-          if (r < my_rows) {
-            const double* src = Sd + (int64_t)(i0 + r) * ld + g * 4;
-            cp_async16(dst + r * 4, src);
-            cp_async16(dst + r * 4 + 2, src + 2);
-          }
-        }
+      if (lane_on && g < ngroups) {
+        const uint32_t dst = ring_s + (uint32_t)((g % kNwDepth) * (WARP * kNwLane * 8));
+        const int c = g * 4;
+        cp_async16_s(dst + 0, src0 + c);
+        cp_async16_s(dst + 16, src0 + c + 2);
+        cp_async16_s(dst + 32, src1 + c);
+        cp_async16_s(dst + 48, src1 + c + 2);
+        cp_async16_s(dst + 64, src2 + c);
+        cp_async16_s(dst + 80, src2 + c + 2);
+        cp_async16_s(dst + 96, src3 + c);
+        cp_async16_s(dst + 112, src3 + c + 2);
       }
       cp_async_commit();
     };
-    __syncwarp();  // the previous item's ring reads are complete
+    __syncwarp();
 #pragma unroll 1
     for (int g = 0; g < kNwDepth - 1; ++g) issue_group(g);
 
-    double left[kBandR];
-#pragma unroll
-    for (int r = 0; r < kBandR; ++r) left[r] = (double)(i0 + r + 1) * p;  // C[i+1][0]
-    double bot = 0.0;
-#pragma unroll
-    for (int r = 0; r < kBandR; ++r)
-      if (r == my_rows - 1) bot = left[r];
-    double prev_recv = (double)i0 * p;
-    double bchunk = 0.0;                 // boundary values of the current 32-column chunk
-    double prev_up = (double)row0 * p;   // C[row0][j] for lane 0 (the diagonal)
-    uint32_t dword = 0;
-    const int steps = m + nl - 1;
-    for (int s = 0; s < steps; ++s) {
-      const int j = s - lane;
-      const bool active = lane < nl && j >= 0 && j < m;
-      // band > 0: lane 0's column s needs chunk s/32 of the band above; each
-      // lane waits for its own value of the chunk to be published
-      if (band > 0 && (s & 31) == 0 && s < m) {
-        const int c = s + lane;
+    double l0 = (double)(i0 + 1) * p, l1 = (double)(i0 + 2) * p;  // C[i+1][4g]: left of block
+    double l2 = (double)(i0 + 3) * p, l3 = (double)(i0 + 4) * p;
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;  // last row of the block
+    double dgn = (double)i0 * p;                     // C[i0][4g] for the next block
+    const int cost_lane = (band == nbands - 1) ? (n - 1 - row0) / kBandR : -1;
+    const int steps = ngroups + nl - 1;
+    for (int t = 0; t < steps; ++t) {
+      const int g = t - lane;
+      if ((t & 7) == 0 && 4 * t < m) {
+        NW_PROF(const unsigned long long w0 = gtimer();)
+        // lane 0's next 8 groups: the band above's last row (band 0: border)
+        const int c = 4 * t + lane;
+        double v = 0.0;
         if (c < m) {
-          uint64_t v;
-          while ((v = ld_relaxed_u64(bnd_up + c)) == kBndSentinel) __nanosleep(32);
-          bchunk = __longlong_as_double((long long)v);
-        }
-      }
-      const double recv = __shfl_up_sync(FULL, bot, 1);
-      const double bval = __shfl_sync(FULL, bchunk, s & 31);
-      double up, dg;
-      if (lane == 0) {
-        if (band == 0) {
-          up = (double)(j + 1) * p;
-          dg = (double)j * p;
-        } else {
-          up = bval;
-          dg = prev_up;
-          prev_up = bval;
-        }
-      } else {
-        up = recv;
-        dg = prev_recv;
-      }
-      prev_recv = recv;
-      if (active) {
-        const int jj = j & 3;
-        const int g = j >> 2;
-        if (jj == 0) {
-          issue_group(g + kNwDepth - 1);
-          cp_async_wait_depth();
-        }
-        const double* cur = my_ring + (size_t)(g % kNwDepth) * (WARP * kBandR * 4);
-        uint32_t codes = 0;
-#pragma unroll
-        for (int r = 0; r < kBandR; ++r) {
-          if (r < my_rows) {
-            const double sv = cur[r * 4 + jj];
-            const double dcand = __dadd_rn(dg, __dsub_rn(1.0, sv));
-            const double lcand = __dadd_rn(left[r], p);
-            // reference comparison semantics; l folded first (order-equivalent)
-            double best = dcand;
-            if (lcand < best) best = lcand;
-            const double ucand = __dadd_rn(up, p);
-            if (ucand < best) best = ucand;
-            const uint32_t code = best == dcand ? 0u : (best == ucand ? 1u : 2u);
-            codes |= code << (2 * r);
-            dg = left[r];
-            left[r] = best;
-            up = best;
-            bot = best;  // the last valid row of the lane ends the chain
+          if (band == 0) {
+            v = (double)(c + 1) * p;
+          } else {
+            uint64_t x;
+            while ((x = ld_relaxed_u64(bnd_up + c)) == kBndSentinel) {
+#if defined(BM_NW_PROFILE) && defined(BM_NW_NOSLEEP)
+#else
+              __nanosleep(32);
+#endif
+            }
+            v = __longlong_as_double((long long)x);
           }
         }
-        dword |= codes << (8 * jj);
-        if (jj == 3 || j == m - 1) {
-          dirs[(int64_t)g * WARP] = dword;
-          dword = 0;
+        __syncwarp();
+        bnd_s[lane] = v;
+        __syncwarp();
+        NW_PROF(if (t > 0) spins += gtimer() - w0;
+                if (lane == 0 && it < 16 && (t >> 3) < 256) {
+                  g_nw_chunk[it][t >> 3][0] = w0;
+                  g_nw_chunk[it][t >> 3][1] = gtimer();
+                })
+      }
+      double u0 = __shfl_up_sync(kFull, b0, 1);
+      double u1 = __shfl_up_sync(kFull, b1, 1);
+      double u2 = __shfl_up_sync(kFull, b2, 1);
+      double u3 = __shfl_up_sync(kFull, b3, 1);
+      if (lane == 0) {
+        const double2 x = *(const double2*)(bnd_s + 4 * (t & 7));
+        const double2 y = *(const double2*)(bnd_s + 4 * (t & 7) + 2);
+        u0 = x.x;
+        u1 = x.y;
+        u2 = y.x;
+        u3 = y.y;
+      }
+      if (lane_on && g >= 0 && g < ngroups) {
+        NW_PROF(if (first && lane == 0 && it < 8192) g_nw_prof[it][1] = gtimer(); first = false;)
+        issue_group(g + kNwDepth - 1);
+        cp_async_wait_depth();
+        const double* cur = nw_ring + (size_t)lane * kNwLane + (size_t)(g % kNwDepth) * (WARP * kNwLane);
+        uint32_t codes;
+        const double up_last = u3;  // C[i0][4g+4]: the next block's diagonal
+        // Columns past m in a lane's last group read the pitch padding and
+        // compute values nobody reads (codes past m are never traced), so
+        // every lane stays on the straight-line block; only the lane holding
+        // cell (n-1, m-1) takes the exact path, once per matrix, to emit cost.
+        if (g != ngroups - 1 || lane != cost_lane) {
+          nw_block_full(cur, p, dgn, u0, u1, u2, u3, l0, l1, l2, l3, codes);
+        } else {
+          nw_block_last(cur, p, dgn, u0, u1, u2, u3, l0, l1, l2, l3, codes, m - 4 * g, n - 1 - i0,
+                        a.cost + d);
         }
-        if (bnd_me != nullptr && lane == nl - 1)
-          asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(bnd_me + j), "d"(bot) : "memory");
+        b0 = u0;
+        b1 = u1;
+        b2 = u2;
+        b3 = u3;
+        dgn = up_last;
+        const int cmax = m - 4 * g;  // >= 4 except in the last group
+        dirs[(int64_t)g * WARP] = codes;
+        if (bnd_me != nullptr && lane == nl - 1) {
+          double* dst = bnd_me + 4 * g;
+          st_relaxed_f64(dst, b0);
+          if (cmax > 1) st_relaxed_f64(dst + 1, b1);
+          if (cmax > 2) st_relaxed_f64(dst + 2, b2);
+          if (cmax > 3) st_relaxed_f64(dst + 3, b3);
+          NW_PROF(if ((g & 7) == 7 && it < 16 && (g >> 3) < 256) g_nw_chunk[it][g >> 3][2] = gtimer();)
+        }
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    // C[n][m] lives in the last band, in the lane that owns row n-1
-    if (band == nbands - 1 && lane == (n - 1 - row0) / kBandR) {
-#pragma unroll
-      for (int r = 0; r < kBandR; ++r)
-        if (i0 + r == n - 1) a.cost[d] = left[r];
-    }
+    __syncwarp();
+    NW_PROF(if (lane == 0 && it < 8192) { g_nw_prof[it][2] = gtimer(); g_nw_prof[it][3] = spins; })
   }
 }
 
 cudaError_t launch_nw(const NwArgs& a, int n_warps, cudaStream_t st) {
   if (a.n_items == 0) return cudaSuccess;
+  static const int pad = getenv("BM_NW_SMEM") ? atoi(getenv("BM_NW_SMEM")) : kNwSmem;
+  const int smem = pad > kNwSmem ? pad : kNwSmem;
   cudaError_t e = cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kNwSmem);
+                                       smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  nw_band_kernel<<<n_warps, WARP, kNwSmem, st>>>(a);
+  nw_band_kernel<<<n_warps, WARP, smem, st>>>(a);
   return counted(cudaGetLastError());
 }
 
