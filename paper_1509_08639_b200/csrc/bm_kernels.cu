@@ -248,9 +248,11 @@ cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, doub
 // atomic ticket, so a wait always targets a band that is resident or finished.
 // ---------------------------------------------------------------------------
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNwDepth = 8;                                // groups in flight per lane
-constexpr int kNwLane = kBandR * 4 + 2;                     // doubles per lane slice (+pad)
-constexpr int kNwSmem = kNwDepth * WARP * kNwLane * 8 + WARP * 8;  // ~37 KB per warp
+constexpr int kNwDepth = 8;                                 // groups in flight per lane
+constexpr int kNwSlots = kNwDepth + 1;                       // + a dummy slot
+constexpr int kNwLane = kBandR * 4 + 2;                      // doubles per lane slice (+pad)
+constexpr int kNwSlotBytes = WARP * kNwLane * 8;
+constexpr int kNwSmem = kNwSlots * kNwSlotBytes + WARP * 8;  // ~41 KB per warp
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -288,93 +290,6 @@ __device__ __forceinline__ void nw_cell(double dg, double up, double lf, double 
   best = b;
 }
 
-// One 4x4 block, every cell valid: straight-line code in anti-diagonal
-// order, so the 4-wide independent cells of a diagonal interleave in the
-// in-order issue stream. On entry u* is the row above (columns 0..3), dg the
-// cell above-left of column 0 and l* the column left of the block; on exit u*
-// is the block's last row and l* its last column.
-__device__ __forceinline__ void nw_block_full(const double* cur, double p, double dg, double& u0,
-                                              double& u1, double& u2, double& u3, double& l0,
-                                              double& l1, double& l2, double& l3, uint32_t& codes) {
-  double o[16];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const double2 s = *(const double2*)(cur + 2 * q);
-    o[2 * q] = __dsub_rn(1.0, s.x);
-    o[2 * q + 1] = __dsub_rn(1.0, s.y);
-  }
-  double v[4][4];
-  uint32_t k[4][4];
-  const double up[4] = {u0, u1, u2, u3};
-  const double lf[4] = {l0, l1, l2, l3};
-#pragma unroll
-  for (int diag = 0; diag < 7; ++diag) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int c = diag - r;
-      if (c < 0 || c > 3) continue;
-      const double dgv = r == 0 ? (c == 0 ? dg : up[c - 1]) : (c == 0 ? lf[r - 1] : v[r - 1][c - 1]);
-      const double upv = r == 0 ? up[c] : v[r - 1][c];
-      const double lfv = c == 0 ? lf[r] : v[r][c - 1];
-      nw_cell(dgv, upv, lfv, o[4 * r + c], p, v[r][c], k[r][c]);
-    }
-  }
-  uint32_t cw = 0;
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) cw |= k[r][c] << (8 * c + 2 * r);
-  codes = cw;
-  u0 = v[3][0];
-  u1 = v[3][1];
-  u2 = v[3][2];
-  u3 = v[3][3];
-  l0 = v[0][3];
-  l1 = v[1][3];
-  l2 = v[2][3];
-  l3 = v[3][3];
-}
-
-// The last block of a lane: cmax (1..4) valid columns; writes the DP cost of
-// the matrix when this lane holds row n-1 (cost_r = its index in the block).
-__device__ __forceinline__ void nw_block_last(const double* cur, double p, double dg, double& u0,
-                                           double& u1, double& u2, double& u3, double& l0,
-                                           double& l1, double& l2, double& l3, uint32_t& codes,
-                                           int cmax, int cost_r, double* cost) {
-  double up[4] = {u0, u1, u2, u3};
-  double lf[4] = {l0, l1, l2, l3};
-  uint32_t cw = 0;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    double left = lf[r];
-    double d = dg;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (c < cmax) {
-        double v;
-        uint32_t kk;
-        nw_cell(d, up[c], left, __dsub_rn(1.0, cur[4 * r + c]), p, v, kk);
-        cw |= kk << (8 * c + 2 * r);
-        d = up[c];
-        up[c] = v;
-        left = v;
-      }
-    }
-    dg = lf[r];
-    lf[r] = left;
-    if (r == cost_r) *cost = left;
-  }
-  codes = cw;
-  u0 = up[0];
-  u1 = up[1];
-  u2 = up[2];
-  u3 = up[3];
-  l0 = lf[0];
-  l1 = lf[1];
-  l2 = lf[2];
-  l3 = lf[3];
-}
-
 #ifdef BM_NW_PROFILE
 // tools/nw_trace.py builds a variant with per-item timestamps (globaltimer):
 // [0] ticket taken, [1] first block, [2] done, [3] boundary wait ns after the first chunk
@@ -392,11 +307,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define NW_PROF(stmt)
 #endif
 
+// Blocked wavefront: at super-step t lane L computes the 4x4 block of its rows
+// (4L..4L+3) x columns 4(t-L)..4(t-L)+3. Its inputs from the row above (4
+// values) arrive by shuffle from lane L-1's previous super-step; lane 0 reads
+// them from the band above (or the border) through a 32-column chunk in
+// shared memory. Every super-step is one straight-line basic block for all
+// lanes (lanes outside their column range compute values nobody reads; stores
+// are predicated), so the in-order issue can interleave the S prefetch of the
+// next block, shuffles and stores with the 7-cell dependency chain of the
+// current one. S for block g+1 is loaded and turned into 1-S during block g
+// (two register sets, ping-pong by a 2x unrolled loop).
 __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   extern __shared__ __align__(16) double nw_ring[];
   const int lane = threadIdx.x;
-  double* bnd_s = nw_ring + kNwDepth * WARP * kNwLane;  // current 32-column boundary chunk
-  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(nw_ring + (size_t)lane * kNwLane);
+  double* bnd_s = nw_ring + kNwSlots * WARP * kNwLane;  // current 32-column boundary chunk
+  const double* ring_l = nw_ring + (size_t)lane * kNwLane;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring_l);
   for (;;) {
     int it = 0;
     if (lane == 0) it = (int)atomicAdd(a.ticket, 1u);
@@ -418,38 +344,54 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     double* bnd_me = band < nbands - 1 ? a.bnd + a.bnd_off[d] + (int64_t)band * m : nullptr;
     const int i0 = row0 + lane * kBandR;
     const bool lane_on = lane < nl;
+    const bool pub_lane = bnd_me != nullptr && lane == nl - 1;
+    const int cost_lane = (band == nbands - 1) ? (n - 1 - row0) / kBandR : -1;
     // rows past n (only in the last lane of the last band) re-read row n-1:
     // they compute unused values, which keeps the block free of row checks
     const double* src0 = a.S + a.s_off[d] + (int64_t)min(i0 + 0, n - 1) * ld;
     const double* src1 = a.S + a.s_off[d] + (int64_t)min(i0 + 1, n - 1) * ld;
     const double* src2 = a.S + a.s_off[d] + (int64_t)min(i0 + 2, n - 1) * ld;
     const double* src3 = a.S + a.s_off[d] + (int64_t)min(i0 + 3, n - 1) * ld;
-    auto issue_group = [&](int g) {
-      if (lane_on && g < ngroups) {
-        const uint32_t dst = ring_s + (uint32_t)((g % kNwDepth) * (WARP * kNwLane * 8));
-        const int c = g * 4;
-        cp_async16_s(dst + 0, src0 + c);
-        cp_async16_s(dst + 16, src0 + c + 2);
-        cp_async16_s(dst + 32, src1 + c);
-        cp_async16_s(dst + 48, src1 + c + 2);
-        cp_async16_s(dst + 64, src2 + c);
-        cp_async16_s(dst + 80, src2 + c + 2);
-        cp_async16_s(dst + 96, src3 + c);
-        cp_async16_s(dst + 112, src3 + c + 2);
-      }
+    // one commit per call on every lane; groups outside [0, ngroups) go to
+    // the dummy slot so the per-lane group accounting stays uniform
+    auto issue = [&](int gi) {
+      const bool ok = (unsigned)gi < (unsigned)ngroups;
+      const int c = ok ? gi * 4 : 0;
+      const uint32_t dst = ring_s + (uint32_t)((ok ? (gi & (kNwDepth - 1)) : kNwDepth) * kNwSlotBytes);
+      cp_async16_s(dst + 0, src0 + c);
+      cp_async16_s(dst + 16, src0 + c + 2);
+      cp_async16_s(dst + 32, src1 + c);
+      cp_async16_s(dst + 48, src1 + c + 2);
+      cp_async16_s(dst + 64, src2 + c);
+      cp_async16_s(dst + 80, src2 + c + 2);
+      cp_async16_s(dst + 96, src3 + c);
+      cp_async16_s(dst + 112, src3 + c + 2);
       cp_async_commit();
+    };
+    auto load = [&](int gi, double(&o)[16]) {
+      const double* cur = ring_l + (size_t)(gi & (kNwDepth - 1)) * (WARP * kNwLane);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 s = *(const double2*)(cur + 2 * q);
+        o[2 * q] = __dsub_rn(1.0, s.x);
+        o[2 * q + 1] = __dsub_rn(1.0, s.y);
+      }
     };
     __syncwarp();
 #pragma unroll 1
-    for (int g = 0; g < kNwDepth - 1; ++g) issue_group(g);
+    for (int q = 0; q < kNwDepth; ++q) issue(q - lane);
+    cp_async_wait_depth();
+    double oA[16], oB[16];
+    load(-lane, oA);
 
-    double l0 = (double)(i0 + 1) * p, l1 = (double)(i0 + 2) * p;  // C[i+1][4g]: left of block
-    double l2 = (double)(i0 + 3) * p, l3 = (double)(i0 + 4) * p;
-    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;  // last row of the block
-    double dgn = (double)i0 * p;                     // C[i0][4g] for the next block
-    const int cost_lane = (band == nbands - 1) ? (n - 1 - row0) / kBandR : -1;
-    const int steps = ngroups + nl - 1;
-    for (int t = 0; t < steps; ++t) {
+    const double il0 = (double)(i0 + 1) * p, il1 = (double)(i0 + 2) * p;
+    const double il2 = (double)(i0 + 3) * p, il3 = (double)(i0 + 4) * p;
+    const double idg = (double)i0 * p;
+    double l0 = il0, l1 = il1, l2 = il2, l3 = il3;  // C[i+1][4g]: left of the block
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;  // last row of the previous block
+    double dgn = idg;                                // C[i0][4g]: above-left of the block
+
+    auto step = [&](const int t, double(&oc)[16], double(&on)[16]) {
       const int g = t - lane;
       if ((t & 7) == 0 && 4 * t < m) {
         NW_PROF(const unsigned long long w0 = gtimer();)
@@ -462,8 +404,7 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
           } else {
             uint64_t x;
             while ((x = ld_relaxed_u64(bnd_up + c)) == kBndSentinel) {
-#if defined(BM_NW_PROFILE) && defined(BM_NW_NOSLEEP)
-#else
+#if !(defined(BM_NW_PROFILE) && defined(BM_NW_NOSLEEP))
               __nanosleep(32);
 #endif
             }
@@ -479,51 +420,89 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
                   g_nw_chunk[it][t >> 3][1] = gtimer();
                 })
       }
-      double u0 = __shfl_up_sync(kFull, b0, 1);
-      double u1 = __shfl_up_sync(kFull, b1, 1);
-      double u2 = __shfl_up_sync(kFull, b2, 1);
-      double u3 = __shfl_up_sync(kFull, b3, 1);
-      if (lane == 0) {
+      NW_PROF(if (first && g == 0 && lane == 0 && it < 8192) { g_nw_prof[it][1] = gtimer(); first = false; })
+      double u[4];
+      u[0] = __shfl_up_sync(kFull, b0, 1);
+      u[1] = __shfl_up_sync(kFull, b1, 1);
+      u[2] = __shfl_up_sync(kFull, b2, 1);
+      u[3] = __shfl_up_sync(kFull, b3, 1);
+      {
         const double2 x = *(const double2*)(bnd_s + 4 * (t & 7));
         const double2 y = *(const double2*)(bnd_s + 4 * (t & 7) + 2);
-        u0 = x.x;
-        u1 = x.y;
-        u2 = y.x;
-        u3 = y.y;
-      }
-      if (lane_on && g >= 0 && g < ngroups) {
-        NW_PROF(if (first && lane == 0 && it < 8192) g_nw_prof[it][1] = gtimer(); first = false;)
-        issue_group(g + kNwDepth - 1);
-        cp_async_wait_depth();
-        const double* cur = nw_ring + (size_t)lane * kNwLane + (size_t)(g % kNwDepth) * (WARP * kNwLane);
-        uint32_t codes;
-        const double up_last = u3;  // C[i0][4g+4]: the next block's diagonal
-        // Columns past m in a lane's last group read the pitch padding and
-        // compute values nobody reads (codes past m are never traced), so
-        // every lane stays on the straight-line block; only the lane holding
-        // cell (n-1, m-1) takes the exact path, once per matrix, to emit cost.
-        if (g != ngroups - 1 || lane != cost_lane) {
-          nw_block_full(cur, p, dgn, u0, u1, u2, u3, l0, l1, l2, l3, codes);
-        } else {
-          nw_block_last(cur, p, dgn, u0, u1, u2, u3, l0, l1, l2, l3, codes, m - 4 * g, n - 1 - i0,
-                        a.cost + d);
-        }
-        b0 = u0;
-        b1 = u1;
-        b2 = u2;
-        b3 = u3;
-        dgn = up_last;
-        const int cmax = m - 4 * g;  // >= 4 except in the last group
-        dirs[(int64_t)g * WARP] = codes;
-        if (bnd_me != nullptr && lane == nl - 1) {
-          double* dst = bnd_me + 4 * g;
-          st_relaxed_f64(dst, b0);
-          if (cmax > 1) st_relaxed_f64(dst + 1, b1);
-          if (cmax > 2) st_relaxed_f64(dst + 2, b2);
-          if (cmax > 3) st_relaxed_f64(dst + 3, b3);
-          NW_PROF(if ((g & 7) == 7 && it < 16 && (g >> 3) < 256) g_nw_chunk[it][g >> 3][2] = gtimer();)
+        if (lane == 0) {
+          u[0] = x.x;
+          u[1] = x.y;
+          u[2] = y.x;
+          u[3] = y.y;
         }
       }
+      if (g == 0) {  // the lane's first block: the left border of its rows
+        l0 = il0;
+        l1 = il1;
+        l2 = il2;
+        l3 = il3;
+        dgn = idg;
+      }
+      issue(g + kNwDepth);
+      cp_async_wait_depth();  // block g+1 has landed
+      load(g + 1, on);
+
+      // the 4x4 block, anti-diagonal order
+      double v[4][4];
+      uint32_t kc[4][4];
+      const double lf[4] = {l0, l1, l2, l3};
+#pragma unroll
+      for (int dd = 0; dd < 7; ++dd) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int c = dd - r;
+          if (c < 0 || c > 3) continue;
+          const double dgv = r == 0 ? (c == 0 ? dgn : u[c - 1]) : (c == 0 ? lf[r - 1] : v[r - 1][c - 1]);
+          const double upv = r == 0 ? u[c] : v[r - 1][c];
+          const double lfv = c == 0 ? lf[r] : v[r][c - 1];
+          nw_cell(dgv, upv, lfv, oc[4 * r + c], p, v[r][c], kc[r][c]);
+        }
+      }
+      uint32_t codes = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) codes |= kc[r][c] << (8 * c + 2 * r);
+      dgn = u[3];  // C[i0][4g+4]: the next block's above-left cell
+      l0 = v[0][3];
+      l1 = v[1][3];
+      l2 = v[2][3];
+      l3 = v[3][3];
+      b0 = v[3][0];
+      b1 = v[3][1];
+      b2 = v[3][2];
+      b3 = v[3][3];
+      const bool act = lane_on && (unsigned)g < (unsigned)ngroups;
+      if (act) dirs[(int64_t)g * WARP] = codes;
+      const int cmax = m - 4 * g;  // >= 4 except in the last group
+      if (act && pub_lane) {
+        double* dst = bnd_me + 4 * g;
+        st_relaxed_f64(dst, b0);
+        if (cmax > 1) st_relaxed_f64(dst + 1, b1);
+        if (cmax > 2) st_relaxed_f64(dst + 2, b2);
+        if (cmax > 3) st_relaxed_f64(dst + 3, b3);
+        NW_PROF(if ((g & 7) == 7 && it < 16 && (g >> 3) < 256) g_nw_chunk[it][g >> 3][2] = gtimer();)
+      }
+      if (act && lane == cost_lane && g == ngroups - 1) {
+        // cell (n-1, m-1): row n-1-i0 of the block, column cmax-1
+        const int r = n - 1 - i0;
+        double row[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          row[c] = r == 0 ? v[0][c] : r == 1 ? v[1][c] : r == 2 ? v[2][c] : v[3][c];
+        a.cost[d] = cmax == 1 ? row[0] : cmax == 2 ? row[1] : cmax == 3 ? row[2] : row[3];
+      }
+    };
+    const int steps = ngroups + nl - 1;
+#pragma unroll 1
+    for (int t = 0; t < steps; t += 2) {
+      step(t, oA, oB);
+      step(t + 1, oB, oA);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
@@ -556,100 +535,206 @@ int nw_resident_warps() {
 }
 
 // ---------------------------------------------------------------------------
-// K4: traceback over the 2-bit codes (tie order D > GS > GT is baked into the
+// K4: path walks over the 2-bit codes (tie order D > GS > GT is baked into the
 // codes; borders walk GS on column 0 and GT on row 0, aligner.py:176-206).
-// One thread per document; codes are read through L1 with the next group to
-// the left prefetched.
+// One warp per document. The walk is inherently serial, so the warp's job is
+// to keep its inputs close: codes are staged in shared-memory windows of one
+// band x 32 groups (128 x 128 cells, 4 KB, contiguous in the dirs layout); the
+// windows to the left and above are prefetched with cp.async while the
+// current one is walked, and a code word (4x4 cells) stays in a register while
+// the path is inside it. All lanes run the walk in lockstep (uniform control
+// flow); per-cell work that needs memory (S, gold keys) is batched 32 cells at
+// a time and done lane-parallel.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t band_code(const uint32_t* dirs, int ncg, int i, int j) {
-  const int band = i / kBandRows;
-  const int li = i - band * kBandRows;
-  const uint32_t wv = __ldg(dirs + ((int64_t)band * ncg + (j >> 2)) * WARP + (li >> 2));
-  return (wv >> (8 * (j & 3) + 2 * (li & 3))) & 3u;
+constexpr int kWalkWarps = 4;                        // documents per CTA
+constexpr int kWinWords = 32 * WARP;                 // 32 groups x 32 row-quads
+constexpr int kWalkSmem = kWalkWarps * 3 * kWinWords * 4;  // 48 KB
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
 
-__global__ void traceback_kernel(const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
-                                 const int32_t* __restrict__ nn, const int32_t* __restrict__ mm,
-                                 int n_docs, const int64_t* __restrict__ mv_off, int8_t* mv_op,
-                                 int32_t* mv_i, int32_t* mv_j, int32_t* mv_len) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+// Stage window (band, w) of a document's codes into buf (one commit group).
+__device__ __forceinline__ void win_load(uint32_t* buf, const uint32_t* dd, int nbands, int ngroups,
+                                         int band, int w, int lane) {
+  if (band >= 0 && w >= 0 && band < nbands) {
+    const uint32_t* base = dd + ((int64_t)band * ngroups + w * 32) * WARP + lane;
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + lane);
+    const int gl = min(32, ngroups - w * 32);
+    for (int q = 0; q < gl; ++q) cp_async4(dst + q * WARP * 4, base + q * WARP);
+  }
+  cp_async_commit();
+}
+
+// Walk the path of one document from (n, m) towards (0, 0), calling
+// visit(op, i, j) for every interior move (0-based cell (i, j)) with all lanes
+// converged; returns the position where the path reaches a border.
+template <class Visit>
+__device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int n, int m, int lane,
+                                          Visit&& visit) {
+  const int ngroups = (m + 3) >> 2;
+  const int nbands = (n + kBandRows - 1) / kBandRows;
+  int i = n, j = m;
+  if (i == 0 || j == 0) return make_int2(i, j);
+  int cur = 0, fl = 1, fu = 2;  // buffer roles: current, left prefetch, up prefetch
+  int cb = (i - 1) / kBandRows, cw = (j - 1) >> 7;
+  win_load(win + cur * kWinWords, dd, nbands, ngroups, cb, cw, lane);
+  win_load(win + fl * kWinWords, dd, nbands, ngroups, cb, cw - 1, lane);
+  win_load(win + fu * kWinWords, dd, nbands, ngroups, cb - 1, cw, lane);
+  asm volatile("cp.async.wait_group 2;" ::: "memory");
+  __syncwarp();
+  int wkey = -1;
+  uint32_t word = 0;
+  while (i > 0 && j > 0) {
+    const int li = i - 1, lj = j - 1;
+    const int b = li / kBandRows, w = lj >> 7;
+    if (b != cb || w != cw) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+      int nb;
+      if (b == cb && w == cw - 1) {
+        nb = fl;
+      } else if (b == cb - 1 && w == cw) {
+        nb = fu;
+      } else {  // diagonal exit through the corner: fetch it now
+        nb = fl;
+        win_load(win + nb * kWinWords, dd, nbands, ngroups, b, w, lane);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+      }
+      const int f1 = nb == fl ? fu : fl;  // the two free buffers
+      const int f2 = cur;
+      cur = nb;
+      fl = f1;
+      fu = f2;
+      cb = b;
+      cw = w;
+      win_load(win + fl * kWinWords, dd, nbands, ngroups, cb, cw - 1, lane);
+      win_load(win + fu * kWinWords, dd, nbands, ngroups, cb - 1, cw, lane);
+      wkey = -1;
+    }
+    const int key = (((lj >> 2) & 31) << 5) | ((li & (kBandRows - 1)) >> 2);
+    if (key != wkey) {
+      word = win[cur * kWinWords + key];
+      wkey = key;
+    }
+    const int op = (int)((word >> (8 * (lj & 3) + 2 * (li & 3))) & 3u);
+    visit(op, li, lj);
+    i -= op != BM_MOVE_GT;
+    j -= op != BM_MOVE_GS;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  return make_int2(i, j);
+}
+
+__global__ void __launch_bounds__(kWalkWarps * WARP) traceback_kernel(
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+    const int32_t* __restrict__ nn, const int32_t* __restrict__ mm, int n_docs,
+    const int64_t* __restrict__ mv_off, int8_t* mv_op, int32_t* mv_i, int32_t* mv_j,
+    int32_t* mv_len) {
+  extern __shared__ __align__(16) uint32_t walk_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int d = blockIdx.x * kWalkWarps + wid;
   if (d >= n_docs) return;
+  uint32_t* win = walk_smem + wid * 3 * kWinWords;
   const int n = nn[d], m = mm[d];
-  const int ncg = (m + kBandCols - 1) / kBandCols;
-  const uint32_t* dd = dirs + dir_off[d];
   const int64_t base = mv_off[d];
-  int i = n, j = m, k = 0;
-  while (i > 0 || j > 0) {
-    int op;
-    if (i > 0 && j > 0)
-      op = (int)band_code(dd, ncg, i - 1, j - 1);
-    else
-      op = i > 0 ? BM_MOVE_GS : BM_MOVE_GT;
-    mv_op[base + k] = (int8_t)op;
-    mv_i[base + k] = op == BM_MOVE_GT ? -1 : i - 1;
-    mv_j[base + k] = op == BM_MOVE_GS ? -1 : j - 1;
+  int k = 0;
+  const int2 e = warp_walk(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
+    if (lane == 0) {
+      mv_op[base + k] = (int8_t)op;
+      mv_i[base + k] = op == BM_MOVE_GT ? -1 : i;
+      mv_j[base + k] = op == BM_MOVE_GS ? -1 : j;
+    }
     ++k;
-    if (op == BM_MOVE_D) {
-      --i;
-      --j;
-    } else if (op == BM_MOVE_GS) {
-      --i;
+  });
+  // border runs: GS down column 0, or GT along row 0 (lane-parallel)
+  const int run = e.x > 0 ? e.x : e.y;
+  for (int q = lane; q < run; q += WARP) {
+    const int64_t o = base + k + q;
+    if (e.x > 0) {
+      mv_op[o] = (int8_t)BM_MOVE_GS;
+      mv_i[o] = e.x - 1 - q;
+      mv_j[o] = -1;
     } else {
-      --j;
+      mv_op[o] = (int8_t)BM_MOVE_GT;
+      mv_i[o] = -1;
+      mv_j[o] = e.y - 1 - q;
     }
   }
-  mv_len[d] = k;  // moves are stored in reverse path order
+  if (lane == 0) mv_len[d] = k + run;  // moves are stored in reverse path order
 }
 
 cudaError_t launch_traceback(const uint32_t* dirs, const int64_t* dir_off, const int32_t* n,
                              const int32_t* m, int n_docs, const int64_t* mv_off, int8_t* op,
                              int32_t* mi, int32_t* mj, int32_t* len, cudaStream_t st) {
   if (n_docs == 0) return cudaSuccess;
-  traceback_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, n, m, n_docs, mv_off, op,
-                                                          mi, mj, len);
+  cudaError_t e = cudaFuncSetAttribute(traceback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kWalkSmem);
+  if (e != cudaSuccess) return e;
+  traceback_kernel<<<(n_docs + kWalkWarps - 1) / kWalkWarps, kWalkWarps * WARP, kWalkSmem, st>>>(
+      dirs, dir_off, n, m, n_docs, mv_off, op, mi, mj, len);
   return counted(cudaGetLastError());
 }
 
-__global__ void extract_kernel(const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
-                               const double* __restrict__ S, const int64_t* __restrict__ s_off,
-                               const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
-                               const int32_t* __restrict__ mm, int n_docs, double threshold,
-                               const int64_t* __restrict__ rec_off, bm_record* rec,
-                               int32_t* rec_count) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+// Records of one document, filled back to front while walking (the walk runs
+// from the end of the path); 32 diagonal cells are gathered per batch.
+__global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+    const double* __restrict__ S, const int64_t* __restrict__ s_off,
+    const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
+    const int32_t* __restrict__ mm, int n_docs, double threshold,
+    const int64_t* __restrict__ rec_off, bm_record* rec, int32_t* rec_count) {
+  extern __shared__ __align__(16) uint32_t walk_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int d = blockIdx.x * kWalkWarps + wid;
   if (d >= n_docs) return;
+  uint32_t* win = walk_smem + wid * 3 * kWinWords;
   const int n = nn[d], m = mm[d];
-  const int ncg = (m + kBandCols - 1) / kBandCols;
-  const uint32_t* dd = dirs + dir_off[d];
   const double* Sd = S + s_off[d];
   const int64_t ld = pitch[d];
   const int cap = min(n, m);
   bm_record* out = rec + rec_off[d];
-  int i = n, j = m, k = 0;
-  while (i > 0 && j > 0) {
-    const uint32_t op = band_code(dd, ncg, i - 1, j - 1);
-    if (op == BM_MOVE_D) {
-      const double c = Sd[(int64_t)(i - 1) * ld + (j - 1)];
-      if (c >= threshold) {
-        ++k;
-        bm_record r;
-        r.doc = d;
-        r.i = i - 1;
-        r.j = j - 1;
-        r.pad = 0;
-        r.conf = c;
-        out[cap - k] = r;  // filled back to front
-      }
-      --i;
-      --j;
-    } else if (op == BM_MOVE_GS) {
-      --i;
-    } else {
-      --j;
+  int nd = 0, kept = 0, ci = 0, cj = 0;
+  auto flush = [&](int valid) {
+    const bool have = lane < valid;
+    const double c = have ? Sd[(int64_t)ci * ld + cj] : 0.0;
+    const bool keep = have && c >= threshold;
+    const unsigned mask = __ballot_sync(kFull, keep);
+    if (keep) {
+      const int rank = __popc(mask & ((1u << lane) - 1u));
+      bm_record r;
+      r.doc = d;
+      r.i = ci;
+      r.j = cj;
+      r.pad = 0;
+      r.conf = c;
+      out[cap - 1 - (kept + rank)] = r;
     }
+    kept += __popc(mask);
+  };
+  warp_walk(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
+    if (op == BM_MOVE_D) {
+      if (lane == (nd & 31)) {
+        ci = i;
+        cj = j;
+      }
+      if ((++nd & 31) == 0) flush(32);
+    }
+  });
+  if (nd & 31) flush(nd & 31);
+  __syncwarp();
+  // move the kept records to the front, in chunks of 32 (source >= target)
+  for (int q0 = 0; q0 < kept; q0 += WARP) {
+    const int q = q0 + lane;
+    bm_record r;
+    if (q < kept) r = out[cap - kept + q];
+    __syncwarp();
+    if (q < kept) out[q] = r;
+    __syncwarp();
   }
-  for (int q = 0; q < k; ++q) out[q] = out[cap - k + q];
-  rec_count[d] = k;
+  if (lane == 0) rec_count[d] = kept;
 }
 
 cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const double* S,
@@ -657,8 +742,11 @@ cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const d
                            const int32_t* m, int n_docs, double thr, const int64_t* rec_off,
                            bm_record* rec, int32_t* cnt, cudaStream_t st) {
   if (n_docs == 0) return cudaSuccess;
-  extract_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, S, s_off, pitch, n, m, n_docs,
-                                                        thr, rec_off, rec, cnt);
+  cudaError_t e = cudaFuncSetAttribute(extract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kWalkSmem);
+  if (e != cudaSuccess) return e;
+  extract_kernel<<<(n_docs + kWalkWarps - 1) / kWalkWarps, kWalkWarps * WARP, kWalkSmem, st>>>(
+      dirs, dir_off, S, s_off, pitch, n, m, n_docs, thr, rec_off, rec, cnt);
   return counted(cudaGetLastError());
 }
 
@@ -691,64 +779,78 @@ int fused_rows_per_lane(int n) {
 
 // ---------------------------------------------------------------------------
 // K5: per-(penalty, threshold) prediction and gold-hit counts of one penalty.
-// One thread per document walks its path; a warp reduces before the atomics.
+// One warp per document walks its path (warp_walk); each batch of 32 diagonal
+// cells is scored lane-parallel (S gather + binary search in the document's
+// sorted gold keys), and every threshold is counted with two ballots. Lane l
+// owns the counters of thresholds l and l + 32.
 // ---------------------------------------------------------------------------
 constexpr int kMaxThr = 64;
 
-__global__ void tune_count_kernel(const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
-                                  const double* __restrict__ S, const int64_t* __restrict__ s_off,
-                                  const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
-                                  const int32_t* __restrict__ mm, int n_docs,
-                                  const double* __restrict__ thr, int n_thr,
-                                  const int64_t* __restrict__ gold,
-                                  const int64_t* __restrict__ gold_off, unsigned long long* pred,
-                                  unsigned long long* hit) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t cp[kMaxThr], ch[kMaxThr];
-  for (int l = 0; l < n_thr; ++l) cp[l] = ch[l] = 0;
-  if (d < n_docs) {
-    const int n = nn[d], m = mm[d];
-    const int ncg = (m + kBandCols - 1) / kBandCols;
-    const uint32_t* dd = dirs + dir_off[d];
-    const double* Sd = S + s_off[d];
-    const int64_t ld = pitch[d];
-    const int64_t g0 = gold_off[d], g1 = gold_off[d + 1];
-    int i = n, j = m;
-    while (i > 0 && j > 0) {
-      const uint32_t op = band_code(dd, ncg, i - 1, j - 1);
-      if (op == BM_MOVE_D) {
-        const double c = Sd[(int64_t)(i - 1) * ld + (j - 1)];
-        const int64_t key = (int64_t)(i - 1) * m + (j - 1);
-        int64_t lo = g0, hi = g1;
-        while (lo < hi) {
-          int64_t mid = (lo + hi) >> 1;
-          if (gold[mid] < key)
-            lo = mid + 1;
-          else
-            hi = mid;
-        }
-        const uint32_t g = (lo < g1 && gold[lo] == key) ? 1u : 0u;
-        for (int l = 0; l < n_thr; ++l) {
-          const uint32_t ok = c >= thr[l] ? 1u : 0u;
-          cp[l] += ok;
-          ch[l] += ok & g;
-        }
-        --i;
-        --j;
-      } else if (op == BM_MOVE_GS) {
-        --i;
-      } else {
-        --j;
+__global__ void __launch_bounds__(kWalkWarps * WARP) tune_count_kernel(
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+    const double* __restrict__ S, const int64_t* __restrict__ s_off,
+    const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
+    const int32_t* __restrict__ mm, int n_docs, const double* __restrict__ thr, int n_thr,
+    const int64_t* __restrict__ gold, const int64_t* __restrict__ gold_off,
+    unsigned long long* pred, unsigned long long* hit) {
+  extern __shared__ __align__(16) uint32_t walk_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int d = blockIdx.x * kWalkWarps + wid;
+  if (d >= n_docs) return;
+  uint32_t* win = walk_smem + wid * 3 * kWinWords;
+  const int n = nn[d], m = mm[d];
+  const double* Sd = S + s_off[d];
+  const int64_t ld = pitch[d];
+  const int64_t g0 = gold_off[d], g1 = gold_off[d + 1];
+  uint32_t p_lo = 0, p_hi = 0, h_lo = 0, h_hi = 0;
+  int nd = 0, ci = 0, cj = 0;
+  auto flush = [&](int valid) {
+    const bool have = lane < valid;
+    double c = 0.0;
+    bool g = false;
+    if (have) {
+      c = Sd[(int64_t)ci * ld + cj];
+      const int64_t key = (int64_t)ci * m + cj;
+      int64_t lo = g0, hi = g1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (gold[mid] < key)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      g = lo < g1 && gold[lo] == key;
+    }
+    for (int l = 0; l < n_thr; ++l) {
+      const bool ok = have && c >= thr[l];
+      const uint32_t np = __popc(__ballot_sync(kFull, ok));
+      const uint32_t nh = __popc(__ballot_sync(kFull, ok && g));
+      if (l == lane) {
+        p_lo += np;
+        h_lo += nh;
+      } else if (l == lane + 32) {
+        p_hi += np;
+        h_hi += nh;
       }
     }
-  }
-  for (int l = 0; l < n_thr; ++l) {
-    const uint32_t sp = __reduce_add_sync(0xffffffffu, cp[l]);
-    const uint32_t sh = __reduce_add_sync(0xffffffffu, ch[l]);
-    if ((threadIdx.x & 31) == 0) {
-      if (sp) atomicAdd(pred + l, (unsigned long long)sp);
-      if (sh) atomicAdd(hit + l, (unsigned long long)sh);
+  };
+  warp_walk(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
+    if (op == BM_MOVE_D) {
+      if (lane == (nd & 31)) {
+        ci = i;
+        cj = j;
+      }
+      if ((++nd & 31) == 0) flush(32);
     }
+  });
+  if (nd & 31) flush(nd & 31);
+  if (lane < n_thr) {
+    if (p_lo) atomicAdd(pred + lane, (unsigned long long)p_lo);
+    if (h_lo) atomicAdd(hit + lane, (unsigned long long)h_lo);
+  }
+  if (lane + 32 < n_thr) {
+    if (p_hi) atomicAdd(pred + lane + 32, (unsigned long long)p_hi);
+    if (h_hi) atomicAdd(hit + lane + 32, (unsigned long long)h_hi);
   }
 }
 
@@ -759,9 +861,11 @@ cudaError_t launch_tune_count(const uint32_t* dirs, const int64_t* dir_off, cons
                               unsigned long long* pred, unsigned long long* hit, cudaStream_t st) {
   if (n_docs == 0) return cudaSuccess;
   if (n_thr > kMaxThr) return cudaErrorInvalidValue;
-  tune_count_kernel<<<(n_docs + 127) / 128, 128, 0, st>>>(dirs, dir_off, S, s_off, pitch, n, m,
-                                                           n_docs, thr, n_thr, gold, gold_off, pred,
-                                                           hit);
+  cudaError_t e = cudaFuncSetAttribute(tune_count_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem);
+  if (e != cudaSuccess) return e;
+  tune_count_kernel<<<(n_docs + kWalkWarps - 1) / kWalkWarps, kWalkWarps * WARP, kWalkSmem, st>>>(
+      dirs, dir_off, S, s_off, pitch, n, m, n_docs, thr, n_thr, gold, gold_off, pred, hit);
   return counted(cudaGetLastError());
 }
 
