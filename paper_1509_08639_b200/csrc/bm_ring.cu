@@ -6,29 +6,33 @@
 //                     88-105) into dense per-cell coverage hit counts, written
 //                     to HBM scratch (2 B/cell). High occupancy hides the
 //                     dependent lexicon lookups.
-//   mine_ring_kernel  one CTA (4 warps) per document. The document's hit
+//   mine_ring_kernel  one CTA (5 warps) per document. The document's hit
 //                     counts arrive in shared memory by one TMA bulk copy
-//                     (cp.async.bulk + mbarrier complete_tx). Warps 1-3
-//                     (producers) score exactly the cells the DP wavefront
-//                     needs, in wavefront-step order, into a shared-memory ring
-//                     of (1 - S) values; warp 0 runs the lane-skewed
-//                     anti-diagonal DP over the ring (full/empty mbarriers per
-//                     block of kGroup steps). Thread 0 then walks the 2-bit
-//                     codes (tie order D > GS > GT) and all threads re-score
-//                     the diagonal cells of the path, threshold them and
-//                     compact them in path order.
+//                     (cp.async.bulk + mbarrier complete_tx). Warps 1-4
+//                     (producers) score the R x 4 lane blocks the DP needs,
+//                     super-step by super-step, as 32-cell tasks dealt
+//                     round-robin, into a 4-slot shared-memory ring of
+//                     (1 - S); warp 0 runs the blocked wavefront DP of
+//                     nw_band_kernel over it (full/empty mbarriers per slot,
+//                     waits suspend in hardware). Thread 0 then walks the
+//                     2-bit codes (tie order D > GS > GT) and all threads
+//                     re-score the diagonal cells of the path, threshold them
+//                     and compact them in path order.
 // The similarity matrix never exists in memory; every value is computed with
 // the same operation order as bm_kernels.cu (bit-identical to the reference).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "bm_kernels.cuh"
 
 namespace bm {
 
-constexpr int kRingThreads = 128;
-constexpr int kProducers = kRingThreads - WARP;
-constexpr int kGroup = 8;  // wavefront steps per mbarrier block
+constexpr int kProdWarps = 4;
+constexpr int kRingThreads = (kProdWarps + 1) * WARP;  // warp 0: DP, warps 1..4: scoring
+constexpr int kProducers = kProdWarps * WARP;
+constexpr int kSlots = 4;  // ring depth in super-steps
 constexpr int kFixedBytes = kExpTableWords * 8 + 256;
 constexpr int kHitsThreads = 64;
 
@@ -77,37 +81,35 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Ring of (1 - S) values: at least two mbarrier blocks of kGroup steps.
-// Same as mbar_wait but sleeps between polls: the DP warp idles on the
-// producers and must not steal their issue slots.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+// Waits that suspend the thread in hardware (try_wait with a suspend-time
+// hint) until the phase completes, instead of polling: a warp stalled on its
+// partner must not take issue slots from the other CTAs on the SM.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
-  for (;;) {
+  do {
     asm volatile(
-        "{\n .reg .pred P1;\n mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
         " selp.u32 %0, 1, 0, P1;\n}\n"
         : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
         : "memory");
-    if (done) return;
-    __nanosleep(64);
-  }
+  } while (!done);
 }
 
-__host__ __device__ constexpr int ring_bytes(int R) {
-  return (2 * kGroup * WARP * R * 8) > 16384 ? 2 * kGroup * WARP * R * 8 : 16384;
-}
-__host__ __device__ constexpr int ring_depth(int R) { return ring_bytes(R) / (WARP * R * 8); }
+__host__ __device__ constexpr int ring_lane(int R) { return R * 4 + 2; }
+__host__ __device__ constexpr int ring_slot_doubles(int R) { return WARP * ring_lane(R); }
+__host__ __device__ constexpr int ring_bytes(int R) { return kSlots * ring_slot_doubles(R) * 8; }
+// 2-bit codes of one lane block (R rows x 4 columns, bit 2*(c*R + r))
+__host__ __device__ constexpr int code_bytes(int R) { return R == 8 ? 8 : 4; }
 
 __host__ __device__ inline size_t hits_bytes(int n, int m) { return align16(((size_t)n * m + 1) / 2 * 4); }
 
 // Per-document shared memory of the ring kernel (must match the carve below).
 __host__ __device__ inline size_t ring_var_bytes(int n, int m, int R) {
-  const int cpw = 16 / R;
   size_t b = hits_bytes(n, m);
-  b += (size_t)(n + m) * 16;                                   // SPack per sentence
-  b += align16((size_t)((m + cpw - 1) / cpw) * WARP * 4);      // direction codes
-  b += align16((size_t)(n < m ? n : m) * 4);                   // path diagonal cells
+  b += (size_t)(n + m) * 16;                                         // SPack per sentence
+  b += align16((size_t)((m + 3) / 4) * WARP * code_bytes(R));        // direction codes
+  b += align16((size_t)(n < m ? n : m) * 4);                         // path diagonal cells
   return b;
 }
 
@@ -187,30 +189,25 @@ __device__ __forceinline__ double staged_score(const bm_sentences& S, const Mode
   return bmexp::confidence_from_z(margin(M, f), exp_tab);
 }
 
-// Valid (lane, row) slots of wavefront step s: lanes max(0, s-m+1) ..
-// min(nl-1, s), R rows each.
-__device__ __forceinline__ int step_slots(int s, int steps, int m, int nl, int R) {
-  if (s >= steps) return 0;
-  const int L0 = max(0, s - (m - 1));
-  const int L1 = min(nl - 1, s);
-  return (L1 - L0 + 1) * R;
+// Lanes of the DP warp active at super-step t (lane L works on column group
+// t - L): [L0, L1], empty when L0 > L1.
+__device__ __forceinline__ int2 active_lanes(int t, int ngroups, int nl) {
+  return make_int2(max(0, t - ngroups + 1), min(nl - 1, t));
 }
 
 template <int R>
-__global__ void __launch_bounds__(kRingThreads, 5) mine_ring_kernel(FusedArgs a) {
-  constexpr int K = ring_depth(R);  // ring depth in steps
-  constexpr int NB = K / kGroup;    // mbarrier blocks in the ring
-  constexpr int CPW = 16 / R;       // columns per direction word
-  static_assert(NB >= 2, "ring too shallow");
+__global__ void __launch_bounds__(kRingThreads, 4) mine_ring_kernel(FusedArgs a) {
+  using CodeT = typename std::conditional<R == 8, uint64_t, uint32_t>::type;
+  constexpr int RL = ring_lane(R);
+  constexpr int BPT = 8 / R;  // lane blocks per 32-cell scoring task
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const unsigned FULL = 0xffffffffu;
   const bm_sentences& S = a.S;
 
   uint64_t* exp_tab = (uint64_t*)smem;
   uint64_t* bar_full = (uint64_t*)(smem + kExpTableWords * 8);
-  uint64_t* bar_empty = bar_full + NB;
-  uint64_t* bar_load = bar_empty + NB;
+  uint64_t* bar_empty = bar_full + kSlots;
+  uint64_t* bar_load = bar_empty + kSlots;
   int* misc = (int*)(bar_load + 1);
   double* ring = (double*)(smem + kFixedBytes);
   uint8_t* var = smem + kFixedBytes + ring_bytes(R);
@@ -221,15 +218,15 @@ __global__ void __launch_bounds__(kRingThreads, 5) mine_ring_kernel(FusedArgs a)
     const int n = a.D.n[doc], m = a.D.m[doc];
     const int s0 = a.D.src0[doc], t0 = a.D.tgt0[doc];
     const double p = a.p;
-    const int ncg = (m + CPW - 1) / CPW;
+    const int ngroups = (m + 3) >> 2;
     uint32_t* hits = (uint32_t*)var;
     SPack* sp = (SPack*)(var + hits_bytes(n, m));
-    uint32_t* dirs = (uint32_t*)((uint8_t*)sp + (size_t)(n + m) * 16);
-    int32_t* dlist = (int32_t*)((uint8_t*)dirs + align16((size_t)ncg * WARP * 4));
+    CodeT* dirs = (CodeT*)((uint8_t*)sp + (size_t)(n + m) * 16);
+    int32_t* dlist = (int32_t*)((uint8_t*)dirs + align16((size_t)ngroups * WARP * sizeof(CodeT)));
 
     __syncthreads();  // the previous document is done with every buffer
     if (tid == 0) {
-      for (int q = 0; q < NB; ++q) {
+      for (int q = 0; q < kSlots; ++q) {
         mbar_init(bar_full + q, kProducers);
         mbar_init(bar_empty + q, 1);
       }
@@ -254,125 +251,117 @@ __global__ void __launch_bounds__(kRingThreads, 5) mine_ring_kernel(FusedArgs a)
     mbar_wait(bar_load, 0);
 
     const int nl = (n + R - 1) / R;
-    const int steps = m + nl - 1;
-    const int nblocks = (steps + kGroup - 1) / kGroup;
+    const int steps = ngroups + nl - 1;
 
     if (warp == 0) {
       // ------------------------------------------------------------ DP warp
+      // blocked wavefront (see nw_band_kernel): lane L owns rows RL..RL+R-1
+      // and at super-step t computes the R x 4 block of column group t - L
       const int i0 = lane * R;
-      const int my_rows = lane < nl ? min(R, n - i0) : 0;
-      double left[R];
+      const bool lane_on = lane < nl;
+      double lf[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) left[r] = (double)(i0 + r + 1) * p;
-      double bot = 0.0;
+      for (int r = 0; r < R; ++r) lf[r] = (double)(i0 + r + 1) * p;
+      double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+      double dgn = (double)i0 * p;
+      const int cost_lane = (n - 1) / R;
+      for (int t = 0; t < steps; ++t) {
+        const int g = t - lane;
+        double u[4];
+        u[0] = __shfl_up_sync(kFull, b0, 1);
+        u[1] = __shfl_up_sync(kFull, b1, 1);
+        u[2] = __shfl_up_sync(kFull, b2, 1);
+        u[3] = __shfl_up_sync(kFull, b3, 1);
+        if (lane == 0) {  // row 0 border C[0][j] = j * p
+          u[0] = (double)(4 * g + 1) * p;
+          u[1] = (double)(4 * g + 2) * p;
+          u[2] = (double)(4 * g + 3) * p;
+          u[3] = (double)(4 * g + 4) * p;
+          dgn = (double)(4 * g) * p;
+        }
+        mbar_wait_backoff(bar_full + (t % kSlots), (uint32_t)((t / kSlots) & 1));
+        const bool act = lane_on && (unsigned)g < (unsigned)ngroups;
+        if (act) {
+          const double* om = ring + (size_t)(t % kSlots) * ring_slot_doubles(R) + lane * RL;
+          double v[R][4];
+          CodeT codes = 0;
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (r == my_rows - 1) bot = left[r];
-      double prev_recv = (double)i0 * p;
-      uint32_t dword = 0;
-      for (int b = 0; b < nblocks; ++b) {
-        mbar_wait_sleep(bar_full + (b % NB), (uint32_t)((b / NB) & 1));
-        const int s_end = min(steps, (b + 1) * kGroup);
-        for (int s = b * kGroup; s < s_end; ++s) {
-          const int j = s - lane;
-          const double recv = __shfl_up_sync(FULL, bot, 1);
-          double up, dg;
-          if (lane == 0) {
-            up = (double)(j + 1) * p;
-            dg = (double)j * p;
-          } else {
-            up = recv;
-            dg = prev_recv;
-          }
-          prev_recv = recv;
-          if (lane < nl && j >= 0 && j < m) {
-            const double* om = ring + ((size_t)(s % K) * WARP + lane) * R;
-            double omv[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) omv[r] = om[r];
-            uint32_t codes = 0;
+          for (int dd = 0; dd < R + 3; ++dd) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              if (r < my_rows) {
-                const double dcand = __dadd_rn(dg, omv[r]);
-                const double lcand = __dadd_rn(left[r], p);
-                // min(d, u, l) with the reference's comparison semantics; l is
-                // folded in first because it does not depend on the row above
-                double best = dcand;
-                if (lcand < best) best = lcand;
-                const double ucand = __dadd_rn(up, p);
-                if (ucand < best) best = ucand;
-                const uint32_t code = best == dcand ? 0u : (best == ucand ? 1u : 2u);
-                codes |= code << (2 * r);
-                dg = left[r];
-                left[r] = best;
-                up = best;
-                bot = best;  // the last valid row of the lane ends the chain
-              }
-            }
-            const int slot = j % CPW;
-            dword |= codes << (2 * R * slot);
-            if (slot == CPW - 1 || j == m - 1) {
-              dirs[(j / CPW) * WARP + lane] = dword;
-              dword = 0;
+              const int c = dd - r;
+              if (c < 0 || c > 3) continue;
+              const double dgv = r == 0 ? (c == 0 ? dgn : u[c - 1]) : (c == 0 ? lf[r - 1] : v[r - 1][c - 1]);
+              const double upv = r == 0 ? u[c] : v[r - 1][c];
+              const double lfv = c == 0 ? lf[r] : v[r][c - 1];
+              uint32_t kc;
+              nw_cell(dgv, upv, lfv, om[r * 4 + c], p, v[r][c], kc);
+              codes |= (CodeT)kc << (2 * (c * R + r));
             }
           }
+          dirs[g * WARP + lane] = codes;
+          if (lane == cost_lane && g == ngroups - 1) {
+            const int r = n - 1 - i0, c = m - 1 - 4 * g;
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc)
+                if (rr == r && cc == c) a.cost[doc] = v[rr][cc];
+          }
+          dgn = u[3];
+#pragma unroll
+          for (int r = 0; r < R; ++r) lf[r] = v[r][3];
+          b0 = v[R - 1][0];
+          b1 = v[R - 1][1];
+          b2 = v[R - 1][2];
+          b3 = v[R - 1][3];
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_empty + (b % NB));
-      }
-      if (lane == (n - 1) / R) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (i0 + r == n - 1) a.cost[doc] = left[r];
+        if (lane == 0) mbar_arrive(bar_empty + (t % kSlots));
       }
     } else {
       // ------------------------------------------------------ score warps
-      const int ptid = tid - WARP;
-      for (int b = 0; b < nblocks; ++b) {
-        if (b >= NB) mbar_wait(bar_empty + (b % NB), (uint32_t)(((b / NB) - 1) & 1));
-        const int s_end = min(steps, (b + 1) * kGroup);
-        // walk this thread's slots (stride kProducers over the concatenated
-        // valid slots of the block's steps); the step state (s, first valid
-        // lane L0, slot count) only changes when the walk crosses a step
-        int s = b * kGroup, rem = ptid;
-        int L0 = max(0, s - (m - 1));
-        int cnt = step_slots(s, steps, m, nl, R);
-        while (s < s_end && rem >= cnt) {
-          rem -= cnt;
-          ++s;
-          L0 = max(0, s - (m - 1));
-          cnt = step_slots(s, steps, m, nl, R);
-        }
-        while (s < s_end) {
-          const int L = L0 + rem / R;
-          const int r = rem % R;
-          const int i = L * R + r;
-          if (i < n) {
-            const int j = s - L;
-            const uint32_t hv = ((const uint16_t*)hits)[i * m + j];
+      // tasks: 32 cells = BPT lane blocks of one super-step; the tasks of all
+      // super-steps form one sequence and producer warp w takes every 4th
+      // (w, w + 4, ...), which balances the ragged fill/drain super-steps.
+      // Rows/columns past the matrix are skipped (never read by the DP).
+      static_assert(kProdWarps == 4, "task striding assumes 4 producer warps");
+      const int pw = warp - 1;
+      const int tb = lane / (4 * R), r = (lane >> 2) % R, c = lane & 3;
+      const int toff = tb * RL + r * 4 + c;
+      const uint16_t* hits16 = (const uint16_t*)hits;
+      int q0 = 0;  // sequence index of super-step t's first task
+      for (int t = 0; t < steps; ++t) {
+        if (t >= kSlots) mbar_wait_backoff(bar_empty + (t % kSlots), (uint32_t)(((t / kSlots) - 1) & 1));
+        const int2 la = active_lanes(t, ngroups, nl);
+        const int ntask = (la.y - la.x + BPT) / BPT;
+        double* slot = ring + (size_t)(t % kSlots) * ring_slot_doubles(R) + la.x * RL + toff;
+        for (int kt = (pw - q0) & 3; kt < ntask; kt += kProdWarps) {
+          const int L = la.x + kt * BPT + tb;
+          const int i = L * R + r, j = 4 * (t - L) + c;
+          if (L <= la.y && i < n && j < m) {
+            const uint32_t hv = hits16[i * m + j];
             const double sv = staged_score(S, a.M, exp_tab, a.tabs, sp[i], sp[n + j], hv & 0xff, hv >> 8);
-            ring[((s % K) * WARP + L) * R + r] = __dsub_rn(1.0, sv);
-          }
-          rem += kProducers;
-          while (rem >= cnt && s < s_end) {
-            rem -= cnt;
-            ++s;
-            L0 = max(0, s - (m - 1));
-            cnt = step_slots(s, steps, m, nl, R);
+            slot[kt * (BPT * RL)] = __dsub_rn(1.0, sv);
           }
         }
-        mbar_arrive(bar_full + (b % NB));
+        q0 += ntask;
+        mbar_arrive(bar_full + (t % kSlots));
       }
     }
     __syncthreads();  // DP complete: direction codes final
 
     if (tid == 0) {
-      int k = 0, i = n, j = m;
+      int k = 0, i = n, j = m, wkey = -1;
+      CodeT wv = 0;
       while (i > 0 && j > 0) {
         const int ci = i - 1, cj = j - 1;
-        const uint32_t wv = dirs[(cj / CPW) * WARP + ci / R];
-        const uint32_t op = (wv >> (2 * R * (cj % CPW) + 2 * (ci % R))) & 3u;
+        const int key = (cj >> 2) * WARP + ci / R;
+        if (key != wkey) {  // the path stays inside a R x 4 block for a few moves
+          wv = dirs[key];
+          wkey = key;
+        }
+        const uint32_t op = (uint32_t)(wv >> (2 * ((cj & 3) * R + ci % R))) & 3u;
         if (op == BM_MOVE_D) {
           dlist[k++] = ci * m + cj;
           --i;
@@ -404,24 +393,24 @@ __global__ void __launch_bounds__(kRingThreads, 5) mine_ring_kernel(FusedArgs a)
         sv = staged_score(S, a.M, exp_tab, a.tabs, sp[ci], sp[n + cj], hv & 0xff, hv >> 8);
         keep = sv >= a.threshold;
       }
-      const unsigned mask = __ballot_sync(FULL, keep);
+      const unsigned mask = __ballot_sync(kFull, keep);
       if (lane == 0) misc[4 + warp] = __popc(mask);
       __syncthreads();
       int before = 0, chunk = 0;
 #pragma unroll
       for (int w = 0; w < kRingThreads / WARP; ++w) {
-        const int c = misc[4 + w];
-        before += w < warp ? c : 0;
-        chunk += c;
+        const int cw = misc[4 + w];
+        before += w < warp ? cw : 0;
+        chunk += cw;
       }
       if (keep) {
-        bm_record r;
-        r.doc = doc;
-        r.i = ci;
-        r.j = cj;
-        r.pad = 0;
-        r.conf = sv;
-        out[base + before + __popc(mask & ((1u << lane) - 1u))] = r;
+        bm_record rec;
+        rec.doc = doc;
+        rec.i = ci;
+        rec.j = cj;
+        rec.pad = 0;
+        rec.conf = sv;
+        out[base + before + __popc(mask & ((1u << lane) - 1u))] = rec;
       }
       base += chunk;
       __syncthreads();  // misc reused by the next chunk

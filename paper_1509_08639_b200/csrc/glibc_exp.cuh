@@ -104,17 +104,31 @@ BM_HD double special(double tmp, uint64_t sbits, uint64_t ki) {
   return mul_(y, 0x1p-1022);
 }
 
+#if defined(__CUDACC__)
+// Device copies of the polynomial constants: read from the constant bank they
+// are direct DFMA operands instead of being rebuilt in registers per call.
+__constant__ double c_exp_k[8] = {0x1.71547652b82fep7,  0x1.8p52,
+                                  -0x1.62e42fefa0000p-8, -0x1.cf79abc9e3b3ap-47,
+                                  0x1.ffffffffffdbdp-2,  0x1.555555555543cp-3,
+                                  0x1.55555cf172b91p-5,  0x1.1111167a4d017p-7};
+#endif
+#if defined(__CUDA_ARCH__)
+#define BM_EXPK(i, lit) c_exp_k[i]
+#else
+#define BM_EXPK(i, lit) (lit)
+#endif
+
 // T: the 256-entry table (glibc_exp_table.h); on the GPU it is staged in
 // shared memory because lanes index it divergently.
 BM_HD double exp_glibc(double x, const uint64_t* T) {
-  const double InvLn2N = 0x1.71547652b82fep7;
-  const double Shift = 0x1.8p52;
-  const double NegLn2hiN = -0x1.62e42fefa0000p-8;
-  const double NegLn2loN = -0x1.cf79abc9e3b3ap-47;
-  const double C2 = 0x1.ffffffffffdbdp-2;
-  const double C3 = 0x1.555555555543cp-3;
-  const double C4 = 0x1.55555cf172b91p-5;
-  const double C5 = 0x1.1111167a4d017p-7;
+  const double InvLn2N = BM_EXPK(0, 0x1.71547652b82fep7);
+  const double Shift = BM_EXPK(1, 0x1.8p52);
+  const double NegLn2hiN = BM_EXPK(2, -0x1.62e42fefa0000p-8);
+  const double NegLn2loN = BM_EXPK(3, -0x1.cf79abc9e3b3ap-47);
+  const double C2 = BM_EXPK(4, 0x1.ffffffffffdbdp-2);
+  const double C3 = BM_EXPK(5, 0x1.555555555543cp-3);
+  const double C4 = BM_EXPK(6, 0x1.55555cf172b91p-5);
+  const double C5 = BM_EXPK(7, 0x1.1111167a4d017p-7);
 
   uint32_t abstop = (uint32_t)(asu64(x) >> 52) & 0x7ffu;
   if (abstop - 0x3c9u >= 0x3fu) {
