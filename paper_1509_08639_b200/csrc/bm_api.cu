@@ -502,6 +502,21 @@ cudaStream_t copy_stream() {
   return s;
 }
 
+// Second compute stream of the calling thread: bm_mine_host alternates chunks
+// between the caller's stream and this one so a chunk's kernel tails overlap
+// the next chunk's kernels.
+cudaStream_t side_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  static thread_local int dev_of = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (s == nullptr || dev_of != dev) {
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    dev_of = dev;
+  }
+  return s;
+}
+
 // Host source of a streamed batch: either the plain bm_sentences arrays or the
 // compact wire format (narrow types, widened on the device per chunk).
 struct HostSource {
@@ -601,18 +616,20 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   bm_record *rec = nullptr, *dense = nullptr;
   int32_t* cnt = nullptr;
   double* cost = nullptr;
-  int64_t* total = nullptr;
   BM_CK(sc.alloc(&droff, nd), "alloc");
   BM_CK(sc.alloc(&rec, (size_t)rt), "alloc");
   BM_CK(sc.alloc(&dense, (size_t)rt), "alloc");
   BM_CK(sc.alloc(&cnt, nd), "alloc");
   BM_CK(sc.alloc(&cost, nd), "alloc");
+  int64_t* total = nullptr;
   BM_CK(sc.alloc(&total, 1), "alloc");
   // the copy stream may only touch the scratch once it is allocated on st
   cudaEvent_t ready;
   BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
   BM_CK(cudaEventRecord(ready, st), "event");
   BM_CK(cudaStreamWaitEvent(cs, ready, 0), "event");
+  cudaStream_t s2 = side_stream();
+  BM_CK(cudaStreamWaitEvent(s2, ready, 0), "event");
   auto h2d = [&](void* dst, const void* from, size_t bytes) -> cudaError_t {
     return bytes ? cudaMemcpyAsync(dst, from, bytes, cudaMemcpyHostToDevice, cs) : cudaSuccess;
   };
@@ -630,12 +647,21 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   // copy stream, mine it on the compute stream once its copy event fired
   const int64_t kChunkCells = 16ll << 20;
   std::vector<cudaEvent_t> evs;
+  // BM_TRACE: GPU timeline (copy done / mined per chunk, relative to t_start)
+  std::vector<cudaEvent_t> tl_copy, tl_mine;
+  cudaEvent_t tl0 = nullptr;
+  if (tr.on) {
+    cudaEventCreate(&tl0);
+    cudaEventRecord(tl0, cs);
+  }
   int d0 = 0;
   while (d0 < nd) {
     int d1 = d0;
     int64_t cells = 0;
     int lo = ns, hi = 0;
-    while (d1 < nd && (d1 == d0 || cells < kChunkCells)) {
+    // a small first chunk starts the GPU early; later chunks amortise launches
+    const int64_t want = evs.empty() ? kChunkCells / 4 : kChunkCells;
+    while (d1 < nd && (d1 == d0 || cells < want)) {
       cells += (int64_t)dh->n[d1] * dh->m[d1];
       if (dh->n[d1] > 0) {
         lo = std::min(lo, dh->src0[d1]);
@@ -669,16 +695,30 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
         BM_CK(h2d(w_id + e0, w->tok_id + e0, (size_t)(e1 - e0) * 2), "h2d");
         BM_CK(h2d(w_al + e0, w->tok_alpha + e0, (size_t)(e1 - e0)), "h2d");
         BM_CK(h2d(w_dg + g0, w->dig_id + g0, (size_t)(g1 - g0) * 2), "h2d");
-        BM_CK(launch_unpack_wire(w_t, w_p, w_a, w_id, w_al, w_dg, lo, hi, e0, e1, g0, g1, a0, a1,
-                                 a2, a4, a7, a6, cs),
-              "unpack_wire_kernel");
       }
     }
     cudaEvent_t ev;
     BM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
     BM_CK(cudaEventRecord(ev, cs), "event");
     evs.push_back(ev);
-    BM_CK(cudaStreamWaitEvent(st, ev, 0), "event");
+    if (tr.on) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, cs);
+      tl_copy.push_back(e);
+    }
+    cudaStream_t sk = (evs.size() & 1) ? st : s2;  // chunk 0 on s2, 1 on st, ...
+    BM_CK(cudaStreamWaitEvent(sk, ev, 0), "event");
+    // the copy stream only moves bytes: widening the wire arrays is a few
+    // microseconds of compute and runs in order on the compute stream (on the
+    // copy stream it would queue behind the mining CTAs and stall the DMA)
+    if (src.wire && hi > lo) {
+      const int64_t e0 = src.tok_off[lo], e1 = src.tok_off[hi];
+      const int64_t g0 = src.dig_off[lo], g1 = src.dig_off[hi];
+      BM_CK(launch_unpack_wire(w_t, w_p, w_a, w_id, w_al, w_dg, lo, hi, e0, e1, g0, g1, a0, a1,
+                               a2, a4, a7, a6, sk),
+            "unpack_wire_kernel");
+    }
     bm_docs dc = dd;
     dc.n_docs = d1 - d0;
     dc.src0 = b0 + d0;
@@ -686,12 +726,24 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     dc.tgt0 = b2 + d0;
     dc.m = b3 + d0;
     int rc = bm_mine(&sd, &dc, dh->n + d0, dh->m + d0, amax.data() + d0, &ld, model, threshold,
-                     penalty, droff + d0, rec, cnt + d0, cost + d0, stream);
+                     penalty, droff + d0, rec, cnt + d0, cost + d0, sk);
     if (rc) return rc;
+    if (tr.on) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, sk);
+      tl_mine.push_back(e);
+    }
     d0 = d1;
   }
+  // join the side stream back into the caller's stream
+  cudaEvent_t joined;
+  BM_CK(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming), "event");
+  BM_CK(cudaEventRecord(joined, s2), "event");
+  BM_CK(cudaStreamWaitEvent(st, joined, 0), "event");
+  evs.push_back(joined);
   tr.mark("chunks enqueued");
-  int rc = bm_compact(rec, droff, cnt, nd, dense, total, stream);
+  int rc = bm_compact(rec, droff, cnt, nd, dense, total, st);
   if (rc) return rc;
   int64_t tot = 0;
   BM_CK(cudaMemcpyAsync(&tot, total, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "d2h");
@@ -702,6 +754,17 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   if (tot) BM_CK(cudaMemcpyAsync(rec_out, dense, tot * sizeof(bm_record), cudaMemcpyDeviceToHost, st), "d2h");
   BM_CK(cudaStreamSynchronize(st), "sync");
   tr.mark("records d2h");
+  if (tr.on) {
+    for (size_t q = 0; q < tl_copy.size(); ++q) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, tl0, tl_copy[q]);
+      cudaEventElapsedTime(&b, tl0, tl_mine[q]);
+      fprintf(stderr, "[bm trace] gpu chunk %2zu copied %8.3f ms  mined %8.3f ms\n", q, a, b);
+      cudaEventDestroy(tl_copy[q]);
+      cudaEventDestroy(tl_mine[q]);
+    }
+    cudaEventDestroy(tl0);
+  }
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
   cudaEventDestroy(ready);
   *n_rec = tot;

@@ -106,7 +106,9 @@ def mine_pinned(pb: PinnedBatch, model, threshold: float, penalty: float, stream
 
 
 def mine_host(corpus: PackedCorpus, plex: PackedLexicon, model, threshold: float, penalty: float,
-              wire: bool = False):
-    pb = PinnedBatch(corpus, plex, pin=False, wire=wire)
+              wire: bool = False, pin: bool = False):
+    """One call with host buffers; pin=True stages them page-locked (records are
+    then written by the GPU straight into the pinned output buffer)."""
+    pb = PinnedBatch(corpus, plex, pin=pin, wire=wire)
     recs, k, _ = mine_pinned(pb, model, threshold, penalty)
     return recs.copy(), pb.cost[: pb.n_docs].copy()

@@ -293,19 +293,37 @@ def test_synth_text_round_trip_same_records():
     assert a.tobytes() == b.tobytes()
 
 
-@pytest.mark.parametrize("wire", [False, True])
-def test_mine_host_entry_point_matches_device_path(oracle_mod, wire):
-    """bm_mine_host / bm_mine_host_wire (host buffers in, records out) == oracle."""
+@pytest.mark.parametrize("wire,pin", [(False, False), (True, False), (True, True), (False, True)])
+def test_mine_host_entry_point_matches_device_path(oracle_mod, wire, pin):
+    """bm_mine_host / bm_mine_host_wire (host buffers in, records out) == oracle,
+    from pageable and from page-locked host buffers."""
     from paper_1509_08639_b200 import hostapi, synth
 
     sc = synth.make_corpus(*synth.c2_shape(3000), seed=11)  # several streamed chunks
     model = bm.load_model(golden("model5k_fwd.json"))
     plex = sc.world.packed_lexicon()
     assert hostapi.wire_ok(sc.packed, plex)
-    recs, cost = hostapi.mine_host(sc.packed, plex, model, 0.5, 0.2, wire=wire)
+    recs, cost = hostapi.mine_host(sc.packed, plex, model, 0.5, 0.2, wire=wire, pin=pin)
     want, wcost = oracle_mod.mine(oracle_mod.HostBatch(sc.packed, plex), model, 0.5, 0.2, threads=16)
     assert recs.tobytes() == want.tobytes()
     assert np.array_equal(bits(cost), bits(wcost))
+
+
+@pytest.mark.parametrize("pin", [False, True])
+def test_mine_host_record_buffer_too_small(pin):
+    """A record buffer smaller than the result fails with BM_ELIMIT (no overrun)."""
+    from paper_1509_08639_b200 import hostapi, synth
+
+    sc = synth.make_corpus(*synth.c2_shape(400), seed=13)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    pb = hostapi.PinnedBatch(sc.packed, sc.world.packed_lexicon(), pin=pin, wire=True)
+    _, k, _ = hostapi.mine_pinned(pb, model, 0.5, 0.2)
+    assert k > 10
+    pb.rec_cap = k - 1
+    guard = pb.rec[k - 1:].copy()
+    with pytest.raises(bm.ResourceLimitError):
+        hostapi.mine_pinned(pb, model, 0.5, 0.2)
+    assert pb.rec[k - 1:].tobytes() == guard.tobytes()
 
 
 # ---------------------------------------------------------------- tuning
