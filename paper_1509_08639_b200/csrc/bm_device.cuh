@@ -276,20 +276,6 @@ __device__ void join_direction(G g, const bm_sentences& S, const int32_t* off,
   }
 }
 
-// Sentence (local index) owning entry e: the largest k with off[k] <= e, over
-// the side's staged offsets off[0..nsent].
-__device__ __forceinline__ int owner_of(const int32_t* off, int nsent, int e) {
-  int lo = 0, hi = nsent - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= e)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;
-}
-
 // Entry-parallel form of join_direction: every loop runs over token entries
 // (coalesced loads, all lanes busy) instead of over sentences. offA / offB are
 // the two sides' tok_off slices staged in shared memory (na+1 / nb+1 ints).
@@ -297,7 +283,7 @@ template <class G, class AddFn>
 __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t* off,
                                        const int32_t* cand, const int32_t* offA, int na,
                                        const int32_t* offB, int b0, int nb, JoinSmem& js,
-                                       uint16_t* chunk_owner, AddFn add) {
+                                       uint16_t* chunk_owner, uint16_t* a_owner, AddFn add) {
   const int eA0 = offA[0], eA1 = offA[na];
   const int eB0 = offB[0], eB1 = offB[nb];
   for (int c0 = eB0; c0 < eB1; c0 += js.emax) {
@@ -341,33 +327,63 @@ __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t
       js.owner[slot] = chunk_owner[e - c0];
     }
     g.sync();
-    for (int e = eA0 + g.rank(); e < eA1; e += g.size()) {
-      const int w = __ldg(S.tok_alpha + e);
-      if (w == 0) continue;
-      const int32_t id = __ldg(S.tok_id + e);
-      const int q0 = __ldg(off + id), q1 = __ldg(off + id + 1);
-      int la = -1;
-      for (int q = q0; q < q1; ++q) {
-        const int32_t c = __ldg(cand + q);
-        const uint32_t bk = bucket_of(c, js.bshift);
-        for (int slot = js.bstart[bk]; slot < js.bstart[bk + 1]; ++slot) {
-          if (js.key[slot] != c) continue;
-          const int lb = js.owner[slot];
-          // an entry hits a sentence once however many candidates it holds
-          bool dup = false;
-          if (q > q0) {
-            const int u0 = __ldg(S.tok_off + b0 + lb);
-            const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
-            for (int qq = q0; qq < q && !dup; ++qq) dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
-          }
-          if (!dup) {
-            if (la < 0) la = owner_of(offA, na, e);
-            add(la, lb, w);
+    // probe side in chunks of emax entries, each with an owner table (a
+    // per-entry binary search over the offsets cost more than the probes)
+    for (int a0 = eA0; a0 < eA1; a0 += js.emax) {
+      const int a1 = min(eA1, a0 + js.emax);
+      for (int k = g.rank(); k < na; k += g.size()) {
+        const int e0 = max(a0, offA[k]), e1 = min(a1, offA[k + 1]);
+        for (int e = e0; e < e1; ++e) a_owner[e - a0] = (uint16_t)k;
+      }
+      g.sync();
+      // kBatch entries per thread at a time: each level of the dependent
+      // lookups (entry -> lexicon offsets -> first candidate) is issued for
+      // all of them before any is used, so their latencies overlap
+#ifndef BM_HITS_BATCH
+#define BM_HITS_BATCH 4
+#endif
+      constexpr int kBatch = BM_HITS_BATCH;
+      for (int eb = a0 + g.rank(); eb < a1; eb += kBatch * g.size()) {
+        int wv[kBatch], idv[kBatch], q0v[kBatch], q1v[kBatch], lav[kBatch], c0v[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int e = eb + u * g.size();
+          const bool ok = e < a1;
+          wv[u] = ok ? __ldg(S.tok_alpha + e) : 0;
+          idv[u] = ok ? __ldg(S.tok_id + e) : 0;
+          lav[u] = ok ? a_owner[e - a0] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          q0v[u] = wv[u] ? __ldg(off + idv[u]) : 0;
+          q1v[u] = wv[u] ? __ldg(off + idv[u] + 1) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) c0v[u] = q0v[u] < q1v[u] ? __ldg(cand + q0v[u]) : 0;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int w = wv[u], la = lav[u], q0 = q0v[u], q1 = q1v[u];
+          for (int q = q0; q < q1; ++q) {
+            const int32_t c = q == q0 ? c0v[u] : __ldg(cand + q);
+            const uint32_t bk = bucket_of(c, js.bshift);
+            const int s1 = js.bstart[bk + 1];
+            for (int slot = js.bstart[bk]; slot < s1; ++slot) {
+              if (js.key[slot] != c) continue;
+              const int lb = js.owner[slot];
+              // an entry hits a sentence once however many candidates it holds
+              bool dup = false;
+              if (q > q0) {
+                const int u0 = __ldg(S.tok_off + b0 + lb);
+                const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
+                for (int qq = q0; qq < q && !dup; ++qq) dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
+              }
+              if (!dup) add(la, lb, w);
+            }
           }
         }
       }
+      g.sync();
     }
-    g.sync();
   }
 }
 
@@ -376,7 +392,7 @@ template <bool kPacked16, class G>
 __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& L, int s0,
                                   int ns, int t0, int nt, const int32_t* offS,
                                   const int32_t* offT, uint32_t* hits, JoinSmem& js,
-                                  uint16_t* chunk_owner, bool zero_hits = true) {
+                                  uint16_t* chunk_owner, uint16_t* a_owner, bool zero_hits = true) {
   const int ncell = ns * nt;
   const int nwords = kPacked16 ? (ncell + 1) / 2 : ncell;
   if (zero_hits) {
@@ -384,7 +400,7 @@ __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& 
     g.sync();
   }
   join_direction_entries(g, S, L.fwd_off, L.fwd_cand, offS, ns, offT, t0, nt, js, chunk_owner,
-                         [&](int ls, int lt, int w) {
+                         a_owner, [&](int ls, int lt, int w) {
                            int cell = ls * nt + lt;
                            if (kPacked16)
                              atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16));
@@ -392,7 +408,7 @@ __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& 
                              atomicAdd(&hits[cell], (uint32_t)w);
                          });
   join_direction_entries(g, S, L.rev_off, L.rev_cand, offT, nt, offS, s0, ns, js, chunk_owner,
-                         [&](int lt, int ls, int w) {
+                         a_owner, [&](int lt, int ls, int w) {
                            int cell = ls * nt + lt;
                            if (kPacked16)
                              atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16 + 8));

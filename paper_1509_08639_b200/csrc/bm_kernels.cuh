@@ -14,7 +14,12 @@ namespace bm {
 constexpr int kTile = 64;              // 64 x 64 cells per CTA
 constexpr int kTileThreads = 256;
 constexpr int kJoinEmax = 1024;        // bucketed ids per join chunk
-constexpr int kJoinBuckets = 512;
+#ifndef BM_JOIN_BUCKETS
+#define BM_JOIN_BUCKETS 512
+#endif
+constexpr int kJoinBuckets = BM_JOIN_BUCKETS;
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+static_assert((kJoinBuckets & (kJoinBuckets - 1)) == 0, "bucket count must be a power of two");
 
 // Banded NW (K2/K3): 4 rows per lane, 128 rows per warp band.
 constexpr int kBandR = 4;
@@ -54,7 +59,7 @@ __device__ __forceinline__ JoinSmem carve_join(uint8_t* p) {
   js.owner = (uint16_t*)p;
   js.emax = kJoinEmax;
   js.nbuckets = kJoinBuckets;
-  js.bshift = 32 - 9;  // log2(512)
+  js.bshift = 32 - ilog2(kJoinBuckets);
   return js;
 }
 

@@ -34,7 +34,10 @@ constexpr int kRingThreads = (kProdWarps + 1) * WARP;  // warp 0: DP, warps 1..4
 constexpr int kProducers = kProdWarps * WARP;
 constexpr int kSlots = 4;  // ring depth in super-steps
 constexpr int kFixedBytes = kExpTableWords * 8 + 256;
-constexpr int kHitsThreads = 64;
+#ifndef BM_HITS_THREADS
+#define BM_HITS_THREADS 64
+#endif
+constexpr int kHitsThreads = BM_HITS_THREADS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -118,7 +121,7 @@ size_t ring_slice_bytes(int n, int m, int R) {
 }
 
 size_t hits_kernel_smem(int n, int m) {
-  return align16(join_smem_bytes()) + align16((size_t)(n + m + 2) * 4) + (size_t)kJoinEmax * 2;
+  return align16(join_smem_bytes()) + align16((size_t)(n + m + 2) * 4) + (size_t)kJoinEmax * 4;
 }
 
 // ---------------------------------------------------------------------------
@@ -139,6 +142,7 @@ __global__ void __launch_bounds__(kHitsThreads, 8) hits_kernel(bm_sentences S, b
   int32_t* offS = (int32_t*)(smem + align16(join_smem_bytes()));
   int32_t* offT = offS + n + 1;
   uint16_t* chunk_owner = (uint16_t*)((uint8_t*)offS + align16((size_t)(n + m + 2) * 4));
+  uint16_t* a_owner = chunk_owner + kJoinEmax;
   const int s0 = D.src0[doc], t0 = D.tgt0[doc];
   for (int k = threadIdx.x; k <= n + m + 1; k += blockDim.x) {
     if (k <= n)
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(kHitsThreads, 8) hits_kernel(bm_sentences S, b
   }
   __syncthreads();
   uint32_t* hits = (uint32_t*)(hits_out + hit_off[doc]);
-  tile_join_entries<true>(CtaGroup(), S, L, s0, n, t0, m, offS, offT, hits, js, chunk_owner,
+  tile_join_entries<true>(CtaGroup(), S, L, s0, n, t0, m, offS, offT, hits, js, chunk_owner, a_owner,
                           /*zero_hits=*/false);
 }
 
