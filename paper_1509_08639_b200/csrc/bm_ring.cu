@@ -100,8 +100,12 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) 
 }
 
 __host__ __device__ constexpr int ring_lane(int R) { return R * 4 + 2; }
-__host__ __device__ constexpr int ring_slot_doubles(int R) { return WARP * ring_lane(R); }
-__host__ __device__ constexpr int ring_bytes(int R) { return kSlots * ring_slot_doubles(R) * 8; }
+// slots hold only the document's nl active DP lanes (smem decides how many
+// CTAs share an SM)
+__host__ __device__ constexpr int ring_slot_doubles(int R, int nl) { return nl * ring_lane(R); }
+__host__ __device__ inline size_t ring_bytes(int R, int nl) {
+  return align16((size_t)kSlots * ring_slot_doubles(R, nl) * 8);
+}
 // 2-bit codes of one lane block (R rows x 4 columns, bit 2*(c*R + r))
 __host__ __device__ constexpr int code_bytes(int R) { return R == 8 ? 8 : 4; }
 
@@ -117,7 +121,7 @@ __host__ __device__ inline size_t ring_var_bytes(int n, int m, int R) {
 }
 
 size_t ring_slice_bytes(int n, int m, int R) {
-  return kFixedBytes + ring_bytes(R) + ring_var_bytes(n, m, R);
+  return kFixedBytes + ring_bytes(R, (n + R - 1) / R) + ring_var_bytes(n, m, R);
 }
 
 size_t hits_kernel_smem(int n, int m) {
@@ -199,8 +203,10 @@ __device__ __forceinline__ int2 active_lanes(int t, int ngroups, int nl) {
   return make_int2(max(0, t - ngroups + 1), min(nl - 1, t));
 }
 
+// 5 CTAs per SM (smem slices of C2-shaped documents fit 5); R = 8 blocks need
+// the registers of 4
 template <int R>
-__global__ void __launch_bounds__(kRingThreads, 4) mine_ring_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel(FusedArgs a) {
   using CodeT = typename std::conditional<R == 8, uint64_t, uint32_t>::type;
   constexpr int RL = ring_lane(R);
   constexpr int BPT = 8 / R;  // lane blocks per 32-cell scoring task
@@ -214,7 +220,6 @@ __global__ void __launch_bounds__(kRingThreads, 4) mine_ring_kernel(FusedArgs a)
   uint64_t* bar_load = bar_empty + kSlots;
   int* misc = (int*)(bar_load + 1);
   double* ring = (double*)(smem + kFixedBytes);
-  uint8_t* var = smem + kFixedBytes + ring_bytes(R);
   stage_exp_table(exp_tab, tid, kRingThreads);
 
   for (int item = blockIdx.x; item < a.n_list; item += gridDim.x) {
@@ -223,6 +228,9 @@ __global__ void __launch_bounds__(kRingThreads, 4) mine_ring_kernel(FusedArgs a)
     const int s0 = a.D.src0[doc], t0 = a.D.tgt0[doc];
     const double p = a.p;
     const int ngroups = (m + 3) >> 2;
+    const int nl = (n + R - 1) / R;
+    const int slot_d = ring_slot_doubles(R, nl);
+    uint8_t* var = smem + kFixedBytes + ring_bytes(R, nl);
     uint32_t* hits = (uint32_t*)var;
     SPack* sp = (SPack*)(var + hits_bytes(n, m));
     CodeT* dirs = (CodeT*)((uint8_t*)sp + (size_t)(n + m) * 16);
@@ -254,7 +262,6 @@ __global__ void __launch_bounds__(kRingThreads, 4) mine_ring_kernel(FusedArgs a)
     __syncthreads();
     mbar_wait(bar_load, 0);
 
-    const int nl = (n + R - 1) / R;
     const int steps = ngroups + nl - 1;
 
     if (warp == 0) {
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(kRingThreads, 4) mine_ring_kernel(FusedArgs a)
         mbar_wait_backoff(bar_full + (t % kSlots), (uint32_t)((t / kSlots) & 1));
         const bool act = lane_on && (unsigned)g < (unsigned)ngroups;
         if (act) {
-          const double* om = ring + (size_t)(t % kSlots) * ring_slot_doubles(R) + lane * RL;
+          const double* om = ring + (size_t)(t % kSlots) * slot_d + lane * RL;
           double v[R][4];
           CodeT codes = 0;
 #pragma unroll
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(kRingThreads, 4) mine_ring_kernel(FusedArgs a)
         if (t >= kSlots) mbar_wait_backoff(bar_empty + (t % kSlots), (uint32_t)(((t / kSlots) - 1) & 1));
         const int2 la = active_lanes(t, ngroups, nl);
         const int ntask = (la.y - la.x + BPT) / BPT;
-        double* slot = ring + (size_t)(t % kSlots) * ring_slot_doubles(R) + la.x * RL + toff;
+        double* slot = ring + (size_t)(t % kSlots) * slot_d + la.x * RL + toff;
         for (int kt = (pw - q0) & 3; kt < ntask; kt += kProdWarps) {
           const int L = la.x + kt * BPT + tb;
           const int i = L * R + r, j = 4 * (t - L) + c;
