@@ -302,7 +302,7 @@ def run_ours(args):
         "n_tok", "n_punct", "n_alpha", "tok_off", "tok_id", "tok_alpha", "dig_off", "dig_id")))
     alg_bytes = 8 * cells + in_bytes + 24 * n_rec
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    traffic, traffic_src = measured_traffic()
+    traffic, traffic_src, compute_util = measured_traffic()
     fp64 = fp64_roof(lib, torch, dev, stream)
 
     # end to end through the C ABI with host buffers (pinned)
@@ -346,6 +346,7 @@ def run_ours(args):
                 "kernel_ms": kern_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)",
             },
             "fp64": fp64,
+            "compute_utilisation": compute_util,
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": pb.h2d_bytes,
                     "d2h_bytes_per_step": d2h[0],
@@ -386,18 +387,29 @@ def kernel_ms(lib, dc, view, dl, mstruct, n_h, m_h, amax, rec_off_d, rec, cnt, c
 
 def measured_traffic():
     """DRAM bytes of one C2 bm_mine launch pair from the committed ncu capture
-    (profiles/, dram__bytes_read.sum + dram__bytes_write.sum)."""
-    prof = sorted(p for p in os.listdir(os.path.join(ROOT, "profiles"))
-                  if p.endswith("_ncu_raw_metrics.json")) if os.path.isdir(os.path.join(ROOT, "profiles")) else []
-    if not prof:
-        return None, None
-    d = json.load(open(os.path.join(ROOT, "profiles", prof[-1])))
-    tot = 0.0
-    for k in ("hits_kernel", "mine_ring_kernel<4>"):
-        if k not in d:
-            return None, None
-        tot += float(d[k]["dram__bytes_read.sum"]) + float(d[k]["dram__bytes_write.sum"])
-    return tot * 1e6, f"profiles/{prof[-1]} (ncu --set full, MB -> bytes)"
+    (profiles/, dram__bytes_read.sum + dram__bytes_write.sum), and the ring
+    kernel's measured issue / FP64-pipe utilisation from the same capture."""
+    pdir = os.path.join(ROOT, "profiles")
+    prof = sorted(p for p in os.listdir(pdir) if p.endswith("_ncu_raw_metrics.json")) \
+        if os.path.isdir(pdir) else []
+    for name in reversed(prof):
+        d = json.load(open(os.path.join(pdir, name)))
+        if not all(k in d for k in ("hits_kernel", "mine_ring_kernel<4>")):
+            continue
+        tot = 0.0
+        for k in ("hits_kernel", "mine_ring_kernel<4>"):
+            tot += float(d[k]["dram__bytes_read.sum"]) + float(d[k]["dram__bytes_write.sum"])
+        ring = d["mine_ring_kernel<4>"]
+        util = {
+            "kernel": "mine_ring_kernel<4>",
+            "issue_slots_busy_pct": ring.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe_active_pct": ring.get(
+                "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "stall_share": ring.get("stall_share"),
+            "source": f"profiles/{name}",
+        }
+        return tot * 1e6, f"profiles/{name} (ncu --set full, MB -> bytes)", util
+    return None, None, None
 
 
 def fp64_roof(lib, torch, dev, stream):

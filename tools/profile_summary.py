@@ -1,0 +1,85 @@
+"""Summarise ncu --set full captures into profiles/ (text + raw metrics JSON).
+
+Usage: python tools/profile_summary.py OUT_PREFIX TITLE rep1.ncu-rep [rep2 ...]
+Writes OUT_PREFIX_ncu_full_summary.txt and OUT_PREFIX_ncu_raw_metrics.json with
+one entry per profiled kernel (name without namespace/arguments).
+"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+DETAILS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput",
+           "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread",
+           "Dynamic Shared Memory Per Block", "Block Limit Registers", "Block Limit Shared Mem",
+           "Theoretical Active Warps per SM", "Achieved Active Warps Per SM",
+           "Executed Instructions", "No Eligible", "L1/TEX Hit Rate", "L2 Hit Rate", "Grid Size",
+           "Block Size"]
+RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+       "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+       "smsp__issue_active.avg.pct_of_peak_sustained_active",
+       "sm__warps_active.avg.pct_of_peak_sustained_active"]
+STALLS = "smsp__pcsamp_warps_issue_stalled_"
+
+
+def short(name):
+    name = re.sub(r"\(.*$", "", name)
+    name = re.sub(r"^void ", "", name)
+    return name.replace("bm::", "")
+
+
+def ncu(rep, page):
+    out = subprocess.run(["ncu", "-i", rep, "--page", page, "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def main():
+    prefix, title, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    text = [f"# {title}"]
+    raw_all = {}
+    for rep in reps:
+        rows = ncu(rep, "details")
+        h = rows[0]
+        ki, mi, ui, vi = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"),
+                          h.index("Metric Value"))
+        by = {}
+        for r in rows[1:]:
+            by.setdefault(short(r[ki]), {})[r[mi]] = (r[vi], r[ui])
+        raw = ncu(rep, "raw")
+        rh = raw[0]
+        kcol = rh.index("Kernel Name")
+        for r in raw[2:]:
+            k = short(r[kcol])
+            ent = raw_all.setdefault(k, {})
+            stalls = {}
+            for i, name in enumerate(rh):
+                if name in RAW:
+                    ent[name] = float(r[i].replace(",", ""))
+                elif name.startswith(STALLS) and not name.endswith("not_issued"):
+                    try:
+                        v = float(r[i].replace(",", ""))
+                    except ValueError:
+                        continue
+                    if v > 0:
+                        stalls[name[len(STALLS):]] = v
+            tot = sum(stalls.values()) or 1.0
+            ent["stall_share"] = {k2: round(v / tot, 3) for k2, v in
+                                  sorted(stalls.items(), key=lambda x: -x[1])[:8]}
+        for k, d in by.items():
+            text.append(f"## {k}")
+            for name in DETAILS:
+                if name in d:
+                    text.append(f"  {name:34s} {d[name][0]} {d[name][1]}")
+            if k in raw_all and "stall_share" in raw_all[k]:
+                text.append("  stall share (pc sampling)         " +
+                            ", ".join(f"{a} {b:.0%}" for a, b in raw_all[k]["stall_share"].items()))
+    open(prefix + "_ncu_full_summary.txt", "w").write("\n".join(text) + "\n")
+    json.dump(raw_all, open(prefix + "_ncu_raw_metrics.json", "w"), indent=1)
+    print("\n".join(text))
+
+
+if __name__ == "__main__":
+    main()
