@@ -517,6 +517,21 @@ cudaStream_t side_stream() {
   return s;
 }
 
+// Page-locked per-chunk record counts of the calling thread (grown on demand).
+int64_t* pinned_counts(size_t n) {
+  static thread_local int64_t* buf = nullptr;
+  static thread_local size_t cap = 0;
+  if (n > cap) {
+    if (buf) cudaFreeHost(buf);
+    cap = std::max<size_t>(n, 256);
+    if (cudaHostAlloc((void**)&buf, cap * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess) {
+      buf = nullptr;
+      cap = 0;
+    }
+  }
+  return buf;
+}
+
 // Host source of a streamed batch: either the plain bm_sentences arrays or the
 // compact wire format (narrow types, widened on the device per chunk).
 struct HostSource {
@@ -621,8 +636,13 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   BM_CK(sc.alloc(&dense, (size_t)rt), "alloc");
   BM_CK(sc.alloc(&cnt, nd), "alloc");
   BM_CK(sc.alloc(&cost, nd), "alloc");
-  int64_t* total = nullptr;
-  BM_CK(sc.alloc(&total, 1), "alloc");
+  int64_t* doff = nullptr;
+  BM_CK(sc.alloc(&doff, nd), "alloc");
+  // chunk count upper bound: every chunk but the last holds >= 1 document
+  int64_t* ctot = nullptr;
+  BM_CK(sc.alloc(&ctot, nd + 1), "alloc");
+  int64_t* hcnt = pinned_counts((size_t)nd + 1);
+  if (hcnt == nullptr) return fail(BM_ENOMEM, "pinned count buffer");
   // the copy stream may only touch the scratch once it is allocated on st
   cudaEvent_t ready;
   BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
@@ -645,7 +665,11 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   tr.mark("alloc + small h2d");
   // chunks of documents: H2D the sentence range each chunk touches on the
   // copy stream, mine it on the compute stream once its copy event fired
-  const int64_t kChunkCells = 16ll << 20;
+  static const int64_t kChunkCells =
+      getenv("BM_CHUNK_CELLS") ? atoll(getenv("BM_CHUNK_CELLS")) : (16ll << 20);
+  // per chunk: docs [d0, d1), compacted into dense + roff[d0], count -> ctot[k]
+  std::vector<int> ch_d0, ch_d1;
+  std::vector<cudaEvent_t> ch_ev;
   std::vector<cudaEvent_t> evs;
   // BM_TRACE: GPU timeline (copy done / mined per chunk, relative to t_start)
   std::vector<cudaEvent_t> tl_copy, tl_mine;
@@ -728,6 +752,23 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     int rc = bm_mine(&sd, &dc, dh->n + d0, dh->m + d0, amax.data() + d0, &ld, model, threshold,
                      penalty, droff + d0, rec, cnt + d0, cost + d0, sk);
     if (rc) return rc;
+    // compact the chunk into its own region of `dense` (starting at its first
+    // document's record slot) and fetch its record count; the host copies the
+    // records out as soon as the count arrives, overlapping later chunks
+    {
+      const int kq = (int)ch_d0.size();
+      BM_CK(launch_compact(rec, droff + d0, cnt + d0, d1 - d0, doff + d0, ctot + kq,
+                           dense + roff[d0], sk, d0),
+            "compact");
+      BM_CK(cudaMemcpyAsync(hcnt + kq, ctot + kq, sizeof(int64_t), cudaMemcpyDeviceToHost, sk),
+            "d2h");
+      cudaEvent_t ce;
+      BM_CK(cudaEventCreateWithFlags(&ce, cudaEventDisableTiming), "event");
+      BM_CK(cudaEventRecord(ce, sk), "event");
+      ch_d0.push_back(d0);
+      ch_d1.push_back(d1);
+      ch_ev.push_back(ce);
+    }
     if (tr.on) {
       cudaEvent_t e;
       cudaEventCreate(&e);
@@ -743,15 +784,23 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   BM_CK(cudaStreamWaitEvent(st, joined, 0), "event");
   evs.push_back(joined);
   tr.mark("chunks enqueued");
-  int rc = bm_compact(rec, droff, cnt, nd, dense, total, st);
-  if (rc) return rc;
   int64_t tot = 0;
-  BM_CK(cudaMemcpyAsync(&tot, total, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "d2h");
-  if (cost_out) BM_CK(cudaMemcpyAsync(cost_out, cost, nd * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
-  BM_CK(cudaStreamSynchronize(st), "sync");
+  for (size_t q = 0; q < ch_ev.size(); ++q) {
+    BM_CK(cudaEventSynchronize(ch_ev[q]), "sync");
+    const int64_t c = hcnt[q];
+    if (tot + c > rec_cap) {
+      cudaStreamSynchronize(cs);
+      return fail(BM_ELIMIT, "record buffer too small");
+    }
+    if (c) BM_CK(cudaMemcpyAsync(rec_out + tot, dense + roff[ch_d0[q]], c * sizeof(bm_record),
+                                 cudaMemcpyDeviceToHost, cs),
+                 "d2h");
+    tot += c;
+    cudaEventDestroy(ch_ev[q]);
+  }
   tr.mark("mined + compacted");
-  if (tot > rec_cap) return fail(BM_ELIMIT, "record buffer too small");
-  if (tot) BM_CK(cudaMemcpyAsync(rec_out, dense, tot * sizeof(bm_record), cudaMemcpyDeviceToHost, st), "d2h");
+  if (cost_out) BM_CK(cudaMemcpyAsync(cost_out, cost, nd * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+  BM_CK(cudaStreamSynchronize(cs), "sync");
   BM_CK(cudaStreamSynchronize(st), "sync");
   tr.mark("records d2h");
   if (tr.on) {

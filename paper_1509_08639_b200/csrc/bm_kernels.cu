@@ -916,7 +916,7 @@ __global__ void gather_records_kernel(const bm_record* __restrict__ rec,
                                       const int64_t* __restrict__ rec_off,
                                       const int32_t* __restrict__ cnt,
                                       const int64_t* __restrict__ dense_off, int n_docs,
-                                      bm_record* __restrict__ dense) {
+                                      int doc0, bm_record* __restrict__ dense) {
   const int d = blockIdx.x * (blockDim.x / WARP) + threadIdx.x / WARP;
   if (d >= n_docs) return;
   const int lane = threadIdx.x & (WARP - 1);
@@ -924,18 +924,18 @@ __global__ void gather_records_kernel(const bm_record* __restrict__ rec,
   bm_record* dst = dense + dense_off[d];
   for (int k = lane; k < cnt[d]; k += WARP) {
     bm_record r = src[k];
-    r.doc = d;  // document index of the compacted batch
+    r.doc = doc0 + d;  // document index in the caller's batch
     dst[k] = r;
   }
 }
 
 cudaError_t launch_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* cnt,
                            int n_docs, int64_t* dense_off, int64_t* total, bm_record* dense,
-                           cudaStream_t st) {
+                           cudaStream_t st, int doc0) {
   if (n_docs == 0) return cudaMemsetAsync(total, 0, sizeof(int64_t), st);
   scan_counts_kernel<<<1, 1024, 0, st>>>(cnt, n_docs, dense_off, total);
   gather_records_kernel<<<(n_docs + 7) / 8, 256, 0, st>>>(rec, rec_off, cnt, dense_off, n_docs,
-                                                          dense);
+                                                          doc0, dense);
   return counted(cudaGetLastError(), 2);
 }
 

@@ -125,7 +125,7 @@ cudaError_t launch_tune_count(const uint32_t*, const int64_t*, const double*, co
                               int, const int64_t*, const int64_t*, unsigned long long*,
                               unsigned long long*, cudaStream_t);
 cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int, int64_t*,
-                           int64_t*, bm_record*, cudaStream_t);
+                           int64_t*, bm_record*, cudaStream_t, int doc0 = 0);
 size_t score_smem_bytes();
 cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();

@@ -112,8 +112,21 @@ __host__ __device__ constexpr int code_bytes(int R) { return R == 8 ? 8 : 4; }
 __host__ __device__ inline size_t hits_bytes(int n, int m) { return align16(((size_t)n * m + 1) / 2 * 4); }
 
 // Per-document shared memory of the ring kernel (must match the carve below).
+#ifndef BM_RING_SMEM_HITS
+#define BM_RING_SMEM_HITS 1
+#endif
+// hit counts live in shared memory (TMA-staged) or are read from the L2/HBM
+// scratch through the read-only path
+__device__ __forceinline__ uint32_t hit_load(const uint16_t* p) {
+#if BM_RING_SMEM_HITS
+  return *p;
+#else
+  return __ldg(p);
+#endif
+}
+
 __host__ __device__ inline size_t ring_var_bytes(int n, int m, int R) {
-  size_t b = hits_bytes(n, m);
+  size_t b = BM_RING_SMEM_HITS ? hits_bytes(n, m) : 0;
   b += (size_t)(n + m) * 16;                                         // SPack per sentence
   b += align16((size_t)((m + 3) / 4) * WARP * code_bytes(R));        // direction codes
   b += align16((size_t)(n < m ? n : m) * 4);                         // path diagonal cells
@@ -206,7 +219,8 @@ __device__ __forceinline__ int2 active_lanes(int t, int ngroups, int nl) {
 // 5 CTAs per SM (smem slices of C2-shaped documents fit 5); R = 8 blocks need
 // the registers of 4
 template <int R>
-__global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : (BM_RING_SMEM_HITS ? 5 : 6))
+    mine_ring_kernel(FusedArgs a) {
   using CodeT = typename std::conditional<R == 8, uint64_t, uint32_t>::type;
   constexpr int RL = ring_lane(R);
   constexpr int BPT = 8 / R;  // lane blocks per 32-cell scoring task
@@ -231,8 +245,15 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel
     const int nl = (n + R - 1) / R;
     const int slot_d = ring_slot_doubles(R, nl);
     uint8_t* var = smem + kFixedBytes + ring_bytes(R, nl);
+#if BM_RING_SMEM_HITS
     uint32_t* hits = (uint32_t*)var;
     SPack* sp = (SPack*)(var + hits_bytes(n, m));
+    const uint16_t* hits16 = (const uint16_t*)hits;
+#else
+    // hit counts straight from the scratch (2 B per cell, read once; L2)
+    const uint16_t* hits16 = (const uint16_t*)(a.hits + a.hit_off[doc]);
+    SPack* sp = (SPack*)var;
+#endif
     CodeT* dirs = (CodeT*)((uint8_t*)sp + (size_t)(n + m) * 16);
     int32_t* dlist = (int32_t*)((uint8_t*)dirs + align16((size_t)ngroups * WARP * sizeof(CodeT)));
 
@@ -244,9 +265,11 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel
       }
       mbar_init(bar_load, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#if BM_RING_SMEM_HITS
       const uint32_t bytes = (uint32_t)hits_bytes(n, m);
       mbar_arrive_expect_tx(bar_load, bytes);
       bulk_g2s(hits, a.hits + a.hit_off[doc], bytes, bar_load);
+#endif
     }
     // sentences of the document (rows 0..n-1, then columns)
     for (int k = tid; k < n + m; k += kRingThreads) {
@@ -260,7 +283,9 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel
       sp[k] = q;
     }
     __syncthreads();
+#if BM_RING_SMEM_HITS
     mbar_wait(bar_load, 0);
+#endif
 
     const int steps = ngroups + nl - 1;
 
@@ -340,7 +365,6 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel
       const int pw = warp - 1;
       const int tb = lane / (4 * R), r = (lane >> 2) % R, c = lane & 3;
       const int toff = tb * RL + r * 4 + c;
-      const uint16_t* hits16 = (const uint16_t*)hits;
       int q0 = 0;  // sequence index of super-step t's first task
       for (int t = 0; t < steps; ++t) {
         if (t >= kSlots) mbar_wait_backoff(bar_empty + (t % kSlots), (uint32_t)(((t / kSlots) - 1) & 1));
@@ -351,7 +375,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel
           const int L = la.x + kt * BPT + tb;
           const int i = L * R + r, j = 4 * (t - L) + c;
           if (L <= la.y && i < n && j < m) {
-            const uint32_t hv = hits16[i * m + j];
+            const uint32_t hv = hit_load(hits16 + i * m + j);
             const double sv = staged_score(S, a.M, exp_tab, a.tabs, sp[i], sp[n + j], hv & 0xff, hv >> 8);
             slot[kt * (BPT * RL)] = __dsub_rn(1.0, sv);
           }
@@ -400,7 +424,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel
         const int cell = dlist[K_path - 1 - f];
         ci = cell / m;
         cj = cell - ci * m;
-        const uint32_t hv = ((const uint16_t*)hits)[cell];
+        const uint32_t hv = hit_load(hits16 + cell);
         sv = staged_score(S, a.M, exp_tab, a.tabs, sp[ci], sp[n + cj], hv & 0xff, hv >> 8);
         keep = sv >= a.threshold;
       }
