@@ -231,6 +231,50 @@ struct HostTrace {
   }
 };
 
+// Banded tier for the documents of `g` (K1 -> K2/K3 -> K4, then scatter into
+// the caller's per-document record slots).
+int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* docs,
+                 const bm_lexicon* lex, const Model& M, double threshold, double penalty,
+                 const int64_t* rec_off, bm_record* rec, int32_t* rec_count, double* cost,
+                 Scratch& sc, cudaStream_t st) {
+  {
+    const int k = (int)g.docs.size();
+    GeneralDev dv;
+    int rc = general_prepare(g, docs, sc, dv, st);
+    if (rc) return rc;
+    const bm_docs D = local_docs(dv, k);
+    BM_CK(launch_score(*sent, D, *lex, M, dv.tiles, (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S,
+                       st),
+          "score_tile_kernel");
+    double* cost_l = nullptr;
+    BM_CK(sc.alloc(&cost_l, k), "alloc");
+    rc = general_nw(g, dv, penalty, cost_l, st);
+    if (rc) return rc;
+    std::vector<int64_t> roff(k);
+    int64_t rt = 0;
+    for (int q = 0; q < k; ++q) {
+      roff[q] = rt;
+      rt += std::min(g.n[q], g.m[q]);
+    }
+    int64_t* droff = nullptr;
+    bm_record* rl = nullptr;
+    int32_t* cl = nullptr;
+    int32_t* idx = nullptr;
+    BM_CK(sc.upload(&droff, roff), "upload");
+    BM_CK(sc.alloc(&rl, (size_t)rt), "alloc");
+    BM_CK(sc.alloc(&cl, k), "alloc");
+    BM_CK(sc.upload(&idx, g.docs), "upload");
+    BM_CK(launch_extract(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, k, threshold,
+                         droff, rl, cl, st),
+          "extract_kernel");
+    scatter_results_kernel<<<k, 128, 0, st>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
+                                              rec_count);
+    BM_CK(cudaGetLastError(), "scatter_results");
+    note_launch();
+  }
+  return BM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -408,11 +452,13 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   if (hit_total > 0) {
     uint8_t* hits = nullptr;
     int64_t* dho = nullptr;
-    BM_CK(sc.alloc(&hits, (size_t)hit_total), "alloc hits");
-    BM_CK(cudaMemsetAsync(hits, 0, (size_t)hit_total, st), "memset hits");
-    tr.mark("alloc hits");
-    BM_CK(sc.upload(&dho, hit_off), "upload");
-    tr.mark("upload hit_off");
+    if (!BM_RING_FUSED_JOIN) {
+      BM_CK(sc.alloc(&hits, (size_t)hit_total), "alloc hits");
+      BM_CK(cudaMemsetAsync(hits, 0, (size_t)hit_total, st), "memset hits");
+      tr.mark("alloc hits");
+      BM_CK(sc.upload(&dho, hit_off), "upload");
+      tr.mark("upload hit_off");
+    }
     for (int q = 0; q < 4; ++q) {
       if (fused[q].empty()) continue;
       int32_t* list = nullptr;
@@ -434,46 +480,18 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       a.hit_off = dho;
       a.tabs = pair_tables();
       tr.mark("upload list");
-      BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
-      tr.mark("launch hits");
+      if (!BM_RING_FUSED_JOIN) {
+        BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
+        tr.mark("launch hits");
+      }
       BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
       tr.mark("launch ring");
     }
   }
   if (!g.docs.empty()) {
-    const int k = (int)g.docs.size();
-    GeneralDev dv;
-    int rc = general_prepare(g, docs, sc, dv, st);
+    int rc = mine_general(g, sent, docs, lex, M, threshold, penalty, rec_off, rec, rec_count, cost,
+                          sc, st);
     if (rc) return rc;
-    const bm_docs D = local_docs(dv, k);
-    BM_CK(launch_score(*sent, D, *lex, M, dv.tiles, (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S,
-                       st),
-          "score_tile_kernel");
-    double* cost_l = nullptr;
-    BM_CK(sc.alloc(&cost_l, k), "alloc");
-    rc = general_nw(g, dv, penalty, cost_l, st);
-    if (rc) return rc;
-    std::vector<int64_t> roff(k);
-    int64_t rt = 0;
-    for (int q = 0; q < k; ++q) {
-      roff[q] = rt;
-      rt += std::min(g.n[q], g.m[q]);
-    }
-    int64_t* droff = nullptr;
-    bm_record* rl = nullptr;
-    int32_t* cl = nullptr;
-    int32_t* idx = nullptr;
-    BM_CK(sc.upload(&droff, roff), "upload");
-    BM_CK(sc.alloc(&rl, (size_t)rt), "alloc");
-    BM_CK(sc.alloc(&cl, k), "alloc");
-    BM_CK(sc.upload(&idx, g.docs), "upload");
-    BM_CK(launch_extract(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, k, threshold,
-                         droff, rl, cl, st),
-          "extract_kernel");
-    scatter_results_kernel<<<k, 128, 0, st>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
-                                              rec_count);
-    BM_CK(cudaGetLastError(), "scatter_results");
-    note_launch();
   }
   return BM_OK;
 }
@@ -615,6 +633,10 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   BM_CK(sc.alloc(&b1, nd), "alloc");
   BM_CK(sc.alloc(&b2, nd), "alloc");
   BM_CK(sc.alloc(&b3, nd), "alloc");
+  dd.src0 = b0;
+  dd.n = b1;
+  dd.tgt0 = b2;
+  dd.m = b3;
   bm_lexicon ld;
   ld.n_ids = nid;
   int32_t *c0, *c1, *c2, *c3;
@@ -643,6 +665,49 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   BM_CK(sc.alloc(&ctot, nd + 1), "alloc");
   int64_t* hcnt = pinned_counts((size_t)nd + 1);
   if (hcnt == nullptr) return fail(BM_ENOMEM, "pinned count buffer");
+  // route every document once (global indices) and stage the fused tier's
+  // document lists, hit offsets and zeroed hit scratch before the chunk loop,
+  // so a chunk is only kernel launches (no per-chunk host planning or small
+  // uploads queued behind the bulk copies)
+  const Model M = to_model(model);
+  if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
+  std::vector<int32_t> fl[4];
+  size_t fsm[4] = {0, 0, 0, 0}, hsm[4] = {0, 0, 0, 0};
+  std::vector<int64_t> hoff(nd, 0);
+  std::vector<char> banded(nd, 0);
+  int64_t htot = 0;
+  {
+    const char* route = getenv("BM_ROUTE");
+    const bool force_banded = route != nullptr && strcmp(route, "banded") == 0;
+    for (int d = 0; d < nd; ++d) {
+      const int n = dh->n[d], m = dh->m[d];
+      if (n <= 0 || m <= 0) continue;
+      const int R = fused_rows_per_lane(n);
+      const size_t sl = ring_slice_bytes(n, m, R);
+      if (!force_banded && n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax[d] <= 255) {
+        const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
+        fl[q].push_back(d);
+        fsm[q] = std::max(fsm[q], sl);
+        hsm[q] = std::max(hsm[q], hits_kernel_smem(n, m));
+        hoff[d] = htot;
+        htot += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
+      } else {
+        banded[d] = 1;
+      }
+    }
+  }
+  int32_t* dfl[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int q = 0; q < 4; ++q)
+    if (!fl[q].empty()) BM_CK(sc.upload(&dfl[q], fl[q]), "upload");
+  int64_t* dhoff = nullptr;
+  uint8_t* hits = nullptr;
+  if (htot > 0 && !BM_RING_FUSED_JOIN) {
+    BM_CK(sc.upload(&dhoff, hoff), "upload");
+    BM_CK(sc.alloc(&hits, (size_t)htot), "alloc hits");
+    BM_CK(cudaMemsetAsync(hits, 0, (size_t)htot, st), "memset hits");
+  }
+  BM_CK(cudaMemsetAsync(cnt, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
+  const PairTables tabs = pair_tables();
   // the copy stream may only touch the scratch once it is allocated on st
   cudaEvent_t ready;
   BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
@@ -743,15 +808,41 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
                                a2, a4, a7, a6, sk),
             "unpack_wire_kernel");
     }
-    bm_docs dc = dd;
-    dc.n_docs = d1 - d0;
-    dc.src0 = b0 + d0;
-    dc.n = b1 + d0;
-    dc.tgt0 = b2 + d0;
-    dc.m = b3 + d0;
-    int rc = bm_mine(&sd, &dc, dh->n + d0, dh->m + d0, amax.data() + d0, &ld, model, threshold,
-                     penalty, droff + d0, rec, cnt + d0, cost + d0, sk);
-    if (rc) return rc;
+    for (int q = 0; q < 4; ++q) {
+      // the chunk's documents of this class: a contiguous slice of the list
+      const auto b = std::lower_bound(fl[q].begin(), fl[q].end(), d0);
+      const auto e = std::lower_bound(b, fl[q].end(), d1);
+      if (b == e) continue;
+      FusedArgs a;
+      a.S = sd;
+      a.D = dd;
+      a.L = ld;
+      a.M = M;
+      a.threshold = threshold;
+      a.p = penalty;
+      a.list = dfl[q] + (b - fl[q].begin());
+      a.n_list = (int)(e - b);
+      a.rec_off = droff;
+      a.rec = rec;
+      a.rec_count = cnt;
+      a.cost = cost;
+      a.hits = hits;
+      a.hit_off = dhoff;
+      a.tabs = tabs;
+      if (!BM_RING_FUSED_JOIN) BM_CK(launch_hits(a, hsm[q], sk), "hits_kernel");
+      BM_CK(launch_ring(a, 1 << q, fsm[q], sk), "mine_ring_kernel");
+    }
+    {
+      GeneralPlan gp;
+      for (int d = d0; d < d1; ++d)
+        if (banded[d]) gp.add(d, dh->n[d], dh->m[d]);
+      if (!gp.docs.empty()) {
+        Scratch scg(sk);
+        int rc = mine_general(gp, &sd, &dd, &ld, M, threshold, penalty, droff, rec, cnt, cost,
+                              scg, sk);
+        if (rc) return rc;
+      }
+    }
     // compact the chunk into its own region of `dense` (starting at its first
     // document's record slot) and fetch its record count; the host copies the
     // records out as soon as the count arrives, overlapping later chunks
