@@ -43,6 +43,8 @@ extern "C" {
 #define BM_ECUDA -2    /* CUDA runtime error                           */
 #define BM_ENOMEM -3   /* device allocation failed                     */
 #define BM_ELIMIT -4   /* size over a hard bound (ResourceLimitError)  */
+#define BM_EUNSUPPORTED -5 /* input outside the native ingest subset:  run
+                              the Python path (bm_ingest_jsonl only)      */
 
 /* Move codes (bimine/aligner.py:76-82): diagonal, skip-source, skip-target. */
 #define BM_MOVE_D 0
@@ -246,6 +248,47 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
  * document-ordered array; *total (device) receives the record count. */
 int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_count,
                int32_t n_docs, bm_record* dense, int64_t* total, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Native corpus path: host C++, no device work.
+ * Replaces, for ASCII JSONL input, bimine/corpus.py:129-193 load_document_pairs
+ * (+ segment_sentences :92-126, tokenize :28, normalize :38-40), the packing
+ * of pack.py, bimine/miner.py:131-155 bidirectional_merge and :253-260
+ * format_pair_line. Anything outside the accepted subset (non-ASCII bytes,
+ * JSON the validator refuses, non-string/int ids or langs, missing fields,
+ * equal langs) returns BM_EUNSUPPORTED with the reason in `why`; the caller
+ * then runs the Python path, which reproduces the reference exactly
+ * (including its DataError messages).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t n_sent, n_docs, n_ids, n_skipped;
+  int64_t n_tok_entries, n_dig_entries;
+  const int32_t *n_tok, *n_punct, *n_alpha, *tok_off, *tok_id;
+  const uint16_t* tok_alpha;
+  const int32_t *dig_off, *dig_id;
+  const int32_t *src0, *n, *tgt0, *m;
+} bm_ingest_arrays;
+
+/* Parse + segment + tokenize + intern a JSONL file of document pairs; pairs
+ * with an empty side are dropped (listed by bm_ingest_skipped). *handle owns
+ * every array until bm_ingest_free. */
+int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len);
+void bm_ingest_free(void* handle);
+int bm_ingest_view(void* handle, bm_ingest_arrays* out);
+int bm_ingest_doc(void* handle, int32_t k, const char** id, const char** src_lang,
+                  const char** tgt_lang);
+int bm_ingest_skipped(void* handle, int32_t q, int64_t* lineno, const char** id,
+                      const char** side);
+/* Lexicon (src_words[q] -> tgt_words[q]) as forward/reverse CSR over the
+ * handle's id space (pack.py pack_lexicon); arrays owned by the handle. */
+int bm_ingest_lexicon(void* handle, const char* const* src_words, const char* const* tgt_words,
+                      int64_t n_entries, bm_lexicon* out);
+/* Re-orient, merge (when has_bwd) and format the mined records as TSV bytes
+ * in document order; report = {pairs, forward, backward, unique src tokens,
+ * unique tgt tokens, docs mined}. *out stays valid until the next call. */
+int bm_ingest_emit(void* handle, const bm_record* fwd, int64_t n_fwd, const bm_record* bwd,
+                   int64_t n_bwd, int32_t has_bwd, const uint8_t* swap_f, const uint8_t* swap_b,
+                   const uint8_t* skip, const char** out, int64_t* out_len, int64_t* report);
 
 #ifdef __cplusplus
 }

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libbimine_b200.so")
-SOURCES = ["bm_lib.cu"]
+SOURCES = ["bm_lib.cu", "bm_ingest.cpp"]
 HEADERS = ["bm_kernels.cu", "bm_ring.cu", "bm_api.cu", "bm_device.cuh", "bm_kernels.cuh", "glibc_exp.cuh", "glibc_exp_table.h"]
 
 NVCC_FLAGS = [

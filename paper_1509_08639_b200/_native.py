@@ -17,7 +17,7 @@ from .errors import NativeUnavailableError, ResourceLimitError
 LIB_PATH = os.environ.get("BM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                         "libbimine_b200.so")
 
-BM_OK, BM_EINVAL, BM_ECUDA, BM_ENOMEM, BM_ELIMIT = 0, -1, -2, -3, -4
+BM_OK, BM_EINVAL, BM_ECUDA, BM_ENOMEM, BM_ELIMIT, BM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 MOVE_D, MOVE_GS, MOVE_GT = 0, 1, 2
 
 _p = C.c_void_p
@@ -62,6 +62,15 @@ class Record(C.Structure):
 
 RECORD_DTYPE = [("doc", "<i4"), ("i", "<i4"), ("j", "<i4"), ("pad", "<i4"), ("conf", "<f8")]
 
+class IngestArrays(C.Structure):
+    _fields_ = [("n_sent", C.c_int32), ("n_docs", C.c_int32), ("n_ids", C.c_int32),
+                ("n_skipped", C.c_int32), ("n_tok_entries", C.c_int64),
+                ("n_dig_entries", C.c_int64)] + [
+        (name, C.c_void_p) for name in ("n_tok", "n_punct", "n_alpha", "tok_off", "tok_id",
+                                        "tok_alpha", "dig_off", "dig_id", "src0", "n", "tgt0",
+                                        "m")]
+
+
 _SIGS = {
     "bm_abi_version": (C.c_int, []),
     "bm_last_error": (C.c_char_p, []),
@@ -90,6 +99,17 @@ _SIGS = {
     "bm_tune": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, C.POINTER(LexiconC),
                           C.POINTER(ModelC), _p, C.c_int32, _p, C.c_int32, _p, _p, _p, _p, _p]),
     "bm_compact": (C.c_int, [_p, _p, _p, C.c_int32, _p, _p, _p]),
+    "bm_ingest_jsonl": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32]),
+    "bm_ingest_free": (None, [C.c_void_p]),
+    "bm_ingest_view": (C.c_int, [C.c_void_p, C.POINTER(IngestArrays)]),
+    "bm_ingest_doc": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_char_p),
+                                C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]),
+    "bm_ingest_skipped": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]),
+    "bm_ingest_lexicon": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
+                                    C.c_int64, C.POINTER(LexiconC)]),
+    "bm_ingest_emit": (C.c_int, [C.c_void_p, _p, C.c_int64, _p, C.c_int64, C.c_int32, _p, _p, _p,
+                                 C.POINTER(C.c_char_p), C.POINTER(C.c_int64), _p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,0 +1,226 @@
+"""Native corpus path behind the reference's API.
+
+``mine_corpus_file(path, forward, backward, lex, cfg, out)`` produces exactly
+what ``mine_corpus(load_document_pairs(path), forward, backward, lex, cfg,
+out)`` produces -- the same TSV bytes and the same ``MiningReport`` counts --
+but reads, segments, tokenizes and packs the JSONL file in C++
+(``csrc/bm_ingest.cpp``), lowers the lexicon there, mines on the GPU, and
+merges / formats the records in C++ too.
+
+The native reader accepts a file only when its semantics reduce to fixed
+ASCII tables (every byte ASCII, JSON inside a validated subset, string or
+integer ids); anything else -- and any document whose orientation check would
+raise -- takes the Python path, which is the reference behaviour by
+construction. Empty-side pairs are reported through ``on_skip`` (and the log)
+before mining starts rather than interleaved with the output; the TSV and the
+report do not depend on that order.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+import time
+from typing import IO, Callable
+
+import numpy as np
+
+from . import _native as N
+from .classifier import ClassifierModel
+from .lexicon import Lexicon
+from .pack import PackedCorpus, PackedLexicon
+
+log = logging.getLogger(__name__)
+
+_SENT_FIELDS = (("n_tok", np.int32, "n_sent"), ("n_punct", np.int32, "n_sent"),
+                ("n_alpha", np.int32, "n_sent"), ("tok_off", np.int32, "n_sent+1"),
+                ("tok_id", np.int32, "n_tok_entries"), ("tok_alpha", np.uint16, "n_tok_entries"),
+                ("dig_off", np.int32, "n_sent+1"), ("dig_id", np.int32, "n_dig_entries"),
+                ("src0", np.int32, "n_docs"), ("n", np.int32, "n_docs"),
+                ("tgt0", np.int32, "n_docs"), ("m", np.int32, "n_docs"))
+
+
+def _view(ptr: int, dtype, count: int) -> np.ndarray:
+    if count == 0 or not ptr:
+        return np.zeros(0, dtype=dtype)
+    buf = (C.c_char * (count * np.dtype(dtype).itemsize)).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype, count=count)
+
+
+class NativeCorpus:
+    """A JSONL file ingested by bm_ingest_jsonl (arrays owned by the handle)."""
+
+    def __init__(self, handle: int):
+        self._lib = N.load_library()
+        self._h = C.c_void_p(handle)
+        a = N.IngestArrays()
+        N.check(self._lib.bm_ingest_view(self._h, C.byref(a)))
+        sizes = {"n_sent": a.n_sent, "n_sent+1": a.n_sent + 1, "n_docs": a.n_docs,
+                 "n_tok_entries": a.n_tok_entries, "n_dig_entries": a.n_dig_entries}
+        arrs = {name: _view(getattr(a, name), dt, sizes[sz]) for name, dt, sz in _SENT_FIELDS}
+        self.n_ids = a.n_ids
+        self.packed = PackedCorpus(**arrs)
+        self.doc_ids: list[str] = []
+        self.langs: list[tuple[str, str]] = []
+        pid, psl, ptl = C.c_char_p(), C.c_char_p(), C.c_char_p()
+        for k in range(a.n_docs):
+            N.check(self._lib.bm_ingest_doc(self._h, k, C.byref(pid), C.byref(psl), C.byref(ptl)))
+            self.doc_ids.append(pid.value.decode("ascii"))
+            self.langs.append((psl.value.decode("ascii"), ptl.value.decode("ascii")))
+        self.skipped: list[tuple[int, str, str]] = []
+        ln = C.c_int64()
+        for q in range(a.n_skipped):
+            N.check(self._lib.bm_ingest_skipped(self._h, q, C.byref(ln), C.byref(pid), C.byref(psl)))
+            self.skipped.append((ln.value, pid.value.decode("ascii"), psl.value.decode("ascii")))
+
+    @classmethod
+    def load(cls, path: str) -> "NativeCorpus | None":
+        """Ingest ``path``; None when it is outside the native subset."""
+        lib = N.load_library()
+        h = C.c_void_p()
+        why = C.create_string_buffer(256)
+        rc = lib.bm_ingest_jsonl(path.encode(), C.byref(h), why, len(why))
+        if rc == N.BM_EUNSUPPORTED:
+            log.info("native ingest declined %s (%s); using the Python reader", path,
+                     why.value.decode("ascii", "replace"))
+            return None
+        N.check(rc)
+        return cls(h.value)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.bm_ingest_free(h)
+            self._h = None
+
+    def lexicon(self, lex: Lexicon) -> PackedLexicon:
+        """pack_lexicon(lex, corpus) computed natively (forward entries; the
+        reverse CSR is their transpose, i.e. lex.reversed())."""
+        src: list[bytes] = []
+        tgt: list[bytes] = []
+        for word, cands in lex.entries.items():
+            wb = word.encode("utf-8")
+            for c, _p in cands:
+                src.append(wb)
+                tgt.append(c.encode("utf-8"))
+        n = len(src)
+        sa = (C.c_char_p * max(n, 1))(*src)
+        ta = (C.c_char_p * max(n, 1))(*tgt)
+        out = N.LexiconC()
+        N.check(self._lib.bm_ingest_lexicon(self._h, sa, ta, n, C.byref(out)))
+        nid = self.n_ids
+        nf = int(_view(out.fwd_off, np.int32, nid + 1)[-1]) if nid else 0
+        nr = int(_view(out.rev_off, np.int32, nid + 1)[-1]) if nid else 0
+        return PackedLexicon(nid, _view(out.fwd_off, np.int32, nid + 1).copy(),
+                             _view(out.fwd_cand, np.int32, nf).copy(),
+                             _view(out.rev_off, np.int32, nid + 1).copy(),
+                             _view(out.rev_cand, np.int32, nr).copy())
+
+    def emit(self, fwd: np.ndarray, bwd: np.ndarray | None, swap_f: np.ndarray,
+             swap_b: np.ndarray, skip: np.ndarray) -> tuple[bytes, list[int]]:
+        fwd = np.ascontiguousarray(fwd)
+        b = np.ascontiguousarray(bwd) if bwd is not None else fwd[:0]
+        sf = np.ascontiguousarray(swap_f, dtype=np.uint8)
+        sb = np.ascontiguousarray(swap_b, dtype=np.uint8)
+        sk = np.ascontiguousarray(skip, dtype=np.uint8)
+        out = C.c_char_p()
+        olen = C.c_int64()
+        rep = np.zeros(6, dtype=np.int64)
+        N.check(self._lib.bm_ingest_emit(self._h, fwd.ctypes.data, fwd.shape[0], b.ctypes.data,
+                                         b.shape[0], int(bwd is not None), sf.ctypes.data,
+                                         sb.ctypes.data, sk.ctypes.data, C.byref(out),
+                                         C.byref(olen), rep.ctypes.data))
+        data = C.string_at(out, olen.value) if olen.value else b""
+        return data, rep.tolist()
+
+
+def _orientations(langs, model: ClassifierModel, lex: Lexicon) -> np.ndarray | None:
+    """Per-doc swapped flags (miner.py _orientation), or None when any
+    document would raise DataError (the Python path then reproduces it)."""
+    direction = tuple(model.direction)
+    if tuple(lex.direction) != direction:
+        return None
+    out = np.zeros(len(langs), dtype=np.uint8)
+    for k, (sl, tl) in enumerate(langs):
+        if (sl, tl) == direction:
+            continue
+        if (tl, sl) == direction:
+            out[k] = 1
+            continue
+        return None
+    return out
+
+
+def mine_corpus_file(
+    docs_path: str,
+    forward: ClassifierModel,
+    backward: ClassifierModel | None,
+    lex: Lexicon,
+    cfg,
+    out: IO[str],
+    on_skip: Callable[[str, str], None] | None = None,
+):
+    """``mine_corpus(load_document_pairs(docs_path, on_skip=on_skip), ...)``
+    with the native reader, lexicon lowering, merge and TSV emission."""
+    from . import aligner, engine
+    from .corpus import load_document_pairs
+    from .miner import MiningReport, mine_corpus
+
+    start = time.perf_counter()
+    nc = NativeCorpus.load(docs_path)
+    sw_f = sw_b = None
+    if nc is not None:
+        sw_f = _orientations(nc.langs, forward, lex)
+        if backward is not None and sw_f is not None:
+            sw_b = _orientations(nc.langs, backward, lex.reversed())
+            if sw_b is None:
+                sw_f = None
+    if nc is None or sw_f is None:
+        return mine_corpus(load_document_pairs(docs_path, on_skip=on_skip), forward, backward,
+                           lex, cfg, out)
+    if sw_b is None:
+        sw_b = np.zeros_like(sw_f)
+    for _ln, pid, side in nc.skipped:
+        log.warning("skipping pair %r: empty %s document", pid, side)
+        if on_skip is not None:
+            on_skip(pid, f"empty {side} document")
+    c = nc.packed
+    n = c.n.astype(np.int64)
+    m = c.m.astype(np.int64)
+    skip = (n * m > aligner.MAX_CELLS).astype(np.uint8)
+    for k in np.nonzero(skip)[0].tolist():
+        a, b = (int(c.m[k]), int(c.n[k])) if sw_f[k] else (int(c.n[k]), int(c.m[k]))
+        log.warning("skipping: %s", f"document pair {nc.doc_ids[k]!r} needs a {a}x{b} matrix, "
+                                    f"over the {aligner.MAX_CELLS} cell limit")
+    work = np.nonzero(skip == 0)[0].astype(np.int64)
+    rec_dtype = np.dtype(N.RECORD_DTYPE)
+    fwd = np.zeros(0, dtype=rec_dtype)
+    bwd = None if backward is None else np.zeros(0, dtype=rec_dtype)
+    if work.size:
+        plex = nc.lexicon(lex)
+        dc = engine.DeviceCorpus.upload(c)
+        idx = work.tolist()
+
+        def run(model, pl, swapped):
+            dl = engine.DeviceLexicon.upload(pl)
+            view = engine.DocView.of(c, idx, [bool(x) for x in swapped[work]])
+            recs, _ = engine.mine(dc, dl, view, model, cfg.params.threshold, cfg.params.penalty)
+            recs = recs.copy()
+            recs["doc"] = work[recs["doc"]]
+            return recs
+
+        fwd = run(forward, plex, sw_f)
+        if backward is not None:
+            bwd = run(backward, plex.swapped(), sw_b)
+    data, rep = nc.emit(fwd, bwd, sw_f, sw_b, skip)
+    out.write(data.decode("ascii"))
+    report = MiningReport()
+    report.pairs_emitted = rep[0]
+    report.per_direction["forward"] = rep[1]
+    report.per_direction["backward"] = rep[2]
+    report.unique_src_tokens = rep[3]
+    report.unique_tgt_tokens = rep[4]
+    report.docs_processed = rep[5]
+    report.docs_skipped = int(skip.sum())
+    report.wall_clock_seconds = time.perf_counter() - start
+    return report

@@ -191,6 +191,62 @@ def test_mine_corpus_tsv_byte_identical(docs, tsv, bidir, t, p, world, request):
         assert rep == open(golden(tsv.replace(".tsv", ".report.json"))).read()
 
 
+@pytest.mark.parametrize("docs,tsv,bidir,t,p,world", [
+    ("docs40.jsonl", "mine40_fwd.tsv", False, 0.5, 0.2, "world500"),
+    ("docs40.jsonl", "mine40_bi.tsv", True, 0.5, 0.2, "world500"),
+    ("docs40.jsonl", "mine40_bi_t03_p005.tsv", True, 0.3, 0.05, "world500"),
+    ("doc200.jsonl", "mine200_fwd.tsv", False, 0.5, 0.2, "world5k"),
+    ("doc200.jsonl", "mine200_bi.tsv", True, 0.5, 0.2, "world5k"),
+    ("docs100x6.jsonl", "mine100x6_bi.tsv", True, 0.5, 0.2, "world5k"),
+])
+def test_mine_corpus_file_native_path_byte_identical(docs, tsv, bidir, t, p, world, request):
+    """Native JSONL reader + lexicon lowering + merge/TSV emission (ingest.py):
+    the reference's TSV bytes and report."""
+    from paper_1509_08639_b200.ingest import NativeCorpus
+
+    lex, fwd, bwd = request.getfixturevalue(world)
+    path = golden(docs)
+    assert NativeCorpus.load(path) is not None  # ASCII fixtures take the native path
+    sink = io.StringIO()
+    rep = bm.mine_corpus_file(path, fwd, bwd if bidir else None, lex,
+                              bm.MinerConfig(bm.MiningParams(t, p)), sink)
+    rep.wall_clock_seconds = 0.0
+    assert sink.getvalue() == open(golden(tsv), encoding="utf-8").read()
+    if tsv in ("mine40_fwd.tsv", "mine40_bi.tsv"):
+        assert bm.report_to_json(rep) == open(golden(tsv.replace(".tsv", ".report.json"))).read()
+
+
+def test_mine_corpus_file_1000_docs_sha256(world500, tmp_path):
+    import gzip
+
+    lex, fwd, bwd = world500
+    p = str(tmp_path / "docs1000.jsonl")
+    with gzip.open(golden("docs1000_s77.jsonl.gz"), "rb") as fi, open(p, "wb") as fo:
+        fo.write(fi.read())
+    sink = io.StringIO()
+    bm.mine_corpus_file(p, fwd, bwd, lex, bm.MinerConfig(bm.MiningParams(0.5, 0.2)), sink)
+    want = json.load(open(golden("mine1000_bi.json")))
+    text = sink.getvalue()
+    assert text.count("\n") == want["lines"]
+    assert hashlib.sha256(text.encode()).hexdigest() == want["sha256"]
+
+
+def test_mine_corpus_file_falls_back_outside_the_subset(world500, tmp_path):
+    """Non-ASCII text takes the Python reader: same output as mine_corpus."""
+    lex, fwd, bwd = world500
+    docs = load_docs("docs40.jsonl")[:5]
+    docs[1]["src"][0] = docs[1]["src"][0] + " caf\u00e9"
+    p = str(tmp_path / "mixed.jsonl")
+    with open(p, "w", encoding="utf-8") as fh:
+        for d in docs:
+            fh.write(json.dumps(d, ensure_ascii=False) + "\n")
+    cfg = bm.MinerConfig(bm.MiningParams(0.5, 0.2))
+    a, b = io.StringIO(), io.StringIO()
+    bm.mine_corpus_file(p, fwd, bwd, lex, cfg, a)
+    bm.mine_corpus(bm.load_document_pairs(p), fwd, bwd, lex, cfg, b)
+    assert a.getvalue() == b.getvalue() and a.getvalue()
+
+
 def test_mine_corpus_1000_docs_sha256(world500):
     lex, fwd, bwd = world500
     text, _ = _mine_text(pairs_of(load_docs("docs1000_s77.jsonl.gz")), fwd, bwd, lex)

@@ -1,0 +1,213 @@
+"""Native corpus path (csrc/bm_ingest.cpp, ingest.py) vs the Python reader.
+
+Host-only: ingestion, lexicon lowering and TSV emission run without a GPU, so
+these parity checks are CPU tests. The GPU round trip (mine_corpus_file ==
+mine_corpus(load_document_pairs(...))) is in test_gpu_parity.py.
+"""
+
+import gzip
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1509_08639_b200 as bm
+from paper_1509_08639_b200 import _native as N
+from paper_1509_08639_b200.aligner import MinedPair
+from paper_1509_08639_b200.corpus import load_document_pairs, tokenize
+from paper_1509_08639_b200.ingest import NativeCorpus
+from paper_1509_08639_b200.miner import bidirectional_merge, format_pair_line
+from paper_1509_08639_b200.pack import pack_lexicon, pack_pairs
+
+from conftest import golden
+
+FIELDS = ("n_tok", "n_punct", "n_alpha", "tok_off", "tok_id", "tok_alpha", "dig_off", "dig_id",
+          "src0", "n", "tgt0", "m")
+
+EDGE_LINES = [
+    # segmentation: abbreviations, digits after a period, ! and ?, trailing spaces
+    {"id": "e1", "src_lang": "xx", "tgt_lang": "yy",
+     "src": "Dr. Smith met Mr. Jones at 5 p.m. today! Was it 2019? 42 is the answer.  ",
+     "tgt": ["a b", "   ", "C-d e_f g__h", "x\tyz"]},
+    # escapes, punctuation-only tokens, mixed case, digit tokens, underscores
+    {"id": 7, "src_lang": "yy", "tgt_lang": "xx", "src": ["HELLO, World!!", "abc123 4567 _x_"],
+     "tgt": "Line one.\nLine Two.\tEnd.\r\nno. 5 etc. Vs. X", "extra": {"a": [1, 2.5e3, None, True]}},
+    # empty side: dropped at load (reported), nothing interned
+    {"id": "empty", "src_lang": "xx", "tgt_lang": "yy", "src": "   ", "tgt": ["kept"]},
+    {"id": "empty2", "src_lang": "xx", "tgt_lang": "yy", "src": ["a"], "tgt": []},
+    # duplicate keys: the last one wins
+    {"id": "dup", "src_lang": "xx", "tgt_lang": "yy", "src": "first", "tgt": "T"},
+]
+
+
+def write_jsonl(path, lines, raw_extra=(), newline="\n"):
+    with open(path, "w", newline="") as fh:
+        for obj in lines:
+            fh.write(json.dumps(obj) + newline)
+        for raw in raw_extra:
+            fh.write(raw + newline)
+
+
+def python_side(path):
+    skipped = []
+    pairs = list(load_document_pairs(path, on_skip=lambda pid, why: skipped.append((pid, why))))
+    return pairs, pack_pairs(pairs), skipped
+
+
+def assert_same_pack(nc, pc):
+    for f in FIELDS:
+        a, b = getattr(nc.packed, f), getattr(pc, f)
+        assert a.shape == b.shape and np.array_equal(a, b), f
+    assert nc.n_ids == len(pc.strings)
+
+
+@pytest.fixture(scope="module")
+def lex():
+    return bm.load_lexicon(golden("lex5k.tsv"), "xx", "yy")
+
+
+@pytest.mark.parametrize("name", ["docs40.jsonl", "doc200.jsonl", "docs10_noisy.jsonl",
+                                  "docs100x6.jsonl", "docs_stress.jsonl"])
+def test_ingest_matches_python_packer(name, lex):
+    path = golden(name)
+    nc = NativeCorpus.load(path)
+    if nc is None:  # outside the ASCII subset: the Python path is the behaviour
+        with open(path, encoding="utf-8") as fh:
+            text = "".join(json.dumps(json.loads(l), ensure_ascii=False) for l in fh if l.strip())
+        assert any(ord(ch) > 127 for ch in text)
+        return
+    pairs, pc, skipped = python_side(path)
+    assert_same_pack(nc, pc)
+    assert nc.doc_ids == [p.id for p in pairs]
+    assert nc.langs == [(p.source.lang, p.target.lang) for p in pairs]
+    assert [(pid, f"empty {side} document") for _l, pid, side in nc.skipped] == skipped
+    pl, nl = pack_lexicon(lex, pc), nc.lexicon(lex)
+    for f in ("fwd_off", "fwd_cand", "rev_off", "rev_cand"):
+        assert np.array_equal(getattr(pl, f), getattr(nl, f)), f
+
+
+def test_ingest_edge_cases(tmp_path, lex):
+    p = str(tmp_path / "edge.jsonl")
+    raw = ['{"id": "dup", "src_lang": "xx", "tgt_lang": "yy", "src": "first", "src": ["second one", "x"], "tgt": "t", "tgt": "U V."}',
+           "   \t",
+           '{"id": 12, "src_lang": "xx", "tgt_lang": "yy", "src": ["\\u0041b\\/c"], "tgt": ["q\\\\r"]}']
+    write_jsonl(p, EDGE_LINES, raw, newline="\r\n")
+    nc = NativeCorpus.load(p)
+    assert nc is not None
+    pairs, pc, skipped = python_side(p)
+    assert_same_pack(nc, pc)
+    assert nc.doc_ids == [x.id for x in pairs]
+    assert [(pid, f"empty {side} document") for _l, pid, side in nc.skipped] == skipped
+    assert len(skipped) == 2
+
+
+def test_ingest_bare_cr_lines(tmp_path):
+    p = str(tmp_path / "cr.jsonl")
+    write_jsonl(p, EDGE_LINES[:2], newline="\r")
+    nc = NativeCorpus.load(p)
+    pairs, pc, _ = python_side(p)
+    assert_same_pack(nc, pc)
+
+
+@pytest.mark.parametrize("line", [
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "café", "tgt": "x"}',   # non-ASCII
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "caf\\u00e9", "tgt": "x"}',  # escaped
+    '{"id": 1.5, "src_lang": "xx", "tgt_lang": "yy", "src": "a", "tgt": "b"}',          # float id
+    '{"id": "a", "src_lang": "xx", "tgt_lang": "xx", "src": "a", "tgt": "b"}',          # same langs
+    '{"id": "a", "src_lang": "xx", "src": "a", "tgt": "b"}',                           # missing
+    '{"id": "a", "src_lang": "xx", "tgt_lang": "yy", "src": [1], "tgt": "b"}',          # bad item
+    '{"id": "a", "src_lang": "xx", "tgt_lang": "yy", "src": "a", "tgt": "b"',           # truncated
+    '{"id": "a", "src_lang": "xx", "tgt_lang": "yy", "src": "a", "tgt": "b", "x": NaN}',
+    '["not", "an", "object"]',
+])
+def test_ingest_declines_outside_the_subset(tmp_path, line):
+    p = str(tmp_path / "bad.jsonl")
+    with open(p, "w", encoding="utf-8") as fh:
+        fh.write(line + "\n")
+    assert NativeCorpus.load(p) is None
+
+
+def _fake_records(pc, seed, dirn):
+    """Plausible mined records: per doc some diagonal cells with quantized
+    confidences (ties exercise the merge rules)."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for d in range(pc.n_docs):
+        n, m = int(pc.n[d]), int(pc.m[d])
+        k = min(n, m)
+        for i in range(k):
+            if rng.random() < 0.6:
+                rows.append((d, i, min(m - 1, i + (dirn and rng.random() < 0.2)), 0,
+                             round(rng.random() * 4) / 4 * 0.5 + 0.5))
+    return np.array(rows, dtype=np.dtype(N.RECORD_DTYPE))
+
+
+def test_emit_matches_python_merge_and_format(tmp_path):
+    path = golden("docs40.jsonl")
+    nc = NativeCorpus.load(path)
+    pairs, pc, _ = python_side(path)
+    nd = pc.n_docs
+    rng = np.random.default_rng(3)
+    sw_f = (rng.random(nd) < 0.3).astype(np.uint8)
+    sw_b = 1 - sw_f
+    skip = (rng.random(nd) < 0.1).astype(np.uint8)
+    fwd = _fake_records(pc, 1, 0)
+    bwd = _fake_records(pc, 2, 1)
+
+    def to_pairs(k, recs, swapped):
+        pair = pairs[k]
+        src, tgt = pair.source.sentences, pair.target.sentences
+        out = []
+        for r in recs[recs["doc"] == k]:
+            i, j, c = int(r["i"]), int(r["j"]), float(r["conf"])
+            if swapped:  # records index the oriented pair (source = pair.target)
+                i, j = j, i
+            if i >= len(src) or j >= len(tgt):
+                continue
+            out.append(MinedPair(src[i], tgt[j], c, pair.id, "backward" if swapped else "forward",
+                                 i, j))
+        return out
+
+    # records must index the oriented pair: drop the ones a swap makes invalid
+    def valid(recs, sw):
+        keep = []
+        for r in recs:
+            d, i, j = int(r["doc"]), int(r["i"]), int(r["j"])
+            n, m = int(pc.n[d]), int(pc.m[d])
+            if sw[d]:
+                n, m = m, n
+            keep.append(i < n and j < m)
+        return recs[np.array(keep, dtype=bool)]
+
+    fwd, bwd = valid(fwd, sw_f), valid(bwd, sw_b)
+    for has_bwd in (False, True):
+        data, rep = nc.emit(fwd, bwd if has_bwd else None, sw_f, sw_b, skip)
+        want = []
+        for k in range(nd):
+            if skip[k]:
+                continue
+            mined = to_pairs(k, fwd, sw_f[k])
+            if has_bwd:
+                mined = bidirectional_merge(mined, to_pairs(k, bwd, sw_b[k]))
+            want.extend(mined)
+        text = "".join(format_pair_line(r) for r in want)
+        assert data.decode("ascii") == text
+        src_tok, tgt_tok = set(), set()
+        for r in want:
+            src_tok.update(tokenize(r.src.normalized))
+            tgt_tok.update(tokenize(r.tgt.normalized))
+        assert rep == [len(want), sum(r.direction == "forward" for r in want),
+                       sum(r.direction == "backward" for r in want), len(src_tok), len(tgt_tok),
+                       int((skip == 0).sum())]
+
+
+def test_ingest_1000_doc_corpus(tmp_path):
+    src = golden("docs1000_s77.jsonl.gz")
+    p = str(tmp_path / "docs1000.jsonl")
+    with gzip.open(src, "rb") as fi, open(p, "wb") as fo:
+        fo.write(fi.read())
+    nc = NativeCorpus.load(p)
+    assert nc is not None
+    _, pc, _ = python_side(p)
+    assert_same_pack(nc, pc)
