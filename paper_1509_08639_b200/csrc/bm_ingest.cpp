@@ -21,7 +21,11 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -37,6 +41,67 @@ inline bool is_alnum(unsigned char c) { return is_alpha(c) || is_digit(c); }
 inline bool is_upper(unsigned char c) { return c >= 'A' && c <= 'Z'; }
 inline char lower(char c) { return (c >= 'A' && c <= 'Z') ? (char)(c + 32) : c; }
 
+// Open-addressing table of byte strings (arena-backed, looked up by pointer
+// + length, no allocation per lookup) -> int32 value.
+struct StrTable {
+  struct E {
+    uint64_t h;
+    uint32_t off, len;
+    int32_t val;
+  };
+  std::vector<uint32_t> slot;  // entry index + 1; 0 = empty
+  std::vector<E> ents;
+  std::string arena;
+  uint32_t mask = 0;
+  StrTable() { rehash(1u << 12); }
+  static uint64_t hash(const char* s, size_t n) {
+    uint64_t h = 0xcbf29ce484222325ull ^ n;
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      uint64_t w;
+      memcpy(&w, s + i, 8);
+      h = (h ^ w) * 0x100000001b3ull;
+      h ^= h >> 29;
+    }
+    uint64_t w = 0;
+    memcpy(&w, s + i, n - i);
+    h = (h ^ w) * 0x100000001b3ull;
+    h ^= h >> 32;
+    return h * 0x9E3779B97F4A7C15ull;
+  }
+  void rehash(uint32_t cap) {
+    slot.assign(cap, 0);
+    mask = cap - 1;
+    for (uint32_t q = 0; q < ents.size(); ++q) {
+      uint32_t s = (uint32_t)(ents[q].h >> 32) & mask;
+      while (slot[s]) s = (s + 1) & mask;
+      slot[s] = q + 1;
+    }
+  }
+  // value of the string, or -1
+  int32_t find(const char* s, size_t n, uint64_t h) const {
+    uint32_t q = (uint32_t)(h >> 32) & mask;
+    while (slot[q]) {
+      const E& e = ents[slot[q] - 1];
+      if (e.h == h && e.len == n && memcmp(arena.data() + e.off, s, n) == 0) return e.val;
+      q = (q + 1) & mask;
+    }
+    return -1;
+  }
+  int32_t find(const char* s, size_t n) const { return find(s, n, hash(s, n)); }
+  // insert a string known to be absent
+  void insert(const char* s, size_t n, uint64_t h, int32_t val) {
+    if ((ents.size() + 1) * 2 > slot.size()) rehash((uint32_t)slot.size() * 2);
+    E e{h, (uint32_t)arena.size(), (uint32_t)n, val};
+    arena.append(s, n);
+    ents.push_back(e);
+    uint32_t q = (uint32_t)(h >> 32) & mask;
+    while (slot[q]) q = (q + 1) & mask;
+    slot[q] = (uint32_t)ents.size();
+  }
+  size_t size() const { return ents.size(); }
+};
+
 struct Doc {
   std::string id, src_lang, tgt_lang;
   int32_t src0 = 0, n = 0, tgt0 = 0, m = 0;
@@ -47,34 +112,38 @@ struct Ingest {
   std::vector<int32_t> n_tok, n_punct, n_alpha, tok_off{0}, tok_id, dig_off{0}, dig_id;
   std::vector<uint16_t> tok_alpha;
   std::vector<int32_t> src0, n, tgt0, m;
-  // interned token strings (normalized tokens and raw digit tokens)
-  std::vector<std::string> strings;
-  std::unordered_map<std::string, int32_t> ids;
-  // per sentence: raw text, normalized text and its interned id (merge key)
+  // interned token strings (normalized tokens and raw digit tokens) -> id
+  StrTable ids;
+  // per sentence: raw text, normalized text and its interned id (merge key;
+  // unique within a chunk -- keys are only compared inside one document)
   std::string raw, norm;
   std::vector<int64_t> raw_off{0}, norm_off{0};
   std::vector<int32_t> norm_key;
-  std::unordered_map<std::string, int32_t> norm_ids;
+  StrTable norm_ids;
   std::vector<Doc> docs;
   std::vector<int64_t> skipped_lines;  // empty-side pairs dropped at load
   std::vector<std::string> skipped_ids, skipped_side;
   // lexicon CSR over the id space (bm_ingest_lexicon)
   std::vector<int32_t> fwd_off, fwd_cand, rev_off, rev_cand;
-  // token scratch
+  // raw token -> (normalized id, digit id, isalpha, punctuation-only)
   struct TokInfo {
     int32_t nid, did;
     bool alpha, punct;
   };
-  std::unordered_map<std::string, TokInfo> tok_cache;
+  StrTable tok_cache;
+  std::vector<TokInfo> tok_info;
   std::string out;  // TSV bytes of bm_ingest_emit
   std::string err;
+  std::vector<std::pair<int32_t, int32_t>> alpha_scratch;
+  std::vector<int32_t> digit_scratch;
+  std::string tmp;
 
-  int32_t intern(const std::string& s) {
-    auto it = ids.find(s);
-    if (it != ids.end()) return it->second;
-    const int32_t k = (int32_t)strings.size();
-    ids.emplace(s, k);
-    strings.push_back(s);
+  int32_t intern(const char* s, size_t n) {
+    const uint64_t h = StrTable::hash(s, n);
+    const int32_t v = ids.find(s, n, h);
+    if (v >= 0) return v;
+    const int32_t k = (int32_t)ids.size();
+    ids.insert(s, n, h, k);
     return k;
   }
 };
@@ -100,32 +169,34 @@ void for_tokens(const char* s, size_t len, F&& f) {
   }
 }
 
-// normalize (corpus.py:38-40): NFC (identity on ASCII), lower, " ".join(split())
-std::string normalize(const char* s, size_t len) {
-  std::string o;
-  o.reserve(len);
+// normalize (corpus.py:38-40): NFC (identity on ASCII), lower, " ".join(split());
+// appended to o
+void normalize_into(std::string& o, const char* s, size_t len) {
+  const size_t start = o.size();
   size_t i = 0;
   while (i < len) {
     while (i < len && is_space((unsigned char)s[i])) ++i;
     if (i >= len) break;
-    if (!o.empty()) o.push_back(' ');
+    if (o.size() > start) o.push_back(' ');
     while (i < len && !is_space((unsigned char)s[i])) o.push_back(lower(s[i++]));
   }
-  return o;
 }
 
 // Packer.add_sentence (pack.py) for one raw sentence
 bool add_sentence(Ingest& g, const char* s, size_t len) {
   int32_t T = 0, P = 0, A = 0;
-  std::vector<std::pair<int32_t, int32_t>> alpha;  // (normalized id, isalpha count)
-  std::vector<int32_t> digits;
-  std::string key;
+  auto& alpha = g.alpha_scratch;  // (normalized id, isalpha count)
+  auto& digits = g.digit_scratch;
+  alpha.clear();
+  digits.clear();
   for_tokens(s, len, [&](const char* t, size_t tl) {
-    key.assign(t, tl);
-    auto it = g.tok_cache.find(key);
-    if (it == g.tok_cache.end()) {
+    const uint64_t h = StrTable::hash(t, tl);
+    int32_t ix = g.tok_cache.find(t, tl, h);
+    if (ix < 0) {
       Ingest::TokInfo ti;
-      ti.nid = g.intern(normalize(t, tl));
+      g.tmp.clear();
+      normalize_into(g.tmp, t, tl);
+      ti.nid = g.intern(g.tmp.data(), g.tmp.size());
       bool all_alpha = tl > 0, all_digit = tl > 0, any_alnum = false;
       for (size_t q = 0; q < tl; ++q) {
         const unsigned char c = (unsigned char)t[q];
@@ -133,12 +204,14 @@ bool add_sentence(Ingest& g, const char* s, size_t len) {
         all_digit &= is_digit(c);
         any_alnum |= is_alnum(c);
       }
-      ti.did = all_digit ? g.intern(key) : -1;
+      ti.did = all_digit ? g.intern(t, tl) : -1;
       ti.alpha = all_alpha;
       ti.punct = !any_alnum;
-      it = g.tok_cache.emplace(key, ti).first;
+      ix = (int32_t)g.tok_info.size();
+      g.tok_info.push_back(ti);
+      g.tok_cache.insert(t, tl, h, ix);
     }
-    const Ingest::TokInfo& ti = it->second;
+    const Ingest::TokInfo ti = g.tok_info[ix];
     ++T;
     P += ti.punct ? 1 : 0;
     bool found = false;
@@ -172,17 +245,17 @@ bool add_sentence(Ingest& g, const char* s, size_t len) {
   // raw + normalized text of the Sentence object
   g.raw.append(s, len);
   g.raw_off.push_back((int64_t)g.raw.size());
-  std::string nm = normalize(s, len);
-  auto nit = g.norm_ids.find(nm);
-  int32_t nk;
-  if (nit == g.norm_ids.end()) {
+  const size_t n0 = g.norm.size();
+  normalize_into(g.norm, s, len);
+  const char* nm = g.norm.data() + n0;
+  const size_t nl = g.norm.size() - n0;
+  const uint64_t h = StrTable::hash(nm, nl);
+  int32_t nk = g.norm_ids.find(nm, nl, h);
+  if (nk < 0) {
     nk = (int32_t)g.norm_ids.size();
-    g.norm_ids.emplace(nm, nk);
-  } else {
-    nk = nit->second;
+    g.norm_ids.insert(nm, nl, h, nk);
   }
   g.norm_key.push_back(nk);
-  g.norm.append(nm);
   g.norm_off.push_back((int64_t)g.norm.size());
   return true;
 }
@@ -541,6 +614,106 @@ int parse_line(Ingest& g, const char* b, const char* e, int64_t lineno) {
   return 1;
 }
 
+// Merge chunks parsed independently (local id spaces) into part[0]. Local
+// ids are in first-appearance order within their chunk, so re-interning each
+// chunk's strings in chunk order gives exactly the ids one sequential pass
+// assigns (sequential, cheap: unique token strings only). The arrays are then
+// rewritten chunk-parallel into preallocated global slices, each sentence's
+// id lists re-sorted under the new ids.
+void merge_parts(std::vector<Ingest*>& part) {
+  const size_t np = part.size();
+  Ingest& G = *part[0];
+  std::vector<std::vector<int32_t>> rid(np);
+  for (size_t t = 1; t < np; ++t) {
+    Ingest& L = *part[t];
+    rid[t].resize(L.ids.size());
+    for (const StrTable::E& e : L.ids.ents)
+      rid[t][(size_t)e.val] = G.intern(L.ids.arena.data() + e.off, e.len);
+  }
+  // slice bases
+  std::vector<size_t> sb(np + 1, 0), tb(np + 1, 0), db(np + 1, 0), kb(np + 1, 0);
+  std::vector<int64_t> rb(np + 1, 0), nb(np + 1, 0);
+  for (size_t t = 0; t < np; ++t) {
+    Ingest& L = *part[t];
+    sb[t + 1] = sb[t] + L.n_tok.size();
+    tb[t + 1] = tb[t] + L.tok_id.size();
+    db[t + 1] = db[t] + L.dig_id.size();
+    kb[t + 1] = kb[t] + L.docs.size();
+    rb[t + 1] = rb[t] + (int64_t)L.raw.size();
+    nb[t + 1] = nb[t] + (int64_t)L.norm.size();
+  }
+  G.n_tok.resize(sb[np]);
+  G.n_punct.resize(sb[np]);
+  G.n_alpha.resize(sb[np]);
+  G.norm_key.resize(sb[np]);
+  G.tok_off.resize(sb[np] + 1);
+  G.dig_off.resize(sb[np] + 1);
+  G.raw_off.resize(sb[np] + 1);
+  G.norm_off.resize(sb[np] + 1);
+  G.tok_id.resize(tb[np]);
+  G.tok_alpha.resize(tb[np]);
+  G.dig_id.resize(db[np]);
+  G.raw.resize((size_t)rb[np]);
+  G.norm.resize((size_t)nb[np]);
+  G.docs.resize(kb[np]);
+  G.src0.resize(kb[np]);
+  G.n.resize(kb[np]);
+  G.tgt0.resize(kb[np]);
+  G.m.resize(kb[np]);
+  auto fill = [&](size_t t) {
+    Ingest& L = *part[t];
+    const size_t ns = L.n_tok.size(), s0 = sb[t];
+    std::copy(L.n_tok.begin(), L.n_tok.end(), G.n_tok.begin() + s0);
+    std::copy(L.n_punct.begin(), L.n_punct.end(), G.n_punct.begin() + s0);
+    std::copy(L.n_alpha.begin(), L.n_alpha.end(), G.n_alpha.begin() + s0);
+    memcpy(&G.raw[(size_t)rb[t]], L.raw.data(), L.raw.size());
+    memcpy(&G.norm[(size_t)nb[t]], L.norm.data(), L.norm.size());
+    std::vector<std::pair<int32_t, uint16_t>> ta;
+    for (size_t s = 0; s < ns; ++s) {
+      const int32_t a = L.tok_off[s], b = L.tok_off[s + 1];
+      ta.clear();
+      for (int32_t q = a; q < b; ++q) ta.emplace_back(rid[t][(size_t)L.tok_id[q]], L.tok_alpha[q]);
+      std::sort(ta.begin(), ta.end());
+      for (int32_t q = a; q < b; ++q) {
+        G.tok_id[tb[t] + (size_t)q] = ta[(size_t)(q - a)].first;
+        G.tok_alpha[tb[t] + (size_t)q] = ta[(size_t)(q - a)].second;
+      }
+      G.tok_off[s0 + s + 1] = (int32_t)(tb[t] + (size_t)b);
+      const int32_t c = L.dig_off[s], d = L.dig_off[s + 1];
+      for (int32_t q = c; q < d; ++q) G.dig_id[db[t] + (size_t)q] = rid[t][(size_t)L.dig_id[q]];
+      std::sort(G.dig_id.begin() + (long)(db[t] + (size_t)c), G.dig_id.begin() + (long)(db[t] + (size_t)d));
+      G.dig_off[s0 + s + 1] = (int32_t)(db[t] + (size_t)d);
+      // merge keys are compared only within a document, and a document never
+      // spans chunks: chunk-local keys need no remapping
+      G.norm_key[s0 + s] = L.norm_key[s];
+      G.raw_off[s0 + s + 1] = rb[t] + L.raw_off[s + 1];
+      G.norm_off[s0 + s + 1] = nb[t] + L.norm_off[s + 1];
+    }
+    for (size_t q = 0; q < L.docs.size(); ++q) {
+      Doc D = std::move(L.docs[q]);
+      D.src0 += (int32_t)s0;
+      D.tgt0 += (int32_t)s0;
+      const size_t k = kb[t] + q;
+      G.src0[k] = D.src0;
+      G.n[k] = D.n;
+      G.tgt0[k] = D.tgt0;
+      G.m[k] = D.m;
+      G.docs[k] = std::move(D);
+    }
+  };
+  {
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < np; ++t) th.emplace_back(fill, t);
+    for (auto& x : th) x.join();
+  }
+  for (size_t t = 1; t < np; ++t) {
+    Ingest& L = *part[t];
+    G.skipped_lines.insert(G.skipped_lines.end(), L.skipped_lines.begin(), L.skipped_lines.end());
+    G.skipped_ids.insert(G.skipped_ids.end(), L.skipped_ids.begin(), L.skipped_ids.end());
+    G.skipped_side.insert(G.skipped_side.end(), L.skipped_side.begin(), L.skipped_side.end());
+  }
+}
+
 }  // namespace bm_ingest
 
 using bm_ingest::Ingest;
@@ -562,29 +735,84 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
   fclose(fh);
   for (unsigned char c : data)
     if (c >= 0x80) return fail_why("non-ASCII input");
-  Ingest* g = new Ingest();
-  const char* s = data.data();
-  const char* end = s + data.size();
-  int64_t lineno = 0;
-  while (s < end) {
-    // text-mode line splitting: \n, \r\n and \r end a line
-    const char* q = s;
-    while (q < end && *q != '\n' && *q != '\r') ++q;
-    ++lineno;
-    bool blank = true;
-    for (const char* t = s; t < q; ++t) blank &= bm_ingest::is_space((unsigned char)*t);
-    if (!blank) {
-      const int rc = bm_ingest::parse_line(*g, s, q, lineno);
-      if (rc < 0) {
-        char msg[160];
-        snprintf(msg, sizeof(msg), "line %lld: %s", (long long)lineno,
-                 g->err.empty() ? "outside the native JSON subset" : g->err.c_str());
-        delete g;
-        return fail_why(msg);
+  // lines: text-mode splitting, \n, \r\n and \r end a line
+  struct Line {
+    size_t b, e;
+  };
+  std::vector<Line> lines;
+  {
+    const char* base = data.data();
+    size_t i = 0;
+    const size_t size = data.size();
+    while (i < size) {
+      size_t q = i;
+      while (q < size && base[q] != '\n' && base[q] != '\r') ++q;
+      lines.push_back(Line{i, q});
+      if (q < size && base[q] == '\r' && q + 1 < size && base[q + 1] == '\n') ++q;
+      i = q + 1;
+    }
+  }
+  // chunks of about equal bytes, parsed in parallel into local id spaces
+  const size_t nlines = lines.size();
+  unsigned hw = std::thread::hardware_concurrency();
+  const char* env = getenv("BM_INGEST_THREADS");
+  if (env) hw = (unsigned)atoi(env);
+  const size_t nthr = std::max<size_t>(1, std::min<size_t>({(size_t)std::max(hw, 1u), (size_t)32,
+                                                            nlines / 64 + 1}));
+  std::vector<size_t> cut(nthr + 1, nlines);
+  cut[0] = 0;
+  {
+    const size_t per = data.size() / nthr + 1;
+    size_t t = 1;
+    for (size_t q = 0; q < nlines && t < nthr; ++q)
+      if (lines[q].b >= t * per) cut[t++] = q;
+    for (; t < nthr; ++t) cut[t] = nlines;
+  }
+  std::vector<Ingest*> part(nthr, nullptr);
+  std::vector<int64_t> bad(nthr, -1);
+  auto work = [&](size_t t) {
+    Ingest* L = new Ingest();
+    part[t] = L;
+    const char* base = data.data();
+    for (size_t q = cut[t]; q < cut[t + 1]; ++q) {
+      const char* b = base + lines[q].b;
+      const char* e = base + lines[q].e;
+      bool blank = true;
+      for (const char* x = b; x < e; ++x) blank &= bm_ingest::is_space((unsigned char)*x);
+      if (blank) continue;
+      if (bm_ingest::parse_line(*L, b, e, (int64_t)q + 1) < 0) {
+        bad[t] = (int64_t)q + 1;
+        return;
       }
     }
-    if (q < end && *q == '\r' && q + 1 < end && q[1] == '\n') ++q;
-    s = q + 1;
+  };
+  const bool trace = getenv("BM_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  if (nthr == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < nthr; ++t) th.emplace_back(work, t);
+    for (auto& x : th) x.join();
+  }
+  for (size_t t = 0; t < nthr; ++t) {
+    if (bad[t] >= 0) {
+      char msg[160];
+      snprintf(msg, sizeof(msg), "line %lld: %s", (long long)bad[t],
+               part[t]->err.empty() ? "outside the native JSON subset" : part[t]->err.c_str());
+      for (Ingest* x : part) delete x;
+      return fail_why(msg);
+    }
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  Ingest* g = part[0];
+  if (nthr > 1) bm_ingest::merge_parts(part);
+  for (size_t t = 1; t < nthr; ++t) delete part[t];
+  if (trace) {
+    auto t2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[bm trace] ingest %zu threads: parse %.3f ms, merge %.3f ms\n", nthr,
+            std::chrono::duration<double, std::milli>(t1 - t0).count(),
+            std::chrono::duration<double, std::milli>(t2 - t1).count());
   }
   *handle = g;
   return BM_OK;
@@ -596,7 +824,7 @@ int bm_ingest_view(void* h, bm_ingest_arrays* v) {
   Ingest* g = (Ingest*)h;
   v->n_sent = (int32_t)g->n_tok.size();
   v->n_docs = (int32_t)g->docs.size();
-  v->n_ids = (int32_t)g->strings.size();
+  v->n_ids = (int32_t)g->ids.size();
   v->n_tok_entries = (int64_t)g->tok_id.size();
   v->n_dig_entries = (int64_t)g->dig_id.size();
   v->n_tok = g->n_tok.data();
@@ -643,17 +871,15 @@ int bm_ingest_skipped(void* h, int32_t q, int64_t* lineno, const char** id, cons
 int bm_ingest_lexicon(void* h, const char* const* src_words, const char* const* tgt_words,
                       int64_t n_entries, bm_lexicon* out) {
   Ingest* g = (Ingest*)h;
-  const int32_t nid = (int32_t)g->strings.size();
+  const int32_t nid = (int32_t)g->ids.size();
   std::vector<std::vector<int32_t>> fw(nid), rv(nid);
-  std::string a, b;
   for (int64_t q = 0; q < n_entries; ++q) {
-    a = src_words[q];
-    b = tgt_words[q];
-    auto ia = g->ids.find(a);
-    auto ib = g->ids.find(b);
-    if (ia == g->ids.end() || ib == g->ids.end()) continue;
-    fw[ia->second].push_back(ib->second);
-    rv[ib->second].push_back(ia->second);
+    const int32_t ia = g->ids.find(src_words[q], strlen(src_words[q]));
+    if (ia < 0) continue;
+    const int32_t ib = g->ids.find(tgt_words[q], strlen(tgt_words[q]));
+    if (ib < 0) continue;
+    fw[ia].push_back(ib);
+    rv[ib].push_back(ia);
   }
   auto csr = [&](std::vector<std::vector<int32_t>>& lists, std::vector<int32_t>& off,
                  std::vector<int32_t>& cand) {
@@ -692,22 +918,37 @@ int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record
   std::string& o = g->out;
   o.clear();
   int64_t pairs = 0, nf = 0, nb = 0, mined = 0;
-  std::unordered_map<std::string, char> src_tok, tgt_tok;
+  // unique-token counts (miner.py count_unique_tokens): for ASCII text
+  // tokenize(normalize(raw)) is exactly the sentence's set U of normalized
+  // token ids, so the sets are bitmaps over the id space
+  const size_t nid = g->ids.size();
+  std::vector<uint8_t> src_seen(nid, 0), tgt_seen(nid, 0);
+  int64_t n_src_tok = 0, n_tgt_tok = 0;
+  auto mark = [&](std::vector<uint8_t>& seen, int64_t& cnt, int32_t s) {
+    for (int32_t q = g->tok_off[s]; q < g->tok_off[s + 1]; ++q) {
+      uint8_t& b = seen[(size_t)g->tok_id[q]];
+      cnt += b ^ 1;
+      b = 1;
+    }
+  };
   struct Rec {
     int32_t si, tj;  // src / tgt sentence index in the pair's own orientation
     double conf;
     bool forward;
+    uint64_t key;
   };
   int64_t pf = 0, pb = 0;
-  std::vector<Rec> recs;
-  std::unordered_map<uint64_t, size_t> best;
-  auto sent_raw = [&](int32_t s) {
-    return std::string(g->raw.data() + g->raw_off[s], (size_t)(g->raw_off[s + 1] - g->raw_off[s]));
+  std::vector<Rec> recs, outr;
+  std::vector<uint32_t> ord;
+  // _sanitize (miner.py:253-258): tab / newline / carriage return -> space
+  auto put_sanitized = [&](const char* t, size_t n) {
+    const size_t o0 = o.size();
+    o.append(t, n);
+    for (size_t q = o0; q < o.size(); ++q)
+      if (o[q] == '\t' || o[q] == '\n' || o[q] == '\r') o[q] = ' ';
   };
-  auto sanitize = [](std::string t) {
-    for (char& c : t)
-      if (c == '\t' || c == '\n' || c == '\r') c = ' ';
-    return t;
+  auto put_raw = [&](int32_t s) {
+    put_sanitized(g->raw.data() + g->raw_off[s], (size_t)(g->raw_off[s + 1] - g->raw_off[s]));
   };
   char num[64];
   for (int32_t d = 0; d < nd; ++d) {
@@ -721,61 +962,61 @@ int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record
     if (skip[d]) continue;
     ++mined;
     recs.clear();
-    auto take = [&](const bm_record& r, bool swapped, bool forward) {
+    auto take = [&](const bm_record& r, bool swapped) {
       Rec x;
       // oriented source is the pair's target when swapped (miner.py:117-128)
       x.si = swapped ? r.j : r.i;
       x.tj = swapped ? r.i : r.j;
       x.conf = r.conf;
-      x.forward = forward;
+      x.forward = !swapped;
+      x.key = ((uint64_t)(uint32_t)g->norm_key[D.src0 + x.si] << 32) |
+              (uint32_t)g->norm_key[D.tgt0 + x.tj];
       recs.push_back(x);
     };
-    for (int64_t q = f0; q < pf; ++q) take(fwd[q], swap_f[d] != 0, !swap_f[d]);
-    std::vector<Rec> outr;
-    if (!has_bwd) {
-      outr = recs;
-    } else {
-      for (int64_t q = b0; q < pb; ++q) take(bwd[q], swap_b[d] != 0, !swap_b[d]);
-      best.clear();
-      std::vector<Rec> uniq;
-      for (const Rec& x : recs) {
-        const uint64_t key = ((uint64_t)(uint32_t)g->norm_key[D.src0 + x.si] << 32) |
-                             (uint32_t)g->norm_key[D.tgt0 + x.tj];
-        auto it = best.find(key);
-        if (it == best.end()) {
-          best.emplace(key, uniq.size());
-          uniq.push_back(x);
-        } else {
-          Rec& cur = uniq[it->second];
+    for (int64_t q = f0; q < pf; ++q) take(fwd[q], swap_f[d] != 0);
+    const std::vector<Rec>* emit = &recs;
+    if (has_bwd) {
+      for (int64_t q = b0; q < pb; ++q) take(bwd[q], swap_b[d] != 0);
+      // bidirectional_merge (miner.py:131-155): per normalized-text key the
+      // first record wins unless a later one is better (higher confidence,
+      // or forward over backward on an exact tie); then sort by indices
+      ord.resize(recs.size());
+      for (uint32_t q = 0; q < ord.size(); ++q) ord[q] = q;
+      std::stable_sort(ord.begin(), ord.end(),
+                       [&](uint32_t a, uint32_t b) { return recs[a].key < recs[b].key; });
+      outr.clear();
+      for (size_t q = 0; q < ord.size();) {
+        size_t w = q;
+        size_t r = q + 1;
+        for (; r < ord.size() && recs[ord[r]].key == recs[ord[q]].key; ++r) {
+          const Rec& x = recs[ord[r]];
+          const Rec& cur = recs[ord[w]];
           const bool better = x.conf != cur.conf ? x.conf > cur.conf : (x.forward && !cur.forward);
-          if (better) cur = x;
+          if (better) w = r;
         }
+        outr.push_back(recs[ord[w]]);
+        q = r;
       }
-      std::stable_sort(uniq.begin(), uniq.end(), [](const Rec& a, const Rec& b) {
+      std::sort(outr.begin(), outr.end(), [](const Rec& a, const Rec& b) {
         return a.si != b.si ? a.si < b.si : a.tj < b.tj;
       });
-      outr.swap(uniq);
+      emit = &outr;
     }
-    const std::string did = sanitize(D.id);
-    for (const Rec& x : outr) {
+    for (const Rec& x : *emit) {
       const int32_t ss = D.src0 + x.si, ts = D.tgt0 + x.tj;
-      o += sanitize(sent_raw(ss));
+      put_raw(ss);
       o += '\t';
-      o += sanitize(sent_raw(ts));
+      put_raw(ts);
       o += '\t';
-      snprintf(num, sizeof(num), "%.6f", x.conf);
-      o += num;
+      const int nc = snprintf(num, sizeof(num), "%.6f", x.conf);
+      o.append(num, (size_t)nc);
       o += '\t';
-      o += did;
+      put_sanitized(D.id.data(), D.id.size());
       o += x.forward ? "\tforward\n" : "\tbackward\n";
       ++pairs;
       (x.forward ? nf : nb) += 1;
-      const char* ns = g->norm.data() + g->norm_off[ss];
-      bm_ingest::for_tokens(ns, (size_t)(g->norm_off[ss + 1] - g->norm_off[ss]),
-                            [&](const char* t, size_t tl) { src_tok.emplace(std::string(t, tl), 1); });
-      const char* nt = g->norm.data() + g->norm_off[ts];
-      bm_ingest::for_tokens(nt, (size_t)(g->norm_off[ts + 1] - g->norm_off[ts]),
-                            [&](const char* t, size_t tl) { tgt_tok.emplace(std::string(t, tl), 1); });
+      mark(src_seen, n_src_tok, ss);
+      mark(tgt_seen, n_tgt_tok, ts);
     }
   }
   *out = o.data();
@@ -783,8 +1024,8 @@ int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record
   report[0] = pairs;
   report[1] = nf;
   report[2] = nb;
-  report[3] = (int64_t)src_tok.size();
-  report[4] = (int64_t)tgt_tok.size();
+  report[3] = n_src_tok;
+  report[4] = n_tgt_tok;
   report[5] = mined;
   return BM_OK;
 }

@@ -32,6 +32,9 @@ from .pack import PackedCorpus, PackedLexicon
 
 log = logging.getLogger(__name__)
 
+# phase timings (seconds) of the last mine_corpus_file call on the native path
+LAST_TIMINGS: dict[str, float] = {}
+
 _SENT_FIELDS = (("n_tok", np.int32, "n_sent"), ("n_punct", np.int32, "n_sent"),
                 ("n_alpha", np.int32, "n_sent"), ("tok_off", np.int32, "n_sent+1"),
                 ("tok_id", np.int32, "n_tok_entries"), ("tok_alpha", np.uint16, "n_tok_entries"),
@@ -167,7 +170,9 @@ def mine_corpus_file(
     from .miner import MiningReport, mine_corpus
 
     start = time.perf_counter()
+    LAST_TIMINGS.clear()
     nc = NativeCorpus.load(docs_path)
+    LAST_TIMINGS["ingest"] = time.perf_counter() - start
     sw_f = sw_b = None
     if nc is not None:
         sw_f = _orientations(nc.langs, forward, lex)
@@ -196,8 +201,10 @@ def mine_corpus_file(
     rec_dtype = np.dtype(N.RECORD_DTYPE)
     fwd = np.zeros(0, dtype=rec_dtype)
     bwd = None if backward is None else np.zeros(0, dtype=rec_dtype)
+    t0 = time.perf_counter()
     if work.size:
         plex = nc.lexicon(lex)
+        LAST_TIMINGS["lexicon"] = time.perf_counter() - t0
         dc = engine.DeviceCorpus.upload(c)
         idx = work.tolist()
 
@@ -212,8 +219,13 @@ def mine_corpus_file(
         fwd = run(forward, plex, sw_f)
         if backward is not None:
             bwd = run(backward, plex.swapped(), sw_b)
+    t1 = time.perf_counter()
+    LAST_TIMINGS["mine"] = t1 - t0 - LAST_TIMINGS.get("lexicon", 0.0)
     data, rep = nc.emit(fwd, bwd, sw_f, sw_b, skip)
+    t2 = time.perf_counter()
     out.write(data.decode("ascii"))
+    LAST_TIMINGS["emit"] = t2 - t1
+    LAST_TIMINGS["write"] = time.perf_counter() - t2
     report = MiningReport()
     report.pairs_emitted = rep[0]
     report.per_direction["forward"] = rep[1]

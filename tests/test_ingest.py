@@ -202,12 +202,42 @@ def test_emit_matches_python_merge_and_format(tmp_path):
                        int((skip == 0).sum())]
 
 
-def test_ingest_1000_doc_corpus(tmp_path):
-    src = golden("docs1000_s77.jsonl.gz")
-    p = str(tmp_path / "docs1000.jsonl")
-    with gzip.open(src, "rb") as fi, open(p, "wb") as fo:
+@pytest.fixture(scope="module")
+def docs1000(tmp_path_factory):
+    p = str(tmp_path_factory.mktemp("c") / "docs1000.jsonl")
+    with gzip.open(golden("docs1000_s77.jsonl.gz"), "rb") as fi, open(p, "wb") as fo:
         fo.write(fi.read())
+    return p, python_side(p)
+
+
+@pytest.mark.parametrize("threads", ["1", "3", "7", "16"])
+def test_ingest_1000_doc_corpus_any_thread_count(docs1000, threads, monkeypatch):
+    """Chunks parsed in parallel re-intern into the sequential id order."""
+    monkeypatch.setenv("BM_INGEST_THREADS", threads)
+    p, (_, pc, _) = docs1000
     nc = NativeCorpus.load(p)
     assert nc is not None
-    _, pc, _ = python_side(p)
     assert_same_pack(nc, pc)
+
+
+def test_emit_on_a_multi_chunk_ingest(docs1000, monkeypatch):
+    """Merge keys are chunk-local: the merge must still match Python's."""
+    monkeypatch.setenv("BM_INGEST_THREADS", "5")
+    p, (pairs, pc, _) = docs1000
+    nc = NativeCorpus.load(p)
+    nd = pc.n_docs
+    fwd = _fake_records(pc, 4, 0)
+    bwd = _fake_records(pc, 5, 1)
+    z = np.zeros(nd, dtype=np.uint8)
+    data, rep = nc.emit(fwd, bwd, z, z, z)
+    want = []
+    for k in range(nd):
+        pair = pairs[k]
+        src, tgt = pair.source.sentences, pair.target.sentences
+        f = [MinedPair(src[int(r["i"])], tgt[int(r["j"])], float(r["conf"]), pair.id, "forward",
+                       int(r["i"]), int(r["j"])) for r in fwd[fwd["doc"] == k]]
+        b = [MinedPair(src[int(r["i"])], tgt[int(r["j"])], float(r["conf"]), pair.id, "forward",
+                       int(r["i"]), int(r["j"])) for r in bwd[bwd["doc"] == k]]
+        want.extend(bidirectional_merge(f, b))
+    assert data.decode("ascii") == "".join(format_pair_line(r) for r in want)
+    assert rep[0] == len(want)
