@@ -233,19 +233,54 @@ struct HostTrace {
 
 // Banded tier for the documents of `g` (K1 -> K2/K3 -> K4, then scatter into
 // the caller's per-document record slots).
+// K1 over a banded plan: the document-level join + scoring kernels when every
+// document's counts fit 16 bits (doc_join: max tokens per sentence <= 65535,
+// checked by the caller; sides <= 65535 sentences, checked here), else the
+// per-tile kernel.
+int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs& D,
+                  const bm_lexicon* lex, const Model& M, GeneralDev& dv, bool doc_join,
+                  Scratch& sc, cudaStream_t st) {
+  const int k = (int)g.docs.size();
+  for (int q = 0; q < k && doc_join; ++q) doc_join = g.n[q] <= 65535 && g.m[q] <= 65535;
+  if (!doc_join) {
+    BM_CK(launch_score(*sent, D, *lex, M, dv.tiles, (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S,
+                       st),
+          "score_tile_kernel");
+    return BM_OK;
+  }
+  std::vector<int64_t> hoff(k);
+  int64_t ht = 0;
+  for (int q = 0; q < k; ++q) {
+    hoff[q] = ht;
+    ht += (int64_t)g.n[q] * g.m[q];
+  }
+  std::vector<int4> items;
+  join_items(g.n.data(), g.m.data(), k, items);
+  uint32_t* hits = nullptr;
+  int64_t* dho = nullptr;
+  int4* dit = nullptr;
+  BM_CK(sc.alloc(&hits, (size_t)ht), "alloc hits");
+  BM_CK(cudaMemsetAsync(hits, 0, (size_t)ht * 4, st), "memset hits");
+  BM_CK(sc.upload(&dho, hoff), "upload");
+  BM_CK(sc.upload(&dit, items), "upload");
+  BM_CK(launch_score_hits(*sent, D, *lex, M, dit, (int)items.size(), hits, dho, dv.tiles,
+                          (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S, st),
+        "score_hits_kernel");
+  return BM_OK;
+}
+
 int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* docs,
                  const bm_lexicon* lex, const Model& M, double threshold, double penalty,
                  const int64_t* rec_off, bm_record* rec, int32_t* rec_count, double* cost,
-                 Scratch& sc, cudaStream_t st) {
+                 bool doc_join, Scratch& sc, cudaStream_t st) {
   {
     const int k = (int)g.docs.size();
     GeneralDev dv;
     int rc = general_prepare(g, docs, sc, dv, st);
     if (rc) return rc;
     const bm_docs D = local_docs(dv, k);
-    BM_CK(launch_score(*sent, D, *lex, M, dv.tiles, (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S,
-                       st),
-          "score_tile_kernel");
+    rc = score_general(g, sent, D, lex, M, dv, doc_join, sc, st);
+    if (rc) return rc;
     double* cost_l = nullptr;
     BM_CK(sc.alloc(&cost_l, k), "alloc");
     rc = general_nw(g, dv, penalty, cost_l, st);
@@ -489,8 +524,10 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     }
   }
   if (!g.docs.empty()) {
+    bool doc_join = true;
+    for (int32_t d : g.docs) doc_join &= amax_host[d] <= 65535;
     int rc = mine_general(g, sent, docs, lex, M, threshold, penalty, rec_off, rec, rec_count, cost,
-                          sc, st);
+                          doc_join, sc, st);
     if (rc) return rc;
   }
   return BM_OK;
@@ -520,19 +557,21 @@ cudaStream_t copy_stream() {
   return s;
 }
 
-// Second compute stream of the calling thread: bm_mine_host alternates chunks
-// between the caller's stream and this one so a chunk's kernel tails overlap
-// the next chunk's kernels.
-cudaStream_t side_stream() {
-  static thread_local cudaStream_t s = nullptr;
+// Extra compute streams of the calling thread: bm_mine_host deals chunks
+// round-robin over the caller's stream and these, so a chunk's kernel tails
+// overlap the next chunks' kernels.
+constexpr int kMaxMineStreams = 4;
+cudaStream_t side_stream(int q) {
+  static thread_local cudaStream_t s[kMaxMineStreams] = {};
   static thread_local int dev_of = -1;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (s == nullptr || dev_of != dev) {
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (dev_of != dev) {
+    for (auto& x : s) x = nullptr;
     dev_of = dev;
   }
-  return s;
+  if (s[q] == nullptr) cudaStreamCreateWithFlags(&s[q], cudaStreamNonBlocking);
+  return s[q];
 }
 
 // Page-locked per-chunk record counts of the calling thread (grown on demand).
@@ -713,8 +752,13 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
   BM_CK(cudaEventRecord(ready, st), "event");
   BM_CK(cudaStreamWaitEvent(cs, ready, 0), "event");
-  cudaStream_t s2 = side_stream();
-  BM_CK(cudaStreamWaitEvent(s2, ready, 0), "event");
+  static const int n_ms = std::max(1, std::min(kMaxMineStreams,
+      getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 3));
+  std::vector<cudaStream_t> ms(1, st);
+  for (int q = 1; q < n_ms; ++q) {
+    ms.push_back(side_stream(q));
+    BM_CK(cudaStreamWaitEvent(ms.back(), ready, 0), "event");
+  }
   auto h2d = [&](void* dst, const void* from, size_t bytes) -> cudaError_t {
     return bytes ? cudaMemcpyAsync(dst, from, bytes, cudaMemcpyHostToDevice, cs) : cudaSuccess;
   };
@@ -796,7 +840,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
       cudaEventRecord(e, cs);
       tl_copy.push_back(e);
     }
-    cudaStream_t sk = (evs.size() & 1) ? st : s2;  // chunk 0 on s2, 1 on st, ...
+    cudaStream_t sk = ms[(ch_d0.size() + 1) % ms.size()];  // chunk 0 on a side stream
     BM_CK(cudaStreamWaitEvent(sk, ev, 0), "event");
     // the copy stream only moves bytes: widening the wire arrays is a few
     // microseconds of compute and runs in order on the compute stream (on the
@@ -838,8 +882,10 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
         if (banded[d]) gp.add(d, dh->n[d], dh->m[d]);
       if (!gp.docs.empty()) {
         Scratch scg(sk);
+        bool doc_join = true;
+        for (int32_t d : gp.docs) doc_join &= amax[d] <= 65535;
         int rc = mine_general(gp, &sd, &dd, &ld, M, threshold, penalty, droff, rec, cnt, cost,
-                              scg, sk);
+                              doc_join, scg, sk);
         if (rc) return rc;
       }
     }
@@ -868,12 +914,14 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     }
     d0 = d1;
   }
-  // join the side stream back into the caller's stream
-  cudaEvent_t joined;
-  BM_CK(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming), "event");
-  BM_CK(cudaEventRecord(joined, s2), "event");
-  BM_CK(cudaStreamWaitEvent(st, joined, 0), "event");
-  evs.push_back(joined);
+  // join the side streams back into the caller's stream
+  for (size_t q = 1; q < ms.size(); ++q) {
+    cudaEvent_t joined;
+    BM_CK(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming), "event");
+    BM_CK(cudaEventRecord(joined, ms[q]), "event");
+    BM_CK(cudaStreamWaitEvent(st, joined, 0), "event");
+    evs.push_back(joined);
+  }
   tr.mark("chunks enqueued");
   int64_t tot = 0;
   for (size_t q = 0; q < ch_ev.size(); ++q) {

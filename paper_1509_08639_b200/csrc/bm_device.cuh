@@ -279,112 +279,146 @@ __device__ void join_direction(G g, const bm_sentences& S, const int32_t* off,
 // Entry-parallel form of join_direction: every loop runs over token entries
 // (coalesced loads, all lanes busy) instead of over sentences. offA / offB are
 // the two sides' tok_off slices staged in shared memory (na+1 / nb+1 ints).
+// First sentence k of [0, ns) whose entries reach past e (off[k+1] > e).
+__device__ __forceinline__ int first_sentence_after(const int32_t* off, int ns, int e) {
+  int lo = 0, hi = ns;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid + 1] <= e)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// One chunk [c0, c1) of side B's entries: bucket it, then probe with every
+// alpha entry of side A (in chunks with an owner table). offA / offB: the
+// sides' tok_off slices (shared or global memory), na / nb sentences.
+template <class G, class AddFn>
+__device__ void join_chunk_entries(G g, const bm_sentences& S, const int32_t* off,
+                                   const int32_t* cand, const int32_t* offA, int na,
+                                   const int32_t* offB, int b0, int nb, int c0, int c1,
+                                   JoinSmem& js, uint16_t* chunk_owner, uint16_t* a_owner,
+                                   AddFn add) {
+  const int eA0 = offA[0], eA1 = offA[na];
+  for (int b = g.rank(); b < js.nbuckets; b += g.size()) js.bfill[b] = 0;
+  g.sync();
+  for (int e = c0 + g.rank(); e < c1; e += g.size())
+    atomicAdd(&js.bfill[bucket_of(__ldg(S.tok_id + e), js.bshift)], 1);
+  // owner sentence of every entry of the chunk (stores only)
+  {
+    const int kb0 = first_sentence_after(offB, nb, c0);
+    for (int k = kb0 + g.rank(); k < nb; k += g.size()) {
+      const int bk = offB[k];
+      if (bk >= c1) break;
+      const int e0 = max(c0, bk), e1 = min(c1, offB[k + 1]);
+      for (int e = e0; e < e1; ++e) chunk_owner[e - c0] = (uint16_t)k;
+    }
+  }
+  g.sync();
+  if (g.scanner()) {
+    int lane = threadIdx.x & (WARP - 1);
+    int per = (js.nbuckets + WARP - 1) / WARP;
+    int q0 = lane * per, q1 = min(js.nbuckets, q0 + per);
+    int sum = 0;
+    for (int b = q0; b < q1; ++b) sum += js.bfill[b];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < WARP; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - sum;
+    for (int b = q0; b < q1; ++b) {
+      int c = js.bfill[b];
+      js.bstart[b] = run;
+      js.bfill[b] = run;
+      run += c;
+    }
+    if (lane == WARP - 1) js.bstart[js.nbuckets] = incl;
+  }
+  g.sync();
+  for (int e = c0 + g.rank(); e < c1; e += g.size()) {
+    const int32_t id = __ldg(S.tok_id + e);
+    const int slot = atomicAdd(&js.bfill[bucket_of(id, js.bshift)], 1);
+    js.key[slot] = id;
+    js.owner[slot] = chunk_owner[e - c0];
+  }
+  g.sync();
+  // probe side in chunks of emax entries, each with an owner table (a
+  // per-entry binary search over the offsets cost more than the probes)
+  for (int a0 = eA0; a0 < eA1; a0 += js.emax) {
+    const int a1 = min(eA1, a0 + js.emax);
+    {
+      const int ka0 = first_sentence_after(offA, na, a0);
+      for (int k = ka0 + g.rank(); k < na; k += g.size()) {
+        const int ak = offA[k];
+        if (ak >= a1) break;
+        const int e0 = max(a0, ak), e1 = min(a1, offA[k + 1]);
+        for (int e = e0; e < e1; ++e) a_owner[e - a0] = (uint16_t)k;
+      }
+    }
+    g.sync();
+    // kBatch entries per thread at a time: each level of the dependent
+    // lookups (entry -> lexicon offsets -> first candidate) is issued for
+    // all of them before any is used, so their latencies overlap
+#ifndef BM_HITS_BATCH
+#define BM_HITS_BATCH 4
+#endif
+    constexpr int kBatch = BM_HITS_BATCH;
+    for (int eb = a0 + g.rank(); eb < a1; eb += kBatch * g.size()) {
+      int wv[kBatch], idv[kBatch], q0v[kBatch], q1v[kBatch], lav[kBatch], c0v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int e = eb + u * g.size();
+        const bool ok = e < a1;
+        wv[u] = ok ? __ldg(S.tok_alpha + e) : 0;
+        idv[u] = ok ? __ldg(S.tok_id + e) : 0;
+        lav[u] = ok ? a_owner[e - a0] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        q0v[u] = wv[u] ? __ldg(off + idv[u]) : 0;
+        q1v[u] = wv[u] ? __ldg(off + idv[u] + 1) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) c0v[u] = q0v[u] < q1v[u] ? __ldg(cand + q0v[u]) : 0;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int w = wv[u], la = lav[u], q0 = q0v[u], q1 = q1v[u];
+        for (int q = q0; q < q1; ++q) {
+          const int32_t c = q == q0 ? c0v[u] : __ldg(cand + q);
+          const uint32_t bk = bucket_of(c, js.bshift);
+          const int s1 = js.bstart[bk + 1];
+          for (int slot = js.bstart[bk]; slot < s1; ++slot) {
+            if (js.key[slot] != c) continue;
+            const int lb = js.owner[slot];
+            // an entry hits a sentence once however many candidates it holds
+            bool dup = false;
+            if (q > q0) {
+              const int u0 = __ldg(S.tok_off + b0 + lb);
+              const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
+              for (int qq = q0; qq < q && !dup; ++qq) dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
+            }
+            if (!dup) add(la, lb, w);
+          }
+        }
+      }
+    }
+    g.sync();
+  }
+}
+
 template <class G, class AddFn>
 __device__ void join_direction_entries(G g, const bm_sentences& S, const int32_t* off,
                                        const int32_t* cand, const int32_t* offA, int na,
                                        const int32_t* offB, int b0, int nb, JoinSmem& js,
                                        uint16_t* chunk_owner, uint16_t* a_owner, AddFn add) {
-  const int eA0 = offA[0], eA1 = offA[na];
   const int eB0 = offB[0], eB1 = offB[nb];
-  for (int c0 = eB0; c0 < eB1; c0 += js.emax) {
-    const int c1 = min(eB1, c0 + js.emax);
-    for (int b = g.rank(); b < js.nbuckets; b += g.size()) js.bfill[b] = 0;
-    g.sync();
-    for (int e = c0 + g.rank(); e < c1; e += g.size())
-      atomicAdd(&js.bfill[bucket_of(__ldg(S.tok_id + e), js.bshift)], 1);
-    // owner sentence of every entry of the chunk (stores only)
-    for (int k = g.rank(); k < nb; k += g.size()) {
-      const int e0 = max(c0, offB[k]), e1 = min(c1, offB[k + 1]);
-      for (int e = e0; e < e1; ++e) chunk_owner[e - c0] = (uint16_t)k;
-    }
-    g.sync();
-    if (g.scanner()) {
-      int lane = threadIdx.x & (WARP - 1);
-      int per = (js.nbuckets + WARP - 1) / WARP;
-      int q0 = lane * per, q1 = min(js.nbuckets, q0 + per);
-      int sum = 0;
-      for (int b = q0; b < q1; ++b) sum += js.bfill[b];
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < WARP; o <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      int run = incl - sum;
-      for (int b = q0; b < q1; ++b) {
-        int c = js.bfill[b];
-        js.bstart[b] = run;
-        js.bfill[b] = run;
-        run += c;
-      }
-      if (lane == WARP - 1) js.bstart[js.nbuckets] = incl;
-    }
-    g.sync();
-    for (int e = c0 + g.rank(); e < c1; e += g.size()) {
-      const int32_t id = __ldg(S.tok_id + e);
-      const int slot = atomicAdd(&js.bfill[bucket_of(id, js.bshift)], 1);
-      js.key[slot] = id;
-      js.owner[slot] = chunk_owner[e - c0];
-    }
-    g.sync();
-    // probe side in chunks of emax entries, each with an owner table (a
-    // per-entry binary search over the offsets cost more than the probes)
-    for (int a0 = eA0; a0 < eA1; a0 += js.emax) {
-      const int a1 = min(eA1, a0 + js.emax);
-      for (int k = g.rank(); k < na; k += g.size()) {
-        const int e0 = max(a0, offA[k]), e1 = min(a1, offA[k + 1]);
-        for (int e = e0; e < e1; ++e) a_owner[e - a0] = (uint16_t)k;
-      }
-      g.sync();
-      // kBatch entries per thread at a time: each level of the dependent
-      // lookups (entry -> lexicon offsets -> first candidate) is issued for
-      // all of them before any is used, so their latencies overlap
-#ifndef BM_HITS_BATCH
-#define BM_HITS_BATCH 4
-#endif
-      constexpr int kBatch = BM_HITS_BATCH;
-      for (int eb = a0 + g.rank(); eb < a1; eb += kBatch * g.size()) {
-        int wv[kBatch], idv[kBatch], q0v[kBatch], q1v[kBatch], lav[kBatch], c0v[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int e = eb + u * g.size();
-          const bool ok = e < a1;
-          wv[u] = ok ? __ldg(S.tok_alpha + e) : 0;
-          idv[u] = ok ? __ldg(S.tok_id + e) : 0;
-          lav[u] = ok ? a_owner[e - a0] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          q0v[u] = wv[u] ? __ldg(off + idv[u]) : 0;
-          q1v[u] = wv[u] ? __ldg(off + idv[u] + 1) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) c0v[u] = q0v[u] < q1v[u] ? __ldg(cand + q0v[u]) : 0;
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int w = wv[u], la = lav[u], q0 = q0v[u], q1 = q1v[u];
-          for (int q = q0; q < q1; ++q) {
-            const int32_t c = q == q0 ? c0v[u] : __ldg(cand + q);
-            const uint32_t bk = bucket_of(c, js.bshift);
-            const int s1 = js.bstart[bk + 1];
-            for (int slot = js.bstart[bk]; slot < s1; ++slot) {
-              if (js.key[slot] != c) continue;
-              const int lb = js.owner[slot];
-              // an entry hits a sentence once however many candidates it holds
-              bool dup = false;
-              if (q > q0) {
-                const int u0 = __ldg(S.tok_off + b0 + lb);
-                const int un = __ldg(S.tok_off + b0 + lb + 1) - u0;
-                for (int qq = q0; qq < q && !dup; ++qq) dup = sorted_contains(S.tok_id + u0, un, __ldg(cand + qq));
-              }
-              if (!dup) add(la, lb, w);
-            }
-          }
-        }
-      }
-      g.sync();
-    }
-  }
+  for (int c0 = eB0; c0 < eB1; c0 += js.emax)
+    join_chunk_entries(g, S, off, cand, offA, na, offB, b0, nb, c0, min(eB1, c0 + js.emax), js,
+                       chunk_owner, a_owner, add);
 }
 
 // Entry-parallel full join; offS / offT: staged tok_off slices (ns+1 / nt+1).

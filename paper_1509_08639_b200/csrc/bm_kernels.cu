@@ -128,6 +128,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
   TileScalars* rows = (TileScalars*)(smem + kExpTableWords * 8 + kTile * kTile * 4);
   TileScalars* cols = rows + 1;
   JoinSmem js = carve_join((uint8_t*)(cols + 1));
+  int32_t* offS = (int32_t*)((uint8_t*)(cols + 1) + align16(join_smem_bytes()));
+  int32_t* offT = offS + kTile + 1;
+  uint16_t* chunk_owner = (uint16_t*)(offT + kTile + 1);
+  uint16_t* a_owner = chunk_owner + kJoinEmax;
 
   const int4 tile = tiles[blockIdx.x];
   const int doc = tile.x, r0 = tile.y, c0 = tile.z;
@@ -148,7 +152,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
     dst->d0[local] = sc.d0;
     dst->pos[local] = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
   }
-  tile_join<false>(CtaGroup(), S, L, s0, ns, t0, nt, hits, js);  // ends with a barrier
+  for (int q = threadIdx.x; q <= ns + nt + 1; q += blockDim.x) {
+    if (q <= ns)
+      offS[q] = __ldg(S.tok_off + s0 + q);
+    else
+      offT[q - ns - 1] = __ldg(S.tok_off + t0 + (q - ns - 1));
+  }
+  __syncthreads();
+  // entry-parallel join (all threads probe), ends with a barrier
+  tile_join_entries<false>(CtaGroup(), S, L, s0, ns, t0, nt, offS, offT, hits, js, chunk_owner,
+                           a_owner);
 
   double* dst = out + s_off[doc] + (int64_t)r0 * pitch[doc] + c0;
   const int64_t ld = pitch[doc];
@@ -161,8 +174,131 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 for large documents, in two passes:
+//   hits_doc_kernel    the dictionary join once per document (work items =
+//                      (document, direction, 128-sentence range of the indexed
+//                      side)), hit counts hf | hr << 16 accumulated with L2
+//                      atomics into a per-document scratch (4 B per cell)
+//   score_hits_kernel  per 64x64 tile: staged sentence scalars + the hit
+//                      counts -> S (no join, no barrier-heavy phase)
+// The per-tile kernel above re-probes every row's lexicon candidates once per
+// column tile; this splits the probes by indexed-side ranges instead (about
+// 4x fewer probes on long documents). Needs |A| <= 65535 per sentence and at
+// most 65535 sentences per side (16-bit counts / owners); otherwise callers
+// keep score_tile_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kJoinSentChunk = 128;
+
+__global__ void __launch_bounds__(64, 8) hits_doc_kernel(bm_sentences S, bm_docs D, bm_lexicon L,
+                                                         const int4* __restrict__ items,
+                                                         int n_items,
+                                                         const int64_t* __restrict__ h_off,
+                                                         uint32_t* __restrict__ hits) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int4 it = items[blockIdx.x];
+  const int d = it.x, dir = it.y, k0 = it.z, k1 = it.w;
+  const int n = D.n[d], m = D.m[d];
+  const int s0 = D.src0[d], t0 = D.tgt0[d];
+  JoinSmem js = carve_join(smem);
+  uint16_t* chunk_owner = (uint16_t*)(smem + align16(join_smem_bytes()));
+  uint16_t* a_owner = chunk_owner + kJoinEmax;
+  uint32_t* hd = hits + h_off[d];
+  const int a0 = dir == 0 ? s0 : t0, b0 = dir == 0 ? t0 : s0;
+  const int na = dir == 0 ? n : m, nb = dir == 0 ? m : n;
+  const int32_t* offA = S.tok_off + a0;
+  const int32_t* offB = S.tok_off + b0;
+  const int32_t* off = dir == 0 ? L.fwd_off : L.rev_off;
+  const int32_t* cand = dir == 0 ? L.fwd_cand : L.rev_cand;
+  const int c_end = __ldg(offB + k1);
+  for (int c0 = __ldg(offB + k0); c0 < c_end; c0 += kJoinEmax) {
+    const int c1 = min(c_end, c0 + kJoinEmax);
+    if (dir == 0)
+      join_chunk_entries(CtaGroup(), S, off, cand, offA, na, offB, b0, nb, c0, c1, js, chunk_owner,
+                         a_owner, [&](int ls, int lt, int w) {
+                           atomicAdd(hd + (int64_t)ls * m + lt, (uint32_t)w);
+                         });
+    else
+      join_chunk_entries(CtaGroup(), S, off, cand, offA, na, offB, b0, nb, c0, c1, js, chunk_owner,
+                         a_owner, [&](int lt, int ls, int w) {
+                           atomicAdd(hd + (int64_t)ls * m + lt, (uint32_t)w << 16);
+                         });
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
+    bm_sentences S, bm_docs D, Model M, const int4* __restrict__ tiles,
+    const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
+    const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
+    double* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* exp_tab = (uint64_t*)smem;
+  TileScalars* rows = (TileScalars*)(smem + kExpTableWords * 8);
+  TileScalars* cols = rows + 1;
+  const int4 tile = tiles[blockIdx.x];
+  const int doc = tile.x, r0 = tile.y, c0 = tile.z;
+  const int n = D.n[doc], m = D.m[doc];
+  const int ns = min(kTile, n - r0), nt = min(kTile, m - c0);
+  const int s0 = D.src0[doc] + r0, t0 = D.tgt0[doc] + c0;
+  stage_exp_table(exp_tab, threadIdx.x, blockDim.x);
+  for (int k = threadIdx.x; k < ns + nt; k += blockDim.x) {
+    const bool is_row = k < ns;
+    const int local = is_row ? k : k - ns;
+    SentScalars sc = load_scalars(S, is_row ? s0 + local : t0 + local);
+    TileScalars* dst = is_row ? rows : cols;
+    dst->T[local] = sc.T;
+    dst->P[local] = sc.P;
+    dst->nA[local] = sc.nA;
+    dst->nD[local] = sc.nD;
+    dst->d0[local] = sc.d0;
+    dst->pos[local] = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
+  }
+  __syncthreads();
+  const uint32_t* hd = hits + h_off[doc] + (int64_t)r0 * m + c0;
+  double* dst = out + s_off[doc] + (int64_t)r0 * pitch[doc] + c0;
+  const int64_t ld = pitch[doc];
+  for (int c = threadIdx.x; c < ns * nt; c += blockDim.x) {
+    const int i = c / nt, j = c - (c / nt) * nt;
+    const uint32_t hv = __ldg(hd + (int64_t)i * m + j);
+    dst[i * ld + j] = cell_score(S, M, exp_tab, get_scalars(*rows, i), get_scalars(*cols, j),
+                                 (int)(hv & 0xffffu), (int)(hv >> 16), rows->pos[i], cols->pos[j]);
+  }
+}
+
+size_t hits_doc_smem_bytes() { return align16(join_smem_bytes()) + (size_t)kJoinEmax * 4; }
+
+// Items of the document-level join for local docs 0..nd-1 (host side).
+void join_items(const int32_t* n, const int32_t* m, int nd, std::vector<int4>& items) {
+  items.clear();
+  for (int d = 0; d < nd; ++d) {
+    if (n[d] <= 0 || m[d] <= 0) continue;
+    for (int k = 0; k < m[d]; k += kJoinSentChunk)
+      items.push_back(make_int4(d, 0, k, std::min(m[d], k + kJoinSentChunk)));
+    for (int k = 0; k < n[d]; k += kJoinSentChunk)
+      items.push_back(make_int4(d, 1, k, std::min(n[d], k + kJoinSentChunk)));
+  }
+}
+
+cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_lexicon& L,
+                              const Model& M, const int4* items, int n_items, uint32_t* hits,
+                              const int64_t* h_off, const int4* tiles, int n_tiles,
+                              const int64_t* s_off, const int32_t* pitch, double* out,
+                              cudaStream_t st) {
+  if (n_tiles == 0) return cudaSuccess;
+  const size_t hs = hits_doc_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(hits_doc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)hs);
+  if (e != cudaSuccess) return e;
+  if (n_items) hits_doc_kernel<<<n_items, 64, hs, st>>>(S, D, L, items, n_items, h_off, hits);
+  const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars);
+  score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, tiles, s_off, pitch, hits, h_off,
+                                                       out);
+  return counted(cudaGetLastError(), n_items ? 2 : 1);
+}
+
 size_t score_smem_bytes() {
-  return kExpTableWords * 8 + kTile * kTile * 4 + 2 * sizeof(TileScalars) + join_smem_bytes();
+  return kExpTableWords * 8 + kTile * kTile * 4 + 2 * sizeof(TileScalars) +
+         align16(join_smem_bytes()) + (size_t)(2 * kTile + 2) * 4 + (size_t)kJoinEmax * 4;
 }
 
 cudaError_t launch_score(const bm_sentences& S, const bm_docs& D, const bm_lexicon& L,

@@ -6,6 +6,8 @@
 
 #include <atomic>
 
+#include <vector>
+
 #include "bm_device.cuh"
 
 namespace bm {
@@ -124,6 +126,12 @@ cudaError_t launch_tune_count(const uint32_t*, const int64_t*, const double*, co
                               const int32_t*, const int32_t*, const int32_t*, int, const double*,
                               int, const int64_t*, const int64_t*, unsigned long long*,
                               unsigned long long*, cudaStream_t);
+void join_items(const int32_t* n, const int32_t* m, int nd, std::vector<int4>& items);
+cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_lexicon& L,
+                              const Model& M, const int4* items, int n_items, uint32_t* hits,
+                              const int64_t* h_off, const int4* tiles, int n_tiles,
+                              const int64_t* s_off, const int32_t* pitch, double* out,
+                              cudaStream_t st);
 cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int, int64_t*,
                            int64_t*, bm_record*, cudaStream_t, int doc0 = 0);
 size_t score_smem_bytes();
