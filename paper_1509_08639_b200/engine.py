@@ -59,6 +59,7 @@ class DeviceCorpus:
     corpus: PackedCorpus
     tensors: dict
     sent: N.Sentences
+    max_tok: int = 0  # largest token count T of any sentence (routing input)
 
     @classmethod
     def upload(cls, corpus: PackedCorpus) -> "DeviceCorpus":
@@ -67,7 +68,15 @@ class DeviceCorpus:
                  "dig_id")
         t = {k: to_dev(getattr(corpus, k), dev) for k in names}
         sent = N.Sentences(corpus.n_sent, *[_ptr(t[k]) for k in names])
-        return cls(corpus, t, sent)
+        return cls(corpus, t, sent, int(corpus.n_tok.max(initial=0)))
+
+    def doc_token_max(self, view: "DocView") -> np.ndarray:
+        """Per-doc max T of the view's docs (bm_mine's routing input). When no
+        sentence of the corpus exceeds 255 tokens the bound is all a doc needs,
+        so the per-doc scan is skipped; otherwise it is computed once per view."""
+        if self.max_tok <= 255:
+            return np.full(len(view.n), self.max_tok, dtype=np.int32)
+        return view.token_max(self.corpus)
 
 
 @dataclass
@@ -115,10 +124,15 @@ class DocView:
         return cls.upload(s0, n, t0, m)
 
     def token_max(self, corpus: PackedCorpus) -> np.ndarray:
+        cached = getattr(self, "_tmax", None)
+        if cached is not None and cached[0] is corpus:
+            return cached[1]
         view = PackedCorpus(corpus.n_tok, corpus.n_punct, corpus.n_alpha, corpus.tok_off,
                             corpus.tok_id, corpus.tok_alpha, corpus.dig_off, corpus.dig_id,
                             self.src0, self.n, self.tgt0, self.m)
-        return view.doc_token_max()
+        out = view.doc_token_max()
+        self._tmax = (corpus, out)
+        return out
 
 
 def _i64(x) -> np.ndarray:
@@ -242,7 +256,7 @@ def mine(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, threshold: f
     cnt = torch.zeros(max(k, 1), dtype=torch.int32, device=dev)
     cost = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
     rec_off_d = to_dev(rec_off, dev)
-    amax = view.token_max(dc.corpus)
+    amax = dc.doc_token_max(view)
     n_h, m_h, a_h = _i32(n), _i32(m), _i32(amax)
     N.check(lib.bm_mine(C.byref(dc.sent), C.byref(docs), n_h.ctypes.data, m_h.ctypes.data,
                         a_h.ctypes.data, C.byref(lex), C.byref(N.model_struct(model)),
