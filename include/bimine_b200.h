@@ -237,12 +237,14 @@ int bm_mine_host_wire(const bm_wire* wire_h, const bm_docs* docs_h, const bm_lex
  * pred[k*n_thr + l] += #diagonal moves with S >= t_l over all docs, and
  * hit[k*n_thr + l] += those whose (i, j) is in the doc's gold set.
  * gold: per doc ascending keys i*m + j at gold + gold_off[d] (gold_off[n_docs]).
+ * token_bound: an upper bound of the token count of every sentence of the
+ * docs (enables the document-level join for scoring), or -1 if unknown.
  */
 int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
             const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
             const double* penalties_host, int32_t n_pen, const double* thresholds, int32_t n_thr,
             const int64_t* gold, const int64_t* gold_off, unsigned long long* pred,
-            unsigned long long* hit, void* stream);
+            unsigned long long* hit, int32_t token_bound, void* stream);
 
 /* Exclusive-scan compaction of per-doc record slots into a dense,
  * document-ordered array; *total (device) receives the record count. */

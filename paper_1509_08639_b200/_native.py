@@ -97,7 +97,8 @@ _SIGS = {
                                     C.POINTER(ModelC), C.c_double, C.c_double, _p, C.c_int64,
                                     C.POINTER(C.c_int64), _p, _p]),
     "bm_tune": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, C.POINTER(LexiconC),
-                          C.POINTER(ModelC), _p, C.c_int32, _p, C.c_int32, _p, _p, _p, _p, _p]),
+                          C.POINTER(ModelC), _p, C.c_int32, _p, C.c_int32, _p, _p, _p, _p,
+                          C.c_int32, _p]),
     "bm_compact": (C.c_int, [_p, _p, _p, C.c_int32, _p, _p, _p]),
     "bm_ingest_jsonl": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32]),
     "bm_ingest_free": (None, [C.c_void_p]),

@@ -979,7 +979,7 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
             const int32_t* m_host, const bm_lexicon* lex, const bm_model* model,
             const double* penalties_host, int32_t n_pen, const double* thresholds, int32_t n_thr,
             const int64_t* gold, const int64_t* gold_off, unsigned long long* pred,
-            unsigned long long* hit, void* stream) {
+            unsigned long long* hit, int32_t token_bound, void* stream) {
   BM_CK(ensure_quot_table(), "quotient table");
   cudaStream_t st = (cudaStream_t)stream;
   for (int k = 0; k < n_pen; ++k)
@@ -993,9 +993,9 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   if (rc) return rc;
   const int k = (int)g.docs.size();
   const bm_docs D = local_docs(dv, k);
-  BM_CK(launch_score(*sent, D, *lex, to_model(model), dv.tiles, (int)g.tiles.size(), dv.s_off,
-                     dv.pitch, dv.S, st),
-        "score_tile_kernel");
+  rc = score_general(g, sent, D, lex, to_model(model), dv,
+                     token_bound >= 0 && token_bound <= 65535, sc, st);
+  if (rc) return rc;
   double* cost_l = nullptr;
   BM_CK(sc.alloc(&cost_l, k), "alloc");
   for (int q = 0; q < n_pen; ++q) {

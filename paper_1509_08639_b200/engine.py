@@ -280,9 +280,23 @@ def tune_counts(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, penal
     docs, lex, n, m = view.docs, dl.lex, view.n, view.m
     pen = np.ascontiguousarray(np.asarray(penalties, dtype=np.float64))
     thr = np.asarray(thresholds, dtype=np.float64)
+    # per-doc ascending gold keys, packed with one vectorised sort
+    lens = np.fromiter((len(g) for g in gold_keys), dtype=np.int64, count=len(gold_keys))
     goff = np.zeros(len(gold_keys) + 1, dtype=np.int64)
-    goff[1:] = np.cumsum([len(g) for g in gold_keys])
-    gall = np.concatenate([np.sort(np.asarray(g, dtype=np.int64)) for g in gold_keys]) if gold_keys else np.zeros(0, np.int64)
+    np.cumsum(lens, out=goff[1:])
+    if lens.sum():
+        keys = np.concatenate([np.asarray(g, dtype=np.int64).ravel() for g in gold_keys])
+        step = np.diff(keys)
+        inner = goff[1:-1]
+        step[inner[(inner > 0) & (inner < keys.size)] - 1] = 0  # doc boundaries may descend
+        if (step < 0).any():  # sort within docs: one sort of (doc << 40 | key)
+            if keys.min() < 0 or keys.max() >= (1 << 40):
+                raise ValueError("gold keys must lie in [0, 2**40)")
+            owner = np.repeat(np.arange(len(gold_keys), dtype=np.int64), lens)
+            keys = np.sort((owner << 40) | keys) & ((1 << 40) - 1)
+        gall = np.ascontiguousarray(keys)
+    else:
+        gall = np.zeros(0, np.int64)
     pred = torch.zeros((len(pen), len(thr)), dtype=torch.int64, device=dev)
     hit = torch.zeros((len(pen), len(thr)), dtype=torch.int64, device=dev)
     thr_d, gall_d, goff_d = to_dev(thr, dev), to_dev(gall, dev), to_dev(goff, dev)
@@ -290,7 +304,7 @@ def tune_counts(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, penal
     N.check(lib.bm_tune(C.byref(dc.sent), C.byref(docs), n_h.ctypes.data, m_h.ctypes.data,
                         C.byref(lex), C.byref(N.model_struct(model)), pen.ctypes.data, len(pen),
                         _ptr(thr_d), len(thr), _ptr(gall_d), _ptr(goff_d), _ptr(pred), _ptr(hit),
-                        stream_ptr()))
+                        dc.max_tok, stream_ptr()))
     return pred.cpu().numpy(), hit.cpu().numpy()
 
 
