@@ -468,6 +468,8 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   for (int d = 0; d < nd; ++d) {
     const int n = n_host[d], m = m_host[d];
     if (n <= 0 || m <= 0) continue;
+    // hit counts are 16-bit fields: a sentence may hold at most 65535 tokens
+    if (amax_host[d] > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
     const int R = fused_rows_per_lane(n);
     const size_t sl = ring_slice_bytes(n, m, R);
     if (!force_banded && n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax_host[d] <= 255) {
@@ -721,6 +723,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     for (int d = 0; d < nd; ++d) {
       const int n = dh->n[d], m = dh->m[d];
       if (n <= 0 || m <= 0) continue;
+      if (amax[d] > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
       const int R = fused_rows_per_lane(n);
       const size_t sl = ring_slice_bytes(n, m, R);
       if (!force_banded && n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax[d] <= 255) {
@@ -985,6 +988,7 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   for (int k = 0; k < n_pen; ++k)
     if (!check_penalty(penalties_host[k])) return fail(BM_EINVAL, "penalty must be >= 0");
   if (n_thr > 64) return fail(BM_EINVAL, "at most 64 thresholds per call");
+  if (token_bound > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
   GeneralPlan g;
   for (int d = 0; d < docs->n_docs; ++d) g.add(d, n_host[d], m_host[d]);
   Scratch sc(st);

@@ -192,11 +192,20 @@ def mine_corpus_file(
     c = nc.packed
     n = c.n.astype(np.int64)
     m = c.m.astype(np.int64)
-    skip = (n * m > aligner.MAX_CELLS).astype(np.uint8)
+    from .miner import MAX_SENTENCE_TOKENS
+
+    over = n * m > aligner.MAX_CELLS
+    tmax = c.doc_token_max() if int(c.n_tok.max(initial=0)) > MAX_SENTENCE_TOKENS else None
+    skip = (over | (tmax > MAX_SENTENCE_TOKENS if tmax is not None else False)).astype(np.uint8)
     for k in np.nonzero(skip)[0].tolist():
-        a, b = (int(c.m[k]), int(c.n[k])) if sw_f[k] else (int(c.n[k]), int(c.m[k]))
-        log.warning("skipping: %s", f"document pair {nc.doc_ids[k]!r} needs a {a}x{b} matrix, "
-                                    f"over the {aligner.MAX_CELLS} cell limit")
+        if over[k]:
+            a, b = (int(c.m[k]), int(c.n[k])) if sw_f[k] else (int(c.n[k]), int(c.m[k]))
+            why = (f"document pair {nc.doc_ids[k]!r} needs a {a}x{b} matrix, "
+                   f"over the {aligner.MAX_CELLS} cell limit")
+        else:
+            why = (f"document pair {nc.doc_ids[k]!r} has a sentence of {int(tmax[k])} tokens, "
+                   f"over the {MAX_SENTENCE_TOKENS} token limit")
+        log.warning("skipping: %s", why)
     work = np.nonzero(skip == 0)[0].astype(np.int64)
     rec_dtype = np.dtype(N.RECORD_DTYPE)
     fwd = np.zeros(0, dtype=rec_dtype)

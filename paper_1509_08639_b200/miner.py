@@ -109,6 +109,23 @@ def _cap_error(pair: DocumentPair, swapped: bool) -> ResourceLimitError | None:
     return None
 
 
+# hit counts are 16-bit fields on the device (csrc: hits_kernel, K1)
+MAX_SENTENCE_TOKENS = 65535
+
+
+def _token_cap_error(pair: DocumentPair) -> ResourceLimitError | None:
+    """This implementation's own hard bound (not the reference's): a sentence
+    with more than MAX_SENTENCE_TOKENS tokens is skipped like an over-cap
+    matrix, with a ResourceLimitError reason."""
+    for s in pair.source.sentences + pair.target.sentences:
+        if len(s.tokens) > MAX_SENTENCE_TOKENS:
+            return ResourceLimitError(
+                f"document pair {pair.id!r} has a sentence of {len(s.tokens)} tokens, over the "
+                f"{MAX_SENTENCE_TOKENS} token limit"
+            )
+    return None
+
+
 class _Pass:
     """One model direction over a packed batch (lexicon uploaded once)."""
 
@@ -190,6 +207,8 @@ def mine_documents(
             pairs = pairs[:k]
             results = results[:k]
             break
+        if cap is None:
+            cap = _token_cap_error(pair)
         if cap is not None:
             results[k] = ([], str(cap))
             continue

@@ -331,6 +331,31 @@ def test_mine_long_sentences_general_path(oracle_mod):
         [(int(a), int(b), float(c)) for a, b, c in zip(recs["i"], recs["j"], recs["conf"])]
 
 
+def test_sentence_over_the_token_bound_is_skipped(world500, tmp_path):
+    """A sentence longer than 65535 tokens (16-bit device hit counts) is this
+    implementation's own hard limit: the document is skipped with a
+    ResourceLimitError reason, like an over-cap matrix; the rest is mined as
+    usual, through both the Python and the native JSONL paths."""
+    from paper_1509_08639_b200.miner import MAX_SENTENCE_TOKENS
+
+    lex, fwd, bwd = world500
+    docs = load_docs("docs40.jsonl")[:3]
+    words = ["w" + "".join(chr(97 + (k // 26 ** e) % 26) for e in range(4)) for k in range(70000)]
+    big = dict(docs[1], id="big", src=[" ".join(words) + "."] + docs[1]["src"][1:])
+    cfg = bm.MinerConfig(bm.MiningParams(0.5, 0.2))
+    want, _ = _mine_text(pairs_of([docs[0], docs[2]]), fwd, bwd, lex)
+    got, rep = _mine_text(pairs_of([docs[0], big, docs[2]]), fwd, bwd, lex)
+    assert got == want and json.loads(rep)["docs_skipped"] == 1
+    p = str(tmp_path / "big.jsonl")
+    with open(p, "w") as fh:
+        for d in (docs[0], big, docs[2]):
+            fh.write(json.dumps(d) + "\n")
+    sink = io.StringIO()
+    rep2 = bm.mine_corpus_file(p, fwd, bwd, lex, cfg, sink)
+    assert sink.getvalue() == want and rep2.docs_skipped == 1
+    assert len(words) > MAX_SENTENCE_TOKENS
+
+
 def test_synth_text_round_trip_same_records():
     """Packed-by-generator and packed-from-text corpora mine identically."""
     from paper_1509_08639_b200 import engine, synth
