@@ -719,8 +719,6 @@ __device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int
   win_load(win + fu * kWinWords, dd, nbands, ngroups, cb - 1, cw, lane);
   asm volatile("cp.async.wait_group 2;" ::: "memory");
   __syncwarp();
-  int wkey = -1;
-  uint32_t word = 0;
   while (i > 0 && j > 0) {
     const int li = i - 1, lj = j - 1;
     const int b = li / kBandRows, w = lj >> 7;
@@ -747,17 +745,23 @@ __device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int
       cw = w;
       win_load(win + fl * kWinWords, dd, nbands, ngroups, cb, cw - 1, lane);
       win_load(win + fu * kWinWords, dd, nbands, ngroups, cb - 1, cw, lane);
-      wkey = -1;
     }
-    const int key = (((lj >> 2) & 31) << 5) | ((li & (kBandRows - 1)) >> 2);
-    if (key != wkey) {
-      word = win[cur * kWinWords + key];
-      wkey = key;
+    // the 4x4 block holding (li, lj): one code word, walked in registers
+    // until the path leaves the block (the per-step dependency chain is
+    // shift / mask / two compares; block lookups happen once per block)
+    const uint32_t word = win[cur * kWinWords + ((((lj >> 2) & 31) << 5) |
+                                                 ((li & (kBandRows - 1)) >> 2))];
+    int r = li & 3, c = lj & 3;
+    const int bi = li - r, bj = lj - c;
+    for (;;) {
+      const int op = (int)((word >> (8 * c + 2 * r)) & 3u);
+      visit(op, bi + r, bj + c);
+      r -= op != BM_MOVE_GT;
+      c -= op != BM_MOVE_GS;
+      if ((r | c) < 0) break;
     }
-    const int op = (int)((word >> (8 * (lj & 3) + 2 * (li & 3))) & 3u);
-    visit(op, li, lj);
-    i -= op != BM_MOVE_GT;
-    j -= op != BM_MOVE_GS;
+    i = bi + r + 1;
+    j = bj + c + 1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
@@ -777,14 +781,31 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) traceback_kernel(
   const int n = nn[d], m = mm[d];
   const int64_t base = mv_off[d];
   int k = 0;
+  // move k is held by lane k % 32 and written out 32 at a time (coalesced)
+  int8_t h_op = 0;
+  int32_t h_i = 0, h_j = 0;
   const int2 e = warp_walk(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
-    if (lane == 0) {
-      mv_op[base + k] = (int8_t)op;
-      mv_i[base + k] = op == BM_MOVE_GT ? -1 : i;
-      mv_j[base + k] = op == BM_MOVE_GS ? -1 : j;
+    if (lane == (k & 31)) {
+      h_op = (int8_t)op;
+      h_i = op == BM_MOVE_GT ? -1 : i;
+      h_j = op == BM_MOVE_GS ? -1 : j;
     }
-    ++k;
+    if ((++k & 31) == 0) {
+      const int64_t o = base + k - 32 + lane;
+      mv_op[o] = h_op;
+      mv_i[o] = h_i;
+      mv_j[o] = h_j;
+    }
   });
+  if (k & 31) {
+    const int kk = k & 31;
+    if (lane < kk) {
+      const int64_t o = base + k - kk + lane;
+      mv_op[o] = h_op;
+      mv_i[o] = h_i;
+      mv_j[o] = h_j;
+    }
+  }
   // border runs: GS down column 0, or GT along row 0 (lane-parallel)
   const int run = e.x > 0 ? e.x : e.y;
   for (int q = lane; q < run; q += WARP) {
