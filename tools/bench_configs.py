@@ -4,6 +4,7 @@
   C3  skewed corpus (n, m ~ LogNormal, 10..2000 sentences), both tiers
   C4  one 8192x8192 pair: DP-only GCUPS on the reference's random matrix
   C5  tuning sweep, 8 penalties x 8 thresholds, docs shaped like C2
+  C5w the worst case of 64 distinct penalties x 1 threshold
 
 Prints one JSON line per config. Usage: python tools/bench_configs.py [--c3-docs N] ...
 """
@@ -60,6 +61,38 @@ def c1(model, lex):
             "tsv_identical_to_reference": ok}
 
 
+def kernel_resident_ms(dc, dl, view, model, reps=3):
+    """bm_mine + bm_compact with inputs and records resident on the device
+    (SURVEY 8(d) "kernel-resident"); host planning inside bm_mine included."""
+    import ctypes as C
+    from paper_1509_08639_b200 import _native as N
+
+    lib = N.lib()
+    n_h, m_h = np.ascontiguousarray(view.n, np.int32), np.ascontiguousarray(view.m, np.int32)
+    amax = np.ascontiguousarray(dc.doc_token_max(view), np.int32)
+    dev = torch.device("cuda")
+    rec_off = engine.record_offsets(n_h, m_h)
+    cap = int(np.minimum(n_h, m_h).sum())
+    rec = torch.empty(max(cap, 1) * 24, dtype=torch.uint8, device=dev)
+    dense = torch.empty_like(rec)
+    cnt = torch.zeros(max(len(n_h), 1), dtype=torch.int32, device=dev)
+    cost = torch.empty(max(len(n_h), 1), dtype=torch.float64, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    rod = engine.to_dev(rec_off, dev)
+    ms = N.model_struct(model)
+    sp = int(torch.cuda.current_stream().cuda_stream)
+
+    def step():
+        N.check(lib.bm_mine(C.byref(dc.sent), C.byref(view.docs), n_h.ctypes.data, m_h.ctypes.data,
+                            amax.ctypes.data, C.byref(dl.lex), C.byref(ms), 0.5, 0.2,
+                            engine._ptr(rod), engine._ptr(rec), engine._ptr(cnt), engine._ptr(cost),
+                            sp))
+        N.check(lib.bm_compact(engine._ptr(rec), engine._ptr(rod), engine._ptr(cnt), len(n_h),
+                               engine._ptr(dense), engine._ptr(total), sp))
+
+    return cuda_ms(step, reps=reps)
+
+
 def c3(model, n_docs, check_docs):
     g, a, b = synth.c3_shape(n_docs, seed=2026)
     sc = synth.make_corpus(g, a, b, seed=2026)
@@ -70,8 +103,10 @@ def c3(model, n_docs, check_docs):
     view = engine.DocView.of(c)
     cells = int((c.n.astype(np.int64) * c.m).sum())
     res = {}
-    ms = cuda_ms(lambda: res.__setitem__("r", engine.mine(dc, dl, view, model, 0.5, 0.2)), reps=3)
+    ms_host = cuda_ms(lambda: res.__setitem__("r", engine.mine(dc, dl, view, model, 0.5, 0.2)),
+                      reps=3)
     recs, cost = res["r"]
+    ms = kernel_resident_ms(dc, dl, view, model)
     fused = int(((c.n <= 256) & (c.n.astype(np.int64) * c.m <= 40000)).sum())
     # parity on a stratified sample: every k-th document, through the oracle
     idx = np.linspace(0, n_docs - 1, min(check_docs, n_docs)).astype(np.int64)
@@ -81,8 +116,11 @@ def c3(model, n_docs, check_docs):
     got = recs[sel].copy()
     got["doc"] = np.searchsorted(idx, got["doc"])
     ok = got.tobytes() == want.tobytes() and np.array_equal(cost[idx].view(np.uint64), wcost.view(np.uint64))
-    return {"config": f"C3 skewed corpus, {n_docs} docs", "cells": cells, "ms": ms,
-            "doc_pairs_per_s": n_docs / (ms / 1e3), "gcups": cells / (ms / 1e3) / 1e9,
+    return {"config": f"C3 skewed corpus, {n_docs} docs", "cells": cells,
+            "ms": ms, "doc_pairs_per_s": n_docs / (ms / 1e3), "gcups": cells / (ms / 1e3) / 1e9,
+            "timing": "kernel-resident: bm_mine + bm_compact on device buffers (CUDA events)",
+            "ms_to_host": ms_host,
+            "doc_pairs_per_s_to_host": n_docs / (ms_host / 1e3),
             "records": int(recs.shape[0]), "fused_tier_docs_approx": fused,
             "oracle_sample_docs": int(idx.size), "bit_exact_on_sample": bool(ok)}
 
@@ -128,6 +166,22 @@ def c5(model, n_docs, check_docs):
             "oracle_sample_docs": k, "counts_identical_on_sample": bool(np.array_equal(sp, wp) and np.array_equal(sh, wh))}
 
 
+def c5w(model, n_docs):
+    """C5 worst case: 64 distinct penalties x 1 threshold."""
+    sc = synth.make_corpus(*synth.c2_shape(n_docs), seed=55)
+    c = sc.packed
+    plex = sc.world.packed_lexicon()
+    pens = [0.025 * (k + 1) for k in range(64)]
+    keys = [np.asarray(gd[:, 0] * int(c.m[d]) + gd[:, 1], np.int64) for d, gd in enumerate(sc.gold)]
+    dc = engine.DeviceCorpus.upload(c)
+    dl = engine.DeviceLexicon.upload(plex)
+    view = engine.DocView.of(c)
+    ms = cuda_ms(lambda: engine.tune_counts(dc, dl, view, model, pens, [0.5], keys), reps=2)
+    cells = int((c.n.astype(np.int64) * c.m).sum())
+    return {"config": f"C5 worst case: {n_docs} docs x 64 penalties x 1 threshold", "ms": ms,
+            "doc_pairs_per_s": n_docs / (ms / 1e3), "dp_gcups": cells * 64 / (ms / 1e3) / 1e9}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c3-docs", type=int, default=100000)
@@ -148,6 +202,8 @@ def main():
         print(json.dumps(c4(args.c4_check)), flush=True)
     if "c5" in todo:
         print(json.dumps(c5(model, args.c5_docs, args.check_docs)), flush=True)
+    if "c5w" in todo:
+        print(json.dumps(c5w(model, args.c5_docs)), flush=True)
 
 
 if __name__ == "__main__":
