@@ -210,8 +210,7 @@ int general_nw(const GeneralPlan& g, GeneralDev& dv, double penalty, double* cos
   a.bnd_off = dv.bnd_off;
   a.prog = dv.prog;
   a.prog_off = dv.prog_off;
-  const int warps = std::min<int>(nw_resident_warps(), a.n_items);
-  BM_CK(launch_nw(a, warps, st), "nw_band_kernel");
+  BM_CK(launch_nw(a, st), "nw_band_kernel");
   return BM_OK;
 }
 
@@ -415,7 +414,7 @@ int bm_nw(const double* S, const int64_t* s_off, const int32_t* pitch, const int
   a.bnd_off = dbo;
   a.prog = prog;
   a.prog_off = dpo;
-  BM_CK(launch_nw(a, std::min<int>(nw_resident_warps(), a.n_items), st), "nw_band_kernel");
+  BM_CK(launch_nw(a, st), "nw_band_kernel");
   return BM_OK;
 }
 

@@ -372,7 +372,7 @@ cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, doub
 // owns one band; lane L owns rows 4L..4L+3 and runs one 4-column group
 // behind lane L-1 (blocked wavefront, see nw_band_kernel).
 //  * S: every lane streams its own 4x4 blocks with cp.async (16-byte LDGSTS)
-//    into a private, bank-padded slice of a shared-memory ring kNwDepth
+//    into a private, bank-padded slice of a shared-memory ring D
 //    groups deep, so HBM latency is hidden ~32 columns ahead of use.
 //  * Bands hand their bottom row to the band below through global memory: the
 //    band's rows are pre-filled with a sentinel byte pattern, the producer lane
@@ -384,11 +384,12 @@ cudaError_t launch_confidence(const double* feats, int n_q, const Model& M, doub
 // atomic ticket, so a wait always targets a band that is resident or finished.
 // ---------------------------------------------------------------------------
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNwDepth = 8;                                 // groups in flight per lane
-constexpr int kNwSlots = kNwDepth + 1;                       // + a dummy slot
+// ring depth D (groups in flight per lane, a power of two) is a template
+// parameter: 8 for a few large matrices (one warp's latency hiding matters),
+// 4 when many (doc, band) items run at once (smaller rings -> more warps/SM)
 constexpr int kNwLane = kBandR * 4 + 2;                      // doubles per lane slice (+pad)
 constexpr int kNwSlotBytes = WARP * kNwLane * 8;
-constexpr int kNwSmem = kNwSlots * kNwSlotBytes + WARP * 8;  // ~41 KB per warp
+__host__ __device__ constexpr int nw_smem(int D) { return (D + 1) * kNwSlotBytes + WARP * 8; }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -405,8 +406,9 @@ __device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
+template <int D>
 __device__ __forceinline__ void cp_async_wait_depth() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(kNwDepth - 1) : "memory");
+  asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
 }
 
 // Blocked wavefront: per super-step t, lane L computes the 4x4 block of its
@@ -453,10 +455,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // next block, shuffles and stores with the 7-cell dependency chain of the
 // current one. S for block g+1 is loaded and turned into 1-S during block g
 // (two register sets, ping-pong by a 2x unrolled loop).
+template <int D>
 __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
+  static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
   extern __shared__ __align__(16) double nw_ring[];
   const int lane = threadIdx.x;
-  double* bnd_s = nw_ring + kNwSlots * WARP * kNwLane;  // current 32-column boundary chunk
+  double* bnd_s = nw_ring + (D + 1) * WARP * kNwLane;  // current 32-column boundary chunk
   const double* ring_l = nw_ring + (size_t)lane * kNwLane;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring_l);
   for (;;) {
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     auto issue = [&](int gi) {
       const bool ok = (unsigned)gi < (unsigned)ngroups;
       const int c = ok ? gi * 4 : 0;
-      const uint32_t dst = ring_s + (uint32_t)((ok ? (gi & (kNwDepth - 1)) : kNwDepth) * kNwSlotBytes);
+      const uint32_t dst = ring_s + (uint32_t)((ok ? (gi & (D - 1)) : D) * kNwSlotBytes);
       cp_async16_s(dst + 0, src0 + c);
       cp_async16_s(dst + 16, src0 + c + 2);
       cp_async16_s(dst + 32, src1 + c);
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
       cp_async_commit();
     };
     auto load = [&](int gi, double(&o)[16]) {
-      const double* cur = ring_l + (size_t)(gi & (kNwDepth - 1)) * (WARP * kNwLane);
+      const double* cur = ring_l + (size_t)(gi & (D - 1)) * (WARP * kNwLane);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const double2 s = *(const double2*)(cur + 2 * q);
@@ -515,8 +519,8 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     };
     __syncwarp();
 #pragma unroll 1
-    for (int q = 0; q < kNwDepth; ++q) issue(q - lane);
-    cp_async_wait_depth();
+    for (int q = 0; q < D; ++q) issue(q - lane);
+    cp_async_wait_depth<D>();
     double oA[16], oB[16];
     load(-lane, oA);
 
@@ -579,8 +583,8 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
         l3 = il3;
         dgn = idg;
       }
-      issue(g + kNwDepth);
-      cp_async_wait_depth();  // block g+1 has landed
+      issue(g + D);
+      cp_async_wait_depth<D>();  // block g+1 has landed
       load(g + 1, on);
 
       // the 4x4 block, anti-diagonal order
@@ -646,28 +650,34 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   }
 }
 
-cudaError_t launch_nw(const NwArgs& a, int n_warps, cudaStream_t st) {
-  if (a.n_items == 0) return cudaSuccess;
-  static const int pad = getenv("BM_NW_SMEM") ? atoi(getenv("BM_NW_SMEM")) : kNwSmem;
-  const int smem = pad > kNwSmem ? pad : kNwSmem;
-  cudaError_t e = cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return e;
-  nw_band_kernel<<<n_warps, WARP, smem, st>>>(a);
-  return counted(cudaGetLastError());
+template <int D>
+int nw_resident(int sms) {
+  int per_sm = 0;
+  cudaFuncSetAttribute(nw_band_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, nw_smem(D));
+  cudaFuncSetAttribute(nw_band_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel<D>, WARP, nw_smem(D));
+  return sms * std::max(per_sm, 1);
 }
 
-int nw_resident_warps() {
-  int dev = 0, sms = 0, per_sm = 0;
+// Persistent grid of min(resident warps, items); a shallow ring when the items
+// outnumber the warps a deep ring allows.
+cudaError_t launch_nw(const NwArgs& a, cudaStream_t st) {
+  if (a.n_items == 0) return cudaSuccess;
+  int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem);
-  cudaFuncSetAttribute(nw_band_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel, WARP, kNwSmem);
-  if (per_sm < 1) per_sm = 1;
-  return sms * per_sm;
+  static thread_local int r8 = 0, r4 = 0, dev_of = -1;
+  if (dev_of != dev) {
+    r8 = nw_resident<8>(sms);
+    r4 = nw_resident<4>(sms);
+    dev_of = dev;
+  }
+  if (a.n_items > r8) {
+    nw_band_kernel<4><<<std::min(r4, a.n_items), WARP, nw_smem(4), st>>>(a);
+  } else {
+    nw_band_kernel<8><<<std::min(r8, a.n_items), WARP, nw_smem(8), st>>>(a);
+  }
+  return counted(cudaGetLastError());
 }
 
 // ---------------------------------------------------------------------------

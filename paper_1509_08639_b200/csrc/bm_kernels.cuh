@@ -115,8 +115,7 @@ cudaError_t launch_score(const bm_sentences&, const bm_docs&, const bm_lexicon&,
 cudaError_t launch_features(const bm_sentences&, const bm_lexicon&, const int32_t*, const int32_t*,
                             const double*, const double*, int, double*, cudaStream_t);
 cudaError_t launch_confidence(const double*, int, const Model&, double*, cudaStream_t);
-cudaError_t launch_nw(const NwArgs&, int, cudaStream_t);
-int nw_resident_warps();
+cudaError_t launch_nw(const NwArgs&, cudaStream_t);
 cudaError_t launch_traceback(const uint32_t*, const int64_t*, const int32_t*, const int32_t*, int,
                              const int64_t*, int8_t*, int32_t*, int32_t*, int32_t*, cudaStream_t);
 cudaError_t launch_extract(const uint32_t*, const int64_t*, const double*, const int64_t*,
