@@ -84,11 +84,11 @@ inline int32_t pitch_of(int32_t m) { return (m + 3) & ~3; }
 // Unfused general path for a subset of documents: K1 -> K2/K3 -> consumer.
 struct GeneralPlan {
   std::vector<int32_t> docs;  // indices into the batch
-  std::vector<int64_t> s_off, dir_off, bnd_off, prog_off;
+  std::vector<int64_t> s_off, dir_off, bnd_off;
   std::vector<int32_t> pitch, n, m;
   std::vector<int4> tiles;    // doc field = local index
   std::vector<WorkItem> items;
-  int64_t s_total = 0, dir_total = 0, bnd_total = 0, prog_total = 0;
+  int64_t s_total = 0, dir_total = 0, bnd_total = 0;
 
   void add(int32_t d, int32_t nd, int32_t md) {
     const int32_t local = (int32_t)docs.size();
@@ -103,8 +103,6 @@ struct GeneralPlan {
     const int nb = (nd + kBandRows - 1) / kBandRows;
     bnd_off.push_back(bnd_total);
     bnd_total += (int64_t)(nb - 1) * md;
-    prog_off.push_back(prog_total);
-    prog_total += nb;
     for (int r0 = 0; r0 < nd; r0 += kTile)
       for (int c0 = 0; c0 < md; c0 += kTile) tiles.push_back(make_int4(local, r0, c0, 0));
     for (int b = 0; b < nb; ++b) items.push_back(WorkItem{local, b});
@@ -113,12 +111,12 @@ struct GeneralPlan {
 
 // Device copies of a GeneralPlan plus the subset's own bm_docs view.
 struct GeneralDev {
-  int64_t *s_off, *dir_off, *bnd_off, *prog_off;
+  int64_t *s_off, *dir_off, *bnd_off;
   int32_t *pitch, *n, *m, *src0, *tgt0;
   int4* tiles;
   WorkItem* items;
   double *S, *bnd;
-  uint32_t *dirs, *prog;
+  uint32_t* dirs;
   unsigned int* ticket;
 };
 
@@ -158,7 +156,6 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
   BM_CK(sc.upload(&dv.s_off, g.s_off), "upload");
   BM_CK(sc.upload(&dv.dir_off, g.dir_off), "upload");
   BM_CK(sc.upload(&dv.bnd_off, g.bnd_off), "upload");
-  BM_CK(sc.upload(&dv.prog_off, g.prog_off), "upload");
   BM_CK(sc.upload(&dv.pitch, g.pitch), "upload");
   BM_CK(sc.upload(&dv.n, g.n), "upload");
   BM_CK(sc.upload(&dv.m, g.m), "upload");
@@ -169,7 +166,6 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
   BM_CK(sc.alloc(&dv.S, (size_t)g.s_total), "alloc S");
   BM_CK(sc.alloc(&dv.dirs, (size_t)g.dir_total), "alloc dirs");
   BM_CK(sc.alloc(&dv.bnd, (size_t)g.bnd_total), "alloc boundary");
-  BM_CK(sc.alloc(&dv.prog, (size_t)g.prog_total), "alloc progress");
   BM_CK(sc.alloc(&dv.ticket, 1), "alloc ticket");
   gather_docs_kernel<<<(k + 255) / 256, 256, 0, st>>>(*docs, idx, k, dv.src0, dv.tgt0);
   BM_CK(cudaGetLastError(), "gather_docs");
@@ -189,7 +185,6 @@ bm_docs local_docs(const GeneralDev& dv, int k) {
 
 int general_nw(const GeneralPlan& g, GeneralDev& dv, double penalty, double* cost,
                cudaStream_t st) {
-  BM_CK(cudaMemsetAsync(dv.prog, 0, std::max<int64_t>(g.prog_total, 1) * 4, st), "memset");
   BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
   // boundary rows start as the sentinel (negative) pattern consumers spin on
   BM_CK(cudaMemsetAsync(dv.bnd, 0xde, std::max<int64_t>(g.bnd_total, 1) * 8, st), "memset");
@@ -208,8 +203,6 @@ int general_nw(const GeneralPlan& g, GeneralDev& dv, double penalty, double* cos
   a.ticket = dv.ticket;
   a.bnd = dv.bnd;
   a.bnd_off = dv.bnd_off;
-  a.prog = dv.prog;
-  a.prog_off = dv.prog_off;
   BM_CK(launch_nw(a, st), "nw_band_kernel");
   return BM_OK;
 }
@@ -372,30 +365,24 @@ int bm_nw(const double* S, const int64_t* s_off, const int32_t* pitch, const int
   if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<WorkItem> items;
-  std::vector<int64_t> bnd_off(n_docs), prog_off(n_docs);
-  int64_t bt = 0, pt = 0;
+  std::vector<int64_t> bnd_off(n_docs);
+  int64_t bt = 0;
   for (int d = 0; d < n_docs; ++d) {
     const int nb = (n_host[d] + kBandRows - 1) / kBandRows;
     bnd_off[d] = bt;
     bt += (int64_t)std::max(nb - 1, 0) * m_host[d];
-    prog_off[d] = pt;
-    pt += nb;
     for (int b = 0; b < nb; ++b) items.push_back(WorkItem{d, b});
   }
   Scratch sc(st);
   NwArgs a;
   WorkItem* di = nullptr;
-  int64_t *dbo = nullptr, *dpo = nullptr;
+  int64_t* dbo = nullptr;
   BM_CK(sc.upload(&di, items), "upload");
   BM_CK(sc.upload(&dbo, bnd_off), "upload");
-  BM_CK(sc.upload(&dpo, prog_off), "upload");
   double* bnd = nullptr;
-  uint32_t* prog = nullptr;
   unsigned int* ticket = nullptr;
   BM_CK(sc.alloc(&bnd, (size_t)bt), "alloc");
-  BM_CK(sc.alloc(&prog, (size_t)pt), "alloc");
   BM_CK(sc.alloc(&ticket, 1), "alloc");
-  BM_CK(cudaMemsetAsync(prog, 0, std::max<int64_t>(pt, 1) * 4, st), "memset");
   BM_CK(cudaMemsetAsync(ticket, 0, 4, st), "memset");
   BM_CK(cudaMemsetAsync(bnd, 0xde, std::max<int64_t>(bt, 1) * 8, st), "memset");
   a.S = S;
@@ -412,8 +399,6 @@ int bm_nw(const double* S, const int64_t* s_off, const int32_t* pitch, const int
   a.ticket = ticket;
   a.bnd = bnd;
   a.bnd_off = dbo;
-  a.prog = prog;
-  a.prog_off = dpo;
   BM_CK(launch_nw(a, st), "nw_band_kernel");
   return BM_OK;
 }

@@ -78,12 +78,6 @@ static inline cudaError_t counted(cudaError_t e, int n = 1) {
 }
 
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const double* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -94,10 +88,6 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const double* p) {
 // a negative double, and a DP cost is never negative (>= 0, +inf or NaN), so a
 // consumer can spin on the value itself -- no flag, no fence, no ERRBAR.
 constexpr uint64_t kBndSentinel = 0xdedededededededeull;
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 
 

@@ -88,8 +88,6 @@ struct NwArgs {
   unsigned int* ticket;
   double* bnd;               // boundary rows
   const int64_t* bnd_off;    // per doc: start of its (nb-1) x m boundary rows
-  uint32_t* prog;            // per band publication progress (columns)
-  const int64_t* prog_off;   // per doc
 };
 
 struct FusedArgs {

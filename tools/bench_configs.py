@@ -52,13 +52,15 @@ def c1(model, lex):
     doc = json.loads(open(path).read().strip())
     pair = bm.parse_document_pair(doc, "mem", 1)
     cfg = bm.MinerConfig(bm.MiningParams(0.5, 0.2))
-    t0 = time.perf_counter()
-    sink = io.StringIO()
-    bm.mine_corpus([pair], model, None, lex, cfg, sink)
-    wall = time.perf_counter() - t0
+    walls = []
+    for _ in range(3):  # first call: one-time device init; then steady state
+        t0 = time.perf_counter()
+        sink = io.StringIO()
+        bm.mine_corpus([pair], model, None, lex, cfg, sink)
+        walls.append(time.perf_counter() - t0)
     ok = sink.getvalue() == open(os.path.join(ROOT, "tests", "golden", "mine200_fwd.tsv")).read()
-    return {"config": "C1 200x200 single pair", "wall_ms_mine_corpus": 1e3 * wall,
-            "tsv_identical_to_reference": ok}
+    return {"config": "C1 200x200 single pair", "wall_ms_first_call": 1e3 * walls[0],
+            "wall_ms_mine_corpus": 1e3 * min(walls[1:]), "tsv_identical_to_reference": ok}
 
 
 def kernel_resident_ms(dc, dl, view, model, reps=3):
