@@ -32,7 +32,13 @@ namespace bm {
 constexpr int kProdWarps = 4;
 constexpr int kRingThreads = (kProdWarps + 1) * WARP;  // warp 0: DP, warps 1..4: scoring
 constexpr int kProducers = kProdWarps * WARP;
-constexpr int kSlots = 4;  // ring depth in super-steps
+#ifndef BM_RING_SLOTS
+#define BM_RING_SLOTS 2
+#endif
+#ifndef BM_RING_MINB
+#define BM_RING_MINB 6
+#endif
+constexpr int kSlots = BM_RING_SLOTS;  // ring depth in super-steps
 constexpr int kFixedBytes = kExpTableWords * 8 + 256;
 #ifndef BM_HITS_THREADS
 #define BM_HITS_THREADS 64
@@ -230,7 +236,7 @@ __device__ __forceinline__ int2 active_lanes(int t, int ngroups, int nl) {
 // 5 CTAs per SM (smem slices of C2-shaped documents fit 5); R = 8 blocks need
 // the registers of 4
 template <int R>
-__global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : 5) mine_ring_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_ring_kernel(FusedArgs a) {
   using CodeT = typename std::conditional<R == 8, uint64_t, uint32_t>::type;
   constexpr int RL = ring_lane(R);
   constexpr int BPT = 8 / R;  // lane blocks per 32-cell scoring task

@@ -9,5 +9,5 @@ name, defs = sys.argv[1], sys.argv[2:]
 out = os.path.join(ROOT, "tools", "_prof", name + ".so")
 os.makedirs(os.path.dirname(out), exist_ok=True)
 subprocess.check_call(["/usr/local/cuda/bin/nvcc", *B.NVCC_FLAGS, *[f"-D{d}" for d in defs],
-                       f"-I{B.INCLUDE}", f"-I{B.CSRC}", os.path.join(B.CSRC, "bm_lib.cu"), "-o", out])
+                       f"-I{B.INCLUDE}", f"-I{B.CSRC}", *[os.path.join(B.CSRC, s) for s in B.SOURCES], "-o", out])
 print(out)

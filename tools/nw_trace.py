@@ -20,7 +20,7 @@ def build():
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     extra = [f"-D{x}" for x in os.environ.get("BM_PROF_DEFS", "").split(",") if x]
     cmd = ["/usr/local/cuda/bin/nvcc", *B.NVCC_FLAGS, "-DBM_NW_PROFILE", *extra, f"-I{B.INCLUDE}", f"-I{B.CSRC}",
-           os.path.join(B.CSRC, "bm_lib.cu"), "-o", OUT]
+           *[os.path.join(B.CSRC, s) for s in B.SOURCES], "-o", OUT]
     subprocess.check_call(cmd)
 
 
