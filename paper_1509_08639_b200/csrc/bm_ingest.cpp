@@ -9,14 +9,20 @@
 //   pack.py                the packed per-sentence features (T, P, |A|, U, D)
 //   miner.py:131-155       bidirectional_merge (normalized-text key)
 //   miner.py:183-194,253   format_pair_line, _sanitize, unique-token counts
-// Exactness contract: the native path accepts a file only when every byte is
-// ASCII and the JSON stays inside a simple, fully validated subset; otherwise
-// bm_ingest_jsonl returns BM_EUNSUPPORTED and the caller runs the Python path
-// (which also produces the reference's error messages). Under that contract
-// Python's Unicode-aware str methods reduce to fixed ASCII tables:
-//   whitespace (str.isspace, re \s, split, strip) = 09-0D, 1C-1F, 20
-//   alnum / regex word chars without '_'        = [0-9A-Za-z]
-// and NFC is the identity.
+// Exactness contract: the native path accepts a file only when it is valid
+// UTF-8, its JSON stays inside a simple, fully validated subset, and all text
+// passes the checks below; otherwise bm_ingest_jsonl returns BM_EUNSUPPORTED
+// and the caller runs the Python path (which also produces the reference's
+// error messages). Character properties come from tables generated from the
+// reference's own CPython (gen_unicode_tables.py -> unicode_tables.h):
+//   SPACE (str.isspace = re \s = split/strip), ALNUM (isalnum = re \w minus
+//   '_'), ALPHA, DIGIT, UPPER, NFC quick-check Yes, combining class 0, and the
+//   one-code-point lowercase map. Accepted text has every code point NFC-QC
+//   Yes with no two adjacent non-starters -- so NFC(text) == text (UAX #15
+//   quick check) -- and every code point lowercases to one code point of the
+//   same classes (no final-sigma U+03A3), so str.lower() is the per-character
+//   map and lowering never moves a token boundary. Real text (e.g. Polish or
+//   English) passes; anything else goes to Python.
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -31,15 +37,154 @@
 #include <vector>
 
 #include "bimine_b200.h"
+#include "unicode_tables.h"
 
 namespace bm_ingest {
 
-inline bool is_space(unsigned char c) { return (c >= 0x09 && c <= 0x0d) || (c >= 0x1c && c <= 0x1f) || c == 0x20; }
-inline bool is_alpha(unsigned char c) { return (c >= 'A' && c <= 'Z') || (c >= 'a' && c <= 'z'); }
-inline bool is_digit(unsigned char c) { return c >= '0' && c <= '9'; }
-inline bool is_alnum(unsigned char c) { return is_alpha(c) || is_digit(c); }
-inline bool is_upper(unsigned char c) { return c >= 'A' && c <= 'Z'; }
-inline char lower(char c) { return (c >= 'A' && c <= 'Z') ? (char)(c + 32) : c; }
+inline uint8_t uprops(uint32_t cp) {
+  return bm_unicode::kBlocks[bm_unicode::kBlockIndex[cp >> 8]][cp & 255];
+}
+inline bool is_space(uint32_t c) {
+  return c < 128 ? ((c >= 0x09 && c <= 0x0d) || (c >= 0x1c && c <= 0x20)) : (uprops(c) & bm_unicode::SPACE) != 0;
+}
+inline bool is_alpha(uint32_t c) {
+  return c < 128 ? ((c >= 'A' && c <= 'Z') || (c >= 'a' && c <= 'z')) : (uprops(c) & bm_unicode::ALPHA) != 0;
+}
+inline bool is_digit(uint32_t c) {
+  return c < 128 ? (c >= '0' && c <= '9') : (uprops(c) & bm_unicode::DIGIT) != 0;
+}
+inline bool is_alnum(uint32_t c) {
+  return c < 128 ? (is_alpha(c) || is_digit(c)) : (uprops(c) & bm_unicode::ALNUM) != 0;
+}
+inline bool is_upper(uint32_t c) {
+  return c < 128 ? (c >= 'A' && c <= 'Z') : (uprops(c) & bm_unicode::UPPER) != 0;
+}
+// str.lower() of one accepted code point (LOWOK: a single code point)
+inline uint32_t lower_cp(uint32_t c) {
+  if (c < 128) return (c >= 'A' && c <= 'Z') ? c + 32 : c;
+  int lo = 0, hi = bm_unicode::kLowerCount;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (bm_unicode::kLower[mid][0] < c)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < bm_unicode::kLowerCount && bm_unicode::kLower[lo][0] == c) ? bm_unicode::kLower[lo][1] : c;
+}
+
+// UTF-8 of validated text: the code point at s[i], i advanced past it
+inline uint32_t decode(const char* s, size_t& i) {
+  const unsigned char c = (unsigned char)s[i];
+  if (c < 0x80) {
+    ++i;
+    return c;
+  }
+  const unsigned char* u = (const unsigned char*)s + i;
+  if (c < 0xE0) {
+    i += 2;
+    return ((uint32_t)(c & 0x1F) << 6) | (u[1] & 0x3F);
+  }
+  if (c < 0xF0) {
+    i += 3;
+    return ((uint32_t)(c & 0x0F) << 12) | ((uint32_t)(u[1] & 0x3F) << 6) | (u[2] & 0x3F);
+  }
+  i += 4;
+  return ((uint32_t)(c & 0x07) << 18) | ((uint32_t)(u[1] & 0x3F) << 12) |
+         ((uint32_t)(u[2] & 0x3F) << 6) | (u[3] & 0x3F);
+}
+// start of the code point that ends at byte i (i > 0)
+inline size_t prev_start(const char* s, size_t i) {
+  --i;
+  while (i > 0 && ((unsigned char)s[i] & 0xC0) == 0x80) --i;
+  return i;
+}
+inline void encode(std::string& o, uint32_t c) {
+  if (c < 0x80) {
+    o.push_back((char)c);
+  } else if (c < 0x800) {
+    o.push_back((char)(0xC0 | (c >> 6)));
+    o.push_back((char)(0x80 | (c & 0x3F)));
+  } else if (c < 0x10000) {
+    o.push_back((char)(0xE0 | (c >> 12)));
+    o.push_back((char)(0x80 | ((c >> 6) & 0x3F)));
+    o.push_back((char)(0x80 | (c & 0x3F)));
+  } else {
+    o.push_back((char)(0xF0 | (c >> 18)));
+    o.push_back((char)(0x80 | ((c >> 12) & 0x3F)));
+    o.push_back((char)(0x80 | ((c >> 6) & 0x3F)));
+    o.push_back((char)(0x80 | (c & 0x3F)));
+  }
+}
+
+// the next 8 bytes exist and are all ASCII
+inline bool ascii8(const void* p, size_t left) {
+  if (left < 8) return false;
+  uint64_t w;
+  memcpy(&w, p, 8);
+  return (w & 0x8080808080808080ull) == 0;
+}
+
+// Python's strict UTF-8 decoding (no surrogates, no overlongs, <= U+10FFFF)
+bool valid_utf8(const std::string& d) {
+  const unsigned char* s = (const unsigned char*)d.data();
+  const size_t n = d.size();
+  size_t i = 0;
+  while (i < n) {
+    if (ascii8(s + i, n - i)) {
+      i += 8;
+      continue;
+    }
+    const unsigned char c = s[i];
+    if (c < 0x80) {
+      ++i;
+      continue;
+    }
+    int len;
+    uint32_t cp, minv;
+    if (c >= 0xC2 && c <= 0xDF) {
+      len = 2, cp = c & 0x1F, minv = 0x80;
+    } else if (c >= 0xE0 && c <= 0xEF) {
+      len = 3, cp = c & 0x0F, minv = 0x800;
+    } else if (c >= 0xF0 && c <= 0xF4) {
+      len = 4, cp = c & 0x07, minv = 0x10000;
+    } else {
+      return false;
+    }
+    if (i + (size_t)len > n) return false;
+    for (int q = 1; q < len; ++q) {
+      if ((s[i + q] & 0xC0) != 0x80) return false;
+      cp = (cp << 6) | (s[i + q] & 0x3F);
+    }
+    if (cp < minv || cp > 0x10FFFF || (cp >= 0xD800 && cp <= 0xDFFF)) return false;
+    i += (size_t)len;
+  }
+  return true;
+}
+
+// Text the native path can normalize exactly (see the contract above).
+bool text_ok(const char* s, size_t n) {
+  size_t i = 0;
+  bool prev_nonstarter = false;
+  while (i < n) {
+    if (ascii8(s + i, n - i)) {
+      i += 8;
+      prev_nonstarter = false;
+      continue;
+    }
+    const uint32_t cp = decode(s, i);
+    if (cp < 128) {
+      prev_nonstarter = false;
+      continue;
+    }
+    const uint8_t p = uprops(cp);
+    if (!(p & bm_unicode::NFCYES) || !(p & bm_unicode::LOWOK)) return false;
+    const bool ns = !(p & bm_unicode::CCC0);
+    if (ns && prev_nonstarter) return false;
+    prev_nonstarter = ns;
+  }
+  return true;
+}
 
 // Open-addressing table of byte strings (arena-backed, looked up by pointer
 // + length, no allocation per lookup) -> int32 value.
@@ -149,36 +294,46 @@ struct Ingest {
 };
 
 // ------------------------------------------------------------------ tokens
-// tokenize (corpus.py:28): maximal [0-9A-Za-z] runs or one non-space char
+// tokenize (corpus.py:28): maximal alnum runs ([^\W_]+) or one non-space char
 template <class F>
 void for_tokens(const char* s, size_t len, F&& f) {
   size_t i = 0;
   while (i < len) {
-    const unsigned char c = (unsigned char)s[i];
-    if (is_space(c)) {
-      ++i;
-    } else if (is_alnum(c)) {
-      size_t j = i + 1;
-      while (j < len && is_alnum((unsigned char)s[j])) ++j;
-      f(s + i, j - i);
+    const size_t st = i;
+    const uint32_t c = decode(s, i);
+    if (is_space(c)) continue;
+    if (is_alnum(c)) {
+      size_t j = i;
+      while (j < len) {
+        size_t k2 = j;
+        if (!is_alnum(decode(s, k2))) break;
+        j = k2;
+      }
+      f(s + st, j - st);
       i = j;
     } else {
-      f(s + i, 1);
-      ++i;
+      f(s + st, i - st);
     }
   }
 }
 
-// normalize (corpus.py:38-40): NFC (identity on ASCII), lower, " ".join(split());
-// appended to o
+// normalize (corpus.py:38-40): NFC (identity on accepted text), lower(),
+// " ".join(split()); appended to o
 void normalize_into(std::string& o, const char* s, size_t len) {
   const size_t start = o.size();
   size_t i = 0;
+  bool pending_space = false;
   while (i < len) {
-    while (i < len && is_space((unsigned char)s[i])) ++i;
-    if (i >= len) break;
-    if (o.size() > start) o.push_back(' ');
-    while (i < len && !is_space((unsigned char)s[i])) o.push_back(lower(s[i++]));
+    const uint32_t c = decode(s, i);
+    if (is_space(c)) {
+      pending_space = o.size() > start;
+      continue;
+    }
+    if (pending_space) {
+      o.push_back(' ');
+      pending_space = false;
+    }
+    encode(o, lower_cp(c));
   }
 }
 
@@ -198,8 +353,8 @@ bool add_sentence(Ingest& g, const char* s, size_t len) {
       normalize_into(g.tmp, t, tl);
       ti.nid = g.intern(g.tmp.data(), g.tmp.size());
       bool all_alpha = tl > 0, all_digit = tl > 0, any_alnum = false;
-      for (size_t q = 0; q < tl; ++q) {
-        const unsigned char c = (unsigned char)t[q];
+      for (size_t q = 0; q < tl;) {
+        const uint32_t c = decode(t, q);
         all_alpha &= is_alpha(c);
         all_digit &= is_digit(c);
         any_alnum |= is_alnum(c);
@@ -264,48 +419,75 @@ const char* const kAbbrev[] = {"dr", "mr", "mrs", "ms", "prof", "st", "no", "vs"
 
 bool is_abbrev(const char* s, size_t len) {
   for (const char* a : kAbbrev) {
-    if (strlen(a) != len) continue;
+    const size_t al = strlen(a);
+    size_t i = 0, q = 0;
     bool eq = true;
-    for (size_t q = 0; q < len; ++q) eq &= lower(s[q]) == a[q];
-    if (eq) return true;
+    while (i < len && q < al && eq) eq = lower_cp(decode(s, i)) == (uint32_t)(unsigned char)a[q++];
+    if (eq && i == len && q == al) return true;
   }
   return false;
 }
 
 // segment_sentences (corpus.py:92-126): sentence spans [begin, end) of text
+// (byte offsets at code-point boundaries)
 void segment(const std::string& text, std::vector<std::pair<size_t, size_t>>& spans) {
   const size_t size = text.size();
   const char* s = text.data();
   size_t pos = 0;
-  while (pos < size && is_space((unsigned char)s[pos])) ++pos;
+  while (pos < size) {
+    size_t nx = pos;
+    if (!is_space(decode(s, nx))) break;
+    pos = nx;
+  }
   size_t begin = pos;
   while (pos < size) {
-    const char ch = s[pos];
+    size_t next = pos;
+    const uint32_t ch = decode(s, next);
     if (ch != '.' && ch != '!' && ch != '?') {
-      ++pos;
+      pos = next;
       continue;
     }
     if (ch == '.') {
       size_t st = pos;
-      while (st > 0 && is_alpha((unsigned char)s[st - 1])) --st;
+      while (st > 0) {
+        const size_t ps = prev_start(s, st);
+        size_t q = ps;
+        if (!is_alpha(decode(s, q))) break;
+        st = ps;
+      }
       if (is_abbrev(s + st, pos - st)) {
-        ++pos;
+        pos = next;
         continue;
       }
     }
     size_t nxt = pos + 1;
-    if (nxt < size && is_space((unsigned char)s[nxt])) {
-      while (nxt < size && is_space((unsigned char)s[nxt])) ++nxt;
-      if (nxt < size && (is_upper((unsigned char)s[nxt]) || is_digit((unsigned char)s[nxt]))) {
-        spans.emplace_back(begin, pos + 1);
-        begin = pos = nxt;
-        continue;
+    size_t q = nxt;
+    if (nxt < size && is_space(decode(s, q))) {
+      nxt = q;
+      while (nxt < size) {
+        size_t r = nxt;
+        if (!is_space(decode(s, r))) break;
+        nxt = r;
+      }
+      size_t r = nxt;
+      if (nxt < size) {
+        const uint32_t c2 = decode(s, r);
+        if (is_upper(c2) || is_digit(c2)) {
+          spans.emplace_back(begin, pos + 1);
+          begin = pos = nxt;
+          continue;
+        }
       }
     }
-    ++pos;
+    pos = next;
   }
   size_t end = size;
-  while (end > begin && is_space((unsigned char)s[end - 1])) --end;
+  while (end > begin) {
+    const size_t ps = prev_start(s, end);
+    size_t q = ps;
+    if (!is_space(decode(s, q))) break;
+    end = ps;
+  }
   if (end > begin) spans.emplace_back(begin, end);
 }
 
@@ -328,7 +510,20 @@ struct Json {
     }
     return false;
   }
-  // JSON string -> ASCII bytes (\u escapes above 0x7f, raw control chars: fail)
+  bool hex4(unsigned& v) {
+    if (e - p < 4) return false;
+    v = 0;
+    for (int q = 0; q < 4; ++q) {
+      const char h = *p++;
+      v <<= 4;
+      if (h >= '0' && h <= '9') v |= (unsigned)(h - '0');
+      else if (h >= 'a' && h <= 'f') v |= (unsigned)(h - 'a' + 10);
+      else if (h >= 'A' && h <= 'F') v |= (unsigned)(h - 'A' + 10);
+      else return false;
+    }
+    return true;
+  }
+  // JSON string -> UTF-8 (raw control chars and lone surrogates: fail)
   bool str(std::string& out) {
     out.clear();
     if (p >= e || *p != '"') return false;
@@ -338,7 +533,7 @@ struct Json {
       if (c == '"') return true;
       if (c < 0x20) return false;
       if (c != '\\') {
-        out.push_back((char)c);
+        out.push_back((char)c);  // raw UTF-8 (the file was validated)
         continue;
       }
       if (p >= e) return false;
@@ -353,18 +548,18 @@ struct Json {
         case 'r': out.push_back('\r'); break;
         case 't': out.push_back('\t'); break;
         case 'u': {
-          if (e - p < 4) return false;
-          unsigned v = 0;
-          for (int q = 0; q < 4; ++q) {
-            const char h = *p++;
-            v <<= 4;
-            if (h >= '0' && h <= '9') v |= (unsigned)(h - '0');
-            else if (h >= 'a' && h <= 'f') v |= (unsigned)(h - 'a' + 10);
-            else if (h >= 'A' && h <= 'F') v |= (unsigned)(h - 'A' + 10);
-            else return false;
+          unsigned v;
+          if (!hex4(v)) return false;
+          if (v >= 0xD800 && v <= 0xDBFF) {  // a surrogate pair or nothing
+            unsigned lo;
+            if (e - p < 6 || p[0] != '\\' || p[1] != 'u') return false;
+            p += 2;
+            if (!hex4(lo) || lo < 0xDC00 || lo > 0xDFFF) return false;
+            v = 0x10000 + ((v - 0xD800) << 10) + (lo - 0xDC00);
+          } else if (v >= 0xDC00 && v <= 0xDFFF) {
+            return false;
           }
-          if (v >= 0x80) return false;  // non-ASCII text: Python path
-          out.push_back((char)v);
+          encode(out, v);
           break;
         }
         default: return false;
@@ -530,7 +725,7 @@ void field_spans(const Field& f, std::vector<std::pair<const char*, size_t>>& ou
   }
   for (const std::string& s : f.items) {
     bool blank = true;
-    for (char ch : s) blank &= is_space((unsigned char)ch);
+    for (size_t i = 0; i < s.size() && blank;) blank = is_space(decode(s.data(), i));
     if (!blank) out.emplace_back(s.data(), s.size());
   }
 }
@@ -584,6 +779,15 @@ int parse_line(Ingest& g, const char* b, const char* e, int64_t lineno) {
   if (js.p != js.e) return -1;  // trailing data
   if (!has_id || !has_sl || !has_tl || src.kind == 0 || tgt.kind == 0) return -1;
   if (sl == tl) return -1;
+  // ids and languages cross the C ABI as NUL-terminated strings
+  for (const std::string* s : {&id, &sl, &tl})
+    if (s->find('\0') != std::string::npos) return -1;
+  // text the native normalizer reproduces exactly (else: Python path)
+  for (const Field* f : {&src, &tgt}) {
+    if (f->kind == 1 && !text_ok(f->text.data(), f->text.size())) return -1;
+    for (const std::string& it : f->items)
+      if (!text_ok(it.data(), it.size())) return -1;
+  }
   Doc d;
   d.id = id;
   d.src_lang = sl;
@@ -733,8 +937,7 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
   size_t r;
   while ((r = fread(buf, 1, sizeof(buf), fh)) > 0) data.append(buf, r);
   fclose(fh);
-  for (unsigned char c : data)
-    if (c >= 0x80) return fail_why("non-ASCII input");
+  if (!bm_ingest::valid_utf8(data)) return fail_why("not valid UTF-8");
   // lines: text-mode splitting, \n, \r\n and \r end a line
   struct Line {
     size_t b, e;
@@ -778,7 +981,7 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
       const char* b = base + lines[q].b;
       const char* e = base + lines[q].e;
       bool blank = true;
-      for (const char* x = b; x < e; ++x) blank &= bm_ingest::is_space((unsigned char)*x);
+      for (size_t i = 0; i < (size_t)(e - b) && blank;) blank = bm_ingest::is_space(bm_ingest::decode(b, i));
       if (blank) continue;
       if (bm_ingest::parse_line(*L, b, e, (int64_t)q + 1) < 0) {
         bad[t] = (int64_t)q + 1;

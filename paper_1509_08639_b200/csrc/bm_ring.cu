@@ -161,7 +161,10 @@ size_t hits_kernel_smem(int n, int m) {
 // ---------------------------------------------------------------------------
 // hits_kernel: dictionary join of one document -> HBM scratch
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kHitsThreads, 8) hits_kernel(bm_sentences S, bm_docs D,
+#ifndef BM_HITS_MINB
+#define BM_HITS_MINB 8
+#endif
+__global__ void __launch_bounds__(kHitsThreads, BM_HITS_MINB) hits_kernel(bm_sentences S, bm_docs D,
                                                             bm_lexicon L, const int32_t* list,
                                                             int n_list, const int64_t* hit_off,
                                                             uint8_t* hits_out) {

@@ -7,9 +7,10 @@ but reads, segments, tokenizes and packs the JSONL file in C++
 (``csrc/bm_ingest.cpp``), lowers the lexicon there, mines on the GPU, and
 merges / formats the records in C++ too.
 
-The native reader accepts a file only when its semantics reduce to fixed
-ASCII tables (every byte ASCII, JSON inside a validated subset, string or
-integer ids); anything else -- and any document whose orientation check would
+The native reader accepts a file only when it can reproduce Python's Unicode
+semantics exactly (valid UTF-8, JSON inside a validated subset, string or
+integer ids, text that NFC leaves unchanged and that lowercases character by
+character -- see the contract at the top of bm_ingest.cpp); anything else -- and any document whose orientation check would
 raise -- takes the Python path, which is the reference behaviour by
 construction. Empty-side pairs are reported through ``on_skip`` (and the log)
 before mining starts rather than interleaved with the output; the TSV and the
@@ -68,13 +69,13 @@ class NativeCorpus:
         pid, psl, ptl = C.c_char_p(), C.c_char_p(), C.c_char_p()
         for k in range(a.n_docs):
             N.check(self._lib.bm_ingest_doc(self._h, k, C.byref(pid), C.byref(psl), C.byref(ptl)))
-            self.doc_ids.append(pid.value.decode("ascii"))
-            self.langs.append((psl.value.decode("ascii"), ptl.value.decode("ascii")))
+            self.doc_ids.append(pid.value.decode("utf-8"))
+            self.langs.append((psl.value.decode("utf-8"), ptl.value.decode("utf-8")))
         self.skipped: list[tuple[int, str, str]] = []
         ln = C.c_int64()
         for q in range(a.n_skipped):
             N.check(self._lib.bm_ingest_skipped(self._h, q, C.byref(ln), C.byref(pid), C.byref(psl)))
-            self.skipped.append((ln.value, pid.value.decode("ascii"), psl.value.decode("ascii")))
+            self.skipped.append((ln.value, pid.value.decode("utf-8"), psl.value.decode("utf-8")))
 
     @classmethod
     def load(cls, path: str) -> "NativeCorpus | None":
@@ -232,7 +233,7 @@ def mine_corpus_file(
     LAST_TIMINGS["mine"] = t1 - t0 - LAST_TIMINGS.get("lexicon", 0.0)
     data, rep = nc.emit(fwd, bwd, sw_f, sw_b, skip)
     t2 = time.perf_counter()
-    out.write(data.decode("ascii"))
+    out.write(data.decode("utf-8"))
     LAST_TIMINGS["emit"] = t2 - t1
     LAST_TIMINGS["write"] = time.perf_counter() - t2
     report = MiningReport()

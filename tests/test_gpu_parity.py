@@ -231,11 +231,43 @@ def test_mine_corpus_file_1000_docs_sha256(world500, tmp_path):
     assert hashlib.sha256(text.encode()).hexdigest() == want["sha256"]
 
 
+def test_mine_corpus_file_unicode_native_path(tmp_path):
+    """Non-ASCII corpora take the native path too: docs40 and its lexicon with
+    every 'a'/'A' spelled 'ą'/'Ą' (two UTF-8 bytes; no abbreviation contains
+    'a', so segmentation is unchanged) mine to the golden TSV spelled the same
+    way, through raw UTF-8 lines and \\u-escaped lines alike."""
+    from paper_1509_08639_b200.ingest import NativeCorpus
+
+    tr = str.maketrans({"a": "\u0105", "A": "\u0104"})
+    lp = tmp_path / "lex.tsv"
+    lp.write_text(open(golden("lex500.tsv"), encoding="utf-8").read().translate(tr),
+                  encoding="utf-8")
+    lex = bm.load_lexicon(str(lp), "xx", "yy")
+    fwd = bm.load_model(golden("model500_fwd.json"))
+    bwd = bm.load_model(golden("model500_bwd.json"))
+    p = str(tmp_path / "docs.jsonl")
+    with open(p, "w", encoding="utf-8") as fh:
+        for q, d in enumerate(load_docs("docs40.jsonl")):
+            for side in ("src", "tgt"):
+                d[side] = (d[side].translate(tr) if isinstance(d[side], str)
+                           else [s.translate(tr) for s in d[side]])
+            fh.write(json.dumps(d, ensure_ascii=bool(q % 2)) + "\n")
+    assert NativeCorpus.load(p) is not None
+    sink = io.StringIO()
+    bm.mine_corpus_file(p, fwd, bwd, lex, bm.MinerConfig(bm.MiningParams(0.5, 0.2)), sink)
+    want = []
+    for line in open(golden("mine40_bi.tsv"), encoding="utf-8").read().splitlines(True):
+        cols = line.split("\t")
+        want.append("\t".join([cols[0].translate(tr), cols[1].translate(tr)] + cols[2:]))
+    assert "\u0105" in sink.getvalue()
+    assert sink.getvalue() == "".join(want)
+
+
 def test_mine_corpus_file_falls_back_outside_the_subset(world500, tmp_path):
-    """Non-ASCII text takes the Python reader: same output as mine_corpus."""
+    """Text NFC would change takes the Python reader: same output as mine_corpus."""
     lex, fwd, bwd = world500
     docs = load_docs("docs40.jsonl")[:5]
-    docs[1]["src"][0] = docs[1]["src"][0] + " caf\u00e9"
+    docs[1]["src"][0] = docs[1]["src"][0] + " cafe\u0301"
     p = str(tmp_path / "mixed.jsonl")
     with open(p, "w", encoding="utf-8") as fh:
         for d in docs:

@@ -8,6 +8,7 @@ mine_corpus(load_document_pairs(...))) is in test_gpu_parity.py.
 import gzip
 import json
 import os
+import unicodedata
 
 import numpy as np
 import pytest
@@ -72,11 +73,7 @@ def lex():
 def test_ingest_matches_python_packer(name, lex):
     path = golden(name)
     nc = NativeCorpus.load(path)
-    if nc is None:  # outside the ASCII subset: the Python path is the behaviour
-        with open(path, encoding="utf-8") as fh:
-            text = "".join(json.dumps(json.loads(l), ensure_ascii=False) for l in fh if l.strip())
-        assert any(ord(ch) > 127 for ch in text)
-        return
+    assert nc is not None
     pairs, pc, skipped = python_side(path)
     assert_same_pack(nc, pc)
     assert nc.doc_ids == [p.id for p in pairs]
@@ -111,8 +108,16 @@ def test_ingest_bare_cr_lines(tmp_path):
 
 
 @pytest.mark.parametrize("line", [
-    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "café", "tgt": "x"}',   # non-ASCII
-    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "caf\\u00e9", "tgt": "x"}',  # escaped
+    # text NFC would change or that lowercases outside the per-character map
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "cafe\\u0301", "tgt": "x"}',  # e + acute
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "cafe\u0301", "tgt": "x"}',
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "a\u0316\u0317", "tgt": "x"}',  # 2 marks
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "\u212a", "tgt": "x"}',  # Kelvin sign
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "ΟΔΟΣ", "tgt": "x"}',  # final sigma
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": ["x"], "tgt": ["İstanbul"]}',  # 2-cp lower
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "\\ud800", "tgt": "x"}',  # lone surrogate
+    '{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "\\udc00\\ud800", "tgt": "x"}',
+    '{"id": "a\\u0000b", "src_lang": "xx", "tgt_lang": "yy", "src": "a", "tgt": "b"}',  # NUL id
     '{"id": 1.5, "src_lang": "xx", "tgt_lang": "yy", "src": "a", "tgt": "b"}',          # float id
     '{"id": "a", "src_lang": "xx", "tgt_lang": "xx", "src": "a", "tgt": "b"}',          # same langs
     '{"id": "a", "src_lang": "xx", "src": "a", "tgt": "b"}',                           # missing
@@ -126,6 +131,125 @@ def test_ingest_declines_outside_the_subset(tmp_path, line):
     with open(p, "w", encoding="utf-8") as fh:
         fh.write(line + "\n")
     assert NativeCorpus.load(p) is None
+
+
+@pytest.mark.parametrize("raw", [b"\xff", b"\xc0\x80", b"\xed\xa0\x80", b"\xf4\x90\x80\x80",
+                                 b"\xe2\x82"])
+def test_ingest_declines_invalid_utf8(tmp_path, raw):
+    p = tmp_path / "bad.jsonl"
+    p.write_bytes(b'{"id": "u", "src_lang": "xx", "tgt_lang": "yy", "src": "a' + raw +
+                  b'", "tgt": "x"}\n')
+    assert NativeCorpus.load(str(p)) is None
+
+
+UNICODE_LINES = [
+    {"id": "pl-1", "src_lang": "xx", "tgt_lang": "yy",
+     "src": "Zażółć gęślą jaźń. Źdźbło trawy! Ósmy dzień? 3 koty. ŁÓDŹ i GDAŃSK. dr. Żak, prof. Łuk.",
+     "tgt": ["Grüße aus Köln.", "ÉCOLE élève. Ça va!", "Straße ẞ MASSE"]},
+    {"id": "ελ", "src_lang": "yy", "tgt_lang": "xx",
+     "src": "Καλημέρα κόσμε. Η ΑΘΗΝΑ είναι 3η! Ρωσικά: Привет, МИР. Ёлка.",
+     "tgt": "漢字かな交じり文。カタカナ．ＡＢＣ１２３ and ٣٤٥ and ²³ ½ Ⅻ ǅungla ǈ."},
+    {"id": 42, "src_lang": "xx", "tgt_lang": "yy",
+     "src": "nbsp\u00a0here.\u2003Em space\u3000ideographic\u2028line\u0085nel x\u200bzw.",
+     "tgt": ["emoji 😀🎉 ok", "😀 escaped pair", "\u00a0\u2003", "tab\there"]},
+    {"id": "m", "src_lang": "xx", "tgt_lang": "yy",
+     "src": "a\u0316b mark alone \u0316 x. Ünï. Mr. Ø. DR. X. Vs. Y. \u0130 no",
+     "tgt": "ǅ titlecase. ǈ. Ⅻ roman. ℌ script. 𝐀 bold. ᾈ greek"},
+]
+
+
+def test_ingest_unicode_matches_python_packer(tmp_path, lex):
+    """Non-ASCII text the native path accepts reproduces Python's tokenizer,
+    NFC/lower/split normalizer and segmentation exactly (Polish, German,
+    Greek, Cyrillic, CJK, Unicode spaces and digits, astral characters)."""
+    p = str(tmp_path / "uni.jsonl")
+    lines = [dict(x) for x in UNICODE_LINES]
+
+    def write():  # odd lines as \\u escapes (surrogate pairs for astral chars)
+        with open(p, "w", encoding="utf-8") as fh:
+            for q, obj in enumerate(lines):
+                fh.write(json.dumps(obj, ensure_ascii=bool(q % 2)) + "\n")
+
+    write()
+    # İ (U+0130) lowercases to two code points: that file is Python's
+    assert NativeCorpus.load(p) is None
+    lines[3]["src"] = lines[3]["src"].replace("\u0130", "I")
+    write()
+    nc = NativeCorpus.load(p)
+    assert nc is not None
+    pairs, pc, skipped = python_side(p)
+    assert any(ord(ch) > 0xFFFF for pr in pairs for s in pr.target.sentences for ch in s.raw)
+    assert_same_pack(nc, pc)
+    assert nc.doc_ids == [x.id for x in pairs]
+    assert nc.langs == [(x.source.lang, x.target.lang) for x in pairs]
+    pl, nl = pack_lexicon(lex, pc), nc.lexicon(lex)
+    for f in ("fwd_off", "fwd_cand", "rev_off", "rev_cand"):
+        assert np.array_equal(getattr(pl, f), getattr(nl, f)), f
+    # emission: raw sentences and ids go out as UTF-8, unique tokens counted
+    nd = pc.n_docs
+    z = np.zeros(nd, dtype=np.uint8)
+    recs = np.array([(d, i, j, 0, 0.75) for d in range(nd) for i in range(int(pc.n[d]))
+                     for j in range(int(pc.m[d])) if (i + j) % 2 == 0],
+                    dtype=np.dtype(N.RECORD_DTYPE))
+    data, rep = nc.emit(recs, None, z, z, z)
+    want = []
+    for k in range(nd):
+        pr = pairs[k]
+        src, tgt = pr.source.sentences, pr.target.sentences
+        want += [MinedPair(src[int(r["i"])], tgt[int(r["j"])], 0.75, pr.id, "forward", int(r["i"]),
+                           int(r["j"])) for r in recs[recs["doc"] == k]]
+    assert data.decode("utf-8") == "".join(format_pair_line(r) for r in want)
+    st, tt = set(), set()
+    for r in want:
+        st.update(tokenize(r.src.normalized))
+        tt.update(tokenize(r.tgt.normalized))
+    assert rep[:5] == [len(want), len(want), 0, len(st), len(tt)]
+
+
+def _random_text(rng, pool, n):
+    return "".join(pool[int(x)] for x in rng.integers(0, len(pool), n))
+
+
+def test_ingest_unicode_fuzz_accept_implies_identical(tmp_path):
+    """Random text over a wide code-point pool (letters, marks, spaces, digits,
+    punctuation, astral, case-special characters): whenever the native reader
+    accepts a file, its packing equals Python's; it accepts most of the
+    NFC-stable, simply-lowercased pool."""
+    rng = np.random.default_rng(11)
+    wide = [chr(c) for c in list(range(0x20, 0x7f)) + list(range(0xa0, 0x250)) +
+            list(range(0x300, 0x370)) + list(range(0x370, 0x530)) + list(range(0x1e00, 0x1f00)) +
+            list(range(0x2000, 0x2070)) + list(range(0x2150, 0x2190)) + list(range(0x3000, 0x3040)) +
+            list(range(0xac00, 0xac40)) + list(range(0x1100, 0x1180)) + list(range(0xff00, 0xff60)) +
+            [0x1d400, 0x1f600, 0x10400, 0x10428, 0x130, 0x3a3, 0x212a, 0x2126, 0x85, 0x1c, 0x1f]
+            if not 0xd800 <= c <= 0xdfff and c not in (0x22, 0x5c)]
+    def simple(ch):  # NFC-stable starter, one-code-point lower of the same classes
+        lo = ch.lower()
+        return (unicodedata.normalize("NFC", ch) == ch and unicodedata.combining(ch) == 0
+                and not 0x1161 <= ord(ch) <= 0x11c2 and ch != "\u03a3" and len(lo) == 1
+                and (lo.isalnum(), lo.isspace()) == (ch.isalnum(), ch.isspace()))
+
+    safe = [ch for ch in wide if (ch.isalnum() or ch.isspace() or ch in ".!?,;:-") and simple(ch)]
+    accepted = 0
+    for trial in range(60):
+        pool = wide if trial % 2 else safe
+        lines = []
+        for d in range(4):
+            src = ". ".join(_random_text(rng, pool, 12) for _ in range(3))
+            lines.append({"id": f"f{trial}-{d}", "src_lang": "xx", "tgt_lang": "yy", "src": src,
+                          "tgt": [_random_text(rng, pool, 10), _random_text(rng, pool, 6) + "."]})
+        p = str(tmp_path / f"fz{trial}.jsonl")
+        with open(p, "w", encoding="utf-8") as fh:
+            for obj in lines:
+                fh.write(json.dumps(obj, ensure_ascii=bool(trial % 3 == 0)) + "\n")
+        nc = NativeCorpus.load(p)
+        if nc is None:
+            continue
+        accepted += 1
+        pairs, pc, skipped = python_side(p)
+        assert_same_pack(nc, pc)
+        assert nc.doc_ids == [x.id for x in pairs]
+        assert [(pid, f"empty {side} document") for _l, pid, side in nc.skipped] == skipped
+    assert accepted >= 20
 
 
 def _fake_records(pc, seed, dirn):
