@@ -233,6 +233,34 @@ int bm_mine_host_wire(const bm_wire* wire_h, const bm_docs* docs_h, const bm_lex
                       void* stream);
 
 /*
+ * Packed host format for bm_mine_host_packed: the same content in 4 bytes per
+ * sentence plus 2 bytes per distinct token (valid when the id space has
+ * <= 16384 ids, every count is <= 255 and no token occurs more than 3 times
+ * as an alphabetic token in one sentence). Offsets are rebuilt on the device
+ * from the per-sentence counts and one base offset per 32 sentences, so
+ * tok_off / dig_off are read by the host planner only and never copied.
+ * counts[s] = n_tok | n_punct << 8 | n_uniq << 16 | n_dig << 24 with
+ * n_uniq = tok_off[s+1] - tok_off[s], n_dig = dig_off[s+1] - dig_off[s];
+ * n_alpha is the sum of the sentence's alphabetic counts.
+ */
+typedef struct bm_wire_packed {
+  int32_t n_sent;
+  const int32_t* tok_off;    /* [n_sent + 1] host planning only */
+  const int32_t* dig_off;    /* [n_sent + 1] host planning only */
+  const uint32_t* counts;    /* [n_sent] */
+  const int32_t* tok_off32;  /* [n_sent / 32 + 1]: tok_off[32 b] */
+  const int32_t* dig_off32;  /* [n_sent / 32 + 1]: dig_off[32 b] */
+  const uint16_t* tok_pk;    /* [tok_off[n_sent]]: tok_id << 2 | tok_alpha */
+  const uint16_t* dig_id;    /* [dig_off[n_sent]] */
+} bm_wire_packed;
+
+/* bm_mine_host with the packed format (host pointers). */
+int bm_mine_host_packed(const bm_wire_packed* pk_h, const bm_docs* docs_h, const bm_lexicon* lex_h,
+                        const bm_model* model, double threshold, double penalty,
+                        bm_record* rec_out, int64_t rec_cap, int64_t* n_rec, double* cost_out,
+                        void* stream);
+
+/*
  * K5 -- tune (tuner.py:87-154): for every penalty p_k and threshold t_l,
  * pred[k*n_thr + l] += #diagonal moves with S >= t_l over all docs, and
  * hit[k*n_thr + l] += those whose (i, j) is in the doc's gold set.

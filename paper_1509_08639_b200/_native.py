@@ -42,6 +42,14 @@ class Wire(C.Structure):
     ]
 
 
+class WirePacked(C.Structure):
+    _fields_ = [
+        ("n_sent", C.c_int32),
+        ("tok_off", _p), ("dig_off", _p), ("counts", _p), ("tok_off32", _p),
+        ("dig_off32", _p), ("tok_pk", _p), ("dig_id", _p),
+    ]
+
+
 class Docs(C.Structure):
     _fields_ = [("n_docs", C.c_int32), ("src0", _p), ("n", _p), ("tgt0", _p), ("m", _p)]
 
@@ -96,6 +104,9 @@ _SIGS = {
     "bm_mine_host_wire": (C.c_int, [C.POINTER(Wire), C.POINTER(Docs), C.POINTER(LexiconC),
                                     C.POINTER(ModelC), C.c_double, C.c_double, _p, C.c_int64,
                                     C.POINTER(C.c_int64), _p, _p]),
+    "bm_mine_host_packed": (C.c_int, [C.POINTER(WirePacked), C.POINTER(Docs), C.POINTER(LexiconC),
+                                      C.POINTER(ModelC), C.c_double, C.c_double, _p, C.c_int64,
+                                      C.POINTER(C.c_int64), _p, _p]),
     "bm_tune": (C.c_int, [C.POINTER(Sentences), C.POINTER(Docs), _p, _p, C.POINTER(LexiconC),
                           C.POINTER(ModelC), _p, C.c_int32, _p, C.c_int32, _p, _p, _p, _p,
                           C.c_int32, _p]),

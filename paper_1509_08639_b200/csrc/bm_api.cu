@@ -583,7 +583,10 @@ struct HostSource {
   const int32_t* dig_off;  // host, [n_sent + 1]
   const bm_sentences* full;
   const bm_wire* wire;
-  int32_t tok_max(int k) const { return full ? full->n_tok[k] : (int32_t)wire->n_tok[k]; }
+  const bm_wire_packed* pk = nullptr;
+  int32_t tok_max(int k) const {
+    return full ? full->n_tok[k] : wire ? (int32_t)wire->n_tok[k] : (int32_t)(pk->counts[k] & 0xff);
+  }
 };
 
 int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* lh,
@@ -618,8 +621,17 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     roff[d] = rt;
     rt += std::max(0, std::min(dh->n[d], dh->m[d]));
   }
+  if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
+  for (int d = 0; d < nd; ++d)
+    if (amax[d] > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
   tr.mark("host prep");
   Scratch sc(st);
+  // declared after the scratch, so destroyed before it: an early return never
+  // frees scratch (stream-ordered on st) under copies still queued on cs
+  struct CopyFence {
+    cudaStream_t s;
+    ~CopyFence() { cudaStreamSynchronize(s); }
+  } fence{cs};
   bm_sentences sd;
   sd.n_sent = ns;
   int32_t *a0, *a1, *a2, *a3, *a4, *a5, *a6;
@@ -643,6 +655,15 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   // device staging of the narrow wire arrays
   uint8_t *w_t = nullptr, *w_p = nullptr, *w_a = nullptr, *w_al = nullptr;
   uint16_t *w_id = nullptr, *w_dg = nullptr;
+  uint32_t* w_cnt = nullptr;
+  int32_t *w_o32 = nullptr, *w_d32 = nullptr;
+  if (src.pk) {
+    BM_CK(sc.alloc(&w_cnt, ns), "alloc");
+    BM_CK(sc.alloc(&w_o32, ns / 32 + 1), "alloc");
+    BM_CK(sc.alloc(&w_d32, ns / 32 + 1), "alloc");
+    BM_CK(sc.alloc(&w_id, ne), "alloc");
+    BM_CK(sc.alloc(&w_dg, ndig), "alloc");
+  }
   if (src.wire) {
     BM_CK(sc.alloc(&w_t, ns), "alloc");
     BM_CK(sc.alloc(&w_p, ns), "alloc");
@@ -688,64 +709,14 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   // chunk count upper bound: every chunk but the last holds >= 1 document
   int64_t* ctot = nullptr;
   BM_CK(sc.alloc(&ctot, nd + 1), "alloc");
+  tr.mark("allocs");
   int64_t* hcnt = pinned_counts((size_t)nd + 1);
   if (hcnt == nullptr) return fail(BM_ENOMEM, "pinned count buffer");
-  // route every document once (global indices) and stage the fused tier's
-  // document lists, hit offsets and zeroed hit scratch before the chunk loop,
-  // so a chunk is only kernel launches (no per-chunk host planning or small
-  // uploads queued behind the bulk copies)
-  const Model M = to_model(model);
-  if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
-  std::vector<int32_t> fl[4];
-  size_t fsm[4] = {0, 0, 0, 0}, hsm[4] = {0, 0, 0, 0};
-  std::vector<int64_t> hoff(nd, 0);
-  std::vector<char> banded(nd, 0);
-  int64_t htot = 0;
-  {
-    const char* route = getenv("BM_ROUTE");
-    const bool force_banded = route != nullptr && strcmp(route, "banded") == 0;
-    for (int d = 0; d < nd; ++d) {
-      const int n = dh->n[d], m = dh->m[d];
-      if (n <= 0 || m <= 0) continue;
-      if (amax[d] > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
-      const int R = fused_rows_per_lane(n);
-      const size_t sl = ring_slice_bytes(n, m, R);
-      if (!force_banded && n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax[d] <= 255) {
-        const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
-        fl[q].push_back(d);
-        fsm[q] = std::max(fsm[q], sl);
-        hsm[q] = std::max(hsm[q], hits_kernel_smem(n, m));
-        hoff[d] = htot;
-        htot += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
-      } else {
-        banded[d] = 1;
-      }
-    }
-  }
-  int32_t* dfl[4] = {nullptr, nullptr, nullptr, nullptr};
-  for (int q = 0; q < 4; ++q)
-    if (!fl[q].empty()) BM_CK(sc.upload(&dfl[q], fl[q]), "upload");
-  int64_t* dhoff = nullptr;
-  uint8_t* hits = nullptr;
-  if (htot > 0 && !BM_RING_FUSED_JOIN) {
-    BM_CK(sc.upload(&dhoff, hoff), "upload");
-    BM_CK(sc.alloc(&hits, (size_t)htot), "alloc hits");
-    BM_CK(cudaMemsetAsync(hits, 0, (size_t)htot, st), "memset hits");
-  }
-  BM_CK(cudaMemsetAsync(cnt, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
-  const PairTables tabs = pair_tables();
   // the copy stream may only touch the scratch once it is allocated on st
   cudaEvent_t ready;
   BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
   BM_CK(cudaEventRecord(ready, st), "event");
   BM_CK(cudaStreamWaitEvent(cs, ready, 0), "event");
-  static const int n_ms = std::max(1, std::min(kMaxMineStreams,
-      getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 3));
-  std::vector<cudaStream_t> ms(1, st);
-  for (int q = 1; q < n_ms; ++q) {
-    ms.push_back(side_stream(q));
-    BM_CK(cudaStreamWaitEvent(ms.back(), ready, 0), "event");
-  }
   auto h2d = [&](void* dst, const void* from, size_t bytes) -> cudaError_t {
     return bytes ? cudaMemcpyAsync(dst, from, bytes, cudaMemcpyHostToDevice, cs) : cudaSuccess;
   };
@@ -774,64 +745,165 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     cudaEventCreate(&tl0);
     cudaEventRecord(tl0, cs);
   }
+  // pass 1: the chunks' bulk copies (kernels wait on each chunk's copy event).
+  // Chunk 0 goes first so its DMA overlaps the routing below; the rest follow
+  // the small list uploads, which would otherwise queue behind the bulk DMA.
+  struct Chunk {
+    int d0, d1, lo, hi;
+    cudaEvent_t copied;
+  };
+  std::vector<Chunk> chunks;
   int d0 = 0;
-  while (d0 < nd) {
-    int d1 = d0;
-    int64_t cells = 0;
-    int lo = ns, hi = 0;
-    // a small first chunk starts the GPU early; later chunks amortise launches
-    const int64_t want = evs.empty() ? kChunkCells / 4 : kChunkCells;
-    while (d1 < nd && (d1 == d0 || cells < want)) {
-      cells += (int64_t)dh->n[d1] * dh->m[d1];
-      if (dh->n[d1] > 0) {
-        lo = std::min(lo, dh->src0[d1]);
-        hi = std::max(hi, dh->src0[d1] + dh->n[d1]);
+  auto enqueue_copies = [&](size_t upto) -> int {
+    while (d0 < nd && chunks.size() < upto) {
+      int d1 = d0;
+      int64_t cells = 0;
+      int lo = ns, hi = 0;
+      // a small first chunk starts the GPU early; later chunks amortise launches
+      const int64_t want = chunks.empty() ? kChunkCells / 4 : kChunkCells;
+      while (d1 < nd && (d1 == d0 || cells < want)) {
+        cells += (int64_t)dh->n[d1] * dh->m[d1];
+        if (dh->n[d1] > 0) {
+          lo = std::min(lo, dh->src0[d1]);
+          hi = std::max(hi, dh->src0[d1] + dh->n[d1]);
+        }
+        if (dh->m[d1] > 0) {
+          lo = std::min(lo, dh->tgt0[d1]);
+          hi = std::max(hi, dh->tgt0[d1] + dh->m[d1]);
+        }
+        ++d1;
       }
-      if (dh->m[d1] > 0) {
-        lo = std::min(lo, dh->tgt0[d1]);
-        hi = std::max(hi, dh->tgt0[d1] + dh->m[d1]);
+      if (hi > lo) {
+        const int64_t e0 = src.tok_off[lo], e1 = src.tok_off[hi];
+        const int64_t g0 = src.dig_off[lo], g1 = src.dig_off[hi];
+        const size_t cntS = (size_t)(hi - lo);
+        if (src.pk) {
+          // counts from the chunk's first 32-sentence block, bases through hi's
+          const bm_wire_packed* w = src.pk;
+          const int l32 = lo & ~31;
+          BM_CK(h2d(w_cnt + l32, w->counts + l32, (size_t)(hi - l32) * 4), "h2d");
+          BM_CK(h2d(w_o32 + (lo >> 5), w->tok_off32 + (lo >> 5), (size_t)((hi >> 5) - (lo >> 5) + 1) * 4), "h2d");
+          BM_CK(h2d(w_d32 + (lo >> 5), w->dig_off32 + (lo >> 5), (size_t)((hi >> 5) - (lo >> 5) + 1) * 4), "h2d");
+          BM_CK(h2d(w_id + e0, w->tok_pk + e0, (size_t)(e1 - e0) * 2), "h2d");
+          BM_CK(h2d(w_dg + g0, w->dig_id + g0, (size_t)(g1 - g0) * 2), "h2d");
+        } else {
+          BM_CK(h2d(a3 + lo, src.tok_off + lo, (cntS + 1) * 4), "h2d");
+          BM_CK(h2d(a5 + lo, src.dig_off + lo, (cntS + 1) * 4), "h2d");
+        }
+        if (src.full) {
+          const bm_sentences* sh = src.full;
+          BM_CK(h2d(a0 + lo, sh->n_tok + lo, cntS * 4), "h2d");
+          BM_CK(h2d(a1 + lo, sh->n_punct + lo, cntS * 4), "h2d");
+          BM_CK(h2d(a2 + lo, sh->n_alpha + lo, cntS * 4), "h2d");
+          BM_CK(h2d(a4 + e0, sh->tok_id + e0, (size_t)(e1 - e0) * 4), "h2d");
+          BM_CK(h2d(a7 + e0, sh->tok_alpha + e0, (size_t)(e1 - e0) * 2), "h2d");
+          BM_CK(h2d(a6 + g0, sh->dig_id + g0, (size_t)(g1 - g0) * 4), "h2d");
+        } else if (src.wire) {
+          const bm_wire* w = src.wire;
+          BM_CK(h2d(w_t + lo, w->n_tok + lo, cntS), "h2d");
+          BM_CK(h2d(w_p + lo, w->n_punct + lo, cntS), "h2d");
+          BM_CK(h2d(w_a + lo, w->n_alpha + lo, cntS), "h2d");
+          BM_CK(h2d(w_id + e0, w->tok_id + e0, (size_t)(e1 - e0) * 2), "h2d");
+          BM_CK(h2d(w_al + e0, w->tok_alpha + e0, (size_t)(e1 - e0)), "h2d");
+          BM_CK(h2d(w_dg + g0, w->dig_id + g0, (size_t)(g1 - g0) * 2), "h2d");
+        }
       }
-      ++d1;
+      cudaEvent_t ev;
+      BM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      BM_CK(cudaEventRecord(ev, cs), "event");
+      evs.push_back(ev);
+      if (tr.on) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, cs);
+        tl_copy.push_back(e);
+      }
+      chunks.push_back(Chunk{d0, d1, lo, hi, ev});
+      d0 = d1;
     }
-    if (hi > lo) {
-      const int64_t e0 = src.tok_off[lo], e1 = src.tok_off[hi];
-      const int64_t g0 = src.dig_off[lo], g1 = src.dig_off[hi];
-      const size_t cntS = (size_t)(hi - lo);
-      BM_CK(h2d(a3 + lo, src.tok_off + lo, (cntS + 1) * 4), "h2d");
-      BM_CK(h2d(a5 + lo, src.dig_off + lo, (cntS + 1) * 4), "h2d");
-      if (src.full) {
-        const bm_sentences* sh = src.full;
-        BM_CK(h2d(a0 + lo, sh->n_tok + lo, cntS * 4), "h2d");
-        BM_CK(h2d(a1 + lo, sh->n_punct + lo, cntS * 4), "h2d");
-        BM_CK(h2d(a2 + lo, sh->n_alpha + lo, cntS * 4), "h2d");
-        BM_CK(h2d(a4 + e0, sh->tok_id + e0, (size_t)(e1 - e0) * 4), "h2d");
-        BM_CK(h2d(a7 + e0, sh->tok_alpha + e0, (size_t)(e1 - e0) * 2), "h2d");
-        BM_CK(h2d(a6 + g0, sh->dig_id + g0, (size_t)(g1 - g0) * 4), "h2d");
+    return BM_OK;
+  };
+  if (int rc = enqueue_copies(1)) return rc;
+  tr.mark("chunk 0 copies enqueued");
+  // route every document once (global indices) and stage the fused tier's
+  // document lists, hit offsets and zeroed hit scratch before the chunk loop,
+  // so a chunk is only kernel launches (no per-chunk host planning or small
+  // uploads queued behind the bulk copies)
+  const Model M = to_model(model);
+  std::vector<int32_t> fl[4];
+  size_t fsm[4] = {0, 0, 0, 0}, hsm[4] = {0, 0, 0, 0};
+  std::vector<int64_t> hoff(nd, 0);
+  std::vector<char> banded(nd, 0);
+  int64_t htot = 0;
+  {
+    const char* route = getenv("BM_ROUTE");
+    const bool force_banded = route != nullptr && strcmp(route, "banded") == 0;
+    int pn = -1, pm = -1, pq = -1;  // the last shape's class (batches repeat shapes)
+    size_t psl = 0, phs = 0;
+    for (int d = 0; d < nd; ++d) {
+      const int n = dh->n[d], m = dh->m[d];
+      if (n <= 0 || m <= 0) continue;
+      if (n != pn || m != pm) {
+        const int R = fused_rows_per_lane(n);
+        psl = ring_slice_bytes(n, m, R);
+        phs = hits_kernel_smem(n, m);
+        pq = (!force_banded && n <= kFusedMaxRows && psl <= (size_t)kFusedMaxSmem)
+                 ? (R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3)
+                 : -1;
+        pn = n;
+        pm = m;
+      }
+      if (pq >= 0 && amax[d] <= 255) {
+        const int q = pq;
+        fl[q].push_back(d);
+        fsm[q] = std::max(fsm[q], psl);
+        hsm[q] = std::max(hsm[q], phs);
+        hoff[d] = htot;
+        htot += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
       } else {
-        const bm_wire* w = src.wire;
-        BM_CK(h2d(w_t + lo, w->n_tok + lo, cntS), "h2d");
-        BM_CK(h2d(w_p + lo, w->n_punct + lo, cntS), "h2d");
-        BM_CK(h2d(w_a + lo, w->n_alpha + lo, cntS), "h2d");
-        BM_CK(h2d(w_id + e0, w->tok_id + e0, (size_t)(e1 - e0) * 2), "h2d");
-        BM_CK(h2d(w_al + e0, w->tok_alpha + e0, (size_t)(e1 - e0)), "h2d");
-        BM_CK(h2d(w_dg + g0, w->dig_id + g0, (size_t)(g1 - g0) * 2), "h2d");
+        banded[d] = 1;
       }
     }
-    cudaEvent_t ev;
-    BM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-    BM_CK(cudaEventRecord(ev, cs), "event");
-    evs.push_back(ev);
-    if (tr.on) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      cudaEventRecord(e, cs);
-      tl_copy.push_back(e);
-    }
+  }
+  tr.mark("routing");
+  int32_t* dfl[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int q = 0; q < 4; ++q)
+    if (!fl[q].empty()) BM_CK(sc.upload(&dfl[q], fl[q]), "upload");
+  int64_t* dhoff = nullptr;
+  uint8_t* hits = nullptr;
+  if (htot > 0 && !BM_RING_FUSED_JOIN) {
+    BM_CK(sc.upload(&dhoff, hoff), "upload");
+    BM_CK(sc.alloc(&hits, (size_t)htot), "alloc hits");
+    BM_CK(cudaMemsetAsync(hits, 0, (size_t)htot, st), "memset hits");
+  }
+  BM_CK(cudaMemsetAsync(cnt, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
+  const PairTables tabs = pair_tables();
+  tr.mark("list uploads + memsets");
+  // the mining streams start after the list uploads and memsets on st
+  cudaEvent_t planned;
+  BM_CK(cudaEventCreateWithFlags(&planned, cudaEventDisableTiming), "event");
+  BM_CK(cudaEventRecord(planned, st), "event");
+  static const int n_ms = std::max(1, std::min(kMaxMineStreams,
+      getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 4));
+  std::vector<cudaStream_t> ms(1, st);
+  for (int q = 1; q < n_ms; ++q) {
+    ms.push_back(side_stream(q));
+    BM_CK(cudaStreamWaitEvent(ms.back(), planned, 0), "event");
+  }
+  // pass 2: per chunk, widen + mine + compact on a mining stream; chunk 0's
+  // kernels are enqueued before the remaining copies so the GPU starts early
+  auto enqueue_kernels = [&](size_t kc) -> int {
+    const int d0 = chunks[kc].d0, d1 = chunks[kc].d1, lo = chunks[kc].lo, hi = chunks[kc].hi;
+    cudaEvent_t ev = chunks[kc].copied;
     cudaStream_t sk = ms[(ch_d0.size() + 1) % ms.size()];  // chunk 0 on a side stream
     BM_CK(cudaStreamWaitEvent(sk, ev, 0), "event");
     // the copy stream only moves bytes: widening the wire arrays is a few
     // microseconds of compute and runs in order on the compute stream (on the
     // copy stream it would queue behind the mining CTAs and stall the DMA)
+    if (src.pk && hi > lo)
+      BM_CK(launch_unpack_packed(w_cnt, w_o32, w_d32, w_id, w_dg, lo, hi, a0, a1, a2, a3, a4, a7,
+                                 a5, a6, sk),
+            "unpack_packed_kernel");
     if (src.wire && hi > lo) {
       const int64_t e0 = src.tok_off[lo], e1 = src.tok_off[hi];
       const int64_t g0 = src.dig_off[lo], g1 = src.dig_off[hi];
@@ -899,8 +971,13 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
       cudaEventRecord(e, sk);
       tl_mine.push_back(e);
     }
-    d0 = d1;
-  }
+    return BM_OK;
+  };
+  if (int rc = enqueue_kernels(0)) return rc;
+  if (int rc = enqueue_copies(SIZE_MAX)) return rc;
+  tr.mark("copies enqueued");
+  for (size_t kc = 1; kc < chunks.size(); ++kc)
+    if (int rc = enqueue_kernels(kc)) return rc;
   // join the side streams back into the caller's stream
   for (size_t q = 1; q < ms.size(); ++q) {
     cudaEvent_t joined;
@@ -942,6 +1019,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   }
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
   cudaEventDestroy(ready);
+  cudaEventDestroy(planned);
   *n_rec = tot;
   return BM_OK;
 }
@@ -950,6 +1028,16 @@ int bm_mine_host(const bm_sentences* sh, const bm_docs* dh, const bm_lexicon* lh
                  const bm_model* model, double threshold, double penalty, bm_record* rec_out,
                  int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
   HostSource src{sh->n_sent, sh->tok_off, sh->dig_off, sh, nullptr};
+  return mine_host_impl(src, dh, lh, model, threshold, penalty, rec_out, rec_cap, n_rec, cost_out,
+                        stream);
+}
+
+int bm_mine_host_packed(const bm_wire_packed* ph, const bm_docs* dh, const bm_lexicon* lh,
+                        const bm_model* model, double threshold, double penalty,
+                        bm_record* rec_out, int64_t rec_cap, int64_t* n_rec, double* cost_out,
+                        void* stream) {
+  if (lh->n_ids > 16384) return fail(BM_EINVAL, "packed format: more than 16384 ids");
+  HostSource src{ph->n_sent, ph->tok_off, ph->dig_off, nullptr, nullptr, ph};
   return mine_host_impl(src, dh, lh, model, threshold, penalty, rec_out, rec_cap, n_rec, cost_out,
                         stream);
 }

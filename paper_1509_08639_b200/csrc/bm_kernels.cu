@@ -1156,4 +1156,67 @@ cudaError_t launch_unpack_wire(const uint8_t* t8, const uint8_t* p8, const uint8
                                               n_tok, n_punct, n_alpha, tok_id, tok_alpha, dig_id);
   return counted(cudaGetLastError());
 }
+// Packed host format -> bm_sentences (bm_wire_packed in bimine_b200.h): one
+// warp per 32-sentence block rebuilds the offsets from the block's base offset
+// and a shuffle scan of the per-sentence counts, then widens its entries.
+// Counts are read from 32 * (lo / 32) (the caller copies them from there);
+// offsets are written for [lo, hi], everything else for [lo, hi).
+__global__ void unpack_packed_kernel(const uint32_t* __restrict__ cnt,
+                                     const int32_t* __restrict__ o32,
+                                     const int32_t* __restrict__ d32,
+                                     const uint16_t* __restrict__ pk,
+                                     const uint16_t* __restrict__ dg, int lo, int hi,
+                                     int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha,
+                                     int32_t* tok_off, int32_t* tok_id, uint16_t* tok_alpha,
+                                     int32_t* dig_off, int32_t* dig_id) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (int)(gridDim.x * blockDim.x) >> 5;
+  for (int b = (lo >> 5) + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); b <= (hi >> 5);
+       b += nwarps) {
+    const int s = b * 32 + lane;
+    const uint32_t c = s < hi ? cnt[s] : 0u;
+    const int u = (int)((c >> 16) & 0xff), g = (int)(c >> 24);
+    int su = u, sg = g;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, su, d);
+      const int y = __shfl_up_sync(0xffffffffu, sg, d);
+      if (lane >= d) {
+        su += x;
+        sg += y;
+      }
+    }
+    const int tb = o32[b] + su - u, gb = d32[b] + sg - g;
+    if (s >= lo && s <= hi) {
+      tok_off[s] = tb;
+      dig_off[s] = gb;
+    }
+    if (s >= lo && s < hi) {
+      n_tok[s] = (int32_t)(c & 0xff);
+      n_punct[s] = (int32_t)((c >> 8) & 0xff);
+      int na = 0;
+      for (int q = 0; q < u; ++q) {
+        const uint32_t v = pk[tb + q];
+        tok_id[tb + q] = (int32_t)(v >> 2);
+        tok_alpha[tb + q] = (uint16_t)(v & 3u);
+        na += (int)(v & 3u);
+      }
+      n_alpha[s] = na;
+      for (int q = 0; q < g; ++q) dig_id[gb + q] = dg[gb + q];
+    }
+  }
+}
+
+cudaError_t launch_unpack_packed(const uint32_t* cnt, const int32_t* o32, const int32_t* d32,
+                                 const uint16_t* pk, const uint16_t* dg, int lo, int hi,
+                                 int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha,
+                                 int32_t* tok_off, int32_t* tok_id, uint16_t* tok_alpha,
+                                 int32_t* dig_off, int32_t* dig_id, cudaStream_t st) {
+  if (hi <= lo) return cudaSuccess;
+  const int blocks = (hi >> 5) - (lo >> 5) + 1;  // 32-sentence blocks = warps
+  const int grid = std::min((blocks + 7) / 8, 148 * 16);
+  unpack_packed_kernel<<<grid, 256, 0, st>>>(cnt, o32, d32, pk, dg, lo, hi, n_tok, n_punct,
+                                             n_alpha, tok_off, tok_id, tok_alpha, dig_off, dig_id);
+  return counted(cudaGetLastError());
+}
 }  // namespace bm

@@ -20,6 +20,8 @@
 //                     and compact them in path order.
 // The similarity matrix never exists in memory; every value is computed with
 // the same operation order as bm_kernels.cu (bit-identical to the reference).
+#include <mutex>
+#include <unordered_map>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -490,12 +492,26 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
   }
 }
 
+// Raise a kernel's dynamic shared memory limit (and prefer the shared-memory
+// carveout) once per size: the attribute calls cost microseconds of host time
+// per launch, and the host entry launches per chunk.
+static cudaError_t smem_attr(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> set;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = set.find(fn);
+  if (it != set.end() && it->second >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  set[fn] = smem;
+  return cudaSuccess;
+}
+
 cudaError_t launch_hits(const FusedArgs& a, size_t smem, cudaStream_t st) {
   if (a.n_list == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(hits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(hits_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaError_t e = smem_attr((const void*)hits_kernel, smem);
   if (e != cudaSuccess) return e;
   hits_kernel<<<a.n_list, kHitsThreads, smem, st>>>(a.S, a.D, a.L, a.list, a.n_list, a.hit_off,
                                                      a.hits);
@@ -508,13 +524,9 @@ cudaError_t launch_hits(const FusedArgs& a, size_t smem, cudaStream_t st) {
 cudaError_t launch_ring(const FusedArgs& a, int R, size_t smem, cudaStream_t st) {
   if (a.n_list == 0) return cudaSuccess;
   cudaError_t e;
-#define BM_LAUNCH_RING(RR)                                                                   \
-  e = cudaFuncSetAttribute(mine_ring_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                       \
-  if (e != cudaSuccess) return e;                                                            \
-  e = cudaFuncSetAttribute(mine_ring_kernel<RR>,                                             \
-                           cudaFuncAttributePreferredSharedMemoryCarveout, 100);             \
-  if (e != cudaSuccess) return e;                                                            \
+#define BM_LAUNCH_RING(RR)                                  \
+  e = smem_attr((const void*)mine_ring_kernel<RR>, smem);   \
+  if (e != cudaSuccess) return e;                           \
   mine_ring_kernel<RR><<<a.n_list, kRingThreads, smem, st>>>(a);
   switch (R) {
     case 1: BM_LAUNCH_RING(1); break;

@@ -38,6 +38,13 @@ def wire_ok(corpus: PackedCorpus, plex: PackedLexicon) -> bool:
             and int(corpus.tok_alpha.max(initial=0)) <= 255)
 
 
+def packed_ok(corpus: PackedCorpus, plex: PackedLexicon) -> bool:
+    """The packed format holds this batch (14-bit ids, alphabetic counts <= 3)."""
+    return (plex.n_ids <= 16384 and corpus.n_sent > 0
+            and int(corpus.n_tok.max(initial=0)) <= 255
+            and int(corpus.tok_alpha.max(initial=0)) <= 3)
+
+
 def to_wire(corpus: PackedCorpus) -> dict[str, np.ndarray]:
     return {
         "n_tok": corpus.n_tok.astype(np.uint8), "n_punct": corpus.n_punct.astype(np.uint8),
@@ -47,21 +54,54 @@ def to_wire(corpus: PackedCorpus) -> dict[str, np.ndarray]:
     }
 
 
+_PACKED = ("tok_off", "dig_off", "counts", "tok_off32", "dig_off32", "tok_pk", "dig_id")
+
+
+def to_packed(corpus: PackedCorpus) -> dict[str, np.ndarray]:
+    """bm_wire_packed arrays (include/bimine_b200.h)."""
+    to, do = corpus.tok_off, corpus.dig_off
+    counts = (corpus.n_tok.astype(np.uint32) | corpus.n_punct.astype(np.uint32) << 8
+              | np.diff(to).astype(np.uint32) << 16 | np.diff(do).astype(np.uint32) << 24)
+    return {
+        "tok_off": to, "dig_off": do, "counts": counts,
+        "tok_off32": np.ascontiguousarray(to[::32]), "dig_off32": np.ascontiguousarray(do[::32]),
+        "tok_pk": (corpus.tok_id.astype(np.uint16) << 2) | corpus.tok_alpha.astype(np.uint16),
+        "dig_id": corpus.dig_id.astype(np.uint16),
+    }
+
+
 class PinnedBatch:
     """Packed arrays copied once into page-locked host memory + C structs.
 
-    wire=True stages the compact wire format (bm_mine_host_wire) when the
-    batch fits it, halving the per-call host->device bytes.
+    wire=True stages the most compact host format the batch fits: the packed
+    format (bm_mine_host_packed, ~0.6x the wire bytes) or the wire format
+    (bm_mine_host_wire, ~half the plain bytes); wire="wire" / "packed" picks
+    one; wire=False sends the plain bm_sentences arrays (bm_mine_host).
+    ``h2d_bytes`` counts the bytes one call copies host -> device.
     """
 
     def __init__(self, corpus: PackedCorpus, plex: PackedLexicon, pin: bool = True,
-                 wire: bool = True):
+                 wire: bool | str = True):
         self.keep = []
-        self.wire = bool(wire and wire_ok(corpus, plex))
-        arrs = {}
-        src = to_wire(corpus) if self.wire else {k: getattr(corpus, k) for k in _SENT}
-        for name in _SENT:
-            arrs[name] = src[name]
+        if wire is True:
+            fmt = ("packed" if packed_ok(corpus, plex) else
+                   "wire" if wire_ok(corpus, plex) else "full")
+        elif wire in ("packed", "wire"):
+            fmt = wire
+            ok = packed_ok if wire == "packed" else wire_ok
+            if not ok(corpus, plex):
+                raise ValueError(f"the batch does not fit the {wire} format")
+        else:
+            fmt = "full"
+        self.fmt = fmt
+        self.wire = fmt != "full"
+        if fmt == "packed":
+            src, names = to_packed(corpus), _PACKED
+        elif fmt == "wire":
+            src, names = to_wire(corpus), _SENT
+        else:
+            src, names = {k: getattr(corpus, k) for k in _SENT}, _SENT
+        arrs = {name: src[name] for name in names}
         for name in _DOCS:
             arrs[name] = getattr(corpus, name)
         for name in _LEX:
@@ -75,10 +115,11 @@ class PinnedBatch:
                 view = np.ascontiguousarray(v)
             arrs[k] = view
             self.keep.append(view)
-            self.h2d_bytes += view.nbytes
+            if not (fmt == "packed" and k in ("tok_off", "dig_off")):  # planning only
+                self.h2d_bytes += view.nbytes
         self.arrs = arrs
-        cls = N.Wire if self.wire else N.Sentences
-        self.sent = cls(corpus.n_sent, *[arrs[k].ctypes.data for k in _SENT])
+        cls = {"packed": N.WirePacked, "wire": N.Wire, "full": N.Sentences}[fmt]
+        self.sent = cls(corpus.n_sent, *[arrs[k].ctypes.data for k in names])
         self.docs = N.Docs(corpus.n_docs, *[arrs[k].ctypes.data for k in _DOCS])
         self.lex = N.LexiconC(plex.n_ids, *[arrs[k].ctypes.data for k in _LEX])
         n, m = arrs["n"], arrs["m"]
@@ -96,7 +137,8 @@ def mine_pinned(pb: PinnedBatch, model, threshold: float, penalty: float, stream
     """One bm_mine_host call; returns (records view, n_records, d2h bytes)."""
     lib = N.lib()
     n_rec = C.c_int64(0)
-    fn = lib.bm_mine_host_wire if pb.wire else lib.bm_mine_host
+    fn = {"packed": lib.bm_mine_host_packed, "wire": lib.bm_mine_host_wire,
+          "full": lib.bm_mine_host}[pb.fmt]
     N.check(fn(C.byref(pb.sent), C.byref(pb.docs), C.byref(pb.lex),
                C.byref(N.model_struct(model)), float(threshold), float(penalty),
                pb.rec.ctypes.data, pb.rec_cap, C.byref(n_rec), pb.cost.ctypes.data, stream))
@@ -106,7 +148,7 @@ def mine_pinned(pb: PinnedBatch, model, threshold: float, penalty: float, stream
 
 
 def mine_host(corpus: PackedCorpus, plex: PackedLexicon, model, threshold: float, penalty: float,
-              wire: bool = False, pin: bool = False):
+              wire: bool | str = False, pin: bool = False):
     """One call with host buffers; pin=True stages them page-locked (records are
     then written by the GPU straight into the pinned output buffer)."""
     pb = PinnedBatch(corpus, plex, pin=pin, wire=wire)

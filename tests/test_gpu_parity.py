@@ -406,20 +406,40 @@ def test_synth_text_round_trip_same_records():
     assert a.tobytes() == b.tobytes()
 
 
-@pytest.mark.parametrize("wire,pin", [(False, False), (True, False), (True, True), (False, True)])
+@pytest.mark.parametrize("wire,pin", [(False, False), ("wire", False), ("wire", True), (False, True),
+                                      ("packed", False), ("packed", True)])
 def test_mine_host_entry_point_matches_device_path(oracle_mod, wire, pin):
-    """bm_mine_host / bm_mine_host_wire (host buffers in, records out) == oracle,
+    """bm_mine_host / _wire / _packed (host buffers in, records out) == oracle,
     from pageable and from page-locked host buffers."""
     from paper_1509_08639_b200 import hostapi, synth
 
     sc = synth.make_corpus(*synth.c2_shape(3000), seed=11)  # several streamed chunks
     model = bm.load_model(golden("model5k_fwd.json"))
     plex = sc.world.packed_lexicon()
-    assert hostapi.wire_ok(sc.packed, plex)
+    assert hostapi.wire_ok(sc.packed, plex) and hostapi.packed_ok(sc.packed, plex)
     recs, cost = hostapi.mine_host(sc.packed, plex, model, 0.5, 0.2, wire=wire, pin=pin)
     want, wcost = oracle_mod.mine(oracle_mod.HostBatch(sc.packed, plex), model, 0.5, 0.2, threads=16)
     assert recs.tobytes() == want.tobytes()
     assert np.array_equal(bits(cost), bits(wcost))
+
+
+def test_mine_host_formats_on_a_skewed_corpus():
+    """Skewed document sizes put chunk boundaries at arbitrary sentence indices
+    (not multiples of the packed format's 32-sentence blocks) and route some
+    documents to the banded tier: every host format == the device path."""
+    from paper_1509_08639_b200 import engine, hostapi, synth
+
+    g, a, b = synth.c3_shape(1500, seed=5)
+    sc = synth.make_corpus(g, a, b, seed=5)
+    c, plex = sc.packed, sc.world.packed_lexicon()
+    model = bm.load_model(golden("model5k_fwd.json"))
+    assert int((c.n.astype(np.int64) * c.m).sum()) > 20 << 20  # several chunks
+    want, wcost = engine.mine(engine.DeviceCorpus.upload(c), engine.DeviceLexicon.upload(plex),
+                              engine.DocView.of(c), model, 0.5, 0.2)
+    for fmt in ("packed", "wire", False):
+        recs, cost = hostapi.mine_host(c, plex, model, 0.5, 0.2, wire=fmt, pin=True)
+        assert recs.tobytes() == want.tobytes(), fmt
+        assert np.array_equal(bits(cost), bits(wcost)), fmt
 
 
 @pytest.mark.parametrize("pin", [False, True])
