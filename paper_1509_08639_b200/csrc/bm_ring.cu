@@ -240,6 +240,28 @@ __device__ __forceinline__ int2 active_lanes(int t, int ngroups, int nl) {
 
 // 5 CTAs per SM (smem slices of C2-shaped documents fit 5); R = 8 blocks need
 // the registers of 4
+#ifdef BM_RING_PROFILE
+// tools/ring_trace.py: per document (first 16384 of a launch) globaltimer
+// stamps [start, loaded, DP done, traceback done, end] and the SM id
+__device__ unsigned long long g_ring_prof[16384][6];
+__device__ __forceinline__ unsigned long long ring_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RING_PROF(slot)                                                   \
+  if (tid == 0 && item < 16384) {                                         \
+    g_ring_prof[item][slot] = ring_timer();                               \
+    if (slot == 0) {                                                      \
+      unsigned s;                                                         \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(s));                      \
+      g_ring_prof[item][5] = s;                                           \
+    }                                                                     \
+  }
+#else
+#define RING_PROF(slot)
+#endif
+
 template <int R>
 __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_ring_kernel(FusedArgs a) {
   using CodeT = typename std::conditional<R == 8, uint64_t, uint32_t>::type;
@@ -273,6 +295,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
     int32_t* dlist = (int32_t*)((uint8_t*)dirs + align16((size_t)ngroups * WARP * sizeof(CodeT)));
 
     __syncthreads();  // the previous document is done with every buffer
+    RING_PROF(0)
     if (tid == 0) {
       for (int q = 0; q < kSlots; ++q) {
         mbar_init(bar_full + q, kProducers);
@@ -324,6 +347,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
 #if !BM_RING_FUSED_JOIN
     mbar_wait(bar_load, 0);
 #endif
+    RING_PROF(1)
 
     const int steps = ngroups + nl - 1;
 
@@ -414,7 +438,11 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
           const int i = L * R + r, j = 4 * (t - L) + c;
           if (L <= la.y && i < n && j < m) {
             const uint32_t hv = hits16[i * m + j];
+#ifdef BM_PROF_FAKE_SCORE  // timing experiment only: DP side lower bound
+            const double sv = (double)(hv & 0xff) * 0.01 + sp[i].pos;
+#else
             const double sv = staged_score(S, a.M, exp_tab, a.tabs, sp[i], sp[n + j], hv & 0xff, hv >> 8);
+#endif
             slot[kt * (BPT * RL)] = __dsub_rn(1.0, sv);
           }
         }
@@ -423,31 +451,44 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
       }
     }
     __syncthreads();  // DP complete: direction codes final
+    RING_PROF(2)
 
     if (tid == 0) {
-      int k = 0, i = n, j = m, wkey = -1;
-      CodeT wv = 0;
-      while (i > 0 && j > 0) {
-        const int ci = i - 1, cj = j - 1;
-        const int key = (cj >> 2) * WARP + ci / R;
-        if (key != wkey) {  // the path stays inside a R x 4 block for a few moves
-          wv = dirs[key];
-          wkey = key;
-        }
-        const uint32_t op = (uint32_t)(wv >> (2 * ((cj & 3) * R + ci % R))) & 3u;
-        if (op == BM_MOVE_D) {
-          dlist[k++] = ci * m + cj;
-          --i;
-          --j;
-        } else if (op == BM_MOVE_GS) {
-          --i;
-        } else {
-          --j;
+      // block walk: load an R x 4 block's code word once, then step in
+      // registers (bit offset sh = 2 (c R + r) moves by a constant per move
+      // kind) until the path leaves the block through its top or left edge
+      int k = 0, ci = n - 1, cj = m - 1;
+      while (ci >= 0 && cj >= 0) {
+        const CodeT wv = dirs[(cj >> 2) * WARP + ci / R];
+        int r = ci % R, c = cj & 3;
+        int sh = 2 * (c * R + r);
+        for (;;) {
+          const uint32_t op = (uint32_t)(wv >> sh) & 3u;
+          if (op == BM_MOVE_D) {
+            dlist[k++] = (ci << 16) | cj;
+            --ci;
+            --cj;
+            --r;
+            --c;
+            sh -= 2 * (R + 1);
+            if ((r | c) < 0) break;
+          } else if (op == BM_MOVE_GS) {
+            --ci;
+            --r;
+            sh -= 2;
+            if (r < 0) break;
+          } else {
+            --cj;
+            --c;
+            sh -= 2 * R;
+            if (c < 0) break;
+          }
         }
       }
       misc[0] = k;
     }
     __syncthreads();
+    RING_PROF(3)
     const int K_path = misc[0];
 
     // threshold + order-preserving block compaction (extract_pairs)
@@ -459,10 +500,10 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
       int ci = 0, cj = 0;
       double sv = 0.0;
       if (f < K_path) {
-        const int cell = dlist[K_path - 1 - f];
-        ci = cell / m;
-        cj = cell - ci * m;
-        const uint32_t hv = hits16[cell];
+        const int cell = dlist[K_path - 1 - f];  // ci << 16 | cj
+        ci = cell >> 16;
+        cj = cell & 0xffff;
+        const uint32_t hv = hits16[ci * m + cj];
         sv = staged_score(S, a.M, exp_tab, a.tabs, sp[ci], sp[n + cj], hv & 0xff, hv >> 8);
         keep = sv >= a.threshold;
       }
@@ -489,6 +530,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
       __syncthreads();  // misc reused by the next chunk
     }
     if (tid == 0) a.rec_count[doc] = base;
+    RING_PROF(4)
   }
 }
 
@@ -541,4 +583,9 @@ cudaError_t launch_ring(const FusedArgs& a, int R, size_t smem, cudaStream_t st)
   return e;
 }
 
+#ifdef BM_RING_PROFILE
+extern "C" int bm_ring_prof(unsigned long long* host, int n_items) {
+  return (int)cudaMemcpyFromSymbol(host, g_ring_prof, sizeof(unsigned long long) * 6 * n_items);
+}
+#endif
 }  // namespace bm
