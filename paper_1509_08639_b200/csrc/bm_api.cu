@@ -734,6 +734,8 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   // copy stream, mine it on the compute stream once its copy event fired
   static const int64_t kChunkCells =
       getenv("BM_CHUNK_CELLS") ? atoll(getenv("BM_CHUNK_CELLS")) : (16ll << 20);
+  static const int64_t kFirstChunkCells =
+      getenv("BM_FIRST_CHUNK_CELLS") ? atoll(getenv("BM_FIRST_CHUNK_CELLS")) : kChunkCells / 4;
   // per chunk: docs [d0, d1), compacted into dense + roff[d0], count -> ctot[k]
   std::vector<int> ch_d0, ch_d1;
   std::vector<cudaEvent_t> ch_ev;
@@ -760,7 +762,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
       int64_t cells = 0;
       int lo = ns, hi = 0;
       // a small first chunk starts the GPU early; later chunks amortise launches
-      const int64_t want = chunks.empty() ? kChunkCells / 4 : kChunkCells;
+      const int64_t want = chunks.empty() ? kFirstChunkCells : kChunkCells;
       while (d1 < nd && (d1 == d0 || cells < want)) {
         cells += (int64_t)dh->n[d1] * dh->m[d1];
         if (dh->n[d1] > 0) {

@@ -19,5 +19,5 @@ for _ in range(30):
     hostapi.mine_pinned(pb, model, 0.5, 0.2, sp)
     ts.append(time.perf_counter() - t)
 ts.sort()
-print(f"{os.environ.get('BM_CHUNK_CELLS', '-')} {os.environ.get('BM_MINE_STREAMS', '-')} "
+print(f"{os.environ.get('BM_CHUNK_CELLS', '-')} {os.environ.get('BM_FIRST_CHUNK_CELLS', '-')} {os.environ.get('BM_MINE_STREAMS', '-')} "
       f"median {ts[15]*1e3:.3f} ms  min {ts[0]*1e3:.3f} ms")
