@@ -26,6 +26,10 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <stdlib.h>
 
@@ -126,9 +130,8 @@ inline bool ascii8(const void* p, size_t left) {
 }
 
 // Python's strict UTF-8 decoding (no surrogates, no overlongs, <= U+10FFFF)
-bool valid_utf8(const std::string& d) {
-  const unsigned char* s = (const unsigned char*)d.data();
-  const size_t n = d.size();
+bool valid_utf8(const char* d, size_t n) {
+  const unsigned char* s = (const unsigned char*)d;
   size_t i = 0;
   while (i < n) {
     if (ascii8(s + i, n - i)) {
@@ -252,19 +255,48 @@ struct Doc {
   int32_t src0 = 0, n = 0, tgt0 = 0, m = 0;
 };
 
+// std::vector without value-initialization on resize (the merge fills every
+// slot, so zeroing hundreds of MB first would only cost time)
+template <class T>
+struct NoInit : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInit<U>;
+  };
+  NoInit() = default;
+  template <class U>
+  NoInit(const NoInit<U>&) {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new ((void*)p) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new ((void*)p) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using pvec = std::vector<T, NoInit<T>>;
+
 struct Ingest {
   // packed sentences (pack.py layout)
-  std::vector<int32_t> n_tok, n_punct, n_alpha, tok_off{0}, tok_id, dig_off{0}, dig_id;
-  std::vector<uint16_t> tok_alpha;
-  std::vector<int32_t> src0, n, tgt0, m;
+  pvec<int32_t> n_tok, n_punct, n_alpha, tok_off{0}, tok_id, dig_off{0}, dig_id;
+  pvec<uint16_t> tok_alpha;
+  pvec<int32_t> src0, n, tgt0, m;
   // interned token strings (normalized tokens and raw digit tokens) -> id
   StrTable ids;
-  // per sentence: raw text, normalized text and its interned id (merge key;
-  // unique within a chunk -- keys are only compared inside one document)
-  std::string raw, norm;
-  std::vector<int64_t> raw_off{0}, norm_off{0};
-  std::vector<int32_t> norm_key;
+  // per sentence: raw text and the interned id of its normalized text (merge
+  // key; unique within a chunk -- keys are only compared inside one document)
+  std::string raw;
+  pvec<int64_t> raw_off{0};
+  pvec<int32_t> norm_key;
   StrTable norm_ids;
+  std::string norm_tmp;
+  // after ingest: every sentence's raw text (a merged ingest keeps each
+  // chunk's text buffer in raw_store instead of copying them together)
+  std::vector<std::string> raw_store;
+  pvec<const char*> sent_ptr;
+  pvec<int32_t> sent_len;
   std::vector<Doc> docs;
   std::vector<int64_t> skipped_lines;  // empty-side pairs dropped at load
   std::vector<std::string> skipped_ids, skipped_side;
@@ -400,10 +432,10 @@ bool add_sentence(Ingest& g, const char* s, size_t len) {
   // raw + normalized text of the Sentence object
   g.raw.append(s, len);
   g.raw_off.push_back((int64_t)g.raw.size());
-  const size_t n0 = g.norm.size();
-  normalize_into(g.norm, s, len);
-  const char* nm = g.norm.data() + n0;
-  const size_t nl = g.norm.size() - n0;
+  g.norm_tmp.clear();
+  normalize_into(g.norm_tmp, s, len);
+  const char* nm = g.norm_tmp.data();
+  const size_t nl = g.norm_tmp.size();
   const uint64_t h = StrTable::hash(nm, nl);
   int32_t nk = g.norm_ids.find(nm, nl, h);
   if (nk < 0) {
@@ -411,7 +443,6 @@ bool add_sentence(Ingest& g, const char* s, size_t len) {
     g.norm_ids.insert(nm, nl, h, nk);
   }
   g.norm_key.push_back(nk);
-  g.norm_off.push_back((int64_t)g.norm.size());
   return true;
 }
 
@@ -827,6 +858,15 @@ int parse_line(Ingest& g, const char* b, const char* e, int64_t lineno) {
 void merge_parts(std::vector<Ingest*>& part) {
   const size_t np = part.size();
   Ingest& G = *part[0];
+  const bool trace = getenv("BM_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[bm trace]   merge %-10s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  };
   std::vector<std::vector<int32_t>> rid(np);
   for (size_t t = 1; t < np; ++t) {
     Ingest& L = *part[t];
@@ -834,44 +874,47 @@ void merge_parts(std::vector<Ingest*>& part) {
     for (const StrTable::E& e : L.ids.ents)
       rid[t][(size_t)e.val] = G.intern(L.ids.arena.data() + e.off, e.len);
   }
+  lap("intern");
   // slice bases
   std::vector<size_t> sb(np + 1, 0), tb(np + 1, 0), db(np + 1, 0), kb(np + 1, 0);
-  std::vector<int64_t> rb(np + 1, 0), nb(np + 1, 0);
   for (size_t t = 0; t < np; ++t) {
     Ingest& L = *part[t];
     sb[t + 1] = sb[t] + L.n_tok.size();
     tb[t + 1] = tb[t] + L.tok_id.size();
     db[t + 1] = db[t] + L.dig_id.size();
     kb[t + 1] = kb[t] + L.docs.size();
-    rb[t + 1] = rb[t] + (int64_t)L.raw.size();
-    nb[t + 1] = nb[t] + (int64_t)L.norm.size();
   }
+  // chunk texts move (no copy); sentence pointers into them are set below
+  G.raw_store.resize(np);
+  for (size_t t = 0; t < np; ++t) G.raw_store[t] = std::move(part[t]->raw);
+  G.sent_ptr.resize(sb[np]);
+  G.sent_len.resize(sb[np]);
   G.n_tok.resize(sb[np]);
   G.n_punct.resize(sb[np]);
   G.n_alpha.resize(sb[np]);
   G.norm_key.resize(sb[np]);
   G.tok_off.resize(sb[np] + 1);
   G.dig_off.resize(sb[np] + 1);
-  G.raw_off.resize(sb[np] + 1);
-  G.norm_off.resize(sb[np] + 1);
   G.tok_id.resize(tb[np]);
   G.tok_alpha.resize(tb[np]);
   G.dig_id.resize(db[np]);
-  G.raw.resize((size_t)rb[np]);
-  G.norm.resize((size_t)nb[np]);
   G.docs.resize(kb[np]);
   G.src0.resize(kb[np]);
   G.n.resize(kb[np]);
   G.tgt0.resize(kb[np]);
   G.m.resize(kb[np]);
+  lap("resize");
   auto fill = [&](size_t t) {
     Ingest& L = *part[t];
     const size_t ns = L.n_tok.size(), s0 = sb[t];
     std::copy(L.n_tok.begin(), L.n_tok.end(), G.n_tok.begin() + s0);
     std::copy(L.n_punct.begin(), L.n_punct.end(), G.n_punct.begin() + s0);
     std::copy(L.n_alpha.begin(), L.n_alpha.end(), G.n_alpha.begin() + s0);
-    memcpy(&G.raw[(size_t)rb[t]], L.raw.data(), L.raw.size());
-    memcpy(&G.norm[(size_t)nb[t]], L.norm.data(), L.norm.size());
+    const char* text = G.raw_store[t].data();
+    for (size_t s = 0; s < ns; ++s) {
+      G.sent_ptr[s0 + s] = text + L.raw_off[s];
+      G.sent_len[s0 + s] = (int32_t)(L.raw_off[s + 1] - L.raw_off[s]);
+    }
     std::vector<std::pair<int32_t, uint16_t>> ta;
     for (size_t s = 0; s < ns; ++s) {
       const int32_t a = L.tok_off[s], b = L.tok_off[s + 1];
@@ -890,8 +933,6 @@ void merge_parts(std::vector<Ingest*>& part) {
       // merge keys are compared only within a document, and a document never
       // spans chunks: chunk-local keys need no remapping
       G.norm_key[s0 + s] = L.norm_key[s];
-      G.raw_off[s0 + s + 1] = rb[t] + L.raw_off[s + 1];
-      G.norm_off[s0 + s + 1] = nb[t] + L.norm_off[s + 1];
     }
     for (size_t q = 0; q < L.docs.size(); ++q) {
       Doc D = std::move(L.docs[q]);
@@ -908,8 +949,17 @@ void merge_parts(std::vector<Ingest*>& part) {
   {
     std::vector<std::thread> th;
     for (size_t t = 1; t < np; ++t) th.emplace_back(fill, t);
+    // part 0 is G itself: its arrays are in place, only its pointers are new
+    const char* text = G.raw_store[0].data();
+    for (size_t s = 0; s < sb[1]; ++s) {
+      G.sent_ptr[s] = text + G.raw_off[s];
+      G.sent_len[s] = (int32_t)(G.raw_off[s + 1] - G.raw_off[s]);
+    }
     for (auto& x : th) x.join();
   }
+  G.raw_off.clear();
+  G.raw_off.shrink_to_fit();
+  lap("fill");
   for (size_t t = 1; t < np; ++t) {
     Ingest& L = *part[t];
     G.skipped_lines.insert(G.skipped_lines.end(), L.skipped_lines.begin(), L.skipped_lines.end());
@@ -930,14 +980,35 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
     return BM_EUNSUPPORTED;
   };
   *handle = nullptr;
-  FILE* fh = fopen(path, "rb");
-  if (!fh) return fail_why("cannot open file");
-  std::string data;
-  char buf[1 << 16];
-  size_t r;
-  while ((r = fread(buf, 1, sizeof(buf), fh)) > 0) data.append(buf, r);
-  fclose(fh);
-  if (!bm_ingest::valid_utf8(data)) return fail_why("not valid UTF-8");
+  const bool trace = getenv("BM_TRACE") != nullptr;
+  auto tr0 = std::chrono::steady_clock::now();
+  // the file is mapped read-only (nothing keeps pointers into it past this
+  // call: sentence texts are copied into the chunk buffers)
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail_why("cannot open file");
+  struct stat sb;
+  if (fstat(fd, &sb) != 0) {
+    close(fd);
+    return fail_why("cannot stat file");
+  }
+  const size_t fsize = (size_t)sb.st_size;
+  void* map = fsize ? mmap(nullptr, fsize, PROT_READ, MAP_PRIVATE | MAP_POPULATE, fd, 0) : nullptr;
+  close(fd);
+  if (fsize && map == MAP_FAILED) return fail_why("cannot map file");
+  struct Unmap {
+    void* p;
+    size_t n;
+    ~Unmap() {
+      if (p) munmap(p, n);
+    }
+  } unmap{fsize ? map : nullptr, fsize};
+  const struct {
+    const char* p;
+    size_t n;
+    const char* data() const { return p; }
+    size_t size() const { return n; }
+  } data{fsize ? (const char*)map : "", fsize};
+  if (!bm_ingest::valid_utf8(data.data(), data.size())) return fail_why("not valid UTF-8");
   // lines: text-mode splitting, \n, \r\n and \r end a line
   struct Line {
     size_t b, e;
@@ -989,8 +1060,10 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
       }
     }
   };
-  const bool trace = getenv("BM_TRACE") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
+  if (trace)
+    fprintf(stderr, "[bm trace] ingest read + validate + lines %.3f ms\n",
+            std::chrono::duration<double, std::milli>(t0 - tr0).count());
   if (nthr == 1) {
     work(0);
   } else {
@@ -1009,7 +1082,7 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
   }
   auto t1 = std::chrono::steady_clock::now();
   Ingest* g = part[0];
-  if (nthr > 1) bm_ingest::merge_parts(part);
+  bm_ingest::merge_parts(part);  // also sets the sentence text pointers
   for (size_t t = 1; t < nthr; ++t) delete part[t];
   if (trace) {
     auto t2 = std::chrono::steady_clock::now();
@@ -1118,109 +1191,168 @@ int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record
                    const uint8_t* skip, const char** out, int64_t* out_len, int64_t* report) {
   Ingest* g = (Ingest*)h;
   const int32_t nd = (int32_t)g->docs.size();
-  std::string& o = g->out;
-  o.clear();
-  int64_t pairs = 0, nf = 0, nb = 0, mined = 0;
-  // unique-token counts (miner.py count_unique_tokens): for ASCII text
-  // tokenize(normalize(raw)) is exactly the sentence's set U of normalized
-  // token ids, so the sets are bitmaps over the id space
   const size_t nid = g->ids.size();
-  std::vector<uint8_t> src_seen(nid, 0), tgt_seen(nid, 0);
-  int64_t n_src_tok = 0, n_tgt_tok = 0;
-  auto mark = [&](std::vector<uint8_t>& seen, int64_t& cnt, int32_t s) {
-    for (int32_t q = g->tok_off[s]; q < g->tok_off[s + 1]; ++q) {
-      uint8_t& b = seen[(size_t)g->tok_id[q]];
-      cnt += b ^ 1;
-      b = 1;
+  // documents are independent: ranges of documents (about equal record
+  // counts) are formatted on separate threads and concatenated in order
+  unsigned hw = std::thread::hardware_concurrency();
+  if (const char* env = getenv("BM_INGEST_THREADS")) hw = (unsigned)atoi(env);
+  const int64_t nrec = n_fwd + (has_bwd ? n_bwd : 0);
+  const int nthr = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::max(hw, 1u), 32,
+                                                                 nrec / 4096 + 1, (int64_t)nd}));
+  auto doc_lb = [](const bm_record* r, int64_t n, int32_t d) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (r[mid].doc < d)
+        lo = mid + 1;
+      else
+        hi = mid;
     }
+    return lo;
   };
-  struct Rec {
-    int32_t si, tj;  // src / tgt sentence index in the pair's own orientation
-    double conf;
-    bool forward;
-    uint64_t key;
+  std::vector<int32_t> cut(nthr + 1, nd);
+  cut[0] = 0;
+  for (int t = 1; t < nthr; ++t) {  // split the forward stream evenly
+    const int64_t q = n_fwd * t / nthr;
+    cut[t] = q < n_fwd ? fwd[q].doc : nd;
+    cut[t] = std::max(cut[t], cut[t - 1]);
+  }
+  struct Part {
+    std::string o;
+    std::vector<uint8_t> src_seen, tgt_seen;
+    int64_t pairs = 0, nf = 0, nb = 0, mined = 0;
   };
-  int64_t pf = 0, pb = 0;
-  std::vector<Rec> recs, outr;
-  std::vector<uint32_t> ord;
-  // _sanitize (miner.py:253-258): tab / newline / carriage return -> space
-  auto put_sanitized = [&](const char* t, size_t n) {
-    const size_t o0 = o.size();
-    o.append(t, n);
-    for (size_t q = o0; q < o.size(); ++q)
-      if (o[q] == '\t' || o[q] == '\n' || o[q] == '\r') o[q] = ' ';
-  };
-  auto put_raw = [&](int32_t s) {
-    put_sanitized(g->raw.data() + g->raw_off[s], (size_t)(g->raw_off[s + 1] - g->raw_off[s]));
-  };
-  char num[64];
-  for (int32_t d = 0; d < nd; ++d) {
-    const bm_ingest::Doc& D = g->docs[d];
-    // records of doc d (both streams are doc-ordered)
-    const int64_t f0 = pf;
-    while (pf < n_fwd && fwd[pf].doc == d) ++pf;
-    const int64_t b0 = pb;
-    if (has_bwd)
-      while (pb < n_bwd && bwd[pb].doc == d) ++pb;
-    if (skip[d]) continue;
-    ++mined;
-    recs.clear();
-    auto take = [&](const bm_record& r, bool swapped) {
-      Rec x;
-      // oriented source is the pair's target when swapped (miner.py:117-128)
-      x.si = swapped ? r.j : r.i;
-      x.tj = swapped ? r.i : r.j;
-      x.conf = r.conf;
-      x.forward = !swapped;
-      x.key = ((uint64_t)(uint32_t)g->norm_key[D.src0 + x.si] << 32) |
-              (uint32_t)g->norm_key[D.tgt0 + x.tj];
-      recs.push_back(x);
+  std::vector<Part> parts(nthr);
+  auto work = [&](int t) {
+    Part& P = parts[t];
+    std::string& o = P.o;
+    P.src_seen.assign(nid, 0);
+    P.tgt_seen.assign(nid, 0);
+    // unique-token counts (miner.py count_unique_tokens): on accepted text
+    // tokenize(normalize(raw)) is exactly the sentence's set U of normalized
+    // token ids, so the sets are bitmaps over the id space
+    auto mark = [&](std::vector<uint8_t>& seen, int32_t s) {
+      for (int32_t q = g->tok_off[s]; q < g->tok_off[s + 1]; ++q) seen[(size_t)g->tok_id[q]] = 1;
     };
-    for (int64_t q = f0; q < pf; ++q) take(fwd[q], swap_f[d] != 0);
-    const std::vector<Rec>* emit = &recs;
-    if (has_bwd) {
-      for (int64_t q = b0; q < pb; ++q) take(bwd[q], swap_b[d] != 0);
-      // bidirectional_merge (miner.py:131-155): per normalized-text key the
-      // first record wins unless a later one is better (higher confidence,
-      // or forward over backward on an exact tie); then sort by indices
-      ord.resize(recs.size());
-      for (uint32_t q = 0; q < ord.size(); ++q) ord[q] = q;
-      std::stable_sort(ord.begin(), ord.end(),
-                       [&](uint32_t a, uint32_t b) { return recs[a].key < recs[b].key; });
-      outr.clear();
-      for (size_t q = 0; q < ord.size();) {
-        size_t w = q;
-        size_t r = q + 1;
-        for (; r < ord.size() && recs[ord[r]].key == recs[ord[q]].key; ++r) {
-          const Rec& x = recs[ord[r]];
-          const Rec& cur = recs[ord[w]];
-          const bool better = x.conf != cur.conf ? x.conf > cur.conf : (x.forward && !cur.forward);
-          if (better) w = r;
+    struct Rec {
+      int32_t si, tj;  // src / tgt sentence index in the pair's own orientation
+      double conf;
+      bool forward;
+      uint64_t key;
+    };
+    const int32_t d_lo = cut[t], d_hi = cut[t + 1];
+    int64_t pf = doc_lb(fwd, n_fwd, d_lo);
+    int64_t pb = has_bwd ? doc_lb(bwd, n_bwd, d_lo) : 0;
+    std::vector<Rec> recs, outr;
+    std::vector<uint32_t> ord;
+    // _sanitize (miner.py:253-258): tab / newline / carriage return -> space
+    auto put_sanitized = [&](const char* s, size_t n) {
+      const size_t o0 = o.size();
+      o.append(s, n);
+      for (size_t q = o0; q < o.size(); ++q)
+        if (o[q] == '\t' || o[q] == '\n' || o[q] == '\r') o[q] = ' ';
+    };
+    auto put_raw = [&](int32_t s) {
+      put_sanitized(g->sent_ptr[s], (size_t)g->sent_len[s]);
+    };
+    char num[64];
+    for (int32_t d = d_lo; d < d_hi; ++d) {
+      const bm_ingest::Doc& D = g->docs[d];
+      // records of doc d (both streams are doc-ordered)
+      const int64_t f0 = pf;
+      while (pf < n_fwd && fwd[pf].doc == d) ++pf;
+      const int64_t b0 = pb;
+      if (has_bwd)
+        while (pb < n_bwd && bwd[pb].doc == d) ++pb;
+      if (skip[d]) continue;
+      ++P.mined;
+      recs.clear();
+      auto take = [&](const bm_record& r, bool swapped) {
+        Rec x;
+        // oriented source is the pair's target when swapped (miner.py:117-128)
+        x.si = swapped ? r.j : r.i;
+        x.tj = swapped ? r.i : r.j;
+        x.conf = r.conf;
+        x.forward = !swapped;
+        x.key = ((uint64_t)(uint32_t)g->norm_key[D.src0 + x.si] << 32) |
+                (uint32_t)g->norm_key[D.tgt0 + x.tj];
+        recs.push_back(x);
+      };
+      for (int64_t q = f0; q < pf; ++q) take(fwd[q], swap_f[d] != 0);
+      const std::vector<Rec>* emit = &recs;
+      if (has_bwd) {
+        for (int64_t q = b0; q < pb; ++q) take(bwd[q], swap_b[d] != 0);
+        // bidirectional_merge (miner.py:131-155): per normalized-text key the
+        // first record wins unless a later one is better (higher confidence,
+        // or forward over backward on an exact tie); then sort by indices
+        ord.resize(recs.size());
+        for (uint32_t q = 0; q < ord.size(); ++q) ord[q] = q;
+        std::stable_sort(ord.begin(), ord.end(),
+                         [&](uint32_t a, uint32_t b) { return recs[a].key < recs[b].key; });
+        outr.clear();
+        for (size_t q = 0; q < ord.size();) {
+          size_t w = q;
+          size_t r = q + 1;
+          for (; r < ord.size() && recs[ord[r]].key == recs[ord[q]].key; ++r) {
+            const Rec& x = recs[ord[r]];
+            const Rec& cur = recs[ord[w]];
+            const bool better = x.conf != cur.conf ? x.conf > cur.conf : (x.forward && !cur.forward);
+            if (better) w = r;
+          }
+          outr.push_back(recs[ord[w]]);
+          q = r;
         }
-        outr.push_back(recs[ord[w]]);
-        q = r;
+        std::sort(outr.begin(), outr.end(), [](const Rec& a, const Rec& b) {
+          return a.si != b.si ? a.si < b.si : a.tj < b.tj;
+        });
+        emit = &outr;
       }
-      std::sort(outr.begin(), outr.end(), [](const Rec& a, const Rec& b) {
-        return a.si != b.si ? a.si < b.si : a.tj < b.tj;
-      });
-      emit = &outr;
+      for (const Rec& x : *emit) {
+        const int32_t ss = D.src0 + x.si, ts = D.tgt0 + x.tj;
+        put_raw(ss);
+        o += '\t';
+        put_raw(ts);
+        o += '\t';
+        const int nc = snprintf(num, sizeof(num), "%.6f", x.conf);
+        o.append(num, (size_t)nc);
+        o += '\t';
+        put_sanitized(D.id.data(), D.id.size());
+        o += x.forward ? "\tforward\n" : "\tbackward\n";
+        ++P.pairs;
+        (x.forward ? P.nf : P.nb) += 1;
+        mark(P.src_seen, ss);
+        mark(P.tgt_seen, ts);
+      }
     }
-    for (const Rec& x : *emit) {
-      const int32_t ss = D.src0 + x.si, ts = D.tgt0 + x.tj;
-      put_raw(ss);
-      o += '\t';
-      put_raw(ts);
-      o += '\t';
-      const int nc = snprintf(num, sizeof(num), "%.6f", x.conf);
-      o.append(num, (size_t)nc);
-      o += '\t';
-      put_sanitized(D.id.data(), D.id.size());
-      o += x.forward ? "\tforward\n" : "\tbackward\n";
-      ++pairs;
-      (x.forward ? nf : nb) += 1;
-      mark(src_seen, n_src_tok, ss);
-      mark(tgt_seen, n_tgt_tok, ts);
+  };
+  if (nthr == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthr; ++t) th.emplace_back(work, t);
+    for (auto& x : th) x.join();
+  }
+  std::string& o = g->out;
+  size_t total = 0;
+  for (const Part& P : parts) total += P.o.size();
+  o.clear();
+  o.reserve(total);
+  int64_t pairs = 0, nf = 0, nb = 0, mined = 0, n_src_tok = 0, n_tgt_tok = 0;
+  for (Part& P : parts) {
+    o += P.o;
+    pairs += P.pairs;
+    nf += P.nf;
+    nb += P.nb;
+    mined += P.mined;
+  }
+  for (size_t id = 0; id < nid; ++id) {
+    uint8_t s = 0, tg = 0;
+    for (const Part& P : parts) {
+      s |= P.src_seen[id];
+      tg |= P.tgt_seen[id];
     }
+    n_src_tok += s;
+    n_tgt_tok += tg;
   }
   *out = o.data();
   *out_len = (int64_t)o.size();

@@ -365,3 +365,33 @@ def test_emit_on_a_multi_chunk_ingest(docs1000, monkeypatch):
         want.extend(bidirectional_merge(f, b))
     assert data.decode("ascii") == "".join(format_pair_line(r) for r in want)
     assert rep[0] == len(want)
+
+
+def test_emit_thread_count_invariance(docs1000, monkeypatch):
+    """Document ranges formatted on separate threads concatenate to the same
+    bytes and the same unique-token counts as one thread."""
+    p, (pairs, pc, _) = docs1000
+    fwd = _fake_records(pc, 6, 0)
+    bwd = _fake_records(pc, 7, 1)
+    z = np.zeros(pc.n_docs, dtype=np.uint8)
+    skip = (np.random.default_rng(8).random(pc.n_docs) < 0.05).astype(np.uint8)
+    got = []
+    for threads in ("1", "3", "8", "32"):
+        monkeypatch.setenv("BM_INGEST_THREADS", threads)
+        nc = NativeCorpus.load(p)
+        got.append(nc.emit(fwd, bwd, z, z, skip))
+        got.append(nc.emit(fwd, None, z, z, skip))
+    assert all(g == got[0] for g in got[0::2]) and all(g == got[1] for g in got[1::2])
+    assert got[0][1][0] > 1000
+
+
+def test_ingest_empty_and_missing_files(tmp_path):
+    p = tmp_path / "empty.jsonl"
+    p.write_bytes(b"")
+    nc = NativeCorpus.load(str(p))
+    assert nc is not None and nc.packed.n_docs == 0 and nc.n_ids == 0
+    p.write_bytes(b"\n  \n\t\n")
+    nc = NativeCorpus.load(str(p))
+    assert nc is not None and nc.packed.n_docs == 0
+    # the Python reader raises the reference's error for a missing file
+    assert NativeCorpus.load(str(tmp_path / "missing.jsonl")) is None
