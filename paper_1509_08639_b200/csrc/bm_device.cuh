@@ -304,8 +304,20 @@ __device__ void join_chunk_entries(G g, const bm_sentences& S, const int32_t* of
   const int eA0 = offA[0], eA1 = offA[na];
   for (int b = g.rank(); b < js.nbuckets; b += g.size()) js.bfill[b] = 0;
   g.sync();
-  for (int e = c0 + g.rank(); e < c1; e += g.size())
-    atomicAdd(&js.bfill[bucket_of(__ldg(S.tok_id + e), js.bshift)], 1);
+  // the bucket passes load kFill ids per thread before using any of them,
+  // so the global-load latencies overlap (ids are >= 0; -1 marks no entry)
+  constexpr int kFill = 4;
+  for (int eb = c0 + g.rank(); eb < c1; eb += kFill * g.size()) {
+    int idv[kFill];
+#pragma unroll
+    for (int u = 0; u < kFill; ++u) {
+      const int e = eb + u * g.size();
+      idv[u] = e < c1 ? __ldg(S.tok_id + e) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kFill; ++u)
+      if (idv[u] >= 0) atomicAdd(&js.bfill[bucket_of(idv[u], js.bshift)], 1);
+  }
   // owner sentence of every entry of the chunk (stores only)
   {
     const int kb0 = first_sentence_after(offB, nb, c0);
@@ -339,11 +351,20 @@ __device__ void join_chunk_entries(G g, const bm_sentences& S, const int32_t* of
     if (lane == WARP - 1) js.bstart[js.nbuckets] = incl;
   }
   g.sync();
-  for (int e = c0 + g.rank(); e < c1; e += g.size()) {
-    const int32_t id = __ldg(S.tok_id + e);
-    const int slot = atomicAdd(&js.bfill[bucket_of(id, js.bshift)], 1);
-    js.key[slot] = id;
-    js.owner[slot] = chunk_owner[e - c0];
+  for (int eb = c0 + g.rank(); eb < c1; eb += kFill * g.size()) {
+    int idv[kFill];
+#pragma unroll
+    for (int u = 0; u < kFill; ++u) {
+      const int e = eb + u * g.size();
+      idv[u] = e < c1 ? __ldg(S.tok_id + e) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kFill; ++u) {
+      if (idv[u] < 0) continue;
+      const int slot = atomicAdd(&js.bfill[bucket_of(idv[u], js.bshift)], 1);
+      js.key[slot] = idv[u];
+      js.owner[slot] = chunk_owner[eb + u * g.size() - c0];
+    }
   }
   g.sync();
   // probe side in chunks of emax entries, each with an owner table (a
