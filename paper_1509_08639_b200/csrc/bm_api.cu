@@ -500,6 +500,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       a.hits = hits;
       a.hit_off = dho;
       a.tabs = pair_tables();
+      BM_CK(model_tables(M, &a.mt), "model tables");
       tr.mark("upload list");
       if (!BM_RING_FUSED_JOIN) {
         BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
@@ -880,6 +881,8 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   }
   BM_CK(cudaMemsetAsync(cnt, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
   const PairTables tabs = pair_tables();
+  ModelTables mtab;
+  BM_CK(model_tables(M, &mtab), "model tables");
   tr.mark("list uploads + memsets");
   // the mining streams start after the list uploads and memsets on st
   cudaEvent_t planned;
@@ -934,6 +937,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
       a.hits = hits;
       a.hit_off = dhoff;
       a.tabs = tabs;
+      a.mt = mtab;
       if (!BM_RING_FUSED_JOIN) BM_CK(launch_hits(a, hsm[q], sk), "hits_kernel");
       BM_CK(launch_ring(a, 1 << q, fsm[q], sk), "mine_ring_kernel");
     }

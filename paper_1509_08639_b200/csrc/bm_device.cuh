@@ -42,6 +42,17 @@ struct PairTables {
   const double* frac2;
 };
 
+// Per-model tables of the margin's table-driven terms with the weights already
+// applied by the same roundings margin() performs (bm_kernels.cu
+// model_tables): z1 = bias + w0*ratio(aT, bT), p1 = w1*frac(h, A),
+// p2 = w2*frac(h, A), p4 = w4*ratio(aP, bP); kPairMax x kPairMax each.
+struct ModelTables {
+  const double* z1;
+  const double* p1;
+  const double* p2;
+  const double* p4;
+};
+
 __device__ __forceinline__ double quot(int num, int den) {  // 0 < num <= den
   if (den <= kQuotMax) return __ldg(&g_quot[den * kQuotStride + num]);
   return __ddiv_rn((double)num, (double)den);

@@ -9,6 +9,8 @@
 //
 // Everything is fp64 with explicitly rounded intrinsics (the TU is also built
 // with -fmad=false) so every value matches the reference bit for bit.
+#include <mutex>
+#include <cstring>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -26,6 +28,59 @@ PairTables pair_tables() {
   int dev = 0;
   cudaGetDevice(&dev);
   return g_pair_tables[dev];
+}
+
+// Folded margin tables of one model (ModelTables), built on the device with
+// the explicit roundings margin() uses and cached per device and model.
+__global__ void model_tables_kernel(Model M, PairTables tb, double* out) {
+  constexpr int kN = kPairMax * kPairMax;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < kN; q += gridDim.x * blockDim.x) {
+    const double r = tb.ratio2[q], f = tb.frac2[q];
+    out[q] = __dadd_rn(M.bias, __dmul_rn(M.w[0], r));
+    out[kN + q] = __dmul_rn(M.w[1], f);
+    out[2 * kN + q] = __dmul_rn(M.w[2], f);
+    out[3 * kN + q] = __dmul_rn(M.w[4], r);
+  }
+}
+
+cudaError_t model_tables(const Model& M, ModelTables* out) {
+  struct Entry {
+    int dev;
+    Model m;
+    double* tab;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;  // a handful of models per process
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  constexpr int kN = kPairMax * kPairMax;
+  std::lock_guard<std::mutex> lk(mu);
+  double* tab = nullptr;
+  for (const Entry& c : cache)
+    if (c.dev == dev && memcmp(&c.m, &M, sizeof(Model)) == 0) tab = c.tab;
+  if (tab == nullptr) {
+    if (cache.size() >= 16) {  // bounded: drop the oldest model
+      cudaFree(cache.front().tab);
+      cache.erase(cache.begin());
+    }
+    e = cudaMalloc(&tab, 4 * (size_t)kN * sizeof(double));
+    if (e != cudaSuccess) return e;
+    model_tables_kernel<<<128, 256>>>(M, g_pair_tables[dev], tab);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // once per model; any stream may use it
+    if (e != cudaSuccess) {
+      cudaFree(tab);
+      return e;
+    }
+    g_launches += 1;
+    cache.push_back(Entry{dev, M, tab});
+  }
+  out->z1 = tab;
+  out->p1 = tab + kN;
+  out->p2 = tab + 2 * kN;
+  out->p4 = tab + 3 * kN;
+  return cudaSuccess;
 }
 
 // Fill g_quot on the current device (host IEEE division is correctly rounded,

@@ -104,6 +104,7 @@ struct FusedArgs {
   int32_t* rec_count;
   double* cost;
   PairTables tabs;         // branch-free feature tables (device pointers)
+  ModelTables mt;          // the model's folded margin tables (model_tables)
   uint8_t* hits;           // per-doc dense coverage hit counts (hits_kernel output)
   const int64_t* hit_off;  // byte offset of each doc's hits (16-byte aligned)
 };
@@ -136,6 +137,7 @@ cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();
 cudaError_t ensure_quot_table();
 PairTables pair_tables();
+cudaError_t model_tables(const Model& M, ModelTables* out);
 cudaError_t launch_unpack_wire(const uint8_t*, const uint8_t*, const uint8_t*, const uint16_t*,
                                const uint8_t*, const uint16_t*, int, int, int64_t, int64_t, int64_t,
                                int64_t, int32_t*, int32_t*, int32_t*, int32_t*, uint16_t*, int32_t*,

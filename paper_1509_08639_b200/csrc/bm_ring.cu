@@ -206,14 +206,41 @@ struct __align__(16) SPack {
 
 // Features of one cell from staged sentences (same values, operation by
 // operation, as bm_device.cuh cell_features / margin / confidence_from_z).
+// BM_RING_FOLD=1: the margin from the model's folded tables (ModelTables):
+// z = z1[aT,bT] + p1[hf,|A_s|] + p2[hr,|A_t|] + w3*f3 + p4[aP,bP] + w5*f5 + w6,
+// the same additions in the same order as margin(), whose products the tables
+// hold (w*1.0 == w, so f6 and the common f3 = 1 need no multiply).
+#ifndef BM_RING_FOLD
+#define BM_RING_FOLD 1
+#endif
 __device__ __forceinline__ double staged_score(const bm_sentences& S, const Model& M,
                                                const uint64_t* exp_tab, const PairTables& tb,
-                                               const SPack a, const SPack b, int hf, int hr) {
+                                               const ModelTables& mt, const SPack a,
+                                               const SPack b, int hf, int hr) {
   // every count is < 256 here (routing: T <= 255 bounds P, |A|, |D| and hits)
   const int aT = a.tpad & 0xff, aP = (a.tpad >> 8) & 0xff, aA = (a.tpad >> 16) & 0xff,
             aD = a.tpad >> 24;
   const int bT = b.tpad & 0xff, bP = (b.tpad >> 8) & 0xff, bA = (b.tpad >> 16) & 0xff,
             bD = b.tpad >> 24;
+#if BM_RING_FOLD
+  double z = __ldg(mt.z1 + aT * kPairMax + bT);
+  z = __dadd_rn(z, __ldg(mt.p1 + hf * kPairMax + aA));
+  z = __dadd_rn(z, __ldg(mt.p2 + hr * kPairMax + bA));
+  double p3;
+  if ((aD | bD) == 0) {
+    p3 = M.w[3];  // w3 * 1.0
+  } else if (aD == 0 || bD == 0) {
+    p3 = __dmul_rn(M.w[3], 0.0);
+  } else {
+    const int inter = sorted_intersection(S.dig_id + a.d0, aD, S.dig_id + b.d0, bD);
+    p3 = __dmul_rn(M.w[3], frac_or_zero(inter, aD + bD - inter));
+  }
+  z = __dadd_rn(z, p3);
+  z = __dadd_rn(z, __ldg(mt.p4 + aP * kPairMax + bP));
+  z = __dadd_rn(z, __dmul_rn(M.w[5], __dsub_rn(1.0, fabs(__dsub_rn(a.pos, b.pos)))));
+  z = __dadd_rn(z, M.w[6]);  // w6 * 1.0
+  return bmexp::confidence_from_z(z, exp_tab);
+#else
   double f[7];
   f[0] = __ldg(tb.ratio2 + aT * kPairMax + bT);
   f[1] = __ldg(tb.frac2 + hf * kPairMax + aA);
@@ -230,6 +257,7 @@ __device__ __forceinline__ double staged_score(const bm_sentences& S, const Mode
   f[5] = __dsub_rn(1.0, fabs(__dsub_rn(a.pos, b.pos)));
   f[6] = 1.0;
   return bmexp::confidence_from_z(margin(M, f), exp_tab);
+#endif
 }
 
 // Lanes of the DP warp active at super-step t (lane L works on column group
@@ -441,7 +469,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
 #ifdef BM_PROF_FAKE_SCORE  // timing experiment only: DP side lower bound
             const double sv = (double)(hv & 0xff) * 0.01 + sp[i].pos;
 #else
-            const double sv = staged_score(S, a.M, exp_tab, a.tabs, sp[i], sp[n + j], hv & 0xff, hv >> 8);
+            const double sv = staged_score(S, a.M, exp_tab, a.tabs, a.mt, sp[i], sp[n + j], hv & 0xff, hv >> 8);
 #endif
             slot[kt * (BPT * RL)] = __dsub_rn(1.0, sv);
           }
@@ -504,7 +532,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
         ci = cell >> 16;
         cj = cell & 0xffff;
         const uint32_t hv = hits16[ci * m + cj];
-        sv = staged_score(S, a.M, exp_tab, a.tabs, sp[ci], sp[n + cj], hv & 0xff, hv >> 8);
+        sv = staged_score(S, a.M, exp_tab, a.tabs, a.mt, sp[ci], sp[n + cj], hv & 0xff, hv >> 8);
         keep = sv >= a.threshold;
       }
       const unsigned mask = __ballot_sync(kFull, keep);
