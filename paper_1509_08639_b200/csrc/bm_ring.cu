@@ -213,10 +213,9 @@ struct __align__(16) SPack {
 #ifndef BM_RING_FOLD
 #define BM_RING_FOLD 1
 #endif
-__device__ __forceinline__ double staged_score(const bm_sentences& S, const Model& M,
-                                               const uint64_t* exp_tab, const PairTables& tb,
-                                               const ModelTables& mt, const SPack a,
-                                               const SPack b, int hf, int hr) {
+__device__ __forceinline__ double staged_margin(const bm_sentences& S, const Model& M,
+                                                const PairTables& tb, const ModelTables& mt,
+                                                const SPack a, const SPack b, int hf, int hr) {
   // every count is < 256 here (routing: T <= 255 bounds P, |A|, |D| and hits)
   const int aT = a.tpad & 0xff, aP = (a.tpad >> 8) & 0xff, aA = (a.tpad >> 16) & 0xff,
             aD = a.tpad >> 24;
@@ -239,7 +238,7 @@ __device__ __forceinline__ double staged_score(const bm_sentences& S, const Mode
   z = __dadd_rn(z, __ldg(mt.p4 + aP * kPairMax + bP));
   z = __dadd_rn(z, __dmul_rn(M.w[5], __dsub_rn(1.0, fabs(__dsub_rn(a.pos, b.pos)))));
   z = __dadd_rn(z, M.w[6]);  // w6 * 1.0
-  return bmexp::confidence_from_z(z, exp_tab);
+  return z;
 #else
   double f[7];
   f[0] = __ldg(tb.ratio2 + aT * kPairMax + bT);
@@ -256,8 +255,15 @@ __device__ __forceinline__ double staged_score(const bm_sentences& S, const Mode
   f[4] = __ldg(tb.ratio2 + aP * kPairMax + bP);
   f[5] = __dsub_rn(1.0, fabs(__dsub_rn(a.pos, b.pos)));
   f[6] = 1.0;
-  return bmexp::confidence_from_z(margin(M, f), exp_tab);
+  return margin(M, f);
 #endif
+}
+
+__device__ __forceinline__ double staged_score(const bm_sentences& S, const Model& M,
+                                               const uint64_t* exp_tab, const PairTables& tb,
+                                               const ModelTables& mt, const SPack a,
+                                               const SPack b, int hf, int hr) {
+  return bmexp::confidence_from_z(staged_margin(S, M, tb, mt, a, b, hf, hr), exp_tab);
 }
 
 // Lanes of the DP warp active at super-step t (lane L works on column group
@@ -467,11 +473,11 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
           if (L <= la.y && i < n && j < m) {
             const uint32_t hv = hits16[i * m + j];
 #ifdef BM_PROF_FAKE_SCORE  // timing experiment only: DP side lower bound
-            const double sv = (double)(hv & 0xff) * 0.01 + sp[i].pos;
+            slot[kt * (BPT * RL)] = __dsub_rn(1.0, (double)(hv & 0xff) * 0.01 + sp[i].pos);
 #else
-            const double sv = staged_score(S, a.M, exp_tab, a.tabs, a.mt, sp[i], sp[n + j], hv & 0xff, hv >> 8);
+            slot[kt * (BPT * RL)] = bmexp::one_minus_confidence(
+                staged_margin(S, a.M, a.tabs, a.mt, sp[i], sp[n + j], hv & 0xff, hv >> 8), exp_tab);
 #endif
-            slot[kt * (BPT * RL)] = __dsub_rn(1.0, sv);
           }
         }
         q0 += ntask;

@@ -163,7 +163,8 @@ BM_HD double exp_glibc(double x, const uint64_t* T) {
 
 // bimine/classifier.py:100-117: sigmoid, then clamp into [1e-300, 1-2^-53]
 // with Python's min/max semantics (first argument wins unless strictly beaten).
-BM_HD double confidence_from_z(double z, const uint64_t* T) {
+// The unclamped sigmoid (classifier.py:100-104), p in [0, 1] or NaN.
+BM_HD double sigmoid_glibc(double z, const uint64_t* T) {
   // Branch-free form of the two sigmoid branches: exactly one exp and one
   // division per call, so lanes of a warp with mixed signs do not execute both.
   //   z >= 0: 1 / (1 + exp(-z))      z < 0 (or NaN): exp(z) / (1 + exp(z))
@@ -171,14 +172,26 @@ BM_HD double confidence_from_z(double z, const uint64_t* T) {
   const double e = exp_glibc(nonneg ? -z : z, T);
   const double num = nonneg ? 1.0 : e;
 #if defined(__CUDA_ARCH__)
-  const double p = __ddiv_rn(num, add_(1.0, e));
+  return __ddiv_rn(num, add_(1.0, e));
 #else
-  const double p = num / (1.0 + e);
+  return num / (1.0 + e);
 #endif
+}
+
+BM_HD double confidence_from_z(double z, const uint64_t* T) {
+  const double p = sigmoid_glibc(z, T);
   const double PMIN = 1e-300;
   const double PMAX = 1.0 - 0x1p-53;
   double lo = (PMIN > p) ? PMIN : p;   // max(p, PMIN)
   return (PMAX < lo) ? PMAX : lo;      // min(lo, PMAX)
+}
+
+// 1 - confidence_from_z(z): the DP's diagonal cost. The lower clamp is not
+// needed here: for 0 <= p < 2^-54 both 1 - p and 1 - 1e-300 round to 1.0.
+BM_HD double one_minus_confidence(double z, const uint64_t* T) {
+  const double p = sigmoid_glibc(z, T);
+  const double PMAX = 1.0 - 0x1p-53;
+  return sub_(1.0, (PMAX < p) ? PMAX : p);
 }
 
 }  // namespace bmexp

@@ -84,3 +84,40 @@ def test_host_math_exp_is_the_reference_exp():
     z = np.load(golden("exp_golden.npz"))
     for x, b in list(zip(z["z"], z["exp_bits"]))[::37]:
         assert struct.unpack("<Q", struct.pack("<d", math.exp(float(x))))[0] == int(b)
+
+
+ONE_MINUS = r"""
+#include "glibc_exp.cuh"
+#include <stdio.h>
+#include <string.h>
+static const uint64_t T[256] = BM_EXP_TABLE_INIT;
+int main() {
+  /* the DP's diagonal cost 1 - S without the lower clamp == 1 - clamped S */
+  unsigned long long s = 2463534242ull; long bad = 0, n = 0;
+  double zs[] = {0.0, -0.0, 1e-300, -1e-300, 36.0, 37.0, 38.0, 40.0, 700.0, 800.0, -690.0,
+                 -700.0, -745.0, -746.0, -800.0, 1e308, -1e308, 0.0 / 0.0};
+  for (double z : zs) {
+    double a = 1.0 - bmexp::confidence_from_z(z, T), b = bmexp::one_minus_confidence(z, T);
+    n++; if (memcmp(&a, &b, 8) != 0 && !(a != a && b != b)) ++bad;
+  }
+  for (long k = 0; k < 2000000; ++k) {
+    s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+    double z = 1600.0 * ((double)(s >> 11) / 9007199254740992.0 - 0.5);
+    double a = 1.0 - bmexp::confidence_from_z(z, T), b = bmexp::one_minus_confidence(z, T);
+    n++; if (memcmp(&a, &b, 8) != 0) ++bad;
+  }
+  printf("%ld %ld\n", bad, n);
+  return 0;
+}
+"""
+
+
+def test_ring_cost_without_lower_clamp_is_exact(tmp_path):
+    """one_minus_confidence (the ring producers' 1 - S) equals 1 - S with both
+    clamps for every z, including the underflow and saturation ends."""
+    src = tmp_path / "om.cpp"
+    src.write_text(ONE_MINUS)
+    exe = tmp_path / "om"
+    subprocess.check_call(["g++", "-O2", "-ffp-contract=off", f"-I{CSRC}", str(src), "-o", str(exe), "-lm"])
+    bad, n = map(int, subprocess.check_output([str(exe)]).split())
+    assert n > 2_000_000 and bad == 0
