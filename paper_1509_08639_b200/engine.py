@@ -42,6 +42,19 @@ def _ptr(t) -> int:
     return int(t.data_ptr()) if t is not None and t.numel() > 0 else 0
 
 
+def to_host(t) -> np.ndarray:
+    """Device tensor -> numpy. Large results land in page-locked memory from
+    torch's caching host allocator and are returned as a view of it: a plain
+    .cpu() copies into freshly faulted pageable pages (C3's 127 MB of records
+    took 60 ms that way, 2 GB/s)."""
+    torch = torch_mod()
+    if not t.is_cuda or t.numel() * t.element_size() < (1 << 20):
+        return t.cpu().numpy()
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t)
+    return host.numpy()  # keeps `host` alive
+
+
 def to_dev(a: np.ndarray, dev):
     torch = torch_mod()
     a = np.ascontiguousarray(a)
@@ -165,7 +178,7 @@ def score(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model):
 
 
 def matrices_from_buffer(S, s_off, pitch, n, m) -> list[np.ndarray]:
-    host = S.cpu().numpy()
+    host = to_host(S)
     out = []
     for k in range(len(n)):
         o, p, nn, mm = int(s_off[k]), int(pitch[k]), int(n[k]), int(m[k])
@@ -267,7 +280,7 @@ def mine(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, threshold: f
     N.check(lib.bm_compact(_ptr(rec), _ptr(rec_off_d), _ptr(cnt), k, _ptr(dense), _ptr(total),
                            stream_ptr()))
     tot = int(total.item())
-    recs = dense[: tot * 24].cpu().numpy().view(np.dtype(N.RECORD_DTYPE))
+    recs = to_host(dense[: tot * 24]).view(np.dtype(N.RECORD_DTYPE))
     return recs, cost[:k].cpu().numpy()
 
 
