@@ -3,6 +3,7 @@
 // Host-side planning only: which kernel tier each document goes to, tile and
 // band work lists, offsets into stream-ordered scratch (cudaMallocAsync), and
 // error mapping. No arithmetic of the hot path happens here.
+#include <deque>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,6 +42,60 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (_e != cudaSuccess) return cuda_fail(_e, what); \
   } while (0)
 
+constexpr int kMaxMineStreams = 4;
+
+// Page-locked staging for host -> device uploads of host-built plans. A
+// cudaMemcpyAsync from pageable memory may wait for the stream's earlier work
+// before it returns (measured: the banded tier's 9 MB of tiles held the host
+// until the fused tier's kernels finished), so larger uploads are copied into
+// a page-locked block first; a block is reused once the event recorded after
+// its copy has completed.
+// (The blocks live as long as the thread: no CUDA calls at process teardown.)
+class PinnedPool {
+ public:
+  // copies bytes into a free block and enqueues the H2D copy on st
+  cudaError_t upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    Block* blk = nullptr;
+    for (Block& b : blocks_)
+      if (b.cap >= bytes && cudaEventQuery(b.ev) == cudaSuccess) {
+        blk = &b;
+        break;
+      }
+    if (blk == nullptr) {
+      size_t cap = 1 << 16;
+      while (cap < bytes) cap <<= 1;
+      Block b;
+      cudaError_t e = cudaHostAlloc((void**)&b.p, cap, cudaHostAllocDefault);
+      if (e != cudaSuccess) return e;
+      e = cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) {
+        cudaFreeHost(b.p);
+        return e;
+      }
+      b.cap = cap;
+      blocks_.push_back(b);
+      blk = &blocks_.back();
+    }
+    memcpy(blk->p, src, bytes);
+    cudaError_t e = cudaMemcpyAsync(dst, blk->p, bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    return cudaEventRecord(blk->ev, st);
+  }
+
+ private:
+  struct Block {
+    char* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+  };
+  std::deque<Block> blocks_;  // stable addresses
+};
+
+PinnedPool& pinned_pool() {
+  static thread_local PinnedPool pool;
+  return pool;
+}
+
 // Stream-ordered scratch: allocated on `st`, freed on `st` when it goes out of
 // scope, so it stays valid for every kernel enqueued before the free.
 class Scratch {
@@ -62,7 +117,9 @@ class Scratch {
   cudaError_t upload(T** out, const std::vector<T>& v) {
     cudaError_t e = alloc(out, v.size());
     if (e != cudaSuccess || v.empty()) return e;
-    return cudaMemcpyAsync(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st_);
+    const size_t bytes = v.size() * sizeof(T);
+    if (bytes >= (1 << 16)) return pinned_pool().upload(*out, v.data(), bytes, st_);
+    return cudaMemcpyAsync(*out, v.data(), bytes, cudaMemcpyHostToDevice, st_);
   }
 
  private:
@@ -266,17 +323,21 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
                  const int64_t* rec_off, bm_record* rec, int32_t* rec_count, double* cost,
                  bool doc_join, Scratch& sc, cudaStream_t st) {
   {
+    HostTrace tr("mine_general");
     const int k = (int)g.docs.size();
     GeneralDev dv;
     int rc = general_prepare(g, docs, sc, dv, st);
     if (rc) return rc;
+    tr.mark("prepare");
     const bm_docs D = local_docs(dv, k);
     rc = score_general(g, sent, D, lex, M, dv, doc_join, sc, st);
     if (rc) return rc;
+    tr.mark("score enqueued");
     double* cost_l = nullptr;
     BM_CK(sc.alloc(&cost_l, k), "alloc");
     rc = general_nw(g, dv, penalty, cost_l, st);
     if (rc) return rc;
+    tr.mark("nw enqueued");
     std::vector<int64_t> roff(k);
     int64_t rt = 0;
     for (int q = 0; q < k; ++q) {
@@ -444,7 +505,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   size_t fused_smem[4] = {0, 0, 0, 0}, hits_smem[4] = {0, 0, 0, 0};
   std::vector<int64_t> hit_off(nd, 0);
   int64_t hit_total = 0;
-  GeneralPlan g;
+  std::vector<int32_t> banded;  // planned after the fused tier is launched
   // BM_ROUTE=banded forces every document onto the K1 -> K2/K3 -> K4 tier
   // (benchmarking / testing both tiers on the same workload).
   const char* route = getenv("BM_ROUTE");
@@ -464,7 +525,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       hit_off[d] = hit_total;
       hit_total += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
     } else {
-      g.add(d, n, m);
+      banded.push_back(d);
     }
   }
   tr.mark("route");
@@ -510,12 +571,25 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       tr.mark("launch ring");
     }
   }
+  cudaEvent_t tl_fused = nullptr;
+  if (tr.on) {  // BM_TRACE: when the fused tier's kernels finish on the GPU
+    cudaEventCreate(&tl_fused);
+    cudaEventRecord(tl_fused, st);
+  }
+  GeneralPlan g;
+  for (int32_t d : banded) g.add(d, n_host[d], m_host[d]);
   if (!g.docs.empty()) {
     bool doc_join = true;
     for (int32_t d : g.docs) doc_join &= amax_host[d] <= 65535;
     int rc = mine_general(g, sent, docs, lex, M, threshold, penalty, rec_off, rec, rec_count, cost,
                           doc_join, sc, st);
     if (rc) return rc;
+    tr.mark("banded tier enqueued");
+  }
+  if (tr.on) {
+    cudaEventSynchronize(tl_fused);
+    tr.mark("fused tier done on GPU");
+    cudaEventDestroy(tl_fused);
   }
   return BM_OK;
 }
@@ -547,7 +621,6 @@ cudaStream_t copy_stream() {
 // Extra compute streams of the calling thread: bm_mine_host deals chunks
 // round-robin over the caller's stream and these, so a chunk's kernel tails
 // overlap the next chunks' kernels.
-constexpr int kMaxMineStreams = 4;
 cudaStream_t side_stream(int q) {
   static thread_local cudaStream_t s[kMaxMineStreams] = {};
   static thread_local int dev_of = -1;
