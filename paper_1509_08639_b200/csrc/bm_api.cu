@@ -264,7 +264,15 @@ int general_nw(const GeneralPlan& g, GeneralDev& dv, double penalty, double* cos
   return BM_OK;
 }
 
-bool check_penalty(double p) { return p >= 0.0; }  // NaN fails (aligner.py:209-213)
+bool check_penalty(double p) { return p >= 0.0; }
+
+// Largest ring-kernel smem slice a document may need and still take the fused
+// tier (BM_FUSED_MAX_SMEM overrides; experiments).
+size_t fused_max_smem() {
+  static const size_t v =
+      getenv("BM_FUSED_MAX_SMEM") ? (size_t)atoll(getenv("BM_FUSED_MAX_SMEM")) : (size_t)kFusedMaxSmem;
+  return v;
+}  // NaN fails (aligner.py:209-213)
 
 // BM_TRACE=1: host-side phase timings of the planning code on stderr.
 struct HostTrace {
@@ -517,7 +525,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     if (amax_host[d] > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
     const int R = fused_rows_per_lane(n);
     const size_t sl = ring_slice_bytes(n, m, R);
-    if (!force_banded && n <= kFusedMaxRows && sl <= (size_t)kFusedMaxSmem && amax_host[d] <= 255) {
+    if (!force_banded && n <= kFusedMaxRows && sl <= fused_max_smem() && amax_host[d] <= 255) {
       const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
       fused[q].push_back(d);
       fused_smem[q] = std::max(fused_smem[q], sl);
@@ -923,7 +931,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
         const int R = fused_rows_per_lane(n);
         psl = ring_slice_bytes(n, m, R);
         phs = hits_kernel_smem(n, m);
-        pq = (!force_banded && n <= kFusedMaxRows && psl <= (size_t)kFusedMaxSmem)
+        pq = (!force_banded && n <= kFusedMaxRows && psl <= fused_max_smem())
                  ? (R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3)
                  : -1;
         pn = n;

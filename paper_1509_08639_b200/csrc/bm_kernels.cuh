@@ -31,7 +31,7 @@ constexpr int kPublish = 16;             // boundary publication granularity
 
 // Fused miner limits (warp per document, everything in shared memory).
 constexpr int kFusedMaxRows = 256;       // n <= 32 * 8
-constexpr int kFusedMaxSmem = 200 * 1024;
+constexpr int kFusedMaxSmem = 64 * 1024;  // larger slices run 1-3 CTAs/SM: the banded tier is faster
 
 struct WorkItem {
   int32_t doc;

@@ -109,7 +109,6 @@ def c3(model, n_docs, check_docs):
                       reps=3)
     recs, cost = res["r"]
     ms = kernel_resident_ms(dc, dl, view, model)
-    fused = int(((c.n <= 256) & (c.n.astype(np.int64) * c.m <= 40000)).sum())
     # parity on a stratified sample: every k-th document, through the oracle
     idx = np.linspace(0, n_docs - 1, min(check_docs, n_docs)).astype(np.int64)
     hb = oracle.HostBatch(c, plex, c.src0[idx], c.n[idx], c.tgt0[idx], c.m[idx])
@@ -123,7 +122,7 @@ def c3(model, n_docs, check_docs):
             "timing": "kernel-resident: bm_mine + bm_compact on device buffers (CUDA events)",
             "ms_to_host": ms_host,
             "doc_pairs_per_s_to_host": n_docs / (ms_host / 1e3),
-            "records": int(recs.shape[0]), "fused_tier_docs_approx": fused,
+            "records": int(recs.shape[0]),
             "oracle_sample_docs": int(idx.size), "bit_exact_on_sample": bool(ok)}
 
 
