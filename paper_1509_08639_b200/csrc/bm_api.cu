@@ -320,7 +320,9 @@ int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs&
   BM_CK(cudaMemsetAsync(hits, 0, (size_t)ht * 4, st), "memset hits");
   BM_CK(sc.upload(&dho, hoff), "upload");
   BM_CK(sc.upload(&dit, items), "upload");
-  BM_CK(launch_score_hits(*sent, D, *lex, M, dit, (int)items.size(), hits, dho, dv.tiles,
+  ModelTables mt;
+  BM_CK(model_tables(M, &mt), "model tables");
+  BM_CK(launch_score_hits(*sent, D, *lex, M, mt, dit, (int)items.size(), hits, dho, dv.tiles,
                           (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S, st),
         "score_hits_kernel");
   return BM_OK;

@@ -271,8 +271,32 @@ __global__ void __launch_bounds__(64, 8) hits_doc_kernel(bm_sentences S, bm_docs
   }
 }
 
+// z of one cell from the model's folded tables (ModelTables; every count of
+// both sentences < kPairMax): the additions of margin() in its order.
+__device__ __forceinline__ double folded_margin(const bm_sentences& S, const Model& M,
+                                                const ModelTables& mt, const SentScalars& a,
+                                                const SentScalars& b, int hf, int hr,
+                                                double pos_s, double pos_t) {
+  double z = __ldg(mt.z1 + a.T * kPairMax + b.T);
+  z = __dadd_rn(z, __ldg(mt.p1 + hf * kPairMax + a.nA));
+  z = __dadd_rn(z, __ldg(mt.p2 + hr * kPairMax + b.nA));
+  double p3;
+  if ((a.nD | b.nD) == 0) {
+    p3 = M.w[3];  // w3 * 1.0
+  } else if (a.nD == 0 || b.nD == 0) {
+    p3 = __dmul_rn(M.w[3], 0.0);
+  } else {
+    const int inter = sorted_intersection(S.dig_id + a.d0, a.nD, S.dig_id + b.d0, b.nD);
+    p3 = __dmul_rn(M.w[3], frac_or_zero(inter, a.nD + b.nD - inter));
+  }
+  z = __dadd_rn(z, p3);
+  z = __dadd_rn(z, __ldg(mt.p4 + a.P * kPairMax + b.P));
+  z = __dadd_rn(z, __dmul_rn(M.w[5], __dsub_rn(1.0, fabs(__dsub_rn(pos_s, pos_t)))));
+  return __dadd_rn(z, M.w[6]);  // w6 * 1.0
+}
+
 __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
-    bm_sentences S, bm_docs D, Model M, const int4* __restrict__ tiles,
+    bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
     const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
     const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
     double* __restrict__ out) {
@@ -299,14 +323,29 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     dst->pos[local] = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
   }
   __syncthreads();
+  // the folded tables cover the tile when every T (which bounds P, |A|, |D|
+  // and the hit counts) is below kPairMax
+  bool small = true;
+  for (int k = 0; k < ns; ++k) small &= rows->T[k] < kPairMax;
+  for (int k = 0; k < nt; ++k) small &= cols->T[k] < kPairMax;
   const uint32_t* hd = hits + h_off[doc] + (int64_t)r0 * m + c0;
   double* dst = out + s_off[doc] + (int64_t)r0 * pitch[doc] + c0;
   const int64_t ld = pitch[doc];
-  for (int c = threadIdx.x; c < ns * nt; c += blockDim.x) {
-    const int i = c / nt, j = c - (c / nt) * nt;
+  // fixed column per thread (kTile divides the block): no per-cell division
+  static_assert(kTileThreads % kTile == 0, "tile rows per pass");
+  const int j = threadIdx.x % kTile;
+  if (j >= nt) return;
+  const SentScalars b = get_scalars(*cols, j);
+  const double pos_t = cols->pos[j];
+  for (int i = threadIdx.x / kTile; i < ns; i += kTileThreads / kTile) {
     const uint32_t hv = __ldg(hd + (int64_t)i * m + j);
-    dst[i * ld + j] = cell_score(S, M, exp_tab, get_scalars(*rows, i), get_scalars(*cols, j),
-                                 (int)(hv & 0xffffu), (int)(hv >> 16), rows->pos[i], cols->pos[j]);
+    const SentScalars a = get_scalars(*rows, i);
+    dst[i * ld + j] =
+        small ? bmexp::confidence_from_z(folded_margin(S, M, mt, a, b, (int)(hv & 0xffffu),
+                                                       (int)(hv >> 16), rows->pos[i], pos_t),
+                                         exp_tab)
+              : cell_score(S, M, exp_tab, a, b, (int)(hv & 0xffffu), (int)(hv >> 16),
+                           rows->pos[i], pos_t);
   }
 }
 
@@ -325,7 +364,8 @@ void join_items(const int32_t* n, const int32_t* m, int nd, std::vector<int4>& i
 }
 
 cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_lexicon& L,
-                              const Model& M, const int4* items, int n_items, uint32_t* hits,
+                              const Model& M, const ModelTables& mt, const int4* items,
+                              int n_items, uint32_t* hits,
                               const int64_t* h_off, const int4* tiles, int n_tiles,
                               const int64_t* s_off, const int32_t* pitch, double* out,
                               cudaStream_t st) {
@@ -336,7 +376,7 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
   if (e != cudaSuccess) return e;
   if (n_items) hits_doc_kernel<<<n_items, 64, hs, st>>>(S, D, L, items, n_items, h_off, hits);
   const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars);
-  score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, tiles, s_off, pitch, hits, h_off,
+  score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits, h_off,
                                                        out);
   return counted(cudaGetLastError(), n_items ? 2 : 1);
 }

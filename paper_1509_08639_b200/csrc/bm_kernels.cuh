@@ -126,7 +126,7 @@ cudaError_t launch_tune_count(const uint32_t*, const int64_t*, const double*, co
                               unsigned long long*, cudaStream_t);
 void join_items(const int32_t* n, const int32_t* m, int nd, std::vector<int4>& items);
 cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_lexicon& L,
-                              const Model& M, const int4* items, int n_items, uint32_t* hits,
+                              const Model& M, const ModelTables& mt, const int4* items, int n_items, uint32_t* hits,
                               const int64_t* h_off, const int4* tiles, int n_tiles,
                               const int64_t* s_off, const int32_t* pitch, double* out,
                               cudaStream_t st);
