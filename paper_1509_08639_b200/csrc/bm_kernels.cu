@@ -310,10 +310,12 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   const int ns = min(kTile, n - r0), nt = min(kTile, m - c0);
   const int s0 = D.src0[doc] + r0, t0 = D.tgt0[doc] + c0;
   stage_exp_table(exp_tab, threadIdx.x, blockDim.x);
+  int fits = 1;  // every T (which bounds P, |A|, |D| and the hits) < kPairMax
   for (int k = threadIdx.x; k < ns + nt; k += blockDim.x) {
     const bool is_row = k < ns;
     const int local = is_row ? k : k - ns;
     SentScalars sc = load_scalars(S, is_row ? s0 + local : t0 + local);
+    fits &= sc.T < kPairMax;
     TileScalars* dst = is_row ? rows : cols;
     dst->T[local] = sc.T;
     dst->P[local] = sc.P;
@@ -322,12 +324,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     dst->d0[local] = sc.d0;
     dst->pos[local] = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
   }
-  __syncthreads();
-  // the folded tables cover the tile when every T (which bounds P, |A|, |D|
-  // and the hit counts) is below kPairMax
-  bool small = true;
-  for (int k = 0; k < ns; ++k) small &= rows->T[k] < kPairMax;
-  for (int k = 0; k < nt; ++k) small &= cols->T[k] < kPairMax;
+  // the folded tables cover the tile when all of its sentences fit them
+  const bool small = __syncthreads_and(fits) != 0;
   const uint32_t* hd = hits + h_off[doc] + (int64_t)r0 * m + c0;
   double* dst = out + s_off[doc] + (int64_t)r0 * pitch[doc] + c0;
   const int64_t ld = pitch[doc];
