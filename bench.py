@@ -58,7 +58,8 @@ def make_workload(n_docs: int, seed: int):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampled every 200 ms while the timed region runs."""
+    """nvidia-smi sampled every 100 ms while the timed regions run (entering
+    waits for the first sample, so the sampler is live before timing starts)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -73,10 +74,13 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", os.environ.get("BM_CLOCK_MS", "100")],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -283,8 +287,10 @@ def run_ours(args):
             dist.barrier()
         return times, launches
 
-    with ClockSampler(local) as clk:
-        times, launches = timed(step, args.steps, args.warmup)
+    # clocks are sampled across every timed GPU region below (device-resident
+    # steps, the dominant-kernel timing and the end-to-end steps)
+    clk = ClockSampler(local).__enter__()
+    times, launches = timed(step, args.steps, args.warmup)
     ms = float(np.mean(times))
     t_all = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -314,6 +320,7 @@ def run_ours(args):
         d2h[0] = dbytes
 
     e_times, e_launch = timed(e2e_step, args.steps, max(1, args.warmup // 2))
+    clk.__exit__(None, None, None)
     e_tot = torch.tensor([sum(e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
