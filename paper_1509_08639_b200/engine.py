@@ -284,40 +284,63 @@ def mine(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, threshold: f
     return recs, cost[:k].cpu().numpy()
 
 
-def tune_counts(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, penalties,
-                thresholds, gold_keys: list[np.ndarray]):
-    """K5: pred/hit counts [n_pen, n_thr] over the view's docs."""
-    torch = torch_mod()
-    lib = N.lib()
-    dev = device()
-    docs, lex, n, m = view.docs, dl.lex, view.n, view.m
-    pen = np.ascontiguousarray(np.asarray(penalties, dtype=np.float64))
-    thr = np.asarray(thresholds, dtype=np.float64)
-    # per-doc ascending gold keys, packed with one vectorised sort
+def pack_gold(gold_keys: list[np.ndarray]):
+    """Per-doc ascending gold keys (i * m + j) -> (keys int64, offsets int64 [k+1]),
+    packed with one vectorised sort (tuner.py:157-203 gold set, as device keys)."""
     lens = np.fromiter((len(g) for g in gold_keys), dtype=np.int64, count=len(gold_keys))
     goff = np.zeros(len(gold_keys) + 1, dtype=np.int64)
     np.cumsum(lens, out=goff[1:])
-    if lens.sum():
-        keys = np.concatenate([np.asarray(g, dtype=np.int64).ravel() for g in gold_keys])
-        step = np.diff(keys)
-        inner = goff[1:-1]
-        step[inner[(inner > 0) & (inner < keys.size)] - 1] = 0  # doc boundaries may descend
-        if (step < 0).any():  # sort within docs: one sort of (doc << 40 | key)
-            if keys.min() < 0 or keys.max() >= (1 << 40):
-                raise ValueError("gold keys must lie in [0, 2**40)")
-            owner = np.repeat(np.arange(len(gold_keys), dtype=np.int64), lens)
-            keys = np.sort((owner << 40) | keys) & ((1 << 40) - 1)
-        gall = np.ascontiguousarray(keys)
-    else:
-        gall = np.zeros(0, np.int64)
+    if not lens.sum():
+        return np.zeros(0, np.int64), goff
+    keys = np.concatenate([np.asarray(g, dtype=np.int64).ravel() for g in gold_keys])
+    step = np.diff(keys)
+    inner = goff[1:-1]
+    step[inner[(inner > 0) & (inner < keys.size)] - 1] = 0  # doc boundaries may descend
+    if (step < 0).any():  # sort within docs: one sort of (doc << 40 | key)
+        if keys.min() < 0 or keys.max() >= (1 << 40):
+            raise ValueError("gold keys must lie in [0, 2**40)")
+        owner = np.repeat(np.arange(len(gold_keys), dtype=np.int64), lens)
+        keys = np.sort((owner << 40) | keys) & ((1 << 40) - 1)
+    return np.ascontiguousarray(keys), goff
+
+
+class DeviceGold:
+    """Packed gold keys resident on the device (uploaded once per sweep)."""
+
+    def __init__(self, keys: np.ndarray, goff: np.ndarray):
+        dev = device()
+        self.keys = to_dev(keys, dev)
+        self.goff = to_dev(goff, dev)
+
+    @classmethod
+    def of(cls, gold_keys: list[np.ndarray]) -> "DeviceGold":
+        return cls(*pack_gold(gold_keys))
+
+
+def tune_counts_device(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, penalties,
+                       thresholds, gold: DeviceGold):
+    """K5 on device-resident inputs: pred/hit counts [n_pen, n_thr] as device tensors."""
+    torch = torch_mod()
+    lib = N.lib()
+    dev = device()
+    pen = np.ascontiguousarray(np.asarray(penalties, dtype=np.float64))
+    thr = np.asarray(thresholds, dtype=np.float64)
     pred = torch.zeros((len(pen), len(thr)), dtype=torch.int64, device=dev)
     hit = torch.zeros((len(pen), len(thr)), dtype=torch.int64, device=dev)
-    thr_d, gall_d, goff_d = to_dev(thr, dev), to_dev(gall, dev), to_dev(goff, dev)
-    n_h, m_h = _i32(n), _i32(m)
-    N.check(lib.bm_tune(C.byref(dc.sent), C.byref(docs), n_h.ctypes.data, m_h.ctypes.data,
-                        C.byref(lex), C.byref(N.model_struct(model)), pen.ctypes.data, len(pen),
-                        _ptr(thr_d), len(thr), _ptr(gall_d), _ptr(goff_d), _ptr(pred), _ptr(hit),
-                        dc.max_tok, stream_ptr()))
+    thr_d = to_dev(thr, dev)
+    n_h, m_h = _i32(view.n), _i32(view.m)
+    N.check(lib.bm_tune(C.byref(dc.sent), C.byref(view.docs), n_h.ctypes.data, m_h.ctypes.data,
+                        C.byref(dl.lex), C.byref(N.model_struct(model)), pen.ctypes.data, len(pen),
+                        _ptr(thr_d), len(thr), _ptr(gold.keys), _ptr(gold.goff), _ptr(pred),
+                        _ptr(hit), dc.max_tok, stream_ptr()))
+    return pred, hit
+
+
+def tune_counts(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, penalties,
+                thresholds, gold_keys: list[np.ndarray]):
+    """K5: pred/hit counts [n_pen, n_thr] over the view's docs."""
+    pred, hit = tune_counts_device(dc, dl, view, model, penalties, thresholds,
+                                   DeviceGold.of(gold_keys))
     return pred.cpu().numpy(), hit.cpu().numpy()
 
 

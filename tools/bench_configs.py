@@ -126,6 +126,62 @@ def c3(model, n_docs, check_docs):
             "oracle_sample_docs": int(idx.size), "bit_exact_on_sample": bool(ok)}
 
 
+def c3_full(model, n_docs, chunk, check_per_chunk):
+    """C3 at its BASELINE size: n_docs (1M) skewed docs drawn once from
+    c3_shape(n_docs, 2026), generated and mined in chunks of `chunk` docs
+    (chunk k's text seeded 2026 + k). Per chunk: kernel-resident time
+    (bm_mine + bm_compact), time with the records back on the host
+    (engine.mine), and an oracle check of a stratified sample."""
+    g, a, b = synth.c3_shape(n_docs, seed=2026)
+    tot = {"cells": 0, "ms": 0.0, "ms_to_host": 0.0, "records": 0, "checked": 0, "ok": True,
+           "gen_s": 0.0, "oracle_s": 0.0}
+    for k, lo in enumerate(range(0, n_docs, chunk)):
+        hi = min(lo + chunk, n_docs)
+        t0 = time.perf_counter()
+        sc = synth.make_corpus(g[lo:hi], a[lo:hi], b[lo:hi], seed=2026 + k)
+        c = sc.packed
+        plex = sc.world.packed_lexicon()
+        tot["gen_s"] += time.perf_counter() - t0
+        dc = engine.DeviceCorpus.upload(c)
+        dl = engine.DeviceLexicon.upload(plex)
+        view = engine.DocView.of(c)
+        tot["cells"] += int((c.n.astype(np.int64) * c.m).sum())
+        res = {}
+        tot["ms_to_host"] += cuda_ms(
+            lambda: res.__setitem__("r", engine.mine(dc, dl, view, model, 0.5, 0.2)), reps=1)
+        recs, cost = res["r"]
+        tot["ms"] += kernel_resident_ms(dc, dl, view, model, reps=1)
+        tot["records"] += int(recs.shape[0])
+        t0 = time.perf_counter()
+        # stratified by size: every k-th doc of the size-sorted chunk, plus the largest doc
+        order = np.argsort(c.n.astype(np.int64) * c.m, kind="stable")
+        idx = np.unique(np.r_[order[np.linspace(0, hi - lo - 1, check_per_chunk).astype(np.int64)]])
+        hb = oracle.HostBatch(c, plex, c.src0[idx], c.n[idx], c.tgt0[idx], c.m[idx])
+        want, wcost = oracle.mine(hb, model, 0.5, 0.2, threads=os.cpu_count() or 8)
+        sel = np.isin(recs["doc"], idx)
+        got = recs[sel].copy()
+        got["doc"] = np.searchsorted(idx, got["doc"])
+        ok = got.tobytes() == want.tobytes() and np.array_equal(cost[idx].view(np.uint64),
+                                                                wcost.view(np.uint64))
+        tot["oracle_s"] += time.perf_counter() - t0
+        tot["ok"] = tot["ok"] and bool(ok)
+        tot["checked"] += int(idx.size)
+        del dc, dl, view, res, recs, cost, sc, c
+        torch.cuda.empty_cache()
+        print(json.dumps({"chunk": k, "docs": hi - lo, "ms_so_far": tot["ms"], "ok": tot["ok"]}),
+              file=sys.stderr, flush=True)
+    ms = tot["ms"]
+    return {"config": f"C3 skewed corpus, {n_docs} docs (chunks of {chunk})", "cells": tot["cells"],
+            "ms": ms, "doc_pairs_per_s": n_docs / (ms / 1e3), "gcups": tot["cells"] / (ms / 1e3) / 1e9,
+            "timing": "kernel-resident: sum over chunks of bm_mine + bm_compact (CUDA events)",
+            "ms_to_host": tot["ms_to_host"],
+            "doc_pairs_per_s_to_host": n_docs / (tot["ms_to_host"] / 1e3),
+            "records": tot["records"], "oracle_sample_docs": tot["checked"],
+            "oracle_sample": f"{check_per_chunk} docs per chunk, stratified by n*m incl. the largest",
+            "bit_exact_on_sample": tot["ok"], "host_generation_s": tot["gen_s"],
+            "oracle_s": tot["oracle_s"]}
+
+
 def c4(check: bool):
     S = np.random.default_rng(303).random((8192, 8192))
     St, s_off, pitch, n, m = engine.upload_matrices([S])
@@ -153,9 +209,11 @@ def c5(model, n_docs, check_docs):
     dl = engine.DeviceLexicon.upload(plex)
     view = engine.DocView.of(c)
     res = {}
-    ms = cuda_ms(lambda: res.__setitem__("r", engine.tune_counts(dc, dl, view, model, pens, thrs, keys)),
-                 reps=2)
+    ms_call = cuda_ms(lambda: res.__setitem__("r", engine.tune_counts(dc, dl, view, model, pens, thrs, keys)),
+                      reps=2)
     p, h = res["r"]
+    gold = engine.DeviceGold.of(keys)
+    ms = cuda_ms(lambda: engine.tune_counts_device(dc, dl, view, model, pens, thrs, gold), reps=3)
     k = min(check_docs, n_docs)
     hb = oracle.HostBatch(c, plex, c.src0[:k], c.n[:k], c.tgt0[:k], c.m[:k])
     wp, wh = oracle.tune(hb, model, pens, thrs, keys[:k], threads=os.cpu_count() or 8)
@@ -163,6 +221,8 @@ def c5(model, n_docs, check_docs):
     sp, sh = engine.tune_counts(dc, dl, sub, model, pens, thrs, keys[:k])
     cells = int((c.n.astype(np.int64) * c.m).sum())
     return {"config": f"C5 tune sweep {n_docs} docs x 64 grid points", "ms": ms,
+            "timing": "device-resident: bm_tune with gold keys already on the device (CUDA events)",
+            "ms_with_host_gold_packing": ms_call,
             "doc_pairs_per_s": n_docs / (ms / 1e3), "dp_gcups": cells * len(pens) / (ms / 1e3) / 1e9,
             "oracle_sample_docs": k, "counts_identical_on_sample": bool(np.array_equal(sp, wp) and np.array_equal(sh, wh))}
 
@@ -177,7 +237,8 @@ def c5w(model, n_docs):
     dc = engine.DeviceCorpus.upload(c)
     dl = engine.DeviceLexicon.upload(plex)
     view = engine.DocView.of(c)
-    ms = cuda_ms(lambda: engine.tune_counts(dc, dl, view, model, pens, [0.5], keys), reps=2)
+    gold = engine.DeviceGold.of(keys)
+    ms = cuda_ms(lambda: engine.tune_counts_device(dc, dl, view, model, pens, [0.5], gold), reps=2)
     cells = int((c.n.astype(np.int64) * c.m).sum())
     return {"config": f"C5 worst case: {n_docs} docs x 64 penalties x 1 threshold", "ms": ms,
             "doc_pairs_per_s": n_docs / (ms / 1e3), "dp_gcups": cells * 64 / (ms / 1e3) / 1e9}
@@ -189,6 +250,9 @@ def main():
     ap.add_argument("--c5-docs", type=int, default=20000)
     ap.add_argument("--check-docs", type=int, default=300)
     ap.add_argument("--c4-check", action="store_true")
+    ap.add_argument("--c3-full-docs", type=int, default=1000000)
+    ap.add_argument("--c3-chunk", type=int, default=100000)
+    ap.add_argument("--check-per-chunk", type=int, default=100)
     ap.add_argument("--only", default="c1,c3,c4,c5")
     args = ap.parse_args()
     torch.cuda.set_device(0)
@@ -199,6 +263,9 @@ def main():
         print(json.dumps(c1(model, lex)), flush=True)
     if "c3" in todo:
         print(json.dumps(c3(model, args.c3_docs, args.check_docs)), flush=True)
+    if "c3full" in todo:
+        print(json.dumps(c3_full(model, args.c3_full_docs, args.c3_chunk, args.check_per_chunk)),
+              flush=True)
     if "c4" in todo:
         print(json.dumps(c4(args.c4_check)), flush=True)
     if "c5" in todo:
