@@ -1161,15 +1161,55 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   rc = score_general(g, sent, D, lex, to_model(model), dv,
                      token_bound >= 0 && token_bound <= 65535, sc, st);
   if (rc) return rc;
+  // Penalties run in passes of up to 4 (nw_band_kernel<D, NP>): one pass
+  // stages S once for all of its penalties; each penalty has its own codes and
+  // boundary rows. The pass width shrinks when the codes would not fit.
+  int width = n_pen >= 4 ? 4 : n_pen >= 2 ? 2 : 1;
+  const size_t dir_bytes = (size_t)std::max<int64_t>(g.dir_total, 1) * 4;
+  while (width > 1 && (size_t)width * dir_bytes > ((size_t)16 << 30)) width /= 2;
   double* cost_l = nullptr;
-  BM_CK(sc.alloc(&cost_l, k), "alloc");
-  for (int q = 0; q < n_pen; ++q) {
-    rc = general_nw(g, dv, penalties_host[q], cost_l, st);
-    if (rc) return rc;
-    BM_CK(launch_tune_count(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, k,
-                            thresholds, n_thr, gold, gold_off, pred + (size_t)q * n_thr,
-                            hit + (size_t)q * n_thr, st),
-          "tune_count_kernel");
+  BM_CK(sc.alloc(&cost_l, (size_t)k * width), "alloc");
+  uint32_t* dirs = dv.dirs;
+  double* bnd = dv.bnd;
+  const int64_t dstride = std::max<int64_t>(g.dir_total, 1), bstride = std::max<int64_t>(g.bnd_total, 1);
+  if (width > 1) {
+    BM_CK(sc.alloc(&dirs, (size_t)dstride * width), "alloc dirs");
+    BM_CK(sc.alloc(&bnd, (size_t)bstride * width), "alloc boundary");
+  }
+  for (int q0 = 0; q0 < n_pen;) {
+    int np = width;
+    while (q0 + np > n_pen) np /= 2;
+    BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
+    BM_CK(cudaMemsetAsync(bnd, 0xde, (size_t)bstride * np * 8, st), "memset");
+    NwArgs a;
+    a.S = dv.S;
+    a.s_off = dv.s_off;
+    a.pitch = dv.pitch;
+    a.n = dv.n;
+    a.m = dv.m;
+    a.p = penalties_host[q0];
+    a.np = np;
+    for (int q = 0; q < np; ++q) a.pv[q] = penalties_host[q0 + q];
+    a.dirs = dirs;
+    a.dir_stride = dstride;
+    a.dir_off = dv.dir_off;
+    a.cost = cost_l;
+    a.cost_stride = k;
+    a.items = dv.items;
+    a.n_items = (int)g.items.size();
+    a.ticket = dv.ticket;
+    a.bnd = bnd;
+    a.bnd_stride = bstride;
+    a.bnd_off = dv.bnd_off;
+    BM_CK(launch_nw(a, st), "nw_band_kernel");
+    for (int q = 0; q < np; ++q) {
+      const size_t pq = (size_t)(q0 + q) * n_thr;
+      BM_CK(launch_tune_count(dirs + (size_t)q * dstride, dv.dir_off, dv.S, dv.s_off, dv.pitch,
+                              dv.n, dv.m, k, thresholds, n_thr, gold, gold_off, pred + pq,
+                              hit + pq, st),
+            "tune_count_kernel");
+    }
+    q0 += np;
   }
   return BM_OK;
 }

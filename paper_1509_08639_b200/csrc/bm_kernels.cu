@@ -472,7 +472,9 @@ constexpr unsigned kFull = 0xffffffffu;
 // 4 when many (doc, band) items run at once (smaller rings -> more warps/SM)
 constexpr int kNwLane = kBandR * 4 + 2;                      // doubles per lane slice (+pad)
 constexpr int kNwSlotBytes = WARP * kNwLane * 8;
-__host__ __device__ constexpr int nw_smem(int D) { return (D + 1) * kNwSlotBytes + WARP * 8; }
+__host__ __device__ constexpr int nw_smem(int D, int NP = 1) {
+  return (D + 1) * kNwSlotBytes + NP * WARP * 8;
+}
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -538,14 +540,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // next block, shuffles and stores with the 7-cell dependency chain of the
 // current one. S for block g+1 is loaded and turned into 1-S during block g
 // (two register sets, ping-pong by a 2x unrolled loop).
-template <int D>
+template <int D, int NP>
 __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
+  // NP > 1 (tuner): NP penalties run over the same band in one pass. S is
+  // staged and turned into 1-S once for all of them, and their NP independent
+  // dependency chains interleave in the block (ILP the single chain lacks).
   extern __shared__ __align__(16) double nw_ring[];
   const int lane = threadIdx.x;
-  double* bnd_s = nw_ring + (D + 1) * WARP * kNwLane;  // current 32-column boundary chunk
+  double* bnd_s = nw_ring + (D + 1) * WARP * kNwLane;  // NP x 32-column boundary chunks
   const double* ring_l = nw_ring + (size_t)lane * kNwLane;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring_l);
+  double pq[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) pq[q] = NP == 1 ? a.p : a.pv[q];
   for (;;) {
     int it = 0;
     if (lane == 0) it = (int)atomicAdd(a.ticket, 1u);
@@ -556,7 +564,6 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
             if (lane == 0 && it < 8192) g_nw_prof[it][0] = gtimer();)
     const int d = w.doc, band = w.band;
     const int n = a.n[d], m = a.m[d];
-    const double p = a.p;
     const int row0 = band * kBandRows;
     const int nl = (min(kBandRows, n - row0) + kBandR - 1) / kBandR;
     const int nbands = (n + kBandRows - 1) / kBandRows;
@@ -607,12 +614,18 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     double oA[16], oB[16];
     load(-lane, oA);
 
-    const double il0 = (double)(i0 + 1) * p, il1 = (double)(i0 + 2) * p;
-    const double il2 = (double)(i0 + 3) * p, il3 = (double)(i0 + 4) * p;
-    const double idg = (double)i0 * p;
-    double l0 = il0, l1 = il1, l2 = il2, l3 = il3;  // C[i+1][4g]: left of the block
-    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;  // last row of the previous block
-    double dgn = idg;                                // C[i0][4g]: above-left of the block
+    // per penalty: C[i+1][4g] left of the block, the last row of the previous
+    // block, and C[i0][4g] above-left of the block
+    double l[NP][4], b[NP][4], dgn[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        l[q][r] = (double)(i0 + r + 1) * pq[q];
+        b[q][r] = 0.0;
+      }
+      dgn[q] = (double)i0 * pq[q];
+    }
 
     auto step = [&](const int t, double(&oc)[16], double(&on)[16]) {
       const int g = t - lane;
@@ -620,22 +633,25 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
         NW_PROF(const unsigned long long w0 = gtimer();)
         // lane 0's next 8 groups: the band above's last row (band 0: border)
         const int c = 4 * t + lane;
-        double v = 0.0;
-        if (c < m) {
-          if (band == 0) {
-            v = (double)(c + 1) * p;
-          } else {
-            uint64_t x;
-            while ((x = ld_relaxed_u64(bnd_up + c)) == kBndSentinel) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          double v = 0.0;
+          if (c < m) {
+            if (band == 0) {
+              v = (double)(c + 1) * pq[q];
+            } else {
+              uint64_t x;
+              while ((x = ld_relaxed_u64(bnd_up + q * a.bnd_stride + c)) == kBndSentinel) {
 #if !(defined(BM_NW_PROFILE) && defined(BM_NW_NOSLEEP))
-              __nanosleep(32);
+                __nanosleep(32);
 #endif
+              }
+              v = __longlong_as_double((long long)x);
             }
-            v = __longlong_as_double((long long)x);
           }
+          if (q == 0) __syncwarp();
+          bnd_s[q * WARP + lane] = v;
         }
-        __syncwarp();
-        bnd_s[lane] = v;
         __syncwarp();
         NW_PROF(if (t > 0) spins += gtimer() - w0;
                 if (lane == 0 && it < 16 && (t >> 3) < 256) {
@@ -644,81 +660,80 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
                 })
       }
       NW_PROF(if (first && g == 0 && lane == 0 && it < 8192) { g_nw_prof[it][1] = gtimer(); first = false; })
-      double u[4];
-      u[0] = __shfl_up_sync(kFull, b0, 1);
-      u[1] = __shfl_up_sync(kFull, b1, 1);
-      u[2] = __shfl_up_sync(kFull, b2, 1);
-      u[3] = __shfl_up_sync(kFull, b3, 1);
-      {
-        const double2 x = *(const double2*)(bnd_s + 4 * (t & 7));
-        const double2 y = *(const double2*)(bnd_s + 4 * (t & 7) + 2);
+      double u[NP][4];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) u[q][c] = __shfl_up_sync(kFull, b[q][c], 1);
+        const double2 x = *(const double2*)(bnd_s + q * WARP + 4 * (t & 7));
+        const double2 y = *(const double2*)(bnd_s + q * WARP + 4 * (t & 7) + 2);
         if (lane == 0) {
-          u[0] = x.x;
-          u[1] = x.y;
-          u[2] = y.x;
-          u[3] = y.y;
+          u[q][0] = x.x;
+          u[q][1] = x.y;
+          u[q][2] = y.x;
+          u[q][3] = y.y;
         }
-      }
-      if (g == 0) {  // the lane's first block: the left border of its rows
-        l0 = il0;
-        l1 = il1;
-        l2 = il2;
-        l3 = il3;
-        dgn = idg;
+        if (g == 0) {  // the lane's first block: the left border of its rows
+#pragma unroll
+          for (int r = 0; r < 4; ++r) l[q][r] = (double)(i0 + r + 1) * pq[q];
+          dgn[q] = (double)i0 * pq[q];
+        }
       }
       issue(g + D);
       cp_async_wait_depth<D>();  // block g+1 has landed
       load(g + 1, on);
 
-      // the 4x4 block, anti-diagonal order
-      double v[4][4];
-      uint32_t kc[4][4];
-      const double lf[4] = {l0, l1, l2, l3};
+      // the 4x4 block of every penalty, anti-diagonal order
+      double v[NP][4][4];
+      uint32_t codes[NP];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) codes[q] = 0;
 #pragma unroll
       for (int dd = 0; dd < 7; ++dd) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int c = dd - r;
           if (c < 0 || c > 3) continue;
-          const double dgv = r == 0 ? (c == 0 ? dgn : u[c - 1]) : (c == 0 ? lf[r - 1] : v[r - 1][c - 1]);
-          const double upv = r == 0 ? u[c] : v[r - 1][c];
-          const double lfv = c == 0 ? lf[r] : v[r][c - 1];
-          nw_cell(dgv, upv, lfv, oc[4 * r + c], p, v[r][c], kc[r][c]);
+#pragma unroll
+          for (int q = 0; q < NP; ++q) {
+            const double dgv = r == 0 ? (c == 0 ? dgn[q] : u[q][c - 1])
+                                      : (c == 0 ? l[q][r - 1] : v[q][r - 1][c - 1]);
+            const double upv = r == 0 ? u[q][c] : v[q][r - 1][c];
+            const double lfv = c == 0 ? l[q][r] : v[q][r][c - 1];
+            uint32_t kc;
+            nw_cell(dgv, upv, lfv, oc[4 * r + c], pq[q], v[q][r][c], kc);
+            codes[q] |= kc << (8 * c + 2 * r);
+          }
         }
       }
-      uint32_t codes = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) codes |= kc[r][c] << (8 * c + 2 * r);
-      dgn = u[3];  // C[i0][4g+4]: the next block's above-left cell
-      l0 = v[0][3];
-      l1 = v[1][3];
-      l2 = v[2][3];
-      l3 = v[3][3];
-      b0 = v[3][0];
-      b1 = v[3][1];
-      b2 = v[3][2];
-      b3 = v[3][3];
       const bool act = lane_on && (unsigned)g < (unsigned)ngroups;
-      if (act) dirs[(int64_t)g * WARP] = codes;
       const int cmax = m - 4 * g;  // >= 4 except in the last group
-      if (act && pub_lane) {
-        double* dst = bnd_me + 4 * g;
-        st_relaxed_f64(dst, b0);
-        if (cmax > 1) st_relaxed_f64(dst + 1, b1);
-        if (cmax > 2) st_relaxed_f64(dst + 2, b2);
-        if (cmax > 3) st_relaxed_f64(dst + 3, b3);
-        NW_PROF(if ((g & 7) == 7 && it < 16 && (g >> 3) < 256) g_nw_chunk[it][g >> 3][2] = gtimer();)
-      }
-      if (act && lane == cost_lane && g == ngroups - 1) {
-        // cell (n-1, m-1): row n-1-i0 of the block, column cmax-1
-        const int r = n - 1 - i0;
-        double row[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          row[c] = r == 0 ? v[0][c] : r == 1 ? v[1][c] : r == 2 ? v[2][c] : v[3][c];
-        a.cost[d] = cmax == 1 ? row[0] : cmax == 2 ? row[1] : cmax == 3 ? row[2] : row[3];
+      for (int q = 0; q < NP; ++q) {
+        dgn[q] = u[q][3];  // C[i0][4g+4]: the next block's above-left cell
+#pragma unroll
+        for (int r = 0; r < 4; ++r) l[q][r] = v[q][r][3];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) b[q][c] = v[q][3][c];
+        if (act) dirs[q * a.dir_stride + (int64_t)g * WARP] = codes[q];
+        if (act && pub_lane) {
+          double* dst = bnd_me + q * a.bnd_stride + 4 * g;
+          st_relaxed_f64(dst, b[q][0]);
+          if (cmax > 1) st_relaxed_f64(dst + 1, b[q][1]);
+          if (cmax > 2) st_relaxed_f64(dst + 2, b[q][2]);
+          if (cmax > 3) st_relaxed_f64(dst + 3, b[q][3]);
+          NW_PROF(if (q == 0 && (g & 7) == 7 && it < 16 && (g >> 3) < 256) g_nw_chunk[it][g >> 3][2] = gtimer();)
+        }
+        if (act && lane == cost_lane && g == ngroups - 1) {
+          // cell (n-1, m-1): row n-1-i0 of the block, column cmax-1
+          const int r = n - 1 - i0;
+          double row[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            row[c] = r == 0 ? v[q][0][c] : r == 1 ? v[q][1][c] : r == 2 ? v[q][2][c] : v[q][3][c];
+          a.cost[q * a.cost_stride + d] =
+              cmax == 1 ? row[0] : cmax == 2 ? row[1] : cmax == 3 ? row[2] : row[3];
+        }
       }
     };
     const int steps = ngroups + nl - 1;
@@ -733,35 +748,47 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   }
 }
 
-template <int D>
+template <int D, int NP>
 int nw_resident(int sms) {
   int per_sm = 0;
-  cudaFuncSetAttribute(nw_band_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, nw_smem(D));
-  cudaFuncSetAttribute(nw_band_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel<D>, WARP, nw_smem(D));
+  cudaFuncSetAttribute(nw_band_kernel<D, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       nw_smem(D, NP));
+  cudaFuncSetAttribute(nw_band_kernel<D, NP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel<D, NP>, WARP, nw_smem(D, NP));
   return sms * std::max(per_sm, 1);
 }
 
 // Persistent grid of min(resident warps, items); a shallow ring when the items
 // outnumber the warps a deep ring allows.
-cudaError_t launch_nw(const NwArgs& a, cudaStream_t st) {
-  if (a.n_items == 0) return cudaSuccess;
+template <int NP>
+cudaError_t launch_nw_np(const NwArgs& a, cudaStream_t st) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static thread_local int r8 = 0, r4 = 0, dev_of = -1;
   if (dev_of != dev) {
-    r8 = nw_resident<8>(sms);
-    r4 = nw_resident<4>(sms);
+    r8 = nw_resident<8, NP>(sms);
+    r4 = nw_resident<4, NP>(sms);
     dev_of = dev;
   }
   if (a.n_items > r8) {
-    nw_band_kernel<4><<<std::min(r4, a.n_items), WARP, nw_smem(4), st>>>(a);
+    nw_band_kernel<4, NP><<<std::min(r4, a.n_items), WARP, nw_smem(4, NP), st>>>(a);
   } else {
-    nw_band_kernel<8><<<std::min(r8, a.n_items), WARP, nw_smem(8), st>>>(a);
+    nw_band_kernel<8, NP><<<std::min(r8, a.n_items), WARP, nw_smem(8, NP), st>>>(a);
   }
   return counted(cudaGetLastError());
 }
+
+cudaError_t launch_nw(const NwArgs& a, cudaStream_t st) {
+  if (a.n_items == 0) return cudaSuccess;
+  switch (a.np) {
+    case 1: return launch_nw_np<1>(a, st);
+    case 2: return launch_nw_np<2>(a, st);
+    case 4: return launch_nw_np<4>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 
 // ---------------------------------------------------------------------------
 // K4: path walks over the 2-bit codes (tie order D > GS > GT is baked into the

@@ -88,6 +88,12 @@ struct NwArgs {
   unsigned int* ticket;
   double* bnd;               // boundary rows
   const int64_t* bnd_off;    // per doc: start of its (nb-1) x m boundary rows
+  // multi-penalty passes (tuner): penalty q of a pass uses pv[q] and writes
+  // dirs + q * dir_stride, bnd + q * bnd_stride, cost + q * cost_stride
+  int np = 1;
+  double pv[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t dir_stride = 0, bnd_stride = 0;
+  int cost_stride = 0;
 };
 
 struct FusedArgs {

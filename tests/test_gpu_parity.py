@@ -489,6 +489,25 @@ def test_tune_synthetic_vs_oracle(oracle_mod):
     assert np.array_equal(p, wp) and np.array_equal(h, wh)
 
 
+@pytest.mark.parametrize("n_pen", [1, 2, 3, 4, 7, 9])
+def test_tune_multi_penalty_passes_vs_oracle(oracle_mod, n_pen):
+    """Penalties run in passes of 4 / 2 / 1 through nw_band_kernel<D, NP>;
+    mixed sizes (multi-band docs hand boundary rows per penalty), ties from a
+    repeated penalty, and 0.0 (every diagonal wins) == oracle counts."""
+    from paper_1509_08639_b200 import engine
+
+    sc = _synth_mixed(9)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    pens = [0.2, 0.0, 0.6, 0.2, 1.6, 0.05, 0.35, 0.9, 0.1][:n_pen]
+    thrs = [0.3, 0.5, 0.8]
+    keys = [np.asarray(g[:, 0] * int(sc.packed.m[d]) + g[:, 1], np.int64) for d, g in enumerate(sc.gold)]
+    p, h = engine.tune_counts(engine.DeviceCorpus.upload(sc.packed), engine.DeviceLexicon.upload(plex),
+                              engine.DocView.of(sc.packed), model, pens, thrs, keys)
+    wp, wh = oracle_mod.tune(oracle_mod.HostBatch(sc.packed, plex), model, pens, thrs, keys, threads=8)
+    assert np.array_equal(p, wp) and np.array_equal(h, wh)
+
+
 def test_sharded_mining_equals_single(oracle_mod):
     """Two LPT shards mined separately (as two ranks would) == one batch."""
     from paper_1509_08639_b200 import engine, shard, synth
