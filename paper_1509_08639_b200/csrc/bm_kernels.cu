@@ -803,20 +803,32 @@ cudaError_t launch_nw(const NwArgs& a, cudaStream_t st) {
 // a time and done lane-parallel.
 // ---------------------------------------------------------------------------
 constexpr int kWalkWarps = 4;                        // documents per CTA
-constexpr int kWinWords = 32 * WARP;                 // 32 groups x 32 row-quads
-constexpr int kWalkSmem = kWalkWarps * 3 * kWinWords * 4;  // 48 KB
+// a window is WG column groups x 32 row-quads (one band x 4*WG columns)
+template <int WG>
+__host__ __device__ constexpr int win_words() { return WG * WARP; }
+template <int WG>
+__host__ __device__ constexpr int walk_smem() { return kWalkWarps * 3 * win_words<WG>() * 4; }
+constexpr int kWinWords = win_words<32>();
+constexpr int kWalkSmem = walk_smem<32>();  // 48 KB
+// the tuner's walks (many small documents, latency-bound) use half-width
+// windows: 24 KB per CTA -> twice the resident warps
+#ifndef BM_TUNE_WG
+#define BM_TUNE_WG 16
+#endif
+constexpr int kTuneWG = BM_TUNE_WG;
 
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
 
 // Stage window (band, w) of a document's codes into buf (one commit group).
+template <int WG>
 __device__ __forceinline__ void win_load(uint32_t* buf, const uint32_t* dd, int nbands, int ngroups,
                                          int band, int w, int lane) {
   if (band >= 0 && w >= 0 && band < nbands) {
-    const uint32_t* base = dd + ((int64_t)band * ngroups + w * 32) * WARP + lane;
+    const uint32_t* base = dd + ((int64_t)band * ngroups + w * WG) * WARP + lane;
     const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + lane);
-    const int gl = min(32, ngroups - w * 32);
+    const int gl = min(WG, ngroups - w * WG);
     for (int q = 0; q < gl; ++q) cp_async4(dst + q * WARP * 4, base + q * WARP);
   }
   cp_async_commit();
@@ -825,23 +837,26 @@ __device__ __forceinline__ void win_load(uint32_t* buf, const uint32_t* dd, int 
 // Walk the path of one document from (n, m) towards (0, 0), calling
 // visit(op, i, j) for every interior move (0-based cell (i, j)) with all lanes
 // converged; returns the position where the path reaches a border.
-template <class Visit>
+template <int WG = 32, class Visit>
 __device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int n, int m, int lane,
                                           Visit&& visit) {
+  static_assert((WG & (WG - 1)) == 0 && WG <= 32, "window width: a power of two <= 32 groups");
+  constexpr int kW = win_words<WG>();
+  constexpr int kShift = WG == 32 ? 7 : WG == 16 ? 6 : WG == 8 ? 5 : WG == 4 ? 4 : WG == 2 ? 3 : 2;
   const int ngroups = (m + 3) >> 2;
   const int nbands = (n + kBandRows - 1) / kBandRows;
   int i = n, j = m;
   if (i == 0 || j == 0) return make_int2(i, j);
   int cur = 0, fl = 1, fu = 2;  // buffer roles: current, left prefetch, up prefetch
-  int cb = (i - 1) / kBandRows, cw = (j - 1) >> 7;
-  win_load(win + cur * kWinWords, dd, nbands, ngroups, cb, cw, lane);
-  win_load(win + fl * kWinWords, dd, nbands, ngroups, cb, cw - 1, lane);
-  win_load(win + fu * kWinWords, dd, nbands, ngroups, cb - 1, cw, lane);
+  int cb = (i - 1) / kBandRows, cw = (j - 1) >> kShift;
+  win_load<WG>(win + cur * kW, dd, nbands, ngroups, cb, cw, lane);
+  win_load<WG>(win + fl * kW, dd, nbands, ngroups, cb, cw - 1, lane);
+  win_load<WG>(win + fu * kW, dd, nbands, ngroups, cb - 1, cw, lane);
   asm volatile("cp.async.wait_group 2;" ::: "memory");
   __syncwarp();
   while (i > 0 && j > 0) {
     const int li = i - 1, lj = j - 1;
-    const int b = li / kBandRows, w = lj >> 7;
+    const int b = li / kBandRows, w = lj >> kShift;
     if (b != cb || w != cw) {
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncwarp();
@@ -852,7 +867,7 @@ __device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int
         nb = fu;
       } else {  // diagonal exit through the corner: fetch it now
         nb = fl;
-        win_load(win + nb * kWinWords, dd, nbands, ngroups, b, w, lane);
+        win_load<WG>(win + nb * kW, dd, nbands, ngroups, b, w, lane);
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
       }
@@ -863,13 +878,13 @@ __device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int
       fu = f2;
       cb = b;
       cw = w;
-      win_load(win + fl * kWinWords, dd, nbands, ngroups, cb, cw - 1, lane);
-      win_load(win + fu * kWinWords, dd, nbands, ngroups, cb - 1, cw, lane);
+      win_load<WG>(win + fl * kW, dd, nbands, ngroups, cb, cw - 1, lane);
+      win_load<WG>(win + fu * kW, dd, nbands, ngroups, cb - 1, cw, lane);
     }
     // the 4x4 block holding (li, lj): one code word, walked in registers
     // until the path leaves the block (the per-step dependency chain is
     // shift / mask / two compares; block lookups happen once per block)
-    const uint32_t word = win[cur * kWinWords + ((((lj >> 2) & 31) << 5) |
+    const uint32_t word = win[cur * kW + ((((lj >> 2) & (WG - 1)) << 5) |
                                                  ((li & (kBandRows - 1)) >> 2))];
     int r = li & 3, c = lj & 3;
     const int bi = li - r, bj = lj - c;
@@ -1074,7 +1089,7 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) tune_count_kernel(
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int d = blockIdx.x * kWalkWarps + wid;
   if (d >= n_docs) return;
-  uint32_t* win = walk_smem + wid * 3 * kWinWords;
+  uint32_t* win = walk_smem + wid * 3 * win_words<kTuneWG>();
   const int n = nn[d], m = mm[d];
   const double* Sd = S + s_off[d];
   const int64_t ld = pitch[d];
@@ -1111,7 +1126,7 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) tune_count_kernel(
       }
     }
   };
-  warp_walk(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
+  warp_walk<kTuneWG>(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
     if (op == BM_MOVE_D) {
       if (lane == (nd & 31)) {
         ci = i;
@@ -1138,10 +1153,11 @@ cudaError_t launch_tune_count(const uint32_t* dirs, const int64_t* dir_off, cons
                               unsigned long long* pred, unsigned long long* hit, cudaStream_t st) {
   if (n_docs == 0) return cudaSuccess;
   if (n_thr > kMaxThr) return cudaErrorInvalidValue;
+  constexpr int smem = walk_smem<kTuneWG>();
   cudaError_t e = cudaFuncSetAttribute(tune_count_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  tune_count_kernel<<<(n_docs + kWalkWarps - 1) / kWalkWarps, kWalkWarps * WARP, kWalkSmem, st>>>(
+  tune_count_kernel<<<(n_docs + kWalkWarps - 1) / kWalkWarps, kWalkWarps * WARP, smem, st>>>(
       dirs, dir_off, S, s_off, pitch, n, m, n_docs, thr, n_thr, gold, gold_off, pred, hit);
   return counted(cudaGetLastError());
 }
