@@ -540,6 +540,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // next block, shuffles and stores with the 7-cell dependency chain of the
 // current one. S for block g+1 is loaded and turned into 1-S during block g
 // (two register sets, ping-pong by a 2x unrolled loop).
+#ifndef BM_NW_EARLY_BND
+#define BM_NW_EARLY_BND 1
+#endif
 template <int D, int NP>
 __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
@@ -617,6 +620,9 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     // per penalty: C[i+1][4g] left of the block, the last row of the previous
     // block, and C[i0][4g] above-left of the block
     double l[NP][4], b[NP][4], dgn[NP];
+    uint64_t pre[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) pre[q] = kBndSentinel;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
 #pragma unroll
@@ -640,8 +646,9 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
             if (band == 0) {
               v = (double)(c + 1) * pq[q];
             } else {
-              uint64_t x;
-              while ((x = ld_relaxed_u64(bnd_up + q * a.bnd_stride + c)) == kBndSentinel) {
+              uint64_t x = pre[q];  // issued 4 super-steps ago (sentinel: not yet / none)
+              while (x == kBndSentinel &&
+                     (x = ld_relaxed_u64(bnd_up + q * a.bnd_stride + c)) == kBndSentinel) {
 #if !(defined(BM_NW_PROFILE) && defined(BM_NW_NOSLEEP))
                 __nanosleep(32);
 #endif
@@ -658,6 +665,16 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
                   g_nw_chunk[it][t >> 3][0] = w0;
                   g_nw_chunk[it][t >> 3][1] = gtimer();
                 })
+      }
+      if (BM_NW_EARLY_BND && NP < 4 && band > 0 && (t & 7) == 4) {
+        // the next chunk's boundary values, loaded half a chunk early so the
+        // L2 round trip overlaps four super-steps (the band above is normally
+        // 40+ super-steps ahead, so the values are already there). Not at
+        // NP = 4: the extra registers spill there (measured slower).
+        const int c = 4 * (t + 4) + lane;
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+          pre[q] = c < m ? ld_relaxed_u64(bnd_up + q * a.bnd_stride + c) : kBndSentinel;
       }
       NW_PROF(if (first && g == 0 && lane == 0 && it < 8192) { g_nw_prof[it][1] = gtimer(); first = false; })
       double u[NP][4];
