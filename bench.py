@@ -327,7 +327,7 @@ def run_ours(args):
     e2e_value = args.docs * world * args.steps / (float(e_tot.item()) / 1e3)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # CPU baseline: N=1 only
         rate, k, dt = cpu_port_rate(sc, model, args.cpu_seconds, host_cores(), args.docs)
         cpu = {"value": rate, "unit": UNIT, "cores": host_cores(), "kind": "port",
                "sample": f"{k} docs of the workload (100x100) in {dt:.1f}s, oracle/bimine_oracle.c "
