@@ -335,8 +335,22 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   if (j >= nt) return;
   const SentScalars b = get_scalars(*cols, j);
   const double pos_t = cols->pos[j];
-  for (int i = threadIdx.x / kTile; i < ns; i += kTileThreads / kTile) {
+#ifndef BM_SCORE_PREFETCH
+#define BM_SCORE_PREFETCH 1
+#endif
+  constexpr int kRowStep = kTileThreads / kTile;
+  int i = threadIdx.x / kTile;
+#if BM_SCORE_PREFETCH
+  // the next row's hit word is in flight while this cell is scored
+  uint32_t hv_next = i < ns ? __ldg(hd + (int64_t)i * m + j) : 0u;
+#endif
+  for (; i < ns; i += kRowStep) {
+#if BM_SCORE_PREFETCH
+    const uint32_t hv = hv_next;
+    if (i + kRowStep < ns) hv_next = __ldg(hd + (int64_t)(i + kRowStep) * m + j);
+#else
     const uint32_t hv = __ldg(hd + (int64_t)i * m + j);
+#endif
     const SentScalars a = get_scalars(*rows, i);
     dst[i * ld + j] =
         small ? bmexp::confidence_from_z(folded_margin(S, M, mt, a, b, (int)(hv & 0xffffu),
