@@ -277,9 +277,12 @@ __device__ __forceinline__ double folded_margin(const bm_sentences& S, const Mod
                                                 const ModelTables& mt, const SentScalars& a,
                                                 const SentScalars& b, int hf, int hr,
                                                 double pos_s, double pos_t) {
-  double z = __ldg(mt.z1 + a.T * kPairMax + b.T);
-  z = __dadd_rn(z, __ldg(mt.p1 + hf * kPairMax + a.nA));
-  z = __dadd_rn(z, __ldg(mt.p2 + hr * kPairMax + b.nA));
+  // unsigned 32-bit table indices (all counts are < kPairMax here): one
+  // IMAD.WIDE.U32 per address instead of a sign-extended 64-bit add chain
+  const uint32_t K = (uint32_t)kPairMax;
+  double z = __ldg(mt.z1 + ((uint32_t)a.T * K + (uint32_t)b.T));
+  z = __dadd_rn(z, __ldg(mt.p1 + ((uint32_t)hf * K + (uint32_t)a.nA)));
+  z = __dadd_rn(z, __ldg(mt.p2 + ((uint32_t)hr * K + (uint32_t)b.nA)));
   double p3;
   if ((a.nD | b.nD) == 0) {
     p3 = M.w[3];  // w3 * 1.0
@@ -290,7 +293,7 @@ __device__ __forceinline__ double folded_margin(const bm_sentences& S, const Mod
     p3 = __dmul_rn(M.w[3], frac_or_zero(inter, a.nD + b.nD - inter));
   }
   z = __dadd_rn(z, p3);
-  z = __dadd_rn(z, __ldg(mt.p4 + a.P * kPairMax + b.P));
+  z = __dadd_rn(z, __ldg(mt.p4 + ((uint32_t)a.P * K + (uint32_t)b.P)));
   z = __dadd_rn(z, __dmul_rn(M.w[5], __dsub_rn(1.0, fabs(__dsub_rn(pos_s, pos_t)))));
   return __dadd_rn(z, M.w[6]);  // w6 * 1.0
 }
@@ -335,29 +338,23 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   if (j >= nt) return;
   const SentScalars b = get_scalars(*cols, j);
   const double pos_t = cols->pos[j];
-#ifndef BM_SCORE_PREFETCH
-#define BM_SCORE_PREFETCH 1
-#endif
   constexpr int kRowStep = kTileThreads / kTile;
   int i = threadIdx.x / kTile;
-#if BM_SCORE_PREFETCH
-  // the next row's hit word is in flight while this cell is scored
-  uint32_t hv_next = i < ns ? __ldg(hd + (int64_t)i * m + j) : 0u;
-#endif
-  for (; i < ns; i += kRowStep) {
-#if BM_SCORE_PREFETCH
+  // running row pointers (one 64-bit add per cell); the next row's hit word is
+  // in flight while this cell is scored
+  const uint32_t* hp = hd + (int64_t)i * m + j;
+  double* op = dst + (int64_t)i * ld + j;
+  const int64_t hstep = (int64_t)kRowStep * m, ostep = (int64_t)kRowStep * ld;
+  uint32_t hv_next = i < ns ? __ldg(hp) : 0u;
+  for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
     const uint32_t hv = hv_next;
-    if (i + kRowStep < ns) hv_next = __ldg(hd + (int64_t)(i + kRowStep) * m + j);
-#else
-    const uint32_t hv = __ldg(hd + (int64_t)i * m + j);
-#endif
+    if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
     const SentScalars a = get_scalars(*rows, i);
-    dst[i * ld + j] =
-        small ? bmexp::confidence_from_z(folded_margin(S, M, mt, a, b, (int)(hv & 0xffffu),
-                                                       (int)(hv >> 16), rows->pos[i], pos_t),
-                                         exp_tab)
-              : cell_score(S, M, exp_tab, a, b, (int)(hv & 0xffffu), (int)(hv >> 16),
-                           rows->pos[i], pos_t);
+    *op = small ? bmexp::confidence_from_z(folded_margin(S, M, mt, a, b, (int)(hv & 0xffffu),
+                                                         (int)(hv >> 16), rows->pos[i], pos_t),
+                                           exp_tab)
+                : cell_score(S, M, exp_tab, a, b, (int)(hv & 0xffffu), (int)(hv >> 16),
+                             rows->pos[i], pos_t);
   }
 }
 
