@@ -149,18 +149,24 @@ constexpr uint64_t kBndSentinel = 0xdedededededededeull;
 // ---------------------------------------------------------------------------
 // K1: one CTA per 64x64 tile of one document's similarity matrix.
 // ---------------------------------------------------------------------------
+// one staged sentence (32 B): the cell loop reads it with two 16-byte loads
+struct __align__(16) TileSent {
+  int T, P, nA, nD;
+  int d0, pad;
+  double pos;
+};
 struct TileScalars {
-  int T[kTile], P[kTile], nA[kTile], nD[kTile], d0[kTile];
-  double pos[kTile];
+  TileSent s[kTile];
 };
 
 __device__ __forceinline__ SentScalars get_scalars(const TileScalars& t, int k) {
+  const int4 v = *reinterpret_cast<const int4*>(&t.s[k]);
   SentScalars r;
-  r.T = t.T[k];
-  r.P = t.P[k];
-  r.nA = t.nA[k];
-  r.nD = t.nD[k];
-  r.d0 = t.d0[k];
+  r.T = v.x;
+  r.P = v.y;
+  r.nA = v.z;
+  r.nD = v.w;
+  r.d0 = t.s[k].d0;
   return r;
 }
 
@@ -190,12 +196,12 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
     const int local = is_row ? k : k - ns;
     SentScalars sc = load_scalars(S, is_row ? s0 + local : t0 + local);
     TileScalars* dst = is_row ? rows : cols;
-    dst->T[local] = sc.T;
-    dst->P[local] = sc.P;
-    dst->nA[local] = sc.nA;
-    dst->nD[local] = sc.nD;
-    dst->d0[local] = sc.d0;
-    dst->pos[local] = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
+    dst->s[local].T = sc.T;
+    dst->s[local].P = sc.P;
+    dst->s[local].nA = sc.nA;
+    dst->s[local].nD = sc.nD;
+    dst->s[local].d0 = sc.d0;
+    dst->s[local].pos = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
   }
   for (int q = threadIdx.x; q <= ns + nt + 1; q += blockDim.x) {
     if (q <= ns)
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
     int hf, hr;
     read_hits<false>(hits, c, hf, hr);
     dst[i * ld + j] = cell_score(S, M, exp_tab, get_scalars(*rows, i), get_scalars(*cols, j), hf,
-                                 hr, rows->pos[i], cols->pos[j]);
+                                 hr, rows->s[i].pos, cols->s[j].pos);
   }
 }
 
@@ -320,12 +326,12 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     SentScalars sc = load_scalars(S, is_row ? s0 + local : t0 + local);
     fits &= sc.T < kPairMax;
     TileScalars* dst = is_row ? rows : cols;
-    dst->T[local] = sc.T;
-    dst->P[local] = sc.P;
-    dst->nA[local] = sc.nA;
-    dst->nD[local] = sc.nD;
-    dst->d0[local] = sc.d0;
-    dst->pos[local] = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
+    dst->s[local].T = sc.T;
+    dst->s[local].P = sc.P;
+    dst->s[local].nA = sc.nA;
+    dst->s[local].nD = sc.nD;
+    dst->s[local].d0 = sc.d0;
+    dst->s[local].pos = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
   }
   // the folded tables cover the tile when all of its sentences fit them
   const bool small = __syncthreads_and(fits) != 0;
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   const int j = threadIdx.x % kTile;
   if (j >= nt) return;
   const SentScalars b = get_scalars(*cols, j);
-  const double pos_t = cols->pos[j];
+  const double pos_t = cols->s[j].pos;
   constexpr int kRowStep = kTileThreads / kTile;
   int i = threadIdx.x / kTile;
   // running row pointers (one 64-bit add per cell); the next row's hit word is
@@ -351,10 +357,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
     const SentScalars a = get_scalars(*rows, i);
     *op = small ? bmexp::confidence_from_z(folded_margin(S, M, mt, a, b, (int)(hv & 0xffffu),
-                                                         (int)(hv >> 16), rows->pos[i], pos_t),
+                                                         (int)(hv >> 16), rows->s[i].pos, pos_t),
                                            exp_tab)
                 : cell_score(S, M, exp_tab, a, b, (int)(hv & 0xffffu), (int)(hv >> 16),
-                             rows->pos[i], pos_t);
+                             rows->s[i].pos, pos_t);
   }
 }
 
