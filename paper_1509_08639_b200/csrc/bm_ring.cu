@@ -204,6 +204,16 @@ struct __align__(16) SPack {
   double pos;
 };
 
+// One staged sentence as a single 16-byte shared-memory load.
+__device__ __forceinline__ SPack ld_spack(const SPack* p) {
+  const int4 v = *reinterpret_cast<const int4*>(p);
+  SPack q;
+  q.tpad = (uint32_t)v.x;
+  q.d0 = v.y;
+  q.pos = __hiloint2double(v.w, v.z);
+  return q;
+}
+
 // Features of one cell from staged sentences (same values, operation by
 // operation, as bm_device.cuh cell_features / margin / confidence_from_z).
 // BM_RING_FOLD=1: the margin from the model's folded tables (ModelTables):
@@ -476,7 +486,9 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
             slot[kt * (BPT * RL)] = __dsub_rn(1.0, (double)(hv & 0xff) * 0.01 + sp[i].pos);
 #else
             slot[kt * (BPT * RL)] = bmexp::one_minus_confidence(
-                staged_margin(S, a.M, a.tabs, a.mt, sp[i], sp[n + j], hv & 0xff, hv >> 8), exp_tab);
+                staged_margin(S, a.M, a.tabs, a.mt, ld_spack(sp + i), ld_spack(sp + n + j), hv & 0xff,
+                              hv >> 8),
+                exp_tab);
 #endif
           }
         }
@@ -538,7 +550,8 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
         ci = cell >> 16;
         cj = cell & 0xffff;
         const uint32_t hv = hits16[ci * m + cj];
-        sv = staged_score(S, a.M, exp_tab, a.tabs, a.mt, sp[ci], sp[n + cj], hv & 0xff, hv >> 8);
+        sv = staged_score(S, a.M, exp_tab, a.tabs, a.mt, ld_spack(sp + ci), ld_spack(sp + n + cj),
+                          hv & 0xff, hv >> 8);
         keep = sv >= a.threshold;
       }
       const unsigned mask = __ballot_sync(kFull, keep);
