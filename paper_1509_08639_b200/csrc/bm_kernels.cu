@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
 // ---------------------------------------------------------------------------
 constexpr int kJoinSentChunk = 128;
 
-__global__ void __launch_bounds__(64, 8) hits_doc_kernel(bm_sentences S, bm_docs D, bm_lexicon L,
+#ifndef BM_HITS_DOC_MINB
+#define BM_HITS_DOC_MINB 12
+#endif
+__global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sentences S, bm_docs D, bm_lexicon L,
                                                          const int4* __restrict__ items,
                                                          int n_items,
                                                          const int64_t* __restrict__ h_off,
