@@ -69,7 +69,7 @@ typedef struct bm_sentences {
   const int32_t* n_alpha;
   const int32_t* tok_off;    /* [n_sent + 1] */
   const int32_t* tok_id;     /* [tok_off[n_sent]] */
-  const uint16_t* tok_alpha; /* [tok_off[n_sent]] */
+  const uint32_t* tok_alpha; /* [tok_off[n_sent]] */
   const int32_t* dig_off;    /* [n_sent + 1] */
   const int32_t* dig_id;     /* [dig_off[n_sent]] */
 } bm_sentences;
@@ -294,7 +294,7 @@ typedef struct {
   int32_t n_sent, n_docs, n_ids, n_skipped;
   int64_t n_tok_entries, n_dig_entries;
   const int32_t *n_tok, *n_punct, *n_alpha, *tok_off, *tok_id;
-  const uint16_t* tok_alpha;
+  const uint32_t* tok_alpha;
   const int32_t *dig_off, *dig_id;
   const int32_t *src0, *n, *tgt0, *m;
 } bm_ingest_arrays;

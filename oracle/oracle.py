@@ -87,7 +87,7 @@ class HostBatch:
         c = corpus
         self.keep = [
             _a(c.n_tok, np.int32), _a(c.n_punct, np.int32), _a(c.n_alpha, np.int32),
-            _a(c.tok_off, np.int32), _a(c.tok_id, np.int32), _a(c.tok_alpha, np.uint16),
+            _a(c.tok_off, np.int32), _a(c.tok_id, np.int32), _a(c.tok_alpha, np.uint32),
             _a(c.dig_off, np.int32), _a(c.dig_id, np.int32),
         ]
         self.sent = _Sent(c.n_sent, *[k.ctypes.data for k in self.keep])

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libbimine_b200.so")
-SOURCES = ["bm_lib.cu", "bm_ingest.cpp"]
+SOURCES = ["bm_lib.cu", "bm_ingest.cpp", "bm_synth.cpp"]
 HEADERS = ["bm_kernels.cu", "bm_ring.cu", "bm_api.cu", "bm_device.cuh", "bm_kernels.cuh", "glibc_exp.cuh", "glibc_exp_table.h"]
 
 NVCC_FLAGS = [
@@ -26,7 +26,7 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps.append(os.path.join(INCLUDE, "bimine_b200.h"))
+    deps += [os.path.join(INCLUDE, h) for h in ("bimine_b200.h", "bimine_synth.h")]
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 

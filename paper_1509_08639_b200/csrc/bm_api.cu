@@ -523,8 +523,6 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   for (int d = 0; d < nd; ++d) {
     const int n = n_host[d], m = m_host[d];
     if (n <= 0 || m <= 0) continue;
-    // hit counts are 16-bit fields: a sentence may hold at most 65535 tokens
-    if (amax_host[d] > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
     const int R = fused_rows_per_lane(n);
     const size_t sl = ring_slice_bytes(n, m, R);
     if (!force_banded && n <= kFusedMaxRows && sl <= fused_max_smem() && amax_host[d] <= 255) {
@@ -586,13 +584,15 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     cudaEventCreate(&tl_fused);
     cudaEventRecord(tl_fused, st);
   }
-  GeneralPlan g;
-  for (int32_t d : banded) g.add(d, n_host[d], m_host[d]);
-  if (!g.docs.empty()) {
-    bool doc_join = true;
-    for (int32_t d : g.docs) doc_join &= amax_host[d] <= 65535;
-    int rc = mine_general(g, sent, docs, lex, M, threshold, penalty, rec_off, rec, rec_count, cost,
-                          doc_join, sc, st);
+  // banded tier: the document-level join keeps 16-bit hit counts (every
+  // sentence <= 65535 tokens); longer sentences take the per-tile scoring
+  // kernel with 32-bit counts
+  GeneralPlan g, gw;
+  for (int32_t d : banded) (amax_host[d] <= 65535 ? g : gw).add(d, n_host[d], m_host[d]);
+  for (GeneralPlan* gp : {&g, &gw}) {
+    if (gp->docs.empty()) continue;
+    int rc = mine_general(*gp, sent, docs, lex, M, threshold, penalty, rec_off, rec, rec_count,
+                          cost, gp == &g, sc, st);
     if (rc) return rc;
     tr.mark("banded tier enqueued");
   }
@@ -706,8 +706,6 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     rt += std::max(0, std::min(dh->n[d], dh->m[d]));
   }
   if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
-  for (int d = 0; d < nd; ++d)
-    if (amax[d] > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
   tr.mark("host prep");
   Scratch sc(st);
   // declared after the scratch, so destroyed before it: an early return never
@@ -716,10 +714,43 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     cudaStream_t s;
     ~CopyFence() { cudaStreamSynchronize(s); }
   } fence{cs};
+  // Every exit path (early error returns included) joins the side mining
+  // streams back into st before ~Scratch frees on st: their queued kernels
+  // still read and write the scratch. Declared after the scratch, so it runs
+  // first; the events it and the chunk loop create are released on exit.
+  struct StreamJoin {
+    cudaStream_t st;
+    std::vector<cudaStream_t> side;
+    std::vector<cudaEvent_t> events;
+    cudaEvent_t event() {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+      events.push_back(e);
+      return e;
+    }
+    cudaError_t join() {
+      cudaError_t err = cudaSuccess;
+      for (cudaStream_t s : side) {
+        cudaEvent_t e = event();
+        cudaError_t r = e ? cudaEventRecord(e, s) : cudaErrorMemoryAllocation;
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(st, e, 0);
+        if (r != cudaSuccess) {
+          cudaStreamSynchronize(s);  // cannot order it: wait for it instead
+          if (err == cudaSuccess) err = r;
+        }
+      }
+      side.clear();
+      return err;
+    }
+    ~StreamJoin() {
+      join();
+      for (cudaEvent_t e : events) cudaEventDestroy(e);
+    }
+  } joiner{st, {}, {}};
   bm_sentences sd;
   sd.n_sent = ns;
   int32_t *a0, *a1, *a2, *a3, *a4, *a5, *a6;
-  uint16_t* a7;
+  uint32_t* a7;
   BM_CK(sc.alloc(&a0, ns), "alloc");
   BM_CK(sc.alloc(&a1, ns), "alloc");
   BM_CK(sc.alloc(&a2, ns), "alloc");
@@ -797,8 +828,8 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   int64_t* hcnt = pinned_counts((size_t)nd + 1);
   if (hcnt == nullptr) return fail(BM_ENOMEM, "pinned count buffer");
   // the copy stream may only touch the scratch once it is allocated on st
-  cudaEvent_t ready;
-  BM_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+  cudaEvent_t ready = joiner.event();
+  if (ready == nullptr) return fail(BM_ECUDA, "event create failed");
   BM_CK(cudaEventRecord(ready, st), "event");
   BM_CK(cudaStreamWaitEvent(cs, ready, 0), "event");
   auto h2d = [&](void* dst, const void* from, size_t bytes) -> cudaError_t {
@@ -823,7 +854,6 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   // per chunk: docs [d0, d1), compacted into dense + roff[d0], count -> ctot[k]
   std::vector<int> ch_d0, ch_d1;
   std::vector<cudaEvent_t> ch_ev;
-  std::vector<cudaEvent_t> evs;
   // BM_TRACE: GPU timeline (copy done / mined per chunk, relative to t_start)
   std::vector<cudaEvent_t> tl_copy, tl_mine;
   cudaEvent_t tl0 = nullptr;
@@ -882,7 +912,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
           BM_CK(h2d(a1 + lo, sh->n_punct + lo, cntS * 4), "h2d");
           BM_CK(h2d(a2 + lo, sh->n_alpha + lo, cntS * 4), "h2d");
           BM_CK(h2d(a4 + e0, sh->tok_id + e0, (size_t)(e1 - e0) * 4), "h2d");
-          BM_CK(h2d(a7 + e0, sh->tok_alpha + e0, (size_t)(e1 - e0) * 2), "h2d");
+          BM_CK(h2d(a7 + e0, sh->tok_alpha + e0, (size_t)(e1 - e0) * 4), "h2d");
           BM_CK(h2d(a6 + g0, sh->dig_id + g0, (size_t)(g1 - g0) * 4), "h2d");
         } else if (src.wire) {
           const bm_wire* w = src.wire;
@@ -894,10 +924,9 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
           BM_CK(h2d(w_dg + g0, w->dig_id + g0, (size_t)(g1 - g0) * 2), "h2d");
         }
       }
-      cudaEvent_t ev;
-      BM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      cudaEvent_t ev = joiner.event();
+      if (ev == nullptr) return fail(BM_ECUDA, "event create failed");
       BM_CK(cudaEventRecord(ev, cs), "event");
-      evs.push_back(ev);
       if (tr.on) {
         cudaEvent_t e;
         cudaEventCreate(&e);
@@ -968,8 +997,8 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   BM_CK(model_tables(M, &mtab), "model tables");
   tr.mark("list uploads + memsets");
   // the mining streams start after the list uploads and memsets on st
-  cudaEvent_t planned;
-  BM_CK(cudaEventCreateWithFlags(&planned, cudaEventDisableTiming), "event");
+  cudaEvent_t planned = joiner.event();
+  if (planned == nullptr) return fail(BM_ECUDA, "event create failed");
   BM_CK(cudaEventRecord(planned, st), "event");
   static const int n_ms = std::max(1, std::min(kMaxMineStreams,
       getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 4));
@@ -977,6 +1006,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   for (int q = 1; q < n_ms; ++q) {
     ms.push_back(side_stream(q));
     BM_CK(cudaStreamWaitEvent(ms.back(), planned, 0), "event");
+    joiner.side.push_back(ms.back());
   }
   // pass 2: per chunk, widen + mine + compact on a mining stream; chunk 0's
   // kernels are enqueued before the remaining copies so the GPU starts early
@@ -1025,15 +1055,16 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
       BM_CK(launch_ring(a, 1 << q, fsm[q], sk), "mine_ring_kernel");
     }
     {
-      GeneralPlan gp;
+      // 16-bit document-level join, or 32-bit per-tile counts for sentences
+      // longer than 65535 tokens
+      GeneralPlan gp, gw;
       for (int d = d0; d < d1; ++d)
-        if (banded[d]) gp.add(d, dh->n[d], dh->m[d]);
-      if (!gp.docs.empty()) {
+        if (banded[d]) (amax[d] <= 65535 ? gp : gw).add(d, dh->n[d], dh->m[d]);
+      for (GeneralPlan* g : {&gp, &gw}) {
+        if (g->docs.empty()) continue;
         Scratch scg(sk);
-        bool doc_join = true;
-        for (int32_t d : gp.docs) doc_join &= amax[d] <= 65535;
-        int rc = mine_general(gp, &sd, &dd, &ld, M, threshold, penalty, droff, rec, cnt, cost,
-                              doc_join, scg, sk);
+        int rc = mine_general(*g, &sd, &dd, &ld, M, threshold, penalty, droff, rec, cnt, cost,
+                              g == &gp, scg, sk);
         if (rc) return rc;
       }
     }
@@ -1047,8 +1078,8 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
             "compact");
       BM_CK(cudaMemcpyAsync(hcnt + kq, ctot + kq, sizeof(int64_t), cudaMemcpyDeviceToHost, sk),
             "d2h");
-      cudaEvent_t ce;
-      BM_CK(cudaEventCreateWithFlags(&ce, cudaEventDisableTiming), "event");
+      cudaEvent_t ce = joiner.event();
+      if (ce == nullptr) return fail(BM_ECUDA, "event create failed");
       BM_CK(cudaEventRecord(ce, sk), "event");
       ch_d0.push_back(d0);
       ch_d1.push_back(d1);
@@ -1068,13 +1099,7 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   for (size_t kc = 1; kc < chunks.size(); ++kc)
     if (int rc = enqueue_kernels(kc)) return rc;
   // join the side streams back into the caller's stream
-  for (size_t q = 1; q < ms.size(); ++q) {
-    cudaEvent_t joined;
-    BM_CK(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming), "event");
-    BM_CK(cudaEventRecord(joined, ms[q]), "event");
-    BM_CK(cudaStreamWaitEvent(st, joined, 0), "event");
-    evs.push_back(joined);
-  }
+  BM_CK(joiner.join(), "stream join");
   tr.mark("chunks enqueued");
   int64_t tot = 0;
   for (size_t q = 0; q < ch_ev.size(); ++q) {
@@ -1088,7 +1113,6 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
                                  cudaMemcpyDeviceToHost, cs),
                  "d2h");
     tot += c;
-    cudaEventDestroy(ch_ev[q]);
   }
   tr.mark("mined + compacted");
   if (cost_out) BM_CK(cudaMemcpyAsync(cost_out, cost, nd * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
@@ -1106,9 +1130,6 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     }
     cudaEventDestroy(tl0);
   }
-  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
-  cudaEventDestroy(ready);
-  cudaEventDestroy(planned);
   *n_rec = tot;
   return BM_OK;
 }
@@ -1149,7 +1170,6 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   for (int k = 0; k < n_pen; ++k)
     if (!check_penalty(penalties_host[k])) return fail(BM_EINVAL, "penalty must be >= 0");
   if (n_thr > 64) return fail(BM_EINVAL, "at most 64 thresholds per call");
-  if (token_bound > 65535) return fail(BM_ELIMIT, "a sentence has more than 65535 tokens");
   GeneralPlan g;
   for (int d = 0; d < docs->n_docs; ++d) g.add(d, n_host[d], m_host[d]);
   Scratch sc(st);

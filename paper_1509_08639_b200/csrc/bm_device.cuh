@@ -460,7 +460,7 @@ __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& 
                                   const int32_t* offT, uint32_t* hits, JoinSmem& js,
                                   uint16_t* chunk_owner, uint16_t* a_owner, bool zero_hits = true) {
   const int ncell = ns * nt;
-  const int nwords = kPacked16 ? (ncell + 1) / 2 : ncell;
+  const int nwords = kPacked16 ? (ncell + 1) / 2 : 2 * ncell;
   if (zero_hits) {
     for (int k = g.rank(); k < nwords; k += g.size()) hits[k] = 0u;
     g.sync();
@@ -479,18 +479,19 @@ __device__ void tile_join_entries(G g, const bm_sentences& S, const bm_lexicon& 
                            if (kPacked16)
                              atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16 + 8));
                            else
-                             atomicAdd(&hits[cell], (uint32_t)w << 16);
+                             atomicAdd(&hits[ncell + cell], (uint32_t)w);
                          });
 }
 
 // Full join for a tile. Hits are packed per cell into `hits` words:
 //   kPacked16: 16-bit cells, hf in bits 0-7, hr in bits 8-15 (counts <= 255)
-//   otherwise: 32-bit cells, hf in bits 0-15, hr in bits 16-31
+//   otherwise: full 32-bit counts, hf in hits[cell], hr in hits[ns*nt + cell]
+//              (any sentence length: counts are bounded by |A| < 2^31)
 template <bool kPacked16, class G>
 __device__ void tile_join(G g, const bm_sentences& S, const bm_lexicon& L, int s0, int ns,
                           int t0, int nt, uint32_t* hits, JoinSmem& js) {
   const int ncell = ns * nt;
-  const int nwords = kPacked16 ? (ncell + 1) / 2 : ncell;
+  const int nwords = kPacked16 ? (ncell + 1) / 2 : 2 * ncell;
   for (int k = g.rank(); k < nwords; k += g.size()) hits[k] = 0u;
   g.sync();
   // forward: source alpha entries through FWD into target U sets
@@ -507,20 +508,20 @@ __device__ void tile_join(G g, const bm_sentences& S, const bm_lexicon& L, int s
     if (kPacked16)
       atomicAdd(&hits[cell >> 1], (uint32_t)w << ((cell & 1) * 16 + 8));
     else
-      atomicAdd(&hits[cell], (uint32_t)w << 16);
+      atomicAdd(&hits[ncell + cell], (uint32_t)w);
   });
 }
 
 template <bool kPacked16>
-__device__ __forceinline__ void read_hits(const uint32_t* hits, int cell, int& hf, int& hr) {
+__device__ __forceinline__ void read_hits(const uint32_t* hits, int cell, int ncell, int& hf,
+                                          int& hr) {
   if (kPacked16) {
     uint32_t v = hits[cell >> 1] >> ((cell & 1) * 16);
     hf = v & 0xff;
     hr = (v >> 8) & 0xff;
   } else {
-    uint32_t v = hits[cell];
-    hf = v & 0xffff;
-    hr = v >> 16;
+    hf = (int)hits[cell];
+    hr = (int)hits[ncell + cell];
   }
 }
 

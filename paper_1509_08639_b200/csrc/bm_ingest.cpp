@@ -281,7 +281,7 @@ using pvec = std::vector<T, NoInit<T>>;
 struct Ingest {
   // packed sentences (pack.py layout)
   pvec<int32_t> n_tok, n_punct, n_alpha, tok_off{0}, tok_id, dig_off{0}, dig_id;
-  pvec<uint16_t> tok_alpha;
+  pvec<uint32_t> tok_alpha;
   pvec<int32_t> src0, n, tgt0, m;
   // interned token strings (normalized tokens and raw digit tokens) -> id
   StrTable ids;
@@ -416,12 +416,8 @@ bool add_sentence(Ingest& g, const char* s, size_t len) {
   std::sort(alpha.begin(), alpha.end());
   std::sort(digits.begin(), digits.end());
   for (auto& pr : alpha) {
-    if (pr.second > 65535) {
-      g.err = "a sentence repeats one token more than 65535 times";
-      return false;
-    }
     g.tok_id.push_back(pr.first);
-    g.tok_alpha.push_back((uint16_t)pr.second);
+    g.tok_alpha.push_back((uint32_t)pr.second);
   }
   g.n_tok.push_back(T);
   g.n_punct.push_back(P);
@@ -915,7 +911,7 @@ void merge_parts(std::vector<Ingest*>& part) {
       G.sent_ptr[s0 + s] = text + L.raw_off[s];
       G.sent_len[s0 + s] = (int32_t)(L.raw_off[s + 1] - L.raw_off[s]);
     }
-    std::vector<std::pair<int32_t, uint16_t>> ta;
+    std::vector<std::pair<int32_t, uint32_t>> ta;
     for (size_t s = 0; s < ns; ++s) {
       const int32_t a = L.tok_off[s], b = L.tok_off[s + 1];
       ta.clear();

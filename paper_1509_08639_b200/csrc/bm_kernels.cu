@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* exp_tab = (uint64_t*)smem;
   uint32_t* hits = (uint32_t*)(smem + kExpTableWords * 8);
-  TileScalars* rows = (TileScalars*)(smem + kExpTableWords * 8 + kTile * kTile * 4);
+  // 32-bit hf and hr per cell: this tier takes any sentence length
+  TileScalars* rows = (TileScalars*)(smem + kExpTableWords * 8 + kTile * kTile * 8);
   TileScalars* cols = rows + 1;
   JoinSmem js = carve_join((uint8_t*)(cols + 1));
   int32_t* offS = (int32_t*)((uint8_t*)(cols + 1) + align16(join_smem_bytes()));
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
   for (int c = threadIdx.x; c < ns * nt; c += blockDim.x) {
     const int i = c / nt, j = c - (c / nt) * nt;
     int hf, hr;
-    read_hits<false>(hits, c, hf, hr);
+    read_hits<false>(hits, c, ns * nt, hf, hr);
     dst[i * ld + j] = cell_score(S, M, exp_tab, get_scalars(*rows, i), get_scalars(*cols, j), hf,
                                  hr, rows->s[i].pos, cols->s[j].pos);
   }
@@ -400,7 +401,7 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
 }
 
 size_t score_smem_bytes() {
-  return kExpTableWords * 8 + kTile * kTile * 4 + 2 * sizeof(TileScalars) +
+  return kExpTableWords * 8 + kTile * kTile * 8 + 2 * sizeof(TileScalars) +
          align16(join_smem_bytes()) + (size_t)(2 * kTile + 2) * 4 + (size_t)kJoinEmax * 4;
 }
 
@@ -428,12 +429,12 @@ __global__ void features_kernel(bm_sentences S, bm_lexicon L, const int32_t* q_s
   extern __shared__ __align__(16) uint8_t smem[];
   const int q = blockIdx.x;
   JoinSmem js = carve_join(smem);
-  uint32_t* hit = (uint32_t*)(smem + join_smem_bytes());
+  uint32_t* hit = (uint32_t*)(smem + join_smem_bytes());  // hf, hr
   const int s = q_src[q], t = q_tgt[q];
   tile_join<false>(WarpGroup(), S, L, s, 1, t, 1, hit, js);
   if (threadIdx.x == 0) {
     int hf, hr;
-    read_hits<false>(hit, 0, hf, hr);
+    read_hits<false>(hit, 0, 1, hf, hr);
     double f[7];
     cell_features(S, load_scalars(S, s), load_scalars(S, t), hf, hr, q_ps[q], q_pt[q], f);
     for (int k = 0; k < 7; ++k) feats[(int64_t)q * 7 + k] = f[k];
@@ -1303,7 +1304,7 @@ __global__ void unpack_wire_kernel(const uint8_t* __restrict__ t8, const uint8_t
                                    const uint8_t* __restrict__ al8, const uint16_t* __restrict__ dg16,
                                    int lo, int hi, int64_t e0, int64_t e1, int64_t g0, int64_t g1,
                                    int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha,
-                                   int32_t* tok_id, uint16_t* tok_alpha, int32_t* dig_id) {
+                                   int32_t* tok_id, uint32_t* tok_alpha, int32_t* dig_id) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int64_t s = lo + t; s < hi; s += stride) {
@@ -1322,7 +1323,7 @@ cudaError_t launch_unpack_wire(const uint8_t* t8, const uint8_t* p8, const uint8
                                const uint16_t* id16, const uint8_t* al8, const uint16_t* dg16,
                                int lo, int hi, int64_t e0, int64_t e1, int64_t g0, int64_t g1,
                                int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha, int32_t* tok_id,
-                               uint16_t* tok_alpha, int32_t* dig_id, cudaStream_t st) {
+                               uint32_t* tok_alpha, int32_t* dig_id, cudaStream_t st) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unpack_wire_kernel<<<sms * 8, 256, 0, st>>>(t8, p8, a8, id16, al8, dg16, lo, hi, e0, e1, g0, g1,
@@ -1340,7 +1341,7 @@ __global__ void unpack_packed_kernel(const uint32_t* __restrict__ cnt,
                                      const uint16_t* __restrict__ pk,
                                      const uint16_t* __restrict__ dg, int lo, int hi,
                                      int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha,
-                                     int32_t* tok_off, int32_t* tok_id, uint16_t* tok_alpha,
+                                     int32_t* tok_off, int32_t* tok_id, uint32_t* tok_alpha,
                                      int32_t* dig_off, int32_t* dig_id) {
   const int lane = threadIdx.x & 31;
   const int nwarps = (int)(gridDim.x * blockDim.x) >> 5;
@@ -1371,7 +1372,7 @@ __global__ void unpack_packed_kernel(const uint32_t* __restrict__ cnt,
       for (int q = 0; q < u; ++q) {
         const uint32_t v = pk[tb + q];
         tok_id[tb + q] = (int32_t)(v >> 2);
-        tok_alpha[tb + q] = (uint16_t)(v & 3u);
+        tok_alpha[tb + q] = v & 3u;
         na += (int)(v & 3u);
       }
       n_alpha[s] = na;
@@ -1383,7 +1384,7 @@ __global__ void unpack_packed_kernel(const uint32_t* __restrict__ cnt,
 cudaError_t launch_unpack_packed(const uint32_t* cnt, const int32_t* o32, const int32_t* d32,
                                  const uint16_t* pk, const uint16_t* dg, int lo, int hi,
                                  int32_t* n_tok, int32_t* n_punct, int32_t* n_alpha,
-                                 int32_t* tok_off, int32_t* tok_id, uint16_t* tok_alpha,
+                                 int32_t* tok_off, int32_t* tok_id, uint32_t* tok_alpha,
                                  int32_t* dig_off, int32_t* dig_id, cudaStream_t st) {
   if (hi <= lo) return cudaSuccess;
   const int blocks = (hi >> 5) - (lo >> 5) + 1;  // 32-sentence blocks = warps

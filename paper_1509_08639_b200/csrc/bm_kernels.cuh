@@ -146,11 +146,11 @@ PairTables pair_tables();
 cudaError_t model_tables(const Model& M, ModelTables* out);
 cudaError_t launch_unpack_wire(const uint8_t*, const uint8_t*, const uint8_t*, const uint16_t*,
                                const uint8_t*, const uint16_t*, int, int, int64_t, int64_t, int64_t,
-                               int64_t, int32_t*, int32_t*, int32_t*, int32_t*, uint16_t*, int32_t*,
+                               int64_t, int32_t*, int32_t*, int32_t*, int32_t*, uint32_t*, int32_t*,
                                cudaStream_t);
 cudaError_t launch_unpack_packed(const uint32_t*, const int32_t*, const int32_t*, const uint16_t*,
                                  const uint16_t*, int, int, int32_t*, int32_t*, int32_t*, int32_t*,
-                                 int32_t*, uint16_t*, int32_t*, int32_t*, cudaStream_t);
+                                 int32_t*, uint32_t*, int32_t*, int32_t*, cudaStream_t);
 size_t ring_slice_bytes(int n, int m, int R);
 size_t hits_kernel_smem(int n, int m);
 cudaError_t launch_hits(const FusedArgs& a, size_t smem, cudaStream_t st);

@@ -584,17 +584,23 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
 // Raise a kernel's dynamic shared memory limit (and prefer the shared-memory
 // carveout) once per size: the attribute calls cost microseconds of host time
 // per launch, and the host entry launches per chunk.
-static cudaError_t smem_attr(const void* fn, size_t smem) {
+// The attribute belongs to the current device's context, so the cache is keyed
+// by (device, function).
+cudaError_t smem_attr(const void* fn, size_t smem) {
   static std::mutex mu;
-  static std::unordered_map<const void*, size_t> set;
+  static std::unordered_map<const void*, size_t> set[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> lk(mu);
-  auto it = set.find(fn);
-  if (it != set.end() && it->second >= smem) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto it = set[dev].find(fn);
+  if (it != set[dev].end() && it->second >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  set[fn] = smem;
+  set[dev][fn] = smem;
   return cudaSuccess;
 }
 

@@ -58,8 +58,10 @@ def to_host(t) -> np.ndarray:
 def to_dev(a: np.ndarray, dev):
     torch = torch_mod()
     a = np.ascontiguousarray(a)
-    if a.dtype == np.uint16:  # torch has uint16 storage; move the raw bytes
+    if a.dtype == np.uint16:  # move unsigned arrays as raw bytes of the signed type
         t = torch.from_numpy(a.view(np.int16))
+    elif a.dtype == np.uint32:
+        t = torch.from_numpy(a.view(np.int32))
     else:
         t = torch.from_numpy(a)
     return t.to(dev, non_blocking=False)

@@ -38,7 +38,7 @@ LAST_TIMINGS: dict[str, float] = {}
 
 _SENT_FIELDS = (("n_tok", np.int32, "n_sent"), ("n_punct", np.int32, "n_sent"),
                 ("n_alpha", np.int32, "n_sent"), ("tok_off", np.int32, "n_sent+1"),
-                ("tok_id", np.int32, "n_tok_entries"), ("tok_alpha", np.uint16, "n_tok_entries"),
+                ("tok_id", np.int32, "n_tok_entries"), ("tok_alpha", np.uint32, "n_tok_entries"),
                 ("dig_off", np.int32, "n_sent+1"), ("dig_id", np.int32, "n_dig_entries"),
                 ("src0", np.int32, "n_docs"), ("n", np.int32, "n_docs"),
                 ("tgt0", np.int32, "n_docs"), ("m", np.int32, "n_docs"))
@@ -193,19 +193,12 @@ def mine_corpus_file(
     c = nc.packed
     n = c.n.astype(np.int64)
     m = c.m.astype(np.int64)
-    from .miner import MAX_SENTENCE_TOKENS
-
     over = n * m > aligner.MAX_CELLS
-    tmax = c.doc_token_max() if int(c.n_tok.max(initial=0)) > MAX_SENTENCE_TOKENS else None
-    skip = (over | (tmax > MAX_SENTENCE_TOKENS if tmax is not None else False)).astype(np.uint8)
+    skip = over.astype(np.uint8)
     for k in np.nonzero(skip)[0].tolist():
-        if over[k]:
-            a, b = (int(c.m[k]), int(c.n[k])) if sw_f[k] else (int(c.n[k]), int(c.m[k]))
-            why = (f"document pair {nc.doc_ids[k]!r} needs a {a}x{b} matrix, "
-                   f"over the {aligner.MAX_CELLS} cell limit")
-        else:
-            why = (f"document pair {nc.doc_ids[k]!r} has a sentence of {int(tmax[k])} tokens, "
-                   f"over the {MAX_SENTENCE_TOKENS} token limit")
+        a, b = (int(c.m[k]), int(c.n[k])) if sw_f[k] else (int(c.n[k]), int(c.m[k]))
+        why = (f"document pair {nc.doc_ids[k]!r} needs a {a}x{b} matrix, "
+               f"over the {aligner.MAX_CELLS} cell limit")
         log.warning("skipping: %s", why)
     work = np.nonzero(skip == 0)[0].astype(np.int64)
     rec_dtype = np.dtype(N.RECORD_DTYPE)

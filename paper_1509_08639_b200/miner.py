@@ -109,23 +109,6 @@ def _cap_error(pair: DocumentPair, swapped: bool) -> ResourceLimitError | None:
     return None
 
 
-# hit counts are 16-bit fields on the device (csrc: hits_kernel, K1)
-MAX_SENTENCE_TOKENS = 65535
-
-
-def _token_cap_error(pair: DocumentPair) -> ResourceLimitError | None:
-    """This implementation's own hard bound (not the reference's): a sentence
-    with more than MAX_SENTENCE_TOKENS tokens is skipped like an over-cap
-    matrix, with a ResourceLimitError reason."""
-    for s in pair.source.sentences + pair.target.sentences:
-        if len(s.tokens) > MAX_SENTENCE_TOKENS:
-            return ResourceLimitError(
-                f"document pair {pair.id!r} has a sentence of {len(s.tokens)} tokens, over the "
-                f"{MAX_SENTENCE_TOKENS} token limit"
-            )
-    return None
-
-
 class _Pass:
     """One model direction over a packed batch (lexicon uploaded once)."""
 
@@ -207,8 +190,6 @@ def mine_documents(
             pairs = pairs[:k]
             results = results[:k]
             break
-        if cap is None:
-            cap = _token_cap_error(pair)
         if cap is not None:
             results[k] = ([], str(cap))
             continue
@@ -318,20 +299,36 @@ def mine_corpus(
                 src_tokens.update(tokenize(rec.src.normalized))
                 tgt_tokens.update(tokenize(rec.tgt.normalized))
 
-    batch: list[DocumentPair] = []
-    for pair in doc_pairs:
-        batch.append(pair)
-        if len(batch) >= BATCH_DOCS:
-            results, err = mine_documents(batch, forward, backward, lex, cfg)
-            consume(results)
-            if err is not None:
-                raise err
-            batch = []
-    if batch:
+    def flush(batch: list[DocumentPair]) -> None:
         results, err = mine_documents(batch, forward, backward, lex, cfg)
         consume(results)
         if err is not None:
             raise err
+
+    if cfg.workers > 1:
+        # the reference's pool.map submits every document before the first
+        # result is written (miner.py:238-245): a failing iterator writes nothing
+        doc_pairs = list(doc_pairs)
+    batch: list[DocumentPair] = []
+    it = iter(doc_pairs)
+    while True:
+        try:
+            pair = next(it)
+        except StopIteration:
+            break
+        except BaseException:
+            # workers=1 maps lazily (miner.py:236-237): every document read
+            # before the failing one is mined and written (or its own task
+            # error wins), then the iterator's exception propagates
+            if batch:
+                flush(batch)
+            raise
+        batch.append(pair)
+        if len(batch) >= BATCH_DOCS:
+            flush(batch)
+            batch = []
+    if batch:
+        flush(batch)
 
     report.unique_src_tokens = len(src_tokens)
     report.unique_tgt_tokens = len(tgt_tokens)

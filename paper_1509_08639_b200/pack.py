@@ -22,9 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .corpus import DocumentPair, Sentence, normalize
-from .errors import ResourceLimitError
 
-_ALPHA_MAX = 65535  # tok_alpha is uint16
 
 
 @dataclass
@@ -127,11 +125,6 @@ class Packer:
             if did >= 0:
                 digits.add(did)
             punct += is_punct
-        for nid, cnt in alpha.items():
-            if cnt > _ALPHA_MAX:
-                raise ResourceLimitError(
-                    f"a sentence repeats one token {cnt} times (limit {_ALPHA_MAX})"
-                )
         idx = len(self._T)
         self._T.append(len(sent.tokens))
         self._P.append(punct)
@@ -165,7 +158,7 @@ class Packer:
             n_alpha=np.asarray(self._A, dtype=np.int32),
             tok_off=np.asarray(self._tok_off, dtype=np.int32),
             tok_id=np.asarray(self._tok_id, dtype=np.int32),
-            tok_alpha=np.asarray(self._tok_alpha, dtype=np.uint16),
+            tok_alpha=np.asarray(self._tok_alpha, dtype=np.uint32),
             dig_off=np.asarray(self._dig_off, dtype=np.int32),
             dig_id=np.asarray(self._dig_id, dtype=np.int32),
             src0=np.ascontiguousarray(d[:, 0]),

@@ -190,7 +190,7 @@ def make_corpus(n_gold, n_src, n_tgt, vocab: int = 5000, noise: float = 0.1, see
     # unique (sentence, id) with alpha multiplicities
     key = ts * W.n_ids + ti
     uk, inv = np.unique(key, return_inverse=True)
-    alpha = np.bincount(inv, weights=ta, minlength=uk.size).astype(np.uint16)
+    alpha = np.bincount(inv, weights=ta, minlength=uk.size).astype(np.uint32)
     u_sent = uk // W.n_ids
     u_id = (uk % W.n_ids).astype(np.int32)
     tok_off = np.zeros(S + 1, dtype=np.int32)

@@ -216,6 +216,31 @@ def test_mine_corpus_file_native_path_byte_identical(docs, tsv, bidir, t, p, wor
         assert bm.report_to_json(rep) == open(golden(tsv.replace(".tsv", ".report.json"))).read()
 
 
+@pytest.mark.parametrize("workers", [1, 3])
+@pytest.mark.parametrize("entry", ["mine_corpus", "mine_corpus_file"])
+def test_mine_corpus_malformed_line_after_good_docs(world500, tmp_path, workers, entry):
+    """A loader error after 5 good documents (tests/golden/make_golden_r02.py):
+    workers=1 writes those 5 documents first, workers>1 writes nothing, and
+    the loader's DataError propagates either way -- the reference's bytes."""
+    lex, fwd, bwd = world500
+    lines = open(golden("docs40.jsonl"), encoding="utf-8").read().splitlines(True)
+    path = str(tmp_path / "bad.jsonl")
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.writelines(lines[:5])
+        fh.write("{not json\n")
+        fh.writelines(lines[5:])
+    want = json.load(open(golden("mine40_badline.json")))[f"workers{workers}"]
+    sink = io.StringIO()
+    cfg = bm.MinerConfig(bm.MiningParams(0.5, 0.2), workers=workers)
+    with pytest.raises(bm.DataError) as exc:
+        if entry == "mine_corpus":
+            bm.mine_corpus(bm.load_document_pairs(path), fwd, bwd, lex, cfg, sink)
+        else:
+            bm.mine_corpus_file(path, fwd, bwd, lex, cfg, sink)
+    assert str(exc.value).replace(path, "<path>") == want["error"]
+    assert sink.getvalue() == want["tsv"]
+
+
 def test_mine_corpus_file_1000_docs_sha256(world500, tmp_path):
     import gzip
 
@@ -363,29 +388,60 @@ def test_mine_long_sentences_general_path(oracle_mod):
         [(int(a), int(b), float(c)) for a, b, c in zip(recs["i"], recs["j"], recs["conf"])]
 
 
-def test_sentence_over_the_token_bound_is_skipped(world500, tmp_path):
-    """A sentence longer than 65535 tokens (16-bit device hit counts) is this
-    implementation's own hard limit: the document is skipped with a
-    ResourceLimitError reason, like an over-cap matrix; the rest is mined as
-    usual, through both the Python and the native JSONL paths."""
-    from paper_1509_08639_b200.miner import MAX_SENTENCE_TOKENS
-
-    lex, fwd, bwd = world500
+def _big_token_docs():
+    """tests/golden/make_golden_r02.py big_token_docs(): a document whose first
+    sentences hold 70,003 / 66,002 tokens (multiplicities and hit counts past
+    16 bits) between two docs40 documents."""
     docs = load_docs("docs40.jsonl")[:3]
-    words = ["w" + "".join(chr(97 + (k // 26 ** e) % 26) for e in range(4)) for k in range(70000)]
-    big = dict(docs[1], id="big", src=[" ".join(words) + "."] + docs[1]["src"][1:])
-    cfg = bm.MinerConfig(bm.MiningParams(0.5, 0.2))
-    want, _ = _mine_text(pairs_of([docs[0], docs[2]]), fwd, bwd, lex)
-    got, rep = _mine_text(pairs_of([docs[0], big, docs[2]]), fwd, bwd, lex)
-    assert got == want and json.loads(rep)["docs_skipped"] == 1
+    big = dict(docs[1], id="big")
+    big["src"] = ["waaa " * 70000 + "wadf walb."] + docs[1]["src"][1:]
+    big["tgt"] = ["vaaa " * 66000 + "vadf vafr."] + docs[1]["tgt"][1:]
+    return [docs[0], big, docs[2]]
+
+
+def test_sentences_over_65535_tokens_are_mined(world500, tmp_path):
+    """Sentences longer than 65,535 tokens are mined like any other (32-bit
+    counts on the per-tile scoring path): the reference's TSV bytes and report,
+    through both the Python and the native JSONL paths."""
+    lex, fwd, bwd = world500
+    want = json.load(open(golden("mine_big_tokens.json")))
+    docs = _big_token_docs()
+    got, rep = _mine_text(pairs_of(docs), fwd, bwd, lex)
+    assert hashlib.sha256(got.encode()).hexdigest() == want["sha256"]
+    assert rep == want["report"]
+    assert [ln for ln in got.splitlines(True) if len(ln) < 400] == want["short_lines"]
     p = str(tmp_path / "big.jsonl")
     with open(p, "w") as fh:
-        for d in (docs[0], big, docs[2]):
+        for d in docs:
             fh.write(json.dumps(d) + "\n")
     sink = io.StringIO()
-    rep2 = bm.mine_corpus_file(p, fwd, bwd, lex, cfg, sink)
-    assert sink.getvalue() == want and rep2.docs_skipped == 1
-    assert len(words) > MAX_SENTENCE_TOKENS
+    rep2 = bm.mine_corpus_file(p, fwd, bwd, lex, bm.MinerConfig(bm.MiningParams(0.5, 0.2)), sink)
+    assert hashlib.sha256(sink.getvalue().encode()).hexdigest() == want["sha256"]
+    assert rep2.docs_skipped == 0 and rep2.pairs_emitted == want["lines"]
+
+
+def test_big_token_scores_and_tune_vs_oracle(world500, oracle_mod):
+    """The same document's similarity matrix (bm_score) and a tune sweep over it
+    (bm_tune with token_bound > 65535) against the oracle."""
+    from oracle_pipeline import oracle_records  # noqa: F401
+    from paper_1509_08639_b200 import engine
+    from paper_1509_08639_b200.pack import pack_lexicon, pack_pairs
+
+    lex, fwd, _ = world500
+    pairs = pairs_of(_big_token_docs())
+    S = bm.build_similarity_matrix(pairs[1], fwd, lex).cells
+    corpus = pack_pairs(pairs)
+    hb = oracle_mod.HostBatch(corpus, pack_lexicon(lex, corpus))
+    want = oracle_mod.score_doc(hb, fwd, 1)
+    assert np.array_equal(S.view(np.uint64), want.view(np.uint64))
+    gold = [np.asarray([0, 1 * int(corpus.m[d]) + 1], np.int64) for d in range(3)]
+    dc = engine.DeviceCorpus.upload(corpus)
+    dl = engine.DeviceLexicon.upload(pack_lexicon(lex, corpus))
+    assert dc.max_tok > 65535
+    p, h = engine.tune_counts(dc, dl, engine.DocView.of(corpus), fwd, [0.1, 0.2, 0.4],
+                              [0.3, 0.5, 0.9], gold)
+    wp, wh = oracle_mod.tune(hb, fwd, [0.1, 0.2, 0.4], [0.3, 0.5, 0.9], gold)
+    assert np.array_equal(p, wp) and np.array_equal(h, wh)
 
 
 def test_synth_text_round_trip_same_records():
