@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define BM_ABI_VERSION 1
+#define BM_ABI_VERSION 2  /* 2: tok_alpha widened to uint32 (any sentence length) */
 
 #define BM_OK 0
 #define BM_EINVAL -1   /* bad argument (maps to ValueError)            */
@@ -278,6 +278,15 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
  * document-ordered array; *total (device) receives the record count. */
 int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_count,
                int32_t n_docs, bm_record* dense, int64_t* total, void* stream);
+
+/* Multi-GPU result gather, rank 0 (the reference's ordered
+ * pool.map, bimine/miner.py:236-245): the compacted records of `world` ranks
+ * sit in a padded [world][stride] device layout with part_len[r] (device)
+ * valid records each; every rank mined its own documents, ordered by global
+ * document index (record.doc). Writes all of them to out in global document
+ * order (path order within a document) and their number to *total (device). */
+int bm_merge_shards(const bm_record* rec, int64_t stride, const int64_t* part_len, int32_t world,
+                    int32_t n_docs, bm_record* out, int64_t* total, void* stream);
 
 /* ------------------------------------------------------------------------
  * Native corpus path: host C++, no device work.

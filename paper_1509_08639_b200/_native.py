@@ -111,6 +111,7 @@ _SIGS = {
                           C.POINTER(ModelC), _p, C.c_int32, _p, C.c_int32, _p, _p, _p, _p,
                           C.c_int32, _p]),
     "bm_compact": (C.c_int, [_p, _p, _p, C.c_int32, _p, _p, _p]),
+    "bm_merge_shards": (C.c_int, [_p, C.c_int64, _p, C.c_int32, C.c_int32, _p, _p, _p]),
     "bm_ingest_jsonl": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32]),
     "bm_ingest_free": (None, [C.c_void_p]),
     "bm_ingest_view": (C.c_int, [C.c_void_p, C.POINTER(IngestArrays)]),
@@ -125,6 +126,28 @@ _SIGS = {
 }
 
 EXPORTED = tuple(_SIGS)
+
+
+class SynthSpec(C.Structure):
+    _fields_ = [("vocab", C.c_int32), ("noise", C.c_double), ("digit_rate", C.c_double),
+                ("seed", C.c_uint64)]
+
+
+class SynthArrays(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("n_sent", "n_docs", "n_tok_entries", "n_dig_entries",
+                                          "n_gold")] + [
+        (name, C.c_void_p) for name in ("n_tok", "n_punct", "n_alpha", "tok_off", "tok_id",
+                                        "tok_alpha", "dig_off", "dig_id", "src0", "n", "tgt0",
+                                        "m", "gold_off", "gold_i", "gold_j")]
+
+
+# include/bimine_synth.h: benchmark input generation (not the mining boundary)
+SYNTH_SIGS = {
+    "bm_synth_generate": (C.c_int, [C.POINTER(SynthSpec), _p, _p, _p, _p, C.c_int64, C.c_int32,
+                                    C.POINTER(C.c_void_p)]),
+    "bm_synth_view": (C.c_int, [C.c_void_p, C.POINTER(SynthArrays)]),
+    "bm_synth_free": (None, [C.c_void_p]),
+}
 
 _lock = threading.Lock()
 _lib: C.CDLL | None = None
@@ -141,7 +164,7 @@ def load_library(require_device: bool = False) -> C.CDLL:
                     "`python -c 'import __graft_entry__ as g; g.build()'`"
                 )
             lib = C.CDLL(LIB_PATH)
-            for name, (res, args) in _SIGS.items():
+            for name, (res, args) in {**_SIGS, **SYNTH_SIGS}.items():
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -500,27 +500,32 @@ int bm_select(const double* S, int64_t pitch, const int32_t* ci, const int32_t* 
   return BM_OK;
 }
 
-int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
-            const int32_t* m_host, const int32_t* amax_host, const bm_lexicon* lex,
-            const bm_model* model, double threshold, double penalty, const int64_t* rec_off,
-            bm_record* rec, int32_t* rec_count, double* cost, void* stream) {
-  BM_CK(ensure_quot_table(), "quotient table");
-  if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
-  cudaStream_t st = (cudaStream_t)stream;
-  HostTrace tr("bm_mine");
-  const int nd = docs->n_docs;
-  BM_CK(cudaMemsetAsync(rec_count, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
-  tr.mark("memset");
+// Documents per bm_mine group: consecutive documents up to this many cells
+// share one routing pass and one set of scratch buffers (2 B/cell of hit
+// counts for the fused tier, 4 + 8 B/cell for the banded tier), freed
+// stream-ordered before the next group allocates, so any batch size fits.
+static int64_t mine_group_cells() {
+  static const int64_t v =
+      getenv("BM_GROUP_CELLS") ? atoll(getenv("BM_GROUP_CELLS")) : (int64_t)1 << 30;
+  return std::max<int64_t>(v, 1);
+}
+
+static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+               const int32_t* m_host, const int32_t* amax_host, const bm_lexicon* lex,
+               const Model& M, double threshold, double penalty, const int64_t* rec_off,
+               bm_record* rec, int32_t* rec_count, double* cost, int d_lo, int d_hi,
+               HostTrace& tr, cudaStream_t st) {
   std::vector<int32_t> fused[4];
   size_t fused_smem[4] = {0, 0, 0, 0}, hits_smem[4] = {0, 0, 0, 0};
-  std::vector<int64_t> hit_off(nd, 0);
+  std::vector<int64_t> hit_off;  // per document of [d_lo, d_hi)
   int64_t hit_total = 0;
   std::vector<int32_t> banded;  // planned after the fused tier is launched
   // BM_ROUTE=banded forces every document onto the K1 -> K2/K3 -> K4 tier
   // (benchmarking / testing both tiers on the same workload).
   const char* route = getenv("BM_ROUTE");
   const bool force_banded = route != nullptr && strcmp(route, "banded") == 0;
-  for (int d = 0; d < nd; ++d) {
+  hit_off.assign((size_t)(d_hi - d_lo), 0);
+  for (int d = d_lo; d < d_hi; ++d) {
     const int n = n_host[d], m = m_host[d];
     if (n <= 0 || m <= 0) continue;
     const int R = fused_rows_per_lane(n);
@@ -530,7 +535,7 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       fused[q].push_back(d);
       fused_smem[q] = std::max(fused_smem[q], sl);
       hits_smem[q] = std::max(hits_smem[q], hits_kernel_smem(n, m));
-      hit_off[d] = hit_total;
+      hit_off[d - d_lo] = hit_total;
       hit_total += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
     } else {
       banded.push_back(d);
@@ -538,16 +543,14 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   }
   tr.mark("route");
   Scratch sc(st);
-  const Model M = to_model(model);
   if (hit_total > 0) {
     uint8_t* hits = nullptr;
     int64_t* dho = nullptr;
     if (!BM_RING_FUSED_JOIN) {
       BM_CK(sc.alloc(&hits, (size_t)hit_total), "alloc hits");
       BM_CK(cudaMemsetAsync(hits, 0, (size_t)hit_total, st), "memset hits");
-      tr.mark("alloc hits");
       BM_CK(sc.upload(&dho, hit_off), "upload");
-      tr.mark("upload hit_off");
+      tr.mark("alloc hits");
     }
     for (int q = 0; q < 4; ++q) {
       if (fused[q].empty()) continue;
@@ -567,22 +570,13 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
       a.rec_count = rec_count;
       a.cost = cost;
       a.hits = hits;
-      a.hit_off = dho;
+      a.hit_off = dho - d_lo;  // indexed by the batch's document index
       a.tabs = pair_tables();
       BM_CK(model_tables(M, &a.mt), "model tables");
-      tr.mark("upload list");
-      if (!BM_RING_FUSED_JOIN) {
-        BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
-        tr.mark("launch hits");
-      }
+      if (!BM_RING_FUSED_JOIN) BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
       BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
-      tr.mark("launch ring");
+      tr.mark("launch fused tier");
     }
-  }
-  cudaEvent_t tl_fused = nullptr;
-  if (tr.on) {  // BM_TRACE: when the fused tier's kernels finish on the GPU
-    cudaEventCreate(&tl_fused);
-    cudaEventRecord(tl_fused, st);
   }
   // banded tier: the document-level join keeps 16-bit hit counts (every
   // sentence <= 65535 tokens); longer sentences take the per-tile scoring
@@ -596,10 +590,30 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     if (rc) return rc;
     tr.mark("banded tier enqueued");
   }
-  if (tr.on) {
-    cudaEventSynchronize(tl_fused);
-    tr.mark("fused tier done on GPU");
-    cudaEventDestroy(tl_fused);
+  return BM_OK;
+}
+
+int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
+            const int32_t* m_host, const int32_t* amax_host, const bm_lexicon* lex,
+            const bm_model* model, double threshold, double penalty, const int64_t* rec_off,
+            bm_record* rec, int32_t* rec_count, double* cost, void* stream) {
+  BM_CK(ensure_quot_table(), "quotient table");
+  if (!check_penalty(penalty)) return fail(BM_EINVAL, "penalty must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  HostTrace tr("bm_mine");
+  const int nd = docs->n_docs;
+  BM_CK(cudaMemsetAsync(rec_count, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
+  const Model M = to_model(model);
+  const int64_t budget = mine_group_cells();
+  for (int d0 = 0; d0 < nd;) {
+    int d1 = d0;
+    int64_t cells = 0;
+    while (d1 < nd && (d1 == d0 || cells + (int64_t)n_host[d1] * m_host[d1] <= budget))
+      cells += (int64_t)n_host[d1] * m_host[d1], ++d1;
+    int rc = mine_group(sent, docs, n_host, m_host, amax_host, lex, M, threshold, penalty,
+                        rec_off, rec, rec_count, cost, d0, d1, tr, st);
+    if (rc) return rc;
+    d0 = d1;
   }
   return BM_OK;
 }
@@ -608,15 +622,33 @@ int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_
                int32_t n_docs, bm_record* dense, int64_t* total, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   Scratch sc(st);
-  int64_t* doff = nullptr;
+  int64_t *doff = nullptr, *bsum = nullptr;
   BM_CK(sc.alloc(&doff, n_docs), "alloc");
-  BM_CK(launch_compact(rec, rec_off, rec_count, n_docs, doff, total, dense, st), "compact");
+  BM_CK(sc.alloc(&bsum, scan_scratch_count(n_docs)), "alloc");
+  BM_CK(launch_compact(rec, rec_off, rec_count, n_docs, doff, total, dense, bsum, st), "compact");
+  return BM_OK;
+}
+
+int bm_merge_shards(const bm_record* rec, int64_t stride, const int64_t* part_len, int32_t world,
+                    int32_t n_docs, bm_record* out, int64_t* total, void* stream) {
+  if (world < 1 || stride < 0 || n_docs < 0) return fail(BM_EINVAL, "bad shard layout");
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch sc(st);
+  int32_t* counts = nullptr;
+  int64_t *src_start = nullptr, *goff = nullptr, *bsum = nullptr;
+  BM_CK(sc.alloc(&counts, n_docs), "alloc");
+  BM_CK(sc.alloc(&src_start, n_docs), "alloc");
+  BM_CK(sc.alloc(&goff, n_docs), "alloc");
+  BM_CK(sc.alloc(&bsum, scan_scratch_count(n_docs)), "alloc");
+  BM_CK(launch_merge_shards(rec, stride, part_len, world, n_docs, counts, src_start, goff, total,
+                            bsum, out, st),
+        "merge_shards");
   return BM_OK;
 }
 
 // Copy stream of the calling thread on the current device (H2D of chunk k+1
 // overlaps the kernels of chunk k in bm_mine_host).
-cudaStream_t copy_stream() {
+static cudaStream_t copy_stream() {
   static thread_local cudaStream_t s = nullptr;
   static thread_local int dev_of = -1;
   int dev = 0;
@@ -631,7 +663,7 @@ cudaStream_t copy_stream() {
 // Extra compute streams of the calling thread: bm_mine_host deals chunks
 // round-robin over the caller's stream and these, so a chunk's kernel tails
 // overlap the next chunks' kernels.
-cudaStream_t side_stream(int q) {
+static cudaStream_t side_stream(int q) {
   static thread_local cudaStream_t s[kMaxMineStreams] = {};
   static thread_local int dev_of = -1;
   int dev = 0;
@@ -645,7 +677,7 @@ cudaStream_t side_stream(int q) {
 }
 
 // Page-locked per-chunk record counts of the calling thread (grown on demand).
-int64_t* pinned_counts(size_t n) {
+static int64_t* pinned_counts(size_t n) {
   static thread_local int64_t* buf = nullptr;
   static thread_local size_t cap = 0;
   if (n > cap) {
@@ -673,7 +705,7 @@ struct HostSource {
   }
 };
 
-int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* lh,
+static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* lh,
                    const bm_model* model, double threshold, double penalty, bm_record* rec_out,
                    int64_t rec_cap, int64_t* n_rec, double* cost_out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -824,6 +856,8 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   // chunk count upper bound: every chunk but the last holds >= 1 document
   int64_t* ctot = nullptr;
   BM_CK(sc.alloc(&ctot, nd + 1), "alloc");
+  int64_t* bsum_all = nullptr;  // per-chunk scan scratch (see enqueue_kernels)
+  BM_CK(sc.alloc(&bsum_all, 2 * (size_t)nd + 2), "alloc");
   tr.mark("allocs");
   int64_t* hcnt = pinned_counts((size_t)nd + 1);
   if (hcnt == nullptr) return fail(BM_ENOMEM, "pinned count buffer");
@@ -847,10 +881,17 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
   tr.mark("alloc + small h2d");
   // chunks of documents: H2D the sentence range each chunk touches on the
   // copy stream, mine it on the compute stream once its copy event fired
-  static const int64_t kChunkCells =
-      getenv("BM_CHUNK_CELLS") ? atoll(getenv("BM_CHUNK_CELLS")) : (16ll << 20);
-  static const int64_t kFirstChunkCells =
-      getenv("BM_FIRST_CHUNK_CELLS") ? atoll(getenv("BM_FIRST_CHUNK_CELLS")) : kChunkCells / 4;
+  // (16M cells per chunk; large batches use at most ~64 chunks, each at most
+  // mine_group_cells(): per-chunk launches and host planning stay amortised)
+  int64_t all_cells = 0;
+  for (int d = 0; d < nd; ++d) all_cells += (int64_t)dh->n[d] * dh->m[d];
+  static const int64_t kChunkEnv = getenv("BM_CHUNK_CELLS") ? atoll(getenv("BM_CHUNK_CELLS")) : 0;
+  const int64_t kChunkCells =
+      kChunkEnv > 0 ? kChunkEnv
+                    : std::min(mine_group_cells(), std::max<int64_t>(16ll << 20, all_cells / 64));
+  static const int64_t kFirstEnv =
+      getenv("BM_FIRST_CHUNK_CELLS") ? atoll(getenv("BM_FIRST_CHUNK_CELLS")) : 0;
+  const int64_t kFirstChunkCells = kFirstEnv > 0 ? kFirstEnv : (4ll << 20);
   // per chunk: docs [d0, d1), compacted into dense + roff[d0], count -> ctot[k]
   std::vector<int> ch_d0, ch_d1;
   std::vector<cudaEvent_t> ch_ev;
@@ -1073,8 +1114,9 @@ int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lexicon* l
     // records out as soon as the count arrives, overlapping later chunks
     {
       const int kq = (int)ch_d0.size();
+      // chunk kq's scan scratch: [d0 + kq, d1 + kq] (>= its block count + 1)
       BM_CK(launch_compact(rec, droff + d0, cnt + d0, d1 - d0, doff + d0, ctot + kq,
-                           dense + roff[d0], sk, d0),
+                           dense + roff[d0], bsum_all + d0 + kq, sk, d0),
             "compact");
       BM_CK(cudaMemcpyAsync(hcnt + kq, ctot + kq, sizeof(int64_t), cudaMemcpyDeviceToHost, sk),
             "d2h");

@@ -137,7 +137,13 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
                               const int64_t* s_off, const int32_t* pitch, double* out,
                               cudaStream_t st);
 cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int, int64_t*,
-                           int64_t*, bm_record*, cudaStream_t, int doc0 = 0);
+                           int64_t*, bm_record*, int64_t* bsum, cudaStream_t, int doc0 = 0);
+cudaError_t launch_scan_counts(const int32_t* cnt, int n, int64_t* off, int64_t* total,
+                               int64_t* bsum, cudaStream_t st);
+size_t scan_scratch_count(int n);
+cudaError_t launch_merge_shards(const bm_record* rec, int64_t stride, const int64_t* len, int world,
+                                int n_docs, int32_t* counts, int64_t* src_start, int64_t* goff,
+                                int64_t* total, int64_t* bsum, bm_record* out, cudaStream_t st);
 size_t score_smem_bytes();
 cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -54,9 +55,19 @@ struct Rng {  // xoshiro256** seeded by splitmix64
   double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
 };
 
+template <class T>
+struct Buf {  // append-only buffer without zero-fill (sized to an upper bound)
+  T* p = nullptr;
+  size_t n = 0;
+  void init(size_t cap) { p = (T*)malloc(std::max<size_t>(cap, 1) * sizeof(T)); }
+  ~Buf() { free(p); }
+  void push(T v) { p[n++] = v; }
+  size_t size() const { return n; }
+};
+
 struct Part {  // one thread's documents, sentence and entry offsets local
-  std::vector<int32_t> n_tok, n_punct, n_alpha, tok_off{0}, tok_id, dig_off{0}, dig_id;
-  std::vector<uint32_t> tok_alpha;
+  Buf<int32_t> n_tok, n_punct, n_alpha, tok_off, tok_id, dig_off, dig_id;
+  Buf<uint32_t> tok_alpha;
   std::vector<int32_t> src0, n, tgt0, m;
   std::vector<int64_t> gold_off{0};
   std::vector<int32_t> gold_i, gold_j;
@@ -81,32 +92,37 @@ struct Event {
 // one sentence: words (+ year) + "."; U = ascending unique ids with alpha counts
 void emit_sentence(Part& p, const int32_t* words, int k, int year_id, int dot) {
   int32_t ids[11];
-  for (int q = 0; q < k; ++q) ids[q] = words[q];
-  std::sort(ids, ids + k);
+  for (int q = 0; q < k; ++q) {  // insertion sort (k <= 9)
+    const int32_t v = words[q];
+    int u = q;
+    for (; u > 0 && ids[u - 1] > v; --u) ids[u] = ids[u - 1];
+    ids[u] = v;
+  }
+  int32_t* out = p.tok_id.p + p.tok_id.n;
+  uint32_t* cnt = p.tok_alpha.p + p.tok_alpha.n;
   int nu = 0;
-  uint32_t cnt[11];
   for (int q = 0; q < k; ++q) {
-    if (nu > 0 && ids[nu - 1] == ids[q]) {
+    if (nu > 0 && out[nu - 1] == ids[q]) {
       ++cnt[nu - 1];
     } else {
-      ids[nu] = ids[q];
+      out[nu] = ids[q];
       cnt[nu++] = 1;
     }
   }
-  ids[nu] = dot;  // ids: words < 2V = dot < years
+  out[nu] = dot;  // ids: words < 2V = dot < years
   cnt[nu++] = 0;
   if (year_id >= 0) {
-    ids[nu] = year_id;
+    out[nu] = year_id;
     cnt[nu++] = 0;
-    p.dig_id.push_back(year_id);
+    p.dig_id.push(year_id);
   }
-  p.tok_id.insert(p.tok_id.end(), ids, ids + nu);
-  p.tok_alpha.insert(p.tok_alpha.end(), cnt, cnt + nu);
-  p.tok_off.push_back((int32_t)p.tok_id.size());
-  p.dig_off.push_back((int32_t)p.dig_id.size());
-  p.n_tok.push_back(k + (year_id >= 0 ? 1 : 0) + 1);
-  p.n_punct.push_back(1);
-  p.n_alpha.push_back(k);
+  p.tok_id.n += nu;
+  p.tok_alpha.n += nu;
+  p.tok_off.push((int32_t)p.tok_id.n);
+  p.dig_off.push((int32_t)p.dig_id.n);
+  p.n_tok.push(k + (year_id >= 0 ? 1 : 0) + 1);
+  p.n_punct.push(1);
+  p.n_alpha.push(k);
 }
 
 void gen_doc(Part& p, const bm_synth_spec& sp, int64_t doc, int32_t g, int32_t a, int32_t b,
@@ -167,8 +183,12 @@ void gen_doc(Part& p, const bm_synth_spec& sp, int64_t doc, int32_t g, int32_t a
 }
 
 template <class T>
-void append(std::vector<T>& dst, size_t at, const std::vector<T>& src, T add, size_t skip = 0) {
-  for (size_t q = skip; q < src.size(); ++q) dst[at + q - skip] = src[q] + add;
+T src_at(const std::vector<T>& v, size_t q) { return v[q]; }
+template <class T>
+T src_at(const Buf<T>& v, size_t q) { return v.p[q]; }
+template <class T, class S>
+void append(std::vector<T>& dst, size_t at, const S& src, T add, size_t skip = 0) {
+  for (size_t q = skip; q < src.size(); ++q) dst[at + q - skip] = src_at(src, q) + add;
 }
 
 }  // namespace
@@ -186,6 +206,15 @@ int bm_synth_generate(const bm_synth_spec* spec, const int64_t* ids, const int32
   for (int t = 0; t < nt; ++t)
     pool.emplace_back([&, t] {
       const int64_t lo = k * t / nt, hi = k * (t + 1) / nt;
+      int64_t sents = 0;
+      for (int64_t q = lo; q < hi; ++q) sents += 2 * (int64_t)g[q] + a[q] + b[q];
+      Part& p = parts[t];
+      for (auto* v : {&p.n_tok, &p.n_punct, &p.n_alpha, &p.tok_off, &p.dig_off, &p.dig_id})
+        v->init(sents + 1);
+      p.tok_id.init(sents * 11);
+      p.tok_alpha.init(sents * 11);
+      p.tok_off.push(0);
+      p.dig_off.push(0);
       std::vector<Event> ev;
       for (int64_t q = lo; q < hi; ++q) gen_doc(parts[t], *spec, ids[q], g[q], a[q], b[q], ev);
     });
@@ -238,9 +267,6 @@ int bm_synth_generate(const bm_synth_spec* spec, const int64_t* ids, const int32
       append(c->gold_off, kb[t] + 1, p.gold_off, (int64_t)gb[t], 1);
       append(c->gold_i, gb[t], p.gold_i, 0);
       append(c->gold_j, gb[t], p.gold_j, 0);
-      Part().n_tok.swap(p.n_tok);  // release the thread's buffers early
-      std::vector<int32_t>().swap(p.tok_id);
-      std::vector<uint32_t>().swap(p.tok_alpha);
     });
   for (auto& th : pool) th.join();
   *handle = c;

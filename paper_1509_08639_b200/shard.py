@@ -104,3 +104,24 @@ def mine_shard(corpus, plex, model, threshold: float, penalty: float, rank: int,
     recs = recs.copy()
     recs["doc"] = idx[recs["doc"]]
     return recs, idx
+
+
+def merge_shards_device(parts, lens, n_docs: int):
+    """Rank-0 side of the gather on the device: ``parts`` is a [world, stride, 6]
+    int32 CUDA tensor of 24-byte records (doc = global index, each rank's
+    records in document order), ``lens`` the int64 CUDA tensor of valid counts.
+    Returns the records in global document order as a uint8 CUDA tensor
+    (bm_merge_shards)."""
+    import torch
+
+    from . import _native as N
+    from . import engine
+
+    lib = N.lib()
+    world, stride = int(parts.shape[0]), int(parts.shape[1])
+    out = torch.empty(max(world * stride, 1) * RECORD_DTYPE.itemsize, dtype=torch.uint8,
+                      device=parts.device)
+    total = torch.zeros(1, dtype=torch.int64, device=parts.device)
+    N.check(lib.bm_merge_shards(engine._ptr(parts), stride, engine._ptr(lens), world, int(n_docs),
+                                engine._ptr(out), engine._ptr(total), engine.stream_ptr()))
+    return out[: int(total.item()) * RECORD_DTYPE.itemsize]

@@ -249,3 +249,87 @@ def c3_shape(n_docs: int, seed: int = 2026):
     m = np.clip(np.rint(n * np.exp(r.normal(0.0, 0.25, n_docs))), 10, 2000).astype(np.int64)
     g = np.floor(0.6 * np.minimum(n, m)).astype(np.int64)
     return g, n - g, m - g
+
+
+class _SynthHandle:
+    """Owns a bm_synth corpus; numpy views of its arrays keep it alive."""
+
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        if self.h:
+            self.lib.bm_synth_free(self.h)
+            self.h = None
+
+
+def _view(owner, ptr: int, count: int, dtype) -> np.ndarray:
+    import ctypes as C
+
+    dt = np.dtype(dtype)
+    if count == 0:
+        return np.zeros(0, dtype=dt)
+    buf = (C.c_char * (count * dt.itemsize)).from_address(ptr)
+    a = np.frombuffer(buf, dtype=dt, count=count)
+    a.flags.writeable = False
+    # the view's base chain ends in `buf`; hang the owner on it
+    buf._owner = owner
+    return a
+
+
+@dataclass
+class NativeSynthCorpus:
+    """Output of make_corpus_native: the packed batch plus per-doc gold cells
+    (gold_off[d] .. gold_off[d+1] into gold_i / gold_j)."""
+
+    world: SynthWorld
+    packed: PackedCorpus
+    gold_off: np.ndarray
+    gold_i: np.ndarray
+    gold_j: np.ndarray
+
+    def gold_keys(self) -> list[np.ndarray]:
+        """Per-doc gold keys i * m + j (ascending), the tuner's device layout."""
+        m = self.packed.m.astype(np.int64)
+        key = self.gold_i.astype(np.int64) * np.repeat(m, np.diff(self.gold_off)) + self.gold_j
+        return [np.sort(key[self.gold_off[d]:self.gold_off[d + 1]]) for d in range(len(m))]
+
+
+def make_corpus_native(n_gold, n_src, n_tgt, ids=None, vocab: int = 5000, noise: float = 0.1,
+                       seed: int = 0, digit_rate: float = 0.15, threads: int = 0
+                       ) -> NativeSynthCorpus:
+    """make_corpus's distributions, generated natively (csrc/bm_synth.cpp) per
+    document from a stream keyed by (seed, ids[q]): a shard of a corpus is
+    generated on its own and holds the same documents as the whole corpus."""
+    import ctypes as C
+
+    from . import _native as N
+
+    lib = N.load_library()
+    g = np.ascontiguousarray(n_gold, dtype=np.int32)
+    a = np.ascontiguousarray(n_src, dtype=np.int32)
+    b = np.ascontiguousarray(n_tgt, dtype=np.int32)
+    k = g.size
+    ids = np.arange(k, dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+    spec = N.SynthSpec(int(vocab), float(noise), float(digit_rate), int(seed) & (2**64 - 1))
+    h = C.c_void_p()
+    rc = lib.bm_synth_generate(C.byref(spec), ids.ctypes.data, g.ctypes.data, a.ctypes.data,
+                               b.ctypes.data, k, int(threads), C.byref(h))
+    if rc != 0:
+        raise ValueError(f"bm_synth_generate failed ({rc})")
+    owner = _SynthHandle(lib, h.value)
+    v = N.SynthArrays()
+    lib.bm_synth_view(h, C.byref(v))
+    S, E, G, D = v.n_sent, v.n_tok_entries, v.n_dig_entries, v.n_docs
+    i32 = np.int32
+    packed = PackedCorpus(
+        n_tok=_view(owner, v.n_tok, S, i32), n_punct=_view(owner, v.n_punct, S, i32),
+        n_alpha=_view(owner, v.n_alpha, S, i32), tok_off=_view(owner, v.tok_off, S + 1, i32),
+        tok_id=_view(owner, v.tok_id, E, i32), tok_alpha=_view(owner, v.tok_alpha, E, np.uint32),
+        dig_off=_view(owner, v.dig_off, S + 1, i32), dig_id=_view(owner, v.dig_id, G, i32),
+        src0=_view(owner, v.src0, D, i32), n=_view(owner, v.n, D, i32),
+        tgt0=_view(owner, v.tgt0, D, i32), m=_view(owner, v.m, D, i32),
+    )
+    return NativeSynthCorpus(SynthWorld(vocab), packed, _view(owner, v.gold_off, D + 1, np.int64),
+                             _view(owner, v.gold_i, v.n_gold, i32),
+                             _view(owner, v.gold_j, v.n_gold, i32))

@@ -15,8 +15,8 @@ from paper_1509_08639_b200 import _native
 HEADER = os.path.join(ROOT, "include", "bimine_b200.h")
 
 
-def declared_symbols():
-    text = open(HEADER).read()
+def declared_symbols(header=HEADER):
+    text = open(header).read()
     return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(bm_\w+)\s*\(", text, flags=re.M)))
 
 
@@ -39,10 +39,14 @@ def test_library_exports_every_declared_symbol(lib):
     for name in declared_symbols():
         assert hasattr(lib, name), name
     assert set(declared_symbols()) == set(_native.EXPORTED)
+    synth_h = os.path.join(ROOT, "include", "bimine_synth.h")
+    for name in declared_symbols(synth_h):
+        assert hasattr(lib, name), name
+    assert set(declared_symbols(synth_h)) == set(_native.SYNTH_SIGS)
 
 
 def test_abi_version_and_record_layout(lib):
-    assert lib.bm_abi_version() == 1
+    assert lib.bm_abi_version() == 2
     assert ctypes.sizeof(_native.Record) == 24
     assert np.dtype(_native.RECORD_DTYPE).itemsize == 24
     assert lib.bm_dirs_words(128, 4) == 32
