@@ -127,6 +127,59 @@ class Scratch {
   std::vector<void*> ptrs_;
 };
 
+// Grow-only device workspaces for the large per-call scratch (similarity
+// matrices, hit counts, direction codes, boundary rows), one set per stream of
+// the calling thread: work on one stream is ordered, so a buffer is reused by
+// the next group or chunk on that stream without a free / malloc round trip
+// (pool growth between calls cost tens of milliseconds on C3), and a buffer
+// that must grow is released stream-ordered on its own stream.
+enum WsSlot { kWsS, kWsDirs, kWsBnd, kWsHits, kWsHits16, kWsSlots };
+struct Workspace {
+  cudaStream_t st;
+  int dev;
+  void* buf[kWsSlots];
+  size_t cap[kWsSlots];
+};
+
+template <class T>
+cudaError_t ws_get(cudaStream_t st, WsSlot slot, T** out, size_t count) {
+  static thread_local std::vector<Workspace> spaces;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  Workspace* w = nullptr;
+  for (Workspace& x : spaces)
+    if (x.st == st && x.dev == dev) w = &x;
+  if (w == nullptr) {
+    if (spaces.size() >= 16) {  // bounded: release the oldest stream's set
+      int cur = dev;
+      Workspace& old = spaces.front();
+      cudaSetDevice(old.dev);
+      for (int k = 0; k < kWsSlots; ++k)
+        if (old.buf[k]) cudaFreeAsync(old.buf[k], old.st);
+      cudaSetDevice(cur);
+      spaces.erase(spaces.begin());
+    }
+    Workspace fresh{};
+    fresh.st = st;
+    fresh.dev = dev;
+    spaces.push_back(fresh);
+    w = &spaces.back();
+  }
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  if (w->cap[slot] < bytes) {
+    if (w->buf[slot]) cudaFreeAsync(w->buf[slot], st);
+    w->buf[slot] = nullptr;
+    w->cap[slot] = 0;
+    const size_t grow = bytes + bytes / 8;  // headroom: groups differ slightly in size
+    e = cudaMallocAsync(&w->buf[slot], grow, st);
+    if (e != cudaSuccess) return e;
+    w->cap[slot] = grow;
+  }
+  *out = (T*)w->buf[slot];
+  return cudaSuccess;
+}
+
 void note_launch() { bm::g_launches += 1; }
 
 Model to_model(const bm_model* m) {
@@ -220,9 +273,9 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
   BM_CK(sc.upload(&dv.items, g.items), "upload");
   BM_CK(sc.alloc(&dv.src0, k), "alloc");
   BM_CK(sc.alloc(&dv.tgt0, k), "alloc");
-  BM_CK(sc.alloc(&dv.S, (size_t)g.s_total), "alloc S");
-  BM_CK(sc.alloc(&dv.dirs, (size_t)g.dir_total), "alloc dirs");
-  BM_CK(sc.alloc(&dv.bnd, (size_t)g.bnd_total), "alloc boundary");
+  BM_CK(ws_get(st, kWsS, &dv.S, (size_t)g.s_total), "alloc S");
+  BM_CK(ws_get(st, kWsDirs, &dv.dirs, (size_t)g.dir_total), "alloc dirs");
+  BM_CK(ws_get(st, kWsBnd, &dv.bnd, (size_t)g.bnd_total), "alloc boundary");
   BM_CK(sc.alloc(&dv.ticket, 1), "alloc ticket");
   gather_docs_kernel<<<(k + 255) / 256, 256, 0, st>>>(*docs, idx, k, dv.src0, dv.tgt0);
   BM_CK(cudaGetLastError(), "gather_docs");
@@ -316,7 +369,7 @@ int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs&
   uint32_t* hits = nullptr;
   int64_t* dho = nullptr;
   int4* dit = nullptr;
-  BM_CK(sc.alloc(&hits, (size_t)ht), "alloc hits");
+  BM_CK(ws_get(st, kWsHits, &hits, (size_t)ht), "alloc hits");
   BM_CK(cudaMemsetAsync(hits, 0, (size_t)ht * 4, st), "memset hits");
   BM_CK(sc.upload(&dho, hoff), "upload");
   BM_CK(sc.upload(&dit, items), "upload");
@@ -500,6 +553,22 @@ int bm_select(const double* S, int64_t pitch, const int32_t* ci, const int32_t* 
   return BM_OK;
 }
 
+// Extra compute streams of the calling thread: bm_mine_host deals chunks
+// round-robin over the caller's stream and these, so a chunk's kernel tails
+// overlap the next chunks' kernels.
+static cudaStream_t side_stream(int q) {
+  static thread_local cudaStream_t s[kMaxMineStreams] = {};
+  static thread_local int dev_of = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev_of != dev) {
+    for (auto& x : s) x = nullptr;
+    dev_of = dev;
+  }
+  if (s[q] == nullptr) cudaStreamCreateWithFlags(&s[q], cudaStreamNonBlocking);
+  return s[q];
+}
+
 // Documents per bm_mine group: consecutive documents up to this many cells
 // share one routing pass and one set of scratch buffers (2 B/cell of hit
 // counts for the fused tier, 4 + 8 B/cell for the banded tier), freed
@@ -510,11 +579,14 @@ static int64_t mine_group_cells() {
   return std::max<int64_t>(v, 1);
 }
 
+// One group: the fused tier's kernels on stream sf, the banded tier's on sb
+// (bm_mine rotates groups over its streams, so one group's latency-bound DP
+// runs next to another's issue-bound scoring).
 static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host,
                const int32_t* m_host, const int32_t* amax_host, const bm_lexicon* lex,
                const Model& M, double threshold, double penalty, const int64_t* rec_off,
                bm_record* rec, int32_t* rec_count, double* cost, int d_lo, int d_hi,
-               HostTrace& tr, cudaStream_t st) {
+               HostTrace& tr, cudaStream_t sf, cudaStream_t sb) {
   std::vector<int32_t> fused[4];
   size_t fused_smem[4] = {0, 0, 0, 0}, hits_smem[4] = {0, 0, 0, 0};
   std::vector<int64_t> hit_off;  // per document of [d_lo, d_hi)
@@ -542,12 +614,13 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
     }
   }
   tr.mark("route");
-  Scratch sc(st);
+  Scratch sc(sf), scb(sb);
+  cudaStream_t st = sf;
   if (hit_total > 0) {
     uint8_t* hits = nullptr;
     int64_t* dho = nullptr;
     if (!BM_RING_FUSED_JOIN) {
-      BM_CK(sc.alloc(&hits, (size_t)hit_total), "alloc hits");
+      BM_CK(ws_get(st, kWsHits16, &hits, (size_t)hit_total), "alloc hits");
       BM_CK(cudaMemsetAsync(hits, 0, (size_t)hit_total, st), "memset hits");
       BM_CK(sc.upload(&dho, hit_off), "upload");
       tr.mark("alloc hits");
@@ -586,7 +659,7 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
   for (GeneralPlan* gp : {&g, &gw}) {
     if (gp->docs.empty()) continue;
     int rc = mine_general(*gp, sent, docs, lex, M, threshold, penalty, rec_off, rec, rec_count,
-                          cost, gp == &g, sc, st);
+                          cost, gp == &g, scb, sb);
     if (rc) return rc;
     tr.mark("banded tier enqueued");
   }
@@ -605,14 +678,43 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
   BM_CK(cudaMemsetAsync(rec_count, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
   const Model M = to_model(model);
   const int64_t budget = mine_group_cells();
+  // the caller's stream and two side streams take the groups' tiers in turn;
+  // every side stream starts after the memset and is joined back into st on
+  // every exit path (before the per-group scratch on it is reused)
+  cudaStream_t ss[3] = {st, side_stream(1), side_stream(2)};
+  struct Join {
+    cudaStream_t st;
+    cudaStream_t* side;
+    ~Join() {
+      for (int q = 1; q < 3; ++q) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventRecord(e, side[q]) == cudaSuccess && cudaStreamWaitEvent(st, e, 0) == cudaSuccess)
+          cudaEventDestroy(e);
+        else
+          cudaStreamSynchronize(side[q]);
+      }
+    }
+  } join{st, ss};
+  {
+    cudaEvent_t e0;
+    BM_CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming), "event");
+    BM_CK(cudaEventRecord(e0, st), "event");
+    BM_CK(cudaStreamWaitEvent(ss[1], e0, 0), "event");
+    BM_CK(cudaStreamWaitEvent(ss[2], e0, 0), "event");
+    cudaEventDestroy(e0);
+  }
+  int unit = 0;
   for (int d0 = 0; d0 < nd;) {
     int d1 = d0;
     int64_t cells = 0;
     while (d1 < nd && (d1 == d0 || cells + (int64_t)n_host[d1] * m_host[d1] <= budget))
       cells += (int64_t)n_host[d1] * m_host[d1], ++d1;
     int rc = mine_group(sent, docs, n_host, m_host, amax_host, lex, M, threshold, penalty,
-                        rec_off, rec, rec_count, cost, d0, d1, tr, st);
+                        rec_off, rec, rec_count, cost, d0, d1, tr, ss[unit % 3],
+                        ss[(unit + 1) % 3]);
     if (rc) return rc;
+    unit += 2;
     d0 = d1;
   }
   return BM_OK;
@@ -658,22 +760,6 @@ static cudaStream_t copy_stream() {
     dev_of = dev;
   }
   return s;
-}
-
-// Extra compute streams of the calling thread: bm_mine_host deals chunks
-// round-robin over the caller's stream and these, so a chunk's kernel tails
-// overlap the next chunks' kernels.
-static cudaStream_t side_stream(int q) {
-  static thread_local cudaStream_t s[kMaxMineStreams] = {};
-  static thread_local int dev_of = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev_of != dev) {
-    for (auto& x : s) x = nullptr;
-    dev_of = dev;
-  }
-  if (s[q] == nullptr) cudaStreamCreateWithFlags(&s[q], cudaStreamNonBlocking);
-  return s[q];
 }
 
 // Page-locked per-chunk record counts of the calling thread (grown on demand).

@@ -10,6 +10,8 @@
 // Everything is fp64 with explicitly rounded intrinsics (the TU is also built
 // with -fmad=false) so every value matches the reference bit for bit.
 #include <mutex>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -281,6 +283,27 @@ __global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sente
   }
 }
 
+// Digit signature of a sentence (the common digit sets in one word):
+// 0 = no digit token, id + 1 = exactly one (id >= 0), kDigMany = two or more.
+// For two sentences with at most one digit token each, the digit Jaccard
+// (classifier.py:82-87) is 1.0 when the signatures are equal (both empty, or
+// the same single token) and 0.0 otherwise, so w3 * f3 is w3 or w3 * 0.0;
+// only kDigMany needs the sorted intersection.
+constexpr uint32_t kDigMany = 0x80000000u;
+__device__ __forceinline__ uint32_t digit_sig(const bm_sentences& S, int nD, int d0) {
+  return nD == 0 ? 0u : nD == 1 ? (uint32_t)__ldg(S.dig_id + d0) + 1u : kDigMany;
+}
+
+// w3 * f3 of a cell (classifier.py:82-87, 114-116): w3z = w3 * 0.0.
+__device__ __forceinline__ double digit_term(const bm_sentences& S, const Model& M, double w3z,
+                                             uint32_t sa, uint32_t sb, int aD, int ad0, int bD,
+                                             int bd0) {
+  if (((sa | sb) & kDigMany) == 0) return sa == sb ? M.w[3] : w3z;
+  if (aD == 0 || bD == 0) return w3z;
+  const int inter = sorted_intersection(S.dig_id + ad0, aD, S.dig_id + bd0, bD);
+  return __dmul_rn(M.w[3], frac_or_zero(inter, aD + bD - inter));
+}
+
 // z of one cell from the model's folded tables (ModelTables; every count of
 // both sentences < kPairMax): the additions of margin() in its order.
 __device__ __forceinline__ double folded_margin(const bm_sentences& S, const Model& M,
@@ -308,15 +331,46 @@ __device__ __forceinline__ double folded_margin(const bm_sentences& S, const Mod
   return __dadd_rn(z, M.w[6]);  // w6 * 1.0
 }
 
+// One staged sentence of a folded tile (every count < 256): the four counts
+// in one word (T | P << 8 | |A| << 16 | |D| << 24), the digit-set offset and
+// signature, the document position; read with two 16-byte loads.
+struct __align__(16) FoldSent {
+  uint32_t tpad;
+  int d0;
+  uint32_t dsig;
+  int pad;
+  double pos;
+  double pad2;
+};
+
+// folded_margin over FoldSent fields; the column's table offsets are hoisted
+// by the caller (bT, bA, bP fixed per thread).
+__device__ __forceinline__ double fold_cell(const bm_sentences& S, const Model& M,
+                                            const ModelTables& mt, double w3z, uint32_t ta,
+                                            int ad0, uint32_t asig, double pos_s, uint32_t tb,
+                                            int bd0, uint32_t bsig, double pos_t, uint32_t hv) {
+  const uint32_t hf = hv & 0xffffu, hr = hv >> 16;
+  double z = __ldg(mt.z1 + (((ta & 0xffu) << 8) | (tb & 0xffu)));
+  z = __dadd_rn(z, __ldg(mt.p1 + ((hf << 8) | ((ta >> 16) & 0xffu))));
+  z = __dadd_rn(z, __ldg(mt.p2 + ((hr << 8) | ((tb >> 16) & 0xffu))));
+  z = __dadd_rn(z, digit_term(S, M, w3z, asig, bsig, (int)(ta >> 24), ad0, (int)(tb >> 24), bd0));
+  z = __dadd_rn(z, __ldg(mt.p4 + ((ta & 0xff00u) | ((tb >> 8) & 0xffu))));
+  z = __dadd_rn(z, __dmul_rn(M.w[5], __dsub_rn(1.0, fabs(__dsub_rn(pos_s, pos_t)))));
+  return __dadd_rn(z, M.w[6]);  // w6 * 1.0
+}
+
 __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
     const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
     const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
     double* __restrict__ out) {
+  static_assert(kPairMax == 256, "folded tables are indexed by byte fields");
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* exp_tab = (uint64_t*)smem;
   TileScalars* rows = (TileScalars*)(smem + kExpTableWords * 8);
   TileScalars* cols = rows + 1;
+  FoldSent* frows = (FoldSent*)(cols + 1);
+  FoldSent* fcols = frows + kTile;
   const int4 tile = tiles[blockIdx.x];
   const int doc = tile.x, r0 = tile.y, c0 = tile.z;
   const int n = D.n[doc], m = D.m[doc];
@@ -329,13 +383,23 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     const int local = is_row ? k : k - ns;
     SentScalars sc = load_scalars(S, is_row ? s0 + local : t0 + local);
     fits &= sc.T < kPairMax;
+    const double pos = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
     TileScalars* dst = is_row ? rows : cols;
     dst->s[local].T = sc.T;
     dst->s[local].P = sc.P;
     dst->s[local].nA = sc.nA;
     dst->s[local].nD = sc.nD;
     dst->s[local].d0 = sc.d0;
-    dst->s[local].pos = is_row ? doc_pos(r0 + local, n) : doc_pos(c0 + local, m);
+    dst->s[local].pos = pos;
+    FoldSent f;
+    f.tpad = (uint32_t)(sc.T & 0xff) | (uint32_t)(sc.P & 0xff) << 8 | (uint32_t)(sc.nA & 0xff) << 16 |
+             (uint32_t)(sc.nD & 0xff) << 24;
+    f.d0 = sc.d0;
+    f.dsig = digit_sig(S, sc.nD, sc.d0);
+    f.pad = 0;
+    f.pos = pos;
+    f.pad2 = 0.0;
+    (is_row ? frows : fcols)[local] = f;
   }
   // the folded tables cover the tile when all of its sentences fit them
   const bool small = __syncthreads_and(fits) != 0;
@@ -346,8 +410,6 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   static_assert(kTileThreads % kTile == 0, "tile rows per pass");
   const int j = threadIdx.x % kTile;
   if (j >= nt) return;
-  const SentScalars b = get_scalars(*cols, j);
-  const double pos_t = cols->s[j].pos;
   constexpr int kRowStep = kTileThreads / kTile;
   int i = threadIdx.x / kTile;
   // running row pointers (one 64-bit add per cell); the next row's hit word is
@@ -356,15 +418,28 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   double* op = dst + (int64_t)i * ld + j;
   const int64_t hstep = (int64_t)kRowStep * m, ostep = (int64_t)kRowStep * ld;
   uint32_t hv_next = i < ns ? __ldg(hp) : 0u;
-  for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
-    const uint32_t hv = hv_next;
-    if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
-    const SentScalars a = get_scalars(*rows, i);
-    *op = small ? bmexp::confidence_from_z(folded_margin(S, M, mt, a, b, (int)(hv & 0xffffu),
-                                                         (int)(hv >> 16), rows->s[i].pos, pos_t),
-                                           exp_tab)
-                : cell_score(S, M, exp_tab, a, b, (int)(hv & 0xffffu), (int)(hv >> 16),
-                             rows->s[i].pos, pos_t);
+  if (small) {
+    const FoldSent fb = fcols[j];
+    const double w3z = __dmul_rn(M.w[3], 0.0);
+    for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
+      const uint32_t hv = hv_next;
+      if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
+      const int4 fa = *reinterpret_cast<const int4*>(frows + i);
+      const double pos_s = frows[i].pos;
+      *op = bmexp::confidence_from_z(
+          fold_cell(S, M, mt, w3z, (uint32_t)fa.x, fa.y, (uint32_t)fa.z, pos_s, fb.tpad, fb.d0,
+                    fb.dsig, fb.pos, hv),
+          exp_tab);
+    }
+  } else {
+    const SentScalars b = get_scalars(*cols, j);
+    const double pos_t = cols->s[j].pos;
+    for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
+      const uint32_t hv = hv_next;
+      if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
+      *op = cell_score(S, M, exp_tab, get_scalars(*rows, i), b, (int)(hv & 0xffffu),
+                       (int)(hv >> 16), rows->s[i].pos, pos_t);
+    }
   }
 }
 
@@ -394,7 +469,7 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
                                        (int)hs);
   if (e != cudaSuccess) return e;
   if (n_items) hits_doc_kernel<<<n_items, 64, hs, st>>>(S, D, L, items, n_items, h_off, hits);
-  const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars);
+  const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars) + 2 * kTile * sizeof(FoldSent);
   score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits, h_off,
                                                        out);
   return counted(cudaGetLastError(), n_items ? 2 : 1);
@@ -534,6 +609,37 @@ __device__ __forceinline__ void nw_cell(double dg, double up, double lf, double 
   best = b;
 }
 
+// The cell with the neighbours' C + p precomputed (each cell's C + p is
+// computed once and serves as the candidate of the cell below and of the cell
+// to its right): upp = C[i-1][j] + p, lp = C[i][j-1] + p. Returns C in best
+// and C + p in vp. kFinite (p finite, so every value is finite): the minimum
+// is taken as min(min(d, u), l) -- d and u come from the row above, so along
+// a row the dependency chain is one compare-select plus the + p of the left
+// neighbour, not two compare-selects -- and the code follows from the same
+// two compares:  GT if l < min(d, u), else D if d <= u, else GS
+// -- the reference's value and tie order D > GS > GT (aligner.py:124-133,
+// 176-206). With p = inf the border costs are NaN/inf and the reference's
+// literal comparison sequence is kept.
+template <bool kFinite>
+__device__ __forceinline__ void nw_cell2(double dg, double upp, double lp, double om, double p,
+                                         double& best, double& vp, uint32_t& code) {
+  const double dcand = __dadd_rn(dg, om);
+  if (kFinite) {
+    const bool ad = dcand <= upp;
+    const double A = ad ? dcand : upp;
+    const bool gt = lp < A;
+    best = gt ? lp : A;
+    code = gt ? 2u : (ad ? 0u : 1u);
+  } else {
+    double b = dcand;
+    if (lp < b) b = lp;
+    if (upp < b) b = upp;
+    code = b == dcand ? 0u : (b == upp ? 1u : 2u);
+    best = b;
+  }
+  vp = __dadd_rn(best, p);
+}
+
 #ifdef BM_NW_PROFILE
 // tools/nw_trace.py builds a variant with per-item timestamps (globaltimer):
 // [0] ticket taken, [1] first block, [2] done, [3] boundary wait ns after the first chunk
@@ -564,7 +670,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef BM_NW_EARLY_BND
 #define BM_NW_EARLY_BND 1
 #endif
-template <int D, int NP>
+template <int D, int NP, bool kFin>
 __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
   // NP > 1 (tuner): NP penalties run over the same band in one pass. S is
@@ -721,11 +827,20 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
       cp_async_wait_depth<D>();  // block g+1 has landed
       load(g + 1, on);
 
-      // the 4x4 block of every penalty, anti-diagonal order
-      double v[NP][4][4];
+      // the 4x4 block of every penalty, anti-diagonal order; C + p of the row
+      // above and of the left column once per block, every other C + p once
+      // per cell (nw_cell2)
+      double v[NP][4][4], vp[NP][4][4], upp[NP][4], lfp[NP][4];
       uint32_t codes[NP];
 #pragma unroll
-      for (int q = 0; q < NP; ++q) codes[q] = 0;
+      for (int q = 0; q < NP; ++q) {
+        codes[q] = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          upp[q][k] = __dadd_rn(u[q][k], pq[q]);
+          lfp[q][k] = __dadd_rn(l[q][k], pq[q]);
+        }
+      }
 #pragma unroll
       for (int dd = 0; dd < 7; ++dd) {
 #pragma unroll
@@ -736,10 +851,10 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
           for (int q = 0; q < NP; ++q) {
             const double dgv = r == 0 ? (c == 0 ? dgn[q] : u[q][c - 1])
                                       : (c == 0 ? l[q][r - 1] : v[q][r - 1][c - 1]);
-            const double upv = r == 0 ? u[q][c] : v[q][r - 1][c];
-            const double lfv = c == 0 ? l[q][r] : v[q][r][c - 1];
+            const double upv = r == 0 ? upp[q][c] : vp[q][r - 1][c];
+            const double lfv = c == 0 ? lfp[q][r] : vp[q][r][c - 1];
             uint32_t kc;
-            nw_cell(dgv, upv, lfv, oc[4 * r + c], pq[q], v[q][r][c], kc);
+            nw_cell2<kFin>(dgv, upv, lfv, oc[4 * r + c], pq[q], v[q][r][c], vp[q][r][c], kc);
             codes[q] |= kc << (8 * c + 2 * r);
           }
         }
@@ -786,43 +901,57 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
   }
 }
 
-template <int D, int NP>
+template <int D, int NP, bool kFin>
 int nw_resident(int sms) {
   int per_sm = 0;
-  cudaFuncSetAttribute(nw_band_kernel<D, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(nw_band_kernel<D, NP, kFin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        nw_smem(D, NP));
-  cudaFuncSetAttribute(nw_band_kernel<D, NP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel<D, NP>, WARP, nw_smem(D, NP));
+  cudaFuncSetAttribute(nw_band_kernel<D, NP, kFin>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nw_band_kernel<D, NP, kFin>, WARP,
+                                                nw_smem(D, NP));
   return sms * std::max(per_sm, 1);
 }
 
 // Persistent grid of min(resident warps, items); a shallow ring when the items
 // outnumber the warps a deep ring allows.
-template <int NP>
+template <int NP, bool kFin>
 cudaError_t launch_nw_np(const NwArgs& a, cudaStream_t st) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static thread_local int r8 = 0, r4 = 0, dev_of = -1;
   if (dev_of != dev) {
-    r8 = nw_resident<8, NP>(sms);
-    r4 = nw_resident<4, NP>(sms);
+    r8 = nw_resident<8, NP, kFin>(sms);
+    r4 = nw_resident<4, NP, kFin>(sms);
     dev_of = dev;
   }
+  // BM_NW_WARPS_PER_SM caps the persistent grid (experiments: room for the
+  // scoring kernels of other groups next to the latency-bound DP)
+  static const int cap = getenv("BM_NW_WARPS_PER_SM") ? atoi(getenv("BM_NW_WARPS_PER_SM")) : 0;
+  const int lim4 = cap > 0 ? std::min(r4, cap * sms) : r4;
+  const int lim8 = cap > 0 ? std::min(r8, cap * sms) : r8;
   if (a.n_items > r8) {
-    nw_band_kernel<4, NP><<<std::min(r4, a.n_items), WARP, nw_smem(4, NP), st>>>(a);
+    nw_band_kernel<4, NP, kFin><<<std::min(lim4, a.n_items), WARP, nw_smem(4, NP), st>>>(a);
   } else {
-    nw_band_kernel<8, NP><<<std::min(r8, a.n_items), WARP, nw_smem(8, NP), st>>>(a);
+    nw_band_kernel<8, NP, kFin><<<std::min(lim8, a.n_items), WARP, nw_smem(8, NP), st>>>(a);
   }
   return counted(cudaGetLastError());
+}
+
+template <int NP>
+cudaError_t launch_nw_fin(const NwArgs& a, cudaStream_t st) {
+  bool fin = true;
+  for (int q = 0; q < NP; ++q) fin &= std::isfinite(NP == 1 ? a.p : a.pv[q]);
+  return fin ? launch_nw_np<NP, true>(a, st) : launch_nw_np<NP, false>(a, st);
 }
 
 cudaError_t launch_nw(const NwArgs& a, cudaStream_t st) {
   if (a.n_items == 0) return cudaSuccess;
   switch (a.np) {
-    case 1: return launch_nw_np<1>(a, st);
-    case 2: return launch_nw_np<2>(a, st);
-    case 4: return launch_nw_np<4>(a, st);
+    case 1: return launch_nw_fin<1>(a, st);
+    case 2: return launch_nw_fin<2>(a, st);
+    case 4: return launch_nw_fin<4>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }
