@@ -270,7 +270,24 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
   BM_CK(sc.upload(&dv.n, g.n), "upload");
   BM_CK(sc.upload(&dv.m, g.m), "upload");
   BM_CK(sc.upload(&dv.tiles, g.tiles), "upload");
-  BM_CK(sc.upload(&dv.items, g.items), "upload");
+  // (doc, band) work order of the banded DP. A band waits for the band above
+  // to publish its bottom row; BM_NW_STAGGER = K places band b of the q-th
+  // document at position q + b * K instead of next to band b - 1 (K = 0), so
+  // the persistent warps spend less time spinning on bands that have barely
+  // started (C3 200k: 74.0 -> 72.8 ms at K = 512). Band b - 1 always
+  // precedes band b (deadlock freedom).
+  static const int kStagger = getenv("BM_NW_STAGGER") ? atoi(getenv("BM_NW_STAGGER")) : 512;
+  if (kStagger > 0 && g.items.size() > 1) {
+    std::vector<std::pair<int64_t, int>> key(g.items.size());
+    for (size_t q = 0; q < g.items.size(); ++q)
+      key[q] = {(int64_t)g.items[q].doc + (int64_t)g.items[q].band * kStagger, (int)q};
+    std::stable_sort(key.begin(), key.end());
+    std::vector<WorkItem> items(g.items.size());
+    for (size_t q = 0; q < items.size(); ++q) items[q] = g.items[key[q].second];
+    BM_CK(sc.upload(&dv.items, items), "upload");
+  } else {
+    BM_CK(sc.upload(&dv.items, g.items), "upload");
+  }
   BM_CK(sc.alloc(&dv.src0, k), "alloc");
   BM_CK(sc.alloc(&dv.tgt0, k), "alloc");
   BM_CK(ws_get(st, kWsS, &dv.S, (size_t)g.s_total), "alloc S");
