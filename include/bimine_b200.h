@@ -313,6 +313,14 @@ typedef struct {
  * every array until bm_ingest_free. */
 int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len);
 void bm_ingest_free(void* handle);
+/* Gold set (tuner.py:157-203 load_gold_set, §8(f)-4): the same reader for
+ * document-pair JSONL whose lines also hold "gold": [[i, j], ...]. Lines with
+ * an empty side, a missing or malformed "gold", or pairs out of bounds -- where
+ * load_gold_set raises -- and empty files return BM_EUNSUPPORTED (the Python
+ * reader then raises the reference's DataError). bm_ingest_gold: per document
+ * d the ascending unique keys i * m + j at keys[off[d] .. off[d + 1]). */
+int bm_ingest_gold_jsonl(const char* path, void** handle, char* why, int32_t why_len);
+int bm_ingest_gold(void* handle, const int64_t** keys, const int64_t** off, int64_t* n_keys);
 int bm_ingest_view(void* handle, bm_ingest_arrays* out);
 int bm_ingest_doc(void* handle, int32_t k, const char** id, const char** src_lang,
                   const char** tgt_lang);

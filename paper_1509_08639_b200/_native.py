@@ -114,6 +114,9 @@ _SIGS = {
     "bm_merge_shards": (C.c_int, [_p, C.c_int64, _p, C.c_int32, C.c_int32, _p, _p, _p]),
     "bm_ingest_jsonl": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32]),
     "bm_ingest_free": (None, [C.c_void_p]),
+    "bm_ingest_gold_jsonl": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32]),
+    "bm_ingest_gold": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                 C.POINTER(C.c_int64)]),
     "bm_ingest_view": (C.c_int, [C.c_void_p, C.POINTER(IngestArrays)]),
     "bm_ingest_doc": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_char_p),
                                 C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]),

@@ -311,6 +311,12 @@ struct Ingest {
   std::vector<TokInfo> tok_info;
   std::string out;  // TSV bytes of bm_ingest_emit
   std::string err;
+  // gold sets (bm_ingest_gold_jsonl, tuner.py:157-203): per document the
+  // ascending unique keys i * m + j of its "gold" pairs
+  bool gold_mode = false;
+  pvec<int64_t> gold_keys;
+  std::vector<int64_t> gold_cnt;  // per document (merged into gold_off)
+  std::vector<int64_t> gold_off;
   std::vector<std::pair<int32_t, int32_t>> alpha_scratch;
   std::vector<int32_t> digit_scratch;
   std::string tmp;
@@ -740,6 +746,53 @@ bool parse_scalar(Json& js, std::string& out) {
   return true;
 }
 
+// A "gold" value: a list of [i, j] integer pairs. Anything else (floats,
+// booleans, nesting, numbers past int32) is left to the Python reader, which
+// raises the reference's error.
+bool parse_gold(Json& js, std::vector<std::pair<int64_t, int64_t>>& out) {
+  out.clear();
+  js.ws();
+  if (js.p >= js.e || *js.p != '[') return false;
+  ++js.p;
+  js.ws();
+  if (js.p < js.e && *js.p == ']') {
+    ++js.p;
+    return true;
+  }
+  for (;;) {
+    js.ws();
+    if (js.p >= js.e || *js.p != '[') return false;
+    ++js.p;
+    int64_t v[2];
+    for (int q = 0; q < 2; ++q) {
+      js.ws();
+      std::string t;
+      bool is_int = false;
+      if (!js.num(t, &is_int) || !is_int || t.size() > 10) return false;
+      v[q] = strtoll(t.c_str(), nullptr, 10);
+      if (v[q] < INT32_MIN || v[q] > INT32_MAX) return false;
+      js.ws();
+      if (q == 0) {
+        if (js.p >= js.e || *js.p != ',') return false;
+        ++js.p;
+      }
+    }
+    if (js.p >= js.e || *js.p != ']') return false;
+    ++js.p;
+    out.emplace_back(v[0], v[1]);
+    js.ws();
+    if (js.p < js.e && *js.p == ',') {
+      ++js.p;
+      continue;
+    }
+    if (js.p < js.e && *js.p == ']') {
+      ++js.p;
+      return true;
+    }
+    return false;
+  }
+}
+
 // The sentences of a field as (pointer, length) spans: a string is
 // segmented, a list contributes its non-blank items (corpus.py:114-121).
 void field_spans(const Field& f, std::vector<std::pair<const char*, size_t>>& out) {
@@ -764,8 +817,9 @@ int parse_line(Ingest& g, const char* b, const char* e, int64_t lineno) {
   if (js.p >= js.e || *js.p != '{') return -1;
   ++js.p;
   std::string key, id, sl, tl;
-  bool has_id = false, has_sl = false, has_tl = false;
+  bool has_id = false, has_sl = false, has_tl = false, has_gold = false;
   Field src, tgt;
+  std::vector<std::pair<int64_t, int64_t>> gold;
   js.ws();
   if (js.p < js.e && *js.p == '}') return -1;  // missing fields: Python raises
   for (;;) {
@@ -788,6 +842,9 @@ int parse_line(Ingest& g, const char* b, const char* e, int64_t lineno) {
       if (!parse_field(js, src)) return -1;
     } else if (key == "tgt") {
       if (!parse_field(js, tgt)) return -1;
+    } else if (g.gold_mode && key == "gold") {
+      if (!parse_gold(js, gold)) return -1;
+      has_gold = true;
     } else if (!js.skip()) {
       return -1;
     }
@@ -822,6 +879,21 @@ int parse_line(Ingest& g, const char* b, const char* e, int64_t lineno) {
   std::vector<std::pair<const char*, size_t>> ss, ts;
   field_spans(src, ss);
   field_spans(tgt, ts);
+  if (g.gold_mode) {
+    // load_gold_set raises for an empty side, a missing "gold" or a pair out
+    // of bounds: the Python reader reproduces the message
+    if (ss.empty() || ts.empty() || !has_gold) return -1;
+    const int64_t n = (int64_t)ss.size(), m = (int64_t)ts.size();
+    const size_t k0 = g.gold_keys.size();
+    for (auto& c : gold) {
+      if (c.first < 0 || c.first >= n || c.second < 0 || c.second >= m) return -1;
+      g.gold_keys.push_back(c.first * m + c.second);
+    }
+    std::sort(g.gold_keys.begin() + (long)k0, g.gold_keys.end());
+    g.gold_keys.resize((size_t)(std::unique(g.gold_keys.begin() + (long)k0, g.gold_keys.end()) -
+                                g.gold_keys.begin()));
+    g.gold_cnt.push_back((int64_t)(g.gold_keys.size() - k0));
+  }
   if (ss.empty() || ts.empty()) {
     // load_document_pairs skips the pair before anything is packed
     g.skipped_lines.push_back(lineno);
@@ -956,6 +1028,15 @@ void merge_parts(std::vector<Ingest*>& part) {
   G.raw_off.clear();
   G.raw_off.shrink_to_fit();
   lap("fill");
+  if (G.gold_mode) {  // documents keep their order: concatenate the key lists
+    for (size_t t = 1; t < np; ++t) {
+      Ingest& L = *part[t];
+      G.gold_keys.insert(G.gold_keys.end(), L.gold_keys.begin(), L.gold_keys.end());
+      G.gold_cnt.insert(G.gold_cnt.end(), L.gold_cnt.begin(), L.gold_cnt.end());
+    }
+    G.gold_off.assign(G.gold_cnt.size() + 1, 0);
+    for (size_t k = 0; k < G.gold_cnt.size(); ++k) G.gold_off[k + 1] = G.gold_off[k] + G.gold_cnt[k];
+  }
   for (size_t t = 1; t < np; ++t) {
     Ingest& L = *part[t];
     G.skipped_lines.insert(G.skipped_lines.end(), L.skipped_lines.begin(), L.skipped_lines.end());
@@ -970,7 +1051,7 @@ using bm_ingest::Ingest;
 
 extern "C" {
 
-int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len) {
+static int ingest_impl(const char* path, bool gold, void** handle, char* why, int32_t why_len) {
   auto fail_why = [&](const char* w) {
     if (why && why_len > 0) snprintf(why, (size_t)why_len, "%s", w);
     return BM_EUNSUPPORTED;
@@ -1042,6 +1123,7 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
   std::vector<int64_t> bad(nthr, -1);
   auto work = [&](size_t t) {
     Ingest* L = new Ingest();
+    L->gold_mode = gold;
     part[t] = L;
     const char* base = data.data();
     for (size_t q = cut[t]; q < cut[t + 1]; ++q) {
@@ -1087,6 +1169,30 @@ int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len)
             std::chrono::duration<double, std::milli>(t2 - t1).count());
   }
   *handle = g;
+  return BM_OK;
+}
+
+int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len) {
+  return ingest_impl(path, false, handle, why, why_len);
+}
+
+int bm_ingest_gold_jsonl(const char* path, void** handle, char* why, int32_t why_len) {
+  const int rc = ingest_impl(path, true, handle, why, why_len);
+  if (rc == BM_OK && ((Ingest*)*handle)->docs.empty()) {  // load_gold_set raises
+    bm_ingest_free(*handle);
+    *handle = nullptr;
+    if (why && why_len > 0) snprintf(why, (size_t)why_len, "%s", "empty gold set");
+    return BM_EUNSUPPORTED;
+  }
+  return rc;
+}
+
+int bm_ingest_gold(void* h, const int64_t** keys, const int64_t** off, int64_t* n_keys) {
+  Ingest* g = (Ingest*)h;
+  if (!g->gold_mode) return BM_EINVAL;
+  *keys = g->gold_keys.data();
+  *off = g->gold_off.data();
+  *n_keys = (int64_t)g->gold_keys.size();
   return BM_OK;
 }
 

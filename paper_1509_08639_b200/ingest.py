@@ -78,18 +78,26 @@ class NativeCorpus:
             self.skipped.append((ln.value, pid.value.decode("utf-8"), psl.value.decode("utf-8")))
 
     @classmethod
-    def load(cls, path: str) -> "NativeCorpus | None":
-        """Ingest ``path``; None when it is outside the native subset."""
+    def load(cls, path: str, gold: bool = False) -> "NativeCorpus | None":
+        """Ingest ``path`` (a gold set when ``gold``); None when it is outside
+        the native subset or would make the Python reader raise."""
         lib = N.load_library()
         h = C.c_void_p()
         why = C.create_string_buffer(256)
-        rc = lib.bm_ingest_jsonl(path.encode(), C.byref(h), why, len(why))
+        fn = lib.bm_ingest_gold_jsonl if gold else lib.bm_ingest_jsonl
+        rc = fn(path.encode(), C.byref(h), why, len(why))
         if rc == N.BM_EUNSUPPORTED:
             log.info("native ingest declined %s (%s); using the Python reader", path,
                      why.value.decode("ascii", "replace"))
             return None
         N.check(rc)
-        return cls(h.value)
+        out = cls(h.value)
+        if gold:
+            keys, off, nk = C.c_void_p(), C.c_void_p(), C.c_int64()
+            N.check(lib.bm_ingest_gold(out._h, C.byref(keys), C.byref(off), C.byref(nk)))
+            out.gold_off = _view(off.value, np.int64, out.packed.n_docs + 1)
+            out.gold_keys = _view(keys.value, np.int64, nk.value)
+        return out
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -125,3 +125,42 @@ def merge_shards_device(parts, lens, n_docs: int):
     N.check(lib.bm_merge_shards(engine._ptr(parts), stride, engine._ptr(lens), world, int(n_docs),
                                 engine._ptr(out), engine._ptr(total), engine.stream_ptr()))
     return out[: int(total.item()) * RECORD_DTYPE.itemsize]
+
+
+def reduce_tune_counts(pred, hit, group=None):
+    """Sum every rank's per-grid-point (pred, hit) counts (tuner.py:134-145 over
+    a dev set split into shards): one all_reduce of a [2, n_pen, n_thr] int64
+    tensor -- over NCCL for CUDA tensors, gloo for CPU ones. Returns the summed
+    (pred, hit) as numpy arrays on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    both = torch.stack([torch.as_tensor(pred), torch.as_tensor(hit)]).to(torch.int64)
+    if isinstance(pred, torch.Tensor) and pred.is_cuda:
+        both = both.to(pred.device)
+    dist.all_reduce(both, op=dist.ReduceOp.SUM, group=group)
+    out = both.cpu().numpy()
+    return out[0], out[1]
+
+
+def tune_shard(corpus, plex, model, penalties, thresholds, gold_keys, rank: int, world: int,
+               group=None):
+    """This rank's LPT shard of a dev set through bm_tune, then the counts of all
+    ranks summed (reduce_tune_counts over NCCL): every rank returns the whole
+    dev set's (pred, hit)."""
+    from . import engine
+
+    idx = lpt_shards(corpus.n, corpus.m, world)[rank]
+    dev = engine.device()
+    import torch
+
+    if idx.size:
+        dc = engine.DeviceCorpus.upload(corpus)
+        dl = engine.DeviceLexicon.upload(plex)
+        view = engine.DocView.of(corpus, idx)
+        gold = engine.DeviceGold.of([gold_keys[d] for d in idx])
+        pred, hit = engine.tune_counts_device(dc, dl, view, model, penalties, thresholds, gold)
+    else:
+        pred = torch.zeros((len(penalties), len(thresholds)), dtype=torch.int64, device=dev)
+        hit = torch.zeros_like(pred)
+    return reduce_tune_counts(pred, hit, group)

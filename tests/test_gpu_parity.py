@@ -530,6 +530,49 @@ def test_tune_matches_reference(world500, docs, tfile, k, grid):
     assert bm.tune_result_to_json(got) == open(golden(tfile)).read()
 
 
+@pytest.mark.parametrize("docs,tfile,k,grid", [
+    ("docs40.jsonl", "tune10.json", 10, None),
+    ("docs10_noisy.jsonl", "tune_noisy.json", 10, None),
+    ("docs10_noisy.jsonl", "tune_noisy_small.json", 3, ([0.3, 0.6], [0.1, 0.4])),
+])
+def test_tune_file_native_gold_path(world500, tmp_path, docs, tfile, k, grid):
+    """tune_file == tune(load_gold_set(path)) with the gold set read and its keys
+    packed natively: the reference's trace bytes."""
+    from paper_1509_08639_b200.ingest import NativeCorpus
+
+    lex, fwd, _ = world500
+    path = str(tmp_path / "gold.jsonl")
+    with open(path, "w") as fh:
+        for d in load_docs(docs)[:k]:
+            fh.write(json.dumps(d) + "\n")
+    assert NativeCorpus.load(path, gold=True) is not None
+    kw = {} if grid is None else {"thresholds": grid[0], "penalties": grid[1]}
+    got = bm.tune_file(path, fwd, lex, **kw)
+    assert bm.tune_result_to_json(got) == open(golden(tfile)).read()
+
+
+def test_tune_file_errors_match_load_gold_set(world500, tmp_path):
+    """Files the reference rejects take the Python path and raise its errors."""
+    lex, fwd, _ = world500
+    good = load_docs("docs10_noisy.jsonl")[:3]
+    cases = {
+        "bounds": [dict(good[0], gold=[[0, 0], [999, 1]])],
+        "missing": [{k: v for k, v in good[0].items() if k != "gold"}],
+        "entries": [dict(good[0], gold=[[0, 1.5]])],
+        "empty": [dict(good[0], tgt=[])],
+    }
+    for name, docs in cases.items():
+        path = str(tmp_path / f"{name}.jsonl")
+        with open(path, "w") as fh:
+            for d in docs:
+                fh.write(json.dumps(d) + "\n")
+        with pytest.raises(bm.DataError) as a:
+            bm.load_gold_set(path)
+        with pytest.raises(bm.DataError) as b:
+            bm.tune_file(path, fwd, lex)
+        assert str(a.value) == str(b.value)
+
+
 def test_tune_synthetic_vs_oracle(oracle_mod):
     from paper_1509_08639_b200 import engine, synth
 

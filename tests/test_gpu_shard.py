@@ -55,3 +55,28 @@ def test_sharded_mining_merges_to_the_single_gpu_stream(oracle_mod, world):
     got = merged[np.isin(merged["doc"], idx)].copy()
     got["doc"] = np.searchsorted(idx, got["doc"])
     assert got.tobytes() == want.tobytes()
+
+
+def test_sharded_tune_counts_sum_to_the_whole(oracle_mod):
+    """C5 across ranks: bm_tune on every LPT shard, counts summed (what the
+    NCCL all_reduce of shard.reduce_tune_counts adds up) == one pass."""
+    from paper_1509_08639_b200 import engine, shard, synth
+
+    sc = synth.make_corpus_native(*synth.c2_shape(600), seed=5)
+    c = sc.packed
+    keys = sc.gold_keys()
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    dc = engine.DeviceCorpus.upload(c)
+    dl = engine.DeviceLexicon.upload(plex)
+    pens, thrs = [0.05, 0.2, 0.4, 1.6], [0.2, 0.5, 0.8]
+    whole = engine.tune_counts(dc, dl, engine.DocView.of(c), model, pens, thrs, keys)
+    tot = [np.zeros_like(whole[0]), np.zeros_like(whole[1])]
+    for idx in shard.lpt_shards(c.n, c.m, 3):
+        p, h = engine.tune_counts(dc, dl, engine.DocView.of(c, idx), model, pens, thrs,
+                                  [keys[d] for d in idx])
+        tot[0] += p
+        tot[1] += h
+    assert np.array_equal(tot[0], whole[0]) and np.array_equal(tot[1], whole[1])
+    wp, wh = oracle_mod.tune(oracle_mod.HostBatch(c, plex), model, pens, thrs, keys, threads=8)
+    assert np.array_equal(whole[0], wp) and np.array_equal(whole[1], wh)

@@ -395,3 +395,34 @@ def test_ingest_empty_and_missing_files(tmp_path):
     assert nc is not None and nc.packed.n_docs == 0
     # the Python reader raises the reference's error for a missing file
     assert NativeCorpus.load(str(tmp_path / "missing.jsonl")) is None
+
+
+def test_native_gold_set_keys(tmp_path):
+    """bm_ingest_gold_jsonl: per-document ascending unique keys i * m + j equal
+    to load_gold_set's cells; files load_gold_set rejects are declined."""
+    import json
+
+    from conftest import golden, load_docs
+    from paper_1509_08639_b200.ingest import NativeCorpus
+
+    docs = load_docs("docs10_noisy.jsonl")
+    docs[1]["gold"] = docs[1]["gold"] + docs[1]["gold"][:2]  # duplicates: a set
+    path = str(tmp_path / "gold.jsonl")
+    with open(path, "w") as fh:
+        for d in docs:
+            fh.write(json.dumps(d) + "\n")
+    nc = NativeCorpus.load(path, gold=True)
+    assert nc is not None
+    dev = bm.load_gold_set(path)
+    for d, cells in enumerate(dev.gold):
+        m = len(dev.docs[d].target.sentences)
+        want = sorted(i * m + j for i, j in cells)
+        got = nc.gold_keys[nc.gold_off[d] : nc.gold_off[d + 1]].tolist()
+        assert got == want
+    for bad in ([dict(docs[0], gold=[[0, True]])], [dict(docs[0], gold=[[-1, 0]])],
+                [{k: v for k, v in docs[0].items() if k != "gold"}], []):
+        p = str(tmp_path / "bad.jsonl")
+        with open(p, "w") as fh:
+            for d in bad:
+                fh.write(json.dumps(d) + "\n")
+        assert NativeCorpus.load(p, gold=True) is None

@@ -82,3 +82,70 @@ def test_gather_records_world2_gloo(tmp_path):
     for d in (0, 7, 123):
         sel = got[got["doc"] == d]
         assert np.array_equal(sel["i"], np.arange(sel.size))
+
+
+def _mine_worker(rank, world, port, result_path):
+    """A rank of the multi-GPU path with the oracle standing in for its GPU:
+    generate this rank's LPT shard of one C3-shaped corpus on its own (per-
+    document streams), mine it (real records), gather to rank 0 (gloo), and
+    reduce per-grid-point tune counts."""
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    from conftest import ROOT, golden
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    from paper_1509_08639_b200 import synth
+    from paper_1509_08639_b200.classifier import load_model
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g, a, b = c3_shape(240, seed=17)
+    idx = shard.lpt_shards(g + a, g + b, world)[rank]
+    sc = synth.make_corpus_native(g[idx], a[idx], b[idx], ids=idx, seed=17)
+    model = load_model(golden("model5k_fwd.json"))
+    hb = oracle.HostBatch(sc.packed, sc.world.packed_lexicon())
+    recs, _ = oracle.mine(hb, model, 0.5, 0.2, threads=2)
+    recs = recs.copy()
+    recs["doc"] = idx[recs["doc"]]
+    out = shard.gather_records(recs)
+    pens, thrs = [0.1, 0.2, 0.8], [0.3, 0.5, 0.7]
+    pred, hit = oracle.tune(hb, model, pens, thrs, sc.gold_keys(), threads=2)
+    tp, th = shard.reduce_tune_counts(torch.from_numpy(pred), torch.from_numpy(hit))
+    if rank == 0:
+        np.save(result_path, out)
+        np.save(result_path + ".tune.npy", np.stack([tp, th]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_mining_and_tune_reduce_gloo(tmp_path, world):
+    """world ranks mine their own shards; rank 0's gathered stream and the
+    reduced tune counts equal one pass over the whole corpus."""
+    import sys
+
+    from conftest import ROOT, golden
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    from paper_1509_08639_b200 import synth
+    from paper_1509_08639_b200.classifier import load_model
+
+    path = str(tmp_path / "gathered.npy")
+    mp.spawn(_mine_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    got = np.load(path)
+    g, a, b = c3_shape(240, seed=17)
+    sc = synth.make_corpus_native(g, a, b, seed=17)
+    model = load_model(golden("model5k_fwd.json"))
+    hb = oracle.HostBatch(sc.packed, sc.world.packed_lexicon())
+    want, _ = oracle.mine(hb, model, 0.5, 0.2, threads=4)
+    assert got.tobytes() == want.tobytes() and got.size > 1000
+    pred, hit = oracle.tune(hb, model, [0.1, 0.2, 0.8], [0.3, 0.5, 0.7], sc.gold_keys(), threads=4)
+    assert np.array_equal(np.load(path + ".tune.npy"), np.stack([pred, hit]))
