@@ -279,6 +279,23 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
 int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_count,
                int32_t n_docs, bm_record* dense, int64_t* total, void* stream);
 
+/* bidirectional_merge on the device (miner.py:131-155).
+ * fwd / bwd: the two passes' compacted records (document-ordered, doc = batch
+ * index, (i, j) in the pass's orientation, path order). swap_f[d] / swap_b[d]:
+ * the pass read pair d swapped (its records are re-oriented and labelled
+ * "backward", miner.py:115-128). norm_key: per sentence an id of its
+ * normalized text (equal ids <=> equal texts within a document). Writes the
+ * merged records -- one per (source text, target text) key: the higher
+ * confidence, "forward" over "backward" on an exact tie, else the first seen
+ * in F-then-B order -- sorted by (document, source index, target index) in
+ * the pair's orientation, with pad = 0 (forward) / 1 (backward); *total
+ * (device) receives their number. All pointers are device pointers; out
+ * holds n_fwd + n_bwd records. */
+int bm_merge_bidir(const bm_record* fwd, int64_t n_fwd, const bm_record* bwd, int64_t n_bwd,
+                   int32_t n_docs, const int32_t* src0, const int32_t* tgt0,
+                   const int32_t* norm_key, const uint8_t* swap_f, const uint8_t* swap_b,
+                   bm_record* out, int64_t* total, void* stream);
+
 /* Multi-GPU result gather, rank 0 (the reference's ordered
  * pool.map, bimine/miner.py:236-245): the compacted records of `world` ranks
  * sit in a padded [world][stride] device layout with part_len[r] (device)
@@ -336,6 +353,13 @@ int bm_ingest_lexicon(void* handle, const char* const* src_words, const char* co
 int bm_ingest_emit(void* handle, const bm_record* fwd, int64_t n_fwd, const bm_record* bwd,
                    int64_t n_bwd, int32_t has_bwd, const uint8_t* swap_f, const uint8_t* swap_b,
                    const uint8_t* skip, const char** out, int64_t* out_len, int64_t* report);
+/* The same emission for records bm_merge_bidir already re-oriented and merged
+ * (pad = 0 forward / 1 backward; doc = the handle's document index). */
+int bm_ingest_emit_merged(void* handle, const bm_record* recs, int64_t n, const uint8_t* skip,
+                          const char** out, int64_t* out_len, int64_t* report);
+/* Per sentence of the handle, an id of its normalized text (equal ids <=>
+ * equal texts within one document): bm_merge_bidir's key. */
+int bm_ingest_norm_keys(void* handle, const int32_t** keys);
 
 #ifdef __cplusplus
 }

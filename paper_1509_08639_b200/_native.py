@@ -112,6 +112,8 @@ _SIGS = {
                           C.c_int32, _p]),
     "bm_compact": (C.c_int, [_p, _p, _p, C.c_int32, _p, _p, _p]),
     "bm_merge_shards": (C.c_int, [_p, C.c_int64, _p, C.c_int32, C.c_int32, _p, _p, _p]),
+    "bm_merge_bidir": (C.c_int, [_p, C.c_int64, _p, C.c_int64, C.c_int32, _p, _p, _p, _p, _p, _p,
+                                 _p, _p]),
     "bm_ingest_jsonl": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32]),
     "bm_ingest_free": (None, [C.c_void_p]),
     "bm_ingest_gold_jsonl": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int32]),
@@ -126,6 +128,9 @@ _SIGS = {
                                     C.c_int64, C.POINTER(LexiconC)]),
     "bm_ingest_emit": (C.c_int, [C.c_void_p, _p, C.c_int64, _p, C.c_int64, C.c_int32, _p, _p, _p,
                                  C.POINTER(C.c_char_p), C.POINTER(C.c_int64), _p]),
+    "bm_ingest_emit_merged": (C.c_int, [C.c_void_p, _p, C.c_int64, _p, C.POINTER(C.c_char_p),
+                                        C.POINTER(C.c_int64), _p]),
+    "bm_ingest_norm_keys": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
 }
 
 EXPORTED = tuple(_SIGS)

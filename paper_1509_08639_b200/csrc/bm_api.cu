@@ -748,6 +748,62 @@ int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_
   return BM_OK;
 }
 
+int bm_merge_bidir(const bm_record* fwd, int64_t n_fwd, const bm_record* bwd, int64_t n_bwd,
+                   int32_t n_docs, const int32_t* src0, const int32_t* tgt0,
+                   const int32_t* norm_key, const uint8_t* swap_f, const uint8_t* swap_b,
+                   bm_record* out, int64_t* total, void* stream) {
+  if (n_docs < 0 || n_fwd < 0 || n_bwd < 0) return fail(BM_EINVAL, "bad merge sizes");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_docs == 0) {
+    BM_CK(cudaMemsetAsync(total, 0, sizeof(int64_t), st), "memset");
+    return BM_OK;
+  }
+  Scratch sc(st);
+  const int64_t k = n_fwd + n_bwd;
+  MergeArgs a;
+  int64_t *f_off = nullptr, *b_off = nullptr, *out_off = nullptr, *win = nullptr, *bsum = nullptr,
+          *dense_off = nullptr;
+  uint64_t *skey = nullptr, *sconf = nullptr;
+  uint32_t *srank = nullptr, *rslot = nullptr;
+  bm_record* tmp = nullptr;
+  int32_t* cnt = nullptr;
+  BM_CK(sc.alloc(&f_off, (size_t)n_docs + 1), "alloc");
+  BM_CK(sc.alloc(&b_off, (size_t)n_docs + 1), "alloc");
+  BM_CK(sc.alloc(&out_off, (size_t)n_docs), "alloc");
+  BM_CK(sc.alloc(&skey, 4 * (size_t)k), "alloc");
+  BM_CK(sc.alloc(&sconf, 4 * (size_t)k), "alloc");
+  BM_CK(sc.alloc(&srank, 4 * (size_t)k), "alloc");
+  BM_CK(sc.alloc(&rslot, (size_t)k), "alloc");
+  BM_CK(sc.alloc(&win, (size_t)k), "alloc");
+  BM_CK(sc.alloc(&tmp, (size_t)k), "alloc");
+  BM_CK(sc.alloc(&cnt, (size_t)n_docs), "alloc");
+  BM_CK(sc.alloc(&dense_off, (size_t)n_docs), "alloc");
+  BM_CK(sc.alloc(&bsum, scan_scratch_count(n_docs)), "alloc");
+  BM_CK(launch_doc_offsets(fwd, n_fwd, n_docs, f_off, st), "doc_offsets");
+  BM_CK(launch_doc_offsets(bwd, n_bwd, n_docs, b_off, st), "doc_offsets");
+  a.fwd = fwd;
+  a.bwd = bwd;
+  a.f_off = f_off;
+  a.b_off = b_off;
+  a.src0 = src0;
+  a.tgt0 = tgt0;
+  a.norm_key = norm_key;
+  a.swap_f = swap_f;
+  a.swap_b = swap_b;
+  a.n_docs = n_docs;
+  a.slot_key = skey;
+  a.slot_conf = sconf;
+  a.slot_rank = srank;
+  a.rec_slot = rslot;
+  a.win_ij = win;
+  a.out = tmp;
+  a.out_cnt = cnt;
+  a.out_off = out_off;
+  BM_CK(launch_merge_bidir(a, st), "merge_bidir_kernel");
+  BM_CK(launch_compact(tmp, out_off, cnt, n_docs, dense_off, total, out, bsum, st), "compact");
+  return BM_OK;
+}
+
 int bm_merge_shards(const bm_record* rec, int64_t stride, const int64_t* part_len, int32_t world,
                     int32_t n_docs, bm_record* out, int64_t* total, void* stream) {
   if (world < 1 || stride < 0 || n_docs < 0) return fail(BM_EINVAL, "bad shard layout");

@@ -1288,9 +1288,12 @@ int bm_ingest_lexicon(void* h, const char* const* src_words, const char* const* 
 // swap_f/swap_b: per-doc orientation flags; skip: per-doc 1 = not mined
 // (ResourceLimitError), its records are absent. Counts go to report[0..5]:
 // pairs, forward, backward, unique src tokens, unique tgt tokens, docs mined.
-int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record* bwd,
-                   int64_t n_bwd, int32_t has_bwd, const uint8_t* swap_f, const uint8_t* swap_b,
-                   const uint8_t* skip, const char** out, int64_t* out_len, int64_t* report) {
+// merged: fwd holds records already oriented and merged (bm_merge_bidir: pad =
+// 0 forward / 1 backward, (i, j) in the pair's own orientation).
+static int emit_impl(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record* bwd,
+                     int64_t n_bwd, int32_t has_bwd, const uint8_t* swap_f, const uint8_t* swap_b,
+                     const uint8_t* skip, bool merged, const char** out, int64_t* out_len,
+                     int64_t* report) {
   Ingest* g = (Ingest*)h;
   const int32_t nd = (int32_t)g->docs.size();
   const size_t nid = g->ids.size();
@@ -1380,7 +1383,19 @@ int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record
                 (uint32_t)g->norm_key[D.tgt0 + x.tj];
         recs.push_back(x);
       };
-      for (int64_t q = f0; q < pf; ++q) take(fwd[q], swap_f[d] != 0);
+      if (merged) {
+        for (int64_t q = f0; q < pf; ++q) {
+          Rec x;
+          x.si = fwd[q].i;
+          x.tj = fwd[q].j;
+          x.conf = fwd[q].conf;
+          x.forward = fwd[q].pad == 0;
+          x.key = 0;
+          recs.push_back(x);
+        }
+      } else {
+        for (int64_t q = f0; q < pf; ++q) take(fwd[q], swap_f[d] != 0);
+      }
       const std::vector<Rec>* emit = &recs;
       if (has_bwd) {
         for (int64_t q = b0; q < pb; ++q) take(bwd[q], swap_b[d] != 0);
@@ -1464,6 +1479,23 @@ int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record
   report[3] = n_src_tok;
   report[4] = n_tgt_tok;
   report[5] = mined;
+  return BM_OK;
+}
+
+int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record* bwd,
+                   int64_t n_bwd, int32_t has_bwd, const uint8_t* swap_f, const uint8_t* swap_b,
+                   const uint8_t* skip, const char** out, int64_t* out_len, int64_t* report) {
+  return emit_impl(h, fwd, n_fwd, bwd, n_bwd, has_bwd, swap_f, swap_b, skip, false, out, out_len,
+                   report);
+}
+
+int bm_ingest_emit_merged(void* h, const bm_record* recs, int64_t n, const uint8_t* skip,
+                          const char** out, int64_t* out_len, int64_t* report) {
+  return emit_impl(h, recs, n, nullptr, 0, 0, nullptr, nullptr, skip, true, out, out_len, report);
+}
+
+int bm_ingest_norm_keys(void* h, const int32_t** keys) {
+  *keys = ((Ingest*)h)->norm_key.data();
   return BM_OK;
 }
 

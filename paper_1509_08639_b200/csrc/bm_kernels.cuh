@@ -141,6 +141,10 @@ cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int
 cudaError_t launch_scan_counts(const int32_t* cnt, int n, int64_t* off, int64_t* total,
                                int64_t* bsum, cudaStream_t st);
 size_t scan_scratch_count(int n);
+struct MergeArgs;
+cudaError_t launch_merge_bidir(const MergeArgs& a, cudaStream_t st);
+cudaError_t launch_doc_offsets(const bm_record* r, int64_t n, int n_docs, int64_t* off,
+                               cudaStream_t st);
 cudaError_t launch_merge_shards(const bm_record* rec, int64_t stride, const int64_t* len, int world,
                                 int n_docs, int32_t* counts, int64_t* src_start, int64_t* goff,
                                 int64_t* total, int64_t* bsum, bm_record* out, cudaStream_t st);

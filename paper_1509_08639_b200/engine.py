@@ -58,6 +58,8 @@ def to_host(t) -> np.ndarray:
 def to_dev(a: np.ndarray, dev):
     torch = torch_mod()
     a = np.ascontiguousarray(a)
+    if not a.flags.writeable:  # views of native buffers: torch wants writable memory
+        a = a.copy()
     if a.dtype == np.uint16:  # move unsigned arrays as raw bytes of the signed type
         t = torch.from_numpy(a.view(np.int16))
     elif a.dtype == np.uint32:
@@ -251,6 +253,55 @@ def record_offsets(n: np.ndarray, m: np.ndarray) -> np.ndarray:
     if len(n) > 1:
         off[1:] = np.cumsum(cap)[:-1]
     return off
+
+
+def mine_device(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, threshold: float,
+                penalty: float):
+    """Mining of every doc of the view, records left on the device:
+    (dense records uint8 tensor, record count, cost tensor)."""
+    torch = torch_mod()
+    lib = N.lib()
+    dev = device()
+    docs, lex, n, m = view.docs, dl.lex, view.n, view.m
+    k = len(n)
+    rec_off = record_offsets(n, m)
+    cap = int(np.minimum(n, m).clip(min=0).sum())
+    rec = torch.empty(max(cap, 1) * 24, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(max(k, 1), dtype=torch.int32, device=dev)
+    cost = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
+    rec_off_d = to_dev(rec_off, dev)
+    amax = dc.doc_token_max(view)
+    n_h, m_h, a_h = _i32(n), _i32(m), _i32(amax)
+    N.check(lib.bm_mine(C.byref(dc.sent), C.byref(docs), n_h.ctypes.data, m_h.ctypes.data,
+                        a_h.ctypes.data, C.byref(lex), C.byref(N.model_struct(model)),
+                        float(threshold), float(penalty), _ptr(rec_off_d), _ptr(rec), _ptr(cnt),
+                        _ptr(cost), stream_ptr()))
+    dense = torch.empty(max(cap, 1) * 24, dtype=torch.uint8, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    N.check(lib.bm_compact(_ptr(rec), _ptr(rec_off_d), _ptr(cnt), k, _ptr(dense), _ptr(total),
+                           stream_ptr()))
+    return dense, int(total.item()), cost[:k]
+
+
+def merge_bidir(fwd, n_fwd: int, bwd, n_bwd: int, src0, tgt0, norm_key, swap_f, swap_b):
+    """bidirectional_merge on the device (bm_merge_bidir) of two passes' dense
+    records over the same documents: host records in (document, source index,
+    target index) order in the pairs' own orientation, pad = 0 forward /
+    1 backward."""
+    torch = torch_mod()
+    lib = N.lib()
+    dev = device()
+    k = len(src0)
+    s0, t0 = to_dev(_i32(src0), dev), to_dev(_i32(tgt0), dev)
+    sf = to_dev(np.ascontiguousarray(swap_f, dtype=np.uint8), dev)
+    sb = to_dev(np.ascontiguousarray(swap_b, dtype=np.uint8), dev)
+    out = torch.empty(max(n_fwd + n_bwd, 1) * 24, dtype=torch.uint8, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    N.check(lib.bm_merge_bidir(_ptr(fwd), n_fwd, _ptr(bwd), n_bwd, k, _ptr(s0), _ptr(t0),
+                               _ptr(norm_key), _ptr(sf), _ptr(sb), _ptr(out), _ptr(total),
+                               stream_ptr()))
+    tot = int(total.item())
+    return to_host(out[: tot * 24]).view(np.dtype(N.RECORD_DTYPE))
 
 
 def mine(dc: DeviceCorpus, dl: DeviceLexicon, view: DocView, model, threshold: float,

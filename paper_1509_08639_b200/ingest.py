@@ -128,6 +128,25 @@ class NativeCorpus:
                              _view(out.rev_off, np.int32, nid + 1).copy(),
                              _view(out.rev_cand, np.int32, nr).copy())
 
+    def norm_keys(self) -> np.ndarray:
+        """Per sentence, an id of its normalized text (bm_merge_bidir's key)."""
+        p = C.c_void_p()
+        N.check(self._lib.bm_ingest_norm_keys(self._h, C.byref(p)))
+        return _view(p.value, np.int32, self.packed.n_sent)
+
+    def emit_merged(self, recs: np.ndarray, skip: np.ndarray) -> tuple[bytes, list[int]]:
+        """TSV bytes + report of device-merged records (bm_ingest_emit_merged)."""
+        recs = np.ascontiguousarray(recs)
+        sk = np.ascontiguousarray(skip, dtype=np.uint8)
+        out = C.c_char_p()
+        olen = C.c_int64()
+        rep = np.zeros(6, dtype=np.int64)
+        N.check(self._lib.bm_ingest_emit_merged(self._h, recs.ctypes.data, recs.shape[0],
+                                                sk.ctypes.data, C.byref(out), C.byref(olen),
+                                                rep.ctypes.data))
+        data = C.string_at(out, olen.value) if olen.value else b""
+        return data, rep.tolist()
+
     def emit(self, fwd: np.ndarray, bwd: np.ndarray | None, swap_f: np.ndarray,
              swap_b: np.ndarray, skip: np.ndarray) -> tuple[bytes, list[int]]:
         fwd = np.ascontiguousarray(fwd)
@@ -222,17 +241,27 @@ def mine_corpus_file(
         def run(model, pl, swapped):
             dl = engine.DeviceLexicon.upload(pl)
             view = engine.DocView.of(c, idx, [bool(x) for x in swapped[work]])
-            recs, _ = engine.mine(dc, dl, view, model, cfg.params.threshold, cfg.params.penalty)
-            recs = recs.copy()
-            recs["doc"] = work[recs["doc"]]
-            return recs
+            return engine.mine_device(dc, dl, view, model, cfg.params.threshold,
+                                      cfg.params.penalty)
 
-        fwd = run(forward, plex, sw_f)
-        if backward is not None:
-            bwd = run(backward, plex.swapped(), sw_b)
+        f, nf, _ = run(forward, plex, sw_f)
+        if backward is None:
+            fwd = engine.to_host(f[: nf * 24]).view(rec_dtype).copy()
+            fwd["doc"] = work[fwd["doc"]]
+        else:
+            # bidirectional_merge on the device (bm_merge_bidir), keyed on the
+            # native reader's normalized-text ids
+            b, nb, _ = run(backward, plex.swapped(), sw_b)
+            merged = engine.merge_bidir(f, nf, b, nb, c.src0[work], c.tgt0[work],
+                                        engine.to_dev(nc.norm_keys(), engine.device()),
+                                        sw_f[work], sw_b[work]).copy()
+            merged["doc"] = work[merged["doc"]]
     t1 = time.perf_counter()
     LAST_TIMINGS["mine"] = t1 - t0 - LAST_TIMINGS.get("lexicon", 0.0)
-    data, rep = nc.emit(fwd, bwd, sw_f, sw_b, skip)
+    if backward is not None and work.size:
+        data, rep = nc.emit_merged(merged, skip)
+    else:
+        data, rep = nc.emit(fwd, bwd, sw_f, sw_b, skip)
     t2 = time.perf_counter()
     out.write(data.decode("utf-8"))
     LAST_TIMINGS["emit"] = t2 - t1

@@ -132,6 +132,24 @@ class _Pass:
                                   self.cfg.params.threshold, self.cfg.params.penalty)
         return recs
 
+    def run_device(self, idx: list[int], swapped: list[bool]):
+        """The pass's records left on the device: (dense tensor, count)."""
+        from . import engine
+
+        view = engine.DocView.of(self.corpus, idx, swapped)
+        dense, k, _cost = engine.mine_device(self.dc, self.dl, view, self.model,
+                                             self.cfg.params.threshold, self.cfg.params.penalty)
+        return dense, k
+
+
+def _merged_to_pairs(pair: DocumentPair, recs) -> list[MinedPair]:
+    """Device-merged records (pair orientation, pad = 1 for backward) ->
+    MinedPair objects (miner.py:115-128 labels)."""
+    src, tgt = pair.source.sentences, pair.target.sentences
+    return [MinedPair(src[i], tgt[j], c, pair.id, "backward" if b else "forward", i, j)
+            for i, j, c, b in zip(recs["i"].tolist(), recs["j"].tolist(), recs["conf"].tolist(),
+                                  recs["pad"].tolist())]
+
 
 def _records_to_pairs(pair: DocumentPair, recs, swapped: bool) -> list[MinedPair]:
     src, tgt = pair.source.sentences, pair.target.sentences
@@ -203,15 +221,20 @@ def mine_documents(
         corpus = pk.finish()
         dc = engine.DeviceCorpus.upload(corpus)
         local = list(range(len(work)))
-        fwd = _split_by_doc(_Pass(dc, corpus, forward, lex, cfg).run(local, sw_f), len(work))
-        bwd = None
-        if backward is not None:
-            bwd = _split_by_doc(_Pass(dc, corpus, backward, rev, cfg).run(local, sw_b), len(work))
-        for q, k in enumerate(work):
-            mined = _records_to_pairs(pairs[k], fwd[q], sw_f[q])
-            if bwd is not None:
-                mined = bidirectional_merge(mined, _records_to_pairs(pairs[k], bwd[q], sw_b[q]))
-            results[k] = (mined, None)
+        if backward is None:
+            fwd = _split_by_doc(_Pass(dc, corpus, forward, lex, cfg).run(local, sw_f), len(work))
+            for q, k in enumerate(work):
+                results[k] = (_records_to_pairs(pairs[k], fwd[q], sw_f[q]), None)
+        else:
+            # both passes stay on the device; bidirectional_merge runs there
+            # too (bm_merge_bidir, keyed on the packer's normalized-text ids)
+            f, nf = _Pass(dc, corpus, forward, lex, cfg).run_device(local, sw_f)
+            b, nb = _Pass(dc, corpus, backward, rev, cfg).run_device(local, sw_b)
+            nk = engine.to_dev(corpus.norm_key, engine.device())
+            merged = engine.merge_bidir(f, nf, b, nb, corpus.src0, corpus.tgt0, nk, sw_f, sw_b)
+            by_doc = _split_by_doc(merged, len(work))
+            for q, k in enumerate(work):
+                results[k] = (_merged_to_pairs(pairs[k], by_doc[q]), None)
     return [r for r in results if r is not None], error
 
 

@@ -41,6 +41,8 @@ class PackedCorpus:
     m: np.ndarray
     strings: list[str] = field(default_factory=list)
     ids: dict[str, int] = field(default_factory=dict)
+    # per sentence: an id of its normalized text (bidirectional_merge's key)
+    norm_key: np.ndarray | None = None
 
     @property
     def n_sent(self) -> int:
@@ -91,6 +93,8 @@ class Packer:
         self._dig_off: list[int] = [0]
         self._dig_id: list[int] = []
         self._docs: list[tuple[int, int, int, int]] = []
+        self._norm: dict[str, int] = {}
+        self._norm_key: list[int] = []
 
     def intern(self, s: str) -> int:
         k = self.ids.get(s)
@@ -126,6 +130,7 @@ class Packer:
                 digits.add(did)
             punct += is_punct
         idx = len(self._T)
+        self._norm_key.append(self._norm.setdefault(sent.normalized, len(self._norm)))
         self._T.append(len(sent.tokens))
         self._P.append(punct)
         self._A.append(n_alpha)
@@ -167,6 +172,7 @@ class Packer:
             m=np.ascontiguousarray(d[:, 3]),
             strings=self.strings,
             ids=self.ids,
+            norm_key=np.asarray(self._norm_key, dtype=np.int32),
         )
 
 

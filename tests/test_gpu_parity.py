@@ -618,3 +618,61 @@ def test_sharded_mining_equals_single(oracle_mod):
     got = shard.restore_order(parts)
     want, _ = oracle_mod.mine(oracle_mod.HostBatch(sc.packed, plex), model, 0.5, 0.2, threads=8)
     assert got.tobytes() == want.tobytes()
+
+
+def test_device_bidirectional_merge_edge_cases():
+    """bm_merge_bidir against bidirectional_merge (miner.py:131-155) on random
+    paths over documents with repeated sentences (equal normalized keys),
+    confidence ties between and within directions, and swapped passes."""
+    from paper_1509_08639_b200 import engine, miner
+    from paper_1509_08639_b200.pack import Packer
+
+    rng = np.random.default_rng(77)
+    words = ["alpha", "beta", "Gamma", "gamma", "delta"]
+    pairs, fw, bw, sf, sb = [], [], [], [], []
+    for d in range(60):
+        n, m = int(rng.integers(1, 12)), int(rng.integers(1, 12))
+        src = [" ".join(rng.choice(words, 2)) + "." for _ in range(n)]
+        tgt = [" ".join(rng.choice(words, 2)) + "." for _ in range(m)]
+        pairs.append(bm.parse_document_pair({"id": f"d{d}", "src_lang": "xx", "tgt_lang": "yy",
+                                             "src": src, "tgt": tgt}, "mem", d + 1))
+        for out, swap in ((fw, sf), (bw, sb)):
+            s = bool(rng.integers(0, 2))
+            swap.append(s)
+            a, b = (m, n) if s else (n, m)  # the pass's own orientation
+            i = j = 0
+            recs = []
+            while i < a and j < b:  # a random monotone path's diagonal cells
+                if rng.random() < 0.6:
+                    c = float(rng.choice([0.5, 0.75, 0.9, rng.random()]))
+                    recs.append((d, i, j, c))
+                i += int(rng.integers(1, 3))
+                j += int(rng.integers(1, 3))
+            out.extend(recs)
+
+    def to_arr(rs):
+        a = np.zeros(len(rs), dtype=np.dtype(engine.N.RECORD_DTYPE))
+        for q, (d, i, j, c) in enumerate(rs):
+            a[q] = (d, i, j, 0, c)
+        return a
+
+    F, B = to_arr(fw), to_arr(bw)
+    pk = Packer()
+    for p in pairs:
+        pk.add_pair(p)
+    corpus = pk.finish()
+    dev = engine.device()
+    import torch
+
+    fd = torch.from_numpy(F.view(np.uint8).copy()).to(dev)
+    bd = torch.from_numpy(B.view(np.uint8).copy()).to(dev)
+    got = engine.merge_bidir(fd, len(F), bd, len(B), corpus.src0, corpus.tgt0,
+                             engine.to_dev(corpus.norm_key, dev), sf, sb)
+    by_doc = miner._split_by_doc(got, len(pairs))
+    for d, p in enumerate(pairs):
+        want = miner.bidirectional_merge(
+            miner._records_to_pairs(p, F[F["doc"] == d], sf[d]),
+            miner._records_to_pairs(p, B[B["doc"] == d], sb[d]))
+        have = miner._merged_to_pairs(p, by_doc[d])
+        assert [(r.src_index, r.tgt_index, r.confidence, r.direction) for r in have] == \
+            [(r.src_index, r.tgt_index, r.confidence, r.direction) for r in want]
