@@ -360,6 +360,14 @@ int bm_ingest_emit_merged(void* handle, const bm_record* recs, int64_t n, const 
 /* Per sentence of the handle, an id of its normalized text (equal ids <=>
  * equal texts within one document): bm_merge_bidir's key. */
 int bm_ingest_norm_keys(void* handle, const int32_t** keys);
+/* Streaming (mine_corpus_file over large files): ingest the lines of bytes
+ * [b0, b1) of the file (b0 at a line start, b1 < 0: to the end), numbering
+ * them from line0 + 1; *n_lines receives the number of lines of the range. */
+int bm_ingest_jsonl_range(const char* path, int64_t b0, int64_t b1, int64_t line0, void** handle,
+                          int64_t* n_lines, char* why, int32_t why_len);
+/* After an emit: the normalized token strings of the emitted pairs' source
+ * (which = 0) / target (1) sentences, NUL-separated (miner.py:253-260). */
+int bm_ingest_seen(void* handle, int32_t which, const char** buf, int64_t* len);
 
 #ifdef __cplusplus
 }

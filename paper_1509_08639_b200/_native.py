@@ -131,6 +131,11 @@ _SIGS = {
     "bm_ingest_emit_merged": (C.c_int, [C.c_void_p, _p, C.c_int64, _p, C.POINTER(C.c_char_p),
                                         C.POINTER(C.c_int64), _p]),
     "bm_ingest_norm_keys": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "bm_ingest_jsonl_range": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_char_p,
+                                        C.c_int32]),
+    "bm_ingest_seen": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p),
+                                 C.POINTER(C.c_int64)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -314,6 +314,8 @@ struct Ingest {
   // gold sets (bm_ingest_gold_jsonl, tuner.py:157-203): per document the
   // ascending unique keys i * m + j of its "gold" pairs
   bool gold_mode = false;
+  int64_t n_lines = 0;                 // lines of the ingested byte range
+  std::string seen_src, seen_tgt;      // bm_ingest_seen: NUL-separated strings
   pvec<int64_t> gold_keys;
   std::vector<int64_t> gold_cnt;  // per document (merged into gold_off)
   std::vector<int64_t> gold_off;
@@ -1051,7 +1053,9 @@ using bm_ingest::Ingest;
 
 extern "C" {
 
-static int ingest_impl(const char* path, bool gold, void** handle, char* why, int32_t why_len) {
+// [b0, b1) of the file (b1 < 0: to the end), its first line numbered line0 + 1
+static int ingest_impl(const char* path, bool gold, int64_t b0, int64_t b1, int64_t line0,
+                       void** handle, char* why, int32_t why_len) {
   auto fail_why = [&](const char* w) {
     if (why && why_len > 0) snprintf(why, (size_t)why_len, "%s", w);
     return BM_EUNSUPPORTED;
@@ -1079,12 +1083,15 @@ static int ingest_impl(const char* path, bool gold, void** handle, char* why, in
       if (p) munmap(p, n);
     }
   } unmap{fsize ? map : nullptr, fsize};
+  if (b0 < 0 || (size_t)b0 > fsize) return fail_why("bad byte range");
+  const size_t end = (b1 < 0 || (size_t)b1 > fsize) ? fsize : (size_t)b1;
+  if ((size_t)b0 > end) return fail_why("bad byte range");
   const struct {
     const char* p;
     size_t n;
     const char* data() const { return p; }
     size_t size() const { return n; }
-  } data{fsize ? (const char*)map : "", fsize};
+  } data{fsize ? (const char*)map + b0 : "", end - (size_t)b0};
   if (!bm_ingest::valid_utf8(data.data(), data.size())) return fail_why("not valid UTF-8");
   // lines: text-mode splitting, \n, \r\n and \r end a line
   struct Line {
@@ -1132,8 +1139,8 @@ static int ingest_impl(const char* path, bool gold, void** handle, char* why, in
       bool blank = true;
       for (size_t i = 0; i < (size_t)(e - b) && blank;) blank = bm_ingest::is_space(bm_ingest::decode(b, i));
       if (blank) continue;
-      if (bm_ingest::parse_line(*L, b, e, (int64_t)q + 1) < 0) {
-        bad[t] = (int64_t)q + 1;
+      if (bm_ingest::parse_line(*L, b, e, line0 + (int64_t)q + 1) < 0) {
+        bad[t] = line0 + (int64_t)q + 1;
         return;
       }
     }
@@ -1168,16 +1175,24 @@ static int ingest_impl(const char* path, bool gold, void** handle, char* why, in
             std::chrono::duration<double, std::milli>(t1 - t0).count(),
             std::chrono::duration<double, std::milli>(t2 - t1).count());
   }
+  g->n_lines = (int64_t)nlines;
   *handle = g;
   return BM_OK;
 }
 
 int bm_ingest_jsonl(const char* path, void** handle, char* why, int32_t why_len) {
-  return ingest_impl(path, false, handle, why, why_len);
+  return ingest_impl(path, false, 0, -1, 0, handle, why, why_len);
+}
+
+int bm_ingest_jsonl_range(const char* path, int64_t b0, int64_t b1, int64_t line0, void** handle,
+                          int64_t* n_lines, char* why, int32_t why_len) {
+  const int rc = ingest_impl(path, false, b0, b1, line0, handle, why, why_len);
+  if (rc == BM_OK) *n_lines = ((Ingest*)*handle)->n_lines;
+  return rc;
 }
 
 int bm_ingest_gold_jsonl(const char* path, void** handle, char* why, int32_t why_len) {
-  const int rc = ingest_impl(path, true, handle, why, why_len);
+  const int rc = ingest_impl(path, true, 0, -1, 0, handle, why, why_len);
   if (rc == BM_OK && ((Ingest*)*handle)->docs.empty()) {  // load_gold_set raises
     bm_ingest_free(*handle);
     *handle = nullptr;
@@ -1462,6 +1477,10 @@ static int emit_impl(void* h, const bm_record* fwd, int64_t n_fwd, const bm_reco
     nb += P.nb;
     mined += P.mined;
   }
+  g->seen_src.clear();
+  g->seen_tgt.clear();
+  std::vector<const bm_ingest::StrTable::E*> by_id(nid, nullptr);
+  for (const auto& e : g->ids.ents) by_id[(size_t)e.val] = &e;
   for (size_t id = 0; id < nid; ++id) {
     uint8_t s = 0, tg = 0;
     for (const Part& P : parts) {
@@ -1470,6 +1489,9 @@ static int emit_impl(void* h, const bm_record* fwd, int64_t n_fwd, const bm_reco
     }
     n_src_tok += s;
     n_tgt_tok += tg;
+    // the token strings themselves (streamed files: unique counts across chunks)
+    if (s) g->seen_src.append(g->ids.arena.data() + by_id[id]->off, by_id[id]->len).push_back('\0');
+    if (tg) g->seen_tgt.append(g->ids.arena.data() + by_id[id]->off, by_id[id]->len).push_back('\0');
   }
   *out = o.data();
   *out_len = (int64_t)o.size();
@@ -1492,6 +1514,14 @@ int bm_ingest_emit(void* h, const bm_record* fwd, int64_t n_fwd, const bm_record
 int bm_ingest_emit_merged(void* h, const bm_record* recs, int64_t n, const uint8_t* skip,
                           const char** out, int64_t* out_len, int64_t* report) {
   return emit_impl(h, recs, n, nullptr, 0, 0, nullptr, nullptr, skip, true, out, out_len, report);
+}
+
+int bm_ingest_seen(void* h, int32_t which, const char** buf, int64_t* len) {
+  Ingest* g = (Ingest*)h;
+  const std::string& s = which == 0 ? g->seen_src : g->seen_tgt;
+  *buf = s.data();
+  *len = (int64_t)s.size();
+  return BM_OK;
 }
 
 int bm_ingest_norm_keys(void* h, const int32_t** keys) {

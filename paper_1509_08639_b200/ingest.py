@@ -78,6 +78,25 @@ class NativeCorpus:
             self.skipped.append((ln.value, pid.value.decode("utf-8"), psl.value.decode("utf-8")))
 
     @classmethod
+    def load_range(cls, path: str, b0: int, b1: int, line0: int) -> "NativeCorpus | None":
+        """Ingest the lines of bytes [b0, b1) (numbered from line0 + 1); None
+        when they are outside the native subset."""
+        lib = N.load_library()
+        h = C.c_void_p()
+        nl = C.c_int64()
+        why = C.create_string_buffer(256)
+        rc = lib.bm_ingest_jsonl_range(path.encode(), int(b0), int(b1), int(line0), C.byref(h),
+                                       C.byref(nl), why, len(why))
+        if rc == N.BM_EUNSUPPORTED:
+            log.info("native ingest declined %s bytes [%d, %d) (%s); using the Python reader",
+                     path, b0, b1, why.value.decode("ascii", "replace"))
+            return None
+        N.check(rc)
+        out = cls(h.value)
+        out.n_lines = nl.value
+        return out
+
+    @classmethod
     def load(cls, path: str, gold: bool = False) -> "NativeCorpus | None":
         """Ingest ``path`` (a gold set when ``gold``); None when it is outside
         the native subset or would make the Python reader raise."""
@@ -127,6 +146,16 @@ class NativeCorpus:
                              _view(out.fwd_cand, np.int32, nf).copy(),
                              _view(out.rev_off, np.int32, nid + 1).copy(),
                              _view(out.rev_cand, np.int32, nr).copy())
+
+    def seen_tokens(self) -> tuple[list[str], list[str]]:
+        """Normalized token strings of the last emit's source / target sentences."""
+        out = []
+        for which in (0, 1):
+            p, n = C.c_void_p(), C.c_int64()
+            N.check(self._lib.bm_ingest_seen(self._h, which, C.byref(p), C.byref(n)))
+            raw = C.string_at(p, n.value) if n.value else b""
+            out.append(raw.decode("utf-8").split("\0")[:-1] if raw else [])
+        return out[0], out[1]
 
     def norm_keys(self) -> np.ndarray:
         """Per sentence, an id of its normalized text (bm_merge_bidir's key)."""
@@ -182,6 +211,39 @@ def _orientations(langs, model: ClassifierModel, lex: Lexicon) -> np.ndarray | N
     return out
 
 
+# streamed files: chunks of about this many bytes are ingested, mined and
+# emitted in turn (the next chunk is ingested on a host thread meanwhile)
+CHUNK_BYTES = 256 << 20
+
+
+def _chunk_cuts(path: str, chunk: int) -> list[int]:
+    """Byte offsets of line starts splitting the file into ~chunk-byte pieces
+    (cuts after a newline byte; a file without one stays whole)."""
+    import os
+
+    size = os.path.getsize(path)
+    cuts = [0]
+    with open(path, "rb") as fh:
+        pos = chunk
+        while pos < size:
+            fh.seek(pos)
+            buf = fh.read(1 << 16)
+            k = buf.find(b"\n")
+            while k < 0 and buf:
+                pos += len(buf)
+                buf = fh.read(1 << 16)
+                k = buf.find(b"\n")
+            if k < 0:
+                break
+            cut = pos + k + 1
+            if cut >= size:
+                break
+            cuts.append(cut)
+            pos = cut + chunk
+    cuts.append(size)
+    return cuts
+
+
 def mine_corpus_file(
     docs_path: str,
     forward: ClassifierModel,
@@ -192,25 +254,73 @@ def mine_corpus_file(
     on_skip: Callable[[str, str], None] | None = None,
 ):
     """``mine_corpus(load_document_pairs(docs_path, on_skip=on_skip), ...)``
-    with the native reader, lexicon lowering, merge and TSV emission."""
+    with the native reader, lexicon lowering, merge and TSV emission, streamed
+    in chunks of CHUNK_BYTES: each chunk's TSV is written before the next is
+    mined. A chunk the native path cannot reproduce exactly (see the module
+    docstring) hands the rest of the file, from its first line, to the Python
+    reader -- the output up to there is the same either way."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
     from . import aligner, engine
-    from .corpus import load_document_pairs
-    from .miner import MiningReport, mine_corpus
+    from .corpus import _iter_pairs
+    from .miner import MiningReport, _mine_stream
 
     start = time.perf_counter()
     LAST_TIMINGS.clear()
-    nc = NativeCorpus.load(docs_path)
-    LAST_TIMINGS["ingest"] = time.perf_counter() - start
-    sw_f = sw_b = None
-    if nc is not None:
-        sw_f = _orientations(nc.langs, forward, lex)
-        if backward is not None and sw_f is not None:
-            sw_b = _orientations(nc.langs, backward, lex.reversed())
-            if sw_b is None:
-                sw_f = None
-    if nc is None or sw_f is None:
-        return mine_corpus(load_document_pairs(docs_path, on_skip=on_skip), forward, backward,
-                           lex, cfg, out)
+    for k in ("ingest", "lexicon", "mine", "emit", "write"):
+        LAST_TIMINGS[k] = 0.0
+    report = MiningReport()
+    src_tok: set[str] = set()
+    tgt_tok: set[str] = set()
+    if backward is not None:
+        lex.reversed()
+    chunk = int(os.environ.get("BM_STREAM_CHUNK_BYTES", CHUNK_BYTES))
+    cuts = _chunk_cuts(docs_path, max(chunk, 1))
+    LAST_TIMINGS["chunks"] = len(cuts) - 1
+
+    def load(q: int, line0: int):
+        t = time.perf_counter()
+        nc = NativeCorpus.load_range(docs_path, cuts[q], cuts[q + 1], line0)
+        return nc, time.perf_counter() - t
+
+    def python_rest(line0: int):
+        _mine_stream(_iter_pairs(docs_path, on_skip, line0), forward, backward, lex, cfg, out,
+                     report, src_tok, tgt_tok)
+
+    def finish():
+        report.unique_src_tokens = len(src_tok)
+        report.unique_tgt_tokens = len(tgt_tok)
+        report.wall_clock_seconds = time.perf_counter() - start
+        return report
+
+    line0 = 0
+    with ThreadPoolExecutor(max_workers=1) as pool:
+        nxt = pool.submit(load, 0, 0)
+        for q in range(len(cuts) - 1):
+            nc, dt = nxt.result()
+            LAST_TIMINGS["ingest"] += dt
+            ok = nc is not None
+            if ok:
+                sw_f = _orientations(nc.langs, forward, lex)
+                sw_b = None
+                if backward is not None and sw_f is not None:
+                    sw_b = _orientations(nc.langs, backward, lex.reversed())
+                    ok = sw_b is not None
+                ok = ok and sw_f is not None
+            if not ok:
+                python_rest(line0)
+                return finish()
+            if q + 2 < len(cuts):  # the next chunk is read while this one is mined
+                nxt = pool.submit(load, q + 1, line0 + nc.n_lines)
+            _mine_chunk(nc, forward, backward, lex, cfg, out, on_skip, sw_f, sw_b, report,
+                        src_tok, tgt_tok, aligner, engine)
+            line0 += nc.n_lines
+    return finish()
+
+
+def _mine_chunk(nc, forward, backward, lex, cfg, out, on_skip, sw_f, sw_b, report, src_tok,
+                tgt_tok, aligner, engine) -> None:
     if sw_b is None:
         sw_b = np.zeros_like(sw_f)
     for _ln, pid, side in nc.skipped:
@@ -231,10 +341,11 @@ def mine_corpus_file(
     rec_dtype = np.dtype(N.RECORD_DTYPE)
     fwd = np.zeros(0, dtype=rec_dtype)
     bwd = None if backward is None else np.zeros(0, dtype=rec_dtype)
+    merged = None
     t0 = time.perf_counter()
     if work.size:
         plex = nc.lexicon(lex)
-        LAST_TIMINGS["lexicon"] = time.perf_counter() - t0
+        LAST_TIMINGS["lexicon"] += time.perf_counter() - t0
         dc = engine.DeviceCorpus.upload(c)
         idx = work.tolist()
 
@@ -257,22 +368,20 @@ def mine_corpus_file(
                                         sw_f[work], sw_b[work]).copy()
             merged["doc"] = work[merged["doc"]]
     t1 = time.perf_counter()
-    LAST_TIMINGS["mine"] = t1 - t0 - LAST_TIMINGS.get("lexicon", 0.0)
-    if backward is not None and work.size:
+    LAST_TIMINGS["mine"] += t1 - t0
+    if merged is not None:
         data, rep = nc.emit_merged(merged, skip)
     else:
         data, rep = nc.emit(fwd, bwd, sw_f, sw_b, skip)
+    src, tgt = nc.seen_tokens()
+    src_tok.update(src)
+    tgt_tok.update(tgt)
     t2 = time.perf_counter()
     out.write(data.decode("utf-8"))
-    LAST_TIMINGS["emit"] = t2 - t1
-    LAST_TIMINGS["write"] = time.perf_counter() - t2
-    report = MiningReport()
-    report.pairs_emitted = rep[0]
-    report.per_direction["forward"] = rep[1]
-    report.per_direction["backward"] = rep[2]
-    report.unique_src_tokens = rep[3]
-    report.unique_tgt_tokens = rep[4]
-    report.docs_processed = rep[5]
-    report.docs_skipped = int(skip.sum())
-    report.wall_clock_seconds = time.perf_counter() - start
-    return report
+    LAST_TIMINGS["emit"] += t2 - t1
+    LAST_TIMINGS["write"] += time.perf_counter() - t2
+    report.pairs_emitted += rep[0]
+    report.per_direction["forward"] += rep[1]
+    report.per_direction["backward"] += rep[2]
+    report.docs_processed += rep[5]
+    report.docs_skipped += int(skip.sum())

@@ -307,6 +307,18 @@ def mine_corpus(
         lex.reversed()
     src_tokens: set[str] = set()
     tgt_tokens: set[str] = set()
+    _mine_stream(doc_pairs, forward, backward, lex, cfg, out, report, src_tokens, tgt_tokens)
+    report.unique_src_tokens = len(src_tokens)
+    report.unique_tgt_tokens = len(tgt_tokens)
+    report.wall_clock_seconds = time.perf_counter() - start
+    return report
+
+
+def _mine_stream(doc_pairs, forward, backward, lex, cfg, out, report: MiningReport,
+                 src_tokens: set, tgt_tokens: set) -> None:
+    """mine_corpus's body (miner.py:212-245) accumulating into a report and
+    token sets (mine_corpus_file resumes here mid-file when a chunk needs the
+    Python reader)."""
 
     def consume(results) -> None:
         for mined, skip_reason in results:
@@ -352,11 +364,6 @@ def mine_corpus(
             batch = []
     if batch:
         flush(batch)
-
-    report.unique_src_tokens = len(src_tokens)
-    report.unique_tgt_tokens = len(tgt_tokens)
-    report.wall_clock_seconds = time.perf_counter() - start
-    return report
 
 
 def count_unique_tokens(pairs: list[MinedPair]) -> tuple[int, int]:

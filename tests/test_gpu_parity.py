@@ -676,3 +676,62 @@ def test_device_bidirectional_merge_edge_cases():
         have = miner._merged_to_pairs(p, by_doc[d])
         assert [(r.src_index, r.tgt_index, r.confidence, r.direction) for r in have] == \
             [(r.src_index, r.tgt_index, r.confidence, r.direction) for r in want]
+
+
+@pytest.mark.parametrize("chunk", [4096, 65536])
+def test_mine_corpus_file_streams_in_chunks(world500, tmp_path, monkeypatch, chunk):
+    """Chunked mine_corpus_file (ingest, mine, merge, emit per chunk; the next
+    chunk read meanwhile): the reference's 1,000-document TSV bytes and report
+    for any chunk size."""
+    import gzip
+
+    from paper_1509_08639_b200 import ingest
+
+    lex, fwd, bwd = world500
+    p = str(tmp_path / "docs1000.jsonl")
+    with gzip.open(golden("docs1000_s77.jsonl.gz"), "rb") as fi, open(p, "wb") as fo:
+        fo.write(fi.read())
+    monkeypatch.setenv("BM_STREAM_CHUNK_BYTES", str(chunk))
+    sink = io.StringIO()
+    rep = bm.mine_corpus_file(p, fwd, bwd, lex, bm.MinerConfig(bm.MiningParams(0.5, 0.2)), sink)
+    want = json.load(open(golden("mine1000_bi.json")))
+    text = sink.getvalue()
+    assert ingest.LAST_TIMINGS["chunks"] > 3
+    assert text.count("\n") == want["lines"]
+    assert hashlib.sha256(text.encode()).hexdigest() == want["sha256"]
+    ref = io.StringIO()
+    rrep = bm.mine_corpus(bm.load_document_pairs(p), fwd, bwd, lex,
+                          bm.MinerConfig(bm.MiningParams(0.5, 0.2)), ref)
+    rep.wall_clock_seconds = rrep.wall_clock_seconds = 0.0
+    assert bm.report_to_json(rep) == bm.report_to_json(rrep)
+
+
+def test_mine_corpus_file_hands_the_rest_to_python_mid_file(world500, tmp_path, monkeypatch):
+    """A document the native path cannot take (a direction the models do not
+    know, then invalid UTF-8) in a later chunk: earlier chunks are mined
+    natively, the rest by the Python reader -- the same bytes and error as
+    mine_corpus(load_document_pairs(path))."""
+    lex, fwd, bwd = world500
+    docs = load_docs("docs40.jsonl")
+    bad = dict(docs[30], src_lang="zz")
+    lines = [json.dumps(d) + "\n" for d in docs[:30]] + [json.dumps(bad) + "\n"] + \
+            [json.dumps(d) + "\n" for d in docs[31:]]
+    monkeypatch.setenv("BM_STREAM_CHUNK_BYTES", "2048")
+    for tail in (b"", b"\xff\xfe not utf-8\n"):
+        p = str(tmp_path / f"mixed{len(tail)}.jsonl")
+        with open(p, "wb") as fh:
+            fh.write("".join(lines).encode())
+            fh.write(tail)
+        cfg = bm.MinerConfig(bm.MiningParams(0.5, 0.2))
+        outs, errs = [], []
+        for fn in (lambda o: bm.mine_corpus_file(p, fwd, bwd, lex, cfg, o),
+                   lambda o: bm.mine_corpus(bm.load_document_pairs(p), fwd, bwd, lex, cfg, o)):
+            o = io.StringIO()
+            try:
+                fn(o)
+                errs.append(None)
+            except Exception as exc:  # noqa: BLE001 -- compared below
+                errs.append((type(exc), str(exc)))
+            outs.append(o.getvalue())
+        assert outs[0] == outs[1] and outs[0].count("\n") > 100
+        assert errs[0] == errs[1] and errs[0] is not None
