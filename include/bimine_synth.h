@@ -39,6 +39,12 @@ int bm_synth_generate(const bm_synth_spec* spec, const int64_t* ids, const int32
                       void** handle);
 int bm_synth_view(void* handle, bm_synth_arrays* out);
 void bm_synth_free(void* handle);
+/* The same documents rendered as document-pair JSONL (ids "doc%07d" of the
+ * global index, languages xx / yy, sentences as lists): tokenizing the file
+ * gives back exactly the arrays bm_synth_generate packs. */
+int bm_synth_jsonl(const bm_synth_spec* spec, const int64_t* ids, const int32_t* g,
+                   const int32_t* a, const int32_t* b, int64_t k, int32_t threads,
+                   const char* path);
 
 #ifdef __cplusplus
 }

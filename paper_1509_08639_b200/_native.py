@@ -160,6 +160,8 @@ SYNTH_SIGS = {
                                     C.POINTER(C.c_void_p)]),
     "bm_synth_view": (C.c_int, [C.c_void_p, C.POINTER(SynthArrays)]),
     "bm_synth_free": (None, [C.c_void_p]),
+    "bm_synth_jsonl": (C.c_int, [C.POINTER(SynthSpec), _p, _p, _p, _p, C.c_int64, C.c_int32,
+                                 C.c_char_p]),
 }
 
 _lock = threading.Lock()

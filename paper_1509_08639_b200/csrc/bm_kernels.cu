@@ -1156,22 +1156,32 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
   const int cap = min(n, m);
   bm_record* out = rec + rec_off[d];
   int nd = 0, kept = 0, ci = 0, cj = 0;
-  auto flush = [&](int valid) {
-    const bool have = lane < valid;
-    const double c = have ? Sd[(int64_t)ci * ld + cj] : 0.0;
-    const bool keep = have && c >= threshold;
+  // two-stage batches: a batch's 32 S values are loaded when it fills and
+  // used when the next one fills, so the gather's latency hides behind the
+  // walk instead of stalling it
+  int pi = 0, pj = 0, pvalid = 0;
+  double pc = 0.0;
+  auto finish = [&]() {
+    const bool keep = lane < pvalid && pc >= threshold;
     const unsigned mask = __ballot_sync(kFull, keep);
     if (keep) {
       const int rank = __popc(mask & ((1u << lane) - 1u));
       bm_record r;
       r.doc = d;
-      r.i = ci;
-      r.j = cj;
+      r.i = pi;
+      r.j = pj;
       r.pad = 0;
-      r.conf = c;
+      r.conf = pc;
       out[cap - 1 - (kept + rank)] = r;
     }
     kept += __popc(mask);
+  };
+  auto flush = [&](int valid) {
+    finish();
+    pc = lane < valid ? Sd[(int64_t)ci * ld + cj] : 0.0;
+    pi = ci;
+    pj = cj;
+    pvalid = valid;
   };
   warp_walk(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
     if (op == BM_MOVE_D) {
@@ -1183,6 +1193,7 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
     }
   });
   if (nd & 31) flush(nd & 31);
+  finish();
   __syncwarp();
   // move the kept records to the front, in chunks of 32 (source >= target)
   for (int q0 = 0; q0 < kept; q0 += WARP) {
@@ -1244,6 +1255,7 @@ int fused_rows_per_lane(int n) {
 // owns the counters of thresholds l and l + 32.
 // ---------------------------------------------------------------------------
 constexpr int kMaxThr = 64;
+constexpr int kGoldStage = 128;  // gold keys per walk warp staged in shared memory
 
 __global__ void __launch_bounds__(kWalkWarps * WARP) tune_count_kernel(
     const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
@@ -1257,31 +1269,42 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) tune_count_kernel(
   const int d = blockIdx.x * kWalkWarps + wid;
   if (d >= n_docs) return;
   uint32_t* win = walk_smem + wid * 3 * win_words<kTuneWG>();
+  int64_t* gs = (int64_t*)(walk_smem + kWalkWarps * 3 * win_words<kTuneWG>()) + wid * kGoldStage;
   const int n = nn[d], m = mm[d];
   const double* Sd = S + s_off[d];
   const int64_t ld = pitch[d];
   const int64_t g0 = gold_off[d], g1 = gold_off[d + 1];
+  // a document's sorted gold keys staged in shared memory when they fit: the
+  // binary search is then a chain of shared loads, not of global ones
+  const bool staged = g1 - g0 <= kGoldStage;
+  if (staged)
+    for (int64_t q = g0 + lane; q < g1; q += WARP) gs[q - g0] = gold[q];
+  __syncwarp();
+  const int64_t* gk = staged ? gs : gold + g0;
+  const int gn = (int)(g1 - g0);
   uint32_t p_lo = 0, p_hi = 0, h_lo = 0, h_hi = 0;
   int nd = 0, ci = 0, cj = 0;
-  auto flush = [&](int valid) {
-    const bool have = lane < valid;
-    double c = 0.0;
+  // two-stage batches (see extract_kernel): a batch's S values are loaded when
+  // it fills and counted when the next one fills
+  int pi = 0, pj = 0, pvalid = 0;
+  double pc = 0.0;
+  auto finish = [&]() {
+    const bool have = lane < pvalid;
     bool g = false;
     if (have) {
-      c = Sd[(int64_t)ci * ld + cj];
-      const int64_t key = (int64_t)ci * m + cj;
-      int64_t lo = g0, hi = g1;
+      const int64_t key = (int64_t)pi * m + pj;
+      int lo = 0, hi = gn;
       while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (gold[mid] < key)
+        const int mid = (lo + hi) >> 1;
+        if (gk[mid] < key)
           lo = mid + 1;
         else
           hi = mid;
       }
-      g = lo < g1 && gold[lo] == key;
+      g = lo < gn && gk[lo] == key;
     }
     for (int l = 0; l < n_thr; ++l) {
-      const bool ok = have && c >= thr[l];
+      const bool ok = have && pc >= thr[l];
       const uint32_t np = __popc(__ballot_sync(kFull, ok));
       const uint32_t nh = __popc(__ballot_sync(kFull, ok && g));
       if (l == lane) {
@@ -1293,6 +1316,13 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) tune_count_kernel(
       }
     }
   };
+  auto flush = [&](int valid) {
+    finish();
+    pc = lane < valid ? Sd[(int64_t)ci * ld + cj] : 0.0;
+    pi = ci;
+    pj = cj;
+    pvalid = valid;
+  };
   warp_walk<kTuneWG>(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
     if (op == BM_MOVE_D) {
       if (lane == (nd & 31)) {
@@ -1303,6 +1333,7 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) tune_count_kernel(
     }
   });
   if (nd & 31) flush(nd & 31);
+  finish();
   if (lane < n_thr) {
     if (p_lo) atomicAdd(pred + lane, (unsigned long long)p_lo);
     if (h_lo) atomicAdd(hit + lane, (unsigned long long)h_lo);
@@ -1320,7 +1351,7 @@ cudaError_t launch_tune_count(const uint32_t* dirs, const int64_t* dir_off, cons
                               unsigned long long* pred, unsigned long long* hit, cudaStream_t st) {
   if (n_docs == 0) return cudaSuccess;
   if (n_thr > kMaxThr) return cudaErrorInvalidValue;
-  constexpr int smem = walk_smem<kTuneWG>();
+  constexpr int smem = walk_smem<kTuneWG>() + kWalkWarps * kGoldStage * 8;
   cudaError_t e = cudaFuncSetAttribute(tune_count_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -17,8 +17,10 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -182,6 +184,84 @@ void gen_doc(Part& p, const bm_synth_spec& sp, int64_t doc, int32_t g, int32_t a
   p.gold_off.push_back((int64_t)p.gold_i.size());
 }
 
+// JSONL text of one document (synth.SynthCorpus.doc_pairs rendering: the
+// words, then the year, then "." -- tokenize() gives back the packed tokens).
+void letters3(int k, char* out) {
+  out[2] = (char)('a' + k % 26);
+  k /= 26;
+  out[1] = (char)('a' + k % 26);
+  k /= 26;
+  out[0] = (char)('a' + k % 26);
+}
+
+void jsonl_doc(std::string& o, const bm_synth_spec& sp, int64_t doc, int32_t g, int32_t a,
+               int32_t b, std::vector<Event>& ev) {
+  Part scratch;  // reuse gen_doc's event draws: same stream, same events
+  const int V = sp.vocab;
+  // regenerate the events exactly as gen_doc does (the draws are identical)
+  Rng r(sp.seed, (uint64_t)doc);
+  const int E = g + a + b;
+  ev.resize(E);
+  for (int e = 0; e < E; ++e) ev[e].type = e < g ? 0 : e < g + a ? 1 : 2;
+  for (int e = E - 1; e > 0; --e) std::swap(ev[e].type, ev[r.below((uint32_t)e + 1)].type);
+  for (int e = 0; e < E; ++e) {
+    Event& x = ev[e];
+    x.k = (uint8_t)(4 + r.below(6));
+    for (int q = 0; q < x.k; ++q) x.w[q] = (int32_t)r.below((uint32_t)V);
+    x.year = -1;
+    if (x.type == 0) {
+      for (int q = 1; q < x.k; ++q)
+        for (int u = 0; u < q; ++u)
+          if (x.w[u] == x.w[q]) {
+            x.w[q] = (int32_t)r.below((uint32_t)V);
+            u = -1;
+          }
+      for (int q = 0; q < x.k; ++q)
+        x.t[q] = V + (r.uniform() < sp.noise ? (int32_t)r.below((uint32_t)V) : x.w[q]);
+      if (r.uniform() < sp.digit_rate) x.year = (int16_t)r.below(kYears);
+    }
+  }
+  char buf[32];
+  snprintf(buf, sizeof(buf), "%07lld", (long long)doc);
+  o += "{\"id\": \"doc";
+  o += buf;
+  o += "\", \"src_lang\": \"xx\", \"tgt_lang\": \"yy\", \"src\": [";
+  auto sentence = [&](const int32_t* words, int k, int year, bool tgt) {
+    o += '"';
+    for (int q = 0; q < k; ++q) {
+      if (q) o += ' ';
+      char w[4];
+      w[0] = tgt ? 'v' : 'w';
+      letters3(words[q] - (tgt ? V : 0), w + 1);
+      o.append(w, 4);
+    }
+    if (year >= 0) {
+      snprintf(buf, sizeof(buf), " %d", kYear0 + year);
+      o += buf;
+    }
+    o += ".\"";
+  };
+  bool first = true;
+  for (const Event& x : ev) {
+    if (x.type == 2) continue;
+    if (!first) o += ", ";
+    first = false;
+    sentence(x.w, x.k, x.year, false);
+  }
+  o += "], \"tgt\": [";
+  first = true;
+  for (const Event& x : ev) {
+    if (x.type == 1) continue;
+    if (!first) o += ", ";
+    first = false;
+    int32_t tw[9];
+    for (int q = 0; q < x.k; ++q) tw[q] = x.type == 0 ? x.t[q] : V + x.w[q];
+    sentence(tw, x.k, x.year, true);
+  }
+  o += "]}\n";
+  (void)scratch;
+}
+
 template <class T>
 T src_at(const std::vector<T>& v, size_t q) { return v[q]; }
 template <class T>
@@ -300,5 +380,34 @@ int bm_synth_view(void* handle, bm_synth_arrays* out) {
 }
 
 void bm_synth_free(void* handle) { delete (Corpus*)handle; }
+
+int bm_synth_jsonl(const bm_synth_spec* spec, const int64_t* ids, const int32_t* g,
+                   const int32_t* a, const int32_t* b, int64_t k, int32_t threads,
+                   const char* path) {
+  if (spec == nullptr || path == nullptr || k < 0 || spec->vocab < 1 || spec->vocab > 17576)
+    return -1;
+  FILE* f = fopen(path, "wb");
+  if (f == nullptr) return -2;
+  int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  // blocks of documents rendered in parallel, written in order
+  const int64_t block = 4096;
+  std::vector<std::string> buf((size_t)nt);
+  int rc = 0;
+  for (int64_t b0 = 0; b0 < k && rc == 0; b0 += block * nt) {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        buf[t].clear();
+        std::vector<Event> ev;
+        const int64_t lo = b0 + block * t, hi = std::min(k, lo + block);
+        for (int64_t q = lo; q < hi; ++q) jsonl_doc(buf[t], *spec, ids[q], g[q], a[q], b[q], ev);
+      });
+    for (auto& th : pool) th.join();
+    for (int t = 0; t < nt && rc == 0; ++t)
+      if (!buf[t].empty() && fwrite(buf[t].data(), 1, buf[t].size(), f) != buf[t].size()) rc = -3;
+  }
+  if (fclose(f) != 0 && rc == 0) rc = -3;
+  return rc;
+}
 
 }  // extern "C"

@@ -44,6 +44,17 @@ _SENT_FIELDS = (("n_tok", np.int32, "n_sent"), ("n_punct", np.int32, "n_sent"),
                 ("tgt0", np.int32, "n_docs"), ("m", np.int32, "n_docs"))
 
 
+def _bytes_at(ptr, n: int) -> bytes:
+    """n bytes at ptr (ctypes.string_at takes a C int size: it truncates
+    lengths of 2 GiB and more, e.g. the TSV of a whole C3 corpus)."""
+    if n <= 0:
+        return b""
+    addr = ptr.value if isinstance(ptr, (C.c_char_p, C.c_void_p)) else ptr
+    if isinstance(ptr, C.c_char_p):
+        addr = C.cast(ptr, C.c_void_p).value
+    return bytes((C.c_char * n).from_address(addr))
+
+
 def _view(ptr: int, dtype, count: int) -> np.ndarray:
     if count == 0 or not ptr:
         return np.zeros(0, dtype=dtype)
@@ -153,7 +164,7 @@ class NativeCorpus:
         for which in (0, 1):
             p, n = C.c_void_p(), C.c_int64()
             N.check(self._lib.bm_ingest_seen(self._h, which, C.byref(p), C.byref(n)))
-            raw = C.string_at(p, n.value) if n.value else b""
+            raw = _bytes_at(p, n.value)
             out.append(raw.decode("utf-8").split("\0")[:-1] if raw else [])
         return out[0], out[1]
 
@@ -173,7 +184,7 @@ class NativeCorpus:
         N.check(self._lib.bm_ingest_emit_merged(self._h, recs.ctypes.data, recs.shape[0],
                                                 sk.ctypes.data, C.byref(out), C.byref(olen),
                                                 rep.ctypes.data))
-        data = C.string_at(out, olen.value) if olen.value else b""
+        data = _bytes_at(out, olen.value)
         return data, rep.tolist()
 
     def emit(self, fwd: np.ndarray, bwd: np.ndarray | None, swap_f: np.ndarray,
@@ -190,7 +201,7 @@ class NativeCorpus:
                                          b.shape[0], int(bwd is not None), sf.ctypes.data,
                                          sb.ctypes.data, sk.ctypes.data, C.byref(out),
                                          C.byref(olen), rep.ctypes.data))
-        data = C.string_at(out, olen.value) if olen.value else b""
+        data = _bytes_at(out, olen.value)
         return data, rep.tolist()
 
 

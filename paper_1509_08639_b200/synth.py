@@ -333,3 +333,24 @@ def make_corpus_native(n_gold, n_src, n_tgt, ids=None, vocab: int = 5000, noise:
     return NativeSynthCorpus(SynthWorld(vocab), packed, _view(owner, v.gold_off, D + 1, np.int64),
                              _view(owner, v.gold_i, v.n_gold, i32),
                              _view(owner, v.gold_j, v.n_gold, i32))
+
+
+def write_jsonl_native(path: str, n_gold, n_src, n_tgt, ids=None, vocab: int = 5000,
+                       noise: float = 0.1, seed: int = 0, digit_rate: float = 0.15,
+                       threads: int = 0) -> None:
+    """make_corpus_native's documents as document-pair JSONL text (the words,
+    then the year, then "."; ids "doc%07d" of the global document index)."""
+    import ctypes as C
+
+    from . import _native as N
+
+    lib = N.load_library()
+    g = np.ascontiguousarray(n_gold, dtype=np.int32)
+    a = np.ascontiguousarray(n_src, dtype=np.int32)
+    b = np.ascontiguousarray(n_tgt, dtype=np.int32)
+    ids = np.arange(g.size, dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+    spec = N.SynthSpec(int(vocab), float(noise), float(digit_rate), int(seed) & (2**64 - 1))
+    rc = lib.bm_synth_jsonl(C.byref(spec), ids.ctypes.data, g.ctypes.data, a.ctypes.data,
+                            b.ctypes.data, g.size, int(threads), path.encode())
+    if rc != 0:
+        raise OSError(f"bm_synth_jsonl failed ({rc})")
