@@ -1256,16 +1256,33 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
     }
     {
       // 16-bit document-level join, or 32-bit per-tile counts for sentences
-      // longer than 65535 tokens
+      // longer than 65535 tokens. The banded tier runs on the next mining
+      // stream (after this chunk's unpacked arrays are ready), beside the
+      // fused tier; the compaction below waits for both.
       GeneralPlan gp, gw;
       for (int d = d0; d < d1; ++d)
         if (banded[d]) (amax[d] <= 65535 ? gp : gw).add(d, dh->n[d], dh->m[d]);
-      for (GeneralPlan* g : {&gp, &gw}) {
-        if (g->docs.empty()) continue;
-        Scratch scg(sk);
-        int rc = mine_general(*g, &sd, &dd, &ld, M, threshold, penalty, droff, rec, cnt, cost,
-                              g == &gp, scg, sk);
-        if (rc) return rc;
+      if (!gp.docs.empty() || !gw.docs.empty()) {
+        cudaStream_t sb = ms.size() > 1 ? ms[(ch_d0.size() + 2) % ms.size()] : sk;
+        if (sb != sk) {
+          cudaEvent_t ready_b = joiner.event();
+          if (ready_b == nullptr) return fail(BM_ECUDA, "event create failed");
+          BM_CK(cudaEventRecord(ready_b, sk), "event");
+          BM_CK(cudaStreamWaitEvent(sb, ready_b, 0), "event");
+        }
+        for (GeneralPlan* g : {&gp, &gw}) {
+          if (g->docs.empty()) continue;
+          Scratch scg(sb);
+          int rc = mine_general(*g, &sd, &dd, &ld, M, threshold, penalty, droff, rec, cnt, cost,
+                                g == &gp, scg, sb);
+          if (rc) return rc;
+        }
+        if (sb != sk) {
+          cudaEvent_t done_b = joiner.event();
+          if (done_b == nullptr) return fail(BM_ECUDA, "event create failed");
+          BM_CK(cudaEventRecord(done_b, sb), "event");
+          BM_CK(cudaStreamWaitEvent(sk, done_b, 0), "event");
+        }
       }
     }
     // compact the chunk into its own region of `dense` (starting at its first
