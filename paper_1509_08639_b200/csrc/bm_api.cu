@@ -614,16 +614,26 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
   const char* route = getenv("BM_ROUTE");
   const bool force_banded = route != nullptr && strcmp(route, "banded") == 0;
   hit_off.assign((size_t)(d_hi - d_lo), 0);
+  int pn = -1, pm = -1, pq = -1;  // the last shape's class (batches repeat shapes)
+  size_t sl = 0, hs = 0;
   for (int d = d_lo; d < d_hi; ++d) {
     const int n = n_host[d], m = m_host[d];
     if (n <= 0 || m <= 0) continue;
-    const int R = fused_rows_per_lane(n);
-    const size_t sl = ring_slice_bytes(n, m, R);
-    if (!force_banded && n <= kFusedMaxRows && sl <= fused_max_smem() && amax_host[d] <= 255) {
-      const int q = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
+    if (n != pn || m != pm) {
+      const int R = fused_rows_per_lane(n);
+      sl = ring_slice_bytes(n, m, R);
+      hs = hits_kernel_smem(n, m);
+      pq = (!force_banded && n <= kFusedMaxRows && sl <= fused_max_smem())
+               ? (R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3)
+               : -1;
+      pn = n;
+      pm = m;
+    }
+    if (pq >= 0 && amax_host[d] <= 255) {
+      const int q = pq;
       fused[q].push_back(d);
       fused_smem[q] = std::max(fused_smem[q], sl);
-      hits_smem[q] = std::max(hits_smem[q], hits_kernel_smem(n, m));
+      hits_smem[q] = std::max(hits_smem[q], hs);
       hit_off[d - d_lo] = hit_total;
       hit_total += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
     } else {
@@ -1040,14 +1050,15 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   tr.mark("alloc + small h2d");
   // chunks of documents: H2D the sentence range each chunk touches on the
   // copy stream, mine it on the compute stream once its copy event fired
-  // (16M cells per chunk; large batches use at most ~64 chunks, each at most
-  // mine_group_cells(): per-chunk launches and host planning stay amortised)
+  // (16M cells per chunk; large batches use ~16 chunks of at most
+  // mine_group_cells(): a chunk's banded DP must hold enough (doc, band) items
+  // for its persistent grid -- C3 200k in 64 chunks took 181 ms, in groups 75)
   int64_t all_cells = 0;
   for (int d = 0; d < nd; ++d) all_cells += (int64_t)dh->n[d] * dh->m[d];
   static const int64_t kChunkEnv = getenv("BM_CHUNK_CELLS") ? atoll(getenv("BM_CHUNK_CELLS")) : 0;
   const int64_t kChunkCells =
       kChunkEnv > 0 ? kChunkEnv
-                    : std::min(mine_group_cells(), std::max<int64_t>(16ll << 20, all_cells / 64));
+                    : std::min(mine_group_cells(), std::max<int64_t>(16ll << 20, all_cells / 16));
   static const int64_t kFirstEnv =
       getenv("BM_FIRST_CHUNK_CELLS") ? atoll(getenv("BM_FIRST_CHUNK_CELLS")) : 0;
   const int64_t kFirstChunkCells = kFirstEnv > 0 ? kFirstEnv : (4ll << 20);
@@ -1140,63 +1151,17 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   };
   if (int rc = enqueue_copies(1)) return rc;
   tr.mark("chunk 0 copies enqueued");
-  // route every document once (global indices) and stage the fused tier's
-  // document lists, hit offsets and zeroed hit scratch before the chunk loop,
-  // so a chunk is only kernel launches (no per-chunk host planning or small
-  // uploads queued behind the bulk copies)
+  // the chunks are mined like bm_mine's groups (mine_group: routing, fused
+  // tier on one stream, banded tier on the next), rotating over the mining
+  // streams, each chunk once its copies have landed
   const Model M = to_model(model);
-  std::vector<int32_t> fl[4];
-  size_t fsm[4] = {0, 0, 0, 0}, hsm[4] = {0, 0, 0, 0};
-  std::vector<int64_t> hoff(nd, 0);
-  std::vector<char> banded(nd, 0);
-  int64_t htot = 0;
-  {
-    const char* route = getenv("BM_ROUTE");
-    const bool force_banded = route != nullptr && strcmp(route, "banded") == 0;
-    int pn = -1, pm = -1, pq = -1;  // the last shape's class (batches repeat shapes)
-    size_t psl = 0, phs = 0;
-    for (int d = 0; d < nd; ++d) {
-      const int n = dh->n[d], m = dh->m[d];
-      if (n <= 0 || m <= 0) continue;
-      if (n != pn || m != pm) {
-        const int R = fused_rows_per_lane(n);
-        psl = ring_slice_bytes(n, m, R);
-        phs = hits_kernel_smem(n, m);
-        pq = (!force_banded && n <= kFusedMaxRows && psl <= fused_max_smem())
-                 ? (R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3)
-                 : -1;
-        pn = n;
-        pm = m;
-      }
-      if (pq >= 0 && amax[d] <= 255) {
-        const int q = pq;
-        fl[q].push_back(d);
-        fsm[q] = std::max(fsm[q], psl);
-        hsm[q] = std::max(hsm[q], phs);
-        hoff[d] = htot;
-        htot += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
-      } else {
-        banded[d] = 1;
-      }
-    }
-  }
-  tr.mark("routing");
-  int32_t* dfl[4] = {nullptr, nullptr, nullptr, nullptr};
-  for (int q = 0; q < 4; ++q)
-    if (!fl[q].empty()) BM_CK(sc.upload(&dfl[q], fl[q]), "upload");
-  int64_t* dhoff = nullptr;
-  uint8_t* hits = nullptr;
-  if (htot > 0 && !BM_RING_FUSED_JOIN) {
-    BM_CK(sc.upload(&dhoff, hoff), "upload");
-    BM_CK(sc.alloc(&hits, (size_t)htot), "alloc hits");
-    BM_CK(cudaMemsetAsync(hits, 0, (size_t)htot, st), "memset hits");
-  }
   BM_CK(cudaMemsetAsync(cnt, 0, std::max(nd, 1) * sizeof(int32_t), st), "memset");
-  const PairTables tabs = pair_tables();
-  ModelTables mtab;
-  BM_CK(model_tables(M, &mtab), "model tables");
-  tr.mark("list uploads + memsets");
-  // the mining streams start after the list uploads and memsets on st
+  {
+    ModelTables mt;  // built (once per model and device) before any stream uses it
+    BM_CK(model_tables(M, &mt), "model tables");
+  }
+  tr.mark("memsets");
+  // the mining streams start after the memsets on st
   cudaEvent_t planned = joiner.event();
   if (planned == nullptr) return fail(BM_ECUDA, "event create failed");
   BM_CK(cudaEventRecord(planned, st), "event");
@@ -1208,12 +1173,13 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
     BM_CK(cudaStreamWaitEvent(ms.back(), planned, 0), "event");
     joiner.side.push_back(ms.back());
   }
-  // pass 2: per chunk, widen + mine + compact on a mining stream; chunk 0's
+  // pass 2: per chunk, widen + mine + compact on the mining streams; chunk 0's
   // kernels are enqueued before the remaining copies so the GPU starts early
   auto enqueue_kernels = [&](size_t kc) -> int {
     const int d0 = chunks[kc].d0, d1 = chunks[kc].d1, lo = chunks[kc].lo, hi = chunks[kc].hi;
     cudaEvent_t ev = chunks[kc].copied;
     cudaStream_t sk = ms[(ch_d0.size() + 1) % ms.size()];  // chunk 0 on a side stream
+    cudaStream_t sb = ms.size() > 1 ? ms[(ch_d0.size() + 2) % ms.size()] : sk;
     BM_CK(cudaStreamWaitEvent(sk, ev, 0), "event");
     // the copy stream only moves bytes: widening the wire arrays is a few
     // microseconds of compute and runs in order on the compute stream (on the
@@ -1229,61 +1195,22 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
                                a2, a4, a7, a6, sk),
             "unpack_wire_kernel");
     }
-    for (int q = 0; q < 4; ++q) {
-      // the chunk's documents of this class: a contiguous slice of the list
-      const auto b = std::lower_bound(fl[q].begin(), fl[q].end(), d0);
-      const auto e = std::lower_bound(b, fl[q].end(), d1);
-      if (b == e) continue;
-      FusedArgs a;
-      a.S = sd;
-      a.D = dd;
-      a.L = ld;
-      a.M = M;
-      a.threshold = threshold;
-      a.p = penalty;
-      a.list = dfl[q] + (b - fl[q].begin());
-      a.n_list = (int)(e - b);
-      a.rec_off = droff;
-      a.rec = rec;
-      a.rec_count = cnt;
-      a.cost = cost;
-      a.hits = hits;
-      a.hit_off = dhoff;
-      a.tabs = tabs;
-      a.mt = mtab;
-      if (!BM_RING_FUSED_JOIN) BM_CK(launch_hits(a, hsm[q], sk), "hits_kernel");
-      BM_CK(launch_ring(a, 1 << q, fsm[q], sk), "mine_ring_kernel");
+    if (sb != sk) {  // the banded tier starts once the chunk's arrays are ready
+      cudaEvent_t ready_b = joiner.event();
+      if (ready_b == nullptr) return fail(BM_ECUDA, "event create failed");
+      BM_CK(cudaEventRecord(ready_b, sk), "event");
+      BM_CK(cudaStreamWaitEvent(sb, ready_b, 0), "event");
     }
     {
-      // 16-bit document-level join, or 32-bit per-tile counts for sentences
-      // longer than 65535 tokens. The banded tier runs on the next mining
-      // stream (after this chunk's unpacked arrays are ready), beside the
-      // fused tier; the compaction below waits for both.
-      GeneralPlan gp, gw;
-      for (int d = d0; d < d1; ++d)
-        if (banded[d]) (amax[d] <= 65535 ? gp : gw).add(d, dh->n[d], dh->m[d]);
-      if (!gp.docs.empty() || !gw.docs.empty()) {
-        cudaStream_t sb = ms.size() > 1 ? ms[(ch_d0.size() + 2) % ms.size()] : sk;
-        if (sb != sk) {
-          cudaEvent_t ready_b = joiner.event();
-          if (ready_b == nullptr) return fail(BM_ECUDA, "event create failed");
-          BM_CK(cudaEventRecord(ready_b, sk), "event");
-          BM_CK(cudaStreamWaitEvent(sb, ready_b, 0), "event");
-        }
-        for (GeneralPlan* g : {&gp, &gw}) {
-          if (g->docs.empty()) continue;
-          Scratch scg(sb);
-          int rc = mine_general(*g, &sd, &dd, &ld, M, threshold, penalty, droff, rec, cnt, cost,
-                                g == &gp, scg, sb);
-          if (rc) return rc;
-        }
-        if (sb != sk) {
-          cudaEvent_t done_b = joiner.event();
-          if (done_b == nullptr) return fail(BM_ECUDA, "event create failed");
-          BM_CK(cudaEventRecord(done_b, sb), "event");
-          BM_CK(cudaStreamWaitEvent(sk, done_b, 0), "event");
-        }
-      }
+      int rc = mine_group(&sd, &dd, dh->n, dh->m, amax.data(), &ld, M, threshold, penalty, droff,
+                          rec, cnt, cost, d0, d1, tr, sk, sb);
+      if (rc) return rc;
+    }
+    if (sb != sk) {  // compaction after both tiers
+      cudaEvent_t done_b = joiner.event();
+      if (done_b == nullptr) return fail(BM_ECUDA, "event create failed");
+      BM_CK(cudaEventRecord(done_b, sb), "event");
+      BM_CK(cudaStreamWaitEvent(sk, done_b, 0), "event");
     }
     // compact the chunk into its own region of `dense` (starting at its first
     // document's record slot) and fetch its record count; the host copies the
