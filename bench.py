@@ -622,9 +622,10 @@ class TuneWorkload:
         return 8 * self.cells + in_bytes
 
 
-def measured_profile(name: str):
-    """DRAM bytes and issue / FP64-pipe utilisation of the workload's kernels
-    from the latest committed ncu --set full capture (profiles/*_<name>_ncu_raw_metrics.json)."""
+def measured_profile(name: str, cells: int):
+    """DRAM bytes (scaled to `cells` from the capture's profiled cells) and
+    issue / FP64-pipe utilisation of the workload's kernels from the latest
+    committed ncu --set full capture (profiles/*_<name>_ncu_raw_metrics.json)."""
     pdir = os.path.join(ROOT, "profiles")
     if not os.path.isdir(pdir):
         return None
@@ -637,8 +638,11 @@ def measured_profile(name: str):
         return None
     traffic = sum(float(v["dram__bytes_read.sum"]) + float(v["dram__bytes_write.sum"])
                   for v in kernels.values()) * float(d.get("bytes_scale", 1e6))
+    if d.get("profiled_cells"):
+        traffic *= cells / float(d["profiled_cells"])
     top = max(kernels.items(), key=lambda kv: float(kv[1].get("gpu__time_duration.sum", 0)))
     return {"traffic": traffic, "source": f"profiles/{cands[-1]}",
+            "traffic_per_cell": traffic / max(cells, 1),
             "top_kernel": top[0],
             "issue_slots_busy_pct": top[1].get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "fp64_pipe_active_pct": top[1].get(
@@ -679,7 +683,7 @@ def measure(ctx: Ctx, name: str, steps: int, warmup: int, cpu: bool, fp64: dict)
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     alg = w.alg_bytes(n_rec)
     achieved = alg / (kern_ms / 1e3) / 1e9
-    prof = measured_profile(name)
+    prof = measured_profile(name, w.cells)
     npen = len(C5_PENS) if name == "c5" else 1
     dp_cells_s = w.cells * npen / (kern_ms / 1e3)
     dp_peak_cells = fp64["dfma_tflops"] * 1e12 / 2 / DP_OPS_PER_CELL
@@ -692,7 +696,8 @@ def measure(ctx: Ctx, name: str, steps: int, warmup: int, cpu: bool, fp64: dict)
             "alg_bytes_def": "SURVEY 8(d): 8 B/cell similarity matrix + packed inputs + 24 B/record",
             "kernel_ms": kern_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)"}
     if prof is not None:
-        roof["traffic_source"] = prof["source"]
+        roof["traffic_source"] = prof["source"] + " (DRAM bytes per cell of the capture x this step's cells)"
+        roof["traffic_bytes_per_cell"] = prof["traffic_per_cell"]
         roof["measured_dram_gbs"] = prof["traffic"] / (kern_ms / 1e3) / 1e9
         roof["measured_dram_frac"] = roof["measured_dram_gbs"] / hbm_peak
     dp = {"achieved_gcups": dp_cells_s / 1e9, "peak_gcups": dp_peak_cells / 1e9,

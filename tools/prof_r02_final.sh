@@ -1,0 +1,10 @@
+# round-2 profiles: full bench line, C3 launch list, ncu --set full of the top kernels
+set -e
+python bench.py > gpurun_out/r02_bench.log 2>&1
+CMD3="python bench.py --workload c3 --c3-docs 100000 --steps 1 --warmup 1 --extras none --no-cpu"
+$CMD3 > gpurun_out/r02_p3.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_c3_launches.csv $CMD3 > gpurun_out/r02_ncu3.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"score_hits|nw_band|hits_doc|mine_ring|hits_kernel|extract_kernel" -c 8 -o gpurun_out/r02_c3_full $CMD3 > gpurun_out/r02_ncu3f.log 2>&1
+CMD2="python bench.py --workload c2 --steps 1 --warmup 1 --extras none --no-cpu"
+$CMD2 > gpurun_out/r02_p2.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"mine_ring|hits_kernel" -s 4 -c 2 -o gpurun_out/r02_c2_full $CMD2 > gpurun_out/r02_ncu2f.log 2>&1

@@ -49,15 +49,18 @@ def main():
         for r in rows[1:]:
             by.setdefault(short(r[ki]), {})[r[mi]] = (r[vi], r[ui])
         raw = ncu(rep, "raw")
-        rh = raw[0]
+        rh, units = raw[0], raw[1]
         kcol = rh.index("Kernel Name")
+        # normalised units: bytes and milliseconds
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                 "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
         for r in raw[2:]:
             k = short(r[kcol])
             ent = raw_all.setdefault(k, {})
             stalls = {}
             for i, name in enumerate(rh):
                 if name in RAW:
-                    ent[name] = float(r[i].replace(",", ""))
+                    ent[name] = float(r[i].replace(",", "")) * scale.get(units[i], 1.0)
                 elif name.startswith(STALLS) and not name.endswith("not_issued"):
                     try:
                         v = float(r[i].replace(",", ""))
@@ -77,6 +80,8 @@ def main():
                 text.append("  stall share (pc sampling)         " +
                             ", ".join(f"{a} {b:.0%}" for a, b in raw_all[k]["stall_share"].items()))
     open(prefix + "_ncu_full_summary.txt", "w").write("\n".join(text) + "\n")
+    raw_all["bytes_scale"] = 1.0
+    raw_all["units"] = "dram bytes in bytes, gpu__time_duration.sum in ms"
     json.dump(raw_all, open(prefix + "_ncu_raw_metrics.json", "w"), indent=1)
     print("\n".join(text))
 
