@@ -243,6 +243,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
 // keep score_tile_kernel.
 // ---------------------------------------------------------------------------
 constexpr int kJoinSentChunk = 128;
+#ifndef BM_JOIN_PROBE_CHUNK
+#define BM_JOIN_PROBE_CHUNK 1024
+#endif
+constexpr int kJoinProbeChunk = BM_JOIN_PROBE_CHUNK;  // probe-side sentences per item
 
 #ifndef BM_HITS_DOC_MINB
 #define BM_HITS_DOC_MINB 12
@@ -254,7 +258,10 @@ __global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sente
                                                          uint32_t* __restrict__ hits) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int4 it = items[blockIdx.x];
-  const int d = it.x, dir = it.y, k0 = it.z, k1 = it.w;
+  // y = direction | probe chunk << 1: the probe side is cut into chunks of
+  // kJoinProbeChunk sentences so one long document is many CTAs (C4's 8192
+  // rows were 128 CTAs, 1.7 ms)
+  const int d = it.x, dir = it.y & 1, k0 = it.z, k1 = it.w;
   const int n = D.n[d], m = D.m[d];
   const int s0 = D.src0[d], t0 = D.tgt0[d];
   JoinSmem js = carve_join(smem);
@@ -262,8 +269,10 @@ __global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sente
   uint16_t* a_owner = chunk_owner + kJoinEmax;
   uint32_t* hd = hits + h_off[d];
   const int a0 = dir == 0 ? s0 : t0, b0 = dir == 0 ? t0 : s0;
-  const int na = dir == 0 ? n : m, nb = dir == 0 ? m : n;
-  const int32_t* offA = S.tok_off + a0;
+  const int na_all = dir == 0 ? n : m, nb = dir == 0 ? m : n;
+  const int p0 = (it.y >> 1) * kJoinProbeChunk;
+  const int na = min(na_all - p0, kJoinProbeChunk);
+  const int32_t* offA = S.tok_off + a0 + p0;
   const int32_t* offB = S.tok_off + b0;
   const int32_t* off = dir == 0 ? L.fwd_off : L.rev_off;
   const int32_t* cand = dir == 0 ? L.fwd_cand : L.rev_cand;
@@ -273,12 +282,12 @@ __global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sente
     if (dir == 0)
       join_chunk_entries(CtaGroup(), S, off, cand, offA, na, offB, b0, nb, c0, c1, js, chunk_owner,
                          a_owner, [&](int ls, int lt, int w) {
-                           atomicAdd(hd + (int64_t)ls * m + lt, (uint32_t)w);
+                           atomicAdd(hd + (int64_t)(ls + p0) * m + lt, (uint32_t)w);
                          });
     else
       join_chunk_entries(CtaGroup(), S, off, cand, offA, na, offB, b0, nb, c0, c1, js, chunk_owner,
                          a_owner, [&](int lt, int ls, int w) {
-                           atomicAdd(hd + (int64_t)ls * m + lt, (uint32_t)w << 16);
+                           atomicAdd(hd + (int64_t)ls * m + (lt + p0), (uint32_t)w << 16);
                          });
   }
 }
@@ -450,10 +459,12 @@ void join_items(const int32_t* n, const int32_t* m, int nd, std::vector<int4>& i
   items.clear();
   for (int d = 0; d < nd; ++d) {
     if (n[d] <= 0 || m[d] <= 0) continue;
-    for (int k = 0; k < m[d]; k += kJoinSentChunk)
-      items.push_back(make_int4(d, 0, k, std::min(m[d], k + kJoinSentChunk)));
-    for (int k = 0; k < n[d]; k += kJoinSentChunk)
-      items.push_back(make_int4(d, 1, k, std::min(n[d], k + kJoinSentChunk)));
+    for (int p = 0; p * kJoinProbeChunk < n[d]; ++p)
+      for (int k = 0; k < m[d]; k += kJoinSentChunk)
+        items.push_back(make_int4(d, 0 | p << 1, k, std::min(m[d], k + kJoinSentChunk)));
+    for (int p = 0; p * kJoinProbeChunk < m[d]; ++p)
+      for (int k = 0; k < n[d]; k += kJoinSentChunk)
+        items.push_back(make_int4(d, 1 | p << 1, k, std::min(n[d], k + kJoinSentChunk)));
   }
 }
 
