@@ -931,18 +931,25 @@ cudaError_t launch_nw_np(const NwArgs& a, cudaStream_t st) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static thread_local int r8 = 0, r4 = 0, dev_of = -1;
+  static thread_local int r8 = 0, r4 = 0, r2 = 0, dev_of = -1;
   if (dev_of != dev) {
     r8 = nw_resident<8, NP, kFin>(sms);
     r4 = nw_resident<4, NP, kFin>(sms);
+    r2 = nw_resident<2, NP, kFin>(sms);
     dev_of = dev;
   }
   // BM_NW_WARPS_PER_SM caps the persistent grid (experiments: room for the
-  // scoring kernels of other groups next to the latency-bound DP)
+  // scoring kernels of other groups next to the latency-bound DP);
+  // BM_NW_DEEP_ITEMS: item count from which the shallow (D = 2) ring runs
+  // (more resident warps when many bands wait: C5 100k 50.1 -> 48.4 ms)
   static const int cap = getenv("BM_NW_WARPS_PER_SM") ? atoi(getenv("BM_NW_WARPS_PER_SM")) : 0;
+  static const int deep = getenv("BM_NW_DEEP_ITEMS") ? atoi(getenv("BM_NW_DEEP_ITEMS")) : 3000;
   const int lim4 = cap > 0 ? std::min(r4, cap * sms) : r4;
   const int lim8 = cap > 0 ? std::min(r8, cap * sms) : r8;
-  if (a.n_items > r8) {
+  const int lim2 = cap > 0 ? std::min(r2, cap * sms) : r2;
+  if (a.n_items > deep) {
+    nw_band_kernel<2, NP, kFin><<<std::min(lim2, a.n_items), WARP, nw_smem(2, NP), st>>>(a);
+  } else if (a.n_items > r8) {
     nw_band_kernel<4, NP, kFin><<<std::min(lim4, a.n_items), WARP, nw_smem(4, NP), st>>>(a);
   } else {
     nw_band_kernel<8, NP, kFin><<<std::min(lim8, a.n_items), WARP, nw_smem(8, NP), st>>>(a);
