@@ -733,6 +733,8 @@ def measure(ctx: Ctx, name: str, steps: int, warmup: int, cpu: bool, fp64: dict)
             "sample": f"{k} docs drawn uniformly from the workload, {dt:.1f}s, oracle/bimine_oracle.c "
                       f"(C restatement of the reference path), {host_cores()} threads, {cpu_model()}"}
     del w
+    ctx.torch.cuda.synchronize()
+    ctx.lib.bm_trim()  # the next workload starts from an empty scratch
     ctx.torch.cuda.empty_cache()
     return res
 

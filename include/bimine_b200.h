@@ -274,6 +274,11 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
             const int64_t* gold, const int64_t* gold_off, unsigned long long* pred,
             unsigned long long* hit, int32_t token_bound, void* stream);
 
+/* The large mining scratch (similarity matrices, hit counts, codes) is kept
+ * per stream of the calling thread and reused by later calls (grow-only, at
+ * most 8 streams); bm_trim synchronizes the device and releases it. */
+int bm_trim(void);
+
 /* Exclusive-scan compaction of per-doc record slots into a dense,
  * document-ordered array; *total (device) receives the record count. */
 int bm_compact(const bm_record* rec, const int64_t* rec_off, const int32_t* rec_count,

@@ -81,6 +81,7 @@ class IngestArrays(C.Structure):
 
 _SIGS = {
     "bm_abi_version": (C.c_int, []),
+    "bm_trim": (C.c_int, []),
     "bm_last_error": (C.c_char_p, []),
     "bm_device_count": (C.c_int, []),
     "bm_dirs_words": (C.c_int64, [C.c_int32, C.c_int32]),

@@ -141,9 +141,26 @@ struct Workspace {
   size_t cap[kWsSlots];
 };
 
+std::vector<Workspace>& workspaces() {
+  static thread_local std::vector<Workspace> spaces;
+  return spaces;
+}
+
+// Releases a workspace set (the rare eviction path and bm_trim): its stream
+// may be gone, so the device is synchronized and the buffers freed directly.
+void ws_release(Workspace& w) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(w.dev);
+  cudaDeviceSynchronize();
+  for (int k = 0; k < kWsSlots; ++k)
+    if (w.buf[k]) cudaFree(w.buf[k]);
+  cudaSetDevice(cur);
+}
+
 template <class T>
 cudaError_t ws_get(cudaStream_t st, WsSlot slot, T** out, size_t count) {
-  static thread_local std::vector<Workspace> spaces;
+  std::vector<Workspace>& spaces = workspaces();
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -151,13 +168,8 @@ cudaError_t ws_get(cudaStream_t st, WsSlot slot, T** out, size_t count) {
   for (Workspace& x : spaces)
     if (x.st == st && x.dev == dev) w = &x;
   if (w == nullptr) {
-    if (spaces.size() >= 16) {  // bounded: release the oldest stream's set
-      int cur = dev;
-      Workspace& old = spaces.front();
-      cudaSetDevice(old.dev);
-      for (int k = 0; k < kWsSlots; ++k)
-        if (old.buf[k]) cudaFreeAsync(old.buf[k], old.st);
-      cudaSetDevice(cur);
+    if (spaces.size() >= 8) {  // bounded: release the oldest stream's set
+      ws_release(spaces.front());
       spaces.erase(spaces.begin());
     }
     Workspace fresh{};
@@ -448,6 +460,12 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
 extern "C" {
 
 int bm_abi_version(void) { return BM_ABI_VERSION; }
+
+int bm_trim(void) {
+  for (Workspace& w : workspaces()) ws_release(w);
+  workspaces().clear();
+  return BM_OK;
+}
 
 const char* bm_last_error(void) { return g_err.c_str(); }
 

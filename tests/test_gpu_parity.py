@@ -735,3 +735,20 @@ def test_mine_corpus_file_hands_the_rest_to_python_mid_file(world500, tmp_path, 
             outs.append(o.getvalue())
         assert outs[0] == outs[1] and outs[0].count("\n") > 100
         assert errs[0] == errs[1] and errs[0] is not None
+
+
+def test_trim_releases_scratch_and_mining_continues(oracle_mod):
+    """bm_trim drops the per-stream workspaces; the next calls regrow them and
+    give the same records."""
+    from paper_1509_08639_b200 import _native, engine, synth
+
+    g, a, b = synth.c3_shape(300, seed=12)
+    sc = synth.make_corpus_native(g, a, b, seed=12)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    dc = engine.DeviceCorpus.upload(sc.packed)
+    dl = engine.DeviceLexicon.upload(sc.world.packed_lexicon())
+    view = engine.DocView.of(sc.packed)
+    first, _ = engine.mine(dc, dl, view, model, 0.5, 0.2)
+    assert _native.lib().bm_trim() == 0
+    again, _ = engine.mine(dc, dl, view, model, 0.5, 0.2)
+    assert first.tobytes() == again.tobytes()
