@@ -580,7 +580,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNwLane = kBandR * 4 + 2;                      // doubles per lane slice (+pad)
 constexpr int kNwSlotBytes = WARP * kNwLane * 8;
 __host__ __device__ constexpr int nw_smem(int D, int NP = 1) {
-  return (D + 1) * kNwSlotBytes + NP * WARP * 8;
+  return D * kNwSlotBytes + NP * WARP * 8;
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -682,14 +682,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define BM_NW_EARLY_BND 1
 #endif
 template <int D, int NP, bool kFin>
-__global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
+#ifndef BM_NW_MINB2
+#define BM_NW_MINB2 1
+#endif
+// the shallow ring (D = 2) runs when many bands wait: resident warps matter
+// more than registers there (BM_NW_MINB2 caps the registers for that many
+// warps per SM)
+__global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) nw_band_kernel(NwArgs a) {
   static_assert((D & (D - 1)) == 0, "ring depth must be a power of two");
   // NP > 1 (tuner): NP penalties run over the same band in one pass. S is
   // staged and turned into 1-S once for all of them, and their NP independent
   // dependency chains interleave in the block (ILP the single chain lacks).
   extern __shared__ __align__(16) double nw_ring[];
   const int lane = threadIdx.x;
-  double* bnd_s = nw_ring + (D + 1) * WARP * kNwLane;  // NP x 32-column boundary chunks
+  double* bnd_s = nw_ring + D * WARP * kNwLane;  // NP x 32-column boundary chunks
   const double* ring_l = nw_ring + (size_t)lane * kNwLane;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring_l);
   double pq[NP];
@@ -723,12 +729,16 @@ __global__ void __launch_bounds__(WARP, 1) nw_band_kernel(NwArgs a) {
     const double* src1 = a.S + a.s_off[d] + (int64_t)min(i0 + 1, n - 1) * ld;
     const double* src2 = a.S + a.s_off[d] + (int64_t)min(i0 + 2, n - 1) * ld;
     const double* src3 = a.S + a.s_off[d] + (int64_t)min(i0 + 3, n - 1) * ld;
-    // one commit per call on every lane; groups outside [0, ngroups) go to
-    // the dummy slot so the per-lane group accounting stays uniform
+    // one commit per call on every lane. Group gi lands in slot gi & (D-1);
+    // a group outside [0, ngroups) copies row starts into that slot -- either
+    // the slot of a lane that has not started yet, or the slot of the group
+    // this super-step computes, which load() moved to registers one
+    // super-step earlier -- so no slot in use is overwritten and the per-lane
+    // group accounting stays uniform without a spare slot
     auto issue = [&](int gi) {
       const bool ok = (unsigned)gi < (unsigned)ngroups;
       const int c = ok ? gi * 4 : 0;
-      const uint32_t dst = ring_s + (uint32_t)((ok ? (gi & (D - 1)) : D) * kNwSlotBytes);
+      const uint32_t dst = ring_s + (uint32_t)((gi & (D - 1)) * kNwSlotBytes);
       cp_async16_s(dst + 0, src0 + c);
       cp_async16_s(dst + 16, src0 + c + 2);
       cp_async16_s(dst + 32, src1 + c);
