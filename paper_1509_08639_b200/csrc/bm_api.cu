@@ -410,6 +410,16 @@ int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs&
   return BM_OK;
 }
 
+// Band-parallel extraction (launch_extract_banded): documents whose path is at
+// least BM_PAR_WALK_MIN moves long (default 8192; 0 disables), while the exit
+// maps of the plan stay within kParWalkBudget walks (one walk per band and
+// entry column; 2M ~ four 8192^2 documents, ~0.1 ms of the whole GPU).
+constexpr int64_t kParWalkBudget = 2 << 20;
+int64_t par_walk_min() {
+  static const int64_t v = getenv("BM_PAR_WALK_MIN") ? atoll(getenv("BM_PAR_WALK_MIN")) : 8192;
+  return v > 0 ? v : INT64_MAX;
+}
+
 int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* docs,
                  const bm_lexicon* lex, const Model& M, double threshold, double penalty,
                  const int64_t* rec_off, bm_record* rec, int32_t* rec_count, double* cost,
@@ -444,9 +454,61 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
     BM_CK(sc.alloc(&rl, (size_t)rt), "alloc");
     BM_CK(sc.alloc(&cl, k), "alloc");
     BM_CK(sc.upload(&idx, g.docs), "upload");
+    // long paths (n + m >= kParWalkMin) take the band-parallel extraction
+    // while the exit maps stay small next to the rest of the plan's work
+    std::vector<int32_t> big;
+    std::vector<int64_t> e_off, b_off;
+    std::vector<uint8_t> skip;
+    BandedExtract bx;
+    {
+      std::vector<int32_t> cand;
+      for (int q = 0; q < k; ++q)
+        if ((int64_t)g.n[q] + g.m[q] >= par_walk_min() && g.n[q] > 4 * kBandRows &&
+            (g.n[q] + kBandRows - 1) / kBandRows <= kGatherMaxBands)
+          cand.push_back(q);
+      std::sort(cand.begin(), cand.end(), [&](int a, int b) {
+        return (int64_t)g.n[a] + g.m[a] > (int64_t)g.n[b] + g.m[b];
+      });
+      int64_t walks = 0, et = 0, bt = 0;
+      for (int q : cand) {
+        const int nb = (g.n[q] + kBandRows - 1) / kBandRows;
+        const int64_t w = (int64_t)(nb - 1) * g.m[q];
+        if (walks + w > kParWalkBudget) break;
+        walks += w;
+        big.push_back(q);
+        e_off.push_back(et);
+        b_off.push_back(bt);
+        et += (int64_t)nb * (g.m[q] + 1);
+        bt += nb;
+        bx.max_bands = std::max(bx.max_bands, nb);
+        bx.max_exit_walks = std::max(bx.max_exit_walks, w);
+      }
+      if (!big.empty()) {
+        skip.assign(k, 0);
+        for (int q : big) skip[q] = 1;
+        bx.n_big = (int)big.size();
+        int32_t* dbig = nullptr;
+        int64_t *deo = nullptr, *dbo = nullptr;
+        BM_CK(sc.upload(&dbig, big), "upload");
+        BM_CK(sc.upload(&deo, e_off), "upload");
+        BM_CK(sc.upload(&dbo, b_off), "upload");
+        BM_CK(sc.alloc(&bx.exits, (size_t)et), "alloc");
+        BM_CK(sc.alloc(&bx.slots, (size_t)bt * kBandRows), "alloc");
+        BM_CK(sc.alloc(&bx.slot_cnt, (size_t)bt), "alloc");
+        BM_CK(sc.alloc(&bx.entry, (size_t)bt), "alloc");
+        bx.big = dbig;
+        bx.e_off = deo;
+        bx.b_off = dbo;
+      }
+    }
+    uint8_t* dskip = nullptr;
+    if (bx.n_big) BM_CK(sc.upload(&dskip, skip), "upload");
     BM_CK(launch_extract(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, k, threshold,
-                         droff, rl, cl, st),
+                         droff, rl, cl, st, dskip),
           "extract_kernel");
+    BM_CK(launch_extract_banded(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, bx,
+                                threshold, droff, rl, cl, st),
+          "band-parallel extraction");
     scatter_results_kernel<<<k, 128, 0, st>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
                                               rec_count);
     BM_CK(cudaGetLastError(), "scatter_results");

@@ -368,7 +368,16 @@ __device__ __forceinline__ double fold_cell(const bm_sentences& S, const Model& 
   return __dadd_rn(z, M.w[6]);  // w6 * 1.0
 }
 
-__global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
+#ifndef BM_SCORE_HOIST
+#define BM_SCORE_HOIST 0
+#endif
+#ifndef BM_SCORE_PAIR
+#define BM_SCORE_PAIR 0
+#endif
+#ifndef BM_SCORE_MINB
+#define BM_SCORE_MINB 4
+#endif
+__global__ void __launch_bounds__(kTileThreads, BM_SCORE_MINB) score_hits_kernel(
     bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
     const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
     const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
@@ -430,6 +439,44 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   if (small) {
     const FoldSent fb = fcols[j];
     const double w3z = __dmul_rn(M.w[3], 0.0);
+#if BM_SCORE_HOIST
+    // table bases and weights pinned in registers (opaque to the compiler, so
+    // it cannot re-load them from the constant bank in every iteration)
+    const uint64_t z64 = (uint32_t)fb.d0 >> 31;  // 0 (offsets are >= 0), opaque and per thread
+    auto pin = [&](const double* q) { return (const double*)((uintptr_t)q | z64); };
+    auto pind = [&](double v) {
+      return __longlong_as_double((long long)((uint64_t)__double_as_longlong(v) | z64));
+    };
+    ModelTables mtr = mt;
+    Model Mr = M;
+    mtr.z1 = pin(mt.z1);
+    mtr.p1 = pin(mt.p1);
+    mtr.p2 = pin(mt.p2);
+    mtr.p4 = pin(mt.p4);
+    Mr.w[3] = pind(M.w[3]);
+    Mr.w[5] = pind(M.w[5]);
+    Mr.w[6] = pind(M.w[6]);
+#define mt mtr
+#define M Mr
+#endif
+#if BM_SCORE_PAIR
+    // two rows per iteration (i and i + kRowStep): the loop's fixed work and
+    // the constant loads are shared by two independent cells
+    for (; i + kRowStep < ns; i += 2 * kRowStep, hp += 2 * hstep, op += 2 * ostep) {
+      const uint32_t hv0 = hv_next;
+      const uint32_t hv1 = __ldg(hp + hstep);
+      if (i + 2 * kRowStep < ns) hv_next = __ldg(hp + 2 * hstep);
+      const int4 fa0 = *reinterpret_cast<const int4*>(frows + i);
+      const int4 fa1 = *reinterpret_cast<const int4*>(frows + i + kRowStep);
+      const double ps0 = frows[i].pos, ps1 = frows[i + kRowStep].pos;
+      const double z0 = fold_cell(S, M, mt, w3z, (uint32_t)fa0.x, fa0.y, (uint32_t)fa0.z, ps0,
+                                  fb.tpad, fb.d0, fb.dsig, fb.pos, hv0);
+      const double z1 = fold_cell(S, M, mt, w3z, (uint32_t)fa1.x, fa1.y, (uint32_t)fa1.z, ps1,
+                                  fb.tpad, fb.d0, fb.dsig, fb.pos, hv1);
+      op[0] = bmexp::confidence_from_z(z0, exp_tab);
+      op[ostep] = bmexp::confidence_from_z(z1, exp_tab);
+    }
+#endif
     for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
       const uint32_t hv = hv_next;
       if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
@@ -440,6 +487,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
                     fb.dsig, fb.pos, hv),
           exp_tab);
     }
+#if BM_SCORE_HOIST
+#undef mt
+#undef M
+#endif
   } else {
     const SentScalars b = get_scalars(*cols, j);
     const double pos_t = cols->s[j].pos;
@@ -1032,16 +1083,19 @@ __device__ __forceinline__ void win_load(uint32_t* buf, const uint32_t* dd, int 
 // Walk the path of one document from (n, m) towards (0, 0), calling
 // visit(op, i, j) for every interior move (0-based cell (i, j)) with all lanes
 // converged; returns the position where the path reaches a border.
+// warp_walk_from: the same walk from node (i0, j0), stopping once the path
+// reaches node row i_stop (the band-parallel extraction walks one band).
 template <int WG = 32, class Visit>
-__device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int n, int m, int lane,
-                                          Visit&& visit) {
+__device__ __forceinline__ int2 warp_walk_from(uint32_t* win, const uint32_t* dd, int n, int m,
+                                               int lane, int i0, int j0, int i_stop,
+                                               Visit&& visit) {
   static_assert((WG & (WG - 1)) == 0 && WG <= 32, "window width: a power of two <= 32 groups");
   constexpr int kW = win_words<WG>();
   constexpr int kShift = WG == 32 ? 7 : WG == 16 ? 6 : WG == 8 ? 5 : WG == 4 ? 4 : WG == 2 ? 3 : 2;
   const int ngroups = (m + 3) >> 2;
   const int nbands = (n + kBandRows - 1) / kBandRows;
-  int i = n, j = m;
-  if (i == 0 || j == 0) return make_int2(i, j);
+  int i = i0, j = j0;
+  if (i <= i_stop || j == 0) return make_int2(i, j);
   int cur = 0, fl = 1, fu = 2;  // buffer roles: current, left prefetch, up prefetch
   int cb = (i - 1) / kBandRows, cw = (j - 1) >> kShift;
   win_load<WG>(win + cur * kW, dd, nbands, ngroups, cb, cw, lane);
@@ -1049,7 +1103,7 @@ __device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int
   win_load<WG>(win + fu * kW, dd, nbands, ngroups, cb - 1, cw, lane);
   asm volatile("cp.async.wait_group 2;" ::: "memory");
   __syncwarp();
-  while (i > 0 && j > 0) {
+  while (i > i_stop && j > 0) {
     const int li = i - 1, lj = j - 1;
     const int b = li / kBandRows, w = lj >> kShift;
     if (b != cb || w != cw) {
@@ -1096,6 +1150,12 @@ __device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
   return make_int2(i, j);
+}
+
+template <int WG = 32, class Visit>
+__device__ __forceinline__ int2 warp_walk(uint32_t* win, const uint32_t* dd, int n, int m, int lane,
+                                          Visit&& visit) {
+  return warp_walk_from<WG>(win, dd, n, m, lane, n, m, 0, visit);
 }
 
 __global__ void __launch_bounds__(kWalkWarps * WARP) traceback_kernel(
@@ -1165,24 +1225,14 @@ cudaError_t launch_traceback(const uint32_t* dirs, const int64_t* dir_off, const
   return counted(cudaGetLastError());
 }
 
-// Records of one document, filled back to front while walking (the walk runs
-// from the end of the path); 32 diagonal cells are gathered per batch.
-__global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
-    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
-    const double* __restrict__ S, const int64_t* __restrict__ s_off,
-    const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
-    const int32_t* __restrict__ mm, int n_docs, double threshold,
-    const int64_t* __restrict__ rec_off, bm_record* rec, int32_t* rec_count) {
-  extern __shared__ __align__(16) uint32_t walk_smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int d = blockIdx.x * kWalkWarps + wid;
-  if (d >= n_docs) return;
-  uint32_t* win = walk_smem + wid * 3 * kWinWords;
-  const int n = nn[d], m = mm[d];
-  const double* Sd = S + s_off[d];
-  const int64_t ld = pitch[d];
-  const int cap = min(n, m);
-  bm_record* out = rec + rec_off[d];
+// Records of one path segment (the walk from node (i0, j0) to node row
+// i_stop), filled back to front while walking (the walk runs from the end of
+// the path) into out[0, cap), then moved to the front; returns the count.
+// 32 diagonal cells are gathered per batch.
+__device__ __forceinline__ int extract_segment(uint32_t* win, const uint32_t* dd, const double* Sd,
+                                               int64_t ld, int n, int m, int lane, int i0, int j0,
+                                               int i_stop, double threshold, int d, bm_record* out,
+                                               int cap) {
   int nd = 0, kept = 0, ci = 0, cj = 0;
   // two-stage batches: a batch's 32 S values are loaded when it fills and
   // used when the next one fills, so the gather's latency hides behind the
@@ -1211,7 +1261,7 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
     pj = cj;
     pvalid = valid;
   };
-  warp_walk(win, dirs + dir_off[d], n, m, lane, [&](int op, int i, int j) {
+  warp_walk_from(win, dd, n, m, lane, i0, j0, i_stop, [&](int op, int i, int j) {
     if (op == BM_MOVE_D) {
       if (lane == (nd & 31)) {
         ci = i;
@@ -1232,20 +1282,222 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
     if (q < kept) out[q] = r;
     __syncwarp();
   }
+  return kept;
+}
+
+// Records of one document per warp. Documents flagged in `skip` (the long ones
+// the band-parallel extraction below takes) are left alone.
+__global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+    const double* __restrict__ S, const int64_t* __restrict__ s_off,
+    const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
+    const int32_t* __restrict__ mm, int n_docs, double threshold,
+    const int64_t* __restrict__ rec_off, bm_record* rec, int32_t* rec_count,
+    const uint8_t* __restrict__ skip) {
+  extern __shared__ __align__(16) uint32_t walk_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int d = blockIdx.x * kWalkWarps + wid;
+  if (d >= n_docs || (skip != nullptr && skip[d])) return;
+  uint32_t* win = walk_smem + wid * 3 * kWinWords;
+  const int n = nn[d], m = mm[d];
+  const int kept = extract_segment(win, dirs + dir_off[d], S + s_off[d], pitch[d], n, m, lane, n, m,
+                                   0, threshold, d, rec + rec_off[d], min(n, m));
   if (lane == 0) rec_count[d] = kept;
+}
+
+// ---------------------------------------------------------------------------
+// Band-parallel extraction of long documents. The serial walk of one long
+// path (C4: ~16k moves, ~1.1 ms for one warp) is cut at the band borders. For
+// band b and entry column x (the path enters at DP node (min(n, 128 (b+1)), x))
+// let E_b(x) be the column where the walk leaves the band (node row 128 b; 0
+// once it reaches the left border). Traceback paths never cross -- two walks
+// that meet coincide from there on -- so E_b is monotone in x, and a walk
+// starting between two walks that leave at the same column leaves there too.
+//  1. band_exit_kernel pass 0: E_b at every 16th column (and m), one thread
+//     per walk, all bands at once; walks longer than kExitMaxSteps (entries
+//     far off the path, whose gaps run along a row) give up (-1);
+//  2. pass 1: the other columns -- E_b(x1) where the neighbouring samples
+//     agree, a walk where they differ, unknown next to an unknown sample;
+//  3. band_chain_kernel: per document, the true path's entry of every band
+//     (E followed down from (n, m); an unknown entry is walked there);
+//  4. band_walk_kernel: one warp per band walks its segment exactly like
+//     extract_kernel (same codes, same S reads, same threshold), records into
+//     a per-band slot (a band holds at most 128 diagonal moves);
+//  5. band_gather_kernel: the bands' records in band order into the
+//     document's record slots -- the serial walk's records
+//     (aligner.py:176-206, 342-368).
+// ---------------------------------------------------------------------------
+constexpr int kExitStride = 16;
+constexpr int kExitMaxSteps = 1024;
+
+// the walk of band b from node (i, j) (thread-serial, one L2 load per 4x4
+// block); returns the exit column, or -1 after max_steps moves
+__device__ __forceinline__ int band_exit_walk(const uint32_t* dd, int b, int i, int j,
+                                              int max_steps) {
+  const int stop = b * kBandRows;
+  int key = -1, steps = 0;
+  uint32_t word = 0;
+  while (i > stop && j > 0) {
+    if (steps++ == max_steps) return -1;
+    const int li = i - 1, lj = j - 1;
+    const int k = ((lj >> 2) << 5) | ((li & (kBandRows - 1)) >> 2);
+    if (k != key) {
+      key = k;
+      word = __ldg(dd + k);
+    }
+    const int op = (int)((word >> (8 * (lj & 3) + 2 * (li & 3))) & 3u);
+    i -= op != BM_MOVE_GT;
+    j -= op != BM_MOVE_GS;
+  }
+  return j;
+}
+
+__global__ void __launch_bounds__(128) band_exit_kernel(
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+    const int32_t* __restrict__ nn, const int32_t* __restrict__ mm, const int32_t* __restrict__ big,
+    const int64_t* __restrict__ e_off, int32_t* __restrict__ exits, int pass) {
+  const int d = big[blockIdx.y];
+  const int n = nn[d], m = mm[d];
+  const int nb = (n + kBandRows - 1) / kBandRows;
+  const int ns = (m + kExitStride - 1) / kExitStride + 1;  // samples 0, 16, 32, ..., m
+  const int per = pass == 0 ? ns : m + 1;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)(nb - 1) * per) return;
+  const int b = 1 + (int)(t / per), k = (int)(t - (t / per) * per);
+  int32_t* E = exits + e_off[blockIdx.y] + (int64_t)b * (m + 1);
+  const int ngroups = (m + 3) >> 2;
+  const uint32_t* dd = dirs + dir_off[d] + (int64_t)b * ngroups * WARP;
+  const int i0 = min(n, (b + 1) * kBandRows);
+  if (pass == 0) {
+    const int x = min(k * kExitStride, m);
+    E[x] = band_exit_walk(dd, b, i0, x, kExitMaxSteps);
+    return;
+  }
+  const int x = k;
+  if (x % kExitStride == 0 || x == m) return;  // a sample
+  const int x1 = x - x % kExitStride, x2 = min(x1 + kExitStride, m);
+  const int e1 = E[x1], e2 = E[x2];
+  E[x] = (e1 < 0 || e2 < 0) ? -1 : e1 == e2 ? e1 : band_exit_walk(dd, b, i0, x, kExitMaxSteps);
+}
+
+// the true path's entry column of every band of one document (lane 0)
+__global__ void band_chain_kernel(const uint32_t* __restrict__ dirs,
+                                  const int64_t* __restrict__ dir_off,
+                                  const int32_t* __restrict__ nn, const int32_t* __restrict__ mm,
+                                  const int32_t* __restrict__ big,
+                                  const int64_t* __restrict__ e_off,
+                                  const int32_t* __restrict__ exits,
+                                  const int64_t* __restrict__ b_off, int32_t* __restrict__ entry) {
+  if (threadIdx.x != 0) return;
+  const int q = blockIdx.x, d = big[q];
+  const int n = nn[d], m = mm[d];
+  const int nb = (n + kBandRows - 1) / kBandRows;
+  const int ngroups = (m + 3) >> 2;
+  int32_t* en = entry + b_off[q];
+  int x = m;
+  en[nb - 1] = x;
+  for (int b = nb - 1; b >= 1; --b) {
+    int e = x > 0 ? exits[e_off[q] + (int64_t)b * (m + 1) + x] : 0;
+    if (e < 0)
+      e = band_exit_walk(dirs + dir_off[d] + (int64_t)b * ngroups * WARP, b,
+                         min(n, (b + 1) * kBandRows), x, INT_MAX);
+    en[b - 1] = x = e;
+  }
+}
+
+__global__ void __launch_bounds__(kWalkWarps * WARP) band_walk_kernel(
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
+    const double* __restrict__ S, const int64_t* __restrict__ s_off,
+    const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
+    const int32_t* __restrict__ mm, const int32_t* __restrict__ big,
+    const int32_t* __restrict__ entry, const int64_t* __restrict__ b_off, double threshold,
+    bm_record* __restrict__ slots,
+    int32_t* __restrict__ slot_cnt) {
+  extern __shared__ __align__(16) uint32_t walk_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int q = blockIdx.y, d = big[q];
+  const int n = nn[d], m = mm[d];
+  const int nb = (n + kBandRows - 1) / kBandRows;
+  const int b = blockIdx.x * kWalkWarps + wid;
+  if (b >= nb) return;
+  const int x = entry[b_off[q] + b];
+  uint32_t* win = walk_smem + wid * 3 * kWinWords;
+  bm_record* out = slots + (b_off[q] + b) * kBandRows;
+  const int kept = extract_segment(win, dirs + dir_off[d], S + s_off[d], pitch[d], n, m, lane,
+                                   min(n, (b + 1) * kBandRows), x, b * kBandRows, threshold, d, out,
+                                   kBandRows);
+  if (lane == 0) slot_cnt[b_off[q] + b] = kept;
+}
+
+__global__ void __launch_bounds__(256) band_gather_kernel(
+    const int32_t* __restrict__ nn, const int32_t* __restrict__ big,
+    const int64_t* __restrict__ b_off, const bm_record* __restrict__ slots,
+    const int32_t* __restrict__ slot_cnt, const int64_t* __restrict__ rec_off,
+    bm_record* __restrict__ rec, int32_t* __restrict__ rec_count) {
+  __shared__ int pre[kGatherMaxBands + 1];
+  const int q = blockIdx.x, d = big[q];
+  const int nb = (nn[d] + kBandRows - 1) / kBandRows;
+  const int32_t* cnt = slot_cnt + b_off[q];
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      pre[b] = acc;
+      acc += cnt[b];
+    }
+    pre[nb] = acc;
+    rec_count[d] = acc;
+  }
+  __syncthreads();
+  const bm_record* src = slots + b_off[q] * kBandRows;
+  bm_record* dst = rec + rec_off[d];
+  for (int b = threadIdx.x >> 5; b < nb; b += blockDim.x >> 5)
+    for (int k = threadIdx.x & 31; k < pre[b + 1] - pre[b]; k += WARP)
+      dst[pre[b] + k] = src[(int64_t)b * kBandRows + k];
 }
 
 cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const double* S,
                            const int64_t* s_off, const int32_t* pitch, const int32_t* n,
                            const int32_t* m, int n_docs, double thr, const int64_t* rec_off,
-                           bm_record* rec, int32_t* cnt, cudaStream_t st) {
+                           bm_record* rec, int32_t* cnt, cudaStream_t st, const uint8_t* skip) {
   if (n_docs == 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(extract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kWalkSmem);
   if (e != cudaSuccess) return e;
   extract_kernel<<<(n_docs + kWalkWarps - 1) / kWalkWarps, kWalkWarps * WARP, kWalkSmem, st>>>(
-      dirs, dir_off, S, s_off, pitch, n, m, n_docs, thr, rec_off, rec, cnt);
+      dirs, dir_off, S, s_off, pitch, n, m, n_docs, thr, rec_off, rec, cnt, skip);
   return counted(cudaGetLastError());
+}
+
+cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, const double* S,
+                                  const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+                                  const int32_t* m, const BandedExtract& bx, double thr,
+                                  const int64_t* rec_off, bm_record* rec, int32_t* cnt,
+                                  cudaStream_t st) {
+  if (bx.n_big == 0) return cudaSuccess;
+  if (bx.max_bands > kGatherMaxBands) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(band_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kWalkSmem);
+  if (e != cudaSuccess) return e;
+  // pass 0 over (bands - 1) x samples, pass 1 over (bands - 1) x (m + 1)
+  const int64_t w1 = bx.max_exit_walks, w0 = w1 / kExitStride + 2 * bx.max_bands;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t blocks = ((pass == 0 ? w0 : w1) + 127) / 128;
+    if (blocks == 0) continue;
+    band_exit_kernel<<<dim3((unsigned)blocks, bx.n_big), 128, 0, st>>>(dirs, dir_off, n, m, bx.big,
+                                                                       bx.e_off, bx.exits, pass);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  band_chain_kernel<<<bx.n_big, 32, 0, st>>>(dirs, dir_off, n, m, bx.big, bx.e_off, bx.exits,
+                                             bx.b_off, bx.entry);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  band_walk_kernel<<<dim3((bx.max_bands + kWalkWarps - 1) / kWalkWarps, bx.n_big),
+                     kWalkWarps * WARP, kWalkSmem, st>>>(dirs, dir_off, S, s_off, pitch, n, m,
+                                                         bx.big, bx.entry, bx.b_off, thr,
+                                                         bx.slots, bx.slot_cnt);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  band_gather_kernel<<<bx.n_big, 256, 0, st>>>(n, bx.big, bx.b_off, bx.slots, bx.slot_cnt, rec_off,
+                                               rec, cnt);
+  return counted(cudaGetLastError(), bx.max_exit_walks > 0 ? 5 : 3);
 }
 
 // extract_pairs for an explicit path (API primitive): gather S at the given

@@ -125,7 +125,28 @@ cudaError_t launch_traceback(const uint32_t*, const int64_t*, const int32_t*, co
                              const int64_t*, int8_t*, int32_t*, int32_t*, int32_t*, cudaStream_t);
 cudaError_t launch_extract(const uint32_t*, const int64_t*, const double*, const int64_t*,
                            const int32_t*, const int32_t*, const int32_t*, int, double,
-                           const int64_t*, bm_record*, int32_t*, cudaStream_t);
+                           const int64_t*, bm_record*, int32_t*, cudaStream_t,
+                           const uint8_t* skip = nullptr);
+// Band-parallel extraction of the long documents of a banded plan (local
+// indices big[0, n_big)); device arrays, see band_exit_kernel.
+constexpr int kGatherMaxBands = 1024;  // bands per document (n <= 131072)
+struct BandedExtract {
+  int n_big = 0;
+  int max_bands = 0;            // max bands over the big documents
+  int64_t max_exit_walks = 0;   // max (bands - 1) * m over the big documents
+  const int32_t* big = nullptr;
+  const int64_t* e_off = nullptr;   // exit-map offset per big document ((bands) x (m + 1))
+  int32_t* exits = nullptr;
+  int32_t* entry = nullptr;         // per band slot: the true path's entry column
+  const int64_t* b_off = nullptr;   // first band slot per big document
+  bm_record* slots = nullptr;       // kBandRows records per band
+  int32_t* slot_cnt = nullptr;
+};
+cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, const double* S,
+                                  const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+                                  const int32_t* m, const BandedExtract& bx, double thr,
+                                  const int64_t* rec_off, bm_record* rec, int32_t* cnt,
+                                  cudaStream_t st);
 cudaError_t launch_tune_count(const uint32_t*, const int64_t*, const double*, const int64_t*,
                               const int32_t*, const int32_t*, const int32_t*, int, const double*,
                               int, const int64_t*, const int64_t*, unsigned long long*,

@@ -115,3 +115,20 @@ def test_c3_tail_tune_vs_oracle(oracle_mod):
     wp, wh = oracle_mod.tune(oracle_mod.HostBatch(c, plex), model, pens, thrs, keys,
                              threads=os.cpu_count() or 8)
     assert np.array_equal(p, wp) and np.array_equal(h, wh)
+
+
+@pytest.mark.parametrize("seed", [2026, 7])
+def test_band_parallel_extraction_vs_oracle(seed):
+    """The band-parallel extraction (exit maps per band, one warp per band,
+    band-ordered gather) on every tail document with n > 512 and n + m >= 600
+    (BM_PAR_WALK_MIN=600 in a child process), next to serially extracted
+    documents of the same plan: records and costs equal the oracle's."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, BM_PAR_WALK_MIN="600")
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "par_walk_child.py")
+    r = subprocess.run([sys.executable, child, str(seed)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "records equal" in r.stdout
