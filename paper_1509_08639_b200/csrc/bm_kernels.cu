@@ -368,16 +368,7 @@ __device__ __forceinline__ double fold_cell(const bm_sentences& S, const Model& 
   return __dadd_rn(z, M.w[6]);  // w6 * 1.0
 }
 
-#ifndef BM_SCORE_HOIST
-#define BM_SCORE_HOIST 0
-#endif
-#ifndef BM_SCORE_PAIR
-#define BM_SCORE_PAIR 0
-#endif
-#ifndef BM_SCORE_MINB
-#define BM_SCORE_MINB 4
-#endif
-__global__ void __launch_bounds__(kTileThreads, BM_SCORE_MINB) score_hits_kernel(
+__global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
     const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
     const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
@@ -439,44 +430,6 @@ __global__ void __launch_bounds__(kTileThreads, BM_SCORE_MINB) score_hits_kernel
   if (small) {
     const FoldSent fb = fcols[j];
     const double w3z = __dmul_rn(M.w[3], 0.0);
-#if BM_SCORE_HOIST
-    // table bases and weights pinned in registers (opaque to the compiler, so
-    // it cannot re-load them from the constant bank in every iteration)
-    const uint64_t z64 = (uint32_t)fb.d0 >> 31;  // 0 (offsets are >= 0), opaque and per thread
-    auto pin = [&](const double* q) { return (const double*)((uintptr_t)q | z64); };
-    auto pind = [&](double v) {
-      return __longlong_as_double((long long)((uint64_t)__double_as_longlong(v) | z64));
-    };
-    ModelTables mtr = mt;
-    Model Mr = M;
-    mtr.z1 = pin(mt.z1);
-    mtr.p1 = pin(mt.p1);
-    mtr.p2 = pin(mt.p2);
-    mtr.p4 = pin(mt.p4);
-    Mr.w[3] = pind(M.w[3]);
-    Mr.w[5] = pind(M.w[5]);
-    Mr.w[6] = pind(M.w[6]);
-#define mt mtr
-#define M Mr
-#endif
-#if BM_SCORE_PAIR
-    // two rows per iteration (i and i + kRowStep): the loop's fixed work and
-    // the constant loads are shared by two independent cells
-    for (; i + kRowStep < ns; i += 2 * kRowStep, hp += 2 * hstep, op += 2 * ostep) {
-      const uint32_t hv0 = hv_next;
-      const uint32_t hv1 = __ldg(hp + hstep);
-      if (i + 2 * kRowStep < ns) hv_next = __ldg(hp + 2 * hstep);
-      const int4 fa0 = *reinterpret_cast<const int4*>(frows + i);
-      const int4 fa1 = *reinterpret_cast<const int4*>(frows + i + kRowStep);
-      const double ps0 = frows[i].pos, ps1 = frows[i + kRowStep].pos;
-      const double z0 = fold_cell(S, M, mt, w3z, (uint32_t)fa0.x, fa0.y, (uint32_t)fa0.z, ps0,
-                                  fb.tpad, fb.d0, fb.dsig, fb.pos, hv0);
-      const double z1 = fold_cell(S, M, mt, w3z, (uint32_t)fa1.x, fa1.y, (uint32_t)fa1.z, ps1,
-                                  fb.tpad, fb.d0, fb.dsig, fb.pos, hv1);
-      op[0] = bmexp::confidence_from_z(z0, exp_tab);
-      op[ostep] = bmexp::confidence_from_z(z1, exp_tab);
-    }
-#endif
     for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
       const uint32_t hv = hv_next;
       if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
@@ -487,10 +440,6 @@ __global__ void __launch_bounds__(kTileThreads, BM_SCORE_MINB) score_hits_kernel
                     fb.dsig, fb.pos, hv),
           exp_tab);
     }
-#if BM_SCORE_HOIST
-#undef mt
-#undef M
-#endif
   } else {
     const SentScalars b = get_scalars(*cols, j);
     const double pos_t = cols->s[j].pos;
