@@ -811,6 +811,13 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     BM_CK(cudaStreamWaitEvent(ss[2], e0, 0), "event");
     cudaEventDestroy(e0);
   }
+  // BM_TRACE: GPU timeline of the groups (both tiers done, relative to the start)
+  cudaEvent_t tl0 = nullptr;
+  std::vector<cudaEvent_t> tl_a, tl_b;
+  if (tr.on) {
+    cudaEventCreate(&tl0);
+    cudaEventRecord(tl0, st);
+  }
   int unit = 0;
   for (int d0 = 0; d0 < nd;) {
     int d1 = d0;
@@ -821,8 +828,30 @@ int bm_mine(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
                         rec_off, rec, rec_count, cost, d0, d1, tr, ss[unit % 3],
                         ss[(unit + 1) % 3]);
     if (rc) return rc;
+    if (tr.on) {
+      cudaEvent_t ea, eb;
+      cudaEventCreate(&ea);
+      cudaEventCreate(&eb);
+      cudaEventRecord(ea, ss[unit % 3]);
+      cudaEventRecord(eb, ss[(unit + 1) % 3]);
+      tl_a.push_back(ea);
+      tl_b.push_back(eb);
+    }
     unit += 2;
     d0 = d1;
+  }
+  if (tr.on) {
+    tr.mark("groups enqueued");
+    cudaDeviceSynchronize();
+    for (size_t q = 0; q < tl_a.size(); ++q) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, tl0, tl_a[q]);
+      cudaEventElapsedTime(&b, tl0, tl_b[q]);
+      fprintf(stderr, "[bm trace] gpu group %2zu  fused tier %8.3f ms  banded tier %8.3f ms\n", q, a, b);
+      cudaEventDestroy(tl_a[q]);
+      cudaEventDestroy(tl_b[q]);
+    }
+    cudaEventDestroy(tl0);
   }
   return BM_OK;
 }
@@ -1146,7 +1175,7 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   std::vector<int> ch_d0, ch_d1;
   std::vector<cudaEvent_t> ch_ev;
   // BM_TRACE: GPU timeline (copy done / mined per chunk, relative to t_start)
-  std::vector<cudaEvent_t> tl_copy, tl_mine;
+  std::vector<cudaEvent_t> tl_copy, tl_mine, tl_start, tl_fused;
   cudaEvent_t tl0 = nullptr;
   if (tr.on) {
     cudaEventCreate(&tl0);
@@ -1246,7 +1275,7 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   if (planned == nullptr) return fail(BM_ECUDA, "event create failed");
   BM_CK(cudaEventRecord(planned, st), "event");
   static const int n_ms = std::max(1, std::min(kMaxMineStreams,
-      getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 4));
+      getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 3));
   std::vector<cudaStream_t> ms(1, st);
   for (int q = 1; q < n_ms; ++q) {
     ms.push_back(side_stream(q));
@@ -1258,8 +1287,12 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   auto enqueue_kernels = [&](size_t kc) -> int {
     const int d0 = chunks[kc].d0, d1 = chunks[kc].d1, lo = chunks[kc].lo, hi = chunks[kc].hi;
     cudaEvent_t ev = chunks[kc].copied;
-    cudaStream_t sk = ms[(ch_d0.size() + 1) % ms.size()];  // chunk 0 on a side stream
-    cudaStream_t sb = ms.size() > 1 ? ms[(ch_d0.size() + 2) % ms.size()] : sk;
+    // like bm_mine's groups: chunk k's tiers on streams 2k+1, 2k+2 (mod the
+    // stream count), so a chunk's fused tier never queues behind the banded
+    // tier of the chunk just before it (chunk 0 on a side stream)
+    const size_t u = 2 * ch_d0.size() + 1;
+    cudaStream_t sk = ms[u % ms.size()];
+    cudaStream_t sb = ms.size() > 1 ? ms[(u + 1) % ms.size()] : sk;
     BM_CK(cudaStreamWaitEvent(sk, ev, 0), "event");
     // the copy stream only moves bytes: widening the wire arrays is a few
     // microseconds of compute and runs in order on the compute stream (on the
@@ -1281,16 +1314,28 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
       BM_CK(cudaEventRecord(ready_b, sk), "event");
       BM_CK(cudaStreamWaitEvent(sb, ready_b, 0), "event");
     }
+    if (tr.on) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, sk);
+      tl_start.push_back(e);
+    }
     {
       int rc = mine_group(&sd, &dd, dh->n, dh->m, amax.data(), &ld, M, threshold, penalty, droff,
                           rec, cnt, cost, d0, d1, tr, sk, sb);
       if (rc) return rc;
     }
-    if (sb != sk) {  // compaction after both tiers
-      cudaEvent_t done_b = joiner.event();
-      if (done_b == nullptr) return fail(BM_ECUDA, "event create failed");
-      BM_CK(cudaEventRecord(done_b, sb), "event");
-      BM_CK(cudaStreamWaitEvent(sk, done_b, 0), "event");
+    if (tr.on) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, sk);
+      tl_fused.push_back(e);
+    }
+    if (sb != sk) {  // compaction after both tiers, behind the banded tier
+      cudaEvent_t done_f = joiner.event();
+      if (done_f == nullptr) return fail(BM_ECUDA, "event create failed");
+      BM_CK(cudaEventRecord(done_f, sk), "event");
+      BM_CK(cudaStreamWaitEvent(sb, done_f, 0), "event");
     }
     // compact the chunk into its own region of `dense` (starting at its first
     // document's record slot) and fetch its record count; the host copies the
@@ -1299,13 +1344,13 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
       const int kq = (int)ch_d0.size();
       // chunk kq's scan scratch: [d0 + kq, d1 + kq] (>= its block count + 1)
       BM_CK(launch_compact(rec, droff + d0, cnt + d0, d1 - d0, doff + d0, ctot + kq,
-                           dense + roff[d0], bsum_all + d0 + kq, sk, d0),
+                           dense + roff[d0], bsum_all + d0 + kq, sb, d0),
             "compact");
-      BM_CK(cudaMemcpyAsync(hcnt + kq, ctot + kq, sizeof(int64_t), cudaMemcpyDeviceToHost, sk),
+      BM_CK(cudaMemcpyAsync(hcnt + kq, ctot + kq, sizeof(int64_t), cudaMemcpyDeviceToHost, sb),
             "d2h");
       cudaEvent_t ce = joiner.event();
       if (ce == nullptr) return fail(BM_ECUDA, "event create failed");
-      BM_CK(cudaEventRecord(ce, sk), "event");
+      BM_CK(cudaEventRecord(ce, sb), "event");
       ch_d0.push_back(d0);
       ch_d1.push_back(d1);
       ch_ev.push_back(ce);
@@ -1313,16 +1358,24 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
     if (tr.on) {
       cudaEvent_t e;
       cudaEventCreate(&e);
-      cudaEventRecord(e, sk);
+      cudaEventRecord(e, sb);
       tl_mine.push_back(e);
     }
     return BM_OK;
   };
+  // the bulk copies run kCopyAhead chunks ahead of the kernels enqueued so
+  // far: the copy engine serves H2D copies in submission order, so a chunk's
+  // small plan uploads (on its mining stream) would otherwise queue behind all
+  // of the batch's bulk copies (C3 1M: the first chunks' kernels waited ~70 ms)
+  static const size_t kCopyAhead =
+      getenv("BM_COPY_AHEAD") ? (size_t)atoll(getenv("BM_COPY_AHEAD")) : 1;
+  if (int rc = enqueue_copies(1 + kCopyAhead)) return rc;
   if (int rc = enqueue_kernels(0)) return rc;
-  if (int rc = enqueue_copies(SIZE_MAX)) return rc;
-  tr.mark("copies enqueued");
-  for (size_t kc = 1; kc < chunks.size(); ++kc)
+  for (size_t kc = 1; kc < chunks.size(); ++kc) {
+    if (int rc = enqueue_copies(kc + 1 + kCopyAhead)) return rc;
     if (int rc = enqueue_kernels(kc)) return rc;
+  }
+  tr.mark("copies enqueued");
   // join the side streams back into the caller's stream
   BM_CK(joiner.join(), "stream join");
   tr.mark("chunks enqueued");
@@ -1346,12 +1399,17 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   tr.mark("records d2h");
   if (tr.on) {
     for (size_t q = 0; q < tl_copy.size(); ++q) {
-      float a = 0.f, b = 0.f;
+      float a = 0.f, b = 0.f, c = 0.f, f = 0.f;
       cudaEventElapsedTime(&a, tl0, tl_copy[q]);
+      cudaEventElapsedTime(&c, tl0, tl_start[q]);
+      cudaEventElapsedTime(&f, tl0, tl_fused[q]);
       cudaEventElapsedTime(&b, tl0, tl_mine[q]);
-      fprintf(stderr, "[bm trace] gpu chunk %2zu copied %8.3f ms  mined %8.3f ms\n", q, a, b);
+      fprintf(stderr, "[bm trace] gpu chunk %2zu copied %8.3f ms  started %8.3f  fused %8.3f  mined %8.3f ms\n",
+              q, a, c, f, b);
       cudaEventDestroy(tl_copy[q]);
       cudaEventDestroy(tl_mine[q]);
+      cudaEventDestroy(tl_start[q]);
+      cudaEventDestroy(tl_fused[q]);
     }
     cudaEventDestroy(tl0);
   }
