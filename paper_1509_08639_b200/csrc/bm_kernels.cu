@@ -242,16 +242,34 @@ __global__ void __launch_bounds__(kTileThreads, 2) score_tile_kernel(
 // most 65535 sentences per side (16-bit counts / owners); otherwise callers
 // keep score_tile_kernel.
 // ---------------------------------------------------------------------------
-constexpr int kJoinSentChunk = 128;
+// The document-level join's table: kDocJoinEmax bucketed entries of the
+// indexed side per pass (kJoinSentChunk sentences per item); every probe-side
+// entry is looked up once per table, so larger tables mean fewer probes.
+#ifndef BM_DOC_JOIN_EMAX
+#define BM_DOC_JOIN_EMAX 2048
+#endif
+#ifndef BM_DOC_JOIN_SENT
+#define BM_DOC_JOIN_SENT 256
+#endif
+constexpr int kDocJoinEmax = BM_DOC_JOIN_EMAX;
+#ifndef BM_DOC_JOIN_BDIV
+#define BM_DOC_JOIN_BDIV 2
+#endif
+constexpr int kDocJoinBuckets = kDocJoinEmax / BM_DOC_JOIN_BDIV;
+constexpr int kJoinSentChunk = BM_DOC_JOIN_SENT;
+static_assert((kDocJoinEmax & (kDocJoinEmax - 1)) == 0, "table size must be a power of two");
 #ifndef BM_JOIN_PROBE_CHUNK
 #define BM_JOIN_PROBE_CHUNK 1024
 #endif
 constexpr int kJoinProbeChunk = BM_JOIN_PROBE_CHUNK;  // probe-side sentences per item
 
 #ifndef BM_HITS_DOC_MINB
-#define BM_HITS_DOC_MINB 12
+#define BM_HITS_DOC_MINB 7
 #endif
-__global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sentences S, bm_docs D, bm_lexicon L,
+#ifndef BM_HITS_DOC_THREADS
+#define BM_HITS_DOC_THREADS 128
+#endif
+__global__ void __launch_bounds__(BM_HITS_DOC_THREADS, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sentences S, bm_docs D, bm_lexicon L,
                                                          const int4* __restrict__ items,
                                                          int n_items,
                                                          const int64_t* __restrict__ h_off,
@@ -264,9 +282,9 @@ __global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sente
   const int d = it.x, dir = it.y & 1, k0 = it.z, k1 = it.w;
   const int n = D.n[d], m = D.m[d];
   const int s0 = D.src0[d], t0 = D.tgt0[d];
-  JoinSmem js = carve_join(smem);
-  uint16_t* chunk_owner = (uint16_t*)(smem + align16(join_smem_bytes()));
-  uint16_t* a_owner = chunk_owner + kJoinEmax;
+  JoinSmem js = carve_join(smem, kDocJoinEmax, kDocJoinBuckets);
+  uint16_t* chunk_owner = (uint16_t*)(smem + align16(join_smem_bytes(kDocJoinEmax, kDocJoinBuckets)));
+  uint16_t* a_owner = chunk_owner + kDocJoinEmax;
   uint32_t* hd = hits + h_off[d];
   const int a0 = dir == 0 ? s0 : t0, b0 = dir == 0 ? t0 : s0;
   const int na_all = dir == 0 ? n : m, nb = dir == 0 ? m : n;
@@ -277,8 +295,8 @@ __global__ void __launch_bounds__(64, BM_HITS_DOC_MINB) hits_doc_kernel(bm_sente
   const int32_t* off = dir == 0 ? L.fwd_off : L.rev_off;
   const int32_t* cand = dir == 0 ? L.fwd_cand : L.rev_cand;
   const int c_end = __ldg(offB + k1);
-  for (int c0 = __ldg(offB + k0); c0 < c_end; c0 += kJoinEmax) {
-    const int c1 = min(c_end, c0 + kJoinEmax);
+  for (int c0 = __ldg(offB + k0); c0 < c_end; c0 += kDocJoinEmax) {
+    const int c1 = min(c_end, c0 + kDocJoinEmax);
     if (dir == 0)
       join_chunk_entries(CtaGroup(), S, off, cand, offA, na, offB, b0, nb, c0, c1, js, chunk_owner,
                          a_owner, [&](int ls, int lt, int w) {
@@ -452,7 +470,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   }
 }
 
-size_t hits_doc_smem_bytes() { return align16(join_smem_bytes()) + (size_t)kJoinEmax * 4; }
+size_t hits_doc_smem_bytes() {
+  return align16(join_smem_bytes(kDocJoinEmax, kDocJoinBuckets)) + (size_t)kDocJoinEmax * 4;
+}
 
 // Items of the document-level join for local docs 0..nd-1 (host side).
 void join_items(const int32_t* n, const int32_t* m, int nd, std::vector<int4>& items) {
@@ -479,7 +499,7 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
   cudaError_t e = cudaFuncSetAttribute(hits_doc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)hs);
   if (e != cudaSuccess) return e;
-  if (n_items) hits_doc_kernel<<<n_items, 64, hs, st>>>(S, D, L, items, n_items, h_off, hits);
+  if (n_items) hits_doc_kernel<<<n_items, BM_HITS_DOC_THREADS, hs, st>>>(S, D, L, items, n_items, h_off, hits);
   const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars) + 2 * kTile * sizeof(FoldSent);
   score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits, h_off,
                                                        out);

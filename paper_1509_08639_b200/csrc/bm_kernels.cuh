@@ -38,9 +38,9 @@ struct WorkItem {
   int32_t band;
 };
 
-__host__ __device__ constexpr size_t join_smem_bytes() {
-  return (size_t)kJoinEmax * 4 + (size_t)kJoinEmax * 2 + (size_t)(kJoinBuckets + 1) * 4 +
-         (size_t)kJoinBuckets * 4;
+__host__ __device__ constexpr size_t join_smem_bytes(int emax = kJoinEmax,
+                                                     int buckets = kJoinBuckets) {
+  return (size_t)emax * 4 + (size_t)emax * 2 + (size_t)(buckets + 1) * 4 + (size_t)buckets * 4;
 }
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
@@ -50,18 +50,19 @@ __device__ __forceinline__ void stage_exp_table(uint64_t* dst, int rank, int siz
   for (int k = rank; k < kExpTableWords; k += size) dst[k] = g_exp_table[k];
 }
 
-__device__ __forceinline__ JoinSmem carve_join(uint8_t* p) {
+__device__ __forceinline__ JoinSmem carve_join(uint8_t* p, int emax = kJoinEmax,
+                                               int buckets = kJoinBuckets) {
   JoinSmem js;
   js.key = (int32_t*)p;
-  p += kJoinEmax * 4;
+  p += emax * 4;
   js.bstart = (int32_t*)p;
-  p += (kJoinBuckets + 1) * 4;
+  p += (buckets + 1) * 4;
   js.bfill = (int32_t*)p;
-  p += kJoinBuckets * 4;
+  p += buckets * 4;
   js.owner = (uint16_t*)p;
-  js.emax = kJoinEmax;
-  js.nbuckets = kJoinBuckets;
-  js.bshift = 32 - ilog2(kJoinBuckets);
+  js.emax = emax;
+  js.nbuckets = buckets;
+  js.bshift = 32 - ilog2(buckets);
   return js;
 }
 
