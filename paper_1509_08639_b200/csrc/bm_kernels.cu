@@ -448,15 +448,26 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   if (small) {
     const FoldSent fb = fcols[j];
     const double w3z = __dmul_rn(M.w[3], 0.0);
+    // the staged rows and the exp table read through 32-bit shared-window
+    // addresses (ld.shared): no generic-to-shared conversion in the cell loop
+    // (+ z, a per-thread zero the compiler cannot see through, so the bases
+    // stay in registers instead of being recomputed in every iteration)
+    const uint32_t z = (uint32_t)fb.d0 >> 31;
+    const bmexp::SmemTab tab{(uint32_t)__cvta_generic_to_shared(exp_tab) + z};
+    const uint32_t frows_s = (uint32_t)__cvta_generic_to_shared(frows) + z;
     for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
       const uint32_t hv = hv_next;
       if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
-      const int4 fa = *reinterpret_cast<const int4*>(frows + i);
-      const double pos_s = frows[i].pos;
+      int4 fa;
+      double pos_s;
+      const uint32_t ra = frows_s + (uint32_t)i * (uint32_t)sizeof(FoldSent);
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(fa.x), "=r"(fa.y), "=r"(fa.z), "=r"(fa.w) : "r"(ra));
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(pos_s) : "r"(ra + 16u));
       *op = bmexp::confidence_from_z(
           fold_cell(S, M, mt, w3z, (uint32_t)fa.x, fa.y, (uint32_t)fa.z, pos_s, fb.tpad, fb.d0,
                     fb.dsig, fb.pos, hv),
-          exp_tab);
+          tab);
     }
   } else {
     const SentScalars b = get_scalars(*cols, j);

@@ -120,7 +120,24 @@ __constant__ double c_exp_k[8] = {0x1.71547652b82fep7,  0x1.8p52,
 
 // T: the 256-entry table (glibc_exp_table.h); on the GPU it is staged in
 // shared memory because lanes index it divergently.
-BM_HD double exp_glibc(double x, const uint64_t* T) {
+// Table access: a plain pointer (host, global or generic shared memory), or on
+// the device a 32-bit shared-window address read with ld.shared (the cell
+// loops of the scoring kernels: no generic-to-shared conversion per lookup).
+BM_HD void tab_pair(const uint64_t* T, uint32_t i, uint64_t& a, uint64_t& b) {
+  a = T[i];
+  b = T[i + 1];
+}
+#if defined(__CUDACC__)
+struct SmemTab {
+  uint32_t addr;  // __cvta_generic_to_shared of the staged table
+};
+__device__ __forceinline__ void tab_pair(SmemTab T, uint32_t i, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(T.addr + i * 8u));
+}
+#endif
+
+template <class Tab>
+BM_HD double exp_glibc(double x, Tab T) {
   const double InvLn2N = BM_EXPK(0, 0x1.71547652b82fep7);
   const double Shift = BM_EXPK(1, 0x1.8p52);
   const double NegLn2hiN = BM_EXPK(2, -0x1.62e42fefa0000p-8);
@@ -148,8 +165,10 @@ BM_HD double exp_glibc(double x, const uint64_t* T) {
   r = fma_(kd, NegLn2loN, r);
   uint32_t idx = 2u * (uint32_t)(ki & 127u);
   uint64_t top = ki << 45;
-  double tail = asdbl(T[idx]);
-  uint64_t sbits = T[idx + 1] + top;
+  uint64_t w0, w1;
+  tab_pair(T, idx, w0, w1);
+  double tail = asdbl(w0);
+  uint64_t sbits = w1 + top;
   double r2 = mul_(r, r);
   double p23 = fma_(r, C3, C2);
   double p45 = fma_(r, C5, C4);
@@ -164,7 +183,8 @@ BM_HD double exp_glibc(double x, const uint64_t* T) {
 // bimine/classifier.py:100-117: sigmoid, then clamp into [1e-300, 1-2^-53]
 // with Python's min/max semantics (first argument wins unless strictly beaten).
 // The unclamped sigmoid (classifier.py:100-104), p in [0, 1] or NaN.
-BM_HD double sigmoid_glibc(double z, const uint64_t* T) {
+template <class Tab>
+BM_HD double sigmoid_glibc(double z, Tab T) {
   // Branch-free form of the two sigmoid branches: exactly one exp and one
   // division per call, so lanes of a warp with mixed signs do not execute both.
   //   z >= 0: 1 / (1 + exp(-z))      z < 0 (or NaN): exp(z) / (1 + exp(z))
@@ -178,7 +198,8 @@ BM_HD double sigmoid_glibc(double z, const uint64_t* T) {
 #endif
 }
 
-BM_HD double confidence_from_z(double z, const uint64_t* T) {
+template <class Tab>
+BM_HD double confidence_from_z(double z, Tab T) {
   const double p = sigmoid_glibc(z, T);
   const double PMIN = 1e-300;
   const double PMAX = 1.0 - 0x1p-53;
@@ -188,7 +209,8 @@ BM_HD double confidence_from_z(double z, const uint64_t* T) {
 
 // 1 - confidence_from_z(z): the DP's diagonal cost. The lower clamp is not
 // needed here: for 0 <= p < 2^-54 both 1 - p and 1 - 1e-300 round to 1.0.
-BM_HD double one_minus_confidence(double z, const uint64_t* T) {
+template <class Tab>
+BM_HD double one_minus_confidence(double z, Tab T) {
   const double p = sigmoid_glibc(z, T);
   const double PMAX = 1.0 - 0x1p-53;
   return sub_(1.0, (PMAX < p) ? PMAX : p);
