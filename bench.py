@@ -578,35 +578,18 @@ class TuneWorkload:
     def e2e_setup(self):
         from paper_1509_08639_b200 import hostapi
 
-        torch = self.ctx.torch
-        names = ("n_tok", "n_punct", "n_alpha", "tok_off", "tok_id", "tok_alpha", "dig_off",
-                 "dig_id")
-        self.host = {k: hostapi._pinned(getattr(self.c, k)) for k in names}
-        self.host_gold = (hostapi._pinned(self.gk), hostapi._pinned(self.goff))
-        self.h2d = sum(v[1].nbytes for v in self.host.values()) + self.gk.nbytes + self.goff.nbytes
+        self.tp = hostapi.TunePinned(self.c, self.gk, self.goff)
+        self.h2d = self.tp.h2d_bytes
         self.d2h = 2 * len(C5_PENS) * len(C5_THRS) * 8
-        self.dev_bufs = {k: torch.empty(v[1].nbytes, dtype=torch.uint8, device=self.ctx.dev)
-                         for k, v in self.host.items()}
 
     def e2e_step(self):
-        """Host arrays -> device (pinned H2D) -> bm_tune -> counts to the host ->
-        precision/recall/F1 of every grid point (tuner.py:67-84, 134-147)."""
-        from paper_1509_08639_b200 import engine, tuner
-        from paper_1509_08639_b200 import _native as N
+        """Page-locked host dev set -> device, chunk by chunk, each chunk's copy
+        overlapping the previous chunk's bm_tune (hostapi.tune_pinned) -> counts
+        to the host -> precision/recall/F1 of every grid point
+        (tuner.py:67-84, 134-147)."""
+        from paper_1509_08639_b200 import hostapi, tuner
 
-        torch = self.ctx.torch
-        for k, (t, v) in self.host.items():
-            self.dev_bufs[k].copy_(t, non_blocking=True)
-        sent = N.Sentences(self.c.n_sent, *[int(self.dev_bufs[k].data_ptr()) for k in (
-            "n_tok", "n_punct", "n_alpha", "tok_off", "tok_id", "tok_alpha", "dig_off", "dig_id")])
-        gk = self.host_gold[0][0].to(self.ctx.dev, non_blocking=True)
-        go = self.host_gold[1][0].to(self.ctx.dev, non_blocking=True)
-        gold = engine.DeviceGold.__new__(engine.DeviceGold)
-        gold.keys, gold.goff = gk, go
-        dc = engine.DeviceCorpus(self.c, self.dev_bufs, sent, self.dc.max_tok)
-        pred, hit = engine.tune_counts_device(dc, self.dl, self.view, self.ctx.model, C5_PENS,
-                                              C5_THRS, gold)
-        p, h = pred.cpu().numpy(), hit.cpu().numpy()
+        p, h = hostapi.tune_pinned(self.tp, self.dl, self.ctx.model, C5_PENS, C5_THRS)
         n_gold = int(self.gk.size)
         trace = [tuner._prf(int(p[a, b]), n_gold, int(h[a, b]))
                  for b in range(len(C5_THRS)) for a in range(len(C5_PENS))]
@@ -718,7 +701,8 @@ def measure(ctx: Ctx, name: str, steps: int, warmup: int, cpu: bool, fp64: dict)
         "records_per_step": n_rec, "roofline": roof, "roofline_dp_alu": dp,
         "e2e": {"value": gdocs * steps / (e_tot / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": ("host arrays -> pinned H2D -> bm_tune -> counts D2H -> P/R/F1"
+                "path": ("hostapi.tune_pinned: page-locked dev set -> chunked H2D overlapping "
+                         "bm_tune per chunk -> counts D2H -> P/R/F1"
                          if name == "c5" else
                          "bm_mine_host_*: pinned host buffers -> H2D -> mine -> compact -> D2H"
                          + (" -> NCCL gather -> bm_merge_shards on rank 0" if ctx.world > 1

@@ -51,23 +51,44 @@ constexpr int kMaxMineStreams = 4;
 // a page-locked block first; a block is reused once the event recorded after
 // its copy has completed.
 // (The blocks live as long as the thread: no CUDA calls at process teardown.)
+// Plan uploads are copied by a kernel that reads the page-locked block over
+// the bus (mapped through unified addressing), not by the copy engine: the
+// engine serves H2D copies of all streams in submission order, so an upload
+// queued on a busy stream behind its kernels would hold up the bulk copies of
+// another stream submitted after it (and those would hold up the next plan
+// upload), serialising copies and kernels (hostapi.tune_pinned: 31 + 38 ms).
+__global__ void h2d_plan_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t n16,
+                                const uint8_t* __restrict__ src_b, uint8_t* __restrict__ dst_b,
+                                int tail) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n16; k += stride)
+    dst[k] = src[k];
+  if (blockIdx.x == 0 && (int)threadIdx.x < tail) dst_b[threadIdx.x] = src_b[threadIdx.x];
+}
+
 class PinnedPool {
  public:
   // copies bytes into a free block and enqueues the H2D copy on st
   cudaError_t upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     Block* blk = nullptr;
-    for (Block& b : blocks_)
+    // blocks are taken round robin (their uploads complete roughly in order),
+    // so the search usually stops at the first block it queries
+    const size_t nb = blocks_.size();
+    for (size_t q = 0; q < nb && blk == nullptr; ++q) {
+      Block& b = blocks_[(next_ + q) % nb];
       if (b.cap >= bytes && cudaEventQuery(b.ev) == cudaSuccess) {
         blk = &b;
-        break;
+        next_ = (next_ + q + 1) % nb;
       }
+    }
     if (blk == nullptr) {
-      size_t cap = 1 << 16;
+      size_t cap = 1 << 12;
       while (cap < bytes) cap <<= 1;
       Block b;
-      cudaError_t e = cudaHostAlloc((void**)&b.p, cap, cudaHostAllocDefault);
+      cudaError_t e = cudaHostAlloc((void**)&b.p, cap, cudaHostAllocMapped | cudaHostAllocPortable);
       if (e != cudaSuccess) return e;
-      e = cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming);
+      e = cudaHostGetDevicePointer((void**)&b.d, b.p, 0);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming);
       if (e != cudaSuccess) {
         cudaFreeHost(b.p);
         return e;
@@ -77,18 +98,34 @@ class PinnedPool {
       blk = &blocks_.back();
     }
     memcpy(blk->p, src, bytes);
-    cudaError_t e = cudaMemcpyAsync(dst, blk->p, bytes, cudaMemcpyHostToDevice, st);
+    cudaError_t e;
+    static const bool by_kernel =
+        getenv("BM_PLAN_COPY_KERNEL") ? atoi(getenv("BM_PLAN_COPY_KERNEL")) != 0 : true;
+    if (by_kernel && ((uintptr_t)dst & 15) == 0) {
+      const size_t n16 = bytes / 16;
+      const int tail = (int)(bytes - n16 * 16);
+      const int grid = (int)std::min<size_t>(256, std::max<size_t>(1, (n16 + 255) / 256));
+      h2d_plan_kernel<<<grid, 256, 0, st>>>((const uint4*)blk->d, (uint4*)dst, n16,
+                                            (const uint8_t*)blk->d + n16 * 16,
+                                            (uint8_t*)dst + n16 * 16, tail);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) bm::g_launches += 1;
+    } else {
+      e = cudaMemcpyAsync(dst, blk->p, bytes, cudaMemcpyHostToDevice, st);
+    }
     if (e != cudaSuccess) return e;
     return cudaEventRecord(blk->ev, st);
   }
 
  private:
   struct Block {
-    char* p = nullptr;
+    char* p = nullptr;  // host address
+    char* d = nullptr;  // device address of the mapped block
     size_t cap = 0;
     cudaEvent_t ev = nullptr;
   };
   std::deque<Block> blocks_;  // stable addresses
+  size_t next_ = 0;
 };
 
 PinnedPool& pinned_pool() {
@@ -118,8 +155,7 @@ class Scratch {
     cudaError_t e = alloc(out, v.size());
     if (e != cudaSuccess || v.empty()) return e;
     const size_t bytes = v.size() * sizeof(T);
-    if (bytes >= (1 << 16)) return pinned_pool().upload(*out, v.data(), bytes, st_);
-    return cudaMemcpyAsync(*out, v.data(), bytes, cudaMemcpyHostToDevice, st_);
+    return pinned_pool().upload(*out, v.data(), bytes, st_);
   }
 
  private:
@@ -1275,7 +1311,7 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   if (planned == nullptr) return fail(BM_ECUDA, "event create failed");
   BM_CK(cudaEventRecord(planned, st), "event");
   static const int n_ms = std::max(1, std::min(kMaxMineStreams,
-      getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 3));
+      getenv("BM_MINE_STREAMS") ? atoi(getenv("BM_MINE_STREAMS")) : 4));
   std::vector<cudaStream_t> ms(1, st);
   for (int q = 1; q < n_ms; ++q) {
     ms.push_back(side_stream(q));
@@ -1287,12 +1323,15 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
   auto enqueue_kernels = [&](size_t kc) -> int {
     const int d0 = chunks[kc].d0, d1 = chunks[kc].d1, lo = chunks[kc].lo, hi = chunks[kc].hi;
     cudaEvent_t ev = chunks[kc].copied;
-    // like bm_mine's groups: chunk k's tiers on streams 2k+1, 2k+2 (mod the
-    // stream count), so a chunk's fused tier never queues behind the banded
-    // tier of the chunk just before it (chunk 0 on a side stream)
-    const size_t u = 2 * ch_d0.size() + 1;
+    // chunk k: fused tier on stream k + 1, banded tier on stream k + 3 (mod
+    // the stream count): every stream takes fused tiers in turn, and a chunk's
+    // fused tier queues behind the banded tier of the chunk two before it, not
+    // the one just before (chunk 0 on a side stream). The chunk's compaction
+    // follows its fused tier on the same stream once the banded tier is done.
+    const size_t u = ch_d0.size() + 1;
     cudaStream_t sk = ms[u % ms.size()];
-    cudaStream_t sb = ms.size() > 1 ? ms[(u + 1) % ms.size()] : sk;
+    cudaStream_t sb = ms.size() > 1 ? ms[(u + (ms.size() > 2 ? 2 : 1)) % ms.size()] : sk;
+    cudaStream_t sc_ = sk, so_ = sb;
     BM_CK(cudaStreamWaitEvent(sk, ev, 0), "event");
     // the copy stream only moves bytes: widening the wire arrays is a few
     // microseconds of compute and runs in order on the compute stream (on the
@@ -1331,11 +1370,11 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
       cudaEventRecord(e, sk);
       tl_fused.push_back(e);
     }
-    if (sb != sk) {  // compaction after both tiers, behind the banded tier
+    if (sb != sk) {  // compaction after both tiers
       cudaEvent_t done_f = joiner.event();
       if (done_f == nullptr) return fail(BM_ECUDA, "event create failed");
-      BM_CK(cudaEventRecord(done_f, sk), "event");
-      BM_CK(cudaStreamWaitEvent(sb, done_f, 0), "event");
+      BM_CK(cudaEventRecord(done_f, so_), "event");
+      BM_CK(cudaStreamWaitEvent(sc_, done_f, 0), "event");
     }
     // compact the chunk into its own region of `dense` (starting at its first
     // document's record slot) and fetch its record count; the host copies the
@@ -1344,13 +1383,13 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
       const int kq = (int)ch_d0.size();
       // chunk kq's scan scratch: [d0 + kq, d1 + kq] (>= its block count + 1)
       BM_CK(launch_compact(rec, droff + d0, cnt + d0, d1 - d0, doff + d0, ctot + kq,
-                           dense + roff[d0], bsum_all + d0 + kq, sb, d0),
+                           dense + roff[d0], bsum_all + d0 + kq, sc_, d0),
             "compact");
-      BM_CK(cudaMemcpyAsync(hcnt + kq, ctot + kq, sizeof(int64_t), cudaMemcpyDeviceToHost, sb),
+      BM_CK(cudaMemcpyAsync(hcnt + kq, ctot + kq, sizeof(int64_t), cudaMemcpyDeviceToHost, sc_),
             "d2h");
       cudaEvent_t ce = joiner.event();
       if (ce == nullptr) return fail(BM_ECUDA, "event create failed");
-      BM_CK(cudaEventRecord(ce, sb), "event");
+      BM_CK(cudaEventRecord(ce, sc_), "event");
       ch_d0.push_back(d0);
       ch_d1.push_back(d1);
       ch_ev.push_back(ce);
@@ -1358,7 +1397,7 @@ static int mine_host_impl(const HostSource& src, const bm_docs* dh, const bm_lex
     if (tr.on) {
       cudaEvent_t e;
       cudaEventCreate(&e);
-      cudaEventRecord(e, sb);
+      cudaEventRecord(e, sc_);
       tl_mine.push_back(e);
     }
     return BM_OK;

@@ -154,3 +154,161 @@ def mine_host(corpus: PackedCorpus, plex: PackedLexicon, model, threshold: float
     pb = PinnedBatch(corpus, plex, pin=pin, wire=wire)
     recs, k, _ = mine_pinned(pb, model, threshold, penalty)
     return recs.copy(), pb.cost[: pb.n_docs].copy()
+
+
+class TunePinned:
+    """A tuning dev set staged page-locked once (tuner.py:112-154 inputs): the
+    packed sentences, the documents' ranges and the packed gold keys
+    (engine.pack_gold). ``tune_pinned`` copies it to the GPU chunk by chunk,
+    each chunk's copy overlapping the sweep of the chunk before."""
+
+    def __init__(self, corpus: PackedCorpus, gold_keys: np.ndarray, gold_off: np.ndarray):
+        self.corpus = corpus
+        self.n_docs = int(corpus.n_docs)
+        self.host = {k: _pinned(getattr(corpus, k)) for k in _SENT}
+        self.docs = {k: _pinned(np.asarray(getattr(corpus, k), dtype=np.int32)) for k in _DOCS}
+        self.gold = (_pinned(np.asarray(gold_keys, dtype=np.int64)),
+                     _pinned(np.asarray(gold_off, dtype=np.int64)))
+        self.max_tok = int(corpus.n_tok.max(initial=0))
+        self.h2d_bytes = (sum(v[1].nbytes for v in self.host.values())
+                          + sum(v[1].nbytes for v in self.docs.values())
+                          + self.gold[0][1].nbytes + self.gold[1][1].nbytes)
+        self._dev = None
+        n = self.docs["n"][1].astype(np.int64)
+        m = self.docs["m"][1].astype(np.int64)
+        s_end = np.maximum(self.docs["src0"][1] + n, self.docs["tgt0"][1] + m)
+        # sentences [0, hi_k) must be resident before documents < d1 of chunk k run
+        self._hi = np.maximum.accumulate(s_end) if self.n_docs else s_end
+        self._cells = np.cumsum(n * m)
+
+    def chunks(self, n_chunks: int):
+        """[d0, d1) ranges: a small first chunk (the GPU starts early), then
+        equal cell counts."""
+        if self.n_docs == 0:
+            return []
+        total = int(self._cells[-1])
+        first = total / (4 * n_chunks)
+        cuts = [first + (total - first) * k / n_chunks for k in range(n_chunks)]
+        ends = sorted({int(np.searchsorted(self._cells, c, side="left")) + 1 for c in cuts})
+        ends = [min(e, self.n_docs) for e in ends] + [self.n_docs]
+        out, d0 = [], 0
+        for e in ends:
+            if e > d0:
+                out.append((d0, e))
+                d0 = e
+        return out
+
+    def device_buffers(self):
+        if self._dev is None:
+            import torch
+
+            dev = torch.device("cuda", torch.cuda.current_device())
+            mk = lambda v: torch.empty(max(v[1].nbytes, 1), dtype=torch.uint8, device=dev)  # noqa: E731
+            self._dev = ({k: mk(v) for k, v in self.host.items()},
+                         {k: mk(v) for k, v in self.docs.items()},
+                         (mk(self.gold[0]), mk(self.gold[1])))
+        return self._dev
+
+
+_STREAMS = {}
+
+
+def _private_streams():
+    """(work, copy) streams of the current device for tune_pinned. The sweep
+    runs on its own stream, not the caller's: the caller's is usually the
+    legacy default stream, which would order every copy-stream operation
+    against the sweep and serialise the copies with the kernels."""
+    import torch
+
+    d = torch.cuda.current_device()
+    if d not in _STREAMS:
+        _STREAMS[d] = (torch.cuda.Stream(device=d), torch.cuda.Stream(device=d))
+    return _STREAMS[d]
+
+
+def tune_pinned(tp: TunePinned, dl, model, penalties, thresholds, n_chunks: int | None = None):
+    """tune's counting sweep end to end from page-locked host buffers: chunk k's
+    sentences, documents and gold keys are copied on a copy stream one chunk
+    ahead of the bm_tune call of chunk k - 1 on the current stream (so the
+    sweep's own small plan uploads never queue behind the whole dev set's
+    bulk copy), and every chunk's pred/hit counts add into the same device
+    totals (bm_tune accumulates). Returns (pred, hit) [n_pen, n_thr] int64 on
+    the host."""
+    import torch
+
+    from . import engine
+
+    import os
+
+    if n_chunks is None:
+        n_chunks = int(os.environ.get("BM_TUNE_CHUNKS", "6"))
+    lib = N.lib()
+    sent_d, docs_d, (gk_d, go_d) = tp.device_buffers()
+    caller = torch.cuda.current_stream()
+    main, cs = _private_streams()
+    main.wait_stream(caller)
+    pen = np.ascontiguousarray(np.asarray(penalties, dtype=np.float64))
+    thr = np.asarray(thresholds, dtype=np.float64)
+    dev = sent_d["n_tok"].device
+    with torch.cuda.stream(main):
+        pred = torch.zeros((len(pen), len(thr)), dtype=torch.int64, device=dev)
+        hit = torch.zeros((len(pen), len(thr)), dtype=torch.int64, device=dev)
+        thr_d = torch.from_numpy(thr).pin_memory().to(dev, non_blocking=True)
+    c = tp.corpus
+    tok_off, dig_off = tp.host["tok_off"][1], tp.host["dig_off"][1]
+    goff = tp.gold[1][1]
+    cs.wait_stream(main)  # the device buffers are free once earlier work on main is done
+
+    def cp(dst, src, lo, hi):
+        if hi > lo:
+            isz = src[1].itemsize
+            dst[lo * isz: hi * isz].copy_(src[0][lo * isz: hi * isz], non_blocking=True)
+
+    state = {"hi": 0}
+    events = []
+
+    def enqueue_copy(d0, d1):
+        with torch.cuda.stream(cs):
+            if not events:  # the documents' ranges, once
+                for k in _DOCS:
+                    cp(docs_d[k], tp.docs[k], 0, tp.n_docs)
+            a, b = state["hi"], int(tp._hi[d1 - 1])
+            if b > a:
+                for k in ("n_tok", "n_punct", "n_alpha"):
+                    cp(sent_d[k], tp.host[k], a, b)
+                cp(sent_d["tok_off"], tp.host["tok_off"], a, b + 1)
+                cp(sent_d["dig_off"], tp.host["dig_off"], a, b + 1)
+                e0, e1 = int(tok_off[a]), int(tok_off[b])
+                cp(sent_d["tok_id"], tp.host["tok_id"], e0, e1)
+                cp(sent_d["tok_alpha"], tp.host["tok_alpha"], e0, e1)
+                cp(sent_d["dig_id"], tp.host["dig_id"], int(dig_off[a]), int(dig_off[b]))
+                state["hi"] = b
+            cp(go_d, tp.gold[1], d0, d1 + 1)
+            cp(gk_d, tp.gold[0], int(goff[d0]), int(goff[d1]))
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append(ev)
+
+    sent = N.Sentences(c.n_sent, *[int(sent_d[k].data_ptr()) for k in _SENT])
+    chunks = tp.chunks(n_chunks)
+    if chunks:
+        enqueue_copy(*chunks[0])
+    n_h = tp.docs["n"][1]
+    m_h = tp.docs["m"][1]
+    for q, (d0, d1) in enumerate(chunks):
+        if q + 1 < len(chunks):
+            enqueue_copy(*chunks[q + 1])
+        main.wait_event(events[q])
+        docs = N.Docs(d1 - d0, *[int(docs_d[k].data_ptr()) + 4 * d0 for k in _DOCS])
+        nh = np.ascontiguousarray(n_h[d0:d1])
+        mh = np.ascontiguousarray(m_h[d0:d1])
+        N.check(lib.bm_tune(C.byref(sent), C.byref(docs), nh.ctypes.data, mh.ctypes.data,
+                            C.byref(dl.lex), C.byref(N.model_struct(model)), pen.ctypes.data,
+                            len(pen), engine._ptr(thr_d), len(thr), int(gk_d.data_ptr()),
+                            int(go_d.data_ptr()) + 8 * d0, engine._ptr(pred), engine._ptr(hit),
+                            tp.max_tok, int(main.cuda_stream)))
+    main.wait_stream(cs)
+    caller.wait_stream(main)
+    with torch.cuda.stream(main):
+        out = pred.cpu().numpy(), hit.cpu().numpy()
+    return out

@@ -752,3 +752,25 @@ def test_trim_releases_scratch_and_mining_continues(oracle_mod):
     assert _native.lib().bm_trim() == 0
     again, _ = engine.mine(dc, dl, view, model, 0.5, 0.2)
     assert first.tobytes() == again.tobytes()
+
+
+def test_tune_pinned_chunks_equal_device_sweep():
+    """hostapi.tune_pinned (chunked H2D overlapping per-chunk bm_tune, counts
+    added across chunks) gives the device-resident sweep's counts exactly, for
+    several chunk counts, including chunks of one document."""
+    from paper_1509_08639_b200 import engine, hostapi, synth
+
+    sc = synth.make_corpus(*synth.c3_shape(300, seed=77), seed=77)
+    c = sc.packed
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    dl = engine.DeviceLexicon.upload(plex)
+    keys = [np.asarray(gd[:, 0] * int(c.m[d]) + gd[:, 1], np.int64) for d, gd in enumerate(sc.gold)]
+    pens, thrs = [0.05, 0.2, 0.4, 1.6, 0.1], [0.3, 0.5, 0.7]
+    want_p, want_h = engine.tune_counts(engine.DeviceCorpus.upload(c), dl, engine.DocView.of(c),
+                                        model, pens, thrs, keys)
+    gk, goff = engine.pack_gold(keys)
+    tp = hostapi.TunePinned(c, gk, goff)
+    for k in (1, 3, 7, 300):
+        p, h = hostapi.tune_pinned(tp, dl, model, pens, thrs, n_chunks=k)
+        assert np.array_equal(p, want_p) and np.array_equal(h, want_h), k
