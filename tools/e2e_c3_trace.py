@@ -12,7 +12,7 @@ from paper_1509_08639_b200 import engine, hostapi, synth  # noqa: E402
 from paper_1509_08639_b200.classifier import load_model  # noqa: E402
 
 n_docs = int(sys.argv[1]) if len(sys.argv) > 1 else 200000
-g, a, b = synth.c3_shape(n_docs, seed=2026)
+g, a, b = synth.c2_shape(n_docs) if "--c2" in sys.argv else synth.c3_shape(n_docs, seed=2026)
 sc = synth.make_corpus_native(g, a, b, seed=2026)
 model = load_model(os.path.join(ROOT, "tests", "golden", "model5k_fwd.json"))
 plex = sc.world.packed_lexicon()

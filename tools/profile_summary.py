@@ -7,6 +7,7 @@ one entry per profiled kernel (name without namespace/arguments).
 import csv
 import io
 import json
+import os
 import re
 import subprocess
 import sys
@@ -45,22 +46,47 @@ def main():
         h = rows[0]
         ki, mi, ui, vi = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"),
                           h.index("Metric Value"))
+        # launches of the same kernel are kept apart (name#launch id) in the
+        # text and summed per kernel name in the raw metrics
+        ii = h.index("ID")
+        names = {}
+        for r in rows[1:]:
+            names.setdefault(short(r[ki]), set()).add(r[ii])
         by = {}
         for r in rows[1:]:
-            by.setdefault(short(r[ki]), {})[r[mi]] = (r[vi], r[ui])
+            if int(os.environ.get("PROFILE_MAX_ID", "-1")) >= 0 and int(r[ii]) > int(
+                    os.environ["PROFILE_MAX_ID"]):
+                continue
+            k = short(r[ki])
+            if len(names[k]) > 1:
+                k = f"{k}#{r[ii]}"
+            by.setdefault(k, {})[r[mi]] = (r[vi], r[ui])
         raw = ncu(rep, "raw")
         rh, units = raw[0], raw[1]
         kcol = rh.index("Kernel Name")
         # normalised units: bytes and milliseconds
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
                  "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+        sums = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                "smsp__inst_executed.sum")
+        max_id = int(os.environ.get("PROFILE_MAX_ID", "-1"))
+        idc = rh.index("ID")
         for r in raw[2:]:
+            if max_id >= 0 and int(r[idc]) > max_id:
+                continue
             k = short(r[kcol])
+            first = k not in raw_all
             ent = raw_all.setdefault(k, {})
+            ent["launches"] = ent.get("launches", 0) + 1
             stalls = {}
             for i, name in enumerate(rh):
                 if name in RAW:
-                    ent[name] = float(r[i].replace(",", "")) * scale.get(units[i], 1.0)
+                    v = float(r[i].replace(",", "")) * scale.get(units[i], 1.0)
+                    # additive metrics summed over launches; ratios from the longest
+                    if name in sums:
+                        ent[name] = ent.get(name, 0.0) + v
+                    elif first or v > 0:
+                        ent[name] = v
                 elif name.startswith(STALLS) and not name.endswith("not_issued"):
                     try:
                         v = float(r[i].replace(",", ""))
@@ -76,6 +102,7 @@ def main():
             for name in DETAILS:
                 if name in d:
                     text.append(f"  {name:34s} {d[name][0]} {d[name][1]}")
+            k = k.split("#")[0]
             if k in raw_all and "stall_share" in raw_all[k]:
                 text.append("  stall share (pc sampling)         " +
                             ", ".join(f"{a} {b:.0%}" for a, b in raw_all[k]["stall_share"].items()))
