@@ -712,6 +712,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef BM_NW_EARLY_BND
 #define BM_NW_EARLY_BND 1
 #endif
+// groups per boundary chunk (2, 4 or 8): the band below waits for a whole
+// chunk, so a band trails the one above by 31 + kNwChunkG super-steps plus the
+// L2 round trip
+#ifndef BM_NW_CHUNK_G
+#define BM_NW_CHUNK_G 4
+#endif
+constexpr int kNwChunkG = BM_NW_CHUNK_G;
+static_assert(kNwChunkG == 2 || kNwChunkG == 4 || kNwChunkG == 8, "chunk of 2, 4 or 8 groups");
 template <int D, int NP, bool kFin>
 #ifndef BM_NW_MINB2
 #define BM_NW_MINB2 1
@@ -814,10 +822,11 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
 
     auto step = [&](const int t, double(&oc)[16], double(&on)[16]) {
       const int g = t - lane;
-      if ((t & 7) == 0 && 4 * t < m) {
+      if ((t & (kNwChunkG - 1)) == 0 && 4 * t < m) {
         NW_PROF(const unsigned long long w0 = gtimer();)
-        // lane 0's next 8 groups: the band above's last row (band 0: border)
-        const int c = 4 * t + lane;
+        // lane 0's next kNwChunkG groups: the band above's last row (band 0:
+        // border); lanes past the chunk's 4 * kNwChunkG columns load nothing
+        const int c = lane < 4 * kNwChunkG ? 4 * t + lane : m;
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
           double v = 0.0;
@@ -845,12 +854,12 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
                   g_nw_chunk[it][t >> 3][1] = gtimer();
                 })
       }
-      if (BM_NW_EARLY_BND && NP < 4 && band > 0 && (t & 7) == 4) {
+      if (BM_NW_EARLY_BND && NP < 4 && band > 0 && (t & (kNwChunkG - 1)) == kNwChunkG / 2) {
         // the next chunk's boundary values, loaded half a chunk early so the
-        // L2 round trip overlaps four super-steps (the band above is normally
-        // 40+ super-steps ahead, so the values are already there). Not at
-        // NP = 4: the extra registers spill there (measured slower).
-        const int c = 4 * (t + 4) + lane;
+        // L2 round trip overlaps half a chunk of super-steps (the band above is
+        // normally ahead, so the values are already there). Not at NP = 4: the
+        // extra registers spill there (measured slower).
+        const int c = lane < 4 * kNwChunkG ? 4 * (t + kNwChunkG / 2) + lane : m;
 #pragma unroll
         for (int q = 0; q < NP; ++q)
           pre[q] = c < m ? ld_relaxed_u64(bnd_up + q * a.bnd_stride + c) : kBndSentinel;
@@ -861,8 +870,8 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
       for (int q = 0; q < NP; ++q) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) u[q][c] = __shfl_up_sync(kFull, b[q][c], 1);
-        const double2 x = *(const double2*)(bnd_s + q * WARP + 4 * (t & 7));
-        const double2 y = *(const double2*)(bnd_s + q * WARP + 4 * (t & 7) + 2);
+        const double2 x = *(const double2*)(bnd_s + q * WARP + 4 * (t & (kNwChunkG - 1)));
+        const double2 y = *(const double2*)(bnd_s + q * WARP + 4 * (t & (kNwChunkG - 1)) + 2);
         if (lane == 0) {
           u[q][0] = x.x;
           u[q][1] = x.y;
