@@ -276,6 +276,9 @@ struct GeneralDev {
   double *S, *bnd;
   uint32_t* dirs;
   unsigned int* ticket;
+  uint32_t* hits = nullptr;     // document-level join output (doc_join plans)
+  int64_t* h_off = nullptr;
+  std::vector<WorkItem> order;  // the DP's (doc, band) work order (host copy)
 };
 
 // Gathers src0/tgt0/n/m of the subset on the device from the batch arrays.
@@ -307,7 +310,7 @@ __global__ void scatter_results_kernel(const int32_t* idx, int k, const double* 
 }
 
 int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, GeneralDev& dv,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool store_s = true) {
   const int k = (int)g.docs.size();
   int32_t* idx = nullptr;
   BM_CK(sc.upload(&idx, g.docs), "upload");
@@ -330,15 +333,16 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
     for (size_t q = 0; q < g.items.size(); ++q)
       key[q] = {(int64_t)g.items[q].doc + (int64_t)g.items[q].band * kStagger, (int)q};
     std::stable_sort(key.begin(), key.end());
-    std::vector<WorkItem> items(g.items.size());
-    for (size_t q = 0; q < items.size(); ++q) items[q] = g.items[key[q].second];
-    BM_CK(sc.upload(&dv.items, items), "upload");
+    dv.order.resize(g.items.size());
+    for (size_t q = 0; q < dv.order.size(); ++q) dv.order[q] = g.items[key[q].second];
   } else {
-    BM_CK(sc.upload(&dv.items, g.items), "upload");
+    dv.order = g.items;
   }
+  BM_CK(sc.upload(&dv.items, dv.order), "upload");
   BM_CK(sc.alloc(&dv.src0, k), "alloc");
   BM_CK(sc.alloc(&dv.tgt0, k), "alloc");
-  BM_CK(ws_get(st, kWsS, &dv.S, (size_t)g.s_total), "alloc S");
+  dv.S = nullptr;  // the fused banded tier never stores the matrix
+  if (store_s) BM_CK(ws_get(st, kWsS, &dv.S, (size_t)g.s_total), "alloc S");
   BM_CK(ws_get(st, kWsDirs, &dv.dirs, (size_t)g.dir_total), "alloc dirs");
   BM_CK(ws_get(st, kWsBnd, &dv.bnd, (size_t)g.bnd_total), "alloc boundary");
   BM_CK(sc.alloc(&dv.ticket, 1), "alloc ticket");
@@ -414,7 +418,7 @@ struct HostTrace {
 // per-tile kernel.
 int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs& D,
                   const bm_lexicon* lex, const Model& M, GeneralDev& dv, bool doc_join,
-                  Scratch& sc, cudaStream_t st) {
+                  Scratch& sc, cudaStream_t st, bool join_only = false) {
   const int k = (int)g.docs.size();
   for (int q = 0; q < k && doc_join; ++q) doc_join = g.n[q] <= 65535 && g.m[q] <= 65535;
   if (!doc_join) {
@@ -426,8 +430,8 @@ int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs&
   std::vector<int64_t> hoff(k);
   int64_t ht = 0;
   for (int q = 0; q < k; ++q) {
-    hoff[q] = ht;
-    ht += (int64_t)g.n[q] * g.m[q];
+    hoff[q] = ht;  // rows of pitch_of(m) words: 16-byte aligned rows
+    ht += (int64_t)g.n[q] * g.pitch[q];
   }
   std::vector<int4> items;
   join_items(g.n.data(), g.m.data(), k, items);
@@ -441,8 +445,11 @@ int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs&
   ModelTables mt;
   BM_CK(model_tables(M, &mt), "model tables");
   BM_CK(launch_score_hits(*sent, D, *lex, M, mt, dit, (int)items.size(), hits, dho, dv.tiles,
-                          (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S, st),
+                          join_only ? 0 : (int)g.tiles.size(), dv.s_off, dv.pitch,
+                          join_only ? nullptr : dv.S, st),
         "score_hits_kernel");
+  dv.hits = hits;
+  dv.h_off = dho;
   return BM_OK;
 }
 
@@ -459,23 +466,58 @@ int64_t par_walk_min() {
 int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* docs,
                  const bm_lexicon* lex, const Model& M, double threshold, double penalty,
                  const int64_t* rec_off, bm_record* rec, int32_t* rec_count, double* cost,
-                 bool doc_join, Scratch& sc, cudaStream_t st) {
+                 bool doc_join, Scratch& sc, cudaStream_t st, bool fused = false) {
   {
     HostTrace tr("mine_general");
     const int k = (int)g.docs.size();
+    for (int q = 0; q < k && fused; ++q) fused = g.n[q] <= 65535 && g.m[q] <= 65535;
+    fused = fused && doc_join;
     GeneralDev dv;
-    int rc = general_prepare(g, docs, sc, dv, st);
+    int rc = general_prepare(g, docs, sc, dv, st, /*store_s=*/!fused);
     if (rc) return rc;
     tr.mark("prepare");
     const bm_docs D = local_docs(dv, k);
-    rc = score_general(g, sent, D, lex, M, dv, doc_join, sc, st);
+    rc = score_general(g, sent, D, lex, M, dv, doc_join, sc, st, /*join_only=*/fused);
     if (rc) return rc;
     tr.mark("score enqueued");
     double* cost_l = nullptr;
     BM_CK(sc.alloc(&cost_l, k), "alloc");
-    rc = general_nw(g, dv, penalty, cost_l, st);
-    if (rc) return rc;
+    if (fused) {
+      // score + DP per (doc, band) item in one kernel (bm_band.cu)
+      BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
+      BM_CK(cudaMemsetAsync(dv.bnd, 0xde, std::max<int64_t>(g.bnd_total, 1) * 8, st), "memset");
+      BandArgs a;
+      a.S = *sent;
+      a.D = D;
+      a.M = M;
+      BM_CK(model_tables(M, &a.mt), "model tables");
+      a.hits = dv.hits;
+      a.h_off = dv.h_off;
+      a.pitch = dv.pitch;
+      a.p = penalty;
+      a.dirs = dv.dirs;
+      a.dir_off = dv.dir_off;
+      a.cost = cost_l;
+      a.items = dv.items;
+      a.n_items = (int)g.items.size();
+      a.ticket = dv.ticket;
+      a.bnd = dv.bnd;
+      a.bnd_off = dv.bnd_off;
+      const int m_max = *std::max_element(g.m.begin(), g.m.end());
+      BM_CK(launch_band(a, m_max, st), "mine_band_kernel");
+    } else {
+      rc = general_nw(g, dv, penalty, cost_l, st);
+      if (rc) return rc;
+    }
     tr.mark("nw enqueued");
+    CellSrc cs;
+    cs.S = dv.S;
+    cs.s_off = dv.s_off;
+    cs.sent = *sent;
+    cs.D = D;
+    cs.M = M;
+    cs.hits = dv.hits;
+    cs.h_off = dv.h_off;
     std::vector<int64_t> roff(k);
     int64_t rt = 0;
     for (int q = 0; q < k; ++q) {
@@ -539,10 +581,10 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
     }
     uint8_t* dskip = nullptr;
     if (bx.n_big) BM_CK(sc.upload(&dskip, skip), "upload");
-    BM_CK(launch_extract(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, k, threshold,
+    BM_CK(launch_extract(dv.dirs, dv.dir_off, cs, dv.pitch, dv.n, dv.m, k, threshold,
                          droff, rl, cl, st, dskip),
           "extract_kernel");
-    BM_CK(launch_extract_banded(dv.dirs, dv.dir_off, dv.S, dv.s_off, dv.pitch, dv.n, dv.m, bx,
+    BM_CK(launch_extract_banded(dv.dirs, dv.dir_off, cs, dv.pitch, dv.n, dv.m, bx,
                                 threshold, droff, rl, cl, st),
           "band-parallel extraction");
     scatter_results_kernel<<<k, 128, 0, st>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
@@ -673,7 +715,11 @@ int bm_extract(const uint32_t* dirs, const int64_t* dir_off, const double* S, co
                const int32_t* pitch, const int32_t* n, const int32_t* m, int32_t n_docs,
                double threshold, const int64_t* rec_off, bm_record* rec, int32_t* rec_count,
                void* stream) {
-  BM_CK(launch_extract(dirs, dir_off, S, s_off, pitch, n, m, n_docs, threshold, rec_off, rec,
+  if (S == nullptr && n_docs > 0) return fail(BM_EINVAL, "S is null");
+  CellSrc cs;
+  cs.S = S;
+  cs.s_off = s_off;
+  BM_CK(launch_extract(dirs, dir_off, cs, pitch, n, m, n_docs, threshold, rec_off, rec,
                        rec_count, (cudaStream_t)stream),
         "extract_kernel");
   return BM_OK;
@@ -700,6 +746,23 @@ static cudaStream_t side_stream(int q) {
   }
   if (s[q] == nullptr) cudaStreamCreateWithFlags(&s[q], cudaStreamNonBlocking);
   return s[q];
+}
+
+// Fused banded tier (bm_band.cu) routing, opt-in: BM_BAND_FUSED=1 sends the
+// banded documents whose sentences fit the folded tables there instead of
+// score_hits_kernel -> nw_band_kernel. Measured on C3 200k:
+// 70.6 ms fused vs 68.5 ms unfused -- the fused kernel issues at ~45-50 %
+// against score_hits' 67 %, which the saved S round trip does not make up.
+// BM_BAND_MIN_ITEMS: (doc, band) items a group needs for the fused tier
+// (default 4 per SM: fewer bands leave the scoring warps idle; C4's 64 bands
+// ran 2.9 -> 9 ms fused).
+static bool band_fused_on() {
+  static const bool v = getenv("BM_BAND_FUSED") ? atoi(getenv("BM_BAND_FUSED")) != 0 : false;
+  return v;
+}
+static int64_t band_fused_min_items() {
+  static const int64_t v = getenv("BM_BAND_MIN_ITEMS") ? atoll(getenv("BM_BAND_MIN_ITEMS")) : 4 * 148;
+  return v;
 }
 
 // Documents per bm_mine group: consecutive documents up to this many cells
@@ -797,12 +860,26 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
   // banded tier: the document-level join keeps 16-bit hit counts (every
   // sentence <= 65535 tokens); longer sentences take the per-tile scoring
   // kernel with 32-bit counts
-  GeneralPlan g, gw;
-  for (int32_t d : banded) (amax_host[d] <= 65535 ? g : gw).add(d, n_host[d], m_host[d]);
-  for (GeneralPlan* gp : {&g, &gw}) {
+  // every sentence <= 255 tokens (the folded tables' range): the fused banded
+  // tier (bm_band.cu) when the group has enough bands to fill the GPU with its
+  // CTAs; a few long documents (C4) keep the unfused tier, whose DP runs a
+  // warp per band without waiting on 4 scoring warps per band
+  GeneralPlan gf, g, gw;
+  for (int32_t d : banded) {
+    const int32_t md = m_host[d];
+    GeneralPlan& t = amax_host[d] > 65535 ? gw
+                     : (!band_fused_on() || amax_host[d] > 255 || md > 65535) ? g
+                     : gf;
+    t.add(d, n_host[d], md);
+  }
+  if (!gf.docs.empty() && (int64_t)gf.items.size() < band_fused_min_items()) {
+    for (size_t q = 0; q < gf.docs.size(); ++q) g.add(gf.docs[q], gf.n[q], gf.m[q]);
+    gf = GeneralPlan();
+  }
+  for (GeneralPlan* gp : {&gf, &g, &gw}) {
     if (gp->docs.empty()) continue;
     int rc = mine_general(*gp, sent, docs, lex, M, threshold, penalty, rec_off, rec, rec_count,
-                          cost, gp == &g, scb, sb);
+                          cost, gp != &gw, scb, sb, gp == &gf);
     if (rc) return rc;
     tr.mark("banded tier enqueued");
   }

@@ -135,6 +135,42 @@ static inline cudaError_t counted(cudaError_t e, int n = 1) {
 }
 
 
+// Streamed hit counts (read once per cell): not allocated in L1, which stays
+// with the model's margin tables the cells look up (BM_HITS_NOALLOC=0: __ldg).
+#ifndef BM_HITS_NOALLOC
+#define BM_HITS_NOALLOC 1
+#endif
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+#if BM_HITS_NOALLOC
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ uint4 ld_stream_v4(const uint32_t* p) {
+#if BM_HITS_NOALLOC
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p));
+  return v;
+#else
+  return __ldg(reinterpret_cast<const uint4*>(p));
+#endif
+}
+
+__device__ __forceinline__ uint2 ld_stream_v2(const uint32_t* p) {
+#if BM_HITS_NOALLOC
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+#else
+  return __ldg(reinterpret_cast<const uint2*>(p));
+#endif
+}
+
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const double* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -273,6 +309,7 @@ __global__ void __launch_bounds__(BM_HITS_DOC_THREADS, BM_HITS_DOC_MINB) hits_do
                                                          const int4* __restrict__ items,
                                                          int n_items,
                                                          const int64_t* __restrict__ h_off,
+                                                         const int32_t* __restrict__ h_pitch,
                                                          uint32_t* __restrict__ hits) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int4 it = items[blockIdx.x];
@@ -281,6 +318,7 @@ __global__ void __launch_bounds__(BM_HITS_DOC_THREADS, BM_HITS_DOC_MINB) hits_do
   // rows were 128 CTAs, 1.7 ms)
   const int d = it.x, dir = it.y & 1, k0 = it.z, k1 = it.w;
   const int n = D.n[d], m = D.m[d];
+  const int64_t hp = h_pitch[d];  // hit-count row pitch (m rounded up to 4)
   const int s0 = D.src0[d], t0 = D.tgt0[d];
   JoinSmem js = carve_join(smem, kDocJoinEmax, kDocJoinBuckets);
   uint16_t* chunk_owner = (uint16_t*)(smem + align16(join_smem_bytes(kDocJoinEmax, kDocJoinBuckets)));
@@ -300,12 +338,12 @@ __global__ void __launch_bounds__(BM_HITS_DOC_THREADS, BM_HITS_DOC_MINB) hits_do
     if (dir == 0)
       join_chunk_entries(CtaGroup(), S, off, cand, offA, na, offB, b0, nb, c0, c1, js, chunk_owner,
                          a_owner, [&](int ls, int lt, int w) {
-                           atomicAdd(hd + (int64_t)(ls + p0) * m + lt, (uint32_t)w);
+                           atomicAdd(hd + (int64_t)(ls + p0) * hp + lt, (uint32_t)w);
                          });
     else
       join_chunk_entries(CtaGroup(), S, off, cand, offA, na, offB, b0, nb, c0, c1, js, chunk_owner,
                          a_owner, [&](int lt, int ls, int w) {
-                           atomicAdd(hd + (int64_t)ls * m + (lt + p0), (uint32_t)w << 16);
+                           atomicAdd(hd + (int64_t)ls * hp + (lt + p0), (uint32_t)w << 16);
                          });
   }
 }
@@ -430,9 +468,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   }
   // the folded tables cover the tile when all of its sentences fit them
   const bool small = __syncthreads_and(fits) != 0;
-  const uint32_t* hd = hits + h_off[doc] + (int64_t)r0 * m + c0;
-  double* dst = out + s_off[doc] + (int64_t)r0 * pitch[doc] + c0;
-  const int64_t ld = pitch[doc];
+  const int64_t ld = pitch[doc];  // row pitch of S and of the hit counts
+  const uint32_t* hd = hits + h_off[doc] + (int64_t)r0 * ld + c0;
+  double* dst = out + s_off[doc] + (int64_t)r0 * ld + c0;
   // fixed column per thread (kTile divides the block): no per-cell division
   static_assert(kTileThreads % kTile == 0, "tile rows per pass");
   const int j = threadIdx.x % kTile;
@@ -441,10 +479,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   int i = threadIdx.x / kTile;
   // running row pointers (one 64-bit add per cell); the next row's hit word is
   // in flight while this cell is scored
-  const uint32_t* hp = hd + (int64_t)i * m + j;
+  const uint32_t* hp = hd + (int64_t)i * ld + j;
   double* op = dst + (int64_t)i * ld + j;
-  const int64_t hstep = (int64_t)kRowStep * m, ostep = (int64_t)kRowStep * ld;
-  uint32_t hv_next = i < ns ? __ldg(hp) : 0u;
+  const int64_t hstep = (int64_t)kRowStep * ld, ostep = (int64_t)kRowStep * ld;
+  uint32_t hv_next = i < ns ? ld_stream_u32(hp) : 0u;
   if (small) {
     const FoldSent fb = fcols[j];
     const double w3z = __dmul_rn(M.w[3], 0.0);
@@ -457,7 +495,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     const uint32_t frows_s = (uint32_t)__cvta_generic_to_shared(frows) + z;
     for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
       const uint32_t hv = hv_next;
-      if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
+      if (i + kRowStep < ns) hv_next = ld_stream_u32(hp + hstep);
       int4 fa;
       double pos_s;
       const uint32_t ra = frows_s + (uint32_t)i * (uint32_t)sizeof(FoldSent);
@@ -474,7 +512,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     const double pos_t = cols->s[j].pos;
     for (; i < ns; i += kRowStep, hp += hstep, op += ostep) {
       const uint32_t hv = hv_next;
-      if (i + kRowStep < ns) hv_next = __ldg(hp + hstep);
+      if (i + kRowStep < ns) hv_next = ld_stream_u32(hp + hstep);
       *op = cell_score(S, M, exp_tab, get_scalars(*rows, i), b, (int)(hv & 0xffffu),
                        (int)(hv >> 16), rows->s[i].pos, pos_t);
     }
@@ -505,12 +543,13 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
                               const int64_t* h_off, const int4* tiles, int n_tiles,
                               const int64_t* s_off, const int32_t* pitch, double* out,
                               cudaStream_t st) {
-  if (n_tiles == 0) return cudaSuccess;
+  if (n_tiles == 0 && out != nullptr) return cudaSuccess;
   const size_t hs = hits_doc_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(hits_doc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)hs);
   if (e != cudaSuccess) return e;
-  if (n_items) hits_doc_kernel<<<n_items, BM_HITS_DOC_THREADS, hs, st>>>(S, D, L, items, n_items, h_off, hits);
+  if (n_items) hits_doc_kernel<<<n_items, BM_HITS_DOC_THREADS, hs, st>>>(S, D, L, items, n_items, h_off, pitch, hits);
+  if (out == nullptr) return counted(cudaGetLastError(), n_items ? 1 : 0);  // join only (fused band tier)
   const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars) + 2 * kTile * sizeof(FoldSent);
   score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits, h_off,
                                                        out);
@@ -1218,8 +1257,9 @@ cudaError_t launch_traceback(const uint32_t* dirs, const int64_t* dir_off, const
 // i_stop), filled back to front while walking (the walk runs from the end of
 // the path) into out[0, cap), then moved to the front; returns the count.
 // 32 diagonal cells are gathered per batch.
-__device__ __forceinline__ int extract_segment(uint32_t* win, const uint32_t* dd, const double* Sd,
-                                               int64_t ld, int n, int m, int lane, int i0, int j0,
+template <class Val>
+__device__ __forceinline__ int extract_segment(uint32_t* win, const uint32_t* dd, const Val& val,
+                                               int n, int m, int lane, int i0, int j0,
                                                int i_stop, double threshold, int d, bm_record* out,
                                                int cap) {
   int nd = 0, kept = 0, ci = 0, cj = 0;
@@ -1245,7 +1285,7 @@ __device__ __forceinline__ int extract_segment(uint32_t* win, const uint32_t* dd
   };
   auto flush = [&](int valid) {
     finish();
-    pc = lane < valid ? Sd[(int64_t)ci * ld + cj] : 0.0;
+    pc = lane < valid ? val(ci, cj) : 0.0;
     pi = ci;
     pj = cj;
     pvalid = valid;
@@ -1274,11 +1314,30 @@ __device__ __forceinline__ int extract_segment(uint32_t* win, const uint32_t* dd
   return kept;
 }
 
+// A path cell's confidence: S[i][j] of the stored matrix, or (kRescore, the
+// fused banded tier) the cell scored again from the join's hit counts and the
+// sentences -- cell_score, the value score_hits_kernel and mine_band_kernel
+// compute for it (aligner.py:332-338).
+template <bool kRescore>
+struct PathCell {
+  const CellSrc* cs;
+  int d, n, m;
+  int64_t ld;
+  __device__ __forceinline__ double operator()(int i, int j) const {
+    if (!kRescore) return cs->S[cs->s_off[d] + (int64_t)i * ld + j];
+    const SentScalars a = load_scalars(cs->sent, cs->D.src0[d] + i);
+    const SentScalars b = load_scalars(cs->sent, cs->D.tgt0[d] + j);
+    const uint32_t hv = cs->hits[cs->h_off[d] + (int64_t)i * ld + j];
+    return cell_score(cs->sent, cs->M, g_exp_table, a, b, (int)(hv & 0xffffu), (int)(hv >> 16),
+                      doc_pos(i, n), doc_pos(j, m));
+  }
+};
+
 // Records of one document per warp. Documents flagged in `skip` (the long ones
 // the band-parallel extraction below takes) are left alone.
+template <bool kRescore>
 __global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
-    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
-    const double* __restrict__ S, const int64_t* __restrict__ s_off,
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off, const CellSrc cs,
     const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
     const int32_t* __restrict__ mm, int n_docs, double threshold,
     const int64_t* __restrict__ rec_off, bm_record* rec, int32_t* rec_count,
@@ -1289,8 +1348,9 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
   if (d >= n_docs || (skip != nullptr && skip[d])) return;
   uint32_t* win = walk_smem + wid * 3 * kWinWords;
   const int n = nn[d], m = mm[d];
-  const int kept = extract_segment(win, dirs + dir_off[d], S + s_off[d], pitch[d], n, m, lane, n, m,
-                                   0, threshold, d, rec + rec_off[d], min(n, m));
+  const PathCell<kRescore> val{&cs, d, n, m, pitch[d]};
+  const int kept = extract_segment(win, dirs + dir_off[d], val, n, m, lane, n, m, 0, threshold, d,
+                                   rec + rec_off[d], min(n, m));
   if (lane == 0) rec_count[d] = kept;
 }
 
@@ -1394,9 +1454,9 @@ __global__ void band_chain_kernel(const uint32_t* __restrict__ dirs,
   }
 }
 
+template <bool kRescore>
 __global__ void __launch_bounds__(kWalkWarps * WARP) band_walk_kernel(
-    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off,
-    const double* __restrict__ S, const int64_t* __restrict__ s_off,
+    const uint32_t* __restrict__ dirs, const int64_t* __restrict__ dir_off, const CellSrc cs,
     const int32_t* __restrict__ pitch, const int32_t* __restrict__ nn,
     const int32_t* __restrict__ mm, const int32_t* __restrict__ big,
     const int32_t* __restrict__ entry, const int64_t* __restrict__ b_off, double threshold,
@@ -1412,7 +1472,8 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) band_walk_kernel(
   const int x = entry[b_off[q] + b];
   uint32_t* win = walk_smem + wid * 3 * kWinWords;
   bm_record* out = slots + (b_off[q] + b) * kBandRows;
-  const int kept = extract_segment(win, dirs + dir_off[d], S + s_off[d], pitch[d], n, m, lane,
+  const PathCell<kRescore> val{&cs, d, n, m, pitch[d]};
+  const int kept = extract_segment(win, dirs + dir_off[d], val, n, m, lane,
                                    min(n, (b + 1) * kBandRows), x, b * kBandRows, threshold, d, out,
                                    kBandRows);
   if (lane == 0) slot_cnt[b_off[q] + b] = kept;
@@ -1444,28 +1505,36 @@ __global__ void __launch_bounds__(256) band_gather_kernel(
       dst[pre[b] + k] = src[(int64_t)b * kBandRows + k];
 }
 
-cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const double* S,
-                           const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const CellSrc& cs,
+                           const int32_t* pitch, const int32_t* n,
                            const int32_t* m, int n_docs, double thr, const int64_t* rec_off,
                            bm_record* rec, int32_t* cnt, cudaStream_t st, const uint8_t* skip) {
   if (n_docs == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(extract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kWalkSmem);
+  const bool rs = cs.S == nullptr;
+  const void* fn = rs ? (const void*)extract_kernel<true> : (const void*)extract_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem);
   if (e != cudaSuccess) return e;
-  extract_kernel<<<(n_docs + kWalkWarps - 1) / kWalkWarps, kWalkWarps * WARP, kWalkSmem, st>>>(
-      dirs, dir_off, S, s_off, pitch, n, m, n_docs, thr, rec_off, rec, cnt, skip);
+  const int grid = (n_docs + kWalkWarps - 1) / kWalkWarps;
+  if (rs)
+    extract_kernel<true><<<grid, kWalkWarps * WARP, kWalkSmem, st>>>(dirs, dir_off, cs, pitch, n, m,
+                                                                    n_docs, thr, rec_off, rec, cnt, skip);
+  else
+    extract_kernel<false><<<grid, kWalkWarps * WARP, kWalkSmem, st>>>(dirs, dir_off, cs, pitch, n, m,
+                                                                     n_docs, thr, rec_off, rec, cnt, skip);
   return counted(cudaGetLastError());
 }
 
-cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, const double* S,
-                                  const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, const CellSrc& cs,
+                                  const int32_t* pitch, const int32_t* n,
                                   const int32_t* m, const BandedExtract& bx, double thr,
                                   const int64_t* rec_off, bm_record* rec, int32_t* cnt,
                                   cudaStream_t st) {
   if (bx.n_big == 0) return cudaSuccess;
   if (bx.max_bands > kGatherMaxBands) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(band_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kWalkSmem);
+  const bool rs = cs.S == nullptr;
+  cudaError_t e = cudaFuncSetAttribute(
+      rs ? (const void*)band_walk_kernel<true> : (const void*)band_walk_kernel<false>,
+      cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem);
   if (e != cudaSuccess) return e;
   // pass 0 over (bands - 1) x samples, pass 1 over (bands - 1) x (m + 1)
   const int64_t w1 = bx.max_exit_walks, w0 = w1 / kExitStride + 2 * bx.max_bands;
@@ -1479,10 +1548,13 @@ cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, 
   band_chain_kernel<<<bx.n_big, 32, 0, st>>>(dirs, dir_off, n, m, bx.big, bx.e_off, bx.exits,
                                              bx.b_off, bx.entry);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  band_walk_kernel<<<dim3((bx.max_bands + kWalkWarps - 1) / kWalkWarps, bx.n_big),
-                     kWalkWarps * WARP, kWalkSmem, st>>>(dirs, dir_off, S, s_off, pitch, n, m,
-                                                         bx.big, bx.entry, bx.b_off, thr,
-                                                         bx.slots, bx.slot_cnt);
+  const dim3 wg((bx.max_bands + kWalkWarps - 1) / kWalkWarps, bx.n_big);
+  if (rs)
+    band_walk_kernel<true><<<wg, kWalkWarps * WARP, kWalkSmem, st>>>(
+        dirs, dir_off, cs, pitch, n, m, bx.big, bx.entry, bx.b_off, thr, bx.slots, bx.slot_cnt);
+  else
+    band_walk_kernel<false><<<wg, kWalkWarps * WARP, kWalkSmem, st>>>(
+        dirs, dir_off, cs, pitch, n, m, bx.big, bx.entry, bx.b_off, thr, bx.slots, bx.slot_cnt);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   band_gather_kernel<<<bx.n_big, 256, 0, st>>>(n, bx.big, bx.b_off, bx.slots, bx.slot_cnt, rec_off,
                                                rec, cnt);

@@ -116,6 +116,42 @@ struct FusedArgs {
   const int64_t* hit_off;  // byte offset of each doc's hits (16-byte aligned)
 };
 
+// Fused banded tier (bm_band.cu): (doc, band) items of a banded plan, scored
+// from the document-level join's hit counts and aligned in one kernel.
+struct BandArgs {
+  bm_sentences S;
+  bm_docs D;                 // the plan's documents (local indices)
+  Model M;
+  ModelTables mt;
+  const uint32_t* hits;      // hf | hr << 16 per cell, rows of pitch[d] words
+  const int64_t* h_off;
+  const int32_t* pitch;
+  double p;
+  uint32_t* dirs;
+  const int64_t* dir_off;
+  double* cost;
+  const WorkItem* items;
+  int n_items;
+  unsigned int* ticket;
+  double* bnd;
+  const int64_t* bnd_off;
+};
+size_t band_smem_bytes(int m_max);
+cudaError_t launch_band(const BandArgs& a, int m_max, cudaStream_t st);
+
+// Where extraction reads a path cell's confidence: the similarity matrix
+// (S != nullptr), or -- for the fused banded tier, which never stores it --
+// re-scored from the hit counts and the sentences (same value, bit for bit).
+struct CellSrc {
+  const double* S = nullptr;
+  const int64_t* s_off = nullptr;
+  bm_sentences sent;
+  bm_docs D;
+  Model M;
+  const uint32_t* hits = nullptr;
+  const int64_t* h_off = nullptr;
+};
+
 cudaError_t launch_score(const bm_sentences&, const bm_docs&, const bm_lexicon&, const Model&,
                          const int4*, int, const int64_t*, const int32_t*, double*, cudaStream_t);
 cudaError_t launch_features(const bm_sentences&, const bm_lexicon&, const int32_t*, const int32_t*,
@@ -124,7 +160,7 @@ cudaError_t launch_confidence(const double*, int, const Model&, double*, cudaStr
 cudaError_t launch_nw(const NwArgs&, cudaStream_t);
 cudaError_t launch_traceback(const uint32_t*, const int64_t*, const int32_t*, const int32_t*, int,
                              const int64_t*, int8_t*, int32_t*, int32_t*, int32_t*, cudaStream_t);
-cudaError_t launch_extract(const uint32_t*, const int64_t*, const double*, const int64_t*,
+cudaError_t launch_extract(const uint32_t*, const int64_t*, const CellSrc&,
                            const int32_t*, const int32_t*, const int32_t*, int, double,
                            const int64_t*, bm_record*, int32_t*, cudaStream_t,
                            const uint8_t* skip = nullptr);
@@ -143,8 +179,8 @@ struct BandedExtract {
   bm_record* slots = nullptr;       // kBandRows records per band
   int32_t* slot_cnt = nullptr;
 };
-cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, const double* S,
-                                  const int64_t* s_off, const int32_t* pitch, const int32_t* n,
+cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, const CellSrc& cs,
+                                  const int32_t* pitch, const int32_t* n,
                                   const int32_t* m, const BandedExtract& bx, double thr,
                                   const int64_t* rec_off, bm_record* rec, int32_t* cnt,
                                   cudaStream_t st);

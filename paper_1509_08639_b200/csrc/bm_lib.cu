@@ -3,5 +3,6 @@
 // cudaMemcpyToSymbol initialises what every kernel reads.
 #include "bm_kernels.cu"
 #include "bm_ring.cu"
+#include "bm_band.cu"
 #include "bm_merge.cu"
 #include "bm_api.cu"

@@ -132,7 +132,9 @@ struct SmemTab {
   uint32_t addr;  // __cvta_generic_to_shared of the staged table
 };
 __device__ __forceinline__ void tab_pair(SmemTab T, uint32_t i, uint64_t& a, uint64_t& b) {
-  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(T.addr + i * 8u));
+  // not volatile: a read-only table, so independent lookups may be scheduled
+  // freely (several cells' exp chains interleave)
+  asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(T.addr + i * 8u));
 }
 #endif
 

@@ -1,7 +1,8 @@
-"""Child process of test_gpu_large.test_band_parallel_extraction_vs_oracle:
-BM_PAR_WALK_MIN is read once per process, so the low threshold that sends the
-C3 tail documents through the band-parallel extraction needs its own process.
-Mines the corpus and exits 0 when records and costs equal the oracle's."""
+"""Child process of test_gpu_large's routing tests: BM_PAR_WALK_MIN (the
+band-parallel extraction threshold) and BM_BAND_FUSED / BM_BAND_MIN_ITEMS (the
+fused banded tier) are read once per process, so each setting needs its own
+process. Mines the C3 tail corpus and exits 0 when records and costs equal the
+oracle's."""
 
 import os
 import sys
@@ -27,12 +28,12 @@ def main():
     dl = engine.DeviceLexicon.upload(plex)
     view = engine.DocView.of(c)
     hb = oracle.HostBatch(c, plex)
-    for t, p in ((0.5, 0.2), (0.4, 0.8), (0.0, 0.05)):
+    for t, p in ((0.5, 0.2), (0.4, 0.8), (0.0, 0.05), (0.3, float("inf"))):
         recs, cost = engine.mine(dc, dl, view, model, t, p)
         want, wcost = oracle.mine(hb, model, t, p, threads=os.cpu_count() or 8)
         assert np.array_equal(cost.view(np.uint64), wcost.view(np.uint64)), (t, p)
         assert recs.tobytes() == want.tobytes(), (t, p)
-    print("band-parallel extraction: records equal")
+    print("records equal")
 
 
 if __name__ == "__main__":

@@ -132,3 +132,22 @@ def test_band_parallel_extraction_vs_oracle(seed):
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "records equal" in r.stdout
+
+
+@pytest.mark.parametrize("env", [
+    {"BM_BAND_FUSED": "1", "BM_BAND_MIN_ITEMS": "1"},
+    {"BM_BAND_FUSED": "1", "BM_BAND_MIN_ITEMS": "1", "BM_PAR_WALK_MIN": "600"},
+])
+def test_fused_band_tier_vs_oracle(env):
+    """The fused banded tier (mine_band_kernel: scoring warps feeding the DP
+    warp through a shared-memory ring, no similarity matrix; extraction
+    re-scores the path cells), serial and band-parallel extraction, four
+    penalties including inf: records and costs equal the oracle's."""
+    import subprocess
+    import sys
+
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "par_walk_child.py")
+    r = subprocess.run([sys.executable, child, "2026"], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "records equal" in r.stdout

@@ -358,7 +358,8 @@ def test_mine_mixed_sizes_vs_oracle(oracle_mod, seed):
     dc = engine.DeviceCorpus.upload(sc.packed)
     dl = engine.DeviceLexicon.upload(plex)
     view = engine.DocView.of(sc.packed)
-    for t, p in ((0.5, 0.2), (0.2, 0.05)):
+    # 0 and inf: the DP's edge penalties (inf keeps the literal compare order)
+    for t, p in ((0.5, 0.2), (0.2, 0.05), (0.5, 0.0), (0.4, float("inf"))):
         recs, cost = engine.mine(dc, dl, view, model, t, p)
         hb = oracle_mod.HostBatch(sc.packed, plex)
         want, wcost = oracle_mod.mine(hb, model, t, p, threads=8)
