@@ -84,26 +84,9 @@ __device__ __forceinline__ BandSent band_sent(const bm_sentences& S, int g, doub
   const SentScalars v = load_scalars(S, g);
   BandSent b;
   b.tpad = (uint32_t)v.T | ((uint32_t)v.P << 8) | ((uint32_t)v.nA << 16) | ((uint32_t)v.nD << 24);
-  b.dx = v.nD == 0 ? 0u : v.nD == 1 ? (uint32_t)__ldg(S.dig_id + v.d0) + 1u : (kDigMany | (uint32_t)v.d0);
+  b.dx = digit_word(S, v.nD, v.d0);
   b.pos = pos;
   return b;
-}
-
-// w3 * f3 from two digit words (classifier.py:82-87): equal words with at
-// most one digit token each give the Jaccard 1.0 / 0.0 directly; otherwise the
-// intersection of the sorted digit sets (a single token is a one-id set).
-__device__ __forceinline__ double band_digit_term(const bm_sentences& S, const Model& M, double w3z,
-                                                  uint32_t ax, uint32_t bx, int aD, int bD) {
-  if (((ax | bx) & kDigMany) == 0) return ax == bx ? M.w[3] : w3z;
-  if (aD == 0 || bD == 0) return w3z;
-  int inter;
-  if (ax & bx & kDigMany)
-    inter = sorted_intersection(S.dig_id + (ax & ~kDigMany), aD, S.dig_id + (bx & ~kDigMany), bD);
-  else if (ax & kDigMany)
-    inter = sorted_contains(S.dig_id + (ax & ~kDigMany), aD, (int32_t)(bx - 1u)) ? 1 : 0;
-  else
-    inter = sorted_contains(S.dig_id + (bx & ~kDigMany), bD, (int32_t)(ax - 1u)) ? 1 : 0;
-  return __dmul_rn(M.w[3], frac_or_zero(inter, aD + bD - inter));
 }
 
 // 1 - S of one cell: folded_margin's additions in margin()'s order, then
@@ -116,7 +99,7 @@ __device__ __forceinline__ double band_cost(const bm_sentences& S, const Model& 
   double z = __ldg(mt.z1 + (((ta & 0xffu) << 8) | (tb & 0xffu)));
   z = __dadd_rn(z, __ldg(mt.p1 + ((hf << 8) | ((ta >> 16) & 0xffu))));
   z = __dadd_rn(z, __ldg(mt.p2 + ((hr << 8) | ((tb >> 16) & 0xffu))));
-  z = __dadd_rn(z, band_digit_term(S, M, w3z, ax, bx, (int)(ta >> 24), (int)(tb >> 24)));
+  z = __dadd_rn(z, digit_term_w(S, M, w3z, ax, bx, (int)(ta >> 24), (int)(tb >> 24)));
   z = __dadd_rn(z, __ldg(mt.p4 + ((ta & 0xff00u) | ((tb >> 8) & 0xffu))));
   z = __dadd_rn(z, __dmul_rn(M.w[5], __dsub_rn(1.0, fabs(__dsub_rn(pos_s, pos_t)))));
   z = __dadd_rn(z, M.w[6]);  // w6 * 1.0

@@ -369,6 +369,34 @@ __device__ __forceinline__ double digit_term(const bm_sentences& S, const Model&
   return __dmul_rn(M.w[3], frac_or_zero(inter, aD + bD - inter));
 }
 
+// Digit word of a sentence: its digit signature, or kDigMany | dig_off when it
+// has two or more digit tokens (the offset of its sorted digit set).
+__device__ __forceinline__ uint32_t digit_word(const bm_sentences& S, int nD, int d0) {
+  return nD == 0 ? 0u : nD == 1 ? (uint32_t)__ldg(S.dig_id + d0) + 1u : (kDigMany | (uint32_t)d0);
+}
+
+// |D_s & D_t| from two digit words, both sentences with a digit token.
+__device__ __forceinline__ int digit_inter(const bm_sentences& S, uint32_t ax, uint32_t bx, int aD,
+                                           int bD) {
+  if (((ax | bx) & kDigMany) == 0) return ax == bx ? 1 : 0;
+  if (ax & bx & kDigMany)
+    return sorted_intersection(S.dig_id + (ax & ~kDigMany), aD, S.dig_id + (bx & ~kDigMany), bD);
+  if (ax & kDigMany) return sorted_contains(S.dig_id + (ax & ~kDigMany), aD, (int32_t)(bx - 1u)) ? 1 : 0;
+  return sorted_contains(S.dig_id + (bx & ~kDigMany), bD, (int32_t)(ax - 1u)) ? 1 : 0;
+}
+
+// w3 * f3 from two digit words (classifier.py:82-87): equal words with at
+// most one digit token each give the Jaccard 1.0 / 0.0 directly; otherwise the
+// intersection of the sorted digit sets (a single token is a one-id set).
+// w3z = w3 * 0.0.
+__device__ __forceinline__ double digit_term_w(const bm_sentences& S, const Model& M, double w3z,
+                                               uint32_t ax, uint32_t bx, int aD, int bD) {
+  if (((ax | bx) & kDigMany) == 0) return ax == bx ? M.w[3] : w3z;
+  if (aD == 0 || bD == 0) return w3z;
+  const int inter = digit_inter(S, ax, bx, aD, bD);
+  return __dmul_rn(M.w[3], frac_or_zero(inter, aD + bD - inter));
+}
+
 // z of one cell from the model's folded tables (ModelTables; every count of
 // both sentences < kPairMax): the additions of margin() in its order.
 __device__ __forceinline__ double folded_margin(const bm_sentences& S, const Model& M,

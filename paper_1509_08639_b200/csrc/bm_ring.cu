@@ -37,6 +37,11 @@ constexpr int kProducers = kProdWarps * WARP;
 #ifndef BM_RING_SLOTS
 #define BM_RING_SLOTS 2
 #endif
+// cells per scoring thread and task (one row of a lane block: 4; half a row:
+// 2; one cell: 1)
+#ifndef BM_RING_CPT
+#define BM_RING_CPT 2
+#endif
 #ifndef BM_RING_MINB
 #define BM_RING_MINB 6
 #endif
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(kHitsThreads, BM_HITS_MINB) hits_kernel(bm_sen
 // the other three), the offset of its digit set, its document position.
 struct __align__(16) SPack {
   uint32_t tpad;  // T | P << 8 | nA << 16 | nD << 24
-  int32_t d0;
+  uint32_t dx;    // digit word (digit_word: signature, or kDigMany | offset)
   double pos;
 };
 
@@ -209,7 +214,7 @@ __device__ __forceinline__ SPack ld_spack(const SPack* p) {
   const int4 v = *reinterpret_cast<const int4*>(p);
   SPack q;
   q.tpad = (uint32_t)v.x;
-  q.d0 = v.y;
+  q.dx = (uint32_t)v.y;
   q.pos = __hiloint2double(v.w, v.z);
   return q;
 }
@@ -235,16 +240,7 @@ __device__ __forceinline__ double staged_margin(const bm_sentences& S, const Mod
   double z = __ldg(mt.z1 + aT * kPairMax + bT);
   z = __dadd_rn(z, __ldg(mt.p1 + hf * kPairMax + aA));
   z = __dadd_rn(z, __ldg(mt.p2 + hr * kPairMax + bA));
-  double p3;
-  if ((aD | bD) == 0) {
-    p3 = M.w[3];  // w3 * 1.0
-  } else if (aD == 0 || bD == 0) {
-    p3 = __dmul_rn(M.w[3], 0.0);
-  } else {
-    const int inter = sorted_intersection(S.dig_id + a.d0, aD, S.dig_id + b.d0, bD);
-    p3 = __dmul_rn(M.w[3], frac_or_zero(inter, aD + bD - inter));
-  }
-  z = __dadd_rn(z, p3);
+  z = __dadd_rn(z, digit_term_w(S, M, __dmul_rn(M.w[3], 0.0), a.dx, b.dx, aD, bD));
   z = __dadd_rn(z, __ldg(mt.p4 + aP * kPairMax + bP));
   z = __dadd_rn(z, __dmul_rn(M.w[5], __dsub_rn(1.0, fabs(__dsub_rn(a.pos, b.pos)))));
   z = __dadd_rn(z, M.w[6]);  // w6 * 1.0
@@ -259,7 +255,7 @@ __device__ __forceinline__ double staged_margin(const bm_sentences& S, const Mod
   } else if (aD == 0 || bD == 0) {
     f[3] = 0.0;  // 0 / |D_s | D_t|
   } else {
-    const int inter = sorted_intersection(S.dig_id + a.d0, aD, S.dig_id + b.d0, bD);
+    const int inter = digit_inter(S, a.dx, b.dx, aD, bD);
     f[3] = frac_or_zero(inter, aD + bD - inter);
   }
   f[4] = __ldg(tb.ratio2 + aP * kPairMax + bP);
@@ -310,7 +306,6 @@ template <int R>
 __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_ring_kernel(FusedArgs a) {
   using CodeT = typename std::conditional<R == 8, uint64_t, uint32_t>::type;
   constexpr int RL = ring_lane(R);
-  constexpr int BPT = 8 / R;  // lane blocks per 32-cell scoring task
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bm_sentences& S = a.S;
@@ -383,7 +378,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
       const SentScalars v = load_scalars(S, g);
       SPack q;
       q.tpad = (uint32_t)v.T | ((uint32_t)v.P << 8) | ((uint32_t)v.nA << 16) | ((uint32_t)v.nD << 24);
-      q.d0 = v.d0;
+      q.dx = digit_word(S, v.nD, v.d0);
       q.pos = row ? doc_pos(k, n) : doc_pos(k - n, m);
       sp[k] = q;
     }
@@ -463,33 +458,52 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
       }
     } else {
       // ------------------------------------------------------ score warps
-      // tasks: 32 cells = BPT lane blocks of one super-step; the tasks of all
-      // super-steps form one sequence and producer warp w takes every 4th
-      // (w, w + 4, ...), which balances the ragged fill/drain super-steps.
-      // Rows/columns past the matrix are skipped (never read by the DP).
+      // a task is 32 / R lane blocks of one super-step; a thread scores one row
+      // of its R x 4 block (4 cells: the row's sentence and hit words loaded
+      // once). The tasks of all super-steps form one sequence and producer
+      // warp w takes every 4th (w, w + 4, ...), which balances the ragged
+      // fill/drain super-steps. Rows past the matrix are skipped; a column
+      // past m re-scores column m - 1 (never read by the DP).
       static_assert(kProdWarps == 4, "task striding assumes 4 producer warps");
+      constexpr int CPT = BM_RING_CPT;              // cells per thread and task
+      constexpr int TPB = R * (4 / CPT);            // threads per R x 4 lane block
+      constexpr int TL = WARP / TPB;                // lane blocks per task
       const int pw = warp - 1;
-      const int tb = lane / (4 * R), r = (lane >> 2) % R, c = lane & 3;
-      const int toff = tb * RL + r * 4 + c;
+      const int sub = lane / TPB, r = (lane % TPB) / (4 / CPT), c0 = (lane % (4 / CPT)) * CPT;
+      const double w3z = __dmul_rn(a.M.w[3], 0.0);
       int q0 = 0;  // sequence index of super-step t's first task
       for (int t = 0; t < steps; ++t) {
         if (t >= kSlots) mbar_wait_backoff(bar_empty + (t % kSlots), (uint32_t)(((t / kSlots) - 1) & 1));
         const int2 la = active_lanes(t, ngroups, nl);
-        const int ntask = (la.y - la.x + BPT) / BPT;
-        double* slot = ring + (size_t)(t % kSlots) * slot_d + la.x * RL + toff;
+        const int ntask = (la.y - la.x + TL) / TL;
+        double* slot = ring + (size_t)(t % kSlots) * slot_d;
         for (int kt = (pw - q0) & 3; kt < ntask; kt += kProdWarps) {
-          const int L = la.x + kt * BPT + tb;
-          const int i = L * R + r, j = 4 * (t - L) + c;
-          if (L <= la.y && i < n && j < m) {
-            const uint32_t hv = hits16[i * m + j];
+          const int L = la.x + kt * TL + sub;
+          const int i = L * R + r, j0 = 4 * (t - L) + c0;
+          if (L <= la.y && i < n) {
+            const SPack sa = ld_spack(sp + i);
+            const uint16_t* hrow = hits16 + i * m;
+            double o[CPT];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              const int j = min(j0 + c, m - 1);
+              const uint32_t hv = hrow[j];
 #ifdef BM_PROF_FAKE_SCORE  // timing experiment only: DP side lower bound
-            slot[kt * (BPT * RL)] = __dsub_rn(1.0, (double)(hv & 0xff) * 0.01 + sp[i].pos);
+              o[c] = __dsub_rn(1.0, (double)(hv & 0xff) * 0.01 + sa.pos);
 #else
-            slot[kt * (BPT * RL)] = bmexp::one_minus_confidence(
-                staged_margin(S, a.M, a.tabs, a.mt, ld_spack(sp + i), ld_spack(sp + n + j), hv & 0xff,
-                              hv >> 8),
-                exp_tab);
+              o[c] = bmexp::one_minus_confidence(
+                  staged_margin(S, a.M, a.tabs, a.mt, sa, ld_spack(sp + n + j), hv & 0xff, hv >> 8),
+                  exp_tab);
 #endif
+            }
+            double* dst = slot + L * RL + r * 4 + c0;
+            if (CPT == 1) {
+              dst[0] = o[0];
+            } else {
+#pragma unroll
+              for (int c = 0; c < CPT; c += 2)
+                *reinterpret_cast<double2*>(dst + c) = make_double2(o[c], o[(c + 1) % CPT]);
+            }
           }
         }
         q0 += ntask;
