@@ -309,9 +309,24 @@ __global__ void scatter_results_kernel(const int32_t* idx, int k, const double* 
   }
 }
 
+// BM_TRACE=1: host-side phase timings of the planning code on stderr.
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  const char* fn;
+  explicit HostTrace(const char* f) : on(getenv("BM_TRACE") != nullptr), t0(std::chrono::steady_clock::now()), fn(f) {}
+  void mark(const char* what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[bm trace] %s %-24s %8.3f ms\n", fn, what,
+            std::chrono::duration<double, std::milli>(t - t0).count());
+  }
+};
+
 int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, GeneralDev& dv,
                     cudaStream_t st, bool store_s = true) {
   const int k = (int)g.docs.size();
+  HostTrace tr("general_prepare");
   int32_t* idx = nullptr;
   BM_CK(sc.upload(&idx, g.docs), "upload");
   BM_CK(sc.upload(&dv.s_off, g.s_off), "upload");
@@ -321,6 +336,7 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
   BM_CK(sc.upload(&dv.n, g.n), "upload");
   BM_CK(sc.upload(&dv.m, g.m), "upload");
   BM_CK(sc.upload(&dv.tiles, g.tiles), "upload");
+  tr.mark("plan uploads");
   // (doc, band) work order of the banded DP. A band waits for the band above
   // to publish its bottom row; BM_NW_STAGGER = K places band b of the q-th
   // document at position q + b * K instead of next to band b - 1 (K = 0), so
@@ -339,13 +355,16 @@ int general_prepare(const GeneralPlan& g, const bm_docs* docs, Scratch& sc, Gene
     dv.order = g.items;
   }
   BM_CK(sc.upload(&dv.items, dv.order), "upload");
+  tr.mark("items");
   BM_CK(sc.alloc(&dv.src0, k), "alloc");
   BM_CK(sc.alloc(&dv.tgt0, k), "alloc");
   dv.S = nullptr;  // the fused banded tier never stores the matrix
   if (store_s) BM_CK(ws_get(st, kWsS, &dv.S, (size_t)g.s_total), "alloc S");
+  tr.mark("S workspace");
   BM_CK(ws_get(st, kWsDirs, &dv.dirs, (size_t)g.dir_total), "alloc dirs");
   BM_CK(ws_get(st, kWsBnd, &dv.bnd, (size_t)g.bnd_total), "alloc boundary");
   BM_CK(sc.alloc(&dv.ticket, 1), "alloc ticket");
+  tr.mark("workspaces");
   gather_docs_kernel<<<(k + 255) / 256, 256, 0, st>>>(*docs, idx, k, dv.src0, dv.tgt0);
   BM_CK(cudaGetLastError(), "gather_docs");
   note_launch();
@@ -396,19 +415,6 @@ size_t fused_max_smem() {
   return v;
 }  // NaN fails (aligner.py:209-213)
 
-// BM_TRACE=1: host-side phase timings of the planning code on stderr.
-struct HostTrace {
-  bool on;
-  std::chrono::steady_clock::time_point t0;
-  const char* fn;
-  explicit HostTrace(const char* f) : on(getenv("BM_TRACE") != nullptr), t0(std::chrono::steady_clock::now()), fn(f) {}
-  void mark(const char* what) {
-    if (!on) return;
-    auto t = std::chrono::steady_clock::now();
-    fprintf(stderr, "[bm trace] %s %-24s %8.3f ms\n", fn, what,
-            std::chrono::duration<double, std::milli>(t - t0).count());
-  }
-};
 
 // Banded tier for the documents of `g` (K1 -> K2/K3 -> K4, then scatter into
 // the caller's per-document record slots).
@@ -453,6 +459,38 @@ int score_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs&
   return BM_OK;
 }
 
+// `after` waits for everything enqueued on `before` so far.
+static cudaError_t stream_after(cudaStream_t after, cudaStream_t before) {
+  cudaEvent_t e;
+  cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (r != cudaSuccess) return r;
+  r = cudaEventRecord(e, before);
+  if (r == cudaSuccess) r = cudaStreamWaitEvent(after, e, 0);
+  cudaEventDestroy(e);
+  return r;
+}
+
+static bool dp_prio_on() {
+  static const bool v = getenv("BM_DP_PRIO") ? atoi(getenv("BM_DP_PRIO")) != 0 : false;
+  return v;
+}
+
+// The high-priority companion stream of a mining stream (one per stream and
+// device, created on first use, kept for the thread's lifetime).
+static cudaStream_t dp_stream(cudaStream_t st) {
+  static thread_local std::vector<std::pair<std::pair<cudaStream_t, int>, cudaStream_t>> map;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (auto& e : map)
+    if (e.first.first == st && e.first.second == dev) return e.second;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess) return st;
+  map.push_back({{st, dev}, s});
+  return s;
+}
+
 // Band-parallel extraction (launch_extract_banded): documents whose path is at
 // least BM_PAR_WALK_MIN moves long (default 8192; 0 disables), while the exit
 // maps of the plan stay within kParWalkBudget walks (one walk per band and
@@ -480,44 +518,13 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
     rc = score_general(g, sent, D, lex, M, dv, doc_join, sc, st, /*join_only=*/fused);
     if (rc) return rc;
     tr.mark("score enqueued");
+    // every buffer of the DP and extraction phase is allocated and uploaded on
+    // st first; the phase itself may then run on the high-priority DP stream
     double* cost_l = nullptr;
     BM_CK(sc.alloc(&cost_l, k), "alloc");
-    if (fused) {
-      // score + DP per (doc, band) item in one kernel (bm_band.cu)
-      BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
-      BM_CK(cudaMemsetAsync(dv.bnd, 0xde, std::max<int64_t>(g.bnd_total, 1) * 8, st), "memset");
-      BandArgs a;
-      a.S = *sent;
-      a.D = D;
-      a.M = M;
-      BM_CK(model_tables(M, &a.mt), "model tables");
-      a.hits = dv.hits;
-      a.h_off = dv.h_off;
-      a.pitch = dv.pitch;
-      a.p = penalty;
-      a.dirs = dv.dirs;
-      a.dir_off = dv.dir_off;
-      a.cost = cost_l;
-      a.items = dv.items;
-      a.n_items = (int)g.items.size();
-      a.ticket = dv.ticket;
-      a.bnd = dv.bnd;
-      a.bnd_off = dv.bnd_off;
-      const int m_max = *std::max_element(g.m.begin(), g.m.end());
-      BM_CK(launch_band(a, m_max, st), "mine_band_kernel");
-    } else {
-      rc = general_nw(g, dv, penalty, cost_l, st);
-      if (rc) return rc;
-    }
-    tr.mark("nw enqueued");
-    CellSrc cs;
-    cs.S = dv.S;
-    cs.s_off = dv.s_off;
-    cs.sent = *sent;
-    cs.D = D;
-    cs.M = M;
-    cs.hits = dv.hits;
-    cs.h_off = dv.h_off;
+    BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
+    // boundary rows start as the sentinel (negative) pattern consumers spin on
+    BM_CK(cudaMemsetAsync(dv.bnd, 0xde, std::max<int64_t>(g.bnd_total, 1) * 8, st), "memset");
     std::vector<int64_t> roff(k);
     int64_t rt = 0;
     for (int q = 0; q < k; ++q) {
@@ -581,13 +588,77 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
     }
     uint8_t* dskip = nullptr;
     if (bx.n_big) BM_CK(sc.upload(&dskip, skip), "upload");
+    ModelTables mt;
+    BM_CK(model_tables(M, &mt), "model tables");
+    // BM_DP_PRIO: the latency-bound phase (DP, extraction) on a high-priority
+    // stream, so its CTAs are dispatched next to the scoring kernels of other
+    // groups instead of queueing behind their waves (experiments)
+    cudaStream_t sd = st;
+    if (dp_prio_on()) {
+      sd = dp_stream(st);
+      BM_CK(stream_after(sd, st), "event");
+    }
+    struct Rejoin {
+      cudaStream_t st, sd;
+      ~Rejoin() {
+        if (sd != st && stream_after(st, sd) != cudaSuccess) cudaStreamSynchronize(sd);
+      }
+    } rejoin{st, sd};
+    if (fused) {
+      // score + DP per (doc, band) item in one kernel (bm_band.cu)
+      BandArgs a;
+      a.S = *sent;
+      a.D = D;
+      a.M = M;
+      a.mt = mt;
+      a.hits = dv.hits;
+      a.h_off = dv.h_off;
+      a.pitch = dv.pitch;
+      a.p = penalty;
+      a.dirs = dv.dirs;
+      a.dir_off = dv.dir_off;
+      a.cost = cost_l;
+      a.items = dv.items;
+      a.n_items = (int)g.items.size();
+      a.ticket = dv.ticket;
+      a.bnd = dv.bnd;
+      a.bnd_off = dv.bnd_off;
+      const int m_max = *std::max_element(g.m.begin(), g.m.end());
+      BM_CK(launch_band(a, m_max, sd), "mine_band_kernel");
+    } else {
+      NwArgs a;
+      a.S = dv.S;
+      a.s_off = dv.s_off;
+      a.pitch = dv.pitch;
+      a.n = dv.n;
+      a.m = dv.m;
+      a.p = penalty;
+      a.dirs = dv.dirs;
+      a.dir_off = dv.dir_off;
+      a.cost = cost_l;
+      a.items = dv.items;
+      a.n_items = (int)g.items.size();
+      a.ticket = dv.ticket;
+      a.bnd = dv.bnd;
+      a.bnd_off = dv.bnd_off;
+      BM_CK(launch_nw(a, sd), "nw_band_kernel");
+    }
+    tr.mark("nw enqueued");
+    CellSrc cs;
+    cs.S = dv.S;
+    cs.s_off = dv.s_off;
+    cs.sent = *sent;
+    cs.D = D;
+    cs.M = M;
+    cs.hits = dv.hits;
+    cs.h_off = dv.h_off;
     BM_CK(launch_extract(dv.dirs, dv.dir_off, cs, dv.pitch, dv.n, dv.m, k, threshold,
-                         droff, rl, cl, st, dskip),
+                         droff, rl, cl, sd, dskip),
           "extract_kernel");
     BM_CK(launch_extract_banded(dv.dirs, dv.dir_off, cs, dv.pitch, dv.n, dv.m, bx,
-                                threshold, droff, rl, cl, st),
+                                threshold, droff, rl, cl, sd),
           "band-parallel extraction");
-    scatter_results_kernel<<<k, 128, 0, st>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
+    scatter_results_kernel<<<k, 128, 0, sd>>>(idx, k, cost_l, cost, rl, droff, cl, rec_off, rec,
                                               rec_count);
     BM_CK(cudaGetLastError(), "scatter_results");
     note_launch();

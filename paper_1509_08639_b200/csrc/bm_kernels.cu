@@ -776,6 +776,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // next block, shuffles and stores with the 7-cell dependency chain of the
 // current one. S for block g+1 is loaded and turned into 1-S during block g
 // (two register sets, ping-pong by a 2x unrolled loop).
+#ifndef BM_NW_DIRECT
+#define BM_NW_DIRECT 0
+#endif
 #ifndef BM_NW_EARLY_BND
 #define BM_NW_EARLY_BND 1
 #endif
@@ -867,9 +870,15 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
     __syncwarp();
 #pragma unroll 1
     for (int q = 0; q < D; ++q) issue(q - lane);
+#if BM_NW_DIRECT
+    // direct mode: a block's S is read from its ring slot right before the
+    // block is computed (no second register set); the slot is refilled after
+    double oA[1], oB[1];
+#else
     cp_async_wait_depth<D>();
     double oA[16], oB[16];
     load(-lane, oA);
+#endif
 
     // per penalty: C[i+1][4g] left of the block, the last row of the previous
     // block, and C[i0][4g] above-left of the block
@@ -887,7 +896,7 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
       dgn[q] = (double)i0 * pq[q];
     }
 
-    auto step = [&](const int t, double(&oc)[16], double(&on)[16]) {
+    auto step = [&](const int t, double(&oc_)[BM_NW_DIRECT ? 1 : 16], double(&on)[BM_NW_DIRECT ? 1 : 16]) {
       const int g = t - lane;
       if ((t & (kNwChunkG - 1)) == 0 && 4 * t < m) {
         NW_PROF(const unsigned long long w0 = gtimer();)
@@ -951,9 +960,18 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
           dgn[q] = (double)i0 * pq[q];
         }
       }
+#if BM_NW_DIRECT
+      cp_async_wait_depth<D>();  // block g has landed (g+1 .. g+D-1 in flight)
+      double oc[16];
+      load(g, oc);
+      (void)oc_;
+      (void)on;
+#else
+      auto& oc = oc_;
       issue(g + D);
       cp_async_wait_depth<D>();  // block g+1 has landed
       load(g + 1, on);
+#endif
 
       // the 4x4 block of every penalty, anti-diagonal order; C + p of the row
       // above and of the left column once per block, every other C + p once
@@ -1016,6 +1034,9 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
               cmax == 1 ? row[0] : cmax == 2 ? row[1] : cmax == 3 ? row[2] : row[3];
         }
       }
+#if BM_NW_DIRECT
+      issue(g + D);  // into the slot block g was read from (its values are consumed)
+#endif
     };
     const int steps = ngroups + nl - 1;
 #pragma unroll 1
