@@ -470,6 +470,12 @@ static cudaError_t stream_after(cudaStream_t after, cudaStream_t before) {
   return r;
 }
 
+// BM_NW_SEQ=0: the tuner's single-band documents keep one DP item each
+static bool nw_seq_on() {
+  static const bool v = getenv("BM_NW_SEQ") ? atoi(getenv("BM_NW_SEQ")) != 0 : true;
+  return v;
+}
+
 static bool dp_prio_on() {
   static const bool v = getenv("BM_DP_PRIO") ? atoi(getenv("BM_DP_PRIO")) != 0 : false;
   return v;
@@ -1666,10 +1672,44 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     BM_CK(sc.alloc(&dirs, (size_t)dstride * width), "alloc dirs");
     BM_CK(sc.alloc(&bnd, (size_t)bstride * width), "alloc boundary");
   }
+  // single-band documents (n <= 128) run end to end in runs (nw_seq_kernel:
+  // the wavefront's fill and drain once per run instead of once per
+  // document); the others keep their (doc, band) items
+  std::vector<int32_t> seq_off;  // (begin, end) plan indices per run
+  std::vector<WorkItem> multi;
+  if (nw_seq_on()) {
+    int64_t single = 0;
+    for (int q = 0; q < k; ++q) single += g.n[q] <= kBandRows;
+    // about 4 runs per resident DP warp (8 per SM at 4 penalties): runs long
+    // enough to amortise the fill, numerous enough to balance the warps
+    const int run = (int)std::max<int64_t>(1, std::min<int64_t>(kSeqMaxDocs, single / (4 * 8 * 148)));
+    for (int q = 0; q < k;) {
+      if (g.n[q] > kBandRows) {
+        ++q;
+        continue;
+      }
+      const int q1 = q;
+      while (q < k && q - q1 < run && g.n[q] <= kBandRows) ++q;
+      seq_off.push_back(q1);
+      seq_off.push_back(q);
+    }
+    for (const WorkItem& w : dv.order)
+      if (g.n[w.doc] > kBandRows) multi.push_back(w);
+  }
+  int32_t* d_seq = nullptr;
+  WorkItem* d_multi = nullptr;
+  unsigned int* seq_ticket = nullptr;
+  const int n_runs = (int)seq_off.size() / 2;
+  if (n_runs > 0) {
+    BM_CK(sc.upload(&d_seq, seq_off), "upload");
+    BM_CK(sc.upload(&d_multi, multi), "upload");
+    BM_CK(sc.alloc(&seq_ticket, 1), "alloc");
+  }
   for (int q0 = 0; q0 < n_pen;) {
     int np = width;
     while (q0 + np > n_pen) np /= 2;
     BM_CK(cudaMemsetAsync(dv.ticket, 0, 4, st), "memset");
+    if (n_runs > 0) BM_CK(cudaMemsetAsync(seq_ticket, 0, 4, st), "memset");
     BM_CK(cudaMemsetAsync(bnd, 0xde, (size_t)bstride * np * 8, st), "memset");
     NwArgs a;
     a.S = dv.S;
@@ -1691,7 +1731,18 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     a.bnd = bnd;
     a.bnd_stride = bstride;
     a.bnd_off = dv.bnd_off;
-    BM_CK(launch_nw(a, st), "nw_band_kernel");
+    if (n_runs > 0) {
+      a.items = d_multi;
+      a.n_items = (int)multi.size();
+      BM_CK(launch_nw(a, st), "nw_band_kernel");
+      NwArgs b = a;
+      b.ticket = seq_ticket;
+      b.seq_off = d_seq;
+      b.n_seq = n_runs;
+      BM_CK(launch_nw_seq(b, st), "nw_seq_kernel");
+    } else {
+      BM_CK(launch_nw(a, st), "nw_band_kernel");
+    }
     for (int q = 0; q < np; ++q) {
       const size_t pq = (size_t)(q0 + q) * n_thr;
       BM_CK(launch_tune_count(dirs + (size_t)q * dstride, dv.dir_off, dv.S, dv.s_off, dv.pitch,

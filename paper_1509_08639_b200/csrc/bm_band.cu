@@ -43,6 +43,15 @@ namespace bm {
 #ifndef BM_BAND_MINB
 #define BM_BAND_MINB (BM_BAND_CPT == 4 ? 5 : 3)
 #endif
+// scoring warps: one arrival per warp on the full barriers (fewer mbarrier
+// events wake fewer sleeping waiters); empty-slot waits sleep up to
+// BM_BAND_SLEEP_NS instead of retrying try_wait (0: try_wait loop)
+#ifndef BM_BAND_WARP_ARRIVE
+#define BM_BAND_WARP_ARRIVE 1
+#endif
+#ifndef BM_BAND_SLEEP_NS
+#define BM_BAND_SLEEP_NS 256
+#endif
 constexpr int kBandCpt = BM_BAND_CPT;
 static_assert(kBandCpt == 4 || kBandCpt == 2, "2 or 4 cells per thread");
 constexpr int kBandProdWarps = 16 / kBandCpt;        // every lane block of a super-step scored at once
@@ -127,7 +136,7 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
     if (tid == 0) {
       misc[0] = (int)atomicAdd(a.ticket, 1u);
       for (int q = 0; q < kBandSlots; ++q) {
-        mbar_init(bar_full + q, kBandProdWarps * WARP);
+        mbar_init(bar_full + q, BM_BAND_WARP_ARRIVE ? kBandProdWarps : kBandProdWarps * WARP);
         mbar_init(bar_empty + q, 1);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -336,7 +345,12 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
         q0 += ntask_of(t);
         nk = task_of(t + 1, q0);
         nh = hits_of(nk);
-        if (t >= kBandSlots) mbar_wait_backoff(bar_empty + slot, (uint32_t)(((t / kBandSlots) - 1) & 1));
+        if (t >= kBandSlots) {
+          if (BM_BAND_SLEEP_NS > 0)
+            mbar_wait_sleep(bar_empty + slot, (uint32_t)(((t / kBandSlots) - 1) & 1), BM_BAND_SLEEP_NS);
+          else
+            mbar_wait_backoff(bar_empty + slot, (uint32_t)(((t / kBandSlots) - 1) & 1));
+        }
         if (pw == t % kBandProdWarps && lane < 4) {
           const int j = 4 * (t + kBandAhead) + lane;
           if (j < m)
@@ -376,7 +390,14 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
                            : "memory");
           }
         }
-        mbar_arrive(bar_full + slot);
+        if (BM_BAND_WARP_ARRIVE) {
+          // the warp's ring stores are ordered before lane 0's (release)
+          // arrival by the warp barrier
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_full + slot);
+        } else {
+          mbar_arrive(bar_full + slot);
+        }
       }
     }
   }

@@ -95,7 +95,12 @@ struct NwArgs {
   double pv[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t dir_stride = 0, bnd_stride = 0;
   int cost_stride = 0;
+  // runs of single-band documents (nw_seq_kernel): run r is the plan's
+  // documents [seq_off[2r], seq_off[2r + 1]), at most kSeqMaxDocs
+  const int32_t* seq_off = nullptr;
+  int n_seq = 0;
 };
+cudaError_t launch_nw_seq(const NwArgs& a, cudaStream_t st);
 
 struct FusedArgs {
   bm_sentences S;

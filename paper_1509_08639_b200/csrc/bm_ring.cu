@@ -37,6 +37,14 @@ constexpr int kProducers = kProdWarps * WARP;
 #ifndef BM_RING_SLOTS
 #define BM_RING_SLOTS 2
 #endif
+// scoring warps: one full-barrier arrival per warp; empty-slot waits sleep up
+// to BM_RING_SLEEP_NS (0: try_wait loop)
+#ifndef BM_RING_WARP_ARRIVE
+#define BM_RING_WARP_ARRIVE 0
+#endif
+#ifndef BM_RING_SLEEP_NS
+#define BM_RING_SLEEP_NS 0
+#endif
 // cells per scoring thread and task (one row of a lane block: 4; half a row:
 // 2; one cell: 1)
 #ifndef BM_RING_CPT
@@ -110,6 +118,29 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) 
         : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
         : "memory");
   } while (!done);
+}
+
+// A wait that does not spin on the issue slots: a non-blocking phase test,
+// then a sleep that doubles up to max_ns. For warps whose wait is not on the
+// critical path (scoring warps ahead of their DP warp): try_wait with a
+// suspend hint wakes at every mbarrier event of the CTA, and the producers'
+// retry loop took a quarter of the fused banded kernel's issue slots.
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred P1;\n mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, uint32_t max_ns) {
+  uint32_t ns = 32;
+  while (!mbar_test(b, parity)) {
+    __nanosleep(ns);
+    ns = ns < max_ns ? 2 * ns : max_ns;
+  }
 }
 
 __host__ __device__ constexpr int ring_lane(int R) { return R * 4 + 2; }
@@ -337,7 +368,7 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
     RING_PROF(0)
     if (tid == 0) {
       for (int q = 0; q < kSlots; ++q) {
-        mbar_init(bar_full + q, kProducers);
+        mbar_init(bar_full + q, BM_RING_WARP_ARRIVE ? kProdWarps : kProducers);
         mbar_init(bar_empty + q, 1);
       }
       mbar_init(bar_load, 1);
@@ -473,7 +504,12 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
       const double w3z = __dmul_rn(a.M.w[3], 0.0);
       int q0 = 0;  // sequence index of super-step t's first task
       for (int t = 0; t < steps; ++t) {
-        if (t >= kSlots) mbar_wait_backoff(bar_empty + (t % kSlots), (uint32_t)(((t / kSlots) - 1) & 1));
+        if (t >= kSlots) {
+          if (BM_RING_SLEEP_NS > 0)
+            mbar_wait_sleep(bar_empty + (t % kSlots), (uint32_t)(((t / kSlots) - 1) & 1), BM_RING_SLEEP_NS);
+          else
+            mbar_wait_backoff(bar_empty + (t % kSlots), (uint32_t)(((t / kSlots) - 1) & 1));
+        }
         const int2 la = active_lanes(t, ngroups, nl);
         const int ntask = (la.y - la.x + TL) / TL;
         double* slot = ring + (size_t)(t % kSlots) * slot_d;
@@ -507,7 +543,12 @@ __global__ void __launch_bounds__(kRingThreads, R == 8 ? 4 : BM_RING_MINB) mine_
           }
         }
         q0 += ntask;
-        mbar_arrive(bar_full + (t % kSlots));
+        if (BM_RING_WARP_ARRIVE) {
+          __syncwarp();  // the warp's ring stores before lane 0's (release) arrival
+          if (lane == 0) mbar_arrive(bar_full + (t % kSlots));
+        } else {
+          mbar_arrive(bar_full + (t % kSlots));
+        }
       }
     }
     __syncthreads();  // DP complete: direction codes final
