@@ -470,6 +470,15 @@ static cudaError_t stream_after(cudaStream_t after, cudaStream_t before) {
   return r;
 }
 
+// BM_DP_OVERLAP=1: a few long documents' DP starts each band as soon as its
+// tiles are scored (opt-in: measured on C4 2.81 -> 4.5 ms -- the 64 DP warps
+// share their SMs' schedulers with the scoring CTAs and their latency chain
+// slows by more than the scoring time it hides)
+static bool dp_overlap_on() {
+  static const bool v = getenv("BM_DP_OVERLAP") ? atoi(getenv("BM_DP_OVERLAP")) != 0 : false;
+  return v;
+}
+
 // BM_NW_SEQ=0: the tuner's single-band documents keep one DP item each
 static bool nw_seq_on() {
   static const bool v = getenv("BM_NW_SEQ") ? atoi(getenv("BM_NW_SEQ")) != 0 : true;
@@ -516,14 +525,42 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
     const int k = (int)g.docs.size();
     for (int q = 0; q < k && fused; ++q) fused = g.n[q] <= 65535 && g.m[q] <= 65535;
     fused = fused && doc_join;
+    // a few long documents (C4: 64 bands of one 8192^2 pair) leave most SMs to
+    // the scoring kernel while their DP runs: the DP starts each band as soon
+    // as the band's tiles are scored (readiness counters) instead of after the
+    // whole matrix. Only with at most one band per SM, so the spinning DP
+    // warps can never take the resources the scoring CTAs need.
+    bool dj = doc_join;
+    for (int q = 0; q < k && dj; ++q) dj = g.n[q] <= 65535 && g.m[q] <= 65535;
+    int sms = 0;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const bool overlap = !fused && dj && dp_overlap_on() && (int64_t)g.items.size() <= sms;
     GeneralDev dv;
     int rc = general_prepare(g, docs, sc, dv, st, /*store_s=*/!fused);
     if (rc) return rc;
     tr.mark("prepare");
     const bm_docs D = local_docs(dv, k);
-    rc = score_general(g, sent, D, lex, M, dv, doc_join, sc, st, /*join_only=*/fused);
+    rc = score_general(g, sent, D, lex, M, dv, doc_join, sc, st, /*join_only=*/fused || overlap);
     if (rc) return rc;
     tr.mark("score enqueued");
+    int* ready = nullptr;
+    int32_t* band_base = nullptr;
+    if (overlap) {
+      BM_CK(preload_score_hits(), "load score_hits_kernel");
+      std::vector<int32_t> bb(k);
+      int32_t nb = 0;
+      for (int q = 0; q < k; ++q) {
+        bb[q] = nb;
+        nb += (g.n[q] + kBandRows - 1) / kBandRows;
+      }
+      BM_CK(sc.upload(&band_base, bb), "upload");
+      BM_CK(sc.alloc(&ready, (size_t)nb), "alloc");
+      BM_CK(cudaMemsetAsync(ready, 0, (size_t)nb * 4, st), "memset");
+    }
     // every buffer of the DP and extraction phase is allocated and uploaded on
     // st first; the phase itself may then run on the high-priority DP stream
     double* cost_l = nullptr;
@@ -600,7 +637,7 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
     // stream, so its CTAs are dispatched next to the scoring kernels of other
     // groups instead of queueing behind their waves (experiments)
     cudaStream_t sd = st;
-    if (dp_prio_on()) {
+    if (dp_prio_on() || overlap) {
       sd = dp_stream(st);
       BM_CK(stream_after(sd, st), "event");
     }
@@ -647,7 +684,16 @@ int mine_general(const GeneralPlan& g, const bm_sentences* sent, const bm_docs* 
       a.ticket = dv.ticket;
       a.bnd = dv.bnd;
       a.bnd_off = dv.bnd_off;
+      a.ready = ready;
+      a.band_base = band_base;
       BM_CK(launch_nw(a, sd), "nw_band_kernel");
+      if (overlap) {
+        // the scoring kernel beside the DP; extraction reads S after both
+        BM_CK(launch_score_hits(*sent, D, *lex, M, mt, nullptr, 0, dv.hits, dv.h_off, dv.tiles,
+                                (int)g.tiles.size(), dv.s_off, dv.pitch, dv.S, st, ready, band_base),
+              "score_hits_kernel");
+        BM_CK(stream_after(sd, st), "event");
+      }
     }
     tr.mark("nw enqueued");
     CellSrc cs;

@@ -171,6 +171,12 @@ __device__ __forceinline__ uint2 ld_stream_v2(const uint32_t* p) {
 #endif
 }
 
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const double* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -452,11 +458,11 @@ __device__ __forceinline__ double fold_cell(const bm_sentences& S, const Model& 
   return __dadd_rn(z, M.w[6]);  // w6 * 1.0
 }
 
-__global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
-    bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
-    const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
-    const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
-    double* __restrict__ out) {
+__device__ __forceinline__ void score_hits_tile(
+    const bm_sentences& S, const bm_docs& D, const Model& M, const ModelTables& mt,
+    const int4* __restrict__ tiles, const int64_t* __restrict__ s_off,
+    const int32_t* __restrict__ pitch, const uint32_t* __restrict__ hits,
+    const int64_t* __restrict__ h_off, double* __restrict__ out) {
   static_assert(kPairMax == 256, "folded tables are indexed by byte fields");
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* exp_tab = (uint64_t*)smem;
@@ -547,6 +553,34 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
   }
 }
 
+// One 64 x 64 tile of S. With `ready` (scoring overlapped with the DP, see
+// mine_general): once the tile is written, its CTA adds 1 to the counter of
+// the 128-row band it belongs to; nw_band_kernel starts a band when all of
+// the band's tiles are counted (the fence orders the tile's stores first).
+__global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
+    bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
+    const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
+    const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
+    double* __restrict__ out, int* __restrict__ ready, const int32_t* __restrict__ band_base) {
+  score_hits_tile(S, D, M, mt, tiles, s_off, pitch, hits, h_off, out);
+  if (ready != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int4 tile = tiles[blockIdx.x];
+      __threadfence();
+      atomicAdd(ready + band_base[tile.x] + tile.y / kBandRows, 1);
+    }
+  }
+}
+
+// Loads score_hits_kernel's code (lazy module loading would otherwise load
+// it at its first launch, which waits for the device -- where the DP warps of
+// an overlapped launch spin on the tiles this kernel has not scored yet).
+cudaError_t preload_score_hits() {
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, score_hits_kernel);
+}
+
 size_t hits_doc_smem_bytes() {
   return align16(join_smem_bytes(kDocJoinEmax, kDocJoinBuckets)) + (size_t)kDocJoinEmax * 4;
 }
@@ -570,7 +604,7 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
                               int n_items, uint32_t* hits,
                               const int64_t* h_off, const int4* tiles, int n_tiles,
                               const int64_t* s_off, const int32_t* pitch, double* out,
-                              cudaStream_t st) {
+                              cudaStream_t st, int* ready, const int32_t* band_base) {
   if (n_tiles == 0 && out != nullptr) return cudaSuccess;
   const size_t hs = hits_doc_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(hits_doc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -580,7 +614,7 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
   if (out == nullptr) return counted(cudaGetLastError(), n_items ? 1 : 0);  // join only (fused band tier)
   const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars) + 2 * kTile * sizeof(FoldSent);
   score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits, h_off,
-                                                       out);
+                                                       out, ready, band_base);
   return counted(cudaGetLastError(), n_items ? 2 : 1);
 }
 
@@ -821,6 +855,16 @@ __global__ void __launch_bounds__(WARP, (D == 2 && NP == 1) ? BM_NW_MINB2 : 1) n
     const int d = w.doc, band = w.band;
     const int n = a.n[d], m = a.m[d];
     const int row0 = band * kBandRows;
+    if (a.ready != nullptr) {
+      // scoring runs beside the DP: wait for every 64 x 64 tile of the band
+      const int want = ((min(kBandRows, n - row0) + kTile - 1) / kTile) * ((m + kTile - 1) / kTile);
+      if (lane == 0) {
+        const int* rp = a.ready + a.band_base[d] + band;
+        int got;
+        while ((got = ld_acquire_s32(rp)) < want) __nanosleep(256);
+      }
+      __syncwarp();
+    }
     const int nl = (min(kBandRows, n - row0) + kBandR - 1) / kBandR;
     const int nbands = (n + kBandRows - 1) / kBandRows;
     const int64_t ld = a.pitch[d];

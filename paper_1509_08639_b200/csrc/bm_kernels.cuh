@@ -99,6 +99,10 @@ struct NwArgs {
   // documents [seq_off[2r], seq_off[2r + 1]), at most kSeqMaxDocs
   const int32_t* seq_off = nullptr;
   int n_seq = 0;
+  // scoring overlapped with the DP: per (doc, band) count of scored 64 x 64
+  // tiles (ready[band_base[d] + band]); nullptr when S is complete at launch
+  const int* ready = nullptr;
+  const int32_t* band_base = nullptr;
 };
 cudaError_t launch_nw_seq(const NwArgs& a, cudaStream_t st);
 
@@ -198,7 +202,8 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
                               const Model& M, const ModelTables& mt, const int4* items, int n_items, uint32_t* hits,
                               const int64_t* h_off, const int4* tiles, int n_tiles,
                               const int64_t* s_off, const int32_t* pitch, double* out,
-                              cudaStream_t st);
+                              cudaStream_t st, int* ready = nullptr,
+                              const int32_t* band_base = nullptr);
 cudaError_t launch_compact(const bm_record*, const int64_t*, const int32_t*, int, int64_t*,
                            int64_t*, bm_record*, int64_t* bsum, cudaStream_t, int doc0 = 0);
 cudaError_t launch_scan_counts(const int32_t* cnt, int n, int64_t* off, int64_t* total,
@@ -212,6 +217,7 @@ cudaError_t launch_merge_shards(const bm_record* rec, int64_t stride, const int6
                                 int n_docs, int32_t* counts, int64_t* src_start, int64_t* goff,
                                 int64_t* total, int64_t* bsum, bm_record* out, cudaStream_t st);
 size_t score_smem_bytes();
+cudaError_t preload_score_hits();
 cudaError_t launch_fp64_probe(double*, int, int, cudaStream_t);
 long long launches();
 cudaError_t ensure_quot_table();

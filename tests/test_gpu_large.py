@@ -137,12 +137,15 @@ def test_band_parallel_extraction_vs_oracle(seed):
 @pytest.mark.parametrize("env", [
     {"BM_BAND_FUSED": "1", "BM_BAND_MIN_ITEMS": "1"},
     {"BM_BAND_FUSED": "1", "BM_BAND_MIN_ITEMS": "1", "BM_PAR_WALK_MIN": "600"},
+    {"BM_DP_OVERLAP": "1"},
 ])
 def test_fused_band_tier_vs_oracle(env):
-    """The fused banded tier (mine_band_kernel: scoring warps feeding the DP
-    warp through a shared-memory ring, no similarity matrix; extraction
-    re-scores the path cells), serial and band-parallel extraction, four
-    penalties including inf: records and costs equal the oracle's."""
+    """The opt-in routes in child processes: the fused banded tier
+    (mine_band_kernel: scoring warps feeding the DP warp through a
+    shared-memory ring, no similarity matrix; extraction re-scores the path
+    cells) with serial and band-parallel extraction, and the DP overlapped with
+    the scoring kernel (per-band readiness counters); four penalties including
+    inf: records and costs equal the oracle's."""
     import subprocess
     import sys
 
