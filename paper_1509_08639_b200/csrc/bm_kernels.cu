@@ -557,13 +557,14 @@ __device__ __forceinline__ void score_hits_tile(
 // mine_general): once the tile is written, its CTA adds 1 to the counter of
 // the 128-row band it belongs to; nw_band_kernel starts a band when all of
 // the band's tiles are counted (the fence orders the tile's stores first).
+template <bool kSignal>
 __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
     bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
     const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
     const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
     double* __restrict__ out, int* __restrict__ ready, const int32_t* __restrict__ band_base) {
   score_hits_tile(S, D, M, mt, tiles, s_off, pitch, hits, h_off, out);
-  if (ready != nullptr) {
+  if (kSignal) {
     __syncthreads();
     if (threadIdx.x == 0) {
       const int4 tile = tiles[blockIdx.x];
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
 // an overlapped launch spin on the tiles this kernel has not scored yet).
 cudaError_t preload_score_hits() {
   cudaFuncAttributes fa;
-  return cudaFuncGetAttributes(&fa, score_hits_kernel);
+  return cudaFuncGetAttributes(&fa, score_hits_kernel<true>);
 }
 
 size_t hits_doc_smem_bytes() {
@@ -613,8 +614,12 @@ cudaError_t launch_score_hits(const bm_sentences& S, const bm_docs& D, const bm_
   if (n_items) hits_doc_kernel<<<n_items, BM_HITS_DOC_THREADS, hs, st>>>(S, D, L, items, n_items, h_off, pitch, hits);
   if (out == nullptr) return counted(cudaGetLastError(), n_items ? 1 : 0);  // join only (fused band tier)
   const size_t ss = kExpTableWords * 8 + 2 * sizeof(TileScalars) + 2 * kTile * sizeof(FoldSent);
-  score_hits_kernel<<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits, h_off,
-                                                       out, ready, band_base);
+  if (ready != nullptr)
+    score_hits_kernel<true><<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits,
+                                                             h_off, out, ready, band_base);
+  else
+    score_hits_kernel<false><<<n_tiles, kTileThreads, ss, st>>>(S, D, M, mt, tiles, s_off, pitch, hits,
+                                                              h_off, out, nullptr, nullptr);
   return counted(cudaGetLastError(), n_items ? 2 : 1);
 }
 

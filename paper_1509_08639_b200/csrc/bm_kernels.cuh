@@ -15,7 +15,10 @@ namespace bm {
 // K1 tile shape and join capacity.
 constexpr int kTile = 64;              // 64 x 64 cells per CTA
 constexpr int kTileThreads = 256;
-constexpr int kJoinEmax = 1024;        // bucketed ids per join chunk
+#ifndef BM_JOIN_EMAX
+#define BM_JOIN_EMAX 1024
+#endif
+constexpr int kJoinEmax = BM_JOIN_EMAX;  // bucketed ids per join chunk
 #ifndef BM_JOIN_BUCKETS
 #define BM_JOIN_BUCKETS 512
 #endif

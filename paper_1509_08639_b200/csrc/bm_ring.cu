@@ -48,7 +48,7 @@ constexpr int kProducers = kProdWarps * WARP;
 // cells per scoring thread and task (one row of a lane block: 4; half a row:
 // 2; one cell: 1)
 #ifndef BM_RING_CPT
-#define BM_RING_CPT 2
+#define BM_RING_CPT 1
 #endif
 #ifndef BM_RING_MINB
 #define BM_RING_MINB 6
