@@ -1728,7 +1728,10 @@ int bm_tune(const bm_sentences* sent, const bm_docs* docs, const int32_t* n_host
     for (int q = 0; q < k; ++q) single += g.n[q] <= kBandRows;
     // about 4 runs per resident DP warp (8 per SM at 4 penalties): runs long
     // enough to amortise the fill, numerous enough to balance the warps
-    const int run = (int)std::max<int64_t>(1, std::min<int64_t>(kSeqMaxDocs, single / (4 * 8 * 148)));
+    // (BM_NW_SEQ_RUN, read per call: a fixed run length, for tests)
+    const char* fr = getenv("BM_NW_SEQ_RUN");
+    const int run = fr ? std::max(1, std::min(kSeqMaxDocs, atoi(fr)))
+                       : (int)std::max<int64_t>(1, std::min<int64_t>(kSeqMaxDocs, single / (4 * 8 * 148)));
     for (int q = 0; q < k;) {
       if (g.n[q] > kBandRows) {
         ++q;

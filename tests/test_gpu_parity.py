@@ -608,6 +608,35 @@ def test_tune_multi_penalty_passes_vs_oracle(oracle_mod, n_pen):
     assert np.array_equal(p, wp) and np.array_equal(h, wh)
 
 
+@pytest.mark.parametrize("run", ["2", "7", "32"])
+def test_tune_runs_of_single_band_documents_vs_oracle(oracle_mod, monkeypatch, run):
+    """nw_seq_kernel: runs of single-band documents laid end to end (forced run
+    lengths; n from 1 to 128, m from 1 to 300 incl. m < 4 and m % 4 != 0, with
+    multi-band documents between runs), 8 penalties incl. 0 and inf in passes of
+    4, 8 thresholds: pred / hit counts == oracle."""
+    from paper_1509_08639_b200 import engine, synth
+
+    monkeypatch.setenv("BM_NW_SEQ_RUN", run)
+    r = np.random.default_rng(77)
+    D = 160
+    n = r.integers(1, 129, D)
+    m = r.integers(1, 301, D)
+    n[:8] = [1, 128, 127, 4, 3, 100, 300, 129]
+    m[:8] = [1, 1, 3, 300, 5, 100, 200, 64]
+    n[40::37] = r.integers(129, 400, len(n[40::37]))  # multi-band documents between runs
+    g = np.minimum(n, m) // 2
+    sc = synth.make_corpus(g, n - g, m - g, vocab=2000, seed=31)
+    model = bm.load_model(golden("model5k_fwd.json"))
+    plex = sc.world.packed_lexicon()
+    pens = [0.05, 0.0, 0.2, float("inf"), 0.4, 0.6, 0.8, 1.6]
+    thrs = [0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9]
+    keys = [np.asarray(gd[:, 0] * int(sc.packed.m[d]) + gd[:, 1], np.int64) for d, gd in enumerate(sc.gold)]
+    p, h = engine.tune_counts(engine.DeviceCorpus.upload(sc.packed), engine.DeviceLexicon.upload(plex),
+                              engine.DocView.of(sc.packed), model, pens, thrs, keys)
+    wp, wh = oracle_mod.tune(oracle_mod.HostBatch(sc.packed, plex), model, pens, thrs, keys, threads=8)
+    assert np.array_equal(p, wp) and np.array_equal(h, wh)
+
+
 def test_sharded_mining_equals_single(oracle_mod):
     """Two LPT shards mined separately (as two ranks would) == one batch."""
     from paper_1509_08639_b200 import engine, shard, synth
