@@ -12,16 +12,22 @@
 //                to the band below through global memory exactly as in
 //                nw_band_kernel (sentinel-valued boundary rows, same codes,
 //                same cost), so extraction is unchanged;
-//   warps 1..P   score the blocks each super-step needs: a task is 8 lane
-//                blocks x 4 rows (one thread = one row of 4 columns: one
-//                16-byte hit-count load, 4 cells); the tasks of all
-//                super-steps form one sequence dealt round-robin to the
-//                producer warps, so the wavefront's fill and drain leave few
+//   warps 1..P   score the blocks each super-step needs: one thread scores
+//                BM_BAND_CPT cells of one row of a 4 x 4 lane block (one hit
+//                count load, the row's staged sentence once); the tasks of
+//                all super-steps form one sequence dealt round-robin to the
+//                scoring warps, so the wavefront's fill and drain leave few
 //                threads idle. Full / empty mbarriers per slot.
 // The hit counts come from the document-level join (hits_doc_kernel) in rows
 // of pitch_of(m) words. The matrix never exists; extraction re-scores the
 // path's diagonal cells (extract_kernel<true>). Documents with a sentence over
 // 255 tokens (the folded tables' range) keep the unfused tier.
+//
+// Opt-in (BM_BAND_FUSED=1, bm_api.cu): parity-green but slower than the
+// unfused tier on C3 (70.6 vs 68.5 ms for 200k documents). A CTA's progress is
+// its one DP warp's: with 8 scoring warps per DP warp only ~3 DP warps run per
+// SM (nw_band_kernel keeps ~12), so the scoring warps wait on their rings
+// (profiles/r02g_c3_band_ncu_full_summary.txt).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
