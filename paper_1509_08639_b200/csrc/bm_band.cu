@@ -46,8 +46,13 @@ namespace bm {
 #ifndef BM_BAND_SLOTS
 #define BM_BAND_SLOTS 4
 #endif
+// scoring warps per DP warp (a CTA runs one (doc, band) item)
+#ifndef BM_BAND_PROD_WARPS
+#define BM_BAND_PROD_WARPS (16 / BM_BAND_CPT)
+#endif
 #ifndef BM_BAND_MINB
-#define BM_BAND_MINB (BM_BAND_CPT == 4 ? 5 : 3)
+#define BM_BAND_MINB \
+  (BM_BAND_PROD_WARPS == 1 ? 8 : BM_BAND_PROD_WARPS == 2 ? 6 : BM_BAND_PROD_WARPS == 4 ? 5 : 3)
 #endif
 // scoring warps: one arrival per warp on the full barriers (fewer mbarrier
 // events wake fewer sleeping waiters); empty-slot waits sleep up to
@@ -60,7 +65,7 @@ namespace bm {
 #endif
 constexpr int kBandCpt = BM_BAND_CPT;
 static_assert(kBandCpt == 4 || kBandCpt == 2, "2 or 4 cells per thread");
-constexpr int kBandProdWarps = 16 / kBandCpt;        // every lane block of a super-step scored at once
+constexpr int kBandProdWarps = BM_BAND_PROD_WARPS;
 constexpr int kBandThreads = (1 + kBandProdWarps) * WARP;
 constexpr int kBandSlots = BM_BAND_SLOTS;
 constexpr int kBandLaneD = kBandR * 4 + 2;  // doubles per DP lane in a slot (+2: banks)
@@ -303,28 +308,34 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
       const uint32_t cols_s = (uint32_t)__cvta_generic_to_shared(cols) + zz;
       const uint32_t rows_s = (uint32_t)__cvta_generic_to_shared(rows) + zz;
       const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + zz;
-      // at most one task per warp and super-step (ntask <= 4 = P): the task of
-      // super-step t + 1 is located, and its hit words loaded, before the
-      // task of t is scored
-      static_assert(WARP / kBandTaskLanes <= kBandProdWarps, "one task per warp per super-step");
+      // this warp's tasks: every P-th of the sequence of all super-steps'
+      // tasks; the next task's hit words are loaded before the current task
+      // is scored
       struct Task {
-        int L, il, j0;
+        int t, kt, L, il, j0;
         bool on;
-      };
-      auto task_of = [&](int t, int q0) {
-        const int lx = max(0, t - ngroups + 1), ly = min(nl - 1, t);
-        int kt = (pw - q0) % kBandProdWarps;
-        if (kt < 0) kt += kBandProdWarps;
-        Task k;
-        k.L = lx + kt * kBandTaskLanes + sub;
-        k.il = k.L * kBandR + r;
-        k.j0 = 4 * (t - k.L) + c0;
-        k.on = t < steps && kt * kBandTaskLanes <= ly - lx && k.L <= ly && k.il < nrow;
-        return k;
       };
       auto ntask_of = [&](int t) {
         const int lx = max(0, t - ngroups + 1), ly = min(nl - 1, t);
         return (ly - lx + kBandTaskLanes) / kBandTaskLanes;
+      };
+      // (t, kt) -> the first own task at or after it (t == steps: none)
+      auto task_at = [&](int t, int kt) {
+        while (t < steps) {
+          const int nt = ntask_of(t);
+          if (kt < nt) break;
+          kt -= nt;
+          ++t;
+        }
+        Task k;
+        k.t = t;
+        k.kt = kt;
+        const int lx = max(0, t - ngroups + 1), ly = min(nl - 1, t);
+        k.L = lx + kt * kBandTaskLanes + sub;
+        k.il = k.L * kBandR + r;
+        k.j0 = 4 * (t - k.L) + c0;
+        k.on = t < steps && k.L <= ly && k.il < nrow;
+        return k;
       };
       auto hits_of = [&](const Task& k) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -340,17 +351,11 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
         }
         return v;
       };
-      int q0 = 0;  // sequence index of super-step t's first task
-      Task nk = task_of(0, 0);
-      uint4 nh = hits_of(nk);
+      Task k = task_at(0, pw);
+      uint4 hv = hits_of(k);
 #pragma unroll 1
       for (int t = 0; t < steps; ++t) {
         const int slot = t % kBandSlots;
-        const Task k = nk;
-        const uint4 hv = nh;
-        q0 += ntask_of(t);
-        nk = task_of(t + 1, q0);
-        nh = hits_of(nk);
         if (t >= kBandSlots) {
           if (BM_BAND_SLEEP_NS > 0)
             mbar_wait_sleep(bar_empty + slot, (uint32_t)(((t / kBandSlots) - 1) & 1), BM_BAND_SLEEP_NS);
@@ -362,7 +367,11 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
           if (j < m)
             cols[j & (4 * kBandWinGroups - 1)] = band_sent(S, a.D.tgt0[d] + j, doc_pos(j, m));
         }
-        {
+        __syncwarp();
+#pragma unroll 1
+        while (k.t == t) {
+          const Task nk = task_at(k.t, k.kt + kBandProdWarps);
+          const uint4 nh = hits_of(nk);
           const int L = k.L, il = k.il;
           if (k.on) {
             const int j0 = k.j0;
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
               asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(ta), "=r"(ax) : "r"(ra));
               asm("ld.shared.f64 %0, [%1];" : "=d"(pos_s) : "r"(ra + 8u));
             }
-            // the 4 cells are independent chains: no branches between them
+            // the cells are independent chains: no branches between them
             // (a column past m re-scores column m - 1; the DP never reads it)
             double o[kBandCpt];
             const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
@@ -395,6 +404,8 @@ __global__ void __launch_bounds__(kBandThreads, BM_BAND_MINB) mine_band_kernel(B
                            "d"(o[c + 1])
                            : "memory");
           }
+          k = nk;
+          hv = nh;
         }
         if (BM_BAND_WARP_ARRIVE) {
           // the warp's ring stores are ordered before lane 0's (release)
