@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libbimine_b200.so")
 SOURCES = ["bm_lib.cu", "bm_ingest.cpp", "bm_synth.cpp"]
-HEADERS = ["bm_kernels.cu", "bm_ring.cu", "bm_merge.cu", "bm_api.cu", "bm_device.cuh", "bm_kernels.cuh", "glibc_exp.cuh", "glibc_exp_table.h"]
+HEADERS = ["bm_kernels.cu", "bm_ring.cu", "bm_band.cu", "bm_seq.cu", "bm_merge.cu", "bm_api.cu", "bm_device.cuh", "bm_kernels.cuh", "glibc_exp.cuh", "glibc_exp_table.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
