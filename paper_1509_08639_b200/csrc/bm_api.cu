@@ -871,6 +871,16 @@ static cudaStream_t side_stream(int q) {
   return s[q];
 }
 
+// Ring-kernel shared-memory buckets (bytes of a document's slice): 9 / 7 / 5 /
+// 3 CTAs per SM. BM_RING_BUCKETS=0: one launch per R (a launch's slice is its
+// largest document's).
+constexpr int kRingSmemBuckets = 4;
+static int ring_smem_bucket(size_t sl) {
+  static const bool on = getenv("BM_RING_BUCKETS") ? atoi(getenv("BM_RING_BUCKETS")) != 0 : true;
+  if (!on) return kRingSmemBuckets - 1;
+  return sl <= 24 * 1024 ? 0 : sl <= 32 * 1024 ? 1 : sl <= 44 * 1024 ? 2 : 3;
+}
+
 // Fused banded tier (bm_band.cu) routing, opt-in: BM_BAND_FUSED=1 sends the
 // banded documents whose sentences fit the folded tables there instead of
 // score_hits_kernel -> nw_band_kernel. Measured on C3 200k:
@@ -906,8 +916,12 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
                const Model& M, double threshold, double penalty, const int64_t* rec_off,
                bm_record* rec, int32_t* rec_count, double* cost, int d_lo, int d_hi,
                HostTrace& tr, cudaStream_t sf, cudaStream_t sb) {
-  std::vector<int32_t> fused[4];
-  size_t fused_smem[4] = {0, 0, 0, 0}, hits_smem[4] = {0, 0, 0, 0};
+  // fused tier: one launch per (rows per lane R, shared-memory bucket): a
+  // launch's slice is its largest document's, so a few documents with large
+  // hit-count matrices would otherwise cut every CTA of the class to 3 per SM
+  constexpr int kNB = kRingSmemBuckets;
+  std::vector<int32_t> fused[4 * kNB];
+  size_t fused_smem[4 * kNB] = {}, hits_smem[4 * kNB] = {};
   std::vector<int64_t> hit_off;  // per document of [d_lo, d_hi)
   int64_t hit_total = 0;
   std::vector<int32_t> banded;  // planned after the fused tier is launched
@@ -933,9 +947,10 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
     }
     if (pq >= 0 && amax_host[d] <= 255) {
       const int q = pq;
-      fused[q].push_back(d);
-      fused_smem[q] = std::max(fused_smem[q], sl);
-      hits_smem[q] = std::max(hits_smem[q], hs);
+      const int qq = q * kNB + ring_smem_bucket(sl);
+      fused[qq].push_back(d);
+      fused_smem[qq] = std::max(fused_smem[qq], sl);
+      hits_smem[qq] = std::max(hits_smem[qq], hs);
       hit_off[d - d_lo] = hit_total;
       hit_total += (int64_t)align16(((size_t)n * m + 1) / 2 * 4);
     } else {
@@ -954,7 +969,7 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
       BM_CK(sc.upload(&dho, hit_off), "upload");
       tr.mark("alloc hits");
     }
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 4 * kNB; ++q) {
       if (fused[q].empty()) continue;
       int32_t* list = nullptr;
       BM_CK(sc.upload(&list, fused[q]), "upload");
@@ -976,7 +991,7 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
       a.tabs = pair_tables();
       BM_CK(model_tables(M, &a.mt), "model tables");
       if (!BM_RING_FUSED_JOIN) BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
-      BM_CK(launch_ring(a, 1 << q, fused_smem[q], st), "mine_ring_kernel");
+      BM_CK(launch_ring(a, 1 << (q / kNB), fused_smem[q], st), "mine_ring_kernel");
       tr.mark("launch fused tier");
     }
   }
