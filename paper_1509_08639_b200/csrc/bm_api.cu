@@ -872,13 +872,13 @@ static cudaStream_t side_stream(int q) {
 }
 
 // Ring-kernel shared-memory buckets (bytes of a document's slice): 9 / 7 / 5 /
-// 3 CTAs per SM. BM_RING_BUCKETS=0: one launch per R (a launch's slice is its
+// 3 / fewer CTAs per SM. BM_RING_BUCKETS=0: one launch per R (a launch's slice is its
 // largest document's).
-constexpr int kRingSmemBuckets = 4;
+constexpr int kRingSmemBuckets = 5;
 static int ring_smem_bucket(size_t sl) {
   static const bool on = getenv("BM_RING_BUCKETS") ? atoi(getenv("BM_RING_BUCKETS")) != 0 : true;
   if (!on) return kRingSmemBuckets - 1;
-  return sl <= 24 * 1024 ? 0 : sl <= 32 * 1024 ? 1 : sl <= 44 * 1024 ? 2 : 3;
+  return sl <= 24 * 1024 ? 0 : sl <= 32 * 1024 ? 1 : sl <= 44 * 1024 ? 2 : sl <= 64 * 1024 ? 3 : 4;
 }
 
 // Fused banded tier (bm_band.cu) routing, opt-in: BM_BAND_FUSED=1 sends the
