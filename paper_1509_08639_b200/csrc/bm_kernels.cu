@@ -557,8 +557,11 @@ __device__ __forceinline__ void score_hits_tile(
 // mine_general): once the tile is written, its CTA adds 1 to the counter of
 // the 128-row band it belongs to; nw_band_kernel starts a band when all of
 // the band's tiles are counted (the fence orders the tile's stores first).
+#ifndef BM_SCORE_MINB
+#define BM_SCORE_MINB 5
+#endif
 template <bool kSignal>
-__global__ void __launch_bounds__(kTileThreads, 4) score_hits_kernel(
+__global__ void __launch_bounds__(kTileThreads, BM_SCORE_MINB) score_hits_kernel(
     bm_sentences S, bm_docs D, Model M, ModelTables mt, const int4* __restrict__ tiles,
     const int64_t* __restrict__ s_off, const int32_t* __restrict__ pitch,
     const uint32_t* __restrict__ hits, const int64_t* __restrict__ h_off,
