@@ -1185,6 +1185,14 @@ template <int WG>
 __host__ __device__ constexpr int walk_smem() { return kWalkWarps * 3 * win_words<WG>() * 4; }
 constexpr int kWinWords = win_words<32>();
 constexpr int kWalkSmem = walk_smem<32>();  // 48 KB
+// extraction's windows (extract_kernel, band_walk_kernel): BM_EXTRACT_WG
+// column groups (32: 48 KB per CTA; 16: 24 KB, twice the resident warps --
+// C3 200k 66.3 -> 65.8 ms)
+#ifndef BM_EXTRACT_WG
+#define BM_EXTRACT_WG 16
+#endif
+constexpr int kExtractWG = BM_EXTRACT_WG;
+constexpr int kExtractSmem = walk_smem<kExtractWG>();
 // the tuner's walks (many small documents, latency-bound) use half-width
 // windows: 24 KB per CTA -> twice the resident warps
 #ifndef BM_TUNE_WG
@@ -1391,7 +1399,7 @@ __device__ __forceinline__ int extract_segment(uint32_t* win, const uint32_t* dd
     pj = cj;
     pvalid = valid;
   };
-  warp_walk_from(win, dd, n, m, lane, i0, j0, i_stop, [&](int op, int i, int j) {
+  warp_walk_from<kExtractWG>(win, dd, n, m, lane, i0, j0, i_stop, [&](int op, int i, int j) {
     if (op == BM_MOVE_D) {
       if (lane == (nd & 31)) {
         ci = i;
@@ -1447,7 +1455,7 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) extract_kernel(
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int d = blockIdx.x * kWalkWarps + wid;
   if (d >= n_docs || (skip != nullptr && skip[d])) return;
-  uint32_t* win = walk_smem + wid * 3 * kWinWords;
+  uint32_t* win = walk_smem + wid * 3 * win_words<kExtractWG>();
   const int n = nn[d], m = mm[d];
   const PathCell<kRescore> val{&cs, d, n, m, pitch[d]};
   const int kept = extract_segment(win, dirs + dir_off[d], val, n, m, lane, n, m, 0, threshold, d,
@@ -1571,7 +1579,7 @@ __global__ void __launch_bounds__(kWalkWarps * WARP) band_walk_kernel(
   const int b = blockIdx.x * kWalkWarps + wid;
   if (b >= nb) return;
   const int x = entry[b_off[q] + b];
-  uint32_t* win = walk_smem + wid * 3 * kWinWords;
+  uint32_t* win = walk_smem + wid * 3 * win_words<kExtractWG>();
   bm_record* out = slots + (b_off[q] + b) * kBandRows;
   const PathCell<kRescore> val{&cs, d, n, m, pitch[d]};
   const int kept = extract_segment(win, dirs + dir_off[d], val, n, m, lane,
@@ -1613,14 +1621,14 @@ cudaError_t launch_extract(const uint32_t* dirs, const int64_t* dir_off, const C
   if (n_docs == 0) return cudaSuccess;
   const bool rs = cs.S == nullptr;
   const void* fn = rs ? (const void*)extract_kernel<true> : (const void*)extract_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kExtractSmem);
   if (e != cudaSuccess) return e;
   const int grid = (n_docs + kWalkWarps - 1) / kWalkWarps;
   if (rs)
-    extract_kernel<true><<<grid, kWalkWarps * WARP, kWalkSmem, st>>>(dirs, dir_off, cs, pitch, n, m,
+    extract_kernel<true><<<grid, kWalkWarps * WARP, kExtractSmem, st>>>(dirs, dir_off, cs, pitch, n, m,
                                                                     n_docs, thr, rec_off, rec, cnt, skip);
   else
-    extract_kernel<false><<<grid, kWalkWarps * WARP, kWalkSmem, st>>>(dirs, dir_off, cs, pitch, n, m,
+    extract_kernel<false><<<grid, kWalkWarps * WARP, kExtractSmem, st>>>(dirs, dir_off, cs, pitch, n, m,
                                                                      n_docs, thr, rec_off, rec, cnt, skip);
   return counted(cudaGetLastError());
 }
@@ -1635,7 +1643,7 @@ cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, 
   const bool rs = cs.S == nullptr;
   cudaError_t e = cudaFuncSetAttribute(
       rs ? (const void*)band_walk_kernel<true> : (const void*)band_walk_kernel<false>,
-      cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem);
+      cudaFuncAttributeMaxDynamicSharedMemorySize, kExtractSmem);
   if (e != cudaSuccess) return e;
   // pass 0 over (bands - 1) x samples, pass 1 over (bands - 1) x (m + 1)
   const int64_t w1 = bx.max_exit_walks, w0 = w1 / kExitStride + 2 * bx.max_bands;
@@ -1651,10 +1659,10 @@ cudaError_t launch_extract_banded(const uint32_t* dirs, const int64_t* dir_off, 
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const dim3 wg((bx.max_bands + kWalkWarps - 1) / kWalkWarps, bx.n_big);
   if (rs)
-    band_walk_kernel<true><<<wg, kWalkWarps * WARP, kWalkSmem, st>>>(
+    band_walk_kernel<true><<<wg, kWalkWarps * WARP, kExtractSmem, st>>>(
         dirs, dir_off, cs, pitch, n, m, bx.big, bx.entry, bx.b_off, thr, bx.slots, bx.slot_cnt);
   else
-    band_walk_kernel<false><<<wg, kWalkWarps * WARP, kWalkSmem, st>>>(
+    band_walk_kernel<false><<<wg, kWalkWarps * WARP, kExtractSmem, st>>>(
         dirs, dir_off, cs, pitch, n, m, bx.big, bx.entry, bx.b_off, thr, bx.slots, bx.slot_cnt);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   band_gather_kernel<<<bx.n_big, 256, 0, st>>>(n, bx.big, bx.b_off, bx.slots, bx.slot_cnt, rec_off,
