@@ -969,10 +969,21 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
       BM_CK(sc.upload(&dho, hit_off), "upload");
       tr.mark("alloc hits");
     }
-    for (int q = 0; q < 4 * kNB; ++q) {
-      if (fused[q].empty()) continue;
+    // per rows-per-lane class: one hits_kernel over all of its documents,
+    // then one ring launch per shared-memory bucket (a sub-range of the list)
+    for (int c = 0; c < 4; ++c) {
+      std::vector<int32_t> all;
+      int boff[kNB + 1];
+      size_t hs = 0;
+      for (int b = 0; b < kNB; ++b) {
+        boff[b] = (int)all.size();
+        all.insert(all.end(), fused[c * kNB + b].begin(), fused[c * kNB + b].end());
+        hs = std::max(hs, hits_smem[c * kNB + b]);
+      }
+      boff[kNB] = (int)all.size();
+      if (all.empty()) continue;
       int32_t* list = nullptr;
-      BM_CK(sc.upload(&list, fused[q]), "upload");
+      BM_CK(sc.upload(&list, all), "upload");
       FusedArgs a;
       a.S = *sent;
       a.D = *docs;
@@ -981,7 +992,7 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
       a.threshold = threshold;
       a.p = penalty;
       a.list = list;
-      a.n_list = (int)fused[q].size();
+      a.n_list = (int)all.size();
       a.rec_off = rec_off;
       a.rec = rec;
       a.rec_count = rec_count;
@@ -990,8 +1001,13 @@ static int mine_group(const bm_sentences* sent, const bm_docs* docs, const int32
       a.hit_off = dho - d_lo;  // indexed by the batch's document index
       a.tabs = pair_tables();
       BM_CK(model_tables(M, &a.mt), "model tables");
-      if (!BM_RING_FUSED_JOIN) BM_CK(launch_hits(a, hits_smem[q], st), "hits_kernel");
-      BM_CK(launch_ring(a, 1 << (q / kNB), fused_smem[q], st), "mine_ring_kernel");
+      if (!BM_RING_FUSED_JOIN) BM_CK(launch_hits(a, hs, st), "hits_kernel");
+      for (int b = 0; b < kNB; ++b) {
+        if (boff[b + 1] == boff[b]) continue;
+        a.list = list + boff[b];
+        a.n_list = boff[b + 1] - boff[b];
+        BM_CK(launch_ring(a, 1 << c, fused_smem[c * kNB + b], st), "mine_ring_kernel");
+      }
       tr.mark("launch fused tier");
     }
   }
